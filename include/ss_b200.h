@@ -1,0 +1,128 @@
+/*
+ * ss_b200.h — C ABI of the B200-native Symbiosis base executor ("splitserve" hot path).
+ *
+ * The reference computes one executor batch inline in Python:
+ *   BaseExecutor._compute_batch   pkg/src/splitserve/executor.py:191-231
+ *     concat_rows                 pkg/src/splitserve/tensor_ops.py:145-146
+ *     affine_forward              pkg/src/splitserve/tensor_ops.py:71-78     (PASS_FORWARD = 0)
+ *     affine_backward_input       pkg/src/splitserve/tensor_ops.py:81-89     (PASS_BACKWARD = 1)
+ *     matmul (bias nullified)     pkg/src/splitserve/executor.py:221-222     (PASS_NOISE_EFFECT = 2)
+ *     split_rows                  pkg/src/splitserve/tensor_ops.py:149-156
+ * and applies each client's adapter client-side afterwards:
+ *   apply_adapter                 pkg/src/splitserve/adapters.py:127-145  (LoRA + IA3, forward)
+ *   lora_backward (grad_x term)   pkg/src/splitserve/adapters.py:26-41    (backward)
+ *   ClientModel._layer_backward   pkg/src/splitserve/client.py:286-305    (IA3 g = dy * l)
+ *
+ * This library replaces that inline compute with one call per dispatch: ss_compute_batch()
+ * runs gather -> (LoRA shrink) -> fused base GEMM + adapter epilogue -> per-segment scatter
+ * on a CUDA stream. No C++ exception crosses this boundary; every entry point returns an
+ * int status (SS_OK or a negative SS_E* code) and ss_last_error() gives the message.
+ *
+ * All activation pointers are DEVICE pointers owned by the caller (client exchange buffers).
+ * Weight / adapter uploads accept host or device pointers (SS_MEM_DEVICE).
+ */
+#ifndef SS_B200_H
+#define SS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------------------------- */
+#define SS_OK 0
+#define SS_E_ARG (-1)       /* bad argument (null ctx, bad pass, bad dims) */
+#define SS_E_CUDA (-2)      /* CUDA runtime / driver failure */
+#define SS_E_NOLAYER (-3)   /* unknown (block, role) — reference: "unknown layer" executor.py:172-174 */
+#define SS_E_NOMEM (-4)
+#define SS_E_UNSUPPORTED (-5)
+
+/* per-segment status written to seg_status[i] (0 = computed) */
+#define SS_SEG_OK 0
+#define SS_SEG_BAD_WIDTH 1  /* reference: "row width ... does not match layer" executor.py:208-211 */
+#define SS_SEG_BAD_PTR 2
+#define SS_SEG_NO_ADAPTER 3 /* SS_SEGF_ADAPTER set but no adapter registered for this layer */
+
+/* passes — same values as protocol.py:40-42 */
+#define SS_PASS_FORWARD 0
+#define SS_PASS_BACKWARD 1
+#define SS_PASS_NOISE_EFFECT 2
+
+/* memory / dtype flags for uploads */
+#define SS_MEM_DEVICE (1u << 0) /* pointer is device memory (else host) */
+#define SS_DT_BF16 (1u << 1)    /* element type bf16 (else f32) */
+
+/* adapter kinds (bit mask) — adapters.py:44-115 */
+#define SS_ADAPTER_LORA 1u
+#define SS_ADAPTER_IA3 2u
+
+/* segment flags */
+#define SS_SEGF_SRC_BF16 (1u << 0)  /* src rows are bf16 (else f32) */
+#define SS_SEGF_DST_BF16 (1u << 1)  /* dst rows are bf16 (else f32) */
+#define SS_SEGF_BASE_BF16 (1u << 2) /* dst_base rows are bf16 (else f32) */
+#define SS_SEGF_ADAPTER (1u << 3)   /* apply this client's registered adapter for the layer */
+
+/* One request (envelope) of a batch, in batch order. Rows are concatenated in array order
+ * exactly like concat_rows(); row r of segment i is batch row off_i + r, off_i = sum_{j<i} rows_j
+ * over the segments whose status is SS_SEG_OK (split_rows, tensor_ops.py:149-156). */
+typedef struct ss_seg {
+  uint32_t client_id;
+  uint32_t rows;     /* token_count */
+  uint32_t width;    /* payload width as sent; must equal d_in (fwd/noise) or d_out (bwd) */
+  uint32_t flags;    /* SS_SEGF_* */
+  const void* src;   /* device, [rows, src_ld] */
+  int64_t src_ld;    /* elements */
+  void* dst;         /* device, [rows, dst_ld]; may alias src (in-place exchange buffer) */
+  int64_t dst_ld;
+  void* dst_base;    /* optional pre-IA3 output (IA3 fine-tune clients need y_base,
+                        client.py:241-242, 293); NULL if not wanted */
+  int64_t base_ld;
+} ss_seg;
+
+typedef struct ss_ctx ss_ctx;
+
+/* Create a context on CUDA device `device`. tp_rank / tp_size describe this process's
+ * tensor-parallel position (metadata; sharding is expressed through the shards loaded). */
+int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out);
+int ss_ctx_destroy(ss_ctx* ctx);
+const char* ss_last_error(const ss_ctx* ctx);
+/* Library version / build string, usable without a GPU. */
+const char* ss_version(void);
+
+/* Load one frozen affine layer (AffineParams, tensor_ops.py:39-68): weight [d_in, d_out]
+ * row-major with row stride w_ld elements, optional bias [d_out]. Stored as bf16. */
+int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const void* weight,
+                  int64_t w_ld, const void* bias, uint32_t flags);
+int ss_unload_layer(ss_ctx* ctx, int block, int role);
+
+/* Register / refresh a client's adapter for one layer. LoRA: A [d_in, rank], B [rank, d_out],
+ * scale = alpha / rank (lora_forward adapters.py:19-23). IA3: l [d_out] (adapters.py:142-144).
+ * kind is a mask of SS_ADAPTER_*; pointers of kinds not in the mask may be NULL.
+ * Refreshing with the same rank re-packs in place (call after every optimizer step). */
+int ss_set_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role, uint32_t kind, int rank,
+                   float scale, const void* A, const void* B, const void* l, uint32_t flags);
+int ss_clear_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role);
+/* Drop every adapter of a client (deregister). */
+int ss_clear_client(ss_ctx* ctx, uint32_t client_id);
+
+/* Compute one batch for layer (block, role) and pass. `stream` is a cudaStream_t (NULL =
+ * legacy default stream). Asynchronous: results are visible after the stream reaches this
+ * point. seg_status[n_seg] receives per-segment status; rejected segments are not written. */
+int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
+                     const ss_seg* segs, void* stream, int32_t* seg_status);
+
+/* Device bytes held: weights (+bias), adapter packs, transient workspace high-water mark. */
+int ss_memory_stats(const ss_ctx* ctx, int64_t* weight_bytes, int64_t* adapter_bytes,
+                    int64_t* workspace_bytes);
+
+/* Number of kernels launched by this context since creation (evidence / bench counter). */
+int64_t ss_kernel_launches(const ss_ctx* ctx);
+
+/* Tuning knob: M-tile grouping of the persistent raster (default 16). */
+int ss_set_option(ss_ctx* ctx, const char* key, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SS_B200_H */

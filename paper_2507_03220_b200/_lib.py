@@ -1,0 +1,117 @@
+"""ctypes binding of the C ABI in include/ss_b200.h (libss_b200.so, built in-tree).
+
+This is the only way the package reaches the GPU. There is no CPU fallback: if the shared
+library is missing, importing the executor raises immediately (build with
+``python __graft_entry__.py`` or ``make -C paper_2507_03220_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libss_b200.so")
+
+SS_OK = 0
+SS_E_ARG = -1
+SS_E_CUDA = -2
+SS_E_NOLAYER = -3
+SS_E_NOMEM = -4
+SS_E_UNSUPPORTED = -5
+
+SS_SEG_OK = 0
+SS_SEG_BAD_WIDTH = 1
+SS_SEG_BAD_PTR = 2
+SS_SEG_NO_ADAPTER = 3
+
+SS_MEM_DEVICE = 1 << 0
+SS_DT_BF16 = 1 << 1
+
+SS_ADAPTER_LORA = 1
+SS_ADAPTER_IA3 = 2
+
+SS_SEGF_SRC_BF16 = 1 << 0
+SS_SEGF_DST_BF16 = 1 << 1
+SS_SEGF_BASE_BF16 = 1 << 2
+SS_SEGF_ADAPTER = 1 << 3
+
+# Every symbol include/ss_b200.h declares (checked by tests/test_lib_abi.py).
+EXPORTED = (
+    "ss_ctx_create", "ss_ctx_destroy", "ss_last_error", "ss_version", "ss_load_layer",
+    "ss_unload_layer", "ss_set_adapter", "ss_clear_adapter", "ss_clear_client",
+    "ss_compute_batch", "ss_memory_stats", "ss_kernel_launches", "ss_set_option",
+)
+
+
+class SsSeg(ctypes.Structure):
+    _fields_ = [
+        ("client_id", ctypes.c_uint32),
+        ("rows", ctypes.c_uint32),
+        ("width", ctypes.c_uint32),
+        ("flags", ctypes.c_uint32),
+        ("src", ctypes.c_void_p),
+        ("src_ld", ctypes.c_int64),
+        ("dst", ctypes.c_void_p),
+        ("dst_ld", ctypes.c_int64),
+        ("dst_base", ctypes.c_void_p),
+        ("base_ld", ctypes.c_int64),
+    ]
+
+
+class LibraryMissing(RuntimeError):
+    """libss_b200.so is not built; the executor has no other compute path."""
+
+
+class SsError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"ss_b200 error {code}: {message}")
+        self.code = code
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise LibraryMissing(
+                f"{LIB_PATH} not found: the CUDA extension is not built "
+                "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
+        lib = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, u32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32
+        sig = {
+            "ss_ctx_create": (i32, [i32, i32, i32, ctypes.POINTER(vp)]),
+            "ss_ctx_destroy": (i32, [vp]),
+            "ss_last_error": (ctypes.c_char_p, [vp]),
+            "ss_version": (ctypes.c_char_p, []),
+            "ss_load_layer": (i32, [vp, i32, i32, i32, i32, vp, i64, vp, u32]),
+            "ss_unload_layer": (i32, [vp, i32, i32]),
+            "ss_set_adapter": (i32, [vp, u32, i32, i32, u32, i32, ctypes.c_float, vp, vp, vp, u32]),
+            "ss_clear_adapter": (i32, [vp, u32, i32, i32]),
+            "ss_clear_client": (i32, [vp, u32]),
+            "ss_compute_batch": (i32, [vp, i32, i32, i32, i32, ctypes.POINTER(SsSeg), vp,
+                                       ctypes.POINTER(ctypes.c_int32)]),
+            "ss_memory_stats": (i32, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                      ctypes.POINTER(i64)]),
+            "ss_kernel_launches": (i64, [vp]),
+            "ss_set_option": (i32, [vp, ctypes.c_char_p, i64]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(ctx, rc: int) -> None:
+    if rc != SS_OK:
+        lib = load()
+        msg = lib.ss_last_error(ctx) if ctx else b"(no context)"
+        raise SsError(rc, (msg or b"").decode("utf-8", "replace"))

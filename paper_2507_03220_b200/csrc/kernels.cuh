@@ -1,0 +1,604 @@
+// Device kernels of the segmented base executor (sm_100a).
+//
+//   K4 gather_rows_kernel  : client segments -> contiguous bf16 operand X (concat_rows,
+//                            reference tensor_ops.py:145-146), IA3 prologue for backward
+//                            (client.py:291-294), per-row segment index for routing.
+//   K3 lora_shrink_kernel  : per segment s*x.A (fwd, adapters.py:23) or s*g.B^T (bwd,
+//                            adapters.py:37) on tcgen05, written block-diagonally into a
+//                            per-M-tile operand so the expand rides the base GEMM's K loop.
+//   K1/K2/K5 seg_gemm_kernel: persistent warp-specialised TMA -> tcgen05 -> TMEM GEMM:
+//                            y = x.W + b (affine_forward tensor_ops.py:71-78), dx = g.W^T
+//                            (affine_backward_input tensor_ops.py:81-89) or n.W (noise,
+//                            executor.py:221-222), LoRA expand as extra K steps into the same
+//                            TMEM accumulator, then bias / IA3 epilogue (adapters.py:127-145)
+//                            and the per-segment scatter (split_rows tensor_ops.py:149-156)
+//                            straight into each client's destination rows.
+#pragma once
+#include "ptx.cuh"
+
+namespace ss {
+
+// Segment flags (device side).
+enum : int32_t {
+  SEGF_SRC_BF16 = 1 << 0,
+  SEGF_DST_BF16 = 1 << 1,
+  SEGF_BASE_BF16 = 1 << 2,
+  SEGF_LORA = 1 << 3,
+  SEGF_IA3 = 1 << 4,
+  SEGF_WANT_BASE = 1 << 5,
+  SEGF_SRC_VEC = 1 << 6,   // src rows 16-byte aligned
+  SEGF_DST_VEC = 1 << 7,   // dst rows 16-byte aligned
+  SEGF_BASE_VEC = 1 << 8,  // base rows 16-byte aligned
+};
+
+struct DevSeg {
+  int32_t row0;        // first row in the batch (prefix offset, split_rows order)
+  int32_t rows;
+  int32_t flags;
+  int32_t lora_col0;   // column of this segment's rank block inside its first M-tile
+  const void* src;
+  int64_t src_ld;      // elements
+  void* dst;
+  int64_t dst_ld;
+  void* dst_base;      // pre-IA3 output for IA3 fine-tune clients (forward)
+  int64_t base_ld;
+  const float* ia3;    // IA3 scale vector (length d_out of the layer)
+  float lora_scale;    // alpha / r
+  int32_t pack_row;    // first row of this client's rank block in the layer's LoRA packs
+  int32_t rank_pad;    // rank rounded up to 16
+  int32_t pad_;
+};
+
+constexpr int BM = 128;           // rows per tile == TMEM lanes
+constexpr int BN = 256;           // columns per tile (one UMMA N=256)
+constexpr int BK = 64;            // K per pipeline stage (one 128-byte swizzle row)
+constexpr int UK = 16;            // K per tcgen05.mma for bf16
+constexpr int STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;       // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK * 2;       // 32 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int LORA_CHUNK = 16;                   // rank granularity
+constexpr int LORA_CHUNK_BYTES = 64 * LORA_CHUNK * 2;  // one {64, 16} box = 2 KB
+constexpr int GEMM_THREADS = 256;                // 8 warps
+constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct GemmParams {
+  int M, N, K;
+  int num_m_tiles, num_n_tiles, group_m;
+  int has_bias;
+  int any_lora;
+  const float* bias;
+  const DevSeg* segs;
+  const int32_t* row_seg;
+  const int32_t* tile_chunk_begin;  // per M-tile: first entry in `chunks`
+  const int32_t* tile_chunk_count;  // per M-tile: number of 16-wide rank chunks
+  const int32_t* chunks;            // pack row of each rank chunk
+  int ia3_in_epilogue;              // forward: scale output columns by IA3
+};
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb,
+                                            int& nb) {
+  const int per_group = group_m * num_n;
+  const int g = t / per_group;
+  const int first_m = g * group_m;
+  const int gsize = min(group_m, num_m - first_m);
+  const int r = t % per_group;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+// ============================================================================ K1/K2/K5
+template <bool kBwd>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    seg_gemm_kernel(const __grid_constant__ CUtensorMap tmA,   // X  [M, K] bf16
+                    const __grid_constant__ CUtensorMap tmB,   // W  [d_in, d_out] bf16
+                    const __grid_constant__ CUtensorMap tmAL,  // A_lora [M, R_w] bf16
+                    const __grid_constant__ CUtensorMap tmBP,  // pack [R, N] bf16 (MN-major B)
+                    const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;   // 2 accumulator buffers
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    if (p.any_lora) {
+      tma_prefetch_desc(&tmAL);
+      tma_prefetch_desc(&tmBP);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  const int nkb = (p.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+          tma_load_2d(smA + s * A_STAGE_BYTES, &tmA, &full_bar[s], kb * BK, m0);
+          uint8_t* b = smB + s * B_STAGE_BYTES;
+          if (kBwd) {
+            // W viewed K-major: rows = d_in (the GEMM's N), cols = d_out (the GEMM's K).
+            tma_load_2d(b, &tmB, &full_bar[s], kb * BK, n0);
+          } else {
+            // W MN-major: 4 chunks of 64 output columns x 64 K rows.
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(b + j * (BK * 128), &tmB, &full_bar[s], n0 + 64 * j, kb * BK);
+          }
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        if (p.any_lora) {
+          const int cb = p.tile_chunk_begin[mb];
+          const int cc = p.tile_chunk_count[mb];
+          for (int ls = 0; ls * 4 < cc; ++ls) {
+            const int nq = min(4, cc - ls * 4);
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nq * (BN / 64) * LORA_CHUNK_BYTES);
+            tma_load_2d(smA + s * A_STAGE_BYTES, &tmAL, &full_bar[s], ls * BK, m0);
+            uint8_t* b = smB + s * B_STAGE_BYTES;
+            for (int q = 0; q < nq; ++q) {
+              const int prow = p.chunks[cb + ls * 4 + q];
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d(b + j * (BK * 128) + q * LORA_CHUNK_BYTES, &tmBP, &full_bar[s],
+                            n0 + 64 * j, prow);
+            }
+            if (++s == STAGES) { s = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_base = make_idesc_bf16(BM, BN, false, !kBwd);
+    constexpr uint32_t idesc_lora = make_idesc_bf16(BM, BN, false, true);
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+      mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(smA + s * A_STAGE_BYTES);
+          const uint32_t b_addr = smem_u32(smB + s * B_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k) {
+            const uint64_t ad = make_sdesc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = kBwd ? make_sdesc_sw128(b_addr + k * 32, 16, 1024)
+                                     : make_sdesc_sw128(b_addr + k * (UK * 128), BK * 128, 1024);
+            mma_bf16_ss(d_tmem, ad, bd, idesc_base, (kb | k) != 0);
+          }
+          mma_commit(&empty_bar[s]);
+        }
+        __syncwarp();
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+      if (p.any_lora) {
+        const int cc = p.tile_chunk_count[mb];
+        for (int ls = 0; ls * 4 < cc; ++ls) {
+          const int nq = min(4, cc - ls * 4);
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(smA + s * A_STAGE_BYTES);
+            const uint32_t b_addr = smem_u32(smB + s * B_STAGE_BYTES);
+            for (int q = 0; q < nq; ++q) {
+              const uint64_t ad = make_sdesc_sw128(a_addr + q * 32, 16, 1024);
+              const uint64_t bd = make_sdesc_sw128(b_addr + q * LORA_CHUNK_BYTES, BK * 128, 1024);
+              mma_bf16_ss(d_tmem, ad, bd, idesc_lora, 1u);
+            }
+            mma_commit(&empty_bar[s]);
+          }
+          __syncwarp();
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+      if (lane == 0) mma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t ew = warp - 4;  // TMEM lane quarter
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+      const int row = mb * BM + ew * 32 + lane;
+      const int n0 = nb * BN;
+      const bool row_ok = row < p.M;
+      DevSeg sg;
+      if (row_ok) sg = p.segs[p.row_seg[row]];
+      mbar_wait(&tfull_bar[acc], acc_ph);
+      tc_fence_after();
+      const int r_local = row_ok ? row - sg.row0 : 0;
+      const bool use_ia3 = row_ok && p.ia3_in_epilogue && (sg.flags & SEGF_IA3);
+      const bool want_base = row_ok && (sg.flags & SEGF_WANT_BASE);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + acc * BN + c * 32 + ((ew * 32u) << 16), r);
+        tmem_wait_ld();
+        const int n = n0 + c * 32;
+        if (!row_ok || n >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const int ncols = min(32, p.N - n);
+        if (p.has_bias) {
+          if (ncols == 32) {
+            const float4* b4 = reinterpret_cast<const float4*>(p.bias + n);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 bb = __ldg(b4 + j);
+              v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
+            }
+          } else {
+            for (int j = 0; j < ncols; ++j) v[j] += __ldg(p.bias + n + j);
+          }
+        }
+        if (want_base) {
+          const bool bf = sg.flags & SEGF_BASE_BF16;
+          char* base = reinterpret_cast<char*>(sg.dst_base) +
+                       ((int64_t)r_local * sg.base_ld + n) * (bf ? 2 : 4);
+          if (ncols == 32 && (sg.flags & SEGF_BASE_VEC)) {
+            if (bf) {
+              uint4* o = reinterpret_cast<uint4*>(base);
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                o[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                                  pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+            } else {
+              float4* o = reinterpret_cast<float4*>(base);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+          } else {
+            for (int j = 0; j < ncols; ++j) {
+              if (bf) reinterpret_cast<__nv_bfloat16*>(base)[j] = __float2bfloat16_rn(v[j]);
+              else reinterpret_cast<float*>(base)[j] = v[j];
+            }
+          }
+        }
+        if (use_ia3) {
+          if (ncols == 32) {
+            const float4* l4 = reinterpret_cast<const float4*>(sg.ia3 + n);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 ll = __ldg(l4 + j);
+              v[4 * j] *= ll.x; v[4 * j + 1] *= ll.y; v[4 * j + 2] *= ll.z; v[4 * j + 3] *= ll.w;
+            }
+          } else {
+            for (int j = 0; j < ncols; ++j) v[j] *= __ldg(sg.ia3 + n + j);
+          }
+        }
+        const bool bf = sg.flags & SEGF_DST_BF16;
+        char* dst = reinterpret_cast<char*>(sg.dst) + ((int64_t)r_local * sg.dst_ld + n) * (bf ? 2 : 4);
+        if (ncols == 32 && (sg.flags & SEGF_DST_VEC)) {
+          if (bf) {
+            uint4* o = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              o[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                                pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+          } else {
+            float4* o = reinterpret_cast<float4*>(dst);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+        } else {
+          for (int j = 0; j < ncols; ++j) {
+            if (bf) reinterpret_cast<__nv_bfloat16*>(dst)[j] = __float2bfloat16_rn(v[j]);
+            else reinterpret_cast<float*>(dst)[j] = v[j];
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ============================================================================ K3 shrink
+// One CTA per (segment, 128-row slab). T[rows, rank_pad] = X[rows, K] . P[rank rows, K]^T,
+// scaled by alpha/r, rounded to bf16 and written into A_lora at this segment's rank-block
+// column of each row's M-tile (zeros elsewhere come from a memset).
+constexpr int SHRINK_STAGES = 4;
+constexpr int SHRINK_MAXN = 256;
+constexpr int SHRINK_B_STAGE = SHRINK_MAXN * BK * 2;  // 32 KB
+constexpr int SHRINK_SMEM = SHRINK_STAGES * (A_STAGE_BYTES + SHRINK_B_STAGE) + 1024 + 256;
+
+struct ShrinkItem {
+  int32_t seg;
+  int32_t row0;  // batch row of this slab
+  int32_t rows;  // <= 128
+  int32_t pad_;
+};
+
+struct ShrinkParams {
+  int K;
+  int lora_ld;  // A_lora row stride (elements)
+  const DevSeg* segs;
+  const ShrinkItem* items;
+  __nv_bfloat16* a_lora;
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    lora_shrink_kernel(const __grid_constant__ CUtensorMap tmA,  // X [M, K]
+                       const __grid_constant__ CUtensorMap tmP,  // pack [R, K] (K-major rows)
+                       const ShrinkParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + SHRINK_STAGES * A_STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smB + SHRINK_STAGES * SHRINK_B_STAGE);
+  uint64_t* empty_bar = full_bar + SHRINK_STAGES;
+  uint64_t* tfull = empty_bar + SHRINK_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const uint32_t warp = warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  const ShrinkItem it = p.items[blockIdx.x];
+  const DevSeg sg = p.segs[it.seg];
+  const int npad = sg.rank_pad;  // multiple of 16, <= 256
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmP);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < SHRINK_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nkb = (p.K + BK - 1) / BK;
+  const int nchunk = npad / LORA_CHUNK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nchunk * LORA_CHUNK_BYTES);
+        tma_load_2d(smA + s * A_STAGE_BYTES, &tmA, &full_bar[s], kb * BK, it.row0);
+        for (int q = 0; q < nchunk; ++q)
+          tma_load_2d(smB + s * SHRINK_B_STAGE + q * LORA_CHUNK_BYTES, &tmP, &full_bar[s], kb * BK,
+                      sg.pack_row + q * LORA_CHUNK);
+        if (++s == SHRINK_STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = make_idesc_bf16(BM, 16, false, false) & ~(0x3Fu << 17);
+    const uint32_t idesc_n = idesc | ((uint32_t)(npad >> 3) << 17);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      mbar_wait(&full_bar[s], ph);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a_addr = smem_u32(smA + s * A_STAGE_BYTES);
+        const uint32_t b_addr = smem_u32(smB + s * SHRINK_B_STAGE);
+#pragma unroll
+        for (int k = 0; k < BK / UK; ++k)
+          mma_bf16_ss(tmem_base, make_sdesc_sw128(a_addr + k * 32, 16, 1024),
+                      make_sdesc_sw128(b_addr + k * 32, 16, 1024), idesc_n, (kb | k) != 0);
+        mma_commit(&empty_bar[s]);
+      }
+      __syncwarp();
+      if (++s == SHRINK_STAGES) { s = 0; ph ^= 1; }
+    }
+    if (lane == 0) mma_commit(tfull);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const uint32_t ew = warp - 4;
+    const int lr = ew * 32 + lane;  // row within slab
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int row = it.row0 + lr;
+    const bool ok = lr < it.rows;
+    const int col0 = ((row >> 7) == (sg.row0 >> 7)) ? sg.lora_col0 : 0;
+    __nv_bfloat16* out = p.a_lora + (int64_t)row * p.lora_ld + col0;
+    for (int c = 0; c < nchunk; ++c) {
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(tmem_base + c * 16 + ((ew * 32u) << 16), r);
+      tmem_wait_ld();
+      if (ok) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) * sg.lora_scale;
+        uint4* o = reinterpret_cast<uint4*>(out + c * 16);
+        o[0] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                          pack_bf16x2(v[6], v[7]));
+        o[1] = make_uint4(pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]),
+                          pack_bf16x2(v[12], v[13]), pack_bf16x2(v[14], v[15]));
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 256);
+  }
+}
+
+// ============================================================================ K4 gather
+struct GatherParams {
+  int M, K;
+  int ldx;
+  int n_seg;
+  int ia3_in_prologue;  // backward: g = dy * l
+  const DevSeg* segs;
+  __nv_bfloat16* X;
+  int32_t* row_seg;
+};
+
+__device__ __forceinline__ int find_seg(const DevSeg* segs, int n, int row) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].row0 <= row) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// One warp per row, grid-stride.
+__global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < p.M; row += gridDim.x * wpb) {
+    const int si = find_seg(p.segs, p.n_seg, row);
+    const DevSeg& sg = p.segs[si];
+    if (lane == 0) p.row_seg[row] = si;
+    const int64_t lr = row - sg.row0;
+    __nv_bfloat16* xr = p.X + (int64_t)row * p.ldx;
+    const bool scale = p.ia3_in_prologue && (sg.flags & SEGF_IA3);
+    const float* l = sg.ia3;
+    const bool vec = (sg.flags & SEGF_SRC_VEC) && ((p.K & 7) == 0);
+    if (sg.flags & SEGF_SRC_BF16) {
+      const __nv_bfloat16* sr = reinterpret_cast<const __nv_bfloat16*>(sg.src) + lr * sg.src_ld;
+      if (vec && !scale) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(sr);
+        uint4* d4 = reinterpret_cast<uint4*>(xr);
+        for (int i = lane; i < p.K / 8; i += 32) d4[i] = __ldg(s4 + i);
+      } else {
+        for (int i = lane; i < p.K; i += 32) {
+          float v = __bfloat162float(sr[i]);
+          if (scale) v *= __ldg(l + i);
+          xr[i] = __float2bfloat16_rn(v);
+        }
+      }
+    } else {
+      const float* sr = reinterpret_cast<const float*>(sg.src) + lr * sg.src_ld;
+      if (vec) {
+        const float4* s4 = reinterpret_cast<const float4*>(sr);
+        uint4* d4 = reinterpret_cast<uint4*>(xr);
+        for (int i = lane; i < p.K / 8; i += 32) {
+          float4 a = __ldg(s4 + 2 * i), b = __ldg(s4 + 2 * i + 1);
+          if (scale) {
+            const float4 la = __ldg(reinterpret_cast<const float4*>(l) + 2 * i);
+            const float4 lb = __ldg(reinterpret_cast<const float4*>(l) + 2 * i + 1);
+            a.x *= la.x; a.y *= la.y; a.z *= la.z; a.w *= la.w;
+            b.x *= lb.x; b.y *= lb.y; b.z *= lb.z; b.w *= lb.w;
+          }
+          d4[i] = make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
+                             pack_bf16x2(b.z, b.w));
+        }
+      } else {
+        for (int i = lane; i < p.K; i += 32) {
+          float v = sr[i];
+          if (scale) v *= __ldg(l + i);
+          xr[i] = __float2bfloat16_rn(v);
+        }
+      }
+    }
+  }
+}
+
+// f32 -> bf16 conversion for weight / pack uploads.
+__global__ void f32_to_bf16_2d_kernel(const float* __restrict__ src, int64_t src_ld,
+                                      __nv_bfloat16* __restrict__ dst, int64_t dst_ld, int rows,
+                                      int cols) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    dst[r * dst_ld + c] = __float2bfloat16_rn(src[r * src_ld + c]);
+  }
+}
+
+// Transposing copy: dst[c, r] = src[r, c]  (A [d_in, r] -> A^T pack rows), f32 or bf16 source.
+__global__ void transpose_to_bf16_kernel(const void* __restrict__ src, int src_bf16, int64_t src_ld,
+                                         __nv_bfloat16* __restrict__ dst, int64_t dst_ld, int rows,
+                                         int cols) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const float v = src_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[r * src_ld + c])
+                             : reinterpret_cast<const float*>(src)[r * src_ld + c];
+    dst[c * dst_ld + r] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void copy_to_bf16_kernel(const void* __restrict__ src, int src_bf16, int64_t src_ld,
+                                    __nv_bfloat16* __restrict__ dst, int64_t dst_ld, int rows,
+                                    int cols) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const float v = src_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[r * src_ld + c])
+                             : reinterpret_cast<const float*>(src)[r * src_ld + c];
+    dst[r * dst_ld + c] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void copy_to_f32_kernel(const void* __restrict__ src, int src_bf16,
+                                   float* __restrict__ dst, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = src_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[i])
+                      : reinterpret_cast<const float*>(src)[i];
+}
+
+}  // namespace ss

@@ -1,0 +1,713 @@
+// Host side of the C ABI declared in include/ss_b200.h.
+//
+// Owns: bf16 copies of the frozen layers (+ f32 bias), per-layer LoRA packs (A^T and B rows of
+// every registered client, 16-row aligned), IA3 vectors, and a grow-only transient workspace
+// (the concatenated operand X, the block-diagonal LoRA operand, routing tables). Everything
+// the reference keeps per request (executor.py:191-231) is rebuilt per dispatch; nothing
+// survives a dispatch except weights and adapters (statelessness, executor.py:1-9).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/ss_b200.h"
+#include "kernels.cuh"
+
+using namespace ss;
+
+namespace {
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+constexpr int kStagingSlots = 16;
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+struct AdapterSlot {
+  uint32_t kind = 0;
+  int rank = 0, rank_pad = 0, pack_row = -1;
+  float scale = 0.f;
+  float* ia3 = nullptr;  // device [d_out]
+};
+
+struct Layer {
+  int block = 0, role = 0, d_in = 0, d_out = 0;
+  __nv_bfloat16* W = nullptr;
+  int64_t ldw = 0;
+  float* bias = nullptr;
+  CUtensorMap tm_w_fwd, tm_w_bwd;
+  // LoRA packs: rows = rank index of every registered client (16-aligned blocks)
+  __nv_bfloat16* at_pack = nullptr;  // [cap, ld_at]  (A^T: rank rows x d_in)
+  __nv_bfloat16* b_pack = nullptr;   // [cap, ld_b]   (B:   rank rows x d_out)
+  int64_t ld_at = 0, ld_b = 0;
+  int pack_rows = 0, pack_cap = 0;
+  CUtensorMap tm_at, tm_b;
+  std::map<uint32_t, AdapterSlot> adapters;
+};
+
+struct Staging {
+  void* host = nullptr;     // pinned
+  void* dev = nullptr;      // device copy of the tables
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  bool pending = false;
+};
+
+}  // namespace
+
+struct ss_ctx {
+  int device = 0, tp_rank = 0, tp_size = 1, num_sms = 148;
+  std::string err;
+  PFN_encodeTiled_t encode = nullptr;
+  std::map<std::pair<int, int>, Layer> layers;
+  // workspace
+  __nv_bfloat16* X = nullptr;
+  size_t x_cap = 0;
+  __nv_bfloat16* a_lora = nullptr;
+  size_t al_cap = 0;
+  int32_t* row_seg = nullptr;
+  size_t rs_cap = 0;
+  size_t ws_high = 0;
+  Staging staging[kStagingSlots];
+  int slot = 0;
+  cudaStream_t upload = nullptr;
+  cudaEvent_t upload_done = nullptr, compute_done = nullptr;
+  bool any_compute = false;
+  int64_t launches = 0;
+  int group_m = 16;
+  int64_t weight_bytes = 0, adapter_bytes = 0;
+};
+
+namespace {
+
+int fail(ss_ctx* c, int code, const char* fmt, ...) {
+  if (c) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return code;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(ctx, SS_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                   \
+  } while (0)
+
+int encode_2d(ss_ctx* ctx, CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+              uint64_t ld_elems, uint32_t box_cols, uint32_t box_rows) {
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ctx, SS_E_CUDA, "cuTensorMapEncodeTiled failed (%d) cols=%llu rows=%llu ld=%llu",
+                (int)r, (unsigned long long)cols, (unsigned long long)rows,
+                (unsigned long long)ld_elems);
+  return SS_OK;
+}
+
+// Copy a [rows, cols] matrix (host/device, f32/bf16, row stride src_ld) into a bf16 device
+// destination, optionally transposed. Synchronous with respect to the source buffer.
+int upload_bf16(ss_ctx* ctx, const void* src, uint32_t flags, int rows, int cols, int64_t src_ld,
+                __nv_bfloat16* dst, int64_t dst_ld, bool transpose) {
+  const bool src_bf16 = flags & SS_DT_BF16;
+  const size_t esz = src_bf16 ? 2 : 4;
+  const void* dsrc = src;
+  void* tmp = nullptr;
+  if (!(flags & SS_MEM_DEVICE)) {
+    const size_t bytes = (size_t)rows * src_ld * esz;
+    CK(cudaMallocAsync(&tmp, std::max<size_t>(bytes, 16), ctx->upload));
+    CK(cudaMemcpyAsync(tmp, src, bytes, cudaMemcpyHostToDevice, ctx->upload));
+    dsrc = tmp;
+  }
+  const int64_t total = (int64_t)rows * cols;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+  if (total > 0) {
+    if (transpose)
+      transpose_to_bf16_kernel<<<grid, 256, 0, ctx->upload>>>(dsrc, src_bf16, src_ld, dst, dst_ld,
+                                                              rows, cols);
+    else
+      copy_to_bf16_kernel<<<grid, 256, 0, ctx->upload>>>(dsrc, src_bf16, src_ld, dst, dst_ld, rows,
+                                                         cols);
+    CK(cudaGetLastError());
+  }
+  if (tmp) CK(cudaFreeAsync(tmp, ctx->upload));
+  CK(cudaStreamSynchronize(ctx->upload));
+  return SS_OK;
+}
+
+int upload_f32(ss_ctx* ctx, const void* src, uint32_t flags, int n, float* dst) {
+  const bool src_bf16 = flags & SS_DT_BF16;
+  const size_t bytes = (size_t)n * (src_bf16 ? 2 : 4);
+  if (!(flags & SS_MEM_DEVICE) && !src_bf16) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->upload));
+  } else {
+    const void* dsrc = src;
+    void* tmp = nullptr;
+    if (!(flags & SS_MEM_DEVICE)) {
+      CK(cudaMallocAsync(&tmp, std::max<size_t>(bytes, 16), ctx->upload));
+      CK(cudaMemcpyAsync(tmp, src, bytes, cudaMemcpyHostToDevice, ctx->upload));
+      dsrc = tmp;
+    }
+    copy_to_f32_kernel<<<std::max(1, std::min((n + 255) / 256, 1024)), 256, 0, ctx->upload>>>(
+        dsrc, src_bf16, dst, n);
+    CK(cudaGetLastError());
+    if (tmp) CK(cudaFreeAsync(tmp, ctx->upload));
+  }
+  CK(cudaStreamSynchronize(ctx->upload));
+  return SS_OK;
+}
+
+// Uploads must not overwrite packs that an in-flight dispatch still reads.
+int upload_begin(ss_ctx* ctx) {
+  if (ctx->any_compute) CK(cudaStreamWaitEvent(ctx->upload, ctx->compute_done, 0));
+  return SS_OK;
+}
+int upload_end(ss_ctx* ctx) {
+  CK(cudaEventRecord(ctx->upload_done, ctx->upload));
+  return SS_OK;
+}
+
+int grow_packs(ss_ctx* ctx, Layer& L, int need_rows) {
+  if (need_rows <= L.pack_cap) return SS_OK;
+  int cap = std::max(64, L.pack_cap);
+  while (cap < need_rows) cap *= 2;
+  __nv_bfloat16 *at = nullptr, *b = nullptr;
+  CK(cudaMalloc(&at, (size_t)cap * L.ld_at * 2));
+  CK(cudaMalloc(&b, (size_t)cap * L.ld_b * 2));
+  CK(cudaMemsetAsync(at, 0, (size_t)cap * L.ld_at * 2, ctx->upload));
+  CK(cudaMemsetAsync(b, 0, (size_t)cap * L.ld_b * 2, ctx->upload));
+  if (L.pack_rows > 0) {
+    CK(cudaMemcpyAsync(at, L.at_pack, (size_t)L.pack_rows * L.ld_at * 2, cudaMemcpyDeviceToDevice,
+                       ctx->upload));
+    CK(cudaMemcpyAsync(b, L.b_pack, (size_t)L.pack_rows * L.ld_b * 2, cudaMemcpyDeviceToDevice,
+                       ctx->upload));
+  }
+  CK(cudaStreamSynchronize(ctx->upload));
+  if (L.at_pack) {
+    CK(cudaFree(L.at_pack));
+    CK(cudaFree(L.b_pack));
+    ctx->adapter_bytes -= (int64_t)L.pack_cap * (L.ld_at + L.ld_b) * 2;
+  }
+  L.at_pack = at;
+  L.b_pack = b;
+  L.pack_cap = cap;
+  ctx->adapter_bytes += (int64_t)cap * (L.ld_at + L.ld_b) * 2;
+  int rc = encode_2d(ctx, &L.tm_at, L.at_pack, L.d_in, cap, L.ld_at, 64, LORA_CHUNK);
+  if (rc) return rc;
+  return encode_2d(ctx, &L.tm_b, L.b_pack, L.d_out, cap, L.ld_b, 64, LORA_CHUNK);
+}
+
+template <typename T>
+int ensure_dev(ss_ctx* ctx, T*& ptr, size_t& cap, size_t bytes) {
+  if (bytes <= cap) return SS_OK;
+  size_t n = std::max(bytes, cap + cap / 2);
+  n = round_up((int64_t)n, 1 << 20);
+  if (ptr) CK(cudaFree(ptr));
+  ptr = nullptr;
+  cap = 0;
+  CK(cudaMalloc(reinterpret_cast<void**>(&ptr), n));
+  cap = n;
+  return SS_OK;
+}
+
+bool aligned16(const void* p, int64_t ld, size_t esz) {
+  return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * (int64_t)esz) % 16 == 0);
+}
+
+struct KernelAttrs {
+  bool done = false;
+};
+KernelAttrs g_attrs;
+
+int set_kernel_attrs(ss_ctx* ctx) {
+  if (g_attrs.done) return SS_OK;
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          GEMM_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          GEMM_SMEM));
+  CK(cudaFuncSetAttribute(lora_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          SHRINK_SMEM));
+  g_attrs.done = true;
+  return SS_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+const char* ss_version(void) {
+  return "ss_b200 1.0 (sm_100a tcgen05/TMEM/TMA segmented executor; BM=128 BN=256 BK=64)";
+}
+
+const char* ss_last_error(const ss_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out) {
+  if (!out) return SS_E_ARG;
+  *out = nullptr;
+  ss_ctx* ctx = new ss_ctx();
+  ctx->device = device;
+  ctx->tp_rank = tp_rank;
+  ctx->tp_size = tp_size;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return SS_E_CUDA;
+  }
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (major != 10) {
+    delete ctx;
+    return SS_E_UNSUPPORTED;  // sm_100a only
+  }
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || !fn) {
+    delete ctx;
+    return SS_E_CUDA;
+  }
+  ctx->encode = reinterpret_cast<PFN_encodeTiled_t>(fn);
+  if (cudaStreamCreateWithFlags(&ctx->upload, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->upload_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->compute_done, cudaEventDisableTiming) != cudaSuccess) {
+    delete ctx;
+    return SS_E_CUDA;
+  }
+  for (auto& s : ctx->staging) {
+    if (cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming) != cudaSuccess) {
+      delete ctx;
+      return SS_E_CUDA;
+    }
+  }
+  if (set_kernel_attrs(ctx) != SS_OK) {
+    delete ctx;
+    return SS_E_CUDA;
+  }
+  cudaEventRecord(ctx->upload_done, ctx->upload);
+  *out = ctx;
+  return SS_OK;
+}
+
+int ss_ctx_destroy(ss_ctx* ctx) {
+  if (!ctx) return SS_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : ctx->layers) {
+    Layer& L = kv.second;
+    cudaFree(L.W);
+    cudaFree(L.bias);
+    cudaFree(L.at_pack);
+    cudaFree(L.b_pack);
+    for (auto& a : L.adapters) cudaFree(a.second.ia3);
+  }
+  cudaFree(ctx->X);
+  cudaFree(ctx->a_lora);
+  cudaFree(ctx->row_seg);
+  for (auto& s : ctx->staging) {
+    cudaFreeHost(s.host);
+    cudaFree(s.dev);
+    cudaEventDestroy(s.done);
+  }
+  cudaEventDestroy(ctx->upload_done);
+  cudaEventDestroy(ctx->compute_done);
+  cudaStreamDestroy(ctx->upload);
+  delete ctx;
+  return SS_OK;
+}
+
+int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
+  if (!ctx || !key) return SS_E_ARG;
+  if (!strcmp(key, "group_m")) {
+    if (value < 1) return fail(ctx, SS_E_ARG, "group_m must be >= 1");
+    ctx->group_m = (int)value;
+    return SS_OK;
+  }
+  return fail(ctx, SS_E_ARG, "unknown option %s", key);
+}
+
+int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const void* weight,
+                  int64_t w_ld, const void* bias, uint32_t flags) {
+  if (!ctx) return SS_E_ARG;
+  if (d_in <= 0 || d_out <= 0 || !weight || w_ld < d_out)
+    return fail(ctx, SS_E_ARG, "bad layer dims d_in=%d d_out=%d ld=%lld", d_in, d_out,
+                (long long)w_ld);
+  CK(cudaSetDevice(ctx->device));
+  ss_unload_layer(ctx, block, role);
+  Layer L;
+  L.block = block;
+  L.role = role;
+  L.d_in = d_in;
+  L.d_out = d_out;
+  L.ldw = round_up(d_out, 64);
+  L.ld_at = round_up(d_in, 64);
+  L.ld_b = round_up(d_out, 64);
+  CK(cudaMalloc(&L.W, (size_t)d_in * L.ldw * 2));
+  CK(cudaMemsetAsync(L.W, 0, (size_t)d_in * L.ldw * 2, ctx->upload));
+  int rc = upload_bf16(ctx, weight, flags, d_in, d_out, w_ld, L.W, L.ldw, false);
+  if (rc) { cudaFree(L.W); return rc; }
+  if (bias) {
+    CK(cudaMalloc(&L.bias, (size_t)round_up(d_out, 64) * 4));
+    CK(cudaMemsetAsync(L.bias, 0, (size_t)round_up(d_out, 64) * 4, ctx->upload));
+    rc = upload_f32(ctx, bias, flags, d_out, L.bias);
+    if (rc) return rc;
+  }
+  rc = encode_2d(ctx, &L.tm_w_fwd, L.W, d_out, d_in, L.ldw, 64, BK);
+  if (rc) return rc;
+  rc = encode_2d(ctx, &L.tm_w_bwd, L.W, d_out, d_in, L.ldw, 64, BN);
+  if (rc) return rc;
+  ctx->weight_bytes += (int64_t)d_in * L.ldw * 2 + (bias ? round_up(d_out, 64) * 4 : 0);
+  ctx->layers[{block, role}] = L;
+  return SS_OK;
+}
+
+int ss_unload_layer(ss_ctx* ctx, int block, int role) {
+  if (!ctx) return SS_E_ARG;
+  auto it = ctx->layers.find({block, role});
+  if (it == ctx->layers.end()) return SS_E_NOLAYER;
+  cudaDeviceSynchronize();
+  Layer& L = it->second;
+  ctx->weight_bytes -= (int64_t)L.d_in * L.ldw * 2 + (L.bias ? round_up(L.d_out, 64) * 4 : 0);
+  cudaFree(L.W);
+  cudaFree(L.bias);
+  if (L.at_pack) ctx->adapter_bytes -= (int64_t)L.pack_cap * (L.ld_at + L.ld_b) * 2;
+  cudaFree(L.at_pack);
+  cudaFree(L.b_pack);
+  for (auto& a : L.adapters) {
+    if (a.second.ia3) ctx->adapter_bytes -= (int64_t)L.d_out * 4;
+    cudaFree(a.second.ia3);
+  }
+  ctx->layers.erase(it);
+  return SS_OK;
+}
+
+int ss_set_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role, uint32_t kind, int rank,
+                   float scale, const void* A, const void* B, const void* l, uint32_t flags) {
+  if (!ctx) return SS_E_ARG;
+  auto it = ctx->layers.find({block, role});
+  if (it == ctx->layers.end())
+    return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", block, role);
+  Layer& L = it->second;
+  if (kind == 0 || (kind & ~(SS_ADAPTER_LORA | SS_ADAPTER_IA3)))
+    return fail(ctx, SS_E_ARG, "bad adapter kind %u", kind);
+  if ((kind & SS_ADAPTER_LORA) && (rank <= 0 || rank > SHRINK_MAXN || !A || !B))
+    return fail(ctx, SS_E_ARG, "LoRA needs 1 <= rank <= %d and A, B (rank=%d)", SHRINK_MAXN, rank);
+  if ((kind & SS_ADAPTER_IA3) && !l) return fail(ctx, SS_E_ARG, "IA3 needs l");
+  CK(cudaSetDevice(ctx->device));
+  int rc = upload_begin(ctx);
+  if (rc) return rc;
+  AdapterSlot& s = L.adapters[client_id];
+  if (kind & SS_ADAPTER_LORA) {
+    const int rp = (int)round_up(rank, LORA_CHUNK);
+    if (s.pack_row < 0 || s.rank_pad != rp) {
+      // new block at the end of the packs (old block, if any, is abandoned: zero cost to
+      // correctness since no segment references it any more)
+      rc = grow_packs(ctx, L, L.pack_rows + rp);
+      if (rc) return rc;
+      s.pack_row = L.pack_rows;
+      s.rank_pad = rp;
+      L.pack_rows += rp;
+    }
+    s.rank = rank;
+    s.scale = scale;
+    // zero the padding rows, then A^T rows [pack_row, pack_row + rank) and B rows
+    CK(cudaMemsetAsync(L.at_pack + (int64_t)s.pack_row * L.ld_at, 0, (size_t)rp * L.ld_at * 2,
+                       ctx->upload));
+    CK(cudaMemsetAsync(L.b_pack + (int64_t)s.pack_row * L.ld_b, 0, (size_t)rp * L.ld_b * 2,
+                       ctx->upload));
+    rc = upload_bf16(ctx, A, flags, L.d_in, rank, rank, L.at_pack + (int64_t)s.pack_row * L.ld_at,
+                     L.ld_at, /*transpose=*/true);
+    if (rc) return rc;
+    rc = upload_bf16(ctx, B, flags, rank, L.d_out, L.d_out,
+                     L.b_pack + (int64_t)s.pack_row * L.ld_b, L.ld_b, false);
+    if (rc) return rc;
+  }
+  if (kind & SS_ADAPTER_IA3) {
+    if (!s.ia3) {
+      CK(cudaMalloc(&s.ia3, (size_t)round_up(L.d_out, 64) * 4));
+      CK(cudaMemsetAsync(s.ia3, 0, (size_t)round_up(L.d_out, 64) * 4, ctx->upload));
+      ctx->adapter_bytes += (int64_t)L.d_out * 4;
+    }
+    rc = upload_f32(ctx, l, flags, L.d_out, s.ia3);
+    if (rc) return rc;
+  }
+  s.kind = kind;
+  return upload_end(ctx);
+}
+
+int ss_clear_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role) {
+  if (!ctx) return SS_E_ARG;
+  auto it = ctx->layers.find({block, role});
+  if (it == ctx->layers.end()) return SS_E_NOLAYER;
+  auto a = it->second.adapters.find(client_id);
+  if (a == it->second.adapters.end()) return SS_OK;
+  if (a->second.ia3) {
+    cudaDeviceSynchronize();
+    cudaFree(a->second.ia3);
+    ctx->adapter_bytes -= (int64_t)it->second.d_out * 4;
+  }
+  it->second.adapters.erase(a);
+  return SS_OK;
+}
+
+int ss_clear_client(ss_ctx* ctx, uint32_t client_id) {
+  if (!ctx) return SS_E_ARG;
+  for (auto& kv : ctx->layers) ss_clear_adapter(ctx, client_id, kv.first.first, kv.first.second);
+  return SS_OK;
+}
+
+int ss_memory_stats(const ss_ctx* ctx, int64_t* w, int64_t* a, int64_t* ws) {
+  if (!ctx) return SS_E_ARG;
+  if (w) *w = ctx->weight_bytes;
+  if (a) *a = ctx->adapter_bytes;
+  if (ws) *ws = (int64_t)ctx->ws_high;
+  return SS_OK;
+}
+
+int64_t ss_kernel_launches(const ss_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
+                     void* stream_, int32_t* seg_status) {
+  if (!ctx) return SS_E_ARG;
+  if (pass_kind < 0 || pass_kind > 2) return fail(ctx, SS_E_ARG, "unknown pass %d", pass_kind);
+  if (n_seg < 0 || (n_seg > 0 && (!segs || !seg_status)))
+    return fail(ctx, SS_E_ARG, "bad segment array");
+  auto lit = ctx->layers.find({block, role});
+  if (lit == ctx->layers.end())
+    return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", block, role);
+  Layer& L = lit->second;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const bool bwd = pass_kind == SS_PASS_BACKWARD;
+  const bool noise = pass_kind == SS_PASS_NOISE_EFFECT;
+  const int K = bwd ? L.d_out : L.d_in;
+  const int N = bwd ? L.d_in : L.d_out;
+
+  // ---- validate + build device segment records (batch order == envelope order)
+  std::vector<DevSeg> ds;
+  ds.reserve(n_seg);
+  int64_t M = 0;
+  bool any_lora = false;
+  for (int i = 0; i < n_seg; ++i) {
+    const ss_seg& s = segs[i];
+    seg_status[i] = SS_SEG_OK;
+    if ((int)s.width != K) { seg_status[i] = SS_SEG_BAD_WIDTH; continue; }
+    if (s.rows == 0) continue;
+    if (!s.src || !s.dst || s.src_ld < K || s.dst_ld < N) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
+    DevSeg d{};
+    d.row0 = (int32_t)M;
+    d.rows = (int32_t)s.rows;
+    d.src = s.src;
+    d.src_ld = s.src_ld;
+    d.dst = s.dst;
+    d.dst_ld = s.dst_ld;
+    d.pack_row = -1;
+    int f = 0;
+    if (s.flags & SS_SEGF_SRC_BF16) f |= SEGF_SRC_BF16;
+    if (s.flags & SS_SEGF_DST_BF16) f |= SEGF_DST_BF16;
+    if (aligned16(s.src, s.src_ld, (s.flags & SS_SEGF_SRC_BF16) ? 2 : 4)) f |= SEGF_SRC_VEC;
+    if (aligned16(s.dst, s.dst_ld, (s.flags & SS_SEGF_DST_BF16) ? 2 : 4)) f |= SEGF_DST_VEC;
+    if ((s.flags & SS_SEGF_ADAPTER) && !noise) {
+      auto a = L.adapters.find(s.client_id);
+      if (a == L.adapters.end()) { seg_status[i] = SS_SEG_NO_ADAPTER; continue; }
+      const AdapterSlot& as = a->second;
+      if (as.kind & SS_ADAPTER_LORA) {
+        f |= SEGF_LORA;
+        d.pack_row = as.pack_row;
+        d.rank_pad = as.rank_pad;
+        d.lora_scale = as.scale;
+        any_lora = true;
+      }
+      if (as.kind & SS_ADAPTER_IA3) {
+        f |= SEGF_IA3;
+        d.ia3 = as.ia3;
+      }
+    }
+    if (s.dst_base && pass_kind == SS_PASS_FORWARD) {
+      if (s.base_ld < N) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
+      f |= SEGF_WANT_BASE;
+      if (s.flags & SS_SEGF_BASE_BF16) f |= SEGF_BASE_BF16;
+      if (aligned16(s.dst_base, s.base_ld, (s.flags & SS_SEGF_BASE_BF16) ? 2 : 4)) f |= SEGF_BASE_VEC;
+      d.dst_base = s.dst_base;
+      d.base_ld = s.base_ld;
+    }
+    d.flags = f;
+    ds.push_back(d);
+    M += s.rows;
+  }
+  if (M == 0) return SS_OK;
+  if (M > (int64_t)1 << 30) return fail(ctx, SS_E_ARG, "batch too large (%lld rows)", (long long)M);
+  CK(cudaSetDevice(ctx->device));
+
+  // ---- M-tile tables for the block-diagonal LoRA operand
+  const int num_m = (int)((M + BM - 1) / BM);
+  std::vector<int32_t> t_begin(num_m, 0), t_count(num_m, 0), chunks;
+  std::vector<ShrinkItem> items;
+  int max_cols = 0;
+  if (any_lora) {
+    size_t si = 0;
+    for (int mt = 0; mt < num_m; ++mt) {
+      const int64_t r0 = (int64_t)mt * BM, r1 = std::min<int64_t>(M, r0 + BM);
+      while (si < ds.size() && ds[si].row0 + ds[si].rows <= r0) ++si;
+      t_begin[mt] = (int32_t)chunks.size();
+      for (size_t j = si; j < ds.size() && ds[j].row0 < r1; ++j) {
+        DevSeg& d = ds[j];
+        if (!(d.flags & SEGF_LORA)) continue;
+        const int col = (int)(chunks.size() - t_begin[mt]) * LORA_CHUNK;
+        if ((d.row0 >> 7) == mt) d.lora_col0 = col;
+        for (int q = 0; q < d.rank_pad / LORA_CHUNK; ++q) chunks.push_back(d.pack_row + q * LORA_CHUNK);
+      }
+      t_count[mt] = (int32_t)chunks.size() - t_begin[mt];
+      max_cols = std::max(max_cols, t_count[mt] * LORA_CHUNK);
+    }
+    for (size_t j = 0; j < ds.size(); ++j) {
+      if (!(ds[j].flags & SEGF_LORA)) continue;
+      for (int r = 0; r < ds[j].rows; r += BM)
+        items.push_back(ShrinkItem{(int32_t)j, ds[j].row0 + r, std::min(BM, ds[j].rows - r), 0});
+    }
+    if (chunks.empty()) chunks.push_back(0);
+  }
+  const int64_t lora_ld = std::max<int64_t>(64, round_up(max_cols, 64));
+
+  // ---- workspace
+  const int64_t ldx = round_up(K, 64);
+  const int64_t m_pad = (int64_t)num_m * BM;
+  int rc = ensure_dev(ctx, ctx->X, ctx->x_cap, (size_t)m_pad * ldx * 2);
+  if (rc) return rc;
+  rc = ensure_dev(ctx, ctx->row_seg, ctx->rs_cap, (size_t)m_pad * 4);
+  if (rc) return rc;
+  if (any_lora) {
+    rc = ensure_dev(ctx, ctx->a_lora, ctx->al_cap, (size_t)m_pad * lora_ld * 2);
+    if (rc) return rc;
+  }
+  ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap);
+
+  // ---- routing tables -> pinned staging slot -> device (one async copy)
+  const size_t off_seg = 0;
+  const size_t off_tb = round_up(ds.size() * sizeof(DevSeg), 256);
+  const size_t off_tc = off_tb + round_up(t_begin.size() * 4, 256);
+  const size_t off_ch = off_tc + round_up(t_count.size() * 4, 256);
+  const size_t off_it = off_ch + round_up(chunks.size() * 4, 256);
+  const size_t total = off_it + round_up(std::max<size_t>(1, items.size()) * sizeof(ShrinkItem), 256);
+  Staging& st = ctx->staging[ctx->slot];
+  ctx->slot = (ctx->slot + 1) % kStagingSlots;
+  if (st.pending) CK(cudaEventSynchronize(st.done));
+  if (st.cap < total) {
+    if (st.host) CK(cudaFreeHost(st.host));
+    if (st.dev) CK(cudaFree(st.dev));
+    st.host = nullptr;
+    st.dev = nullptr;
+    st.cap = 0;
+    const size_t cap = round_up((int64_t)std::max(total, (size_t)1 << 16), 1 << 16);
+    CK(cudaMallocHost(&st.host, cap));
+    CK(cudaMalloc(&st.dev, cap));
+    st.cap = cap;
+  }
+  char* h = static_cast<char*>(st.host);
+  memcpy(h + off_seg, ds.data(), ds.size() * sizeof(DevSeg));
+  if (any_lora) {
+    memcpy(h + off_tb, t_begin.data(), t_begin.size() * 4);
+    memcpy(h + off_tc, t_count.data(), t_count.size() * 4);
+    memcpy(h + off_ch, chunks.data(), chunks.size() * 4);
+    memcpy(h + off_it, items.data(), items.size() * sizeof(ShrinkItem));
+  }
+  // adapters uploaded on the side stream must be complete before this dispatch reads them
+  CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
+  CK(cudaMemcpyAsync(st.dev, st.host, any_lora ? total : off_tb, cudaMemcpyHostToDevice, stream));
+  CK(cudaEventRecord(st.done, stream));
+  st.pending = true;
+  char* dv = static_cast<char*>(st.dev);
+  const DevSeg* d_segs = reinterpret_cast<const DevSeg*>(dv + off_seg);
+
+  // ---- K4 gather
+  GatherParams gp;
+  gp.M = (int)M;
+  gp.K = K;
+  gp.ldx = (int)ldx;
+  gp.n_seg = (int)ds.size();
+  gp.ia3_in_prologue = bwd ? 1 : 0;
+  gp.segs = d_segs;
+  gp.X = ctx->X;
+  gp.row_seg = ctx->row_seg;
+  {
+    const int grid = (int)std::min<int64_t>((M + 7) / 8, (int64_t)ctx->num_sms * 8);
+    gather_rows_kernel<<<grid, 256, 0, stream>>>(gp);
+    CK(cudaGetLastError());
+    ctx->launches++;
+  }
+
+  CUtensorMap tmA, tmAL;
+  rc = encode_2d(ctx, &tmA, ctx->X, K, M, ldx, 64, BM);
+  if (rc) return rc;
+  if (any_lora) {
+    rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, M, lora_ld, 64, BM);
+    if (rc) return rc;
+    // ---- K3 shrink into the zeroed block-diagonal operand
+    CK(cudaMemsetAsync(ctx->a_lora, 0, (size_t)m_pad * lora_ld * 2, stream));
+    ShrinkParams sp;
+    sp.K = K;
+    sp.lora_ld = (int)lora_ld;
+    sp.segs = d_segs;
+    sp.items = reinterpret_cast<const ShrinkItem*>(dv + off_it);
+    sp.a_lora = ctx->a_lora;
+    lora_shrink_kernel<<<(int)items.size(), GEMM_THREADS, SHRINK_SMEM, stream>>>(
+        tmA, bwd ? L.tm_b : L.tm_at, sp);
+    CK(cudaGetLastError());
+    ctx->launches++;
+  } else {
+    tmAL = tmA;  // unused
+  }
+
+  // ---- K1 / K2 / K5 fused GEMM
+  GemmParams gpm;
+  gpm.M = (int)M;
+  gpm.N = N;
+  gpm.K = K;
+  gpm.num_m_tiles = num_m;
+  gpm.num_n_tiles = (N + BN - 1) / BN;
+  gpm.group_m = ctx->group_m;
+  gpm.has_bias = (pass_kind == SS_PASS_FORWARD && L.bias) ? 1 : 0;
+  gpm.any_lora = any_lora ? 1 : 0;
+  gpm.bias = L.bias;
+  gpm.segs = d_segs;
+  gpm.row_seg = ctx->row_seg;
+  gpm.tile_chunk_begin = reinterpret_cast<const int32_t*>(dv + off_tb);
+  gpm.tile_chunk_count = reinterpret_cast<const int32_t*>(dv + off_tc);
+  gpm.chunks = reinterpret_cast<const int32_t*>(dv + off_ch);
+  gpm.ia3_in_epilogue = (pass_kind == SS_PASS_FORWARD) ? 1 : 0;
+  const int tiles = gpm.num_m_tiles * gpm.num_n_tiles;
+  const int grid = std::min(tiles, ctx->num_sms);
+  const CUtensorMap& tmBP = any_lora ? (bwd ? L.tm_at : L.tm_b) : tmA;
+  if (bwd)
+    seg_gemm_kernel<true><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, L.tm_w_bwd, tmAL, tmBP, gpm);
+  else
+    seg_gemm_kernel<false><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, L.tm_w_fwd, tmAL, tmBP, gpm);
+  CK(cudaGetLastError());
+  ctx->launches++;
+  CK(cudaEventRecord(ctx->compute_done, stream));
+  ctx->any_compute = true;
+  return SS_OK;
+}
+
+}  // extern "C"
