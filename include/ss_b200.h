@@ -26,6 +26,12 @@
 
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define SS_API __attribute__((visibility("default")))
+#else
+#define SS_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -84,43 +90,43 @@ typedef struct ss_ctx ss_ctx;
 
 /* Create a context on CUDA device `device`. tp_rank / tp_size describe this process's
  * tensor-parallel position (metadata; sharding is expressed through the shards loaded). */
-int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out);
-int ss_ctx_destroy(ss_ctx* ctx);
-const char* ss_last_error(const ss_ctx* ctx);
+SS_API int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out);
+SS_API int ss_ctx_destroy(ss_ctx* ctx);
+SS_API const char* ss_last_error(const ss_ctx* ctx);
 /* Library version / build string, usable without a GPU. */
-const char* ss_version(void);
+SS_API const char* ss_version(void);
 
 /* Load one frozen affine layer (AffineParams, tensor_ops.py:39-68): weight [d_in, d_out]
  * row-major with row stride w_ld elements, optional bias [d_out]. Stored as bf16. */
-int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const void* weight,
+SS_API int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const void* weight,
                   int64_t w_ld, const void* bias, uint32_t flags);
-int ss_unload_layer(ss_ctx* ctx, int block, int role);
+SS_API int ss_unload_layer(ss_ctx* ctx, int block, int role);
 
 /* Register / refresh a client's adapter for one layer. LoRA: A [d_in, rank], B [rank, d_out],
  * scale = alpha / rank (lora_forward adapters.py:19-23). IA3: l [d_out] (adapters.py:142-144).
  * kind is a mask of SS_ADAPTER_*; pointers of kinds not in the mask may be NULL.
  * Refreshing with the same rank re-packs in place (call after every optimizer step). */
-int ss_set_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role, uint32_t kind, int rank,
+SS_API int ss_set_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role, uint32_t kind, int rank,
                    float scale, const void* A, const void* B, const void* l, uint32_t flags);
-int ss_clear_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role);
+SS_API int ss_clear_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role);
 /* Drop every adapter of a client (deregister). */
-int ss_clear_client(ss_ctx* ctx, uint32_t client_id);
+SS_API int ss_clear_client(ss_ctx* ctx, uint32_t client_id);
 
 /* Compute one batch for layer (block, role) and pass. `stream` is a cudaStream_t (NULL =
  * legacy default stream). Asynchronous: results are visible after the stream reaches this
  * point. seg_status[n_seg] receives per-segment status; rejected segments are not written. */
-int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
+SS_API int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
                      const ss_seg* segs, void* stream, int32_t* seg_status);
 
 /* Device bytes held: weights (+bias), adapter packs, transient workspace high-water mark. */
-int ss_memory_stats(const ss_ctx* ctx, int64_t* weight_bytes, int64_t* adapter_bytes,
+SS_API int ss_memory_stats(const ss_ctx* ctx, int64_t* weight_bytes, int64_t* adapter_bytes,
                     int64_t* workspace_bytes);
 
 /* Number of kernels launched by this context since creation (evidence / bench counter). */
-int64_t ss_kernel_launches(const ss_ctx* ctx);
+SS_API int64_t ss_kernel_launches(const ss_ctx* ctx);
 
 /* Tuning knob: M-tile grouping of the persistent raster (default 16). */
-int ss_set_option(ss_ctx* ctx, const char* key, int64_t value);
+SS_API int ss_set_option(ss_ctx* ctx, const char* key, int64_t value);
 
 #ifdef __cplusplus
 }

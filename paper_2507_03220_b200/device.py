@@ -1,0 +1,220 @@
+"""SsContext — owner of one libss_b200 context (one CUDA device, one TP rank).
+
+Thin, allocation-free translation from torch/numpy objects to the C ABI of
+include/ss_b200.h. The executor (executor.py) drives it; benchmarks may drive it directly
+with prebuilt segment tables (``SegmentTable``) to keep host overhead per dispatch at one
+ctypes call.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Any, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import SsSeg, check
+
+
+def _host_or_device(arr) -> tuple[Any, int, int, Any]:
+    """Returns (pointer, flags, row_stride_elems, keepalive) for an upload source."""
+    if isinstance(arr, torch.Tensor):
+        t = arr
+        if t.dtype not in (torch.float32, torch.bfloat16):
+            t = t.float()
+        if t.dim() == 2 and t.stride(1) != 1:
+            t = t.contiguous()
+        if t.dim() == 1:
+            t = t.contiguous()
+        flags = _lib.SS_DT_BF16 if t.dtype == torch.bfloat16 else 0
+        if t.is_cuda:
+            flags |= _lib.SS_MEM_DEVICE
+        ld = t.stride(0) if t.dim() == 2 else t.numel()
+        return t.data_ptr(), flags, ld, t
+    a = np.ascontiguousarray(arr, dtype=np.float32)
+    ld = a.shape[1] if a.ndim == 2 else a.size
+    return a.ctypes.data, 0, ld, a
+
+
+def tensor_flags(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return 1
+    if t.dtype == torch.float32:
+        return 0
+    raise TypeError(f"activations must be float32 or bfloat16, got {t.dtype}")
+
+
+@dataclass
+class Seg:
+    """One envelope's slice of a dispatch (device tensors, caller-owned)."""
+
+    client_id: int
+    src: torch.Tensor          # [rows, width] (row stride may exceed width)
+    dst: torch.Tensor          # [rows, out_width]
+    base: torch.Tensor | None = None
+    adapter: bool = False
+    width: int | None = None   # declared width (defaults to src.shape[1])
+
+
+class SegmentTable:
+    """A prebuilt ctypes segment array for a fixed set of buffers (reused every step)."""
+
+    def __init__(self, segs: Sequence[Seg]):
+        self.n = len(segs)
+        self.arr = (SsSeg * max(1, self.n))()
+        self.status = (ctypes.c_int32 * max(1, self.n))()
+        self._keep = list(segs)
+        for i, s in enumerate(segs):
+            fill_seg(self.arr[i], s)
+
+    def statuses(self) -> list[int]:
+        return [int(self.status[i]) for i in range(self.n)]
+
+
+def fill_seg(c: SsSeg, s: Seg) -> None:
+    src, dst = s.src, s.dst
+    if src.dim() != 2 or dst.dim() != 2 or src.stride(1) != 1 or dst.stride(1) != 1:
+        raise ValueError("segment tensors must be 2-d with unit column stride")
+    c.client_id = int(s.client_id)
+    c.rows = int(src.shape[0])
+    c.width = int(s.width if s.width is not None else src.shape[1])
+    flags = 0
+    if tensor_flags(src):
+        flags |= _lib.SS_SEGF_SRC_BF16
+    if tensor_flags(dst):
+        flags |= _lib.SS_SEGF_DST_BF16
+    if s.adapter:
+        flags |= _lib.SS_SEGF_ADAPTER
+    c.src = src.data_ptr()
+    c.src_ld = src.stride(0) if src.shape[0] > 1 else max(src.stride(0), src.shape[1])
+    c.dst = dst.data_ptr()
+    c.dst_ld = dst.stride(0) if dst.shape[0] > 1 else max(dst.stride(0), dst.shape[1])
+    if s.base is not None:
+        if tensor_flags(s.base):
+            flags |= _lib.SS_SEGF_BASE_BF16
+        c.dst_base = s.base.data_ptr()
+        c.base_ld = s.base.stride(0) if s.base.shape[0] > 1 else max(s.base.stride(0), s.base.shape[1])
+    else:
+        c.dst_base = None
+        c.base_ld = 0
+    c.flags = flags
+
+
+class SsContext:
+    def __init__(self, device: int | torch.device = 0, tp_rank: int = 0, tp_size: int = 1):
+        self.lib = _lib.load()
+        self.device = torch.device("cuda", device if isinstance(device, int) else device.index or 0)
+        if not torch.cuda.is_available():
+            raise RuntimeError("GpuBaseExecutor needs a CUDA device (no CPU fallback by design)")
+        torch.cuda.set_device(self.device)
+        torch.cuda.init()
+        h = ctypes.c_void_p()
+        rc = self.lib.ss_ctx_create(self.device.index, tp_rank, tp_size, ctypes.byref(h))
+        if rc != _lib.SS_OK:
+            raise _lib.SsError(rc, f"ss_ctx_create(device={self.device.index}) failed "
+                                   "(needs an sm_100 GPU)")
+        self.h = h
+        self.dims: dict[tuple[int, int], tuple[int, int]] = {}
+
+    # -- weights --------------------------------------------------------------------------
+    def load_layer(self, block: int, role: int, weight, bias=None) -> None:
+        wp, wf, wld, wk = _host_or_device(weight)
+        bp, bk = None, None
+        if bias is not None:
+            # one flag set covers both uploads: bring the bias to the weight's dtype / memory
+            if isinstance(weight, torch.Tensor):
+                b = torch.as_tensor(bias).to(device=weight.device, dtype=wk.dtype).contiguous()
+            else:
+                b = np.ascontiguousarray(bias.detach().cpu().float().numpy()
+                                         if isinstance(bias, torch.Tensor) else bias, dtype=np.float32)
+            bp, _, _, bk = _host_or_device(b)
+        d_in, d_out = int(weight.shape[0]), int(weight.shape[1])
+        check(self.h, self.lib.ss_load_layer(self.h, int(block), int(role), d_in, d_out, wp, wld, bp, wf))
+        del wk, bk
+        self.dims[(int(block), int(role))] = (d_in, d_out)
+
+    # -- adapters -------------------------------------------------------------------------
+    def set_adapter(self, client_id: int, block: int, role: int, lora=None, ia3=None) -> None:
+        """lora = (A [d_in, r], B [r, d_out], scale) ; ia3 = l [d_out]."""
+        parts = [p for p in ((lora[0], lora[1]) if lora is not None else ()) + ((ia3,) if ia3 is not None else ())]
+        on_dev = any(isinstance(p, torch.Tensor) and p.is_cuda for p in parts)
+
+        def norm(p):  # one dtype / memory kind for every pointer of this call
+            if on_dev:
+                return torch.as_tensor(p, device=self.device).float().contiguous()
+            if isinstance(p, torch.Tensor):
+                p = p.float().numpy()
+            return np.ascontiguousarray(p, dtype=np.float32)
+
+        kind, rank, scale = 0, 0, 0.0
+        ap = bp = lp = None
+        keep = []
+        if lora is not None:
+            a, b = norm(lora[0]), norm(lora[1])
+            scale = float(lora[2])
+            ap, flags, _, _ = _host_or_device(a)
+            bp, _, _, _ = _host_or_device(b)
+            keep += [a, b]
+            kind |= _lib.SS_ADAPTER_LORA
+            rank = int(a.shape[1])
+        if ia3 is not None:
+            lv = norm(ia3)
+            lp, flags, _, _ = _host_or_device(lv)
+            keep.append(lv)
+            kind |= _lib.SS_ADAPTER_IA3
+        if kind:
+            self._set(client_id, block, role, kind, rank, scale, ap, bp, lp, flags)
+        del keep
+
+    def _set(self, client_id, block, role, kind, rank, scale, ap, bp, lp, flags):
+        check(self.h, self.lib.ss_set_adapter(self.h, int(client_id), int(block), int(role), kind,
+                                              rank, ctypes.c_float(scale), ap, bp, lp, flags or 0))
+
+    def clear_adapter(self, client_id: int, block: int | None = None, role: int | None = None) -> None:
+        if block is None:
+            check(self.h, self.lib.ss_clear_client(self.h, int(client_id)))
+        else:
+            rc = self.lib.ss_clear_adapter(self.h, int(client_id), int(block), int(role))
+            if rc not in (_lib.SS_OK, _lib.SS_E_NOLAYER):
+                check(self.h, rc)
+
+    # -- compute --------------------------------------------------------------------------
+    def compute(self, pass_kind: int, block: int, role: int, segs: Sequence[Seg],
+                stream: torch.cuda.Stream | None = None) -> list[int]:
+        table = SegmentTable(segs)
+        self.compute_table(pass_kind, block, role, table, stream)
+        return table.statuses()
+
+    def compute_table(self, pass_kind: int, block: int, role: int, table: SegmentTable,
+                      stream: torch.cuda.Stream | None = None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self.lib.ss_compute_batch(self.h, int(pass_kind), int(block), int(role), table.n,
+                                       table.arr, ctypes.c_void_p(s.cuda_stream), table.status)
+        check(self.h, rc)
+
+    # -- introspection --------------------------------------------------------------------
+    def memory_stats(self) -> tuple[int, int, int]:
+        w, a, ws = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(self.h, self.lib.ss_memory_stats(self.h, ctypes.byref(w), ctypes.byref(a), ctypes.byref(ws)))
+        return w.value, a.value, ws.value
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.ss_kernel_launches(self.h))
+
+    def set_option(self, key: str, value: int) -> None:
+        check(self.h, self.lib.ss_set_option(self.h, key.encode(), int(value)))
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            torch.cuda.synchronize(self.device)
+            self.lib.ss_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,471 @@
+"""GpuBaseExecutor — drop-in for splitserve.executor.BaseExecutor on one B200.
+
+Same surface as the reference (pkg/src/splitserve/executor.py:95-300): constructor
+``(layers, policy=None, save_activations=False)``, ``start/stop`` / context manager,
+``register/deregister``, ``submit(env, reply_fn)``, ``serve_forward / serve_backward /
+serve_noise_effect``, attributes ``layers, policy, metrics, ledger``. Validation messages,
+batch formation (FIFO segment order, pass-keyed queues, the three policies) and the
+error-isolation rule ("a malformed envelope fails alone") are the reference's.
+
+What changes is ``_compute_batch``: instead of concat -> einsum -> split on the host it
+builds one segment table and makes ONE C-ABI call (ss_compute_batch), which gathers the
+segments on the device, runs the tcgen05 GEMM with each client's LoRA / IA3 delta fused in
+the epilogue, and scatters every segment straight into its destination. Adapters move
+executor-side through a new control call, ``register_adapter`` (SURVEY §7 "adapter
+registration needs a new control message").
+
+Payloads may be host arrays (numpy / CPU tensors: staged through pinned memory, results
+returned as numpy f32 like the reference) or device tensors (zero-copy; results are device
+tensors, written into ``env.reply_to`` when the client supplies its exchange buffer).
+"""
+
+from __future__ import annotations
+
+import csv
+import threading
+import time
+from collections import defaultdict, deque
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import ledger as ledger_mod
+from .config import Role, addr_key
+from .device import Seg, SsContext
+from .errors import ConfigError, ProtocolError
+from .protocol import (COMPUTE_PASSES, PASS_BACKWARD, PASS_FORWARD, PASS_NOISE_EFFECT,
+                       Envelope, error_envelope)
+from . import _lib
+
+POLICY_MODES = ("nolockstep", "lockstep", "opportunistic")
+
+
+@dataclass
+class BatchPolicy:
+    """Dispatch policy (executor.py:32-56): a queue ripens for
+    min(wait_cap, wait_per_token * smallest member's tokens) or until max_batch_tokens."""
+
+    mode: str = "opportunistic"
+    wait_per_token: float = 0.0001
+    wait_cap: float = 0.050
+    max_batch_tokens: int = 8192
+    dispatch_cost: float = 0.0
+
+    def __post_init__(self):
+        if self.mode not in POLICY_MODES:
+            raise ConfigError(f"unknown policy mode {self.mode!r}")
+        if self.wait_per_token < 0 or self.wait_cap < 0:
+            raise ConfigError("wait durations must be non-negative")
+
+    def wait_budget(self, token_counts) -> float:
+        return min(self.wait_cap, self.wait_per_token * min(token_counts))
+
+
+@dataclass
+class ExecutorMetrics:
+    """Per-(block, role, pass) dispatch records (executor.py:59-92)."""
+
+    batch_sizes: dict = field(default_factory=lambda: defaultdict(list))
+    batch_tokens: dict = field(default_factory=lambda: defaultdict(list))
+    wait_times: dict = field(default_factory=lambda: defaultdict(list))
+    dispatches: int = 0
+
+    def record(self, key, size: int, tokens: int, waits) -> None:
+        self.batch_sizes[key].append(size)
+        self.batch_tokens[key].append(tokens)
+        self.wait_times[key].extend(waits)
+        self.dispatches += 1
+
+    def mean_batch_size(self) -> float:
+        sizes = [s for v in self.batch_sizes.values() for s in v]
+        return float(np.mean(sizes)) if sizes else 0.0
+
+    def max_wait(self) -> float:
+        return max((w for v in self.wait_times.values() for w in v), default=0.0)
+
+    def write_csv(self, path) -> None:
+        with open(path, "w", newline="") as fh:
+            out = csv.writer(fh)
+            out.writerow(["block", "role", "pass", "batch_size", "tokens", "mean_wait_s"])
+            for key in sorted(self.batch_sizes):
+                block, role, pass_kind = key
+                waits = self.wait_times[key]
+                mean_wait = float(np.mean(waits)) if waits else 0.0
+                for size, tokens in zip(self.batch_sizes[key], self.batch_tokens[key]):
+                    out.writerow([block, Role(role).name, pass_kind, size, tokens, mean_wait])
+
+
+def _is_device(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _out_dtype(payload) -> torch.dtype:
+    if isinstance(payload, torch.Tensor) and payload.dtype == torch.bfloat16:
+        return torch.bfloat16
+    return torch.float32
+
+
+class GpuBaseExecutor:
+    """Stateless layer server: one scheduler thread, compute on the B200 via libss_b200."""
+
+    def __init__(self, layers, policy: BatchPolicy | None = None, save_activations: bool = False,
+                 *, device: int = 0, stream: torch.cuda.Stream | None = None,
+                 context: SsContext | None = None):
+        self.layers = dict(layers)
+        self.policy = policy or BatchPolicy()
+        self.save_activations = save_activations
+        self._saved_debug: list = []
+        self.ctx = context if context is not None else SsContext(device)
+        self.device = self.ctx.device
+        self.stream = stream
+        self._dims: dict[tuple[int, int], tuple[int, int]] = {}
+        for addr, params in self.layers.items():
+            key = addr_key(addr)
+            self.ctx.load_layer(key[0], key[1], params.weight, getattr(params, "bias", None))
+            self._dims[key] = (int(params.weight.shape[0]), int(params.weight.shape[1]))
+        self._fused: dict[int, set] = defaultdict(set)   # client -> {(block, role)} fused
+        self._queues: dict[tuple, deque] = defaultdict(deque)
+        self._cond = threading.Condition()
+        self._clients: dict[int, bool] = {}
+        self._last_request_id: dict[int, int] = {}
+        self._running = False
+        self._thread: threading.Thread | None = None
+        self.metrics = ExecutorMetrics()
+        self.ledger = ledger_mod.MemoryLedger("executor")
+        self._pinned: dict[str, torch.Tensor] = {}
+        self.last_event: torch.cuda.Event | None = None
+        self._sync_ledger()
+
+    # -- lifecycle ------------------------------------------------------------------------
+    def start(self) -> "GpuBaseExecutor":
+        with self._cond:
+            if self._running:
+                return self
+            self._running = True
+        self._thread = threading.Thread(target=self._loop, daemon=True, name="gpu-base-executor")
+        self._thread.start()
+        return self
+
+    def stop(self, drain: bool = True) -> None:
+        if drain:
+            with self._cond:
+                while self._running and any(self._queues.values()):
+                    self._cond.wait(0.01)
+        with self._cond:
+            self._running = False
+            self._cond.notify_all()
+        if self._thread is not None:
+            self._thread.join()
+            self._thread = None
+
+    def __enter__(self):
+        return self.start()
+
+    def __exit__(self, *exc):
+        self.stop()
+
+    def close(self) -> None:
+        self.stop(drain=False)
+        self.ctx.close()
+
+    # -- registry -------------------------------------------------------------------------
+    def register(self, client_id: int, sends_backward: bool = False) -> None:
+        with self._cond:
+            self._clients[client_id] = sends_backward
+            self._cond.notify_all()
+
+    def deregister(self, client_id: int) -> None:
+        with self._cond:
+            self._clients.pop(client_id, None)
+            self._cond.notify_all()
+
+    def layer_dims(self, block: int, role: int) -> tuple[int, int]:
+        return self._dims[(int(block), int(role))]
+
+    # -- adapters (new control surface) ---------------------------------------------------
+    def register_adapter(self, client_id: int, adapter, addresses=None) -> None:
+        """Move a client's adapter executor-side. ``adapter`` is AdapterState-like
+        (adapters.py:44-60: ``lora {addr: (A, B)}``, ``ia3 {addr: l}``, ``alpha``, ``rank``).
+        Call again after every optimizer step to refresh the device copy. From then on the
+        client must NOT apply the adapter itself on these addresses (client.py:206-209)."""
+        lora = getattr(adapter, "lora", {}) or {}
+        ia3 = getattr(adapter, "ia3", {}) or {}
+        keys = {addr_key(a) for a in list(lora) + list(ia3)}
+        if addresses is not None:
+            keys &= {addr_key(a) for a in addresses}
+        by_key_lora = {addr_key(a): v for a, v in lora.items()}
+        by_key_ia3 = {addr_key(a): v for a, v in ia3.items()}
+        for key in sorted(keys):
+            if key not in self._dims:
+                raise ConfigError(f"adapter targets unknown layer {key}")
+            lo = None
+            if key in by_key_lora:
+                a, b = by_key_lora[key]
+                lo = (a, b, float(adapter.alpha) / float(adapter.rank))
+            self.ctx.set_adapter(client_id, key[0], key[1], lora=lo, ia3=by_key_ia3.get(key))
+            self._fused[client_id].add(key)
+        self._sync_ledger()
+
+    refresh_adapter = register_adapter
+
+    def deregister_adapter(self, client_id: int) -> None:
+        self.ctx.clear_adapter(client_id)
+        self._fused.pop(client_id, None)
+        self._sync_ledger()
+
+    def fused_addresses(self, client_id: int) -> set:
+        return set(self._fused.get(client_id, ()))
+
+    def _sync_ledger(self) -> None:
+        w, a, _ = self.ctx.memory_stats()
+        self.ledger.set(ledger_mod.WEIGHTS, w)
+        self.ledger.set(ledger_mod.ADAPTER, a)
+
+    # -- intake ---------------------------------------------------------------------------
+    def submit(self, env, reply_fn) -> None:
+        if env.pass_kind not in COMPUTE_PASSES:
+            reply_fn(error_envelope(env, f"unknown pass {env.pass_kind}"))
+            return
+        with self._cond:
+            last = self._last_request_id.get(env.client_id)
+            if last is not None and env.request_id <= last:
+                bad = f"request_id {env.request_id} not increasing (last {last})"
+            else:
+                bad = None
+                self._last_request_id[env.client_id] = env.request_id
+        if bad is not None:
+            reply_fn(error_envelope(env, bad))
+            return
+        if (int(env.block), int(env.role)) not in self._dims:
+            reply_fn(error_envelope(env, f"unknown layer {env.layer}"))
+            return
+        with self._cond:
+            self._queues[(env.block, env.role, env.pass_kind)].append((env, reply_fn, time.monotonic()))
+            self._cond.notify_all()
+
+    # -- batch surface --------------------------------------------------------------------
+    def serve_forward(self, envelopes) -> list:
+        return self._compute_batch(PASS_FORWARD, envelopes)
+
+    def serve_backward(self, envelopes) -> list:
+        return self._compute_batch(PASS_BACKWARD, envelopes)
+
+    def serve_noise_effect(self, envelope):
+        return self._compute_batch(PASS_NOISE_EFFECT, [envelope])[0]
+
+    def _pinned_buf(self, name: str, nbytes: int) -> torch.Tensor:
+        buf = self._pinned.get(name)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+            self._pinned[name] = buf
+        return buf
+
+    def _compute_batch(self, pass_kind: int, envelopes) -> list:
+        """One dispatch; per-envelope result is an array/tensor or a ProtocolError.
+
+        Validation and its messages follow executor.py:196-213; the compute is one
+        ss_compute_batch call (gather + GEMM + fused adapter + scatter)."""
+        if not envelopes:
+            return []
+        addr = envelopes[0].layer
+        key = addr_key(addr)
+        d_in, d_out = self._dims[key]
+        expected = d_out if pass_kind == PASS_BACKWARD else d_in
+        out_w = d_in if pass_kind == PASS_BACKWARD else d_out
+        results: list = [None] * len(envelopes)
+        good: list[int] = []
+        for i, env in enumerate(envelopes):
+            if addr_key(env.layer) != key:
+                results[i] = ProtocolError(f"layer mismatch in batch: {env.layer} != {addr}")
+            elif env.pass_kind != pass_kind:
+                results[i] = ProtocolError(f"pass mismatch in batch: {env.pass_kind}")
+            elif env.width != expected:
+                results[i] = ProtocolError(
+                    f"row width {env.width} does not match layer {addr} expected {expected}")
+            else:
+                good.append(i)
+        if not good:
+            return results
+        stream = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device), torch.cuda.stream(stream):
+            for i in good:
+                ev = getattr(envelopes[i], "ready", None)
+                if ev is not None:
+                    stream.wait_event(ev)
+            srcs, host_idx = self._stage_inputs(envelopes, good, stream)
+            dsts, host_out = self._stage_outputs(envelopes, good, out_w, stream)
+            fused = self._fused
+            segs = []
+            for j, i in enumerate(good):
+                env = envelopes[i]
+                base = getattr(env, "base_to", None) if pass_kind == PASS_FORWARD else None
+                segs.append(Seg(client_id=env.client_id, src=srcs[j], dst=dsts[j], base=base,
+                                adapter=(pass_kind != PASS_NOISE_EFFECT
+                                         and key in fused.get(env.client_id, ()))))
+            status = self.ctx.compute(pass_kind, key[0], key[1], segs, stream)
+            rows = sum(envelopes[i].token_count for i in good)
+            esz = 2 if all(s.src.dtype == torch.bfloat16 for s in segs) else 4
+            self.ledger.set(ledger_mod.TRANSIENT_BUFFER, rows * (expected + out_w) * esz)
+            self.ledger.set(ledger_mod.TRANSIENT_BUFFER, 0)
+            if self.save_activations and pass_kind == PASS_FORWARD:
+                saved = [(s.src.clone(), s.dst.clone()) for s in segs]
+                self._saved_debug.append(saved)
+                self.ledger.add(ledger_mod.SAVED_ACTIVATIONS, rows * (expected + out_w) * esz)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self.last_event = ev
+            host_results = self._finish_outputs(host_out, ev)
+        for j, i in enumerate(good):
+            st = status[j]
+            if st != _lib.SS_SEG_OK:
+                results[i] = ProtocolError(f"executor rejected segment (status {st}) for layer {addr}")
+            elif j in host_results:
+                results[i] = host_results[j]
+            else:
+                results[i] = dsts[j]
+        return results
+
+    # -- staging helpers --------------------------------------------------------------------
+    def _stage_inputs(self, envelopes, good, stream):
+        """Device views of every good payload; host payloads go through one pinned buffer and
+        one H2D copy (the only host->device crossing of a dispatch)."""
+        srcs: list = [None] * len(good)
+        host = [j for j, i in enumerate(good) if not _is_device(envelopes[i].payload)]
+        for j, i in enumerate(good):
+            p = envelopes[i].payload
+            if _is_device(p):
+                if p.dtype not in (torch.float32, torch.bfloat16):
+                    p = p.float()
+                if p.stride(-1) != 1:
+                    p = p.contiguous()
+                srcs[j] = p
+        if host:
+            arrays = []
+            for j in host:
+                p = envelopes[good[j]].payload
+                if isinstance(p, torch.Tensor):
+                    a = p if p.dtype in (torch.float32, torch.bfloat16) else p.float()
+                else:
+                    a = torch.from_numpy(np.ascontiguousarray(p, dtype=np.float32))
+                arrays.append(a.contiguous())
+            sizes = [a.numel() * a.element_size() for a in arrays]
+            offs = np.cumsum([0] + [(s + 255) // 256 * 256 for s in sizes])
+            total = int(offs[-1])
+            pin = self._pinned_buf("in", total)
+            stream.synchronize()  # the pinned staging buffer may still feed an earlier copy
+            for a, o, s in zip(arrays, offs, sizes):
+                pin[o:o + s].copy_(a.view(-1).view(torch.uint8))
+            dev = torch.empty(total, dtype=torch.uint8, device=self.device)
+            dev.copy_(pin[:total], non_blocking=True)
+            for j, a, o, s in zip(host, arrays, offs, sizes):
+                srcs[j] = dev[o:o + s].view(a.dtype).view(a.shape)
+        return srcs, host
+
+    def _stage_outputs(self, envelopes, good, out_w, stream):
+        dsts: list = [None] * len(good)
+        host_out = {}
+        need = []
+        for j, i in enumerate(good):
+            env = envelopes[i]
+            r = getattr(env, "reply_to", None)
+            if r is not None:
+                if not _is_device(r) or tuple(r.shape) != (env.token_count, out_w):
+                    raise ProtocolError(f"reply_to must be a device tensor of shape "
+                                        f"{(env.token_count, out_w)}")
+                dsts[j] = r
+            else:
+                need.append(j)
+        if need:
+            dts = {_out_dtype(envelopes[good[j]].payload) for j in need}
+            dt = torch.float32 if torch.float32 in dts else torch.bfloat16
+            rows = sum(envelopes[good[j]].token_count for j in need)
+            out = torch.empty((rows, out_w), dtype=dt, device=self.device)
+            pos = 0
+            for j in need:
+                t = envelopes[good[j]].token_count
+                dsts[j] = out[pos:pos + t]
+                if not _is_device(envelopes[good[j]].payload):
+                    host_out[j] = (pos, t)
+                pos += t
+            if host_out:
+                host_out["__out__"] = out
+        return dsts, host_out
+
+    def _finish_outputs(self, host_out, ev):
+        if not host_out:
+            return {}
+        out = host_out.pop("__out__")
+        pin = self._pinned_buf("out", out.numel() * 4)
+        hv = pin[:out.numel() * 4].view(torch.float32).view(out.shape)
+        hv.copy_(out.float(), non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        full = hv.numpy().copy()   # one array; slots are views of it, like split_rows
+        return {j: full[pos:pos + t] for j, (pos, t) in host_out.items()}
+
+    # -- scheduler (executor.py:235-300 semantics) ------------------------------------------
+    def _loop(self) -> None:
+        torch.cuda.set_device(self.device)
+        while True:
+            with self._cond:
+                while True:
+                    if not self._running:
+                        return
+                    picked, timeout = self._pick_ready(time.monotonic())
+                    if picked is not None:
+                        break
+                    self._cond.wait(timeout)
+            self._dispatch(*picked)
+
+    def _pick_ready(self, now: float):
+        """((key, entries), None) when some queue should dispatch now, else
+        (None, seconds until the earliest opportunistic deadline or None)."""
+        soonest = None
+        for key, q in self._queues.items():
+            if not q:
+                continue
+            pass_kind = key[2]
+            if pass_kind == PASS_NOISE_EFFECT or self.policy.mode == "nolockstep":
+                return (key, [q.popleft()]), None
+            if self.policy.mode == "lockstep":
+                need = {c for c, bwd in self._clients.items() if pass_kind == PASS_FORWARD or bwd}
+                have = {e.client_id for e, _, _ in q}
+                if need <= have:
+                    return (key, self._drain(q)), None
+                continue
+            tokens = [e.token_count for e, _, _ in q]
+            if sum(tokens) >= self.policy.max_batch_tokens:
+                return (key, self._drain(q)), None
+            deadline = min(t for _, _, t in q) + self.policy.wait_budget(tokens)
+            if now >= deadline:
+                return (key, self._drain(q)), None
+            left = deadline - now
+            soonest = left if soonest is None else min(soonest, left)
+        return None, soonest
+
+    @staticmethod
+    def _drain(q: deque) -> list:
+        entries = list(q)
+        q.clear()
+        return entries
+
+    def _dispatch(self, key, entries) -> None:
+        now = time.monotonic()
+        if self.policy.dispatch_cost > 0:
+            time.sleep(self.policy.dispatch_cost)
+        envs = [e for e, _, _ in entries]
+        try:
+            results = self._compute_batch(key[2], envs)
+        except Exception as exc:  # a CUDA failure fails the batch, not the scheduler
+            results = [ProtocolError(f"executor failure: {exc}")] * len(envs)
+        self.metrics.record(key, len(entries), sum(e.token_count for e in envs),
+                            [now - t for _, _, t in entries])
+        done = self.last_event
+        for (env, reply_fn, _), res in zip(entries, results):
+            if isinstance(res, ProtocolError):
+                reply_fn(error_envelope(env, str(res)))
+            else:
+                reply_fn(Envelope(env.client_id, env.request_id, env.block, env.role,
+                                  env.pass_kind, res, done=done))
+        with self._cond:
+            self._cond.notify_all()

@@ -1,0 +1,414 @@
+"""GPU parity: the CUDA path (through the C ABI via GpuBaseExecutor) against the oracle and
+the reference's golden vectors. Run on a B200: ``python -m pytest tests -m gpu``.
+
+Tolerances (stated once, oracle/splitserve_oracle.py TOL_*): against the f32
+oracle fed the same bf16-rounded inputs, normwise max|d|/max|ref| and mean|d|/mean|ref|:
+bf16 activations in/out <= 2e-2 / 3e-3; fp32 outputs <= 1e-2 / 1e-3. fp32 outputs of exactly
+representable integer inputs: bitwise. Routing: bit-exact. Batched == solo: bitwise.
+"""
+
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import splitserve_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+MAX_REL, MEAN_REL = O.TOL_MAX_REL, O.TOL_MEAN_REL
+
+
+def _ex(layers, **kw):
+    from paper_2507_03220_b200 import AffineParams, GpuBaseExecutor, LayerAddress, Role
+    return GpuBaseExecutor({LayerAddress(b, Role(r)): AffineParams(w, bias)
+                            for (b, r), (w, bias) in layers.items()}, **kw)
+
+
+def _env(cid, req, block, role, pass_kind, payload, **kw):
+    from paper_2507_03220_b200 import Envelope
+    return Envelope(cid, req, block, role, pass_kind, payload, **kw)
+
+
+class _Adapter:
+    """AdapterState-like record for register_adapter (adapters.py:44-60 fields)."""
+
+    def __init__(self, lora=None, ia3=None, alpha=0.0, rank=1):
+        self.lora, self.ia3, self.alpha, self.rank = lora or {}, ia3 or {}, alpha, rank
+
+
+def _addr(block, role):
+    from paper_2507_03220_b200 import LayerAddress, Role
+    return LayerAddress(block, Role(role))
+
+
+def _close(got, ref, max_rel=MAX_REL, mean_rel=MEAN_REL, what=""):
+    mx, mn = O.normwise_errors(np.asarray(got, np.float64), np.asarray(ref, np.float64))
+    assert mx <= max_rel and mn <= mean_rel, f"{what}: normwise max {mx:.3e} mean {mn:.3e}"
+
+
+def _register_golden_adapters(ex, g, block=0, role=O.FF_UP):
+    for cid in (0, 3):
+        a, b = g[f"A{cid}"], g[f"B{cid}"]
+        ex.register_adapter(cid, _Adapter(lora={_addr(block, role): (a, b)},
+                                          alpha=float(g[f"alpha{cid}"]), rank=a.shape[1]))
+    ex.register_adapter(1, _Adapter(ia3={_addr(block, role): g["l1"]}))
+
+
+# ----------------------------------------------------------------------- golden: executor
+
+def test_executor_golden_fwd_bwd_noise(golden):
+    g = golden("executor_kat")
+    W, b = g["W"], g["b"]
+    ex = _ex({(0, O.Q): (W, b)})
+    Wr, br = O.bf16_round(W), b
+    fw = [_env(i + 1, 1, 0, O.Q, 0, g[f"fwd/x{i}"]) for i in range(4)]
+    for i, r in enumerate(ex.serve_forward(fw)):
+        assert isinstance(r, np.ndarray) and r.dtype == np.float32
+        assert r.shape == g[f"fwd/y{i}"].shape
+        # same bf16-rounded operands -> tight; vs the reference's un-rounded f32 -> bf16 level
+        ref = O.affine_forward(O.bf16_round(g[f"fwd/x{i}"]), Wr, br)
+        if r.size:
+            _close(r, ref, 1e-5, 1e-5, "fwd vs oracle(bf16 inputs)")
+            _close(r, g[f"fwd/y{i}"], 2e-2, 1e-2, "fwd vs reference golden")
+    bw = [_env(i + 1, 2, 0, O.Q, 1, g[f"bwd/g{i}"]) for i in range(2)]
+    for i, r in enumerate(ex.serve_backward(bw)):
+        _close(r, O.affine_backward_input(O.bf16_round(g[f"bwd/g{i}"]), Wr), 1e-5, 1e-5, "bwd")
+        _close(r, g[f"bwd/dx{i}"], 2e-2, 1e-2, "bwd vs golden")
+    out = ex.serve_noise_effect(_env(1, 3, 0, O.Q, 2, g["noise/x"]))
+    _close(out, O.matmul(O.bf16_round(g["noise/x"]), Wr), 1e-5, 1e-5, "noise")
+    assert np.any(np.abs(out - ex.serve_forward([_env(1, 4, 0, O.Q, 0, g["noise/x"])])[0]) > 1e-3)
+
+
+def test_malformed_envelope_fails_alone_same_messages(golden):
+    from paper_2507_03220_b200 import ProtocolError
+    g = golden("executor_kat")
+    ex = _ex({(0, O.Q): (g["W"], g["b"])})
+    res = ex.serve_forward([_env(1, 4, 0, O.Q, 0, g["bad/x_good"]),
+                            _env(2, 4, 0, O.Q, 0, g["bad/x_bad"]),
+                            _env(5, 4, 0, O.Q, 1, g["bad/x_wrong_pass"])])
+    assert isinstance(res[0], np.ndarray)
+    assert all(isinstance(r, ProtocolError) for r in res[1:])
+    assert [str(r) for r in res[1:]] == [str(m) for m in g["bad/msgs"][1:]]
+
+
+# ----------------------------------------------------------------------- golden: fused adapters
+
+def _fused_run(ex, g, dtype, want_base=True):
+    rows = [int(r) for r in g["rows"]]
+    dev = ex.device
+    xs = [torch.from_numpy(g[f"fwd/x{c}"]).to(dev, dtype) for c in range(len(rows))]
+    d_out = g["W"].shape[1]
+    outs = [torch.empty(r, d_out, dtype=dtype, device=dev) for r in rows]
+    bases = [torch.empty(r, d_out, dtype=dtype, device=dev) for r in rows]
+    envs = [_env(c, 1, 0, O.FF_UP, 0, xs[c], reply_to=outs[c],
+                 base_to=bases[c] if (want_base and c == 1) else None) for c in range(len(rows))]
+    res = ex.serve_forward(envs)
+    assert all(r is outs[c] for c, r in enumerate(res))
+    gs = [torch.from_numpy(g[f"bwd/g{c}"]).to(dev, dtype) for c in range(len(rows))]
+    dxs = ex.serve_backward([_env(c, 2, 0, O.FF_UP, 1, gs[c]) for c in range(len(rows))])
+    torch.cuda.synchronize()
+    return ([o.float().cpu().numpy() for o in outs], [b.float().cpu().numpy() for b in bases],
+            [d.float().cpu().numpy() for d in dxs])
+
+
+def test_fused_integer_kat_bitwise(golden):
+    """Exact-integer KAT: fp32 outputs equal the reference bitwise."""
+    g = golden("fused_int_kat")
+    ex = _ex({(0, O.FF_UP): (g["W"], g["b"])})
+    _register_golden_adapters(ex, g)
+    ys, bases, dxs = _fused_run(ex, g, torch.float32)
+    for c in range(len(ys)):
+        assert np.array_equal(ys[c], g[f"fwd/y{c}"]), f"fwd client {c}"
+        assert np.array_equal(dxs[c], g[f"bwd/dx{c}"]), f"bwd client {c}"
+    assert np.array_equal(bases[1], g["fwd/ybase1"])
+
+
+@pytest.mark.parametrize("name", ["fused_random_small", "fused_random_ragged"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_fused_random_parity(golden, name, dtype):
+    g = golden(name)
+    ex = _ex({(0, O.FF_UP): (g["W"], g["b"])})
+    _register_golden_adapters(ex, g)
+    ys, bases, dxs = _fused_run(ex, g, dtype)
+    tol = (MAX_REL, MEAN_REL) if dtype == torch.bfloat16 else (O.TOL_F32_MAX_REL, O.TOL_F32_MEAN_REL)
+    for c in range(len(ys)):
+        _close(ys[c], g[f"fwd/y{c}"], *tol, what=f"{name} fwd client {c}")
+        if c == 1:
+            # IA3 backward: the GEMM operand is g*l, which the device rounds to bf16 once more
+            # (client.py:291-294 computes it in f32). Same-operand check at the tier, and the
+            # reference golden at the bf16-activation tier.
+            gl = O.bf16_round(g[f"bwd/g{c}"].astype(np.float32) * g["l1"])
+            _close(dxs[c], O.affine_backward_input(gl, g["W"]), *tol, what="IA3 bwd vs oracle(bf16(g*l))")
+            _close(dxs[c], g[f"bwd/dx{c}"], MAX_REL, MEAN_REL, what="IA3 bwd vs golden")
+        else:
+            _close(dxs[c], g[f"bwd/dx{c}"], *tol, what=f"{name} bwd client {c}")
+    _close(bases[1], g["fwd/ybase1"], *tol, what="IA3 y_base")
+
+
+# ----------------------------------------------------------------------- routing & invisibility
+
+def test_routing_bit_exact_with_identity_weight():
+    """W = I, b = 0, integer rows tagging (segment, row): every output row is its own input row
+    (split_rows offsets, tensor_ops.py:149-156), including around a rejected envelope."""
+    from paper_2507_03220_b200 import ProtocolError
+    d = 256
+    ex = _ex({(0, O.Q): (np.eye(d, dtype=np.float32), np.zeros(d, np.float32))})
+    rows = [1, 127, 0, 129, 5, 300, 2]
+    xs = []
+    for s, t in enumerate(rows):
+        x = np.zeros((t, d), np.float32)
+        x[:, 0] = s
+        x[:, 1] = np.arange(t) % 256
+        x[:, 2] = np.arange(t) // 256
+        x[:, 3:] = np.random.default_rng(s).integers(-100, 100, size=(t, d - 3))
+        xs.append(x)
+    envs = [_env(s, 1, 0, O.Q, 0, x) for s, x in enumerate(xs)]
+    envs.insert(3, _env(99, 1, 0, O.Q, 0, np.zeros((4, d - 1), np.float32)))
+    res = ex.serve_forward(envs)
+    assert isinstance(res[3], ProtocolError)
+    for x, r in zip(xs, [r for i, r in enumerate(res) if i != 3]):
+        assert np.array_equal(r, x)
+
+
+def _mixed_clients(ex, d_in, d_out, seed, block=0, role=O.K):
+    rng = np.random.default_rng(seed)
+    specs = [("lora", 8), ("plain", 0), ("lora", 64), ("ia3", 0), ("lora", 16), ("lora", 32), ("plain", 0)]
+    for cid, (kind, r) in enumerate(specs):
+        if kind == "lora":
+            ad = O.lora_params(seed, cid, block, role, d_in, d_out, r, 2.0 * r)
+            ex.register_adapter(cid, _Adapter(lora={_addr(block, role): (ad.a, ad.b)}, alpha=2.0 * r, rank=r))
+        elif kind == "ia3":
+            ex.register_adapter(cid, _Adapter(ia3={_addr(block, role): O.ia3_params(seed, cid, block, role, d_out).ia3}))
+    counts = [int(t) for t in rng.integers(1, 300, size=len(specs))]
+    return specs, counts
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_batched_equals_solo_bitwise(dtype):
+    """GPU analogue of acceptance C5 / test_executor.py:36-45: batching is invisible, bitwise,
+    for every client and adapter kind, forward and backward."""
+    d_in, d_out = 384, 640
+    w, b = O.layer_params(3, 0, O.K, d_in, d_out)
+    ex = _ex({(0, O.K): (w, b)})
+    specs, counts = _mixed_clients(ex, d_in, d_out, seed=5)
+    dev = ex.device
+    gen = torch.Generator(device=dev).manual_seed(0)
+    for pass_kind, width in ((0, d_in), (1, d_out)):
+        xs = [torch.randn(t, width, generator=gen, device=dev).to(dtype) for t in counts]
+        batched = ex._compute_batch(pass_kind, [_env(c, 10 + pass_kind, 0, O.K, pass_kind, x) for c, x in enumerate(xs)])
+        for c, x in enumerate(xs):
+            solo = ex._compute_batch(pass_kind, [_env(c, 20 + pass_kind, 0, O.K, pass_kind, x)])[0]
+            assert torch.equal(batched[c], solo), (pass_kind, c, specs[c])
+        # and in a different batch order / company
+        perm = list(reversed(range(len(xs))))
+        again = ex._compute_batch(pass_kind, [_env(c, 30 + pass_kind, 0, O.K, pass_kind, xs[c]) for c in perm])
+        for j, c in enumerate(perm):
+            assert torch.equal(again[j], batched[c])
+
+
+@pytest.mark.parametrize("shape", [("7b_q", 4096, 4096), ("13b_ff_up", 5120, 13824),
+                                   ("13b_ff_down", 13824, 5120), ("13b_lm_head", 5120, 32000)])
+def test_large_layer_parity_vs_fp32(shape):
+    """Llama2-7B/13B layer shapes, mixed LoRA ranks 8..64 + IA3 + plain, bf16 in/out, against
+    an fp32 torch evaluation of the same math on the same bf16 operands."""
+    name, d_in, d_out = shape
+    role = O.FF_UP if "ff_up" in name else (O.FF_DOWN if "ff_down" in name else (O.LM_HEAD if "head" in name else O.Q))
+    block = 40 if role == O.LM_HEAD else 0
+    w, b = O.layer_params(7, block, role, d_in, d_out)
+    ex = _ex({(block, role): (w, b)})
+    rng = np.random.default_rng(1)
+    dev = ex.device
+    kinds = [("lora", 8), ("lora", 16), ("lora", 32), ("lora", 64), ("plain", 0)]
+    if role in O.IA3_ROLES:
+        kinds.append(("ia3", 0))
+    ads = {}
+    for cid, (kind, r) in enumerate(kinds):
+        if kind == "lora":
+            ad = O.lora_params(7, cid, block, role, d_in, d_out, r, 2.0 * r)
+            ads[cid] = ad
+            ex.register_adapter(cid, _Adapter(lora={_addr(block, role): (ad.a, ad.b)}, alpha=2.0 * r, rank=r))
+        elif kind == "ia3":
+            ad = O.ia3_params(7, cid, block, role, d_out)
+            ads[cid] = ad
+            ex.register_adapter(cid, _Adapter(ia3={_addr(block, role): ad.ia3}))
+    counts = [int(t) for t in rng.integers(64, 700, size=len(kinds))]
+    Wt = torch.from_numpy(w).to(dev).to(torch.bfloat16).float()
+    bt = torch.from_numpy(b).to(dev)
+    for pass_kind, width in ((0, d_in), (1, d_out)):
+        xs = [torch.randn(t, width, device=dev).to(torch.bfloat16) for t in counts]
+        res = ex._compute_batch(pass_kind, [_env(c, 1 + pass_kind, block, role, pass_kind, x) for c, x in enumerate(xs)])
+        for c, (x, y) in enumerate(zip(xs, res)):
+            xf = x.float()
+            ad = ads.get(c)
+            if pass_kind == 0:
+                ref = xf @ Wt + bt
+                if ad is not None and ad.a is not None:
+                    A = torch.from_numpy(ad.a).to(dev).to(torch.bfloat16).float()
+                    B = torch.from_numpy(ad.b).to(dev).to(torch.bfloat16).float()
+                    ref = ref + ((xf @ A) @ B) * ad.scale
+                if ad is not None and ad.ia3 is not None:
+                    ref = ref * torch.from_numpy(ad.ia3).to(dev)
+            else:
+                gf = xf
+                if ad is not None and ad.ia3 is not None:
+                    gf = gf * torch.from_numpy(ad.ia3).to(dev)
+                ref = gf @ Wt.T
+                if ad is not None and ad.a is not None:
+                    A = torch.from_numpy(ad.a).to(dev).to(torch.bfloat16).float()
+                    B = torch.from_numpy(ad.b).to(dev).to(torch.bfloat16).float()
+                    ref = ref + ((gf @ B.T) @ A.T) * ad.scale
+            _close(y.float().cpu().numpy(), ref.cpu().numpy(), what=f"{name} pass {pass_kind} client {c}")
+
+
+# ----------------------------------------------------------------------- statelessness / edges
+
+def test_executor_retains_nothing_between_requests():
+    from paper_2507_03220_b200 import ledger as L
+    w, b = O.layer_params(0, 0, O.Q, 64, 64)
+    ex = _ex({(0, O.Q): (w, b)})
+    weights = ex.ledger.get(L.WEIGHTS)
+    rng = np.random.default_rng(0)
+    for i in range(5):
+        ex.serve_forward([_env(1, i + 1, 0, O.Q, 0, rng.standard_normal((4, 64)).astype(np.float32))])
+        ex.serve_backward([_env(2, i + 1, 0, O.Q, 1, rng.standard_normal((4, 64)).astype(np.float32))])
+    assert ex.ledger.get(L.SAVED_ACTIVATIONS) == 0
+    assert ex.ledger.get(L.TRANSIENT_BUFFER) == 0
+    assert ex.ledger.get(L.WEIGHTS) == weights > 0
+    assert ex.ledger.transient_high_water > 0
+
+
+def test_save_activations_negative_control():
+    from paper_2507_03220_b200 import ledger as L
+    w, b = O.layer_params(0, 0, O.Q, 64, 64)
+    ex = _ex({(0, O.Q): (w, b)}, save_activations=True)
+    x = np.ones((4, 64), np.float32)
+    ex.serve_forward([_env(1, 1, 0, O.Q, 0, x)])
+    first = ex.ledger.get(L.SAVED_ACTIVATIONS)
+    ex.serve_forward([_env(1, 2, 0, O.Q, 0, x)])
+    assert first > 0 and ex.ledger.get(L.SAVED_ACTIVATIONS) == 2 * first
+
+
+def test_edge_cases_empty_and_zero_rows():
+    w, b = O.layer_params(0, 0, O.Q, 64, 96)
+    ex = _ex({(0, O.Q): (w, b)})
+    assert ex.serve_forward([]) == []
+    res = ex.serve_forward([_env(1, 1, 0, O.Q, 0, np.zeros((0, 64), np.float32)),
+                            _env(2, 1, 0, O.Q, 0, np.ones((3, 64), np.float32))])
+    assert res[0].shape == (0, 96) and res[1].shape == (3, 96)
+    res = ex.serve_backward([_env(3, 1, 0, O.Q, 1, np.zeros((0, 96), np.float32))])
+    assert res[0].shape == (0, 64)
+
+
+def test_large_batch_many_small_segments():
+    """Decode-like dispatch: 200 clients x 1-3 tokens, all with LoRA (many rank blocks per tile)."""
+    d = 512
+    w, b = O.layer_params(1, 0, O.V, d, d)
+    ex = _ex({(0, O.V): (w, b)})
+    n = 200
+    rng = np.random.default_rng(3)
+    for cid in range(n):
+        r = [8, 16, 32, 64][cid % 4]
+        ad = O.lora_params(1, cid, 0, O.V, d, d, r, 2.0 * r)
+        ex.register_adapter(cid, _Adapter(lora={_addr(0, O.V): (ad.a, ad.b)}, alpha=2.0 * r, rank=r))
+    xs = [O.bf16_round(rng.standard_normal((int(rng.integers(1, 4)), d)).astype(np.float32)) for _ in range(n)]
+    res = ex.serve_forward([_env(c, 1, 0, O.V, 0, x) for c, x in enumerate(xs)])
+    wr, br = O.bf16_round(w), b
+    for c, (x, y) in enumerate(zip(xs, res)):
+        r = [8, 16, 32, 64][c % 4]
+        ad = O.lora_params(1, c, 0, O.V, d, d, r, 2.0 * r)
+        ref = O.apply_adapter(O.OracleAdapter(a=O.bf16_round(ad.a), b=O.bf16_round(ad.b), alpha=ad.alpha, rank=r),
+                              x, O.affine_forward(x, wr, br))
+        _close(y, ref, what=f"client {c}")
+
+
+def test_adapter_refresh_and_rank_change():
+    d_in, d_out = 256, 256
+    w, b = O.layer_params(2, 0, O.O, d_in, d_out)
+    ex = _ex({(0, O.O): (w, b)})
+    x = O.bf16_round(np.random.default_rng(0).standard_normal((50, d_in)).astype(np.float32))
+    base = O.affine_forward(x, O.bf16_round(w), b)
+    for step, r in enumerate([8, 8, 32, 16]):
+        ad = O.lora_params(10 + step, 0, 0, O.O, d_in, d_out, r, 2.0 * r)
+        ad = O.OracleAdapter(a=O.bf16_round(ad.a), b=O.bf16_round(ad.b), alpha=ad.alpha, rank=r)
+        ex.refresh_adapter(0, _Adapter(lora={_addr(0, O.O): (ad.a, ad.b)}, alpha=ad.alpha, rank=r))
+        y = ex.serve_forward([_env(0, step + 1, 0, O.O, 0, x)])[0]
+        _close(y, O.apply_adapter(ad, x, base), what=f"refresh {step}")
+    ex.deregister_adapter(0)
+    y = ex.serve_forward([_env(0, 9, 0, O.O, 0, x)])[0]
+    _close(y, base, 1e-5, 1e-5, "after deregister_adapter")
+
+
+# ----------------------------------------------------------------------- channel / scheduler
+
+def test_device_channel_virtlayer_roundtrip():
+    from paper_2507_03220_b200 import DeviceChannel, VirtLayer
+    d_in, d_out = 256, 512
+    w, b = O.layer_params(4, 0, O.FF_UP, d_in, d_out)
+    ex = _ex({(0, O.FF_UP): (w, b)})
+    with ex:
+        ch = DeviceChannel(ex, 7, batch_size=2, seq_len=16, max_width=512)
+        ch.register(sends_backward=True)
+        layer = VirtLayer(_addr(0, O.FF_UP), d_in, d_out, ch)
+        x = torch.randn(32, d_in, device=ex.device).to(torch.bfloat16)
+        y = layer.forward(x)
+        g = torch.randn(32, d_out, device=ex.device).to(torch.bfloat16)
+        dx = layer.backward(g)
+    ref_y = ex._compute_batch(0, [_env(7, 100, 0, O.FF_UP, 0, x)])[0]
+    ref_dx = ex._compute_batch(1, [_env(7, 101, 0, O.FF_UP, 1, g)])[0]
+    assert torch.equal(y, ref_y) and torch.equal(dx, ref_dx)
+    assert ch.buffer.resizes == 0
+
+
+def test_lockstep_eight_clients_one_batch_over_device_channels():
+    from paper_2507_03220_b200 import BatchPolicy, DeviceChannel
+    w, b = O.layer_params(5, 0, O.Q, 128, 128)
+    ex = _ex({(0, O.Q): (w, b)}, policy=BatchPolicy(mode="lockstep"))
+    results = {}
+    with ex:
+        chans = [DeviceChannel(ex, c, 1, 8, 128) for c in range(8)]
+        for ch in chans:
+            ch.register()
+        xs = [torch.randn(4, 128, device=ex.device).to(torch.bfloat16) for _ in range(8)]
+
+        def one(c):
+            torch.cuda.set_device(ex.device)
+            results[c] = chans[c].request(0, O.Q, 0, xs[c]).clone()
+
+        ts = [threading.Thread(target=one, args=(c,)) for c in range(8)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(30)
+    assert ex.metrics.mean_batch_size() == 8.0
+    torch.cuda.synchronize()
+    for c in range(8):
+        solo = ex._compute_batch(0, [_env(c, 50, 0, O.Q, 0, xs[c])])[0]
+        assert torch.equal(results[c], solo)
+
+
+def test_submit_rejections_match_reference_messages():
+    from paper_2507_03220_b200 import PASS_ERROR, error_message
+    w, b = O.layer_params(0, 0, O.Q, 64, 64)
+    ex = _ex({(0, O.Q): (w, b)})
+    got = []
+    with ex:
+        ex.register(1)
+        done = threading.Event()
+
+        def reply(e):
+            got.append(e)
+            done.set()
+        x = np.ones((2, 64), np.float32)
+        ex.submit(_env(1, 5, 0, O.Q, 0, x), reply)
+        assert done.wait(10)
+        done.clear()
+        ex.submit(_env(1, 5, 0, O.Q, 0, x), reply)
+        assert done.wait(10)
+        done.clear()
+        ex.submit(_env(1, 6, 3, O.Q, 0, x), reply)
+        assert done.wait(10)
+    assert got[0].pass_kind == 0
+    assert got[1].pass_kind == PASS_ERROR and "not increasing" in error_message(got[1])
+    assert got[2].pass_kind == PASS_ERROR and "unknown layer" in error_message(got[2])
