@@ -1,0 +1,521 @@
+"""Aggregate adapter tokens/sec of the B200 base executor (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload 13b|7b] [--impl ours|reference]
+
+One STEP = one executor pass of the workload: a forward dispatch of every one of
+the 6L+1 frozen layers over all clients' token segments (LoRA / IA3 deltas fused), then a
+backward (input-gradient) dispatch of every layer in reverse over the fine-tuning clients'
+segments. Every client token counts once; fine-tune tokens cost fwd + bwd.
+
+Default workload (BASELINE configs[2], the metric's Llama2-13B shape, on one GPU): d 5120,
+d_ff 13824, L 40, V 32000; 32 clients = 24 LoRA (ranks 8/16/32/64, alpha = 2r, Q/K/V/O) + 8
+IA3 (K, V, FF_UP); 16 fine-tune + 16 inference clients, 2 x 512 tokens each -> 32 768 rows per
+forward dispatch, 16 384 per backward dispatch. Multi-GPU: one process per GPU, each a full
+replica serving its own 32 clients (segment-parallel, no collective on the data path):
+weak scaling, value = all ranks' tokens / max-over-ranks time.
+
+Legs reported on one JSON line (rank 0):
+  value   device-resident exchange buffers, one prebuilt C-ABI dispatch per layer and pass;
+  e2e     the reference-facing API (GpuBaseExecutor._compute_batch with pinned HOST payloads
+          and host reply buffers): H2D + compute + D2H per dispatch, like host clients;
+  roofline  fused GEMM kernel, CUDA events around every launch in the timed region;
+  cpu_baseline  the reference algorithm (oracle port) on host cores, bounded sample.
+``--impl reference`` times only the reference algorithm on the host (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "aggregate adapter tokens/sec (fwd+bwd), Llama2-13B shape, N clients, 1/2/4/8 B200"
+
+WORKLOADS = {
+    # BASELINE configs[2] on one GPU (the metric's model shape)
+    "13b": dict(name="llama2-13b-shape, 32 mixed LoRA(r8-64)+IA3 clients, 16 FT + 16 inference, 2x512 tok",
+                d=5120, d_ff=13824, L=40, V=32000, clients=32, tokens=1024, seq=512, batch=2),
+    # BASELINE configs[1]
+    "7b": dict(name="llama2-7b-shape, 8 LoRA r16 fine-tune clients, 2x512 tok",
+               d=4096, d_ff=11008, L=32, V=32000, clients=8, tokens=1024, seq=512, batch=2),
+}
+Q, K, V, O, FF_UP, FF_DOWN, LM_HEAD = range(7)
+
+
+def client_specs(wl_key: str, n: int):
+    """[(kind, rank, finetune)] per client."""
+    if wl_key == "7b":
+        return [("lora", 16, True) for _ in range(n)]
+    specs = []
+    for c in range(n):
+        if c < 24:
+            specs.append(("lora", (8, 16, 32, 64)[c % 4], c % 2 == 0))
+        else:
+            specs.append(("ia3", 0, c % 2 == 0))
+    return specs
+
+
+def layer_list(wl):
+    d, f, L, Vv = wl["d"], wl["d_ff"], wl["L"], wl["V"]
+    dims = {Q: (d, d), K: (d, d), V: (d, d), O: (d, d), FF_UP: (d, f), FF_DOWN: (f, d), LM_HEAD: (d, Vv)}
+    out = [(b, r) for b in range(L) for r in (Q, K, V, O, FF_UP, FF_DOWN)] + [(L, LM_HEAD)]
+    return out, dims
+
+
+def flops_per_step(wl, specs):
+    """Algorithmic FLOPs of one step: 2*d_in*d_out per token per layer (fwd), the same again
+    for fine-tune tokens (bwd), plus each client's LoRA 2*r*(d_in+d_out) per targeted layer."""
+    layers, dims = layer_list(wl)
+    t = wl["tokens"]
+    total = 0.0
+    for (_, r) in layers:
+        di, do = dims[r]
+        for kind, rank, ft in specs:
+            passes = 2 if ft else 1
+            f = 2.0 * di * do
+            if kind == "lora" and r in (Q, K, V, O):
+                f += 2.0 * rank * (di + do)
+            total += passes * t * f
+    return total
+
+
+# ============================================================================ GPU leg
+
+def nvsmi_sampler(stop: threading.Event, out: list, index: int):
+    cmd = ["nvidia-smi", f"--id={index}",
+           "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+           "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+           "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"]
+    try:
+        p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+    except OSError:
+        return
+    try:
+        while not stop.is_set():
+            line = p.stdout.readline()
+            if not line:
+                break
+            out.append([x.strip() for x in line.split(",")])
+    finally:
+        p.kill()
+        p.wait()
+
+
+def summarize_clocks(samples):
+    if not samples:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+    sm = [float(s[0]) for s in samples if s[0].replace(".", "").isdigit()]
+    mx = [float(s[1]) for s in samples if s[1].replace(".", "").isdigit()]
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    reasons = sorted({n for s in samples for n, v in zip(names, s[3:7]) if v.strip().lower() == "active"})
+    return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+            "reasons": reasons, "samples": len(samples)}
+
+
+def build_gpu_workload(wl_key, device, rank):
+    import torch
+    from paper_2507_03220_b200 import AffineParams, GpuBaseExecutor, LayerAddress, Role
+
+    wl = WORKLOADS[wl_key]
+    layers, dims = layer_list(wl)
+    specs = client_specs(wl_key, wl["clients"])
+    seed = 1234 + 7919 * rank
+
+    def gen_layers():
+        g = torch.Generator(device=device)
+        for (b, r) in layers:
+            di, do = dims[r]
+            g.manual_seed(seed * 1000 + b * 8 + r)
+            w = torch.randn(di, do, generator=g, device=device, dtype=torch.float32)
+            w = (w * (1.0 / math.sqrt(di))).to(torch.bfloat16)
+            bias = 0.05 * torch.randn(do, generator=g, device=device)
+            yield LayerAddress(b, Role(r)), AffineParams(w, bias)
+            del w, bias
+
+    ex = GpuBaseExecutor(gen_layers(), device=device.index, retain_layers=False)
+
+    class Ad:
+        def __init__(self):
+            self.lora, self.ia3, self.alpha, self.rank = {}, {}, 0.0, 1
+
+    g = torch.Generator(device=device)
+    for c, (kind, rank_, ft) in enumerate(specs):
+        ad = Ad()
+        g.manual_seed(seed + 17 * c + 5)
+        if kind == "lora":
+            ad.alpha, ad.rank = 2.0 * rank_, rank_
+            for b in range(wl["L"]):
+                for r in (Q, K, V, O):
+                    di, do = dims[r]
+                    a = torch.randn(di, rank_, generator=g, device=device) / math.sqrt(di)
+                    bm = 0.05 * torch.randn(rank_, do, generator=g, device=device)
+                    ad.lora[LayerAddress(b, Role(r))] = (a, bm)
+        else:
+            for b in range(wl["L"]):
+                for r in (K, V, FF_UP):
+                    ad.ia3[LayerAddress(b, Role(r))] = 1.0 + 0.1 * torch.randn(dims[r][1], generator=g, device=device)
+        ex.register_adapter(c, ad)
+        del ad
+
+    # per-client device exchange buffers (DeviceChannel sizing: tokens x max layer width)
+    t = wl["tokens"]
+    maxw = max(wl["d"], wl["d_ff"], wl["V"])
+    bufs = [torch.randn(t * maxw, generator=g, device=device).to(torch.bfloat16) for _ in specs]
+    base_bufs = {c: torch.empty(t * wl["d_ff"], dtype=torch.bfloat16, device=device)
+                 for c, (k, _, ft) in enumerate(specs) if k == "ia3" and ft}
+    fwd, bwd = [], []
+    for (b, r) in layers:
+        di, do = dims[r]
+        segs = []
+        for c, (kind, _, ft) in enumerate(specs):
+            base = None
+            if c in base_bufs and r in (K, V, FF_UP):
+                base = base_bufs[c][: t * do].view(t, do)
+            segs.append((c, bufs[c][: t * di].view(t, di), bufs[c][: t * do].view(t, do), base))
+        fwd.append(ex.compile_dispatch(0, b, r, segs))
+        segs = [(c, bufs[c][: t * do].view(t, do), bufs[c][: t * di].view(t, di), None)
+                for c, (kind, _, ft) in enumerate(specs) if ft]
+        if segs:
+            bwd.append(ex.compile_dispatch(1, b, r, segs))
+    bwd.reverse()
+    return ex, fwd + bwd, specs, wl
+
+
+def run_step(plan, stream):
+    for d in plan:
+        d.run(stream)
+
+
+def e2e_leg(ex, wl_key, specs, steps, device):
+    """Reference-facing path: numpy-like HOST clients. Each dispatch: pinned host payloads ->
+    H2D -> fused compute -> D2H into pinned host reply buffers (in place, like LocalChannel's
+    SharedBuffer), all inside the timed region."""
+    import torch
+    from paper_2507_03220_b200 import Envelope
+
+    wl = WORKLOADS[wl_key]
+    layers, dims = layer_list(wl)
+    t = wl["tokens"]
+    maxw = max(wl["d"], wl["d_ff"], wl["V"])
+    host = [torch.empty(t * maxw, dtype=torch.bfloat16, pin_memory=True) for _ in specs]
+    for h in host:
+        h.normal_()
+    rid = [0]
+    h2d = d2h = 0
+
+    def step():
+        nonlocal h2d, d2h
+        h2d = d2h = 0
+        for (b, r) in layers:
+            di, do = dims[r]
+            envs = []
+            for c in range(len(specs)):
+                rid[0] += 1
+                envs.append(Envelope(c, rid[0], b, r, 0, host[c][: t * di].view(t, di),
+                                     reply_to=host[c][: t * do].view(t, do)))
+                h2d += t * di * 2
+                d2h += t * do * 2
+            ex._compute_batch(0, envs)
+        for (b, r) in reversed(layers):
+            di, do = dims[r]
+            envs = []
+            for c, (_, _, ft) in enumerate(specs):
+                if not ft:
+                    continue
+                rid[0] += 1
+                envs.append(Envelope(c, rid[0], b, r, 1, host[c][: t * do].view(t, do),
+                                     reply_to=host[c][: t * di].view(t, di)))
+                h2d += t * do * 2
+                d2h += t * di * 2
+            ex._compute_batch(1, envs)
+
+    step()  # warm-up (allocates the device staging)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    return dt, h2d, d2h
+
+
+# ============================================================================ CPU leg (oracle)
+
+_CPU = {}
+
+
+def _cpu_task(args):
+    """One (layer, pass, row-chunk) task of the reference algorithm: the batched base GEMM
+    (executor.py:191-231 via the oracle's einsum) plus each client's own adapter step."""
+    from oracle import splitserve_oracle as Or
+    li, pass_kind, clients = args
+    w, bias, ads = _CPU["layers"][li]
+    xs = [_CPU["x"][pass_kind][li][c] for c in clients]
+    envs = [Or.OracleEnvelope(c, 1, 0, 0, pass_kind, x) for c, x in zip(clients, xs)]
+    t0 = time.perf_counter()
+    if pass_kind == 0:
+        out = Or.compute_batch(0, envs, w, bias)
+        for c, x, y in zip(clients, xs, out):
+            Or.apply_adapter(ads.get(c), x, y)
+    else:
+        gs = [x * ads[c].ia3 if (c in ads and ads[c].ia3 is not None) else x for c, x in zip(clients, xs)]
+        envs = [Or.OracleEnvelope(c, 1, 0, 0, 1, gx) for c, gx in zip(clients, gs)]
+        out = Or.compute_batch(1, envs, w, bias)
+        for c, gx, dx in zip(clients, gs, out):
+            ad = ads.get(c)
+            if ad is not None and ad.a is not None:
+                dx + Or.lora_backward_dx(gx, ad.a, ad.b, ad.alpha, ad.rank)
+    return time.perf_counter() - t0
+
+
+class CpuReference:
+    """Bounded sample of the same workload on host cores: block 0's six layers + LM_HEAD,
+    `tokens_per_client` tokens for every client (fwd for all, bwd for fine-tune clients),
+    through the reference algorithm (oracle port, np.einsum optimize=False). Tasks are
+    (layer, pass, 4-client chunk) spread over a fork pool (rows are independent, so this is
+    the same arithmetic). ``sample()`` returns tokens/s for the full 6L+1-layer workload."""
+
+    def __init__(self, wl_key, tokens_per_client=1, procs=None):
+        from oracle import splitserve_oracle as Or
+
+        self.wl = wl = WORKLOADS[wl_key]
+        layers, dims = layer_list(wl)
+        self.specs = specs = client_specs(wl_key, wl["clients"])
+        self.tpc = tokens_per_client
+        sample = [(0, r) for r in (Q, K, V, O, FF_UP, FF_DOWN)] + [(wl["L"], LM_HEAD)]
+        rng = np.random.default_rng(0)
+        _CPU["layers"], _CPU["x"] = [], {0: [], 1: []}
+        for (b, r) in sample:
+            di, do = dims[r]
+            w, bias = Or.layer_params(99, b, r, di, do)
+            ads = {}
+            for c, (kind, rank, ft) in enumerate(specs):
+                if kind == "lora" and r in (Q, K, V, O):
+                    ads[c] = Or.lora_params(99, c, b, r, di, do, rank, 2.0 * rank)
+                elif kind == "ia3" and r in (K, V, FF_UP):
+                    ads[c] = Or.ia3_params(99, c, b, r, do)
+            _CPU["layers"].append((w, bias, ads))
+            _CPU["x"][0].append({c: rng.standard_normal((tokens_per_client, di)).astype(np.float32)
+                                 for c in range(len(specs))})
+            _CPU["x"][1].append({c: rng.standard_normal((tokens_per_client, do)).astype(np.float32)
+                                 for c in range(len(specs))})
+        all_c = list(range(len(specs)))
+        self.ft_c = ft_c = [c for c, s in enumerate(specs) if s[2]]
+        chunk = lambda cs: [cs[i:i + 4] for i in range(0, len(cs), 4)]  # noqa: E731
+        self.block_tasks = [(li, 0, cs) for li in range(6) for cs in chunk(all_c)] + \
+                           [(li, 1, cs) for li in range(6) for cs in chunk(ft_c)]
+        self.head_tasks = [(6, 0, cs) for cs in chunk(all_c)] + [(6, 1, cs) for cs in chunk(ft_c)]
+        ncpu = procs or os.cpu_count() or 1
+        self.n = max(1, min(ncpu, len(self.block_tasks)))
+        for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[var] = "1"
+        import multiprocessing as mp
+        self.pool = mp.get_context("fork").Pool(self.n)
+        self.pool.map(_cpu_task, self.head_tasks[:1])  # fork + import warm-up, untimed
+
+    def sample(self):
+        wl = self.wl
+        t0 = time.perf_counter()
+        self.pool.map(_cpu_task, self.block_tasks, chunksize=1)
+        t_block = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        self.pool.map(_cpu_task, self.head_tasks, chunksize=1)
+        t_head = time.perf_counter() - t0
+        step_s = wl["tokens"] / self.tpc * (wl["L"] * t_block + t_head)
+        tok_s = len(self.specs) * wl["tokens"] / step_s
+        info = (f"block 0 (6 layers) + LM_HEAD, {self.tpc} tok x {len(self.specs)} clients "
+                f"(fwd all, bwd {len(self.ft_c)} FT), {len(self.block_tasks) + len(self.head_tasks)} "
+                f"tasks on {self.n} procs: block {t_block:.2f}s head {t_head:.2f}s per sample, "
+                f"scaled x{wl['L']} blocks x{wl['tokens']}/{self.tpc} tok")
+        return tok_s, info
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ============================================================================ main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="13b", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=1)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    wl = WORKLOADS[args.workload]
+    specs = client_specs(args.workload, wl["clients"])
+    tokens_per_rank = wl["clients"] * wl["tokens"]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cpu_ref = CpuReference(args.workload, args.cpu_tokens)
+        vals = []
+        for i in range(max(0, args.warmup) + args.steps):
+            tok_s, info = cpu_ref.sample()
+            if i >= args.warmup:
+                vals.append(tok_s)
+        cpu_ref.close()
+        cores = cpu_ref.n
+        v = float(np.mean(vals))
+        line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * tokens_per_rank / v, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded N(0,1) activations, reference-style random init)",
+                "impl": "reference",
+                "config": {"workload": wl["name"], "model": f"d{wl['d']}-ff{wl['d_ff']}-L{wl['L']}-V{wl['V']}",
+                           "clients": wl["clients"], "global_batch": tokens_per_rank, "seq_len": wl["seq"],
+                           "parallelism": "host process pool"},
+                "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
+                                 "sample": info, "cpu": cpu_model()},
+                "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    from paper_2507_03220_b200 import _lib
+
+    ex, plan, specs, wl = build_gpu_workload(args.workload, device, rank)
+    ctx = ex.ctx
+    stream = torch.cuda.current_stream(device)
+    for _ in range(max(3, args.warmup)):
+        run_step(plan, stream)
+    torch.cuda.synchronize()
+
+    samples, stop = [], threading.Event()
+    sampler = threading.Thread(target=nvsmi_sampler, args=(stop, samples, local), daemon=True)
+    sampler.start()
+    time.sleep(0.5)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches()
+    ctx.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        run_step(plan, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stop.set()
+    launches = ctx.kernel_launches() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    gemm = ctx.profile_read(_lib.SS_KERNEL_GEMM)
+    shrink = ctx.profile_read(_lib.SS_KERNEL_SHRINK)
+    gather = ctx.profile_read(_lib.SS_KERNEL_GATHER)
+    ctx.profile(False)
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    sampler.join(timeout=2)
+    clocks = summarize_clocks(samples)
+
+    tokens = tokens_per_rank * world
+    value = tokens / (ms / 1e3)
+    step_flops = flops_per_step(wl, specs)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak = float(peaks.get("bf16_tflops_sustained", 1400.0))
+    gemm_tflops = gemm["flops"] / (gemm["ms"] / 1e3) / 1e12 if gemm["ms"] else None
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    e2e = None
+    if not args.skip_e2e:
+        dt, h2d, d2h = e2e_leg(ex, args.workload, specs, max(1, args.e2e_steps), device)
+        if world > 1:
+            t = torch.tensor([dt], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": tokens / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
+               "path": "GpuBaseExecutor._compute_batch, pinned host bf16 payloads + host reply buffers, "
+                       f"{max(1, args.e2e_steps)} timed step(s) after 1 warm-up"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        cpu_ref = CpuReference(args.workload, args.cpu_tokens)
+        tok_s, info = cpu_ref.sample()
+        tok_s2, info = cpu_ref.sample()
+        cpu_ref.close()
+        cpu = {"value": 0.5 * (tok_s + tok_s2), "unit": "tokens/s", "cores": cpu_ref.n, "kind": "port",
+               "sample": info + " (mean of 2 samples)", "cpu": cpu_model()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights/adapters/activations, per-layer seeds)",
+            "config": {"workload": wl["name"], "model": f"d{wl['d']}-ff{wl['d_ff']}-L{wl['L']}-V{wl['V']}",
+                       "clients": wl["clients"], "global_batch": tokens, "seq_len": wl["seq"],
+                       "batch_per_client": wl["batch"], "rows_per_fwd_dispatch": tokens_per_rank,
+                       "parallelism": f"segment-parallel replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (every step streams all 6L+1 weight matrices)",
+                       "step_tflop": step_flops / 1e12, "achieved_step_tflops": step_flops / (ms / 1e3) / 1e12},
+            "roofline": {"bound": "tensor", "kernel": "seg_gemm_kernel (fused base GEMM + LoRA/IA3 epilogue)",
+                         "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (gemm_tflops / peak) if gemm_tflops else None, "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
+                         "gemm_share_of_step": gemm["ms"] / (ms * args.steps),
+                         "gemm_launches": gemm["launches"],
+                         "shrink_ms_per_step": shrink["ms"] / args.steps,
+                         "gather_ms_per_step": gather["ms"] / args.steps,
+                         "gather_gbs": (gather["bytes"] / (gather["ms"] / 1e3) / 1e9) if gather["ms"] else None},
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

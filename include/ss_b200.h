@@ -125,6 +125,17 @@ SS_API int ss_memory_stats(const ss_ctx* ctx, int64_t* weight_bytes, int64_t* ad
 /* Number of kernels launched by this context since creation (evidence / bench counter). */
 SS_API int64_t ss_kernel_launches(const ss_ctx* ctx);
 
+/* In-stream kernel timing (bench evidence): while enabled, every launch of kind
+ * SS_KERNEL_{GATHER,SHRINK,GEMM} is bracketed by CUDA events on its own stream, and its
+ * algorithmic FLOPs / bytes are accumulated. ss_profile_read synchronizes the recorded events
+ * and returns totals since the last ss_profile(ctx, 1). */
+#define SS_KERNEL_GATHER 0
+#define SS_KERNEL_SHRINK 1
+#define SS_KERNEL_GEMM 2
+SS_API int ss_profile(ss_ctx* ctx, int enable);
+SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* launches,
+                           double* flops, double* bytes);
+
 /* Tuning knob: M-tile grouping of the persistent raster (default 16). */
 SS_API int ss_set_option(ss_ctx* ctx, const char* key, int64_t value);
 

@@ -42,7 +42,12 @@ EXPORTED = (
     "ss_ctx_create", "ss_ctx_destroy", "ss_last_error", "ss_version", "ss_load_layer",
     "ss_unload_layer", "ss_set_adapter", "ss_clear_adapter", "ss_clear_client",
     "ss_compute_batch", "ss_memory_stats", "ss_kernel_launches", "ss_set_option",
+    "ss_profile", "ss_profile_read",
 )
+
+SS_KERNEL_GATHER = 0
+SS_KERNEL_SHRINK = 1
+SS_KERNEL_GEMM = 2
 
 
 class SsSeg(ctypes.Structure):
@@ -101,6 +106,9 @@ def load() -> ctypes.CDLL:
                                       ctypes.POINTER(i64)]),
             "ss_kernel_launches": (i64, [vp]),
             "ss_set_option": (i32, [vp, ctypes.c_char_p, i64]),
+            "ss_profile": (i32, [vp, i32]),
+            "ss_profile_read": (i32, [vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64),
+                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

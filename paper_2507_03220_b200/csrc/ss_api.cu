@@ -54,6 +54,12 @@ struct Layer {
   std::map<uint32_t, AdapterSlot> adapters;
 };
 
+struct ProfRec {
+  cudaEvent_t a, b;
+  int kind;
+  double flops, bytes;
+};
+
 struct Staging {
   void* host = nullptr;     // pinned
   void* dev = nullptr;      // device copy of the tables
@@ -85,6 +91,12 @@ struct ss_ctx {
   int64_t launches = 0;
   int group_m = 16;
   int64_t weight_bytes = 0, adapter_bytes = 0;
+  // in-stream profiling
+  bool profiling = false;
+  std::vector<ProfRec> prof;       // pending event pairs
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[3] = {0, 0, 0}, prof_flops[3] = {0, 0, 0}, prof_bytes[3] = {0, 0, 0};
+  int64_t prof_n[3] = {0, 0, 0};
 };
 
 namespace {
@@ -233,6 +245,43 @@ int ensure_dev(ss_ctx* ctx, T*& ptr, size_t& cap, size_t bytes) {
 
 bool aligned16(const void* p, int64_t ld, size_t esz) {
   return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * (int64_t)esz) % 16 == 0);
+}
+
+cudaEvent_t pool_event(ss_ctx* ctx) {
+  if (!ctx->ev_pool.empty()) {
+    cudaEvent_t e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Bracket one launch: returns the index of the record (or -1 when not profiling).
+int prof_begin(ss_ctx* ctx, cudaStream_t st, int kind, double flops, double bytes) {
+  if (!ctx->profiling) return -1;
+  ProfRec r{pool_event(ctx), pool_event(ctx), kind, flops, bytes};
+  cudaEventRecord(r.a, st);
+  ctx->prof.push_back(r);
+  return (int)ctx->prof.size() - 1;
+}
+void prof_end(ss_ctx* ctx, cudaStream_t st, int idx) {
+  if (idx >= 0) cudaEventRecord(ctx->prof[idx].b, st);
+}
+void prof_drain(ss_ctx* ctx) {
+  for (auto& r : ctx->prof) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    ctx->prof_ms[r.kind] += ms;
+    ctx->prof_flops[r.kind] += r.flops;
+    ctx->prof_bytes[r.kind] += r.bytes;
+    ctx->prof_n[r.kind] += 1;
+    ctx->ev_pool.push_back(r.a);
+    ctx->ev_pool.push_back(r.b);
+  }
+  ctx->prof.clear();
 }
 
 struct KernelAttrs {
@@ -488,6 +537,28 @@ int ss_memory_stats(const ss_ctx* ctx, int64_t* w, int64_t* a, int64_t* ws) {
 
 int64_t ss_kernel_launches(const ss_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+int ss_profile(ss_ctx* ctx, int enable) {
+  if (!ctx) return SS_E_ARG;
+  prof_drain(ctx);
+  for (int k = 0; k < 3; ++k) {
+    ctx->prof_ms[k] = ctx->prof_flops[k] = ctx->prof_bytes[k] = 0;
+    ctx->prof_n[k] = 0;
+  }
+  ctx->profiling = enable != 0;
+  return SS_OK;
+}
+
+int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* launches, double* flops,
+                    double* bytes) {
+  if (!ctx || kernel < 0 || kernel > 2) return SS_E_ARG;
+  prof_drain(ctx);
+  if (total_ms) *total_ms = ctx->prof_ms[kernel];
+  if (launches) *launches = ctx->prof_n[kernel];
+  if (flops) *flops = ctx->prof_flops[kernel];
+  if (bytes) *bytes = ctx->prof_bytes[kernel];
+  return SS_OK;
+}
+
 int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
                      void* stream_, int32_t* seg_status) {
   if (!ctx) return SS_E_ARG;
@@ -652,7 +723,11 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   gp.row_seg = ctx->row_seg;
   {
     const int grid = (int)std::min<int64_t>((M + 7) / 8, (int64_t)ctx->num_sms * 8);
+    double src_bytes = 0;
+    for (const DevSeg& d : ds) src_bytes += (double)d.rows * K * ((d.flags & SEGF_SRC_BF16) ? 2 : 4);
+    const int pi = prof_begin(ctx, stream, SS_KERNEL_GATHER, 0.0, src_bytes + (double)M * K * 2 + M * 4.0);
     gather_rows_kernel<<<grid, 256, 0, stream>>>(gp);
+    prof_end(ctx, stream, pi);
     CK(cudaGetLastError());
     ctx->launches++;
   }
@@ -671,8 +746,16 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     sp.segs = d_segs;
     sp.items = reinterpret_cast<const ShrinkItem*>(dv + off_it);
     sp.a_lora = ctx->a_lora;
+    double sf = 0, sb = 0;
+    for (const DevSeg& d : ds)
+      if (d.flags & SEGF_LORA) {
+        sf += 2.0 * d.rows * d.rank_pad * K;
+        sb += (double)d.rows * K * 2 + (double)d.rank_pad * K * 2 + (double)d.rows * d.rank_pad * 2;
+      }
+    const int pi = prof_begin(ctx, stream, SS_KERNEL_SHRINK, sf, sb);
     lora_shrink_kernel<<<(int)items.size(), GEMM_THREADS, SHRINK_SMEM, stream>>>(
         tmA, bwd ? L.tm_b : L.tm_at, sp);
+    prof_end(ctx, stream, pi);
     CK(cudaGetLastError());
     ctx->launches++;
   } else {
@@ -699,10 +782,20 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   const int tiles = gpm.num_m_tiles * gpm.num_n_tiles;
   const int grid = std::min(tiles, ctx->num_sms);
   const CUtensorMap& tmBP = any_lora ? (bwd ? L.tm_at : L.tm_b) : tmA;
+  // algorithmic work: base GEMM + each LoRA segment's own rank (the block-diagonal zeros of
+  // neighbouring segments are not counted); bytes: X, W, bias, outputs
+  double gf = 2.0 * (double)M * N * K, gb = (double)M * K * 2 + (double)K * N * 2;
+  for (const DevSeg& d : ds) {
+    gb += (double)d.rows * N * ((d.flags & SEGF_DST_BF16) ? 2 : 4);
+    if (d.flags & SEGF_WANT_BASE) gb += (double)d.rows * N * ((d.flags & SEGF_BASE_BF16) ? 2 : 4);
+    if (d.flags & SEGF_LORA) gf += 2.0 * d.rows * d.rank_pad * N;
+  }
+  const int pg = prof_begin(ctx, stream, SS_KERNEL_GEMM, gf, gb);
   if (bwd)
     seg_gemm_kernel<true><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, L.tm_w_bwd, tmAL, tmBP, gpm);
   else
     seg_gemm_kernel<false><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, L.tm_w_fwd, tmAL, tmBP, gpm);
+  prof_end(ctx, stream, pg);
   CK(cudaGetLastError());
   ctx->launches++;
   CK(cudaEventRecord(ctx->compute_done, stream));

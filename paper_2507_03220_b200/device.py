@@ -204,6 +204,17 @@ class SsContext:
     def kernel_launches(self) -> int:
         return int(self.lib.ss_kernel_launches(self.h))
 
+    def profile(self, enable: bool) -> None:
+        """Start (and reset) / stop in-stream CUDA-event timing of every kernel launch."""
+        check(self.h, self.lib.ss_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self, kernel: int) -> dict:
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        fl, by = ctypes.c_double(), ctypes.c_double()
+        check(self.h, self.lib.ss_profile_read(self.h, int(kernel), ctypes.byref(ms), ctypes.byref(n),
+                                               ctypes.byref(fl), ctypes.byref(by)))
+        return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+
     def set_option(self, key: str, value: int) -> None:
         check(self.h, self.lib.ss_set_option(self.h, key.encode(), int(value)))
 

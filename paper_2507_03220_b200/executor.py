@@ -96,6 +96,35 @@ class ExecutorMetrics:
                     out.writerow([block, Role(role).name, pass_kind, size, tokens, mean_wait])
 
 
+@dataclass
+class _LayerShape:
+    d_in: int
+    d_out: int
+
+    @property
+    def nbytes(self) -> int:
+        return 2 * self.d_in * self.d_out + 4 * self.d_out
+
+
+class Dispatch:
+    """A prebuilt dispatch over fixed device buffers (one ss_compute_batch per ``run``).
+
+    For device-resident clients whose exchange buffers do not move (DeviceChannel after its
+    first grow), the segment table is built once; each step is one C-ABI call."""
+
+    def __init__(self, ctx: SsContext, pass_kind: int, key, segs):
+        from .device import SegmentTable
+        self.ctx, self.pass_kind, self.key = ctx, pass_kind, key
+        self.table = SegmentTable(segs)
+        self.rows = sum(int(s.src.shape[0]) for s in segs)
+
+    def run(self, stream: torch.cuda.Stream | None = None) -> None:
+        self.ctx.compute_table(self.pass_kind, self.key[0], self.key[1], self.table, stream)
+        bad = [s for s in self.table.statuses() if s != _lib.SS_SEG_OK]
+        if bad:
+            raise ProtocolError(f"dispatch {self.key} pass {self.pass_kind}: segment status {bad}")
+
+
 def _is_device(x) -> bool:
     return isinstance(x, torch.Tensor) and x.is_cuda
 
@@ -111,8 +140,11 @@ class GpuBaseExecutor:
 
     def __init__(self, layers, policy: BatchPolicy | None = None, save_activations: bool = False,
                  *, device: int = 0, stream: torch.cuda.Stream | None = None,
-                 context: SsContext | None = None):
-        self.layers = dict(layers)
+                 context: SsContext | None = None, retain_layers: bool = True):
+        """``layers``: mapping (or iterable of pairs) LayerAddress -> AffineParams. Weights are
+        copied to the device as bf16 (bias f32). With ``retain_layers=False`` the host-side
+        parameters are dropped after upload (``layers`` then holds shape-only records), so a
+        generator of pairs streams a large model through without a second copy."""
         self.policy = policy or BatchPolicy()
         self.save_activations = save_activations
         self._saved_debug: list = []
@@ -120,10 +152,12 @@ class GpuBaseExecutor:
         self.device = self.ctx.device
         self.stream = stream
         self._dims: dict[tuple[int, int], tuple[int, int]] = {}
-        for addr, params in self.layers.items():
+        self.layers = {}
+        for addr, params in (layers.items() if hasattr(layers, "items") else layers):
             key = addr_key(addr)
             self.ctx.load_layer(key[0], key[1], params.weight, getattr(params, "bias", None))
             self._dims[key] = (int(params.weight.shape[0]), int(params.weight.shape[1]))
+            self.layers[addr] = params if retain_layers else _LayerShape(*self._dims[key])
         self._fused: dict[int, set] = defaultdict(set)   # client -> {(block, role)} fused
         self._queues: dict[tuple, deque] = defaultdict(deque)
         self._cond = threading.Condition()
@@ -134,6 +168,8 @@ class GpuBaseExecutor:
         self.metrics = ExecutorMetrics()
         self.ledger = ledger_mod.MemoryLedger("executor")
         self._pinned: dict[str, torch.Tensor] = {}
+        self._dev_staging: dict = {}
+        self._host_replies: list = []
         self.last_event: torch.cuda.Event | None = None
         self._sync_ledger()
 
@@ -216,6 +252,18 @@ class GpuBaseExecutor:
 
     def fused_addresses(self, client_id: int) -> set:
         return set(self._fused.get(client_id, ()))
+
+    def compile_dispatch(self, pass_kind: int, block: int, role: int, segments) -> Dispatch:
+        """Prebuild a dispatch: ``segments`` = [(client_id, src, dst, base_or_None)] over
+        device tensors, in batch order. Adapters registered for (client, layer) are fused."""
+        key = (int(block), int(role))
+        if key not in self._dims:
+            raise ProtocolError(f"unknown layer {key}")
+        segs = [Seg(client_id=c, src=src, dst=dst,
+                    base=base if pass_kind == PASS_FORWARD else None,
+                    adapter=pass_kind != PASS_NOISE_EFFECT and key in self._fused.get(c, ()))
+                for c, src, dst, base in segments]
+        return Dispatch(self.ctx, pass_kind, key, segs)
 
     def _sync_ledger(self) -> None:
         w, a, _ = self.ctx.memory_stats()
@@ -329,9 +377,11 @@ class GpuBaseExecutor:
     # -- staging helpers --------------------------------------------------------------------
     def _stage_inputs(self, envelopes, good, stream):
         """Device views of every good payload; host payloads go through one pinned buffer and
-        one H2D copy (the only host->device crossing of a dispatch)."""
+        one H2D copy (the only host->device crossing of a dispatch). Payloads that already sit
+        in pinned host memory are copied straight from there."""
         srcs: list = [None] * len(good)
-        host = [j for j, i in enumerate(good) if not _is_device(envelopes[i].payload)]
+        host = []
+        pinned = []
         for j, i in enumerate(good):
             p = envelopes[i].payload
             if _is_device(p):
@@ -340,6 +390,23 @@ class GpuBaseExecutor:
                 if p.stride(-1) != 1:
                     p = p.contiguous()
                 srcs[j] = p
+            elif (isinstance(p, torch.Tensor) and p.is_pinned() and p.is_contiguous()
+                  and p.dtype in (torch.float32, torch.bfloat16)):
+                pinned.append(j)
+            else:
+                host.append(j)
+        if pinned:
+            sizes = [envelopes[good[j]].payload.numel() for j in pinned]
+            dts = {envelopes[good[j]].payload.dtype for j in pinned}
+            dt = dts.pop() if len(dts) == 1 else torch.float32
+            dev = self._dev_buf("in", sum(sizes), dt)
+            pos = 0
+            for j, n in zip(pinned, sizes):
+                p = envelopes[good[j]].payload
+                view = dev[pos:pos + n].view(p.shape)
+                view.copy_(p, non_blocking=True)
+                srcs[j] = view
+                pos += n
         if host:
             arrays = []
             for j in host:
@@ -362,18 +429,34 @@ class GpuBaseExecutor:
                 srcs[j] = dev[o:o + s].view(a.dtype).view(a.shape)
         return srcs, host
 
+    def _dev_buf(self, name: str, numel: int, dtype) -> torch.Tensor:
+        """Grow-only device staging (reported through the ledger's transient category)."""
+        key = (name, dtype)
+        buf = self._dev_staging.get(key)
+        if buf is None or buf.numel() < numel:
+            buf = torch.empty(max(numel, 1 << 20), dtype=dtype, device=self.device)
+            self._dev_staging[key] = buf
+        return buf[:numel]
+
     def _stage_outputs(self, envelopes, good, out_w, stream):
         dsts: list = [None] * len(good)
         host_out = {}
         need = []
+        self._host_replies = []
         for j, i in enumerate(good):
             env = envelopes[i]
             r = getattr(env, "reply_to", None)
             if r is not None:
-                if not _is_device(r) or tuple(r.shape) != (env.token_count, out_w):
-                    raise ProtocolError(f"reply_to must be a device tensor of shape "
-                                        f"{(env.token_count, out_w)}")
-                dsts[j] = r
+                if tuple(r.shape) != (env.token_count, out_w) or not isinstance(r, torch.Tensor):
+                    raise ProtocolError(f"reply_to must be a tensor of shape {(env.token_count, out_w)}")
+                if r.is_cuda:
+                    dsts[j] = r
+                else:
+                    # host reply buffer: compute into device staging, then one D2H into it
+                    n = r.numel()
+                    dev = self._dev_buf(f"out{j}", n, r.dtype if r.dtype == torch.bfloat16 else torch.float32)
+                    dsts[j] = dev.view(r.shape)
+                    self._host_replies.append((r, dsts[j]))
             else:
                 need.append(j)
         if need:
@@ -393,6 +476,11 @@ class GpuBaseExecutor:
         return dsts, host_out
 
     def _finish_outputs(self, host_out, ev):
+        if self._host_replies:
+            for host, dev in self._host_replies:
+                host.copy_(dev, non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize()
+            self._host_replies = []
         if not host_out:
             return {}
         out = host_out.pop("__out__")
