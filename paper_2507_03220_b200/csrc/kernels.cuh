@@ -87,6 +87,100 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int gro
   nb = r / gsize;
 }
 
+// Epilogue of one accumulator tile for the calling thread's row (TMEM lane): + bias,
+// optional pre-IA3 y_base store, * IA3 l, store into the row's segment destination.
+// Every thread of the warp must call it (tcgen05.ld is warp-collective).
+__device__ __forceinline__ void epilogue_rows(const GemmParams& p, uint32_t tmem_acc, uint32_t ew,
+                                              int row, int n0, uint64_t* tfull, uint32_t tfull_ph) {
+  const bool row_ok = row < p.M;
+  DevSeg sg;
+  if (row_ok) sg = p.segs[p.row_seg[row]];
+  mbar_wait(tfull, tfull_ph);
+  tc_fence_after();
+  const int r_local = row_ok ? row - sg.row0 : 0;
+  const bool use_ia3 = row_ok && p.ia3_in_epilogue && (sg.flags & SEGF_IA3);
+  const bool want_base = row_ok && (sg.flags & SEGF_WANT_BASE);
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tmem_acc + c * 32 + ((ew * 32u) << 16), r);
+    tmem_wait_ld();
+    const int n = n0 + c * 32;
+    if (!row_ok || n >= p.N) continue;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    const int ncols = min(32, p.N - n);
+    if (p.has_bias) {
+      if (ncols == 32) {
+        const float4* b4 = reinterpret_cast<const float4*>(p.bias + n);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 bb = __ldg(b4 + j);
+          v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
+        }
+      } else {
+        for (int j = 0; j < ncols; ++j) v[j] += __ldg(p.bias + n + j);
+      }
+    }
+    if (want_base) {
+      const bool bf = sg.flags & SEGF_BASE_BF16;
+      char* base = reinterpret_cast<char*>(sg.dst_base) +
+                   ((int64_t)r_local * sg.base_ld + n) * (bf ? 2 : 4);
+      if (ncols == 32 && (sg.flags & SEGF_BASE_VEC)) {
+        if (bf) {
+          uint4* o = reinterpret_cast<uint4*>(base);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            o[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                              pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+        } else {
+          float4* o = reinterpret_cast<float4*>(base);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+      } else {
+        for (int j = 0; j < ncols; ++j) {
+          if (bf) reinterpret_cast<__nv_bfloat16*>(base)[j] = __float2bfloat16_rn(v[j]);
+          else reinterpret_cast<float*>(base)[j] = v[j];
+        }
+      }
+    }
+    if (use_ia3) {
+      if (ncols == 32) {
+        const float4* l4 = reinterpret_cast<const float4*>(sg.ia3 + n);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 ll = __ldg(l4 + j);
+          v[4 * j] *= ll.x; v[4 * j + 1] *= ll.y; v[4 * j + 2] *= ll.z; v[4 * j + 3] *= ll.w;
+        }
+      } else {
+        for (int j = 0; j < ncols; ++j) v[j] *= __ldg(sg.ia3 + n + j);
+      }
+    }
+    const bool bf = sg.flags & SEGF_DST_BF16;
+    char* dst = reinterpret_cast<char*>(sg.dst) + ((int64_t)r_local * sg.dst_ld + n) * (bf ? 2 : 4);
+    if (ncols == 32 && (sg.flags & SEGF_DST_VEC)) {
+      if (bf) {
+        uint4* o = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          o[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                            pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+      } else {
+        float4* o = reinterpret_cast<float4*>(dst);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+    } else {
+      for (int j = 0; j < ncols; ++j) {
+        if (bf) reinterpret_cast<__nv_bfloat16*>(dst)[j] = __float2bfloat16_rn(v[j]);
+        else reinterpret_cast<float*>(dst)[j] = v[j];
+      }
+    }
+  }
+}
+
 // ============================================================================ K1/K2/K5
 template <bool kBwd>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -247,95 +341,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
-      const int row = mb * BM + ew * 32 + lane;
-      const int n0 = nb * BN;
-      const bool row_ok = row < p.M;
-      DevSeg sg;
-      if (row_ok) sg = p.segs[p.row_seg[row]];
-      mbar_wait(&tfull_bar[acc], acc_ph);
-      tc_fence_after();
-      const int r_local = row_ok ? row - sg.row0 : 0;
-      const bool use_ia3 = row_ok && p.ia3_in_epilogue && (sg.flags & SEGF_IA3);
-      const bool want_base = row_ok && (sg.flags & SEGF_WANT_BASE);
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + acc * BN + c * 32 + ((ew * 32u) << 16), r);
-        tmem_wait_ld();
-        const int n = n0 + c * 32;
-        if (!row_ok || n >= p.N) continue;
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        const int ncols = min(32, p.N - n);
-        if (p.has_bias) {
-          if (ncols == 32) {
-            const float4* b4 = reinterpret_cast<const float4*>(p.bias + n);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 bb = __ldg(b4 + j);
-              v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
-            }
-          } else {
-            for (int j = 0; j < ncols; ++j) v[j] += __ldg(p.bias + n + j);
-          }
-        }
-        if (want_base) {
-          const bool bf = sg.flags & SEGF_BASE_BF16;
-          char* base = reinterpret_cast<char*>(sg.dst_base) +
-                       ((int64_t)r_local * sg.base_ld + n) * (bf ? 2 : 4);
-          if (ncols == 32 && (sg.flags & SEGF_BASE_VEC)) {
-            if (bf) {
-              uint4* o = reinterpret_cast<uint4*>(base);
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                o[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                                  pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
-            } else {
-              float4* o = reinterpret_cast<float4*>(base);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            }
-          } else {
-            for (int j = 0; j < ncols; ++j) {
-              if (bf) reinterpret_cast<__nv_bfloat16*>(base)[j] = __float2bfloat16_rn(v[j]);
-              else reinterpret_cast<float*>(base)[j] = v[j];
-            }
-          }
-        }
-        if (use_ia3) {
-          if (ncols == 32) {
-            const float4* l4 = reinterpret_cast<const float4*>(sg.ia3 + n);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 ll = __ldg(l4 + j);
-              v[4 * j] *= ll.x; v[4 * j + 1] *= ll.y; v[4 * j + 2] *= ll.z; v[4 * j + 3] *= ll.w;
-            }
-          } else {
-            for (int j = 0; j < ncols; ++j) v[j] *= __ldg(sg.ia3 + n + j);
-          }
-        }
-        const bool bf = sg.flags & SEGF_DST_BF16;
-        char* dst = reinterpret_cast<char*>(sg.dst) + ((int64_t)r_local * sg.dst_ld + n) * (bf ? 2 : 4);
-        if (ncols == 32 && (sg.flags & SEGF_DST_VEC)) {
-          if (bf) {
-            uint4* o = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              o[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                                pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
-          } else {
-            float4* o = reinterpret_cast<float4*>(dst);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          }
-        } else {
-          for (int j = 0; j < ncols; ++j) {
-            if (bf) reinterpret_cast<__nv_bfloat16*>(dst)[j] = __float2bfloat16_rn(v[j]);
-            else reinterpret_cast<float*>(dst)[j] = v[j];
-          }
-        }
-      }
+      epilogue_rows(p, tmem_base + acc * BN, ew, mb * BM + ew * 32 + lane, nb * BN, &tfull_bar[acc],
+                    acc_ph);
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
@@ -346,6 +353,203 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ============================================================================ K1/K2/K5, 2-CTA
+// CTA pair (cluster of 2 on one TPC), tcgen05 cta_group::2: one UMMA 256x256x16 per K step.
+// Each CTA stages its own 128 rows of A and HALF of the 256 B columns, so per SM the MMA
+// reads 4 KB + 4 KB of smem per 128-cycle K step instead of 4 KB + 8 KB (the 1-CTA kernel
+// is smem-bandwidth bound, profiles/r01_ncu_gemm_full.md). The leader CTA (rank 0) issues
+// the MMAs; both CTAs run TMA producers (completion counted on the leader's full barrier)
+// and epilogues (each drains its own TMEM lanes = its 128 rows).
+constexpr int BM2 = 256;                        // rows per pair tile
+constexpr int STAGES2 = 6;
+constexpr int B_HALF_BYTES = (BN / 2) * BK * 2;  // 16 KB
+constexpr int STAGE2_BYTES = A_STAGE_BYTES + B_HALF_BYTES;
+constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 256;
+
+template <bool kBwd>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    seg_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,   // X  [M, K] bf16, box {64,128}
+                     const __grid_constant__ CUtensorMap tmB,   // W: fwd box {64,64}; bwd {64,128}
+                     const __grid_constant__ CUtensorMap tmAL,  // A_lora [M, R_w], box {64,128}
+                     const __grid_constant__ CUtensorMap tmBP,  // pack [R, N], box {64,16}
+                     const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES2 * A_STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES2;
+  uint64_t* tfull_bar = empty_bar + STAGES2;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    if (p.any_lora) {
+      tma_prefetch_desc(&tmAL);
+      tma_prefetch_desc(&tmBP);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full_bar[s], 1);    // leader: one arrive.expect_tx per stage (+ both CTAs' bytes)
+      mbar_init(&empty_bar[s], 1);   // one multicast commit per stage
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 8);  // leader: 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  const int nkb = (p.K + BK - 1) / BK;
+  const int cluster_id = blockIdx.x >> 1;
+  const int num_clusters = gridDim.x >> 1;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        int mb, nb;
+        tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+        const int m0 = mb * BM2 + crank * BM;
+        const int nh = nb * BN + crank * (BN / 2);  // this CTA's half of the N columns
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          const uint32_t fb = full0 + s * 8;
+          if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE2_BYTES);
+          tma_load_2d_2sm(smA + s * A_STAGE_BYTES, &tmA, fb, kb * BK, m0);
+          uint8_t* b = smB + s * B_HALF_BYTES;
+          if (kBwd) {
+            tma_load_2d_2sm(b, &tmB, fb, kb * BK, nh);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 128; ++j)
+              tma_load_2d_2sm(b + j * (BK * 128), &tmB, fb, nh + 64 * j, kb * BK);
+          }
+          if (++s == STAGES2) { s = 0; ph ^= 1; }
+        }
+        if (p.any_lora) {
+          const int cb = p.tile_chunk_begin[mb];
+          const int cc = p.tile_chunk_count[mb];
+          for (int ls = 0; ls * 4 < cc; ++ls) {
+            const int nq = min(4, cc - ls * 4);
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            const uint32_t fb = full0 + s * 8;
+            if (leader)
+              mbar_expect_tx(&full_bar[s], 2 * (A_STAGE_BYTES + nq * (BN / 128) * LORA_CHUNK_BYTES));
+            tma_load_2d_2sm(smA + s * A_STAGE_BYTES, &tmAL, fb, ls * BK, m0);
+            uint8_t* b = smB + s * B_HALF_BYTES;
+            for (int q = 0; q < nq; ++q) {
+              const int prow = p.chunks[cb + ls * 4 + q];
+#pragma unroll
+              for (int j = 0; j < BN / 128; ++j)
+                tma_load_2d_2sm(b + j * (BK * 128) + q * LORA_CHUNK_BYTES, &tmBP, fb, nh + 64 * j, prow);
+            }
+            if (++s == STAGES2) { s = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader) {
+      constexpr uint32_t idesc_base = make_idesc_bf16(BM2, BN, false, !kBwd);
+      constexpr uint32_t idesc_lora = make_idesc_bf16(BM2, BN, false, true);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        int mb, nb;
+        tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+        mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(smA + s * A_STAGE_BYTES);
+            const uint32_t b_addr = smem_u32(smB + s * B_HALF_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / UK; ++k) {
+              const uint64_t ad = make_sdesc_sw128(a_addr + k * 32, 16, 1024);
+              const uint64_t bd = kBwd ? make_sdesc_sw128(b_addr + k * 32, 16, 1024)
+                                       : make_sdesc_sw128(b_addr + k * (UK * 128), BK * 128, 1024);
+              mma_bf16_ss_2sm(d_tmem, ad, bd, idesc_base, (kb | k) != 0);
+            }
+            mma_commit_2sm_mc(&empty_bar[s], 0x3);
+          }
+          __syncwarp();
+          if (++s == STAGES2) { s = 0; ph ^= 1; }
+        }
+        if (p.any_lora) {
+          const int cc = p.tile_chunk_count[mb];
+          for (int ls = 0; ls * 4 < cc; ++ls) {
+            const int nq = min(4, cc - ls * 4);
+            mbar_wait(&full_bar[s], ph);
+            tc_fence_after();
+            if (lane == 0) {
+              const uint32_t a_addr = smem_u32(smA + s * A_STAGE_BYTES);
+              const uint32_t b_addr = smem_u32(smB + s * B_HALF_BYTES);
+              for (int q = 0; q < nq; ++q)
+                mma_bf16_ss_2sm(d_tmem, make_sdesc_sw128(a_addr + q * 32, 16, 1024),
+                                make_sdesc_sw128(b_addr + q * LORA_CHUNK_BYTES, BK * 128, 1024),
+                                idesc_lora, 1u);
+              mma_commit_2sm_mc(&empty_bar[s], 0x3);
+            }
+            __syncwarp();
+            if (++s == STAGES2) { s = 0; ph ^= 1; }
+          }
+        }
+        if (lane == 0) mma_commit_2sm_mc(&tfull_bar[acc], 0x3);
+        __syncwarp();
+        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const uint32_t ew = warp - 4;
+    const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+      int mb, nb;
+      tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+      epilogue_rows(p, tmem_base + acc * BN, ew, mb * BM2 + crank * BM + ew * 32 + lane, nb * BN,
+                    &tfull_bar[acc], acc_ph);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, 512);
   }
 }
 
@@ -367,6 +571,7 @@ struct ShrinkItem {
 
 struct ShrinkParams {
   int K;
+  int tile_shift;  // log2 of the GEMM's M-tile height (7: 1-CTA kernel, 8: CTA pair)
   int lora_ld;  // A_lora row stride (elements)
   const DevSeg* segs;
   const ShrinkItem* items;
@@ -456,7 +661,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     const int row = it.row0 + lr;
     const bool ok = lr < it.rows;
-    const int col0 = ((row >> 7) == (sg.row0 >> 7)) ? sg.lora_col0 : 0;
+    const int col0 = ((row >> p.tile_shift) == (sg.row0 >> p.tile_shift)) ? sg.lora_col0 : 0;
     __nv_bfloat16* out = p.a_lora + (int64_t)row * p.lora_ld + col0;
     for (int c = 0; c < nchunk; ++c) {
       uint32_t r[16];

@@ -44,7 +44,7 @@ struct Layer {
   __nv_bfloat16* W = nullptr;
   int64_t ldw = 0;
   float* bias = nullptr;
-  CUtensorMap tm_w_fwd, tm_w_bwd;
+  CUtensorMap tm_w_fwd, tm_w_bwd, tm_w_bwd2;  // bwd: box rows 256 (1-CTA) / 128 (pair)
   // LoRA packs: rows = rank index of every registered client (16-aligned blocks)
   __nv_bfloat16* at_pack = nullptr;  // [cap, ld_at]  (A^T: rank rows x d_in)
   __nv_bfloat16* b_pack = nullptr;   // [cap, ld_b]   (B:   rank rows x d_out)
@@ -90,6 +90,7 @@ struct ss_ctx {
   bool any_compute = false;
   int64_t launches = 0;
   int group_m = 16;
+  int gemm_2cta = 1;  // 1: CTA-pair cta_group::2 kernel, 0: single-CTA kernel
   int64_t weight_bytes = 0, adapter_bytes = 0;
   // in-stream profiling
   bool profiling = false;
@@ -295,6 +296,10 @@ int set_kernel_attrs(ss_ctx* ctx) {
                           GEMM_SMEM));
   CK(cudaFuncSetAttribute(seg_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           GEMM_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          GEMM2_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          GEMM2_SMEM));
   CK(cudaFuncSetAttribute(lora_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           SHRINK_SMEM));
   g_attrs.done = true;
@@ -307,7 +312,7 @@ int set_kernel_attrs(ss_ctx* ctx) {
 extern "C" {
 
 const char* ss_version(void) {
-  return "ss_b200 1.0 (sm_100a tcgen05/TMEM/TMA segmented executor; BM=128 BN=256 BK=64)";
+  return "ss_b200 1.0 (sm_100a tcgen05/TMEM/TMA segmented executor; CTA-pair 256x256x64 / single-CTA 128x256x64)";
 }
 
 const char* ss_last_error(const ss_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -389,6 +394,10 @@ int ss_ctx_destroy(ss_ctx* ctx) {
 
 int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!ctx || !key) return SS_E_ARG;
+  if (!strcmp(key, "gemm_2cta")) {
+    ctx->gemm_2cta = value ? 1 : 0;
+    return SS_OK;
+  }
   if (!strcmp(key, "group_m")) {
     if (value < 1) return fail(ctx, SS_E_ARG, "group_m must be >= 1");
     ctx->group_m = (int)value;
@@ -426,6 +435,8 @@ int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const v
   rc = encode_2d(ctx, &L.tm_w_fwd, L.W, d_out, d_in, L.ldw, 64, BK);
   if (rc) return rc;
   rc = encode_2d(ctx, &L.tm_w_bwd, L.W, d_out, d_in, L.ldw, 64, BN);
+  if (rc) return rc;
+  rc = encode_2d(ctx, &L.tm_w_bwd2, L.W, d_out, d_in, L.ldw, 64, BN / 2);
   if (rc) return rc;
   ctx->weight_bytes += (int64_t)d_in * L.ldw * 2 + (bias ? round_up(d_out, 64) * 4 : 0);
   ctx->layers[{block, role}] = L;
@@ -632,21 +643,24 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   CK(cudaSetDevice(ctx->device));
 
   // ---- M-tile tables for the block-diagonal LoRA operand
-  const int num_m = (int)((M + BM - 1) / BM);
+  const bool pair = ctx->gemm_2cta != 0;
+  const int TM = pair ? BM2 : BM;             // M-tile height of the GEMM kernel
+  const int tshift = pair ? 8 : 7;
+  const int num_m = (int)((M + TM - 1) / TM);
   std::vector<int32_t> t_begin(num_m, 0), t_count(num_m, 0), chunks;
   std::vector<ShrinkItem> items;
   int max_cols = 0;
   if (any_lora) {
     size_t si = 0;
     for (int mt = 0; mt < num_m; ++mt) {
-      const int64_t r0 = (int64_t)mt * BM, r1 = std::min<int64_t>(M, r0 + BM);
+      const int64_t r0 = (int64_t)mt * TM, r1 = std::min<int64_t>(M, r0 + TM);
       while (si < ds.size() && ds[si].row0 + ds[si].rows <= r0) ++si;
       t_begin[mt] = (int32_t)chunks.size();
       for (size_t j = si; j < ds.size() && ds[j].row0 < r1; ++j) {
         DevSeg& d = ds[j];
         if (!(d.flags & SEGF_LORA)) continue;
         const int col = (int)(chunks.size() - t_begin[mt]) * LORA_CHUNK;
-        if ((d.row0 >> 7) == mt) d.lora_col0 = col;
+        if ((d.row0 >> tshift) == mt) d.lora_col0 = col;
         for (int q = 0; q < d.rank_pad / LORA_CHUNK; ++q) chunks.push_back(d.pack_row + q * LORA_CHUNK);
       }
       t_count[mt] = (int32_t)chunks.size() - t_begin[mt];
@@ -663,7 +677,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
 
   // ---- workspace
   const int64_t ldx = round_up(K, 64);
-  const int64_t m_pad = (int64_t)num_m * BM;
+  const int64_t m_pad = (int64_t)num_m * TM;
   int rc = ensure_dev(ctx, ctx->X, ctx->x_cap, (size_t)m_pad * ldx * 2);
   if (rc) return rc;
   rc = ensure_dev(ctx, ctx->row_seg, ctx->rs_cap, (size_t)m_pad * 4);
@@ -742,6 +756,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     CK(cudaMemsetAsync(ctx->a_lora, 0, (size_t)m_pad * lora_ld * 2, stream));
     ShrinkParams sp;
     sp.K = K;
+    sp.tile_shift = tshift;
     sp.lora_ld = (int)lora_ld;
     sp.segs = d_segs;
     sp.items = reinterpret_cast<const ShrinkItem*>(dv + off_it);
@@ -780,7 +795,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   gpm.chunks = reinterpret_cast<const int32_t*>(dv + off_ch);
   gpm.ia3_in_epilogue = (pass_kind == SS_PASS_FORWARD) ? 1 : 0;
   const int tiles = gpm.num_m_tiles * gpm.num_n_tiles;
-  const int grid = std::min(tiles, ctx->num_sms);
+  const int grid = pair ? 2 * std::min(tiles, ctx->num_sms / 2) : std::min(tiles, ctx->num_sms);
   const CUtensorMap& tmBP = any_lora ? (bwd ? L.tm_at : L.tm_b) : tmA;
   // algorithmic work: base GEMM + each LoRA segment's own rank (the block-diagonal zeros of
   // neighbouring segments are not counted); bytes: X, W, bias, outputs
@@ -791,10 +806,16 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     if (d.flags & SEGF_LORA) gf += 2.0 * d.rows * d.rank_pad * N;
   }
   const int pg = prof_begin(ctx, stream, SS_KERNEL_GEMM, gf, gb);
-  if (bwd)
+  if (pair) {
+    if (bwd)
+      seg_gemm2_kernel<true><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(tmA, L.tm_w_bwd2, tmAL, tmBP, gpm);
+    else
+      seg_gemm2_kernel<false><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(tmA, L.tm_w_fwd, tmAL, tmBP, gpm);
+  } else if (bwd) {
     seg_gemm_kernel<true><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, L.tm_w_bwd, tmAL, tmBP, gpm);
-  else
+  } else {
     seg_gemm_kernel<false><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, L.tm_w_fwd, tmAL, tmBP, gpm);
+  }
   prof_end(ctx, stream, pg);
   CK(cudaGetLastError());
   ctx->launches++;

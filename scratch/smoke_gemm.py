@@ -54,6 +54,8 @@ def load(block, role, W, b):
     L.check(ctx, rc)
 
 
+import os
+L.check(ctx, lib.ss_set_option(ctx, b"gemm_2cta", int(os.environ.get("SS_2CTA", "1"))))
 # ---- exact integer KAT
 d_in, d_out = 320, 520
 W = rng.integers(-2, 3, size=(d_in, d_out)).astype(np.float32)
@@ -96,7 +98,11 @@ print("ia3 bwd exact:", np.array_equal(res[0][0], refia), np.abs(res[0][0] - ref
 print("lora bwd exact:", np.array_equal(res[1][0], refl), np.abs(res[1][0] - refl).max())
 
 # ---- large random bf16 perf probe
-for (K, N, M) in [(4096, 4096, 8192), (5120, 13824, 16384), (13824, 5120, 16384)]:
+import os
+mode = int(os.environ.get("SS_2CTA", "1"))
+L.check(ctx, lib.ss_set_option(ctx, b"gemm_2cta", mode))
+print("gemm_2cta =", mode)
+for (K, N, M) in [(4096, 4096, 8192), (5120, 13824, 32768), (13824, 5120, 32768), (5120, 5120, 32768), (5120, 32000, 32768)]:
     W = (rng.standard_normal((K, N), dtype=np.float32) / np.sqrt(K))
     load(1, 4, W, np.zeros(N, np.float32))
     xt = torch.randn(M, K, device=dev, dtype=torch.bfloat16)

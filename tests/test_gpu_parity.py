@@ -3,7 +3,7 @@ the reference's golden vectors. Run on a B200: ``python -m pytest tests -m gpu``
 
 Tolerances (stated once, oracle/splitserve_oracle.py TOL_*): against the f32
 oracle fed the same bf16-rounded inputs, normwise max|d|/max|ref| and mean|d|/mean|ref|:
-bf16 activations in/out <= 2e-2 / 3e-3; fp32 outputs <= 1e-2 / 1e-3. fp32 outputs of exactly
+bf16 activations in/out <= 2e-2 / 3e-3; fp32 outputs <= 1e-2 / 1.5e-3. fp32 outputs of exactly
 representable integer inputs: bitwise. Routing: bit-exact. Batched == solo: bitwise.
 """
 
