@@ -90,7 +90,10 @@ struct ss_ctx {
   bool any_compute = false;
   int64_t launches = 0;
   int group_m = 16;
-  int gemm_2cta = 1;  // 1: CTA-pair cta_group::2 kernel, 0: single-CTA kernel
+  // -1 auto: CTA-pair kernel for K <= 8192 (smem-bandwidth-bound shapes), single-CTA kernel
+  // for long K (the pair's larger raster footprint doubles DRAM traffic there and the
+  // power-capped clock drops; profiles/r01_gemm_variants.md). 1 / 0 force one kernel.
+  int gemm_2cta = -1;
   int64_t weight_bytes = 0, adapter_bytes = 0;
   // in-stream profiling
   bool profiling = false;
@@ -395,7 +398,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
 int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!ctx || !key) return SS_E_ARG;
   if (!strcmp(key, "gemm_2cta")) {
-    ctx->gemm_2cta = value ? 1 : 0;
+    ctx->gemm_2cta = value < 0 ? -1 : (value ? 1 : 0);
     return SS_OK;
   }
   if (!strcmp(key, "group_m")) {
@@ -643,7 +646,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   CK(cudaSetDevice(ctx->device));
 
   // ---- M-tile tables for the block-diagonal LoRA operand
-  const bool pair = ctx->gemm_2cta != 0;
+  const bool pair = ctx->gemm_2cta < 0 ? (K <= 8192 && M > BM) : ctx->gemm_2cta != 0;
   const int TM = pair ? BM2 : BM;             // M-tile height of the GEMM kernel
   const int tshift = pair ? 8 : 7;
   const int num_m = (int)((M + TM - 1) / TM);

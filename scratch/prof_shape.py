@@ -18,9 +18,8 @@ L.check(ctx, lib.ss_set_option(ctx, b"group_m", gm))
 dev = torch.device("cuda:0")
 W = torch.randn(K, N, device=dev, dtype=torch.bfloat16)
 L.check(ctx, lib.ss_load_layer(ctx, 0, 4, K, N, W.data_ptr(), N, None, L.SS_MEM_DEVICE | L.SS_DT_BF16))
-din, dout = (K, N) if pk == 0 else (N, K)
-x = torch.randn(M, din if pk == 0 else dout, device=dev, dtype=torch.bfloat16)
-out = torch.empty(M, dout if pk == 0 else din, device=dev, dtype=torch.bfloat16)
+x = torch.randn(M, K if pk == 0 else N, device=dev, dtype=torch.bfloat16)
+out = torch.empty(M, N if pk == 0 else K, device=dev, dtype=torch.bfloat16)
 arr = (L.SsSeg * 1)()
 s = arr[0]
 s.client_id, s.rows, s.width = 5, M, x.shape[1]
