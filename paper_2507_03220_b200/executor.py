@@ -336,6 +336,16 @@ class GpuBaseExecutor:
         if not good:
             return results
         stream = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+        if self._all_pinned_host(envelopes, good, out_w):
+            with torch.cuda.device(self.device):
+                status = self._pipelined_host(pass_kind, key, envelopes, good, out_w, stream)
+            for j, i in enumerate(good):
+                results[i] = (ProtocolError(f"executor rejected segment (status {status[j]}) for layer {addr}")
+                              if status[j] != _lib.SS_SEG_OK else envelopes[i].reply_to)
+            rows = sum(envelopes[i].token_count for i in good)
+            self.ledger.set(ledger_mod.TRANSIENT_BUFFER, rows * (expected + out_w) * 2)
+            self.ledger.set(ledger_mod.TRANSIENT_BUFFER, 0)
+            return results
         with torch.cuda.device(self.device), torch.cuda.stream(stream):
             for i in good:
                 ev = getattr(envelopes[i], "ready", None)
@@ -373,6 +383,104 @@ class GpuBaseExecutor:
             else:
                 results[i] = dsts[j]
         return results
+
+    # -- pipelined host path ----------------------------------------------------------------
+    pipeline_rows = 4096          # max rows per sub-batch of a host-payload dispatch
+    pipeline_bytes = 24 << 20     # target bytes of the wider side per sub-batch
+    pipeline_slots = 3            # staging ring depth (H2D / compute / D2H in flight)
+
+    def _all_pinned_host(self, envelopes, good, out_w) -> bool:
+        if self.save_activations:
+            return False
+        for i in good:
+            e = envelopes[i]
+            p, r = e.payload, getattr(e, "reply_to", None)
+            if not (isinstance(p, torch.Tensor) and not p.is_cuda and p.is_pinned() and p.is_contiguous()
+                    and isinstance(r, torch.Tensor) and not r.is_cuda and r.is_pinned() and r.is_contiguous()
+                    and p.dtype == r.dtype and p.dtype in (torch.bfloat16, torch.float32)
+                    and tuple(r.shape) == (e.token_count, out_w)
+                    and getattr(e, "base_to", None) is None):
+                return False
+        return True
+
+    def _pipelined_host(self, pass_kind, key, envelopes, good, out_w, stream) -> list[int]:
+        """Host clients (pinned payload + pinned reply buffer): the dispatch runs as row
+        sub-batches so the H2D copy of sub-batch j+1 and the D2H copy of j-1 overlap the GEMM
+        of j (two copy streams, a 3-slot device staging ring). Rows are independent and the
+        kernels never mix rows (tensor_ops.py:1-8), so results are bitwise those of one batch."""
+        if not hasattr(self, "_copy_streams"):
+            self._copy_streams = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
+        s_in, s_out = self._copy_streams
+        in_w = envelopes[good[0]].width
+        esz = envelopes[good[0]].payload.element_size()
+        # sub-batch size by bytes of the wider side, so fill / drain stay ~0.3 ms per dispatch
+        target = max(256, min(self.pipeline_rows, self.pipeline_bytes // (max(in_w, out_w) * esz)))
+        chunks, cur, rows = [], [], 0      # chunk = [(envelope index, row0, row1)]
+        for i in good:
+            t = envelopes[i].token_count
+            r = 0
+            while r < t or (t == 0 and r == 0):
+                take = min(t - r, target - rows)
+                cur.append((i, r, r + take))
+                rows += take
+                r += take
+                if rows >= target:
+                    chunks.append(cur)
+                    cur, rows = [], 0
+                if t == 0:
+                    break
+        if cur:
+            chunks.append(cur)
+        nslot = self.pipeline_slots
+        fused = self._fused
+        ev_c, ev_out = [], []
+        bad: dict[int, int] = {}
+        for j, ch in enumerate(chunks):
+            slot = j % nslot
+            dt = envelopes[ch[0][0]].payload.dtype
+            n_rows = sum(r1 - r0 for _, r0, r1 in ch)
+            with torch.cuda.stream(s_in):
+                if j >= nslot:
+                    s_in.wait_event(ev_c[j - nslot])       # slot's previous GEMM has consumed it
+                dev_in = self._dev_buf(f"pin{slot}", n_rows * in_w, dt)
+                srcs, pos = [], 0
+                for i, r0, r1 in ch:
+                    n = (r1 - r0) * in_w
+                    v = dev_in[pos:pos + n].view(r1 - r0, in_w)
+                    v.copy_(envelopes[i].payload[r0:r1], non_blocking=True)
+                    srcs.append(v)
+                    pos += n
+                e_in = torch.cuda.Event()
+                e_in.record(s_in)
+            stream.wait_event(e_in)
+            if j >= nslot:
+                stream.wait_event(ev_out[j - nslot])      # slot's previous D2H has drained it
+            dev_out = self._dev_buf(f"pout{slot}", n_rows * out_w, dt)
+            segs, pos = [], 0
+            for (i, r0, r1), src in zip(ch, srcs):
+                env = envelopes[i]
+                n = (r1 - r0) * out_w
+                dst = dev_out[pos:pos + n].view(r1 - r0, out_w)
+                pos += n
+                segs.append(Seg(client_id=env.client_id, src=src, dst=dst, width=in_w,
+                                adapter=pass_kind != PASS_NOISE_EFFECT and key in fused.get(env.client_id, ())))
+            st = self.ctx.compute(pass_kind, key[0], key[1], segs, stream)
+            for (i, _, _), s in zip(ch, st):
+                if s != _lib.SS_SEG_OK:
+                    bad[i] = s
+            e_c = torch.cuda.Event()
+            e_c.record(stream)
+            ev_c.append(e_c)
+            s_out.wait_event(e_c)
+            with torch.cuda.stream(s_out):
+                for (i, r0, r1), sg in zip(ch, segs):
+                    envelopes[i].reply_to[r0:r1].copy_(sg.dst, non_blocking=True)
+                e_o = torch.cuda.Event()
+                e_o.record(s_out)
+                ev_out.append(e_o)
+        ev_out[-1].synchronize()
+        self.last_event = ev_out[-1]
+        return [bad.get(i, _lib.SS_SEG_OK) for i in good]
 
     # -- staging helpers --------------------------------------------------------------------
     def _stage_inputs(self, envelopes, good, stream):
@@ -434,6 +542,9 @@ class GpuBaseExecutor:
         key = (name, dtype)
         buf = self._dev_staging.get(key)
         if buf is None or buf.numel() < numel:
+            if buf is not None:
+                # the old buffer may still feed copies / kernels on other streams
+                torch.cuda.synchronize(self.device)
             buf = torch.empty(max(numel, 1 << 20), dtype=dtype, device=self.device)
             self._dev_staging[key] = buf
         return buf[:numel]

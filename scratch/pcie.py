@@ -1,0 +1,14 @@
+import torch, time
+n = 512 << 20  # 1 GiB in bf16 elements
+h = torch.empty(n, dtype=torch.bfloat16).pin_memory(); h2 = torch.empty(n, dtype=torch.bfloat16).pin_memory()
+d = torch.empty(n, dtype=torch.bfloat16, device="cuda"); d2 = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+for name, fn in [("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h2.copy_(d2, non_blocking=True))]:
+    fn(); torch.cuda.synchronize(); t=time.perf_counter()
+    for _ in range(5): fn()
+    torch.cuda.synchronize(); print(name, 5*2*n/(time.perf_counter()-t)/1e9, "GB/s")
+torch.cuda.synchronize(); t=time.perf_counter()
+for _ in range(5):
+    with torch.cuda.stream(s1): d.copy_(h, non_blocking=True)
+    with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
+torch.cuda.synchronize(); print("bidir total", 2*5*2*n/(time.perf_counter()-t)/1e9, "GB/s")

@@ -412,3 +412,23 @@ def test_submit_rejections_match_reference_messages():
     assert got[0].pass_kind == 0
     assert got[1].pass_kind == PASS_ERROR and "not increasing" in error_message(got[1])
     assert got[2].pass_kind == PASS_ERROR and "unknown layer" in error_message(got[2])
+
+
+def test_pipelined_host_dispatch_bitwise_equals_device_dispatch():
+    """Pinned-host clients take the pipelined path (row sub-batches, H2D/GEMM/D2H overlapped);
+    the result must be bitwise the device-resident single-batch result."""
+    d_in, d_out = 512, 768
+    w, b = O.layer_params(6, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)})
+    ex.pipeline_rows = 200   # force several sub-batches and ring reuse
+    specs, counts = _mixed_clients(ex, d_in, d_out, seed=9, role=O.V)
+    for pass_kind, (wi, wo) in ((0, (d_in, d_out)), (1, (d_out, d_in))):
+        hosts = [torch.randn(t, wi).to(torch.bfloat16).pin_memory() for t in counts]
+        replies = [torch.empty(t, wo, dtype=torch.bfloat16).pin_memory() for t in counts]
+        res = ex._compute_batch(pass_kind, [_env(c, 40 + pass_kind, 0, O.V, pass_kind, h, reply_to=r)
+                                            for c, (h, r) in enumerate(zip(hosts, replies))])
+        assert all(r is replies[c] for c, r in enumerate(res))
+        dev = ex._compute_batch(pass_kind, [_env(c, 50 + pass_kind, 0, O.V, pass_kind, h.to(ex.device))
+                                            for c, h in enumerate(hosts)])
+        for c in range(len(counts)):
+            assert torch.equal(replies[c], dev[c].cpu()), (pass_kind, c)
