@@ -32,10 +32,10 @@ enum : int32_t {
 };
 
 struct DevSeg {
-  int32_t row0;        // first row in the batch (prefix offset, split_rows order)
+  int32_t xrow0;       // first row of this segment's packed piece in X (-1: none)
   int32_t rows;
   int32_t flags;
-  int32_t lora_col0;   // column of this segment's rank block inside its first M-tile
+  int32_t xlocal0;     // segment-local row index of that first packed row
   const void* src;
   int64_t src_ld;      // elements
   void* dst;
@@ -62,18 +62,31 @@ constexpr int LORA_CHUNK_BYTES = 64 * LORA_CHUNK * 2;  // one {64, 16} box = 2 K
 constexpr int GEMM_THREADS = 256;                // 8 warps
 constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
+// One M-tile of the dispatch (TM = 128 rows single-CTA, 256 rows CTA pair). A "direct" tile is
+// TM rows of one segment, TMA-loaded straight from the client's buffer through that segment's
+// tensor map; a "packed" tile covers rows of X (small / f32 / IA3-backward pieces gathered by K4).
+struct TileDesc {
+  int32_t amap;         // index into GemmParams::tmaps (0 = packed operand X)
+  int32_t arow;         // row coordinate of the tile's first row in that tensor map
+  int32_t seg;          // direct tile: its segment; packed tile: -1
+  int32_t rows;         // valid rows (<= TM)
+  int32_t chunk_begin;  // LoRA: first entry in `chunks`
+  int32_t chunk_count;  // LoRA: 16-wide rank chunks (block-diagonal over the tile's segments)
+  int32_t pad0, pad1;
+};
+
 struct GemmParams {
-  int M, N, K;
+  int N, K;
   int num_m_tiles, num_n_tiles, group_m;
   int has_bias;
   int any_lora;
+  int ia3_in_epilogue;              // forward: scale output columns by IA3
   const float* bias;
   const DevSeg* segs;
-  const int32_t* row_seg;
-  const int32_t* tile_chunk_begin;  // per M-tile: first entry in `chunks`
-  const int32_t* tile_chunk_count;  // per M-tile: number of 16-wide rank chunks
+  const int32_t* row_seg;           // per packed X row: its segment
+  const TileDesc* tiles;            // per M-tile
   const int32_t* chunks;            // pack row of each rank chunk
-  int ia3_in_epilogue;              // forward: scale output columns by IA3
+  const CUtensorMap* tmaps;         // [0] = X, [1 + i] = direct source i (device memory)
 };
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb,
@@ -91,13 +104,23 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int gro
 // optional pre-IA3 y_base store, * IA3 l, store into the row's segment destination.
 // Every thread of the warp must call it (tcgen05.ld is warp-collective).
 __device__ __forceinline__ void epilogue_rows(const GemmParams& p, uint32_t tmem_acc, uint32_t ew,
-                                              int row, int n0, uint64_t* tfull, uint32_t tfull_ph) {
-  const bool row_ok = row < p.M;
+                                              const TileDesc& td, int r, int n0, uint64_t* tfull,
+                                              uint32_t tfull_ph) {
+  const bool row_ok = r < td.rows;
   DevSeg sg;
-  if (row_ok) sg = p.segs[p.row_seg[row]];
+  int r_local = 0;
+  if (row_ok) {
+    if (td.seg >= 0) {
+      sg = p.segs[td.seg];
+      r_local = td.arow + r;
+    } else {
+      const int xrow = td.arow + r;
+      sg = p.segs[p.row_seg[xrow]];
+      r_local = xrow - sg.xrow0 + sg.xlocal0;
+    }
+  }
   mbar_wait(tfull, tfull_ph);
   tc_fence_after();
-  const int r_local = row_ok ? row - sg.row0 : 0;
   const bool use_ia3 = row_ok && p.ia3_in_epilogue && (sg.flags & SEGF_IA3);
   const bool want_base = row_ok && (sg.flags & SEGF_WANT_BASE);
 #pragma unroll 1
@@ -184,8 +207,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmParams& p, uint32_t tmem
 // ============================================================================ K1/K2/K5
 template <bool kBwd>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    seg_gemm_kernel(const __grid_constant__ CUtensorMap tmA,   // X  [M, K] bf16
-                    const __grid_constant__ CUtensorMap tmB,   // W  [d_in, d_out] bf16
+    seg_gemm_kernel(const __grid_constant__ CUtensorMap tmB,   // W  [d_in, d_out] bf16
                     const __grid_constant__ CUtensorMap tmAL,  // A_lora [M, R_w] bf16
                     const __grid_constant__ CUtensorMap tmBP,  // pack [R, N] bf16 (MN-major B)
                     const GemmParams p) {
@@ -204,7 +226,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     if (p.any_lora) {
       tma_prefetch_desc(&tmAL);
@@ -239,11 +260,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int mb, nb;
         tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+        const TileDesc td = p.tiles[mb];
+        const CUtensorMap* tmA = p.tmaps + td.amap;
         const int m0 = mb * BM, n0 = nb * BN;
+        tensormap_acquire(tmA);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-          tma_load_2d(smA + s * A_STAGE_BYTES, &tmA, &full_bar[s], kb * BK, m0);
+          tma_load_2d(smA + s * A_STAGE_BYTES, tmA, &full_bar[s], kb * BK, td.arow);
           uint8_t* b = smB + s * B_STAGE_BYTES;
           if (kBwd) {
             // W viewed K-major: rows = d_in (the GEMM's N), cols = d_out (the GEMM's K).
@@ -257,8 +281,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
         if (p.any_lora) {
-          const int cb = p.tile_chunk_begin[mb];
-          const int cc = p.tile_chunk_count[mb];
+          const int cb = td.chunk_begin;
+          const int cc = td.chunk_count;
           for (int ls = 0; ls * 4 < cc; ++ls) {
             const int nq = min(4, cc - ls * 4);
             mbar_wait(&empty_bar[s], ph ^ 1);
@@ -310,7 +334,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
       if (p.any_lora) {
-        const int cc = p.tile_chunk_count[mb];
+        const int cc = p.tiles[mb].chunk_count;
         for (int ls = 0; ls * 4 < cc; ++ls) {
           const int nq = min(4, cc - ls * 4);
           mbar_wait(&full_bar[s], ph);
@@ -341,8 +365,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
-      epilogue_rows(p, tmem_base + acc * BN, ew, mb * BM + ew * 32 + lane, nb * BN, &tfull_bar[acc],
-                    acc_ph);
+      const TileDesc td = p.tiles[mb];
+      epilogue_rows(p, tmem_base + acc * BN, ew, td, ew * 32 + lane, nb * BN, &tfull_bar[acc], acc_ph);
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
@@ -371,8 +395,7 @@ constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 256;
 
 template <bool kBwd>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
-    seg_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,   // X  [M, K] bf16, box {64,128}
-                     const __grid_constant__ CUtensorMap tmB,   // W: fwd box {64,64}; bwd {64,128}
+    seg_gemm2_kernel(const __grid_constant__ CUtensorMap tmB,   // W: fwd box {64,64}; bwd {64,128}
                      const __grid_constant__ CUtensorMap tmAL,  // A_lora [M, R_w], box {64,128}
                      const __grid_constant__ CUtensorMap tmBP,  // pack [R, N], box {64,16}
                      const GemmParams p) {
@@ -393,7 +416,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   const bool leader = crank == 0;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     if (p.any_lora) {
       tma_prefetch_desc(&tmAL);
@@ -431,13 +453,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       for (int t = cluster_id; t < num_tiles; t += num_clusters) {
         int mb, nb;
         tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
-        const int m0 = mb * BM2 + crank * BM;
+        const TileDesc td = p.tiles[mb];
+        const CUtensorMap* tmA = p.tmaps + td.amap;
+        const int arow = td.arow + crank * BM;
+        tensormap_acquire(tmA);
+        const int m0 = mb * BM2 + crank * BM;        // row of this CTA's half in A_lora
         const int nh = nb * BN + crank * (BN / 2);  // this CTA's half of the N columns
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           const uint32_t fb = full0 + s * 8;
           if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE2_BYTES);
-          tma_load_2d_2sm(smA + s * A_STAGE_BYTES, &tmA, fb, kb * BK, m0);
+          tma_load_2d_2sm(smA + s * A_STAGE_BYTES, tmA, fb, kb * BK, arow);
           uint8_t* b = smB + s * B_HALF_BYTES;
           if (kBwd) {
             tma_load_2d_2sm(b, &tmB, fb, kb * BK, nh);
@@ -449,8 +475,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           if (++s == STAGES2) { s = 0; ph ^= 1; }
         }
         if (p.any_lora) {
-          const int cb = p.tile_chunk_begin[mb];
-          const int cc = p.tile_chunk_count[mb];
+          const int cb = td.chunk_begin;
+          const int cc = td.chunk_count;
           for (int ls = 0; ls * 4 < cc; ++ls) {
             const int nq = min(4, cc - ls * 4);
             mbar_wait(&empty_bar[s], ph ^ 1);
@@ -504,7 +530,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           if (++s == STAGES2) { s = 0; ph ^= 1; }
         }
         if (p.any_lora) {
-          const int cc = p.tile_chunk_count[mb];
+          const int cc = p.tiles[mb].chunk_count;
           for (int ls = 0; ls * 4 < cc; ++ls) {
             const int nq = min(4, cc - ls * 4);
             mbar_wait(&full_bar[s], ph);
@@ -536,7 +562,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     for (int t = cluster_id; t < num_tiles; t += num_clusters) {
       int mb, nb;
       tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
-      epilogue_rows(p, tmem_base + acc * BN, ew, mb * BM2 + crank * BM + ew * 32 + lane, nb * BN,
+      const TileDesc td = p.tiles[mb];
+      epilogue_rows(p, tmem_base + acc * BN, ew, td, crank * BM + ew * 32 + lane, nb * BN,
                     &tfull_bar[acc], acc_ph);
       tc_fence_before();
       __syncwarp();
@@ -554,9 +581,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ============================================================================ K3 shrink
-// One CTA per (segment, 128-row slab). T[rows, rank_pad] = X[rows, K] . P[rank rows, K]^T,
-// scaled by alpha/r, rounded to bf16 and written into A_lora at this segment's rank-block
-// column of each row's M-tile (zeros elsewhere come from a memset).
+// One CTA per item = (M-tile, LoRA segment piece of that tile, <= 128 rows):
+//   T[rows, rank_pad] = A_src[rows, K] . P[rank rows, K]^T (tcgen05, M=128, N=rank_pad),
+// scaled by alpha/r, rounded to bf16 and written into A_lora rows tile*TM + p0 .. at the piece's
+// column block col0 (zeros elsewhere come from a memset) — the block-diagonal LoRA operand.
 constexpr int SHRINK_STAGES = 4;
 constexpr int SHRINK_MAXN = 256;
 constexpr int SHRINK_B_STAGE = SHRINK_MAXN * BK * 2;  // 32 KB
@@ -564,23 +592,25 @@ constexpr int SHRINK_SMEM = SHRINK_STAGES * (A_STAGE_BYTES + SHRINK_B_STAGE) + 1
 
 struct ShrinkItem {
   int32_t seg;
-  int32_t row0;  // batch row of this slab
-  int32_t rows;  // <= 128
-  int32_t pad_;
+  int32_t amap;   // A source tensor map (0 = X, 1 + i = direct source i)
+  int32_t arow;   // row coordinate of the item's first row in that map
+  int32_t rows;   // <= 128
+  int32_t orow;   // first output row in A_lora (tile * TM + row offset within tile)
+  int32_t col0;   // column of this segment's rank block in its tile
+  int32_t pad0, pad1;
 };
 
 struct ShrinkParams {
   int K;
-  int tile_shift;  // log2 of the GEMM's M-tile height (7: 1-CTA kernel, 8: CTA pair)
   int lora_ld;  // A_lora row stride (elements)
   const DevSeg* segs;
   const ShrinkItem* items;
+  const CUtensorMap* tmaps;
   __nv_bfloat16* a_lora;
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    lora_shrink_kernel(const __grid_constant__ CUtensorMap tmA,  // X [M, K]
-                       const __grid_constant__ CUtensorMap tmP,  // pack [R, K] (K-major rows)
+    lora_shrink_kernel(const __grid_constant__ CUtensorMap tmP,  // pack [R, K] (K-major rows)
                        const ShrinkParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -597,9 +627,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const ShrinkItem it = p.items[blockIdx.x];
   const DevSeg sg = p.segs[it.seg];
   const int npad = sg.rank_pad;  // multiple of 16, <= 256
+  const CUtensorMap* tmA = p.tmaps + it.amap;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
+    tensormap_acquire(tmA);
+    tma_prefetch_desc(tmA);
     tma_prefetch_desc(&tmP);
   }
   if (warp == 1 && lane == 0) {
@@ -625,7 +657,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty_bar[s], ph ^ 1);
         mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nchunk * LORA_CHUNK_BYTES);
-        tma_load_2d(smA + s * A_STAGE_BYTES, &tmA, &full_bar[s], kb * BK, it.row0);
+        tma_load_2d(smA + s * A_STAGE_BYTES, tmA, &full_bar[s], kb * BK, it.arow);
         for (int q = 0; q < nchunk; ++q)
           tma_load_2d(smB + s * SHRINK_B_STAGE + q * LORA_CHUNK_BYTES, &tmP, &full_bar[s], kb * BK,
                       sg.pack_row + q * LORA_CHUNK);
@@ -633,8 +665,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = make_idesc_bf16(BM, 16, false, false) & ~(0x3Fu << 17);
-    const uint32_t idesc_n = idesc | ((uint32_t)(npad >> 3) << 17);
+    const uint32_t idesc = make_idesc_bf16(BM, (uint32_t)npad, false, false);
     int s = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
@@ -646,7 +677,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < BK / UK; ++k)
           mma_bf16_ss(tmem_base, make_sdesc_sw128(a_addr + k * 32, 16, 1024),
-                      make_sdesc_sw128(b_addr + k * 32, 16, 1024), idesc_n, (kb | k) != 0);
+                      make_sdesc_sw128(b_addr + k * 32, 16, 1024), idesc, (kb | k) != 0);
         mma_commit(&empty_bar[s]);
       }
       __syncwarp();
@@ -656,13 +687,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncwarp();
   } else if (warp >= 4) {
     const uint32_t ew = warp - 4;
-    const int lr = ew * 32 + lane;  // row within slab
+    const int lr = ew * 32 + lane;  // row within the item
     mbar_wait(tfull, 0);
     tc_fence_after();
-    const int row = it.row0 + lr;
     const bool ok = lr < it.rows;
-    const int col0 = ((row >> p.tile_shift) == (sg.row0 >> p.tile_shift)) ? sg.lora_col0 : 0;
-    __nv_bfloat16* out = p.a_lora + (int64_t)row * p.lora_ld + col0;
+    __nv_bfloat16* out = p.a_lora + (int64_t)(it.orow + lr) * p.lora_ld + it.col0;
     for (int c = 0; c < nchunk; ++c) {
       uint32_t r[16];
       tmem_ld_32x32b_x16(tmem_base + c * 16 + ((ew * 32u) << 16), r);
@@ -688,34 +717,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ============================================================================ K4 gather
+// Packs the rows that cannot be TMA-loaded in place (tails of segments shorter than a tile,
+// f32 sources, IA3 backward rows that need g = dy * l) into X, in segment order
+// (concat_rows order restricted to packed pieces), and records each X row's segment.
 struct GatherParams {
-  int M, K;
+  int MX, K;              // packed rows, width
   int ldx;
-  int n_seg;
-  int ia3_in_prologue;  // backward: g = dy * l
+  int n_piece;
+  int ia3_in_prologue;    // backward: g = dy * l
   const DevSeg* segs;
+  const int32_t* piece_seg;  // segment of each packed piece, in X order
   __nv_bfloat16* X;
   int32_t* row_seg;
 };
 
-__device__ __forceinline__ int find_seg(const DevSeg* segs, int n, int row) {
-  int lo = 0, hi = n - 1;
+__device__ __forceinline__ int find_piece(const GatherParams& p, int xrow) {
+  int lo = 0, hi = p.n_piece - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].row0 <= row) lo = mid; else hi = mid - 1;
+    if (p.segs[p.piece_seg[mid]].xrow0 <= xrow) lo = mid; else hi = mid - 1;
   }
-  return lo;
+  return p.piece_seg[lo];
 }
 
 // One warp per row, grid-stride.
 __global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) {
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
-  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < p.M; row += gridDim.x * wpb) {
-    const int si = find_seg(p.segs, p.n_seg, row);
+  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < p.MX; row += gridDim.x * wpb) {
+    const int si = find_piece(p, row);
     const DevSeg& sg = p.segs[si];
     if (lane == 0) p.row_seg[row] = si;
-    const int64_t lr = row - sg.row0;
+    const int64_t lr = row - sg.xrow0 + sg.xlocal0;
     __nv_bfloat16* xr = p.X + (int64_t)row * p.ldx;
     const bool scale = p.ia3_in_prologue && (sg.flags & SEGF_IA3);
     const float* l = sg.ia3;

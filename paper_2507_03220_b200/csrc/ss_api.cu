@@ -94,6 +94,7 @@ struct ss_ctx {
   // for long K (the pair's larger raster footprint doubles DRAM traffic there and the
   // power-capped clock drops; profiles/r01_gemm_variants.md). 1 / 0 force one kernel.
   int gemm_2cta = -1;
+  int direct_tiles = 1;  // 1: TMA-load whole tiles of bf16 segments in place (no gather)
   int64_t weight_bytes = 0, adapter_bytes = 0;
   // in-stream profiling
   bool profiling = false;
@@ -397,6 +398,10 @@ int ss_ctx_destroy(ss_ctx* ctx) {
 
 int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!ctx || !key) return SS_E_ARG;
+  if (!strcmp(key, "direct_tiles")) {
+    ctx->direct_tiles = value ? 1 : 0;
+    return SS_OK;
+  }
   if (!strcmp(key, "gemm_2cta")) {
     ctx->gemm_2cta = value < 0 ? -1 : (value ? 1 : 0);
     return SS_OK;
@@ -591,6 +596,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
 
   // ---- validate + build device segment records (batch order == envelope order)
   std::vector<DevSeg> ds;
+  std::vector<const ss_seg*> src_of;
   ds.reserve(n_seg);
   int64_t M = 0;
   bool any_lora = false;
@@ -601,7 +607,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     if (s.rows == 0) continue;
     if (!s.src || !s.dst || s.src_ld < K || s.dst_ld < N) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
     DevSeg d{};
-    d.row0 = (int32_t)M;
+    d.xrow0 = -1;
     d.rows = (int32_t)s.rows;
     d.src = s.src;
     d.src_ld = s.src_ld;
@@ -639,40 +645,76 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     }
     d.flags = f;
     ds.push_back(d);
+    src_of.push_back(&s);
     M += s.rows;
   }
   if (M == 0) return SS_OK;
   if (M > (int64_t)1 << 30) return fail(ctx, SS_E_ARG, "batch too large (%lld rows)", (long long)M);
   CK(cudaSetDevice(ctx->device));
 
-  // ---- M-tile tables for the block-diagonal LoRA operand
+  // ---- M-tiles: segment-aligned direct tiles for whole tiles of bf16 rows, the rest packed
   const bool pair = ctx->gemm_2cta < 0 ? (K <= 8192 && M > BM) : ctx->gemm_2cta != 0;
-  const int TM = pair ? BM2 : BM;             // M-tile height of the GEMM kernel
-  const int tshift = pair ? 8 : 7;
-  const int num_m = (int)((M + TM - 1) / TM);
-  std::vector<int32_t> t_begin(num_m, 0), t_count(num_m, 0), chunks;
+  const int TM = pair ? BM2 : BM;
+  std::vector<TileDesc> tiles;
+  std::vector<int32_t> piece_seg;          // packed pieces in X order
+  std::vector<int32_t> direct_src;         // segment of each direct tensor map (map = 1 + i)
+  int64_t MX = 0;
+  for (size_t j = 0; j < ds.size(); ++j) {
+    DevSeg& d = ds[j];
+    const bool direct_ok = ctx->direct_tiles && (d.flags & SEGF_SRC_BF16) && (d.flags & SEGF_SRC_VEC) &&
+                           !(bwd && (d.flags & SEGF_IA3)) && (d.src_ld * 2) % 16 == 0;
+    const int nd = direct_ok ? (d.rows / TM) * TM : 0;
+    if (nd > 0) {
+      const int amap = 1 + (int)direct_src.size();
+      direct_src.push_back((int32_t)j);
+      for (int r = 0; r < nd; r += TM)
+        tiles.push_back(TileDesc{amap, r, (int32_t)j, TM, 0, 0, 0, 0});
+    }
+    if (d.rows > nd) {
+      d.xrow0 = (int32_t)MX;
+      d.xlocal0 = nd;
+      piece_seg.push_back((int32_t)j);
+      MX += d.rows - nd;
+    }
+  }
+  for (int64_t x = 0; x < MX; x += TM)
+    tiles.push_back(TileDesc{0, (int32_t)x, -1, (int32_t)std::min<int64_t>(TM, MX - x), 0, 0, 0, 0});
+  const int num_m = (int)tiles.size();
+
+  // ---- LoRA: per tile rank-chunk lists (block-diagonal over the tile's segments) + shrink items
+  std::vector<int32_t> chunks;
   std::vector<ShrinkItem> items;
   int max_cols = 0;
   if (any_lora) {
-    size_t si = 0;
+    size_t pi = 0;  // packed-piece cursor
     for (int mt = 0; mt < num_m; ++mt) {
-      const int64_t r0 = (int64_t)mt * TM, r1 = std::min<int64_t>(M, r0 + TM);
-      while (si < ds.size() && ds[si].row0 + ds[si].rows <= r0) ++si;
-      t_begin[mt] = (int32_t)chunks.size();
-      for (size_t j = si; j < ds.size() && ds[j].row0 < r1; ++j) {
-        DevSeg& d = ds[j];
-        if (!(d.flags & SEGF_LORA)) continue;
-        const int col = (int)(chunks.size() - t_begin[mt]) * LORA_CHUNK;
-        if ((d.row0 >> tshift) == mt) d.lora_col0 = col;
+      TileDesc& td = tiles[mt];
+      td.chunk_begin = (int32_t)chunks.size();
+      auto add_piece = [&](int sj, int amap, int arow, int p0, int nrows) {
+        const DevSeg& d = ds[sj];
+        if (!(d.flags & SEGF_LORA)) return;
+        const int col = (int)(chunks.size() - td.chunk_begin) * LORA_CHUNK;
         for (int q = 0; q < d.rank_pad / LORA_CHUNK; ++q) chunks.push_back(d.pack_row + q * LORA_CHUNK);
+        for (int r = 0; r < nrows; r += BM)
+          items.push_back(ShrinkItem{sj, amap, arow + r, std::min(BM, nrows - r), mt * TM + p0 + r, col, 0, 0});
+      };
+      if (td.seg >= 0) {
+        add_piece(td.seg, td.amap, td.arow, 0, td.rows);
+      } else {
+        const int64_t x0 = td.arow, x1 = x0 + td.rows;
+        while (pi < piece_seg.size() &&
+               ds[piece_seg[pi]].xrow0 + (ds[piece_seg[pi]].rows - ds[piece_seg[pi]].xlocal0) <= x0)
+          ++pi;
+        for (size_t k = pi; k < piece_seg.size(); ++k) {
+          const DevSeg& d = ds[piece_seg[k]];
+          const int64_t p0 = std::max<int64_t>(x0, d.xrow0);
+          const int64_t p1 = std::min<int64_t>(x1, d.xrow0 + (d.rows - d.xlocal0));
+          if (p0 >= x1) break;
+          if (p1 > p0) add_piece(piece_seg[k], 0, (int)p0, (int)(p0 - x0), (int)(p1 - p0));
+        }
       }
-      t_count[mt] = (int32_t)chunks.size() - t_begin[mt];
-      max_cols = std::max(max_cols, t_count[mt] * LORA_CHUNK);
-    }
-    for (size_t j = 0; j < ds.size(); ++j) {
-      if (!(ds[j].flags & SEGF_LORA)) continue;
-      for (int r = 0; r < ds[j].rows; r += BM)
-        items.push_back(ShrinkItem{(int32_t)j, ds[j].row0 + r, std::min(BM, ds[j].rows - r), 0});
+      td.chunk_count = (int32_t)chunks.size() - td.chunk_begin;
+      max_cols = std::max(max_cols, td.chunk_count * LORA_CHUNK);
     }
     if (chunks.empty()) chunks.push_back(0);
   }
@@ -680,23 +722,35 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
 
   // ---- workspace
   const int64_t ldx = round_up(K, 64);
-  const int64_t m_pad = (int64_t)num_m * TM;
-  int rc = ensure_dev(ctx, ctx->X, ctx->x_cap, (size_t)m_pad * ldx * 2);
+  const int64_t mx_pad = round_up(std::max<int64_t>(MX, 1), TM);
+  int rc = ensure_dev(ctx, ctx->X, ctx->x_cap, (size_t)mx_pad * ldx * 2);
   if (rc) return rc;
-  rc = ensure_dev(ctx, ctx->row_seg, ctx->rs_cap, (size_t)m_pad * 4);
+  rc = ensure_dev(ctx, ctx->row_seg, ctx->rs_cap, (size_t)mx_pad * 4);
   if (rc) return rc;
+  const int64_t al_rows = (int64_t)num_m * TM;
   if (any_lora) {
-    rc = ensure_dev(ctx, ctx->a_lora, ctx->al_cap, (size_t)m_pad * lora_ld * 2);
+    rc = ensure_dev(ctx, ctx->a_lora, ctx->al_cap, (size_t)al_rows * lora_ld * 2);
     if (rc) return rc;
   }
   ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap);
 
+  // ---- tensor maps: [0] = X, [1 + i] = direct source i (box {64, 128} rows)
+  std::vector<CUtensorMap> tmaps(1 + direct_src.size());
+  rc = encode_2d(ctx, &tmaps[0], ctx->X, K, std::max<int64_t>(MX, 1), ldx, 64, BM);
+  if (rc) return rc;
+  for (size_t i = 0; i < direct_src.size(); ++i) {
+    const DevSeg& d = ds[direct_src[i]];
+    rc = encode_2d(ctx, &tmaps[1 + i], d.src, K, d.rows, d.src_ld, 64, BM);
+    if (rc) return rc;
+  }
+
   // ---- routing tables -> pinned staging slot -> device (one async copy)
-  const size_t off_seg = 0;
-  const size_t off_tb = round_up(ds.size() * sizeof(DevSeg), 256);
-  const size_t off_tc = off_tb + round_up(t_begin.size() * 4, 256);
-  const size_t off_ch = off_tc + round_up(t_count.size() * 4, 256);
-  const size_t off_it = off_ch + round_up(chunks.size() * 4, 256);
+  const size_t off_tm = 0;
+  const size_t off_seg = round_up(tmaps.size() * sizeof(CUtensorMap), 256);
+  const size_t off_tile = off_seg + round_up(ds.size() * sizeof(DevSeg), 256);
+  const size_t off_piece = off_tile + round_up(tiles.size() * sizeof(TileDesc), 256);
+  const size_t off_ch = off_piece + round_up(std::max<size_t>(1, piece_seg.size()) * 4, 256);
+  const size_t off_it = off_ch + round_up(std::max<size_t>(1, chunks.size()) * 4, 256);
   const size_t total = off_it + round_up(std::max<size_t>(1, items.size()) * sizeof(ShrinkItem), 256);
   Staging& st = ctx->staging[ctx->slot];
   ctx->slot = (ctx->slot + 1) % kStagingSlots;
@@ -713,76 +767,78 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     st.cap = cap;
   }
   char* h = static_cast<char*>(st.host);
+  memcpy(h + off_tm, tmaps.data(), tmaps.size() * sizeof(CUtensorMap));
   memcpy(h + off_seg, ds.data(), ds.size() * sizeof(DevSeg));
+  memcpy(h + off_tile, tiles.data(), tiles.size() * sizeof(TileDesc));
+  if (!piece_seg.empty()) memcpy(h + off_piece, piece_seg.data(), piece_seg.size() * 4);
   if (any_lora) {
-    memcpy(h + off_tb, t_begin.data(), t_begin.size() * 4);
-    memcpy(h + off_tc, t_count.data(), t_count.size() * 4);
     memcpy(h + off_ch, chunks.data(), chunks.size() * 4);
     memcpy(h + off_it, items.data(), items.size() * sizeof(ShrinkItem));
   }
   // adapters uploaded on the side stream must be complete before this dispatch reads them
   CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
-  CK(cudaMemcpyAsync(st.dev, st.host, any_lora ? total : off_tb, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(st.dev, st.host, any_lora ? total : off_ch, cudaMemcpyHostToDevice, stream));
   CK(cudaEventRecord(st.done, stream));
   st.pending = true;
   char* dv = static_cast<char*>(st.dev);
+  const CUtensorMap* d_tmaps = reinterpret_cast<const CUtensorMap*>(dv + off_tm);
   const DevSeg* d_segs = reinterpret_cast<const DevSeg*>(dv + off_seg);
 
-  // ---- K4 gather
-  GatherParams gp;
-  gp.M = (int)M;
-  gp.K = K;
-  gp.ldx = (int)ldx;
-  gp.n_seg = (int)ds.size();
-  gp.ia3_in_prologue = bwd ? 1 : 0;
-  gp.segs = d_segs;
-  gp.X = ctx->X;
-  gp.row_seg = ctx->row_seg;
-  {
-    const int grid = (int)std::min<int64_t>((M + 7) / 8, (int64_t)ctx->num_sms * 8);
+  // ---- K4 gather of the packed rows
+  if (MX > 0) {
+    GatherParams gp;
+    gp.MX = (int)MX;
+    gp.K = K;
+    gp.ldx = (int)ldx;
+    gp.n_piece = (int)piece_seg.size();
+    gp.ia3_in_prologue = bwd ? 1 : 0;
+    gp.segs = d_segs;
+    gp.piece_seg = reinterpret_cast<const int32_t*>(dv + off_piece);
+    gp.X = ctx->X;
+    gp.row_seg = ctx->row_seg;
+    const int grid = (int)std::min<int64_t>((MX + 7) / 8, (int64_t)ctx->num_sms * 8);
     double src_bytes = 0;
-    for (const DevSeg& d : ds) src_bytes += (double)d.rows * K * ((d.flags & SEGF_SRC_BF16) ? 2 : 4);
-    const int pi = prof_begin(ctx, stream, SS_KERNEL_GATHER, 0.0, src_bytes + (double)M * K * 2 + M * 4.0);
+    for (size_t k = 0; k < piece_seg.size(); ++k) {
+      const DevSeg& d = ds[piece_seg[k]];
+      src_bytes += (double)(d.rows - d.xlocal0) * K * ((d.flags & SEGF_SRC_BF16) ? 2 : 4);
+    }
+    const int pi = prof_begin(ctx, stream, SS_KERNEL_GATHER, 0.0, src_bytes + (double)MX * K * 2 + MX * 4.0);
     gather_rows_kernel<<<grid, 256, 0, stream>>>(gp);
     prof_end(ctx, stream, pi);
     CK(cudaGetLastError());
     ctx->launches++;
   }
 
-  CUtensorMap tmA, tmAL;
-  rc = encode_2d(ctx, &tmA, ctx->X, K, M, ldx, 64, BM);
-  if (rc) return rc;
+  CUtensorMap tmAL;
   if (any_lora) {
-    rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, M, lora_ld, 64, BM);
+    rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, BM);
     if (rc) return rc;
     // ---- K3 shrink into the zeroed block-diagonal operand
-    CK(cudaMemsetAsync(ctx->a_lora, 0, (size_t)m_pad * lora_ld * 2, stream));
+    CK(cudaMemsetAsync(ctx->a_lora, 0, (size_t)al_rows * lora_ld * 2, stream));
     ShrinkParams sp;
     sp.K = K;
-    sp.tile_shift = tshift;
     sp.lora_ld = (int)lora_ld;
     sp.segs = d_segs;
     sp.items = reinterpret_cast<const ShrinkItem*>(dv + off_it);
+    sp.tmaps = d_tmaps;
     sp.a_lora = ctx->a_lora;
     double sf = 0, sb = 0;
-    for (const DevSeg& d : ds)
-      if (d.flags & SEGF_LORA) {
-        sf += 2.0 * d.rows * d.rank_pad * K;
-        sb += (double)d.rows * K * 2 + (double)d.rank_pad * K * 2 + (double)d.rows * d.rank_pad * 2;
-      }
+    for (const ShrinkItem& it : items) {
+      const DevSeg& d = ds[it.seg];
+      sf += 2.0 * it.rows * d.rank_pad * K;
+      sb += (double)it.rows * K * 2 + (double)d.rank_pad * K * 2 + (double)it.rows * d.rank_pad * 2;
+    }
     const int pi = prof_begin(ctx, stream, SS_KERNEL_SHRINK, sf, sb);
-    lora_shrink_kernel<<<(int)items.size(), GEMM_THREADS, SHRINK_SMEM, stream>>>(
-        tmA, bwd ? L.tm_b : L.tm_at, sp);
+    lora_shrink_kernel<<<(int)items.size(), GEMM_THREADS, SHRINK_SMEM, stream>>>(bwd ? L.tm_b : L.tm_at, sp);
     prof_end(ctx, stream, pi);
     CK(cudaGetLastError());
     ctx->launches++;
   } else {
-    tmAL = tmA;  // unused
+    tmAL = L.tm_w_fwd;  // unused
   }
 
   // ---- K1 / K2 / K5 fused GEMM
   GemmParams gpm;
-  gpm.M = (int)M;
   gpm.N = N;
   gpm.K = K;
   gpm.num_m_tiles = num_m;
@@ -790,18 +846,18 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   gpm.group_m = ctx->group_m;
   gpm.has_bias = (pass_kind == SS_PASS_FORWARD && L.bias) ? 1 : 0;
   gpm.any_lora = any_lora ? 1 : 0;
+  gpm.ia3_in_epilogue = (pass_kind == SS_PASS_FORWARD) ? 1 : 0;
   gpm.bias = L.bias;
   gpm.segs = d_segs;
   gpm.row_seg = ctx->row_seg;
-  gpm.tile_chunk_begin = reinterpret_cast<const int32_t*>(dv + off_tb);
-  gpm.tile_chunk_count = reinterpret_cast<const int32_t*>(dv + off_tc);
+  gpm.tiles = reinterpret_cast<const TileDesc*>(dv + off_tile);
   gpm.chunks = reinterpret_cast<const int32_t*>(dv + off_ch);
-  gpm.ia3_in_epilogue = (pass_kind == SS_PASS_FORWARD) ? 1 : 0;
-  const int tiles = gpm.num_m_tiles * gpm.num_n_tiles;
-  const int grid = pair ? 2 * std::min(tiles, ctx->num_sms / 2) : std::min(tiles, ctx->num_sms);
-  const CUtensorMap& tmBP = any_lora ? (bwd ? L.tm_at : L.tm_b) : tmA;
+  gpm.tmaps = d_tmaps;
+  const int ntiles = gpm.num_m_tiles * gpm.num_n_tiles;
+  const int grid = pair ? 2 * std::min(ntiles, ctx->num_sms / 2) : std::min(ntiles, ctx->num_sms);
+  const CUtensorMap& tmBP = any_lora ? (bwd ? L.tm_at : L.tm_b) : L.tm_w_fwd;
   // algorithmic work: base GEMM + each LoRA segment's own rank (the block-diagonal zeros of
-  // neighbouring segments are not counted); bytes: X, W, bias, outputs
+  // neighbouring segments are not counted); bytes: A rows, W, outputs
   double gf = 2.0 * (double)M * N * K, gb = (double)M * K * 2 + (double)K * N * 2;
   for (const DevSeg& d : ds) {
     gb += (double)d.rows * N * ((d.flags & SEGF_DST_BF16) ? 2 : 4);
@@ -811,13 +867,13 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   const int pg = prof_begin(ctx, stream, SS_KERNEL_GEMM, gf, gb);
   if (pair) {
     if (bwd)
-      seg_gemm2_kernel<true><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(tmA, L.tm_w_bwd2, tmAL, tmBP, gpm);
+      seg_gemm2_kernel<true><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
     else
-      seg_gemm2_kernel<false><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(tmA, L.tm_w_fwd, tmAL, tmBP, gpm);
+      seg_gemm2_kernel<false><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
   } else if (bwd) {
-    seg_gemm_kernel<true><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, L.tm_w_bwd, tmAL, tmBP, gpm);
+    seg_gemm_kernel<true><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(L.tm_w_bwd, tmAL, tmBP, gpm);
   } else {
-    seg_gemm_kernel<false><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, L.tm_w_fwd, tmAL, tmBP, gpm);
+    seg_gemm_kernel<false><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
   }
   prof_end(ctx, stream, pg);
   CK(cudaGetLastError());

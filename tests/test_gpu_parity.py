@@ -432,3 +432,26 @@ def test_pipelined_host_dispatch_bitwise_equals_device_dispatch():
                                             for c, h in enumerate(hosts)])
         for c in range(len(counts)):
             assert torch.equal(replies[c], dev[c].cpu()), (pass_kind, c)
+
+
+@pytest.mark.parametrize("shape", [(384, 640), (13824, 512)])   # pair kernel / single-CTA kernel
+def test_direct_tiles_bitwise_equal_packed_path(shape):
+    """Segment-aligned tiles TMA-loaded in place from the client buffers must give exactly the
+    rows the gather -> packed-operand path gives (block-diagonal LoRA adds exact zeros)."""
+    d_in, d_out = shape
+    w, b = O.layer_params(8, 0, O.K, d_in, d_out)
+    ex = _ex({(0, O.K): (w, b)})
+    specs, _ = _mixed_clients(ex, d_in, d_out, seed=11)
+    counts = [512, 300, 1, 256, 700, 129, 1024][: len(specs)]
+    dev = ex.device
+    for pass_kind, width in ((0, d_in), (1, d_out)):
+        xs = [torch.randn(t, width, device=dev).to(torch.bfloat16) for t in counts]
+        xs[1] = xs[1].float()   # an f32 source always takes the packed path
+        outs = {}
+        for direct in (1, 0):
+            ex.ctx.set_option("direct_tiles", direct)
+            outs[direct] = ex._compute_batch(pass_kind, [_env(c, 60 + 2 * pass_kind + direct, 0, O.K, pass_kind, x)
+                                                         for c, x in enumerate(xs)])
+        ex.ctx.set_option("direct_tiles", 1)
+        for c in range(len(xs)):
+            assert torch.equal(outs[1][c], outs[0][c]), (pass_kind, c, counts[c])
