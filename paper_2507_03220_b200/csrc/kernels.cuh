@@ -585,10 +585,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 //   T[rows, rank_pad] = A_src[rows, K] . P[rank rows, K]^T (tcgen05, M=128, N=rank_pad),
 // scaled by alpha/r, rounded to bf16 and written into A_lora rows tile*TM + p0 .. at the piece's
 // column block col0 (zeros elsewhere come from a memset) — the block-diagonal LoRA operand.
-constexpr int SHRINK_STAGES = 4;
+// The shrink is HBM-bound (it re-reads the LoRA segments' rows once, N = rank is tiny), so it
+// runs 2 CTAs per SM (110 KB smem, 256 TMEM columns each) with as many pipeline stages as the
+// item's rank leaves room for: stage = 16 KB of A + rank_pad x 128 B of the pack.
 constexpr int SHRINK_MAXN = 256;
-constexpr int SHRINK_B_STAGE = SHRINK_MAXN * BK * 2;  // 32 KB
-constexpr int SHRINK_SMEM = SHRINK_STAGES * (A_STAGE_BYTES + SHRINK_B_STAGE) + 1024 + 256;
+constexpr int SHRINK_MAX_STAGES = 12;
+constexpr int SHRINK_SMEM = 110 * 1024;
 
 struct ShrinkItem {
   int32_t seg;
@@ -609,25 +611,29 @@ struct ShrinkParams {
   __nv_bfloat16* a_lora;
 };
 
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 2)
     lora_shrink_kernel(const __grid_constant__ CUtensorMap tmP,  // pack [R, K] (K-major rows)
                        const ShrinkParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* smA = smem;
-  uint8_t* smB = smem + SHRINK_STAGES * A_STAGE_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smB + SHRINK_STAGES * SHRINK_B_STAGE);
-  uint64_t* empty_bar = full_bar + SHRINK_STAGES;
-  uint64_t* tfull = empty_bar + SHRINK_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
   const ShrinkItem it = p.items[blockIdx.x];
   const DevSeg sg = p.segs[it.seg];
   const int npad = sg.rank_pad;  // multiple of 16, <= 256
   const CUtensorMap* tmA = p.tmaps + it.amap;
+  const int b_bytes = npad * BK * 2;
+  const int stage_bytes = A_STAGE_BYTES + b_bytes;
+  const int SHRINK_STAGES = min(SHRINK_MAX_STAGES, (SHRINK_SMEM - 2048) / stage_bytes);
+  // barriers in the first KB, then stages (each A | B, 1 KB aligned)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty_bar = full_bar + SHRINK_MAX_STAGES;
+  uint64_t* tfull = empty_bar + SHRINK_MAX_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint8_t* stage0 = smem + 1024;
+#define SHRINK_A(s) (stage0 + (s) * stage_bytes)
+#define SHRINK_B(s) (stage0 + (s) * stage_bytes + A_STAGE_BYTES)
 
   if (warp == 0 && lane == 0) {
     tensormap_acquire(tmA);
@@ -657,9 +663,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty_bar[s], ph ^ 1);
         mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nchunk * LORA_CHUNK_BYTES);
-        tma_load_2d(smA + s * A_STAGE_BYTES, tmA, &full_bar[s], kb * BK, it.arow);
+        tma_load_2d(SHRINK_A(s), tmA, &full_bar[s], kb * BK, it.arow);
         for (int q = 0; q < nchunk; ++q)
-          tma_load_2d(smB + s * SHRINK_B_STAGE + q * LORA_CHUNK_BYTES, &tmP, &full_bar[s], kb * BK,
+          tma_load_2d(SHRINK_B(s) + q * LORA_CHUNK_BYTES, &tmP, &full_bar[s], kb * BK,
                       sg.pack_row + q * LORA_CHUNK);
         if (++s == SHRINK_STAGES) { s = 0; ph ^= 1; }
       }
@@ -672,8 +678,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&full_bar[s], ph);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t a_addr = smem_u32(smA + s * A_STAGE_BYTES);
-        const uint32_t b_addr = smem_u32(smB + s * SHRINK_B_STAGE);
+        const uint32_t a_addr = smem_u32(SHRINK_A(s));
+        const uint32_t b_addr = smem_u32(SHRINK_B(s));
 #pragma unroll
         for (int k = 0; k < BK / UK; ++k)
           mma_bf16_ss(tmem_base, make_sdesc_sw128(a_addr + k * 32, 16, 1024),
@@ -715,6 +721,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tmem_dealloc(tmem_base, 256);
   }
 }
+#undef SHRINK_A
+#undef SHRINK_B
 
 // ============================================================================ K4 gather
 // Packs the rows that cannot be TMA-loaded in place (tails of segments shorter than a tile,
@@ -759,6 +767,20 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) 
         const uint4* s4 = reinterpret_cast<const uint4*>(sr);
         uint4* d4 = reinterpret_cast<uint4*>(xr);
         for (int i = lane; i < p.K / 8; i += 32) d4[i] = __ldg(s4 + i);
+      } else if (vec) {
+        // IA3 backward prologue, 8 bf16 per lane per step: g = dy * l (client.py:291-294)
+        const uint4* s4 = reinterpret_cast<const uint4*>(sr);
+        uint4* d4 = reinterpret_cast<uint4*>(xr);
+        for (int i = lane; i < p.K / 8; i += 32) {
+          const uint4 raw = __ldg(s4 + i);
+          const float4 la = __ldg(reinterpret_cast<const float4*>(l) + 2 * i);
+          const float4 lb = __ldg(reinterpret_cast<const float4*>(l) + 2 * i + 1);
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+          const float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]);
+          const float2 f2 = __bfloat1622float2(h[2]), f3 = __bfloat1622float2(h[3]);
+          d4[i] = make_uint4(pack_bf16x2(f0.x * la.x, f0.y * la.y), pack_bf16x2(f1.x * la.z, f1.y * la.w),
+                             pack_bf16x2(f2.x * lb.x, f2.y * lb.y), pack_bf16x2(f3.x * lb.z, f3.y * lb.w));
+        }
       } else {
         for (int i = lane; i < p.K; i += 32) {
           float v = __bfloat162float(sr[i]);

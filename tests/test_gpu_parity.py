@@ -455,3 +455,61 @@ def test_direct_tiles_bitwise_equal_packed_path(shape):
         ex.ctx.set_option("direct_tiles", 1)
         for c in range(len(xs)):
             assert torch.equal(outs[1][c], outs[0][c]), (pass_kind, c, counts[c])
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tensor_parallel_shards_through_cuda_path(world):
+    """Every TP rank's shard runs through the real C-ABI path (strided column views in, local
+    outputs); the collective is emulated in-process. Column-split forward / row-split backward
+    (all-gather) must equal the single-GPU executor bitwise; the all-reduce kinds (fp32 partial
+    sums) within the fp32-output tier."""
+    from paper_2507_03220_b200.tp import TensorParallelExecutor, combine_local
+    d, f, v = 512, 768, 1024
+    roles = [(O.Q, d, d), (O.O, d, d), (O.FF_UP, d, f), (O.FF_DOWN, f, d), (O.LM_HEAD, d, v), (O.K, d, d)]
+    layers = {}
+    for role, di, do in roles:
+        blk = 1 if role == O.LM_HEAD else 0
+        layers[(blk, role)] = O.layer_params(12, blk, role, di, do)
+    full = _ex(layers)
+    ranks = [TensorParallelExecutor({_addr(b, r): _params(w, bb) for (b, r), (w, bb) in layers.items()},
+                                    rk, world) for rk in range(world)]
+    ads = {}
+    for cid, (kind, r) in enumerate([("lora", 16), ("ia3", 0), ("plain", 0), ("lora", 64)]):
+        if kind == "lora":
+            lo = {}
+            for role, di, do in roles:
+                blk = 1 if role == O.LM_HEAD else 0
+                ad = O.lora_params(3, cid, blk, role, di, do, r, 2.0 * r)
+                lo[_addr(blk, role)] = (ad.a, ad.b)
+            ads[cid] = _Adapter(lora=lo, alpha=2.0 * r, rank=r)
+        elif kind == "ia3":
+            ads[cid] = _Adapter(ia3={_addr(0, role): O.ia3_params(3, cid, 0, role, do).ia3
+                                     for role, di, do in roles if role in O.IA3_ROLES})
+    for cid, ad in ads.items():
+        full.register_adapter(cid, ad)
+        for rk in ranks:
+            rk.register_adapter(cid, ad)
+    counts = [300, 64, 513, 256]
+    for role, di, do in roles:
+        blk = 1 if role == O.LM_HEAD else 0
+        for pass_kind, width in ((0, di), (1, do)):
+            xs = [torch.randn(t, width, device=full.device).to(torch.bfloat16) for t in counts]
+            ref = full._compute_batch(pass_kind, [_env(c, 900 + pass_kind, blk, role, pass_kind, x)
+                                                  for c, x in enumerate(xs)])
+            parts = [rk.dispatch_local(pass_kind, blk, role, xs, list(range(len(xs)))) for rk in ranks]
+            combined = combine_local([(s, loc) for s, loc, _ in parts], pass_kind)
+            got = combined.to(torch.bfloat16)
+            pos = 0
+            for c, t in enumerate(counts):
+                g, rf = got[pos:pos + t], ref[c]
+                pos += t
+                if parts[0][0].collective(pass_kind) == "all_gather":
+                    assert torch.equal(g, rf), (role, pass_kind, c)
+                else:
+                    _close(g.float().cpu().numpy(), rf.float().cpu().numpy(), MAX_REL, MEAN_REL,
+                           what=f"TP{world} {role} pass {pass_kind} client {c}")
+
+
+def _params(w, b):
+    from paper_2507_03220_b200 import AffineParams
+    return AffineParams(w, b)
