@@ -196,6 +196,68 @@ def run_step(plan, stream):
         d.run(stream)
 
 
+def build_tp_workload(wl_key, device, rank, world):
+    """--parallel tp: every rank serves ALL clients with its column / row shard of every layer
+    (paper_2507_03220_b200.tp); each dispatch ends in one NCCL all-gather or all-reduce.
+    All ranks generate the same full layers (rank-independent seeds) and keep their shard."""
+    import torch
+    from paper_2507_03220_b200 import AffineParams, LayerAddress, Role
+    from paper_2507_03220_b200.tp import TensorParallelExecutor
+
+    wl = WORKLOADS[wl_key]
+    layers, dims = layer_list(wl)
+    specs = client_specs(wl_key, wl["clients"])
+    seed = 1234
+
+    def gen_layers():
+        g = torch.Generator(device=device)
+        for (b, r) in layers:
+            di, do = dims[r]
+            g.manual_seed(seed * 1000 + b * 8 + r)
+            w = (torch.randn(di, do, generator=g, device=device) * (1.0 / math.sqrt(di))).to(torch.bfloat16)
+            yield LayerAddress(b, Role(r)), AffineParams(w, 0.05 * torch.randn(do, generator=g, device=device))
+
+    tp = TensorParallelExecutor(gen_layers(), rank, world, device=device.index)
+
+    class Ad:
+        def __init__(self):
+            self.lora, self.ia3, self.alpha, self.rank = {}, {}, 0.0, 1
+
+    g = torch.Generator(device=device)
+    for c, (kind, rank_, ft) in enumerate(specs):
+        ad = Ad()
+        g.manual_seed(seed + 17 * c + 5)
+        if kind == "lora":
+            ad.alpha, ad.rank = 2.0 * rank_, rank_
+            for b in range(wl["L"]):
+                for r in (Q, K, V, O):
+                    di, do = dims[r]
+                    ad.lora[LayerAddress(b, Role(r))] = (torch.randn(di, rank_, generator=g, device=device) / math.sqrt(di),
+                                                         0.05 * torch.randn(rank_, do, generator=g, device=device))
+        else:
+            for b in range(wl["L"]):
+                for r in (K, V, FF_UP):
+                    ad.ia3[LayerAddress(b, Role(r))] = 1.0 + 0.1 * torch.randn(dims[r][1], generator=g, device=device)
+        tp.register_adapter(c, ad)
+    t = wl["tokens"]
+    maxw = max(wl["d"], wl["d_ff"], wl["V"])
+    bufs = [torch.randn(t * maxw, generator=g, device=device).to(torch.bfloat16) for _ in specs]
+    plan = []
+    for (b, r) in layers:
+        di, do = dims[r]
+        plan.append((0, b, r, [bufs[c][: t * di].view(t, di) for c in range(len(specs))], list(range(len(specs)))))
+    ft = [c for c, s in enumerate(specs) if s[2]]
+    for (b, r) in reversed(layers):
+        di, do = dims[r]
+        plan.append((1, b, r, [bufs[c][: t * do].view(t, do) for c in ft], ft))
+    return tp, plan, specs, wl
+
+
+def run_step_tp(tp, plan):
+    for pass_kind, b, r, payloads, cids in plan:
+        tp.dispatch(pass_kind, b, r, payloads, cids)
+
+
 def e2e_leg(ex, wl_key, specs, steps, device):
     """Reference-facing path: numpy-like HOST clients. Each dispatch: pinned host payloads ->
     H2D -> fused compute -> D2H into pinned host reply buffers (in place, like LocalChannel's
@@ -367,6 +429,9 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=1)
+    ap.add_argument("--parallel", default="replicas", choices=("replicas", "tp"),
+                    help="replicas: segment-parallel full replicas (weak scaling, no data-path "
+                         "collective); tp: column/row-sharded layers + NCCL per dispatch (strong)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -406,17 +471,27 @@ def main():
     import torch
     import torch.distributed as dist
 
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    tp_mode = args.parallel == "tp"
+    if world > 1 or tp_mode:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                rank=rank, world_size=world)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     from paper_2507_03220_b200 import _lib
 
-    ex, plan, specs, wl = build_gpu_workload(args.workload, device, rank)
+    if tp_mode:
+        tp, tp_plan, specs, wl = build_tp_workload(args.workload, device, rank, world)
+        ex, plan = tp.ex, None
+        step_fn = lambda: run_step_tp(tp, tp_plan)  # noqa: E731
+    else:
+        ex, plan, specs, wl = build_gpu_workload(args.workload, device, rank)
+        step_fn = lambda: run_step(plan, stream)  # noqa: E731
     ctx = ex.ctx
     stream = torch.cuda.current_stream(device)
     for _ in range(max(3, args.warmup)):
-        run_step(plan, stream)
+        step_fn()
     torch.cuda.synchronize()
 
     samples, stop = [], threading.Event()
@@ -431,7 +506,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        run_step(plan, stream)
+        step_fn()
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -450,7 +525,7 @@ def main():
     sampler.join(timeout=2)
     clocks = summarize_clocks(samples)
 
-    tokens = tokens_per_rank * world
+    tokens = tokens_per_rank * (1 if tp_mode else world)
     value = tokens / (ms / 1e3)
     step_flops = flops_per_step(wl, specs)
     peaks = {}
@@ -469,7 +544,7 @@ def main():
             traffic = None
 
     e2e = None
-    if not args.skip_e2e:
+    if not args.skip_e2e and not tp_mode:
         dt, h2d, d2h = e2e_leg(ex, args.workload, specs, max(1, args.e2e_steps), device)
         if world > 1:
             t = torch.tensor([dt], device=device)
@@ -493,12 +568,14 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "strong" if tp_mode else "weak", "vs_baseline": None,
+            "dtype": "bf16",
             "data": "synthetic (random-init weights/adapters/activations, per-layer seeds)",
             "config": {"workload": wl["name"], "model": f"d{wl['d']}-ff{wl['d_ff']}-L{wl['L']}-V{wl['V']}",
                        "clients": wl["clients"], "global_batch": tokens, "seq_len": wl["seq"],
                        "batch_per_client": wl["batch"], "rows_per_fwd_dispatch": tokens_per_rank,
-                       "parallelism": f"segment-parallel replicas x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"tensor-parallel x{world} (NCCL all-gather/all-reduce per dispatch)" if tp_mode
+                                       else f"segment-parallel replicas x{world}" if world > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (every step streams all 6L+1 weight matrices)",
                        "step_tflop": step_flops / 1e12, "achieved_step_tflops": step_flops / (ms / 1e3) / 1e12},
             "roofline": {"bound": "tensor", "kernel": "seg_gemm_kernel (fused base GEMM + LoRA/IA3 epilogue)",
@@ -513,7 +590,7 @@ def main():
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or tp_mode:
         dist.destroy_process_group()
 
 
