@@ -287,7 +287,7 @@ def e2e_leg(ex, wl_key, specs, steps, device):
                                      reply_to=host[c][: t * do].view(t, do)))
                 h2d += t * di * 2
                 d2h += t * do * 2
-            ex._compute_batch(0, envs)
+            ex.serve_forward(envs)
         for (b, r) in reversed(layers):
             di, do = dims[r]
             envs = []
@@ -299,7 +299,7 @@ def e2e_leg(ex, wl_key, specs, steps, device):
                                      reply_to=host[c][: t * di].view(t, di)))
                 h2d += t * do * 2
                 d2h += t * di * 2
-            ex._compute_batch(1, envs)
+            ex.serve_backward(envs)
 
     step()  # warm-up (allocates the device staging)
     torch.cuda.synchronize()
@@ -552,7 +552,7 @@ def main():
             dt = float(t.item())
         e2e = {"value": tokens / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
-               "path": "GpuBaseExecutor._compute_batch, pinned host bf16 payloads + host reply buffers, "
+               "path": "GpuBaseExecutor.serve_forward / serve_backward, pinned host bf16 payloads + host reply buffers, "
                        f"{max(1, args.e2e_steps)} timed step(s) after 1 warm-up"}
 
     cpu = None

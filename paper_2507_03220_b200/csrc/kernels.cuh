@@ -103,6 +103,7 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int gro
 // Epilogue of one accumulator tile for the calling thread's row (TMEM lane): + bias,
 // optional pre-IA3 y_base store, * IA3 l, store into the row's segment destination.
 // Every thread of the warp must call it (tcgen05.ld is warp-collective).
+template <int TBN>
 __device__ __forceinline__ void epilogue_rows(const GemmParams& p, uint32_t tmem_acc, uint32_t ew,
                                               const TileDesc& td, int r, int n0, uint64_t* tfull,
                                               uint32_t tfull_ph) {
@@ -124,7 +125,7 @@ __device__ __forceinline__ void epilogue_rows(const GemmParams& p, uint32_t tmem
   const bool use_ia3 = row_ok && p.ia3_in_epilogue && (sg.flags & SEGF_IA3);
   const bool want_base = row_ok && (sg.flags & SEGF_WANT_BASE);
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = 0; c < TBN / 32; ++c) {
     uint32_t r[32];
     tmem_ld_32x32b_x32(tmem_acc + c * 32 + ((ew * 32u) << 16), r);
     tmem_wait_ld();
@@ -205,7 +206,18 @@ __device__ __forceinline__ void epilogue_rows(const GemmParams& p, uint32_t tmem
 }
 
 // ============================================================================ K1/K2/K5
-template <bool kBwd>
+// Single-CTA kernel, tile 128 x TBN. TBN < 256 is used when a dispatch has too few 128 x 256
+// tiles to fill the SMs (decode-style batches): the per-element K-reduction order does not
+// depend on TBN, so every tile width gives bitwise the same rows (batching stays invisible).
+template <int TBN>
+struct TileCfg {
+  static constexpr int B_STAGE = TBN * BK * 2;
+  static constexpr int STAGES_ = TBN == 256 ? 4 : (TBN == 128 ? 6 : 8);
+  static constexpr int STAGE = A_STAGE_BYTES + B_STAGE;
+  static constexpr int SMEM = STAGES_ * STAGE + 1024 + 256;
+};
+
+template <bool kBwd, int TBN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     seg_gemm_kernel(const __grid_constant__ CUtensorMap tmB,   // W  [d_in, d_out] bf16
                     const __grid_constant__ CUtensorMap tmAL,  // A_lora [M, R_w] bf16
@@ -215,6 +227,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* smA = smem;
+  constexpr int STAGES = TileCfg<TBN>::STAGES_;
+  constexpr int B_STAGE_BYTES = TileCfg<TBN>::B_STAGE;
+  constexpr int STAGE_BYTES = TileCfg<TBN>::STAGE;
   uint8_t* smB = smem + STAGES * A_STAGE_BYTES;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
@@ -243,7 +258,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * TBN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -262,7 +277,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
         const TileDesc td = p.tiles[mb];
         const CUtensorMap* tmA = p.tmaps + td.amap;
-        const int m0 = mb * BM, n0 = nb * BN;
+        const int m0 = mb * BM, n0 = nb * TBN;
         tensormap_acquire(tmA);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
@@ -275,7 +290,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           } else {
             // W MN-major: 4 chunks of 64 output columns x 64 K rows.
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
+            for (int j = 0; j < TBN / 64; ++j)
               tma_load_2d(b + j * (BK * 128), &tmB, &full_bar[s], n0 + 64 * j, kb * BK);
           }
           if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -286,13 +301,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int ls = 0; ls * 4 < cc; ++ls) {
             const int nq = min(4, cc - ls * 4);
             mbar_wait(&empty_bar[s], ph ^ 1);
-            mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nq * (BN / 64) * LORA_CHUNK_BYTES);
+            mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nq * (TBN / 64) * LORA_CHUNK_BYTES);
             tma_load_2d(smA + s * A_STAGE_BYTES, &tmAL, &full_bar[s], ls * BK, m0);
             uint8_t* b = smB + s * B_STAGE_BYTES;
             for (int q = 0; q < nq; ++q) {
               const int prow = p.chunks[cb + ls * 4 + q];
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
+              for (int j = 0; j < TBN / 64; ++j)
                 tma_load_2d(b + j * (BK * 128) + q * LORA_CHUNK_BYTES, &tmBP, &full_bar[s],
                             n0 + 64 * j, prow);
             }
@@ -303,8 +318,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc_base = make_idesc_bf16(BM, BN, false, !kBwd);
-    constexpr uint32_t idesc_lora = make_idesc_bf16(BM, BN, false, true);
+    constexpr uint32_t idesc_base = make_idesc_bf16(BM, TBN, false, !kBwd);
+    constexpr uint32_t idesc_lora = make_idesc_bf16(BM, TBN, false, true);
     int s = 0;
     uint32_t ph = 0;
     int acc = 0;
@@ -314,7 +329,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
       mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
+      const uint32_t d_tmem = tmem_base + acc * TBN;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full_bar[s], ph);
         tc_fence_after();
@@ -366,7 +381,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int mb, nb;
       tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
       const TileDesc td = p.tiles[mb];
-      epilogue_rows(p, tmem_base + acc * BN, ew, td, ew * 32 + lane, nb * BN, &tfull_bar[acc], acc_ph);
+      epilogue_rows<TBN>(p, tmem_base + acc * TBN, ew, td, ew * 32 + lane, nb * TBN, &tfull_bar[acc], acc_ph);
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
@@ -376,7 +391,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    tmem_dealloc(tmem_base, 2 * TBN);
   }
 }
 
@@ -563,7 +578,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       int mb, nb;
       tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
       const TileDesc td = p.tiles[mb];
-      epilogue_rows(p, tmem_base + acc * BN, ew, td, crank * BM + ew * 32 + lane, nb * BN,
+      epilogue_rows<BN>(p, tmem_base + acc * BN, ew, td, crank * BM + ew * 32 + lane, nb * BN,
                     &tfull_bar[acc], acc_ph);
       tc_fence_before();
       __syncwarp();

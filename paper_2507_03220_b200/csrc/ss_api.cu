@@ -44,7 +44,7 @@ struct Layer {
   __nv_bfloat16* W = nullptr;
   int64_t ldw = 0;
   float* bias = nullptr;
-  CUtensorMap tm_w_fwd, tm_w_bwd, tm_w_bwd2;  // bwd: box rows 256 (1-CTA) / 128 (pair)
+  CUtensorMap tm_w_fwd, tm_w_bwd, tm_w_bwd2, tm_w_bwd64;  // bwd box rows 256 / 128 / 64
   // LoRA packs: rows = rank index of every registered client (16-aligned blocks)
   __nv_bfloat16* at_pack = nullptr;  // [cap, ld_at]  (A^T: rank rows x d_in)
   __nv_bfloat16* b_pack = nullptr;   // [cap, ld_b]   (B:   rank rows x d_out)
@@ -95,6 +95,7 @@ struct ss_ctx {
   // power-capped clock drops; profiles/r01_gemm_variants.md). 1 / 0 force one kernel.
   int gemm_2cta = -1;
   int direct_tiles = 1;  // 1: TMA-load whole tiles of bf16 segments in place (no gather)
+  int force_tbn = 0;     // testing: force the single-CTA tile width (64 / 128 / 256)
   int64_t weight_bytes = 0, adapter_bytes = 0;
   // in-stream profiling
   bool profiling = false;
@@ -296,10 +297,18 @@ KernelAttrs g_attrs;
 
 int set_kernel_attrs(ss_ctx* ctx) {
   if (g_attrs.done) return SS_OK;
-  CK(cudaFuncSetAttribute(seg_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          GEMM_SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          GEMM_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<256>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<256>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<128>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<128>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<64>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<64>::SMEM));
   CK(cudaFuncSetAttribute(seg_gemm2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           GEMM2_SMEM));
   CK(cudaFuncSetAttribute(seg_gemm2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -398,6 +407,12 @@ int ss_ctx_destroy(ss_ctx* ctx) {
 
 int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!ctx || !key) return SS_E_ARG;
+  if (!strcmp(key, "tile_n")) {
+    if (value != 0 && value != 64 && value != 128 && value != 256)
+      return fail(ctx, SS_E_ARG, "tile_n must be 0 (auto), 64, 128 or 256");
+    ctx->force_tbn = (int)value;
+    return SS_OK;
+  }
   if (!strcmp(key, "direct_tiles")) {
     ctx->direct_tiles = value ? 1 : 0;
     return SS_OK;
@@ -445,6 +460,8 @@ int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const v
   rc = encode_2d(ctx, &L.tm_w_bwd, L.W, d_out, d_in, L.ldw, 64, BN);
   if (rc) return rc;
   rc = encode_2d(ctx, &L.tm_w_bwd2, L.W, d_out, d_in, L.ldw, 64, BN / 2);
+  if (rc) return rc;
+  rc = encode_2d(ctx, &L.tm_w_bwd64, L.W, d_out, d_in, L.ldw, 64, 64);
   if (rc) return rc;
   ctx->weight_bytes += (int64_t)d_in * L.ldw * 2 + (bias ? round_up(d_out, 64) * 4 : 0);
   ctx->layers[{block, role}] = L;
@@ -653,8 +670,18 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   CK(cudaSetDevice(ctx->device));
 
   // ---- M-tiles: segment-aligned direct tiles for whole tiles of bf16 rows, the rest packed
-  const bool pair = ctx->gemm_2cta < 0 ? (K <= 8192 && M > BM) : ctx->gemm_2cta != 0;
+  // Kernel / tile choice depends only on the layer shape and the dispatch size, never on which
+  // segments are present; every choice reduces K in the same order (bitwise-equal rows).
+  const int n256 = (N + BN - 1) / BN;
+  const bool pair = ctx->gemm_2cta < 0 ? (K <= 8192 && ((M + BM2 - 1) / BM2) * n256 >= ctx->num_sms / 2)
+                                       : ctx->gemm_2cta != 0;
   const int TM = pair ? BM2 : BM;
+  int tbn = BN;
+  if (!pair) {
+    const int64_t m128 = (M + BM - 1) / BM;
+    if (m128 * n256 < ctx->num_sms) tbn = (m128 * ((N + 127) / 128) >= ctx->num_sms) ? 128 : 64;
+    if (ctx->force_tbn) tbn = ctx->force_tbn;
+  }
   std::vector<TileDesc> tiles;
   std::vector<int32_t> piece_seg;          // packed pieces in X order
   std::vector<int32_t> direct_src;         // segment of each direct tensor map (map = 1 + i)
@@ -842,7 +869,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   gpm.N = N;
   gpm.K = K;
   gpm.num_m_tiles = num_m;
-  gpm.num_n_tiles = (N + BN - 1) / BN;
+  gpm.num_n_tiles = (N + tbn - 1) / tbn;
   gpm.group_m = ctx->group_m;
   gpm.has_bias = (pass_kind == SS_PASS_FORWARD && L.bias) ? 1 : 0;
   gpm.any_lora = any_lora ? 1 : 0;
@@ -870,10 +897,15 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
       seg_gemm2_kernel<true><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
     else
       seg_gemm2_kernel<false><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
-  } else if (bwd) {
-    seg_gemm_kernel<true><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(L.tm_w_bwd, tmAL, tmBP, gpm);
+  } else if (tbn == 256) {
+    if (bwd) seg_gemm_kernel<true, 256><<<grid, GEMM_THREADS, TileCfg<256>::SMEM, stream>>>(L.tm_w_bwd, tmAL, tmBP, gpm);
+    else seg_gemm_kernel<false, 256><<<grid, GEMM_THREADS, TileCfg<256>::SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
+  } else if (tbn == 128) {
+    if (bwd) seg_gemm_kernel<true, 128><<<grid, GEMM_THREADS, TileCfg<128>::SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
+    else seg_gemm_kernel<false, 128><<<grid, GEMM_THREADS, TileCfg<128>::SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
   } else {
-    seg_gemm_kernel<false><<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
+    if (bwd) seg_gemm_kernel<true, 64><<<grid, GEMM_THREADS, TileCfg<64>::SMEM, stream>>>(L.tm_w_bwd64, tmAL, tmBP, gpm);
+    else seg_gemm_kernel<false, 64><<<grid, GEMM_THREADS, TileCfg<64>::SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
   }
   prof_end(ctx, stream, pg);
   CK(cudaGetLastError());

@@ -513,3 +513,29 @@ def test_tensor_parallel_shards_through_cuda_path(world):
 def _params(w, b):
     from paper_2507_03220_b200 import AffineParams
     return AffineParams(w, b)
+
+
+@pytest.mark.parametrize("shape", [(512, 1280), (5120, 1536)])
+def test_every_kernel_and_tile_width_gives_identical_rows(shape):
+    """The dispatch picks the CTA-pair kernel or the single-CTA kernel with 256/128/64-wide tiles
+    from the dispatch size; all of them must produce bitwise the same rows (the per-element K
+    order is the same), otherwise batching would become visible (acceptance C5)."""
+    d_in, d_out = shape
+    w, b = O.layer_params(13, 0, O.K, d_in, d_out)
+    ex = _ex({(0, O.K): (w, b)})
+    _mixed_clients(ex, d_in, d_out, seed=13)
+    counts = [700, 256, 3, 129, 512, 64, 1]
+    dev = ex.device
+    for pass_kind, width in ((0, d_in), (1, d_out)):
+        xs = [torch.randn(t, width, device=dev).to(torch.bfloat16) for t in counts]
+        outs = []
+        for pair, tn in ((1, 0), (0, 256), (0, 128), (0, 64)):
+            ex.ctx.set_option("gemm_2cta", pair)
+            ex.ctx.set_option("tile_n", tn)
+            outs.append(ex._compute_batch(pass_kind, [_env(c, 70 + 10 * pass_kind + len(outs), 0, O.K, pass_kind, x)
+                                                      for c, x in enumerate(xs)]))
+        ex.ctx.set_option("gemm_2cta", -1)
+        ex.ctx.set_option("tile_n", 0)
+        for k in range(1, len(outs)):
+            for c in range(len(xs)):
+                assert torch.equal(outs[0][c], outs[k][c]), (pass_kind, k, c)
