@@ -29,6 +29,7 @@ enum : int32_t {
   SEGF_SRC_VEC = 1 << 6,   // src rows 16-byte aligned
   SEGF_DST_VEC = 1 << 7,   // dst rows 16-byte aligned
   SEGF_BASE_VEC = 1 << 8,  // base rows 16-byte aligned
+  SEGF_TMA_STORE = 1 << 9, // bf16 destination written by TMA bulk stores
 };
 
 struct DevSeg {
@@ -72,7 +73,8 @@ struct TileDesc {
   int32_t rows;         // valid rows (<= TM)
   int32_t chunk_begin;  // LoRA: first entry in `chunks`
   int32_t chunk_count;  // LoRA: 16-wide rank chunks (block-diagonal over the tile's segments)
-  int32_t pad0, pad1;
+  int32_t store_begin;  // TMA-store ops of this tile: entries in GemmParams::stores
+  int32_t store_count;
 };
 
 struct GemmParams {
@@ -86,7 +88,8 @@ struct GemmParams {
   const int32_t* row_seg;           // per packed X row: its segment
   const TileDesc* tiles;            // per M-tile
   const int32_t* chunks;            // pack row of each rank chunk
-  const CUtensorMap* tmaps;         // [0] = X, [1 + i] = direct source i (device memory)
+  const CUtensorMap* tmaps;         // [0] = X, then per-dispatch source / destination maps
+  const int2* stores;               // (dst tensor map, row coordinate of tile row 0) per op
 };
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb,
@@ -100,14 +103,50 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int gro
   nb = r / gsize;
 }
 
-// Epilogue of one accumulator tile for the calling thread's row (TMEM lane): + bias,
-// optional pre-IA3 y_base store, * IA3 l, store into the row's segment destination.
-// Every thread of the warp must call it (tcgen05.ld is warp-collective).
+// Store `ncols` (<= 64) fp32 values of one row to a bf16 / f32 destination with plain global
+// stores (16-byte vectors when aligned). Used for f32 destinations, misaligned rows and y_base.
+__device__ __forceinline__ void store_row_global(const float* v, int ncols, char* dst, bool bf,
+                                                 bool vec) {
+  if (ncols == 64 && vec) {
+    if (bf) {
+      uint4* o = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        o[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                          pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+    } else {
+      float4* o = reinterpret_cast<float4*>(dst);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+  } else {
+    for (int j = 0; j < ncols; ++j) {
+      if (bf) reinterpret_cast<__nv_bfloat16*>(dst)[j] = __float2bfloat16_rn(v[j]);
+      else reinterpret_cast<float*>(dst)[j] = v[j];
+    }
+  }
+}
+
+constexpr int EPI_CHUNK = 64;                           // columns per epilogue step
+constexpr int EPI_STAGE_BYTES = BM * EPI_CHUNK * 2;     // 16 KB bf16 staging (128 rows x 128 B)
+constexpr int EPI_SMEM = 2 * EPI_STAGE_BYTES;           // double-buffered
+
+// Epilogue of one accumulator tile, executed by the 4 epilogue warps (128 threads, thread =
+// TMEM lane = row r of this CTA's 128 rows). Per 64-column chunk: tcgen05.ld -> + bias ->
+// optional pre-IA3 y_base store -> * IA3 l -> bf16 into a 128B-swizzled staging tile -> one TMA
+// bulk store per destination segment piece of the tile (rows outside a piece are clipped by its
+// tensor map, so a tile shared by several clients needs no masking). Rows whose destination is
+// f32 or misaligned fall back to direct global stores. Releases the TMEM accumulator (tempty)
+// as soon as its last column has been read. `store_row0` = this CTA's first row within the
+// tile (0, or 128 for the second CTA of a pair).
 template <int TBN>
-__device__ __forceinline__ void epilogue_rows(const GemmParams& p, uint32_t tmem_acc, uint32_t ew,
-                                              const TileDesc& td, int r, int n0, uint64_t* tfull,
-                                              uint32_t tfull_ph) {
+__device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, uint32_t ew,
+                                              uint32_t lane, const TileDesc& td, int store_row0, int n0,
+                                              uint64_t* tfull, uint32_t tfull_ph, uint8_t* stage,
+                                              uint32_t tempty_cluster_addr) {
+  const int r = store_row0 + ew * 32 + lane;  // row within the tile
   const bool row_ok = r < td.rows;
+  const bool leader_thread = ew == 0 && lane == 0;
   DevSeg sg;
   int r_local = 0;
   if (row_ok) {
@@ -120,86 +159,93 @@ __device__ __forceinline__ void epilogue_rows(const GemmParams& p, uint32_t tmem
       r_local = xrow - sg.xrow0 + sg.xlocal0;
     }
   }
-  mbar_wait(tfull, tfull_ph);
-  tc_fence_after();
   const bool use_ia3 = row_ok && p.ia3_in_epilogue && (sg.flags & SEGF_IA3);
   const bool want_base = row_ok && (sg.flags & SEGF_WANT_BASE);
+  // TMA box coordinates must be >= 0: a packed piece that starts inside the tile has no bulk
+  // store op (host side) and its rows take the direct-store path.
+  const bool tma_row = row_ok && (sg.flags & SEGF_TMA_STORE) && (td.seg >= 0 || sg.xrow0 <= td.arow);
+  const int lrow = ew * 32 + lane;            // row within this CTA's staging tile
+  if (leader_thread) {
+    for (int k = 0; k < td.store_count; ++k) tensormap_acquire(p.tmaps + p.stores[td.store_begin + k].x);
+  }
+  mbar_wait(tfull, tfull_ph);
+  tc_fence_after();
 #pragma unroll 1
-  for (int c = 0; c < TBN / 32; ++c) {
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(tmem_acc + c * 32 + ((ew * 32u) << 16), r);
+  for (int c = 0; c < TBN / EPI_CHUNK; ++c) {
+    uint32_t ra[32], rb[32];
+    tmem_ld_32x32b_x32(tmem_acc + c * EPI_CHUNK + ((ew * 32u) << 16), ra);
+    tmem_ld_32x32b_x32(tmem_acc + c * EPI_CHUNK + 32 + ((ew * 32u) << 16), rb);
     tmem_wait_ld();
-    const int n = n0 + c * 32;
-    if (!row_ok || n >= p.N) continue;
-    float v[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-    const int ncols = min(32, p.N - n);
-    if (p.has_bias) {
-      if (ncols == 32) {
-        const float4* b4 = reinterpret_cast<const float4*>(p.bias + n);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 bb = __ldg(b4 + j);
-          v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
-        }
-      } else {
-        for (int j = 0; j < ncols; ++j) v[j] += __ldg(p.bias + n + j);
-      }
+    if (c == TBN / EPI_CHUNK - 1) {
+      // every column of the accumulator is in registers: hand TMEM back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_cluster_addr);
     }
-    if (want_base) {
-      const bool bf = sg.flags & SEGF_BASE_BF16;
-      char* base = reinterpret_cast<char*>(sg.dst_base) +
-                   ((int64_t)r_local * sg.base_ld + n) * (bf ? 2 : 4);
-      if (ncols == 32 && (sg.flags & SEGF_BASE_VEC)) {
-        if (bf) {
-          uint4* o = reinterpret_cast<uint4*>(base);
+    const int n = n0 + c * EPI_CHUNK;
+    const int ncols = max(0, min(EPI_CHUNK, p.N - n));
+    float v[64];
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            o[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                              pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+    for (int j = 0; j < 32; ++j) {
+      v[j] = __uint_as_float(ra[j]);
+      v[32 + j] = __uint_as_float(rb[j]);
+    }
+    if (row_ok && ncols > 0) {
+      if (p.has_bias) {
+        if (ncols == 64) {
+          const float4* b4 = reinterpret_cast<const float4*>(p.bias + n);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float4 bb = __ldg(b4 + j);
+            v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
+          }
         } else {
-          float4* o = reinterpret_cast<float4*>(base);
+          for (int j = 0; j < ncols; ++j) v[j] += __ldg(p.bias + n + j);
+        }
+      }
+      if (want_base) {
+        const bool bf = sg.flags & SEGF_BASE_BF16;
+        char* base = reinterpret_cast<char*>(sg.dst_base) + ((int64_t)r_local * sg.base_ld + n) * (bf ? 2 : 4);
+        store_row_global(v, ncols, base, bf, sg.flags & SEGF_BASE_VEC);
+      }
+      if (use_ia3) {
+        if (ncols == 64) {
+          const float4* l4 = reinterpret_cast<const float4*>(sg.ia3 + n);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          for (int j = 0; j < 16; ++j) {
+            const float4 ll = __ldg(l4 + j);
+            v[4 * j] *= ll.x; v[4 * j + 1] *= ll.y; v[4 * j + 2] *= ll.z; v[4 * j + 3] *= ll.w;
+          }
+        } else {
+          for (int j = 0; j < ncols; ++j) v[j] *= __ldg(sg.ia3 + n + j);
         }
-      } else {
-        for (int j = 0; j < ncols; ++j) {
-          if (bf) reinterpret_cast<__nv_bfloat16*>(base)[j] = __float2bfloat16_rn(v[j]);
-          else reinterpret_cast<float*>(base)[j] = v[j];
-        }
+      }
+      if (!tma_row) {
+        const bool bf = sg.flags & SEGF_DST_BF16;
+        char* dst = reinterpret_cast<char*>(sg.dst) + ((int64_t)r_local * sg.dst_ld + n) * (bf ? 2 : 4);
+        store_row_global(v, ncols, dst, bf, sg.flags & SEGF_DST_VEC);
       }
     }
-    if (use_ia3) {
-      if (ncols == 32) {
-        const float4* l4 = reinterpret_cast<const float4*>(sg.ia3 + n);
+    if (td.store_count > 0) {
+      uint8_t* sb = stage + (c & 1) * EPI_STAGE_BYTES;
+      if (leader_thread) bulk_wait_read<1>();      // the store issued 2 chunks ago freed `sb`
+      named_bar_sync(1, 128);
+      if (tma_row && ncols > 0) {
+        uint8_t* rowp = sb + lrow * 128;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 ll = __ldg(l4 + j);
-          v[4 * j] *= ll.x; v[4 * j + 1] *= ll.y; v[4 * j + 2] *= ll.z; v[4 * j + 3] *= ll.w;
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint4*>(rowp + ((j ^ (lrow & 7)) << 4)) =
+              make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                         pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+      }
+      fence_async_smem();
+      named_bar_sync(1, 128);
+      if (leader_thread && ncols > 0) {
+        for (int k = 0; k < td.store_count; ++k) {
+          const int2 op = p.stores[td.store_begin + k];
+          tma_store_2d(p.tmaps + op.x, sb, n, op.y + store_row0);
         }
-      } else {
-        for (int j = 0; j < ncols; ++j) v[j] *= __ldg(sg.ia3 + n + j);
-      }
-    }
-    const bool bf = sg.flags & SEGF_DST_BF16;
-    char* dst = reinterpret_cast<char*>(sg.dst) + ((int64_t)r_local * sg.dst_ld + n) * (bf ? 2 : 4);
-    if (ncols == 32 && (sg.flags & SEGF_DST_VEC)) {
-      if (bf) {
-        uint4* o = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          o[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                            pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
-      } else {
-        float4* o = reinterpret_cast<float4*>(dst);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-      }
-    } else {
-      for (int j = 0; j < ncols; ++j) {
-        if (bf) reinterpret_cast<__nv_bfloat16*>(dst)[j] = __float2bfloat16_rn(v[j]);
-        else reinterpret_cast<float*>(dst)[j] = v[j];
+        bulk_commit();
       }
     }
   }
@@ -214,7 +260,7 @@ struct TileCfg {
   static constexpr int B_STAGE = TBN * BK * 2;
   static constexpr int STAGES_ = TBN == 256 ? 4 : (TBN == 128 ? 6 : 8);
   static constexpr int STAGE = A_STAGE_BYTES + B_STAGE;
-  static constexpr int SMEM = STAGES_ * STAGE + 1024 + 256;
+  static constexpr int SMEM = STAGES_ * STAGE + EPI_SMEM + 1024 + 256;
 };
 
 template <bool kBwd, int TBN>
@@ -231,7 +277,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   constexpr int B_STAGE_BYTES = TileCfg<TBN>::B_STAGE;
   constexpr int STAGE_BYTES = TileCfg<TBN>::STAGE;
   uint8_t* smB = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* epi_stage = smem + STAGES * STAGE_BYTES;  // 2 x 16 KB TMA-store staging
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_stage + EPI_SMEM);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;   // 2 accumulator buffers
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -254,7 +301,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 128);
+      mbar_init(&tempty_bar[b], 4);    // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
@@ -375,17 +422,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const uint32_t ew = warp - 4;  // TMEM lane quarter
+    const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);  // own CTA (cluster of 1)
     int acc = 0;
     uint32_t acc_ph = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
       const TileDesc td = p.tiles[mb];
-      epilogue_rows<TBN>(p, tmem_base + acc * TBN, ew, td, ew * 32 + lane, nb * TBN, &tfull_bar[acc], acc_ph);
-      tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      epilogue_tile<TBN>(p, tmem_base + acc * TBN, ew, lane, td, 0, nb * TBN, &tfull_bar[acc], acc_ph,
+                         epi_stage, tempty0 + acc * 8);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
+    if (ew == 0 && lane == 0) bulk_wait_all();
   }
 
   __syncthreads();
@@ -406,7 +454,7 @@ constexpr int BM2 = 256;                        // rows per pair tile
 constexpr int STAGES2 = 6;
 constexpr int B_HALF_BYTES = (BN / 2) * BK * 2;  // 16 KB
 constexpr int STAGE2_BYTES = A_STAGE_BYTES + B_HALF_BYTES;
-constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 256;
+constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + EPI_SMEM + 1024 + 256;
 
 template <bool kBwd>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
@@ -419,7 +467,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                                              ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES2 * A_STAGE_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint8_t* epi_stage = smem + STAGES2 * STAGE2_BYTES;  // 2 x 16 KB TMA-store staging
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_stage + EPI_SMEM);
   uint64_t* empty_bar = full_bar + STAGES2;
   uint64_t* tfull_bar = empty_bar + STAGES2;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -578,13 +627,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       int mb, nb;
       tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
       const TileDesc td = p.tiles[mb];
-      epilogue_rows<BN>(p, tmem_base + acc * BN, ew, td, crank * BM + ew * 32 + lane, nb * BN,
-                    &tfull_bar[acc], acc_ph);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+      epilogue_tile<BN>(p, tmem_base + acc * BN, ew, lane, td, crank * BM, nb * BN, &tfull_bar[acc],
+                        acc_ph, epi_stage, tempty0 + acc * 8);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
+    if (ew == 0 && lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();

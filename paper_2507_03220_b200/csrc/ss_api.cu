@@ -96,6 +96,7 @@ struct ss_ctx {
   int gemm_2cta = -1;
   int direct_tiles = 1;  // 1: TMA-load whole tiles of bf16 segments in place (no gather)
   int force_tbn = 0;     // testing: force the single-CTA tile width (64 / 128 / 256)
+  int tma_store = 1;     // 1: bf16 outputs leave through swizzled smem + TMA bulk stores
   int64_t weight_bytes = 0, adapter_bytes = 0;
   // in-stream profiling
   bool profiling = false;
@@ -407,6 +408,10 @@ int ss_ctx_destroy(ss_ctx* ctx) {
 
 int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!ctx || !key) return SS_E_ARG;
+  if (!strcmp(key, "tma_store")) {
+    ctx->tma_store = value ? 1 : 0;
+    return SS_OK;
+  }
   if (!strcmp(key, "tile_n")) {
     if (value != 0 && value != 64 && value != 128 && value != 256)
       return fail(ctx, SS_E_ARG, "tile_n must be 0 (auto), 64, 128 or 256");
@@ -761,7 +766,9 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   }
   ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap);
 
-  // ---- tensor maps: [0] = X, [1 + i] = direct source i (box {64, 128} rows)
+  // ---- tensor maps: [0] = X, [1 + i] = direct source i (box {64, 128} rows), then the
+  // destination maps of TMA-stored segments: one over the whole segment (direct tiles) and one
+  // over its packed tail only (so a packed tile's store can never touch the segment's head rows)
   std::vector<CUtensorMap> tmaps(1 + direct_src.size());
   rc = encode_2d(ctx, &tmaps[0], ctx->X, K, std::max<int64_t>(MX, 1), ldx, 64, BM);
   if (rc) return rc;
@@ -770,6 +777,50 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     rc = encode_2d(ctx, &tmaps[1 + i], d.src, K, d.rows, d.src_ld, 64, BM);
     if (rc) return rc;
   }
+  std::vector<int32_t> dmap_full(ds.size(), -1), dmap_tail(ds.size(), -1);
+  for (size_t j = 0; j < ds.size(); ++j) {
+    DevSeg& d = ds[j];
+    if (!ctx->tma_store || !(d.flags & SEGF_DST_BF16) || !(d.flags & SEGF_DST_VEC)) continue;
+    d.flags |= SEGF_TMA_STORE;
+    const bool has_direct = d.xrow0 < 0 || d.xlocal0 > 0;
+    if (has_direct) {
+      dmap_full[j] = (int32_t)tmaps.size();
+      tmaps.emplace_back();
+      rc = encode_2d(ctx, &tmaps.back(), d.dst, N, d.rows, d.dst_ld, 64, BM);
+      if (rc) return rc;
+    }
+    if (d.xrow0 >= 0) {
+      dmap_tail[j] = (int32_t)tmaps.size();
+      tmaps.emplace_back();
+      rc = encode_2d(ctx, &tmaps.back(), static_cast<const char*>(d.dst) + (int64_t)d.xlocal0 * d.dst_ld * 2, N,
+                     d.rows - d.xlocal0, d.dst_ld, 64, BM);
+      if (rc) return rc;
+    }
+  }
+  std::vector<int2> stores;
+  {
+    size_t pi = 0;
+    for (TileDesc& td : tiles) {
+      td.store_begin = (int32_t)stores.size();
+      if (td.seg >= 0) {
+        if (dmap_full[td.seg] >= 0) stores.push_back(make_int2(dmap_full[td.seg], td.arow));
+      } else {
+        const int64_t x0 = td.arow, x1 = x0 + td.rows;
+        while (pi < piece_seg.size() &&
+               ds[piece_seg[pi]].xrow0 + (ds[piece_seg[pi]].rows - ds[piece_seg[pi]].xlocal0) <= x0)
+          ++pi;
+        for (size_t k = pi; k < piece_seg.size(); ++k) {
+          const DevSeg& d = ds[piece_seg[k]];
+          if (d.xrow0 >= x1) break;
+          // only pieces that start at or before the tile's first row (non-negative box
+          // coordinate); the kernel stores rows of later-starting pieces directly
+          if (dmap_tail[piece_seg[k]] >= 0 && d.xrow0 <= x0)
+            stores.push_back(make_int2(dmap_tail[piece_seg[k]], (int32_t)(x0 - d.xrow0)));
+        }
+      }
+      td.store_count = (int32_t)stores.size() - td.store_begin;
+    }
+  }
 
   // ---- routing tables -> pinned staging slot -> device (one async copy)
   const size_t off_tm = 0;
@@ -777,7 +828,8 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   const size_t off_tile = off_seg + round_up(ds.size() * sizeof(DevSeg), 256);
   const size_t off_piece = off_tile + round_up(tiles.size() * sizeof(TileDesc), 256);
   const size_t off_ch = off_piece + round_up(std::max<size_t>(1, piece_seg.size()) * 4, 256);
-  const size_t off_it = off_ch + round_up(std::max<size_t>(1, chunks.size()) * 4, 256);
+  const size_t off_st = off_ch + round_up(std::max<size_t>(1, chunks.size()) * 4, 256);
+  const size_t off_it = off_st + round_up(std::max<size_t>(1, stores.size()) * sizeof(int2), 256);
   const size_t total = off_it + round_up(std::max<size_t>(1, items.size()) * sizeof(ShrinkItem), 256);
   Staging& st = ctx->staging[ctx->slot];
   ctx->slot = (ctx->slot + 1) % kStagingSlots;
@@ -798,13 +850,14 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   memcpy(h + off_seg, ds.data(), ds.size() * sizeof(DevSeg));
   memcpy(h + off_tile, tiles.data(), tiles.size() * sizeof(TileDesc));
   if (!piece_seg.empty()) memcpy(h + off_piece, piece_seg.data(), piece_seg.size() * 4);
+  if (!stores.empty()) memcpy(h + off_st, stores.data(), stores.size() * sizeof(int2));
   if (any_lora) {
     memcpy(h + off_ch, chunks.data(), chunks.size() * 4);
     memcpy(h + off_it, items.data(), items.size() * sizeof(ShrinkItem));
   }
   // adapters uploaded on the side stream must be complete before this dispatch reads them
   CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
-  CK(cudaMemcpyAsync(st.dev, st.host, any_lora ? total : off_ch, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(st.dev, st.host, any_lora ? total : off_it, cudaMemcpyHostToDevice, stream));
   CK(cudaEventRecord(st.done, stream));
   st.pending = true;
   char* dv = static_cast<char*>(st.dev);
@@ -880,6 +933,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   gpm.tiles = reinterpret_cast<const TileDesc*>(dv + off_tile);
   gpm.chunks = reinterpret_cast<const int32_t*>(dv + off_ch);
   gpm.tmaps = d_tmaps;
+  gpm.stores = reinterpret_cast<const int2*>(dv + off_st);
   const int ntiles = gpm.num_m_tiles * gpm.num_n_tiles;
   const int grid = pair ? 2 * std::min(ntiles, ctx->num_sms / 2) : std::min(ntiles, ctx->num_sms);
   const CUtensorMap& tmBP = any_lora ? (bwd ? L.tm_at : L.tm_b) : L.tm_w_fwd;

@@ -539,3 +539,27 @@ def test_every_kernel_and_tile_width_gives_identical_rows(shape):
         for k in range(1, len(outs)):
             for c in range(len(xs)):
                 assert torch.equal(outs[0][c], outs[k][c]), (pass_kind, k, c)
+
+
+@pytest.mark.parametrize("pair", [1, 0])
+def test_tma_store_epilogue_bitwise_equals_direct_stores(pair):
+    """bf16 outputs leave through swizzled smem + TMA bulk stores (clipped per destination
+    segment) or through per-thread global stores; both must write identical bytes, including
+    packed tiles shared by several clients and partial last tiles."""
+    d_in, d_out = 512, 1088
+    w, b = O.layer_params(14, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)})
+    _mixed_clients(ex, d_in, d_out, seed=14, role=O.V)
+    counts = [300, 1, 700, 130, 5, 256, 77]
+    ex.ctx.set_option("gemm_2cta", pair)
+    for pass_kind, width in ((0, d_in), (1, d_out)):
+        xs = [torch.randn(t, width, device=ex.device).to(torch.bfloat16) for t in counts]
+        outs = []
+        for ts in (1, 0):
+            ex.ctx.set_option("tma_store", ts)
+            outs.append(ex._compute_batch(pass_kind, [_env(c, 80 + 4 * pass_kind + 2 * ts, 0, O.V, pass_kind, x)
+                                                      for c, x in enumerate(xs)]))
+        for c in range(len(xs)):
+            assert torch.equal(outs[0][c], outs[1][c]), (pass_kind, c)
+    ex.ctx.set_option("tma_store", 1)
+    ex.ctx.set_option("gemm_2cta", -1)
