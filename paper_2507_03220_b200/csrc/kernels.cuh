@@ -105,7 +105,8 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int gro
 
 // Store `ncols` (<= 64) fp32 values of one row to a bf16 / f32 destination with plain global
 // stores (16-byte vectors when aligned). Used for f32 destinations, misaligned rows and y_base.
-__device__ __forceinline__ void store_row_global(const float* v, int ncols, char* dst, bool bf,
+// (All loops over the 64 values are unrolled with compile-time indices so `v` stays in registers.)
+__device__ __forceinline__ void store_row_global(const float (&v)[64], int ncols, char* dst, bool bf,
                                                  bool vec) {
   if (ncols == 64 && vec) {
     if (bf) {
@@ -120,9 +121,12 @@ __device__ __forceinline__ void store_row_global(const float* v, int ncols, char
       for (int j = 0; j < 16; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
     }
   } else {
-    for (int j = 0; j < ncols; ++j) {
-      if (bf) reinterpret_cast<__nv_bfloat16*>(dst)[j] = __float2bfloat16_rn(v[j]);
-      else reinterpret_cast<float*>(dst)[j] = v[j];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      if (j < ncols) {
+        if (bf) reinterpret_cast<__nv_bfloat16*>(dst)[j] = __float2bfloat16_rn(v[j]);
+        else reinterpret_cast<float*>(dst)[j] = v[j];
+      }
     }
   }
 }
@@ -200,7 +204,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
             v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
           }
         } else {
-          for (int j = 0; j < ncols; ++j) v[j] += __ldg(p.bias + n + j);
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < ncols) v[j] += __ldg(p.bias + n + j);
         }
       }
       if (want_base) {
@@ -217,7 +223,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
             v[4 * j] *= ll.x; v[4 * j + 1] *= ll.y; v[4 * j + 2] *= ll.z; v[4 * j + 3] *= ll.w;
           }
         } else {
-          for (int j = 0; j < ncols; ++j) v[j] *= __ldg(sg.ia3 + n + j);
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < ncols) v[j] *= __ldg(sg.ia3 + n + j);
         }
       }
       if (!tma_row) {
