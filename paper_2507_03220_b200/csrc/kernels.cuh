@@ -452,30 +452,47 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ============================================================================ K1/K2/K5, 2-CTA
-// CTA pair (cluster of 2 on one TPC), tcgen05 cta_group::2: one UMMA 256x256x16 per K step.
-// Each CTA stages its own 128 rows of A and HALF of the 256 B columns, so per SM the MMA
-// reads 4 KB + 4 KB of smem per 128-cycle K step instead of 4 KB + 8 KB (the 1-CTA kernel
-// is smem-bandwidth bound, profiles/r01_ncu_gemm_full.md). The leader CTA (rank 0) issues
-// the MMAs; both CTAs run TMA producers (completion counted on the leader's full barrier)
-// and epilogues (each drains its own TMEM lanes = its 128 rows).
+// CTA pair (cluster of 2 on one TPC), tcgen05 cta_group::2: UMMA 256 x 256 x 16 per K step and
+// 256-column group. Each CTA stages its own 128 rows of A and half of the pair's B columns, so
+// per SM the MMA reads 4 KB of A + 4 KB of B per 128-cycle UMMA (the 1-CTA kernel is
+// smem-bandwidth bound, profiles/r01_ncu_gemm_full.md). The leader CTA (rank 0) issues the
+// MMAs; both CTAs run TMA producers (bytes counted on the leader's full barrier) and epilogues
+// (each drains its own 128 TMEM lanes).
+//   PN = 256: pair tile 256 x 256, double-buffered TMEM accumulator (epilogue overlaps MMA).
+//   PN = 512: pair tile 256 x 512 (two UMMAs per K step into TMEM columns 0-255 / 256-511),
+//             one 512-column accumulator; 25 % fewer operand bytes per FLOP from L2.
+// B columns are interleaved between the CTAs in 128-column groups (group g of CTA c covers
+// pair columns g*256 + c*128 .. +128), so each UMMA's N=256 output maps linearly onto TMEM.
 constexpr int BM2 = 256;                        // rows per pair tile
-constexpr int STAGES2 = 6;
-constexpr int B_HALF_BYTES = (BN / 2) * BK * 2;  // 16 KB
-constexpr int STAGE2_BYTES = A_STAGE_BYTES + B_HALF_BYTES;
-constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + EPI_SMEM + 1024 + 256;
 
-template <bool kBwd>
+template <int PN>
+struct PairCfg {
+  static constexpr int G = PN / 256;            // 256-column UMMA groups per K step
+  static constexpr int NACC = PN == 256 ? 2 : 1;
+  static constexpr int B_BYTES = (PN / 2) * BK * 2;   // this CTA's B slice per stage
+  static constexpr int STAGE = A_STAGE_BYTES + B_BYTES;
+  static constexpr int STAGES_ = PN == 256 ? 6 : 4;
+  static constexpr int SMEM = STAGES_ * STAGE + EPI_SMEM + 1024 + 256;
+};
+constexpr int GEMM2_SMEM = PairCfg<256>::SMEM;
+constexpr int GEMM2W_SMEM = PairCfg<512>::SMEM;
+
+template <bool kBwd, int PN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     seg_gemm2_kernel(const __grid_constant__ CUtensorMap tmB,   // W: fwd box {64,64}; bwd {64,128}
                      const __grid_constant__ CUtensorMap tmAL,  // A_lora [M, R_w], box {64,128}
                      const __grid_constant__ CUtensorMap tmBP,  // pack [R, N], box {64,16}
                      const GemmParams p) {
+  using Cfg = PairCfg<PN>;
+  constexpr int STAGES2 = Cfg::STAGES_;
+  constexpr int G = Cfg::G;
+  constexpr int NACC = Cfg::NACC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES2 * A_STAGE_BYTES;
-  uint8_t* epi_stage = smem + STAGES2 * STAGE2_BYTES;  // 2 x 16 KB TMA-store staging
+  uint8_t* epi_stage = smem + STAGES2 * Cfg::STAGE;  // 2 x 16 KB TMA-store staging
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_stage + EPI_SMEM);
   uint64_t* empty_bar = full_bar + STAGES2;
   uint64_t* tfull_bar = empty_bar + STAGES2;
@@ -529,20 +546,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const CUtensorMap* tmA = p.tmaps + td.amap;
         const int arow = td.arow + crank * BM;
         tensormap_acquire(tmA);
-        const int m0 = mb * BM2 + crank * BM;        // row of this CTA's half in A_lora
-        const int nh = nb * BN + crank * (BN / 2);  // this CTA's half of the N columns
+        const int m0 = mb * BM2 + crank * BM;       // row of this CTA's half in A_lora
+        const int nh = nb * PN + crank * 128;      // first column of this CTA's group 0
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           const uint32_t fb = full0 + s * 8;
-          if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE2_BYTES);
+          if (leader) mbar_expect_tx(&full_bar[s], 2 * Cfg::STAGE);
           tma_load_2d_2sm(smA + s * A_STAGE_BYTES, tmA, fb, kb * BK, arow);
-          uint8_t* b = smB + s * B_HALF_BYTES;
-          if (kBwd) {
-            tma_load_2d_2sm(b, &tmB, fb, kb * BK, nh);
-          } else {
+          uint8_t* b = smB + s * Cfg::B_BYTES;
 #pragma unroll
-            for (int j = 0; j < BN / 128; ++j)
-              tma_load_2d_2sm(b + j * (BK * 128), &tmB, fb, nh + 64 * j, kb * BK);
+          for (int g = 0; g < G; ++g) {
+            if (kBwd) {
+              tma_load_2d_2sm(b + g * 16384, &tmB, fb, kb * BK, nh + g * 256);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                tma_load_2d_2sm(b + g * 16384 + j * (BK * 128), &tmB, fb, nh + g * 256 + 64 * j, kb * BK);
+            }
           }
           if (++s == STAGES2) { s = 0; ph ^= 1; }
         }
@@ -554,14 +574,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             mbar_wait(&empty_bar[s], ph ^ 1);
             const uint32_t fb = full0 + s * 8;
             if (leader)
-              mbar_expect_tx(&full_bar[s], 2 * (A_STAGE_BYTES + nq * (BN / 128) * LORA_CHUNK_BYTES));
+              mbar_expect_tx(&full_bar[s], 2 * (A_STAGE_BYTES + nq * G * 2 * LORA_CHUNK_BYTES));
             tma_load_2d_2sm(smA + s * A_STAGE_BYTES, &tmAL, fb, ls * BK, m0);
-            uint8_t* b = smB + s * B_HALF_BYTES;
+            uint8_t* b = smB + s * Cfg::B_BYTES;
             for (int q = 0; q < nq; ++q) {
               const int prow = p.chunks[cb + ls * 4 + q];
 #pragma unroll
-              for (int j = 0; j < BN / 128; ++j)
-                tma_load_2d_2sm(b + j * (BK * 128) + q * LORA_CHUNK_BYTES, &tmBP, fb, nh + 64 * j, prow);
+              for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                  tma_load_2d_2sm(b + g * 16384 + j * (BK * 128) + q * LORA_CHUNK_BYTES, &tmBP, fb,
+                                  nh + g * 256 + 64 * j, prow);
             }
             if (++s == STAGES2) { s = 0; ph ^= 1; }
           }
@@ -571,8 +594,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader only)
     if (leader) {
-      constexpr uint32_t idesc_base = make_idesc_bf16(BM2, BN, false, !kBwd);
-      constexpr uint32_t idesc_lora = make_idesc_bf16(BM2, BN, false, true);
+      constexpr uint32_t idesc_base = make_idesc_bf16(BM2, 256, false, !kBwd);
+      constexpr uint32_t idesc_lora = make_idesc_bf16(BM2, 256, false, true);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -582,19 +605,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
         mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * 256;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full_bar[s], ph);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a_addr = smem_u32(smA + s * A_STAGE_BYTES);
-            const uint32_t b_addr = smem_u32(smB + s * B_HALF_BYTES);
+            const uint32_t b_addr = smem_u32(smB + s * Cfg::B_BYTES);
 #pragma unroll
             for (int k = 0; k < BK / UK; ++k) {
               const uint64_t ad = make_sdesc_sw128(a_addr + k * 32, 16, 1024);
-              const uint64_t bd = kBwd ? make_sdesc_sw128(b_addr + k * 32, 16, 1024)
-                                       : make_sdesc_sw128(b_addr + k * (UK * 128), BK * 128, 1024);
-              mma_bf16_ss_2sm(d_tmem, ad, bd, idesc_base, (kb | k) != 0);
+#pragma unroll
+              for (int g = 0; g < G; ++g) {
+                const uint32_t bg = b_addr + g * 16384;
+                const uint64_t bd = kBwd ? make_sdesc_sw128(bg + k * 32, 16, 1024)
+                                         : make_sdesc_sw128(bg + k * (UK * 128), BK * 128, 1024);
+                mma_bf16_ss_2sm(d_tmem + g * 256, ad, bd, idesc_base, (kb | k) != 0);
+              }
             }
             mma_commit_2sm_mc(&empty_bar[s], 0x3);
           }
@@ -609,11 +636,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             tc_fence_after();
             if (lane == 0) {
               const uint32_t a_addr = smem_u32(smA + s * A_STAGE_BYTES);
-              const uint32_t b_addr = smem_u32(smB + s * B_HALF_BYTES);
+              const uint32_t b_addr = smem_u32(smB + s * Cfg::B_BYTES);
               for (int q = 0; q < nq; ++q)
-                mma_bf16_ss_2sm(d_tmem, make_sdesc_sw128(a_addr + q * 32, 16, 1024),
-                                make_sdesc_sw128(b_addr + q * LORA_CHUNK_BYTES, BK * 128, 1024),
-                                idesc_lora, 1u);
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                  mma_bf16_ss_2sm(d_tmem + g * 256, make_sdesc_sw128(a_addr + q * 32, 16, 1024),
+                                  make_sdesc_sw128(b_addr + g * 16384 + q * LORA_CHUNK_BYTES, BK * 128, 1024),
+                                  idesc_lora, 1u);
               mma_commit_2sm_mc(&empty_bar[s], 0x3);
             }
             __syncwarp();
@@ -622,7 +651,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         }
         if (lane == 0) mma_commit_2sm_mc(&tfull_bar[acc], 0x3);
         __syncwarp();
-        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+        if (++acc == NACC) { acc = 0; acc_ph ^= 1; }
       }
     }
   } else if (warp >= 4) {
@@ -635,9 +664,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       int mb, nb;
       tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
       const TileDesc td = p.tiles[mb];
-      epilogue_tile<BN>(p, tmem_base + acc * BN, ew, lane, td, crank * BM, nb * BN, &tfull_bar[acc],
+      epilogue_tile<PN>(p, tmem_base + acc * 256, ew, lane, td, crank * BM, nb * PN, &tfull_bar[acc],
                         acc_ph, epi_stage, tempty0 + acc * 8);
-      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      if (++acc == NACC) { acc = 0; acc_ph ^= 1; }
     }
     if (ew == 0 && lane == 0) bulk_wait_all();
   }

@@ -97,6 +97,7 @@ struct ss_ctx {
   int direct_tiles = 1;  // 1: TMA-load whole tiles of bf16 segments in place (no gather)
   int force_tbn = 0;     // testing: force the single-CTA tile width (64 / 128 / 256)
   int tma_store = 1;     // 1: bf16 outputs leave through swizzled smem + TMA bulk stores
+  int pair_n = 256;      // CTA-pair tile width: 256 (double-buffered TMEM) or 512
   int64_t weight_bytes = 0, adapter_bytes = 0;
   // in-stream profiling
   bool profiling = false;
@@ -310,10 +311,14 @@ int set_kernel_attrs(ss_ctx* ctx) {
                           TileCfg<64>::SMEM));
   CK(cudaFuncSetAttribute(seg_gemm_kernel<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           TileCfg<64>::SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(seg_gemm2_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           GEMM2_SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(seg_gemm2_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           GEMM2_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm2_kernel<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          GEMM2W_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm2_kernel<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          GEMM2W_SMEM));
   CK(cudaFuncSetAttribute(lora_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           SHRINK_SMEM));
   g_attrs.done = true;
@@ -408,6 +413,11 @@ int ss_ctx_destroy(ss_ctx* ctx) {
 
 int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!ctx || !key) return SS_E_ARG;
+  if (!strcmp(key, "pair_n")) {
+    if (value != 256 && value != 512) return fail(ctx, SS_E_ARG, "pair_n must be 256 or 512");
+    ctx->pair_n = (int)value;
+    return SS_OK;
+  }
   if (!strcmp(key, "tma_store")) {
     ctx->tma_store = value ? 1 : 0;
     return SS_OK;
@@ -922,7 +932,8 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   gpm.N = N;
   gpm.K = K;
   gpm.num_m_tiles = num_m;
-  gpm.num_n_tiles = (N + tbn - 1) / tbn;
+  const int pn = ctx->pair_n;               // CTA-pair tile width (256 or 512)
+  gpm.num_n_tiles = pair ? (N + pn - 1) / pn : (N + tbn - 1) / tbn;
   gpm.group_m = ctx->group_m;
   gpm.has_bias = (pass_kind == SS_PASS_FORWARD && L.bias) ? 1 : 0;
   gpm.any_lora = any_lora ? 1 : 0;
@@ -946,11 +957,16 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     if (d.flags & SEGF_LORA) gf += 2.0 * d.rows * d.rank_pad * N;
   }
   const int pg = prof_begin(ctx, stream, SS_KERNEL_GEMM, gf, gb);
-  if (pair) {
+  if (pair && pn == 512) {
     if (bwd)
-      seg_gemm2_kernel<true><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
+      seg_gemm2_kernel<true, 512><<<grid, GEMM_THREADS, GEMM2W_SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
     else
-      seg_gemm2_kernel<false><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
+      seg_gemm2_kernel<false, 512><<<grid, GEMM_THREADS, GEMM2W_SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
+  } else if (pair) {
+    if (bwd)
+      seg_gemm2_kernel<true, 256><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
+    else
+      seg_gemm2_kernel<false, 256><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
   } else if (tbn == 256) {
     if (bwd) seg_gemm_kernel<true, 256><<<grid, GEMM_THREADS, TileCfg<256>::SMEM, stream>>>(L.tm_w_bwd, tmAL, tmBP, gpm);
     else seg_gemm_kernel<false, 256><<<grid, GEMM_THREADS, TileCfg<256>::SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);

@@ -15,6 +15,8 @@ ctx = ctypes.c_void_p()
 L.check(None, lib.ss_ctx_create(0, 0, 1, ctypes.byref(ctx)))
 L.check(ctx, lib.ss_set_option(ctx, b"gemm_2cta", mode))
 L.check(ctx, lib.ss_set_option(ctx, b"group_m", gm))
+import os
+L.check(ctx, lib.ss_set_option(ctx, b"pair_n", int(os.environ.get("SS_PAIR_N", "256"))))
 dev = torch.device("cuda:0")
 W = torch.randn(K, N, device=dev, dtype=torch.bfloat16)
 L.check(ctx, lib.ss_load_layer(ctx, 0, 4, K, N, W.data_ptr(), N, None, L.SS_MEM_DEVICE | L.SS_DT_BF16))
