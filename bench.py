@@ -429,6 +429,9 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=1)
+    ap.add_argument("--graph", type=int, default=1,
+                    help="1: replay the step's prebuilt dispatch plans as one CUDA graph (the kernel "
+                         "roofline is still measured on an eager, event-bracketed pass)")
     ap.add_argument("--parallel", default="replicas", choices=("replicas", "tp"),
                     help="replicas: segment-parallel full replicas (weak scaling, no data-path "
                          "collective); tp: column/row-sharded layers + NCCL per dispatch (strong)")
@@ -493,6 +496,14 @@ def main():
     for _ in range(max(3, args.warmup)):
         step_fn()
     torch.cuda.synchronize()
+    eager_step_fn = step_fn
+    graph = None
+    if args.graph and not tp_mode:
+        graph = ex.capture(plan, stream=torch.cuda.Stream(device))
+        step_fn = lambda: graph.replay()  # noqa: E731  (replays on torch's current stream)
+        for _ in range(max(3, args.warmup)):
+            step_fn()
+        torch.cuda.synchronize()
 
     samples, stop = [], threading.Event()
     sampler = threading.Thread(target=nvsmi_sampler, args=(stop, samples, local), daemon=True)
@@ -502,7 +513,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.kernel_launches()
-    ctx.profile(True)
+    if graph is None:
+        ctx.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
@@ -514,6 +526,20 @@ def main():
     stop.set()
     launches = ctx.kernel_launches() - launches0
     ms = e0.elapsed_time(e1) / args.steps
+    prof_steps = args.steps
+    if graph is not None:
+        # graph replays launch no host-side kernels: count the captured launches per step, and
+        # take the per-kernel roofline from an eager pass of the same plans, event-bracketed
+        ctx.profile(True)
+        l0 = ctx.kernel_launches()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        eager_step_fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        launches = (ctx.kernel_launches() - l0) * args.steps
+        eager_ms = ev0.elapsed_time(ev1)
+        prof_steps = 1
     gemm = ctx.profile_read(_lib.SS_KERNEL_GEMM)
     shrink = ctx.profile_read(_lib.SS_KERNEL_SHRINK)
     gather = ctx.profile_read(_lib.SS_KERNEL_GATHER)
@@ -582,12 +608,16 @@ def main():
                          "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
                          "frac": (gemm_tflops / peak) if gemm_tflops else None, "traffic": traffic,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
-                         "gemm_share_of_step": gemm["ms"] / (ms * args.steps),
+                         "gemm_share_of_step": gemm["ms"] / (ms * prof_steps),
                          "gemm_launches": gemm["launches"],
-                         "shrink_ms_per_step": shrink["ms"] / args.steps,
-                         "gather_ms_per_step": gather["ms"] / args.steps,
+                         "shrink_ms_per_step": shrink["ms"] / prof_steps,
+                         "gather_ms_per_step": gather["ms"] / prof_steps,
+                         "measured_on": ("eager event-bracketed pass of the same plans "
+                                         f"({eager_ms:.1f} ms/step eager vs {ms:.1f} graph)") if graph is not None
+                                        else "the timed steps",
                          "gather_gbs": (gather["bytes"] / (gather["ms"] / 1e3) / 1e9) if gather["ms"] else None},
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
+            "launch_mode": "CUDA graph of prebuilt dispatch plans" if graph is not None else "eager prebuilt dispatch plans",
         }
         print(json.dumps(line), flush=True)
     if world > 1 or tp_mode:

@@ -118,6 +118,72 @@ SS_API int ss_clear_client(ss_ctx* ctx, uint32_t client_id);
 SS_API int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
                      const ss_seg* segs, void* stream, int32_t* seg_status);
 
+/* Same dispatch over HOST buffers (the reference's clients hold numpy activations, and the
+ * LocalChannel reply lands in the client's SharedBuffer, transport.py:28-49, 73-98): src / dst /
+ * dst_base are host pointers (page-locked for full PCIe speed). The batch is split into row
+ * sub-batches; the H2D copy of sub-batch j+1, the kernels of j and the D2H copy of j-1 overlap
+ * on the library's copy streams and a 3-slot device staging ring. Rows are independent and the
+ * kernels never mix rows (tensor_ops.py:1-8), so the results are bitwise those of
+ * ss_compute_batch on device copies. Synchronous: the replies are in the host buffers when it
+ * returns. All segments must share one src dtype and one dst dtype. */
+SS_API int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
+                                 const ss_seg* segs, void* stream, int32_t* seg_status);
+
+/* ---- prebuilt dispatch plans ------------------------------------------------------------
+ * For clients whose exchange buffers do not move (DeviceChannel after its first grow), the
+ * routing tables of a dispatch (what ss_compute_batch rebuilds on every call: validation,
+ * M-tiles, LoRA chunk lists, tensor maps) are built once into plan-owned device memory;
+ * ss_plan_launch then only launches the kernels — a few microseconds of host time, and
+ * capturable in a CUDA graph. Same semantics and bitwise the same results as
+ * ss_compute_batch on the same segments. A plan rebuilds itself transparently when the
+ * context's workspace grew or an adapter it references moved (rank change, clear, layer
+ * reload); it fails (SS_E_ARG) if that changed a segment's status. Plans must be destroyed
+ * before their context. */
+typedef struct ss_plan ss_plan;
+SS_API int ss_plan_create(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
+                          const ss_seg* segs, int32_t* seg_status, ss_plan** out);
+SS_API int ss_plan_launch(ss_plan* plan, void* stream);
+SS_API int ss_plan_destroy(ss_plan* plan);
+
+/* ---- adapter weight gradients (the client-side half of a fine-tune step) -----------------
+ * The reference computes these in numpy on the client after every executor backward reply:
+ *   ClientModel._layer_backward   pkg/src/splitserve/client.py:286-305
+ *     IA3  grad_l += sum_rows(dy * y_base)                    client.py:291-293
+ *     LoRA lora_backward(x_saved, g, A, B, alpha, rank)       adapters.py:26-41
+ *          grad_a = s * x^T . (g . B^T),  grad_b = s * (x . A)^T . g,  s = alpha / rank
+ *     accumulated into the grads dict (client.py _accumulate).
+ * ss_adapter_grads computes them on the GPU for every listed client of one layer, using the
+ * adapter registered with ss_set_adapter (its A, B, l). Activations are DEVICE pointers:
+ * x [rows, d_in] and dy [rows, d_out] bf16 with 16-byte aligned rows for LoRA (TMA-loaded);
+ * dy / y_base bf16 or f32 for IA3. Gradients are f32 device buffers, row-major like the
+ * reference's arrays: grad_a [d_in, rank], grad_b [rank, d_out], grad_l [d_out]. Output
+ * buffers of different segments must not overlap. A client with both LoRA and IA3 on one
+ * layer is rejected (SS_SEG_UNSUPPORTED): a reference AdapterState has one method. */
+#define SS_GRADF_ACCUMULATE (1u << 0) /* += into the gradient buffers (else overwrite) */
+#define SS_GRADF_X_BF16 (1u << 1)
+#define SS_GRADF_DY_BF16 (1u << 2)
+#define SS_GRADF_BASE_BF16 (1u << 3)
+#define SS_SEG_UNSUPPORTED 5
+
+typedef struct ss_grad_seg {
+  uint32_t client_id;
+  uint32_t rows;
+  uint32_t flags;        /* SS_GRADF_* */
+  uint32_t reserved;
+  const void* x;         /* LoRA: the layer's forward input (client-saved), [rows, x_ld] */
+  int64_t x_ld;
+  const void* dy;        /* grad of the layer output, [rows, dy_ld] */
+  int64_t dy_ld;
+  const void* y_base;    /* IA3: the pre-IA3 forward output, [rows, base_ld] */
+  int64_t base_ld;
+  float* grad_a;         /* LoRA [d_in, rank] */
+  float* grad_b;         /* LoRA [rank, d_out] */
+  float* grad_l;         /* IA3  [d_out] */
+} ss_grad_seg;
+
+SS_API int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_seg* segs,
+                            void* stream, int32_t* seg_status);
+
 /* Device bytes held: weights (+bias), adapter packs, transient workspace high-water mark. */
 SS_API int ss_memory_stats(const ss_ctx* ctx, int64_t* weight_bytes, int64_t* adapter_bytes,
                     int64_t* workspace_bytes);
@@ -132,6 +198,7 @@ SS_API int64_t ss_kernel_launches(const ss_ctx* ctx);
 #define SS_KERNEL_GATHER 0
 #define SS_KERNEL_SHRINK 1
 #define SS_KERNEL_GEMM 2
+#define SS_KERNEL_GRAD 3   /* K6 + K7 (+ their K3 shrinks) of ss_adapter_grads */
 SS_API int ss_profile(ss_ctx* ctx, int enable);
 SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* launches,
                            double* flops, double* bytes);

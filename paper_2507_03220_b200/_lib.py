@@ -25,6 +25,12 @@ SS_SEG_OK = 0
 SS_SEG_BAD_WIDTH = 1
 SS_SEG_BAD_PTR = 2
 SS_SEG_NO_ADAPTER = 3
+SS_SEG_UNSUPPORTED = 5
+
+SS_GRADF_ACCUMULATE = 1 << 0
+SS_GRADF_X_BF16 = 1 << 1
+SS_GRADF_DY_BF16 = 1 << 2
+SS_GRADF_BASE_BF16 = 1 << 3
 
 SS_MEM_DEVICE = 1 << 0
 SS_DT_BF16 = 1 << 1
@@ -42,12 +48,14 @@ EXPORTED = (
     "ss_ctx_create", "ss_ctx_destroy", "ss_last_error", "ss_version", "ss_load_layer",
     "ss_unload_layer", "ss_set_adapter", "ss_clear_adapter", "ss_clear_client",
     "ss_compute_batch", "ss_memory_stats", "ss_kernel_launches", "ss_set_option",
-    "ss_profile", "ss_profile_read",
+    "ss_profile", "ss_profile_read", "ss_adapter_grads", "ss_plan_create", "ss_plan_launch",
+    "ss_plan_destroy", "ss_compute_batch_host",
 )
 
 SS_KERNEL_GATHER = 0
 SS_KERNEL_SHRINK = 1
 SS_KERNEL_GEMM = 2
+SS_KERNEL_GRAD = 3
 
 
 class SsSeg(ctypes.Structure):
@@ -62,6 +70,24 @@ class SsSeg(ctypes.Structure):
         ("dst_ld", ctypes.c_int64),
         ("dst_base", ctypes.c_void_p),
         ("base_ld", ctypes.c_int64),
+    ]
+
+
+class SsGradSeg(ctypes.Structure):
+    _fields_ = [
+        ("client_id", ctypes.c_uint32),
+        ("rows", ctypes.c_uint32),
+        ("flags", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
+        ("x", ctypes.c_void_p),
+        ("x_ld", ctypes.c_int64),
+        ("dy", ctypes.c_void_p),
+        ("dy_ld", ctypes.c_int64),
+        ("y_base", ctypes.c_void_p),
+        ("base_ld", ctypes.c_int64),
+        ("grad_a", ctypes.c_void_p),
+        ("grad_b", ctypes.c_void_p),
+        ("grad_l", ctypes.c_void_p),
     ]
 
 
@@ -102,6 +128,14 @@ def load() -> ctypes.CDLL:
             "ss_clear_client": (i32, [vp, u32]),
             "ss_compute_batch": (i32, [vp, i32, i32, i32, i32, ctypes.POINTER(SsSeg), vp,
                                        ctypes.POINTER(ctypes.c_int32)]),
+            "ss_adapter_grads": (i32, [vp, i32, i32, i32, ctypes.POINTER(SsGradSeg), vp,
+                                       ctypes.POINTER(ctypes.c_int32)]),
+            "ss_compute_batch_host": (i32, [vp, i32, i32, i32, i32, ctypes.POINTER(SsSeg), vp,
+                                            ctypes.POINTER(ctypes.c_int32)]),
+            "ss_plan_create": (i32, [vp, i32, i32, i32, i32, ctypes.POINTER(SsSeg),
+                                     ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(vp)]),
+            "ss_plan_launch": (i32, [vp, vp]),
+            "ss_plan_destroy": (i32, [vp]),
             "ss_memory_stats": (i32, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                       ctypes.POINTER(i64)]),
             "ss_kernel_launches": (i64, [vp]),

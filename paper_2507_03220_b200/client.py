@@ -88,3 +88,51 @@ def client_backward_input(layer: VirtLayer, fused: set, grad_y):
     if addr_key(layer.addr) not in fused:
         raise ValueError("client_backward_input is for executor-fused addresses")
     return layer.backward(grad_y)
+
+
+def client_layer_backward(layer: VirtLayer, fused: set, executor, client_id: int, adapter,
+                          x_saved, grad_y, grads: dict, y_base=None):
+    """``ClientModel._layer_backward`` (client.py:286-305) for an executor-fused address, with
+    the adapter weight gradients on the GPU as well.
+
+    grad_x = one fused backward dispatch (g = dy * l, g W^T, + the LoRA grad_x term); then
+    ss_adapter_grads adds grad_l = sum_rows(dy * y_base) (IA3) or grad_a / grad_b
+    (lora_backward, adapters.py:26-41) into ``grads`` under the reference's keys
+    ``(addr, "l" | "a" | "b")``, accumulating like the reference's ``_accumulate``.
+    Activations are device tensors (bf16 for LoRA's x and dy)."""
+    from .device import GradSeg
+
+    grad_x = client_backward_input(layer, fused, grad_y)
+    if adapter is None:
+        return grad_x
+    addr = layer.addr
+    key = addr_key(addr)
+    dev = grad_y.device
+    job = GradSeg(client_id=client_id, dy=grad_y)
+    lora = {addr_key(a): v for a, v in (getattr(adapter, "lora", {}) or {}).items()}
+    ia3 = {addr_key(a): v for a, v in (getattr(adapter, "ia3", {}) or {}).items()}
+
+    def slot(part, shape):
+        g = grads.get((addr, part))
+        if g is None:
+            g = torch.zeros(shape, dtype=torch.float32, device=dev)
+            grads[(addr, part)] = g
+        return g
+
+    if key in ia3:
+        if y_base is None:
+            raise ValueError(f"{addr}: IA3 backward needs the forward's y_base")
+        job.y_base = y_base
+        job.grad_l = slot("l", (layer.d_out,))
+    elif key in lora:
+        a, _ = lora[key]
+        job.x = x_saved
+        job.grad_a = slot("a", (layer.d_in, int(a.shape[1])))
+        job.grad_b = slot("b", (int(a.shape[1]), layer.d_out))
+    else:
+        return grad_x
+    job.accumulate = True
+    status = executor.adapter_grads(addr.block, int(addr.role), [job])
+    if status[0] != 0:
+        raise ProtocolError(f"{addr}: adapter gradient job rejected (status {status[0]})")
+    return grad_x

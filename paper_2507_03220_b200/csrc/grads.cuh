@@ -1,0 +1,255 @@
+// Adapter weight-gradient kernels: the client-side half of a fine-tune
+// step that the reference computes in numpy after every executor backward reply.
+//
+//   K6 lora_grad_kernel : grad_b = s * (x.A)^T . g and grad_a = s * x^T . (g.B^T)
+//                         (lora_backward, reference adapters.py:26-41). The two shrinks
+//                         s*x.A and s*g.B^T run first on lora_shrink_kernel (K3, one launch
+//                         for both) into per-segment blocks of one Q buffer; this kernel then contracts over the TOKEN axis:
+//                         D[128 rows of d_in | d_out, npad] = Src^T . Q, with Src = x (grad_a)
+//                         or g (grad_b) loaded MN-major straight from the client's rows.
+//   K7 ia3_grad_kernel  : grad_l = sum_rows dy * y_base (ClientModel._layer_backward,
+//                         reference client.py:291-293), a deterministic column reduction.
+//
+// Both are HBM-bound (each reads the client's saved activations once; LoRA: 2*r FLOP per
+// byte of x / g per contraction), so they run 2 CTAs per SM.
+#pragma once
+#include "kernels.cuh"
+
+namespace ss {
+
+struct LoraGradSeg {
+  int32_t rows;       // tokens t
+  int32_t qrow0;      // first row of this segment's block in Qx / Qg (64-aligned, zero-padded)
+  int32_t rank;
+  int32_t npad;       // UMMA N: rank rounded up to 64 (<= 256)
+  int32_t accumulate; // 1: += into grad_a / grad_b (client.py _accumulate), 0: overwrite
+  int32_t xmap;       // tensor map (box {64, 64}) over x  [t, d_in]
+  int32_t gmap;       // tensor map (box {64, 64}) over g  [t, d_out]
+  int32_t pad_;
+  float* dA;          // [d_in, rank]  row-major f32
+  float* dB;          // [rank, d_out] row-major f32
+};
+
+struct LoraGradItem {
+  int32_t seg;
+  int32_t which;      // 0: grad_a (M over d_in, Src = x, Q = s*g.B^T); 1: grad_b (M over d_out, Src = g, Q = s*x.A)
+  int32_t m0;         // first output row of d_in / d_out
+  int32_t pad_;
+};
+
+struct LoraGradParams {
+  int d_in, d_out;
+  int qrows;          // rows of the s*x.A half of Q; the s*g.B^T half follows
+  const LoraGradSeg* segs;
+  const LoraGradItem* items;
+  const CUtensorMap* tmaps;
+};
+
+constexpr int GRAD_SMEM = 110 * 1024;
+constexpr int GRAD_MAX_STAGES = 8;
+constexpr int GRAD_CHUNK_BYTES = 64 * 64 * 2;  // one {64 MN, 64 K} SW128 box = 8 KB
+
+__global__ void __launch_bounds__(GEMM_THREADS, 2)
+    lora_grad_kernel(const __grid_constant__ CUtensorMap tmQ,  // [s*x.A ; s*g.B^T] [2*qrows, qld] bf16
+                     const LoraGradParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t warp = warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  const LoraGradItem it = p.items[blockIdx.x];
+  const LoraGradSeg sg = p.segs[it.seg];
+  const int npad = sg.npad;
+  const int nq = npad / 64;
+  const CUtensorMap* tmSrc = p.tmaps + (it.which ? sg.gmap : sg.xmap);
+  const int qrow = sg.qrow0 + (it.which ? 0 : p.qrows);
+  const int b_bytes = nq * GRAD_CHUNK_BYTES;
+  const int stage_bytes = A_STAGE_BYTES + b_bytes;
+  const int NST = min(GRAD_MAX_STAGES, (GRAD_SMEM - 2048) / stage_bytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty_bar = full_bar + GRAD_MAX_STAGES;
+  uint64_t* tfull = empty_bar + GRAD_MAX_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint8_t* stage0 = smem + 1024;
+
+  if (warp == 0 && lane == 0) {
+    tensormap_acquire(tmSrc);
+    tma_prefetch_desc(tmSrc);
+    tma_prefetch_desc(&tmQ);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nkb = (sg.rows + 63) / 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        mbar_expect_tx(&full_bar[s], stage_bytes);
+        uint8_t* a = stage0 + s * stage_bytes;
+        // A = Src^T: two MN chunks of 64 output rows x 64 tokens (rows past t are zero-filled)
+        tma_load_2d(a, tmSrc, &full_bar[s], it.m0, kb * 64);
+        tma_load_2d(a + GRAD_CHUNK_BYTES, tmSrc, &full_bar[s], it.m0 + 64, kb * 64);
+        for (int q = 0; q < nq; ++q)
+          tma_load_2d(a + A_STAGE_BYTES + q * GRAD_CHUNK_BYTES, &tmQ, &full_bar[s], q * 64,
+                      qrow + kb * 64);
+        if (++s == NST) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = make_idesc_bf16(BM, (uint32_t)npad, true, true);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      mbar_wait(&full_bar[s], ph);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a_addr = smem_u32(stage0 + s * stage_bytes);
+        const uint32_t b_addr = a_addr + A_STAGE_BYTES;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_bf16_ss(tmem_base, make_sdesc_sw128(a_addr + k * (UK * 128), GRAD_CHUNK_BYTES, 1024),
+                      make_sdesc_sw128(b_addr + k * (UK * 128), GRAD_CHUNK_BYTES, 1024), idesc,
+                      (kb | k) != 0);
+        mma_commit(&empty_bar[s]);
+      }
+      __syncwarp();
+      if (++s == NST) { s = 0; ph ^= 1; }
+    }
+    if (lane == 0) mma_commit(tfull);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const uint32_t ew = warp - 4;
+    const int m = it.m0 + ew * 32 + lane;  // output row (of d_in for grad_a, of d_out for grad_b)
+    const int mdim = it.which ? p.d_out : p.d_in;
+    const bool ok = m < mdim && nkb > 0;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    for (int c = 0; c < npad / 16; ++c) {
+      if (c * 16 >= sg.rank) break;
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(tmem_base + c * 16 + ((ew * 32u) << 16), r);
+      tmem_wait_ld();
+      if (!ok) continue;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = c * 16 + j;
+        if (col < sg.rank) {
+          // grad_a[m, col] (row-major [d_in, r]); grad_b[col, m] (row-major [r, d_out]: a warp
+          // writes 32 consecutive floats per column)
+          float* o = it.which ? sg.dB + (int64_t)col * p.d_out + m : sg.dA + (int64_t)m * sg.rank + col;
+          const float v = __uint_as_float(r[j]);
+          *o = sg.accumulate ? *o + v : v;
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 256);
+  }
+}
+
+// ---------------------------------------------------------------------------- K7 IA3 grad
+struct Ia3GradSeg {
+  int32_t rows;
+  int32_t flags;        // bit0 dy bf16, bit1 y_base bf16, bit2 both 16-byte aligned rows, bit3 accumulate
+  const void* dy;
+  int64_t dy_ld;
+  const void* yb;
+  int64_t yb_ld;
+  float* dl;            // [d_out]
+};
+struct Ia3GradItem {
+  int32_t seg;
+  int32_t c0;           // first of 256 columns
+};
+struct Ia3GradParams {
+  int d_out;
+  const Ia3GradSeg* segs;
+  const Ia3GradItem* items;
+};
+
+__device__ __forceinline__ void load8(const void* base, int64_t off, bool bf, bool vec, int ncols,
+                                      float (&v)[8]) {
+  if (vec && ncols == 8) {
+    if (bf) {
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(base) + off));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+      }
+    } else {
+      const float4* f4 = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base) + off);
+      const float4 a = __ldg(f4), b = __ldg(f4 + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      v[i] = i < ncols ? (bf ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[off + i])
+                             : reinterpret_cast<const float*>(base)[off + i])
+                       : 0.f;
+  }
+}
+
+// Block = 1024 threads over 256 columns: lane group cg owns 8 columns, warp rg (of 32) strides
+// the rows by 32; the 32 partial sums per column are added in fixed order (deterministic, no
+// atomics). 32 warps per block keep enough loads in flight to stream dy / y_base from HBM.
+constexpr int IA3_THREADS = 1024;
+constexpr int IA3_RG = IA3_THREADS / 32;
+
+__global__ void __launch_bounds__(IA3_THREADS) ia3_grad_kernel(const Ia3GradParams p) {
+  __shared__ float part[IA3_RG][257];
+  const Ia3GradItem it = p.items[blockIdx.x];
+  const Ia3GradSeg sg = p.segs[it.seg];
+  const int cg = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const int c = it.c0 + cg * 8;
+  const int ncols = max(0, min(8, p.d_out - c));
+  const bool dbf = sg.flags & 1, bbf = sg.flags & 2, vec = sg.flags & 4;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (ncols > 0) {
+#pragma unroll 4
+    for (int r = rg; r < sg.rows; r += IA3_RG) {
+      float a[8], b[8];
+      load8(sg.dy, (int64_t)r * sg.dy_ld + c, dbf, vec, ncols, a);
+      load8(sg.yb, (int64_t)r * sg.yb_ld + c, bbf, vec, ncols, b);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fmaf(a[i], b[i], acc[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) part[rg][cg * 8 + i] = acc[i];
+  __syncthreads();
+  if (threadIdx.x < 256) {
+    const int col = it.c0 + threadIdx.x;
+    if (col < p.d_out) {
+      float s = 0.f;
+#pragma unroll 8
+      for (int g = 0; g < IA3_RG; ++g) s += part[g][threadIdx.x];
+      float* o = sg.dl + col;
+      *o = (sg.flags & 8) ? *o + s : s;
+    }
+  }
+}
+
+}  // namespace ss

@@ -698,11 +698,12 @@ struct ShrinkItem {
   int32_t rows;   // <= 128
   int32_t orow;   // first output row in A_lora (tile * TM + row offset within tile)
   int32_t col0;   // column of this segment's rank block in its tile
-  int32_t pad0, pad1;
+  int32_t pack;   // 0: pack map tmP, contraction K = p.K; 1: tmP2, K = p.K2 (gradient shrinks)
+  int32_t pad1;
 };
 
 struct ShrinkParams {
-  int K;
+  int K, K2;
   int lora_ld;  // A_lora row stride (elements)
   const DevSeg* segs;
   const ShrinkItem* items;
@@ -711,7 +712,8 @@ struct ShrinkParams {
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 2)
-    lora_shrink_kernel(const __grid_constant__ CUtensorMap tmP,  // pack [R, K] (K-major rows)
+    lora_shrink_kernel(const __grid_constant__ CUtensorMap tmP,   // pack [R, K] (K-major rows)
+                       const __grid_constant__ CUtensorMap tmP2,  // second pack (items with pack = 1)
                        const ShrinkParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -722,6 +724,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
   const DevSeg sg = p.segs[it.seg];
   const int npad = sg.rank_pad;  // multiple of 16, <= 256
   const CUtensorMap* tmA = p.tmaps + it.amap;
+  const CUtensorMap* tmPk = it.pack ? &tmP2 : &tmP;
+  const int Kc = it.pack ? p.K2 : p.K;
   const int b_bytes = npad * BK * 2;
   const int stage_bytes = A_STAGE_BYTES + b_bytes;
   const int SHRINK_STAGES = min(SHRINK_MAX_STAGES, (SHRINK_SMEM - 2048) / stage_bytes);
@@ -737,7 +741,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
   if (warp == 0 && lane == 0) {
     tensormap_acquire(tmA);
     tma_prefetch_desc(tmA);
-    tma_prefetch_desc(&tmP);
+    tma_prefetch_desc(tmPk);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < SHRINK_STAGES; ++s) {
@@ -752,7 +756,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int nkb = (p.K + BK - 1) / BK;
+  const int nkb = (Kc + BK - 1) / BK;
   const int nchunk = npad / LORA_CHUNK;
 
   if (warp == 0) {
@@ -764,7 +768,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
         mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nchunk * LORA_CHUNK_BYTES);
         tma_load_2d(SHRINK_A(s), tmA, &full_bar[s], kb * BK, it.arow);
         for (int q = 0; q < nchunk; ++q)
-          tma_load_2d(SHRINK_B(s) + q * LORA_CHUNK_BYTES, &tmP, &full_bar[s], kb * BK,
+          tma_load_2d(SHRINK_B(s) + q * LORA_CHUNK_BYTES, tmPk, &full_bar[s], kb * BK,
                       sg.pack_row + q * LORA_CHUNK);
         if (++s == SHRINK_STAGES) { s = 0; ph ^= 1; }
       }

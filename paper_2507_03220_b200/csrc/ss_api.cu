@@ -18,6 +18,7 @@
 
 #include "../../include/ss_b200.h"
 #include "kernels.cuh"
+#include "grads.cuh"
 
 using namespace ss;
 
@@ -86,6 +87,18 @@ struct ss_ctx {
   Staging staging[kStagingSlots];
   int slot = 0;
   cudaStream_t upload = nullptr;
+  // host-buffer dispatches (ss_compute_batch_host): copy streams + a device staging ring
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  struct HostSlot {
+    void* in = nullptr;
+    void* out = nullptr;
+    void* base = nullptr;
+    size_t in_cap = 0, out_cap = 0, base_cap = 0;
+    cudaEvent_t ev_in = nullptr, ev_comp = nullptr, ev_out = nullptr;
+    bool used = false;
+  } hslot[3];
+  int64_t pipeline_bytes = 24 << 20;  // target bytes of the wider side per sub-batch
+  int pipeline_rows = 4096;
   cudaEvent_t upload_done = nullptr, compute_done = nullptr;
   bool any_compute = false;
   int64_t launches = 0;
@@ -99,12 +112,18 @@ struct ss_ctx {
   int tma_store = 1;     // 1: bf16 outputs leave through swizzled smem + TMA bulk stores
   int pair_n = 256;      // CTA-pair tile width: 256 (double-buffered TMEM) or 512
   int64_t weight_bytes = 0, adapter_bytes = 0;
+  // Plans (ss_plan_*) cache routing tables that embed workspace and adapter pointers; these
+  // counters tell a plan to rebuild itself after the workspace grew or an adapter moved.
+  uint64_t ws_epoch = 0, ad_epoch = 0;
   // in-stream profiling
   bool profiling = false;
   std::vector<ProfRec> prof;       // pending event pairs
   std::vector<cudaEvent_t> ev_pool;
-  double prof_ms[3] = {0, 0, 0}, prof_flops[3] = {0, 0, 0}, prof_bytes[3] = {0, 0, 0};
-  int64_t prof_n[3] = {0, 0, 0};
+  double prof_ms[4] = {0, 0, 0, 0}, prof_flops[4] = {0, 0, 0, 0}, prof_bytes[4] = {0, 0, 0, 0};
+  int64_t prof_n[4] = {0, 0, 0, 0};
+  // adapter-gradient workspace: s*x.A and s*g.B^T per segment (Qx, Qg)
+  __nv_bfloat16* qx = nullptr;   // [s*x.A ; s*g.B^T]
+  size_t qx_cap = 0;
 };
 
 namespace {
@@ -241,6 +260,7 @@ int grow_packs(ss_ctx* ctx, Layer& L, int need_rows) {
 template <typename T>
 int ensure_dev(ss_ctx* ctx, T*& ptr, size_t& cap, size_t bytes) {
   if (bytes <= cap) return SS_OK;
+  ctx->ws_epoch++;
   size_t n = std::max(bytes, cap + cap / 2);
   n = round_up((int64_t)n, 1 << 20);
   if (ptr) CK(cudaFree(ptr));
@@ -267,8 +287,13 @@ cudaEvent_t pool_event(ss_ctx* ctx) {
 }
 
 // Bracket one launch: returns the index of the record (or -1 when not profiling).
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
 int prof_begin(ss_ctx* ctx, cudaStream_t st, int kind, double flops, double bytes) {
-  if (!ctx->profiling) return -1;
+  if (!ctx->profiling || capturing(st)) return -1;
   ProfRec r{pool_event(ctx), pool_event(ctx), kind, flops, bytes};
   cudaEventRecord(r.a, st);
   ctx->prof.push_back(r);
@@ -292,327 +317,44 @@ void prof_drain(ss_ctx* ctx) {
   ctx->prof.clear();
 }
 
-struct KernelAttrs {
-  bool done = false;
+// Next pinned-host + device staging slot for a dispatch's routing tables (ring of
+// kStagingSlots; a slot is reused only after the dispatch that last used it has copied it).
+int acquire_staging(ss_ctx* ctx, size_t total, Staging*& out) {
+  Staging& st = ctx->staging[ctx->slot];
+  ctx->slot = (ctx->slot + 1) % kStagingSlots;
+  if (st.pending) CK(cudaEventSynchronize(st.done));
+  if (st.cap < total) {
+    if (st.host) CK(cudaFreeHost(st.host));
+    if (st.dev) CK(cudaFree(st.dev));
+    st.host = nullptr;
+    st.dev = nullptr;
+    st.cap = 0;
+    const size_t cap = round_up((int64_t)std::max(total, (size_t)1 << 16), 1 << 16);
+    CK(cudaMallocHost(&st.host, cap));
+    CK(cudaMalloc(&st.dev, cap));
+    st.cap = cap;
+  }
+  out = &st;
+  return SS_OK;
+}
+
+// Everything ss_compute_batch derives from the segment list alone: validation (per-segment
+// status), the M-tile list (direct / packed), LoRA rank-chunk lists and shrink items, TMA-store
+// ops, tensor maps — serialised into one blob of device tables — plus the launch shapes.
+struct Built {
+  int pass_kind = 0, block = 0, role = 0, K = 0, N = 0;
+  int64_t M = 0, MX = 0, lora_ld = 64, al_rows = 0, ldx = 0;
+  bool any_lora = false, pair = false;
+  int tbn = BN, pn = 256, num_m = 0, n_piece = 0, n_items = 0;
+  size_t off_tm = 0, off_seg = 0, off_tile = 0, off_piece = 0, off_ch = 0, off_st = 0, off_it = 0;
+  std::vector<char> blob;
+  std::vector<int32_t> status;
+  double gather_bytes = 0, shrink_flops = 0, shrink_bytes = 0, gemm_flops = 0, gemm_bytes = 0;
+  uint64_t ws_epoch = 0, ad_epoch = 0;
 };
-KernelAttrs g_attrs;
 
-int set_kernel_attrs(ss_ctx* ctx) {
-  if (g_attrs.done) return SS_OK;
-  CK(cudaFuncSetAttribute(seg_gemm_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          TileCfg<256>::SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          TileCfg<256>::SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm_kernel<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          TileCfg<128>::SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm_kernel<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          TileCfg<128>::SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm_kernel<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          TileCfg<64>::SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm_kernel<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          TileCfg<64>::SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm2_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          GEMM2_SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm2_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          GEMM2_SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm2_kernel<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          GEMM2W_SMEM));
-  CK(cudaFuncSetAttribute(seg_gemm2_kernel<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          GEMM2W_SMEM));
-  CK(cudaFuncSetAttribute(lora_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          SHRINK_SMEM));
-  g_attrs.done = true;
-  return SS_OK;
-}
-
-}  // namespace
-
-// =============================================================================== C ABI
-extern "C" {
-
-const char* ss_version(void) {
-  return "ss_b200 1.0 (sm_100a tcgen05/TMEM/TMA segmented executor; CTA-pair 256x256x64 / single-CTA 128x256x64)";
-}
-
-const char* ss_last_error(const ss_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
-
-int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out) {
-  if (!out) return SS_E_ARG;
-  *out = nullptr;
-  ss_ctx* ctx = new ss_ctx();
-  ctx->device = device;
-  ctx->tp_rank = tp_rank;
-  ctx->tp_size = tp_size;
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) {
-    delete ctx;
-    return SS_E_CUDA;
-  }
-  int major = 0;
-  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
-  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (major != 10) {
-    delete ctx;
-    return SS_E_UNSUPPORTED;  // sm_100a only
-  }
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-  if (e != cudaSuccess || !fn) {
-    delete ctx;
-    return SS_E_CUDA;
-  }
-  ctx->encode = reinterpret_cast<PFN_encodeTiled_t>(fn);
-  if (cudaStreamCreateWithFlags(&ctx->upload, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->upload_done, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->compute_done, cudaEventDisableTiming) != cudaSuccess) {
-    delete ctx;
-    return SS_E_CUDA;
-  }
-  for (auto& s : ctx->staging) {
-    if (cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming) != cudaSuccess) {
-      delete ctx;
-      return SS_E_CUDA;
-    }
-  }
-  if (set_kernel_attrs(ctx) != SS_OK) {
-    delete ctx;
-    return SS_E_CUDA;
-  }
-  cudaEventRecord(ctx->upload_done, ctx->upload);
-  *out = ctx;
-  return SS_OK;
-}
-
-int ss_ctx_destroy(ss_ctx* ctx) {
-  if (!ctx) return SS_E_ARG;
-  cudaSetDevice(ctx->device);
-  cudaDeviceSynchronize();
-  for (auto& kv : ctx->layers) {
-    Layer& L = kv.second;
-    cudaFree(L.W);
-    cudaFree(L.bias);
-    cudaFree(L.at_pack);
-    cudaFree(L.b_pack);
-    for (auto& a : L.adapters) cudaFree(a.second.ia3);
-  }
-  cudaFree(ctx->X);
-  cudaFree(ctx->a_lora);
-  cudaFree(ctx->row_seg);
-  for (auto& s : ctx->staging) {
-    cudaFreeHost(s.host);
-    cudaFree(s.dev);
-    cudaEventDestroy(s.done);
-  }
-  cudaEventDestroy(ctx->upload_done);
-  cudaEventDestroy(ctx->compute_done);
-  cudaStreamDestroy(ctx->upload);
-  delete ctx;
-  return SS_OK;
-}
-
-int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
-  if (!ctx || !key) return SS_E_ARG;
-  if (!strcmp(key, "pair_n")) {
-    if (value != 256 && value != 512) return fail(ctx, SS_E_ARG, "pair_n must be 256 or 512");
-    ctx->pair_n = (int)value;
-    return SS_OK;
-  }
-  if (!strcmp(key, "tma_store")) {
-    ctx->tma_store = value ? 1 : 0;
-    return SS_OK;
-  }
-  if (!strcmp(key, "tile_n")) {
-    if (value != 0 && value != 64 && value != 128 && value != 256)
-      return fail(ctx, SS_E_ARG, "tile_n must be 0 (auto), 64, 128 or 256");
-    ctx->force_tbn = (int)value;
-    return SS_OK;
-  }
-  if (!strcmp(key, "direct_tiles")) {
-    ctx->direct_tiles = value ? 1 : 0;
-    return SS_OK;
-  }
-  if (!strcmp(key, "gemm_2cta")) {
-    ctx->gemm_2cta = value < 0 ? -1 : (value ? 1 : 0);
-    return SS_OK;
-  }
-  if (!strcmp(key, "group_m")) {
-    if (value < 1) return fail(ctx, SS_E_ARG, "group_m must be >= 1");
-    ctx->group_m = (int)value;
-    return SS_OK;
-  }
-  return fail(ctx, SS_E_ARG, "unknown option %s", key);
-}
-
-int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const void* weight,
-                  int64_t w_ld, const void* bias, uint32_t flags) {
-  if (!ctx) return SS_E_ARG;
-  if (d_in <= 0 || d_out <= 0 || !weight || w_ld < d_out)
-    return fail(ctx, SS_E_ARG, "bad layer dims d_in=%d d_out=%d ld=%lld", d_in, d_out,
-                (long long)w_ld);
-  CK(cudaSetDevice(ctx->device));
-  ss_unload_layer(ctx, block, role);
-  Layer L;
-  L.block = block;
-  L.role = role;
-  L.d_in = d_in;
-  L.d_out = d_out;
-  L.ldw = round_up(d_out, 64);
-  L.ld_at = round_up(d_in, 64);
-  L.ld_b = round_up(d_out, 64);
-  CK(cudaMalloc(&L.W, (size_t)d_in * L.ldw * 2));
-  CK(cudaMemsetAsync(L.W, 0, (size_t)d_in * L.ldw * 2, ctx->upload));
-  int rc = upload_bf16(ctx, weight, flags, d_in, d_out, w_ld, L.W, L.ldw, false);
-  if (rc) { cudaFree(L.W); return rc; }
-  if (bias) {
-    CK(cudaMalloc(&L.bias, (size_t)round_up(d_out, 64) * 4));
-    CK(cudaMemsetAsync(L.bias, 0, (size_t)round_up(d_out, 64) * 4, ctx->upload));
-    rc = upload_f32(ctx, bias, flags, d_out, L.bias);
-    if (rc) return rc;
-  }
-  rc = encode_2d(ctx, &L.tm_w_fwd, L.W, d_out, d_in, L.ldw, 64, BK);
-  if (rc) return rc;
-  rc = encode_2d(ctx, &L.tm_w_bwd, L.W, d_out, d_in, L.ldw, 64, BN);
-  if (rc) return rc;
-  rc = encode_2d(ctx, &L.tm_w_bwd2, L.W, d_out, d_in, L.ldw, 64, BN / 2);
-  if (rc) return rc;
-  rc = encode_2d(ctx, &L.tm_w_bwd64, L.W, d_out, d_in, L.ldw, 64, 64);
-  if (rc) return rc;
-  ctx->weight_bytes += (int64_t)d_in * L.ldw * 2 + (bias ? round_up(d_out, 64) * 4 : 0);
-  ctx->layers[{block, role}] = L;
-  return SS_OK;
-}
-
-int ss_unload_layer(ss_ctx* ctx, int block, int role) {
-  if (!ctx) return SS_E_ARG;
-  auto it = ctx->layers.find({block, role});
-  if (it == ctx->layers.end()) return SS_E_NOLAYER;
-  cudaDeviceSynchronize();
-  Layer& L = it->second;
-  ctx->weight_bytes -= (int64_t)L.d_in * L.ldw * 2 + (L.bias ? round_up(L.d_out, 64) * 4 : 0);
-  cudaFree(L.W);
-  cudaFree(L.bias);
-  if (L.at_pack) ctx->adapter_bytes -= (int64_t)L.pack_cap * (L.ld_at + L.ld_b) * 2;
-  cudaFree(L.at_pack);
-  cudaFree(L.b_pack);
-  for (auto& a : L.adapters) {
-    if (a.second.ia3) ctx->adapter_bytes -= (int64_t)L.d_out * 4;
-    cudaFree(a.second.ia3);
-  }
-  ctx->layers.erase(it);
-  return SS_OK;
-}
-
-int ss_set_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role, uint32_t kind, int rank,
-                   float scale, const void* A, const void* B, const void* l, uint32_t flags) {
-  if (!ctx) return SS_E_ARG;
-  auto it = ctx->layers.find({block, role});
-  if (it == ctx->layers.end())
-    return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", block, role);
-  Layer& L = it->second;
-  if (kind == 0 || (kind & ~(SS_ADAPTER_LORA | SS_ADAPTER_IA3)))
-    return fail(ctx, SS_E_ARG, "bad adapter kind %u", kind);
-  if ((kind & SS_ADAPTER_LORA) && (rank <= 0 || rank > SHRINK_MAXN || !A || !B))
-    return fail(ctx, SS_E_ARG, "LoRA needs 1 <= rank <= %d and A, B (rank=%d)", SHRINK_MAXN, rank);
-  if ((kind & SS_ADAPTER_IA3) && !l) return fail(ctx, SS_E_ARG, "IA3 needs l");
-  CK(cudaSetDevice(ctx->device));
-  int rc = upload_begin(ctx);
-  if (rc) return rc;
-  AdapterSlot& s = L.adapters[client_id];
-  if (kind & SS_ADAPTER_LORA) {
-    const int rp = (int)round_up(rank, LORA_CHUNK);
-    if (s.pack_row < 0 || s.rank_pad != rp) {
-      // new block at the end of the packs (old block, if any, is abandoned: zero cost to
-      // correctness since no segment references it any more)
-      rc = grow_packs(ctx, L, L.pack_rows + rp);
-      if (rc) return rc;
-      s.pack_row = L.pack_rows;
-      s.rank_pad = rp;
-      L.pack_rows += rp;
-    }
-    s.rank = rank;
-    s.scale = scale;
-    // zero the padding rows, then A^T rows [pack_row, pack_row + rank) and B rows
-    CK(cudaMemsetAsync(L.at_pack + (int64_t)s.pack_row * L.ld_at, 0, (size_t)rp * L.ld_at * 2,
-                       ctx->upload));
-    CK(cudaMemsetAsync(L.b_pack + (int64_t)s.pack_row * L.ld_b, 0, (size_t)rp * L.ld_b * 2,
-                       ctx->upload));
-    rc = upload_bf16(ctx, A, flags, L.d_in, rank, rank, L.at_pack + (int64_t)s.pack_row * L.ld_at,
-                     L.ld_at, /*transpose=*/true);
-    if (rc) return rc;
-    rc = upload_bf16(ctx, B, flags, rank, L.d_out, L.d_out,
-                     L.b_pack + (int64_t)s.pack_row * L.ld_b, L.ld_b, false);
-    if (rc) return rc;
-  }
-  if (kind & SS_ADAPTER_IA3) {
-    if (!s.ia3) {
-      CK(cudaMalloc(&s.ia3, (size_t)round_up(L.d_out, 64) * 4));
-      CK(cudaMemsetAsync(s.ia3, 0, (size_t)round_up(L.d_out, 64) * 4, ctx->upload));
-      ctx->adapter_bytes += (int64_t)L.d_out * 4;
-    }
-    rc = upload_f32(ctx, l, flags, L.d_out, s.ia3);
-    if (rc) return rc;
-  }
-  s.kind = kind;
-  return upload_end(ctx);
-}
-
-int ss_clear_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role) {
-  if (!ctx) return SS_E_ARG;
-  auto it = ctx->layers.find({block, role});
-  if (it == ctx->layers.end()) return SS_E_NOLAYER;
-  auto a = it->second.adapters.find(client_id);
-  if (a == it->second.adapters.end()) return SS_OK;
-  if (a->second.ia3) {
-    cudaDeviceSynchronize();
-    cudaFree(a->second.ia3);
-    ctx->adapter_bytes -= (int64_t)it->second.d_out * 4;
-  }
-  it->second.adapters.erase(a);
-  return SS_OK;
-}
-
-int ss_clear_client(ss_ctx* ctx, uint32_t client_id) {
-  if (!ctx) return SS_E_ARG;
-  for (auto& kv : ctx->layers) ss_clear_adapter(ctx, client_id, kv.first.first, kv.first.second);
-  return SS_OK;
-}
-
-int ss_memory_stats(const ss_ctx* ctx, int64_t* w, int64_t* a, int64_t* ws) {
-  if (!ctx) return SS_E_ARG;
-  if (w) *w = ctx->weight_bytes;
-  if (a) *a = ctx->adapter_bytes;
-  if (ws) *ws = (int64_t)ctx->ws_high;
-  return SS_OK;
-}
-
-int64_t ss_kernel_launches(const ss_ctx* ctx) { return ctx ? ctx->launches : -1; }
-
-int ss_profile(ss_ctx* ctx, int enable) {
-  if (!ctx) return SS_E_ARG;
-  prof_drain(ctx);
-  for (int k = 0; k < 3; ++k) {
-    ctx->prof_ms[k] = ctx->prof_flops[k] = ctx->prof_bytes[k] = 0;
-    ctx->prof_n[k] = 0;
-  }
-  ctx->profiling = enable != 0;
-  return SS_OK;
-}
-
-int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* launches, double* flops,
-                    double* bytes) {
-  if (!ctx || kernel < 0 || kernel > 2) return SS_E_ARG;
-  prof_drain(ctx);
-  if (total_ms) *total_ms = ctx->prof_ms[kernel];
-  if (launches) *launches = ctx->prof_n[kernel];
-  if (flops) *flops = ctx->prof_flops[kernel];
-  if (bytes) *bytes = ctx->prof_bytes[kernel];
-  return SS_OK;
-}
-
-int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
-                     void* stream_, int32_t* seg_status) {
-  if (!ctx) return SS_E_ARG;
+int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
+                int32_t* seg_status, Built& B) {
   if (pass_kind < 0 || pass_kind > 2) return fail(ctx, SS_E_ARG, "unknown pass %d", pass_kind);
   if (n_seg < 0 || (n_seg > 0 && (!segs || !seg_status)))
     return fail(ctx, SS_E_ARG, "bad segment array");
@@ -620,11 +362,16 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   if (lit == ctx->layers.end())
     return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", block, role);
   Layer& L = lit->second;
-  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   const bool bwd = pass_kind == SS_PASS_BACKWARD;
   const bool noise = pass_kind == SS_PASS_NOISE_EFFECT;
   const int K = bwd ? L.d_out : L.d_in;
   const int N = bwd ? L.d_in : L.d_out;
+  B = Built();
+  B.pass_kind = pass_kind;
+  B.block = block;
+  B.role = role;
+  B.K = K;
+  B.N = N;
 
   // ---- validate + build device segment records (batch order == envelope order)
   std::vector<DevSeg> ds;
@@ -680,6 +427,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     src_of.push_back(&s);
     M += s.rows;
   }
+  B.status.assign(seg_status, seg_status + n_seg);
   if (M == 0) return SS_OK;
   if (M > (int64_t)1 << 30) return fail(ctx, SS_E_ARG, "batch too large (%lld rows)", (long long)M);
   CK(cudaSetDevice(ctx->device));
@@ -774,7 +522,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     rc = ensure_dev(ctx, ctx->a_lora, ctx->al_cap, (size_t)al_rows * lora_ld * 2);
     if (rc) return rc;
   }
-  ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap);
+  ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap + ctx->qx_cap);
 
   // ---- tensor maps: [0] = X, [1 + i] = direct source i (box {64, 128} rows), then the
   // destination maps of TMA-stored segments: one over the whole segment (direct tiles) and one
@@ -832,7 +580,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     }
   }
 
-  // ---- routing tables -> pinned staging slot -> device (one async copy)
+  // ---- serialise the device tables
   const size_t off_tm = 0;
   const size_t off_seg = round_up(tmaps.size() * sizeof(CUtensorMap), 256);
   const size_t off_tile = off_seg + round_up(ds.size() * sizeof(DevSeg), 256);
@@ -841,21 +589,8 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   const size_t off_st = off_ch + round_up(std::max<size_t>(1, chunks.size()) * 4, 256);
   const size_t off_it = off_st + round_up(std::max<size_t>(1, stores.size()) * sizeof(int2), 256);
   const size_t total = off_it + round_up(std::max<size_t>(1, items.size()) * sizeof(ShrinkItem), 256);
-  Staging& st = ctx->staging[ctx->slot];
-  ctx->slot = (ctx->slot + 1) % kStagingSlots;
-  if (st.pending) CK(cudaEventSynchronize(st.done));
-  if (st.cap < total) {
-    if (st.host) CK(cudaFreeHost(st.host));
-    if (st.dev) CK(cudaFree(st.dev));
-    st.host = nullptr;
-    st.dev = nullptr;
-    st.cap = 0;
-    const size_t cap = round_up((int64_t)std::max(total, (size_t)1 << 16), 1 << 16);
-    CK(cudaMallocHost(&st.host, cap));
-    CK(cudaMalloc(&st.dev, cap));
-    st.cap = cap;
-  }
-  char* h = static_cast<char*>(st.host);
+  B.blob.assign(total, 0);
+  char* h = B.blob.data();
   memcpy(h + off_tm, tmaps.data(), tmaps.size() * sizeof(CUtensorMap));
   memcpy(h + off_seg, ds.data(), ds.size() * sizeof(DevSeg));
   memcpy(h + off_tile, tiles.data(), tiles.size() * sizeof(TileDesc));
@@ -865,34 +600,66 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     memcpy(h + off_ch, chunks.data(), chunks.size() * 4);
     memcpy(h + off_it, items.data(), items.size() * sizeof(ShrinkItem));
   }
-  // adapters uploaded on the side stream must be complete before this dispatch reads them
-  CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
-  CK(cudaMemcpyAsync(st.dev, st.host, any_lora ? total : off_it, cudaMemcpyHostToDevice, stream));
-  CK(cudaEventRecord(st.done, stream));
-  st.pending = true;
-  char* dv = static_cast<char*>(st.dev);
-  const CUtensorMap* d_tmaps = reinterpret_cast<const CUtensorMap*>(dv + off_tm);
-  const DevSeg* d_segs = reinterpret_cast<const DevSeg*>(dv + off_seg);
+  B.off_tm = off_tm; B.off_seg = off_seg; B.off_tile = off_tile; B.off_piece = off_piece;
+  B.off_ch = off_ch; B.off_st = off_st; B.off_it = off_it;
+  B.M = M; B.MX = MX; B.lora_ld = lora_ld; B.al_rows = al_rows; B.ldx = ldx;
+  B.any_lora = any_lora; B.pair = pair; B.tbn = tbn; B.pn = ctx->pair_n;
+  B.num_m = num_m; B.n_piece = (int)piece_seg.size(); B.n_items = (int)items.size();
+  // algorithmic work for the in-stream profiler
+  for (size_t k = 0; k < piece_seg.size(); ++k) {
+    const DevSeg& d = ds[piece_seg[k]];
+    B.gather_bytes += (double)(d.rows - d.xlocal0) * K * ((d.flags & SEGF_SRC_BF16) ? 2 : 4);
+  }
+  B.gather_bytes += (double)MX * K * 2 + MX * 4.0;
+  for (const ShrinkItem& it : items) {
+    const DevSeg& d = ds[it.seg];
+    B.shrink_flops += 2.0 * it.rows * d.rank_pad * K;
+    B.shrink_bytes += (double)it.rows * K * 2 + (double)d.rank_pad * K * 2 + (double)it.rows * d.rank_pad * 2;
+  }
+  // base GEMM + each LoRA segment's own rank (the block-diagonal zeros of neighbouring
+  // segments are not counted); bytes: A rows, W, outputs
+  B.gemm_flops = 2.0 * (double)M * N * K;
+  B.gemm_bytes = (double)M * K * 2 + (double)K * N * 2;
+  for (const DevSeg& d : ds) {
+    B.gemm_bytes += (double)d.rows * N * ((d.flags & SEGF_DST_BF16) ? 2 : 4);
+    if (d.flags & SEGF_WANT_BASE) B.gemm_bytes += (double)d.rows * N * ((d.flags & SEGF_BASE_BF16) ? 2 : 4);
+    if (d.flags & SEGF_LORA) B.gemm_flops += 2.0 * d.rows * d.rank_pad * N;
+  }
+  B.ws_epoch = ctx->ws_epoch;
+  B.ad_epoch = ctx->ad_epoch;
+  return SS_OK;
+}
 
+// Launch the kernels of a built batch whose tables are at device address `dv` (stream-ordered
+// after whatever copied them there).
+int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
+  auto lit = ctx->layers.find({B.block, B.role});
+  if (lit == ctx->layers.end()) return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", B.block, B.role);
+  Layer& L = lit->second;
+  CK(cudaSetDevice(ctx->device));
+  const int pass_kind = B.pass_kind;
+  const bool bwd = pass_kind == SS_PASS_BACKWARD;
+  const int K = B.K, N = B.N;
+  const int64_t MX = B.MX, lora_ld = B.lora_ld, al_rows = B.al_rows, ldx = B.ldx;
+  const bool any_lora = B.any_lora, pair = B.pair;
+  const int tbn = B.tbn, num_m = B.num_m;
+  int rc = SS_OK;
+  const CUtensorMap* d_tmaps = reinterpret_cast<const CUtensorMap*>(dv + B.off_tm);
+  const DevSeg* d_segs = reinterpret_cast<const DevSeg*>(dv + B.off_seg);
   // ---- K4 gather of the packed rows
   if (MX > 0) {
     GatherParams gp;
     gp.MX = (int)MX;
     gp.K = K;
     gp.ldx = (int)ldx;
-    gp.n_piece = (int)piece_seg.size();
+    gp.n_piece = B.n_piece;
     gp.ia3_in_prologue = bwd ? 1 : 0;
     gp.segs = d_segs;
-    gp.piece_seg = reinterpret_cast<const int32_t*>(dv + off_piece);
+    gp.piece_seg = reinterpret_cast<const int32_t*>(dv + B.off_piece);
     gp.X = ctx->X;
     gp.row_seg = ctx->row_seg;
     const int grid = (int)std::min<int64_t>((MX + 7) / 8, (int64_t)ctx->num_sms * 8);
-    double src_bytes = 0;
-    for (size_t k = 0; k < piece_seg.size(); ++k) {
-      const DevSeg& d = ds[piece_seg[k]];
-      src_bytes += (double)(d.rows - d.xlocal0) * K * ((d.flags & SEGF_SRC_BF16) ? 2 : 4);
-    }
-    const int pi = prof_begin(ctx, stream, SS_KERNEL_GATHER, 0.0, src_bytes + (double)MX * K * 2 + MX * 4.0);
+    const int pi = prof_begin(ctx, stream, SS_KERNEL_GATHER, 0.0, B.gather_bytes);
     gather_rows_kernel<<<grid, 256, 0, stream>>>(gp);
     prof_end(ctx, stream, pi);
     CK(cudaGetLastError());
@@ -909,17 +676,13 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
     sp.K = K;
     sp.lora_ld = (int)lora_ld;
     sp.segs = d_segs;
-    sp.items = reinterpret_cast<const ShrinkItem*>(dv + off_it);
+    sp.items = reinterpret_cast<const ShrinkItem*>(dv + B.off_it);
     sp.tmaps = d_tmaps;
     sp.a_lora = ctx->a_lora;
-    double sf = 0, sb = 0;
-    for (const ShrinkItem& it : items) {
-      const DevSeg& d = ds[it.seg];
-      sf += 2.0 * it.rows * d.rank_pad * K;
-      sb += (double)it.rows * K * 2 + (double)d.rank_pad * K * 2 + (double)it.rows * d.rank_pad * 2;
-    }
-    const int pi = prof_begin(ctx, stream, SS_KERNEL_SHRINK, sf, sb);
-    lora_shrink_kernel<<<(int)items.size(), GEMM_THREADS, SHRINK_SMEM, stream>>>(bwd ? L.tm_b : L.tm_at, sp);
+    const int pi = prof_begin(ctx, stream, SS_KERNEL_SHRINK, B.shrink_flops, B.shrink_bytes);
+    sp.K2 = K;
+    lora_shrink_kernel<<<B.n_items, GEMM_THREADS, SHRINK_SMEM, stream>>>(bwd ? L.tm_b : L.tm_at,
+                                                                               bwd ? L.tm_b : L.tm_at, sp);
     prof_end(ctx, stream, pi);
     CK(cudaGetLastError());
     ctx->launches++;
@@ -932,7 +695,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   gpm.N = N;
   gpm.K = K;
   gpm.num_m_tiles = num_m;
-  const int pn = ctx->pair_n;               // CTA-pair tile width (256 or 512)
+  const int pn = B.pn;                      // CTA-pair tile width (256 or 512)
   gpm.num_n_tiles = pair ? (N + pn - 1) / pn : (N + tbn - 1) / tbn;
   gpm.group_m = ctx->group_m;
   gpm.has_bias = (pass_kind == SS_PASS_FORWARD && L.bias) ? 1 : 0;
@@ -941,22 +704,14 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   gpm.bias = L.bias;
   gpm.segs = d_segs;
   gpm.row_seg = ctx->row_seg;
-  gpm.tiles = reinterpret_cast<const TileDesc*>(dv + off_tile);
-  gpm.chunks = reinterpret_cast<const int32_t*>(dv + off_ch);
+  gpm.tiles = reinterpret_cast<const TileDesc*>(dv + B.off_tile);
+  gpm.chunks = reinterpret_cast<const int32_t*>(dv + B.off_ch);
   gpm.tmaps = d_tmaps;
-  gpm.stores = reinterpret_cast<const int2*>(dv + off_st);
+  gpm.stores = reinterpret_cast<const int2*>(dv + B.off_st);
   const int ntiles = gpm.num_m_tiles * gpm.num_n_tiles;
   const int grid = pair ? 2 * std::min(ntiles, ctx->num_sms / 2) : std::min(ntiles, ctx->num_sms);
   const CUtensorMap& tmBP = any_lora ? (bwd ? L.tm_at : L.tm_b) : L.tm_w_fwd;
-  // algorithmic work: base GEMM + each LoRA segment's own rank (the block-diagonal zeros of
-  // neighbouring segments are not counted); bytes: A rows, W, outputs
-  double gf = 2.0 * (double)M * N * K, gb = (double)M * K * 2 + (double)K * N * 2;
-  for (const DevSeg& d : ds) {
-    gb += (double)d.rows * N * ((d.flags & SEGF_DST_BF16) ? 2 : 4);
-    if (d.flags & SEGF_WANT_BASE) gb += (double)d.rows * N * ((d.flags & SEGF_BASE_BF16) ? 2 : 4);
-    if (d.flags & SEGF_LORA) gf += 2.0 * d.rows * d.rank_pad * N;
-  }
-  const int pg = prof_begin(ctx, stream, SS_KERNEL_GEMM, gf, gb);
+  const int pg = prof_begin(ctx, stream, SS_KERNEL_GEMM, B.gemm_flops, B.gemm_bytes);
   if (pair && pn == 512) {
     if (bwd)
       seg_gemm2_kernel<true, 512><<<grid, GEMM_THREADS, GEMM2W_SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
@@ -982,6 +737,794 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
   ctx->launches++;
   CK(cudaEventRecord(ctx->compute_done, stream));
   ctx->any_compute = true;
+  return SS_OK;
+}
+
+
+struct KernelAttrs {
+  bool done = false;
+};
+KernelAttrs g_attrs;
+
+int set_kernel_attrs(ss_ctx* ctx) {
+  if (g_attrs.done) return SS_OK;
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<256>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<256>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<128>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<128>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<64>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_kernel<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          TileCfg<64>::SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm2_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          GEMM2_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm2_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          GEMM2_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm2_kernel<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          GEMM2W_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm2_kernel<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          GEMM2W_SMEM));
+  CK(cudaFuncSetAttribute(lora_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          SHRINK_SMEM));
+  CK(cudaFuncSetAttribute(lora_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GRAD_SMEM));
+  g_attrs.done = true;
+  return SS_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+const char* ss_version(void) {
+  return "ss_b200 1.0 (sm_100a tcgen05/TMEM/TMA segmented executor; CTA-pair 256x256x64 / single-CTA 128x256x64)";
+}
+
+const char* ss_last_error(const ss_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out) {
+  if (!out) return SS_E_ARG;
+  *out = nullptr;
+  ss_ctx* ctx = new ss_ctx();
+  ctx->device = device;
+  ctx->tp_rank = tp_rank;
+  ctx->tp_size = tp_size;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return SS_E_CUDA;
+  }
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (major != 10) {
+    delete ctx;
+    return SS_E_UNSUPPORTED;  // sm_100a only
+  }
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || !fn) {
+    delete ctx;
+    return SS_E_CUDA;
+  }
+  ctx->encode = reinterpret_cast<PFN_encodeTiled_t>(fn);
+  if (cudaStreamCreateWithFlags(&ctx->upload, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->upload_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->compute_done, cudaEventDisableTiming) != cudaSuccess) {
+    delete ctx;
+    return SS_E_CUDA;
+  }
+  if (cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return SS_E_CUDA;
+  }
+  for (auto& hs : ctx->hslot) {
+    if (cudaEventCreateWithFlags(&hs.ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&hs.ev_comp, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&hs.ev_out, cudaEventDisableTiming) != cudaSuccess) {
+      delete ctx;
+      return SS_E_CUDA;
+    }
+  }
+  for (auto& s : ctx->staging) {
+    if (cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming) != cudaSuccess) {
+      delete ctx;
+      return SS_E_CUDA;
+    }
+  }
+  if (set_kernel_attrs(ctx) != SS_OK) {
+    delete ctx;
+    return SS_E_CUDA;
+  }
+  cudaEventRecord(ctx->upload_done, ctx->upload);
+  *out = ctx;
+  return SS_OK;
+}
+
+int ss_ctx_destroy(ss_ctx* ctx) {
+  if (!ctx) return SS_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : ctx->layers) {
+    Layer& L = kv.second;
+    cudaFree(L.W);
+    cudaFree(L.bias);
+    cudaFree(L.at_pack);
+    cudaFree(L.b_pack);
+    for (auto& a : L.adapters) cudaFree(a.second.ia3);
+  }
+  cudaFree(ctx->X);
+  cudaFree(ctx->a_lora);
+  cudaFree(ctx->row_seg);
+  cudaFree(ctx->qx);
+  for (auto& s : ctx->staging) {
+    cudaFreeHost(s.host);
+    cudaFree(s.dev);
+    cudaEventDestroy(s.done);
+  }
+  cudaEventDestroy(ctx->upload_done);
+  cudaEventDestroy(ctx->compute_done);
+  cudaStreamDestroy(ctx->upload);
+  for (auto& hs : ctx->hslot) {
+    cudaFree(hs.in);
+    cudaFree(hs.out);
+    cudaFree(hs.base);
+    cudaEventDestroy(hs.ev_in);
+    cudaEventDestroy(hs.ev_comp);
+    cudaEventDestroy(hs.ev_out);
+  }
+  cudaStreamDestroy(ctx->h2d);
+  cudaStreamDestroy(ctx->d2h);
+  delete ctx;
+  return SS_OK;
+}
+
+int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
+  if (!ctx || !key) return SS_E_ARG;
+  if (!strcmp(key, "pipeline_rows")) {
+    if (value < 1) return fail(ctx, SS_E_ARG, "pipeline_rows must be >= 1");
+    ctx->pipeline_rows = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "pipeline_bytes")) {
+    if (value < 1) return fail(ctx, SS_E_ARG, "pipeline_bytes must be >= 1");
+    ctx->pipeline_bytes = value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "pair_n")) {
+    if (value != 256 && value != 512) return fail(ctx, SS_E_ARG, "pair_n must be 256 or 512");
+    ctx->pair_n = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "tma_store")) {
+    ctx->tma_store = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "tile_n")) {
+    if (value != 0 && value != 64 && value != 128 && value != 256)
+      return fail(ctx, SS_E_ARG, "tile_n must be 0 (auto), 64, 128 or 256");
+    ctx->force_tbn = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "direct_tiles")) {
+    ctx->direct_tiles = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "gemm_2cta")) {
+    ctx->gemm_2cta = value < 0 ? -1 : (value ? 1 : 0);
+    return SS_OK;
+  }
+  if (!strcmp(key, "group_m")) {
+    if (value < 1) return fail(ctx, SS_E_ARG, "group_m must be >= 1");
+    ctx->group_m = (int)value;
+    return SS_OK;
+  }
+  return fail(ctx, SS_E_ARG, "unknown option %s", key);
+}
+
+int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const void* weight,
+                  int64_t w_ld, const void* bias, uint32_t flags) {
+  if (!ctx) return SS_E_ARG;
+  if (d_in <= 0 || d_out <= 0 || !weight || w_ld < d_out)
+    return fail(ctx, SS_E_ARG, "bad layer dims d_in=%d d_out=%d ld=%lld", d_in, d_out,
+                (long long)w_ld);
+  CK(cudaSetDevice(ctx->device));
+  ss_unload_layer(ctx, block, role);
+  Layer L;
+  L.block = block;
+  L.role = role;
+  L.d_in = d_in;
+  L.d_out = d_out;
+  L.ldw = round_up(d_out, 64);
+  L.ld_at = round_up(d_in, 64);
+  L.ld_b = round_up(d_out, 64);
+  CK(cudaMalloc(&L.W, (size_t)d_in * L.ldw * 2));
+  CK(cudaMemsetAsync(L.W, 0, (size_t)d_in * L.ldw * 2, ctx->upload));
+  int rc = upload_bf16(ctx, weight, flags, d_in, d_out, w_ld, L.W, L.ldw, false);
+  if (rc) { cudaFree(L.W); return rc; }
+  if (bias) {
+    CK(cudaMalloc(&L.bias, (size_t)round_up(d_out, 64) * 4));
+    CK(cudaMemsetAsync(L.bias, 0, (size_t)round_up(d_out, 64) * 4, ctx->upload));
+    rc = upload_f32(ctx, bias, flags, d_out, L.bias);
+    if (rc) return rc;
+  }
+  rc = encode_2d(ctx, &L.tm_w_fwd, L.W, d_out, d_in, L.ldw, 64, BK);
+  if (rc) return rc;
+  rc = encode_2d(ctx, &L.tm_w_bwd, L.W, d_out, d_in, L.ldw, 64, BN);
+  if (rc) return rc;
+  rc = encode_2d(ctx, &L.tm_w_bwd2, L.W, d_out, d_in, L.ldw, 64, BN / 2);
+  if (rc) return rc;
+  rc = encode_2d(ctx, &L.tm_w_bwd64, L.W, d_out, d_in, L.ldw, 64, 64);
+  if (rc) return rc;
+  ctx->weight_bytes += (int64_t)d_in * L.ldw * 2 + (bias ? round_up(d_out, 64) * 4 : 0);
+  ctx->layers[{block, role}] = L;
+  return SS_OK;
+}
+
+int ss_unload_layer(ss_ctx* ctx, int block, int role) {
+  if (!ctx) return SS_E_ARG;
+  auto it = ctx->layers.find({block, role});
+  if (it == ctx->layers.end()) return SS_E_NOLAYER;
+  cudaDeviceSynchronize();
+  Layer& L = it->second;
+  ctx->weight_bytes -= (int64_t)L.d_in * L.ldw * 2 + (L.bias ? round_up(L.d_out, 64) * 4 : 0);
+  cudaFree(L.W);
+  cudaFree(L.bias);
+  if (L.at_pack) ctx->adapter_bytes -= (int64_t)L.pack_cap * (L.ld_at + L.ld_b) * 2;
+  cudaFree(L.at_pack);
+  cudaFree(L.b_pack);
+  for (auto& a : L.adapters) {
+    if (a.second.ia3) ctx->adapter_bytes -= (int64_t)L.d_out * 4;
+    cudaFree(a.second.ia3);
+  }
+  ctx->layers.erase(it);
+  ctx->ad_epoch++;
+  return SS_OK;
+}
+
+int ss_set_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role, uint32_t kind, int rank,
+                   float scale, const void* A, const void* B, const void* l, uint32_t flags) {
+  if (!ctx) return SS_E_ARG;
+  auto it = ctx->layers.find({block, role});
+  if (it == ctx->layers.end())
+    return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", block, role);
+  Layer& L = it->second;
+  if (kind == 0 || (kind & ~(SS_ADAPTER_LORA | SS_ADAPTER_IA3)))
+    return fail(ctx, SS_E_ARG, "bad adapter kind %u", kind);
+  if ((kind & SS_ADAPTER_LORA) && (rank <= 0 || rank > SHRINK_MAXN || !A || !B))
+    return fail(ctx, SS_E_ARG, "LoRA needs 1 <= rank <= %d and A, B (rank=%d)", SHRINK_MAXN, rank);
+  if ((kind & SS_ADAPTER_IA3) && !l) return fail(ctx, SS_E_ARG, "IA3 needs l");
+  CK(cudaSetDevice(ctx->device));
+  int rc = upload_begin(ctx);
+  if (rc) return rc;
+  AdapterSlot& s = L.adapters[client_id];
+  if (kind & SS_ADAPTER_LORA) {
+    const int rp = (int)round_up(rank, LORA_CHUNK);
+    if (s.pack_row < 0 || s.rank_pad != rp) {
+      // new block at the end of the packs (old block, if any, is abandoned: zero cost to
+      // correctness since no segment references it any more)
+      rc = grow_packs(ctx, L, L.pack_rows + rp);
+      if (rc) return rc;
+      s.pack_row = L.pack_rows;
+      ctx->ad_epoch++;
+      s.rank_pad = rp;
+      L.pack_rows += rp;
+    }
+    s.rank = rank;
+    s.scale = scale;
+    // zero the padding rows, then A^T rows [pack_row, pack_row + rank) and B rows
+    CK(cudaMemsetAsync(L.at_pack + (int64_t)s.pack_row * L.ld_at, 0, (size_t)rp * L.ld_at * 2,
+                       ctx->upload));
+    CK(cudaMemsetAsync(L.b_pack + (int64_t)s.pack_row * L.ld_b, 0, (size_t)rp * L.ld_b * 2,
+                       ctx->upload));
+    rc = upload_bf16(ctx, A, flags, L.d_in, rank, rank, L.at_pack + (int64_t)s.pack_row * L.ld_at,
+                     L.ld_at, /*transpose=*/true);
+    if (rc) return rc;
+    rc = upload_bf16(ctx, B, flags, rank, L.d_out, L.d_out,
+                     L.b_pack + (int64_t)s.pack_row * L.ld_b, L.ld_b, false);
+    if (rc) return rc;
+  }
+  if (kind & SS_ADAPTER_IA3) {
+    if (!s.ia3) {
+      ctx->ad_epoch++;
+      CK(cudaMalloc(&s.ia3, (size_t)round_up(L.d_out, 64) * 4));
+      CK(cudaMemsetAsync(s.ia3, 0, (size_t)round_up(L.d_out, 64) * 4, ctx->upload));
+      ctx->adapter_bytes += (int64_t)L.d_out * 4;
+    }
+    rc = upload_f32(ctx, l, flags, L.d_out, s.ia3);
+    if (rc) return rc;
+  }
+  s.kind = kind;
+  return upload_end(ctx);
+}
+
+int ss_clear_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role) {
+  if (!ctx) return SS_E_ARG;
+  auto it = ctx->layers.find({block, role});
+  if (it == ctx->layers.end()) return SS_E_NOLAYER;
+  auto a = it->second.adapters.find(client_id);
+  if (a == it->second.adapters.end()) return SS_OK;
+  if (a->second.ia3) {
+    cudaDeviceSynchronize();
+    cudaFree(a->second.ia3);
+    ctx->adapter_bytes -= (int64_t)it->second.d_out * 4;
+  }
+  it->second.adapters.erase(a);
+  ctx->ad_epoch++;
+  return SS_OK;
+}
+
+int ss_clear_client(ss_ctx* ctx, uint32_t client_id) {
+  if (!ctx) return SS_E_ARG;
+  for (auto& kv : ctx->layers) ss_clear_adapter(ctx, client_id, kv.first.first, kv.first.second);
+  return SS_OK;
+}
+
+int ss_memory_stats(const ss_ctx* ctx, int64_t* w, int64_t* a, int64_t* ws) {
+  if (!ctx) return SS_E_ARG;
+  if (w) *w = ctx->weight_bytes;
+  if (a) *a = ctx->adapter_bytes;
+  if (ws) *ws = (int64_t)ctx->ws_high;
+  return SS_OK;
+}
+
+int64_t ss_kernel_launches(const ss_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int ss_profile(ss_ctx* ctx, int enable) {
+  if (!ctx) return SS_E_ARG;
+  prof_drain(ctx);
+  for (int k = 0; k < 4; ++k) {
+    ctx->prof_ms[k] = ctx->prof_flops[k] = ctx->prof_bytes[k] = 0;
+    ctx->prof_n[k] = 0;
+  }
+  ctx->profiling = enable != 0;
+  return SS_OK;
+}
+
+int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* launches, double* flops,
+                    double* bytes) {
+  if (!ctx || kernel < 0 || kernel > 3) return SS_E_ARG;
+  prof_drain(ctx);
+  if (total_ms) *total_ms = ctx->prof_ms[kernel];
+  if (launches) *launches = ctx->prof_n[kernel];
+  if (flops) *flops = ctx->prof_flops[kernel];
+  if (bytes) *bytes = ctx->prof_bytes[kernel];
+  return SS_OK;
+}
+
+int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
+                     void* stream_, int32_t* seg_status) {
+  if (!ctx) return SS_E_ARG;
+  Built b;
+  int rc = build_batch(ctx, pass_kind, block, role, n_seg, segs, seg_status, b);
+  if (rc || b.M == 0) return rc;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  // routing tables -> pinned staging slot -> device (one async copy)
+  Staging* stp = nullptr;
+  if ((rc = acquire_staging(ctx, b.blob.size(), stp))) return rc;
+  memcpy(stp->host, b.blob.data(), b.blob.size());
+  // adapters uploaded on the side stream must be complete before this dispatch reads them
+  CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
+  CK(cudaMemcpyAsync(stp->dev, stp->host, b.blob.size(), cudaMemcpyHostToDevice, stream));
+  CK(cudaEventRecord(stp->done, stream));
+  stp->pending = true;
+  return launch_batch(ctx, b, static_cast<char*>(stp->dev), stream);
+}
+
+// ---- prebuilt dispatch plans --------------------------------------------------------------
+struct ss_plan {
+  ss_ctx* ctx = nullptr;
+  int pass_kind = 0, block = 0, role = 0;
+  std::vector<ss_seg> segs;
+  Built b;
+  char* dev = nullptr;
+  size_t dev_cap = 0;
+};
+
+static int plan_build(ss_plan* p, int32_t* seg_status) {
+  ss_ctx* ctx = p->ctx;
+  std::vector<int32_t> st(std::max<size_t>(1, p->segs.size()));
+  int rc = build_batch(ctx, p->pass_kind, p->block, p->role, (int)p->segs.size(), p->segs.data(),
+                       seg_status ? seg_status : st.data(), p->b);
+  if (rc) return rc;
+  if (p->b.M == 0) return SS_OK;
+  if (p->dev) CK(cudaDeviceSynchronize());  // rebuild: no launch of this plan may still read p->dev
+  if (p->dev_cap < p->b.blob.size()) {
+    if (p->dev) CK(cudaFree(p->dev));
+    p->dev = nullptr;
+    p->dev_cap = 0;
+    CK(cudaMalloc(&p->dev, p->b.blob.size()));
+    p->dev_cap = p->b.blob.size();
+  }
+  CK(cudaMemcpy(p->dev, p->b.blob.data(), p->b.blob.size(), cudaMemcpyHostToDevice));
+  return SS_OK;
+}
+
+int ss_plan_create(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
+                   int32_t* seg_status, ss_plan** out) {
+  if (!ctx || !out) return SS_E_ARG;
+  *out = nullptr;
+  if (n_seg < 0 || (n_seg > 0 && (!segs || !seg_status))) return fail(ctx, SS_E_ARG, "bad segment array");
+  CK(cudaSetDevice(ctx->device));
+  ss_plan* p = new ss_plan();
+  p->ctx = ctx;
+  p->pass_kind = pass_kind;
+  p->block = block;
+  p->role = role;
+  p->segs.assign(segs, segs + n_seg);
+  int rc = plan_build(p, seg_status);
+  if (rc) {
+    ss_plan_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return SS_OK;
+}
+
+int ss_plan_launch(ss_plan* p, void* stream_) {
+  if (!p) return SS_E_ARG;
+  ss_ctx* ctx = p->ctx;
+  if (p->b.ws_epoch != ctx->ws_epoch || p->b.ad_epoch != ctx->ad_epoch) {
+    // workspace grew or an adapter moved since the tables were built: rebuild them (a plan's
+    // segments were validated at creation; a status change now is reported as an error)
+    std::vector<int32_t> st(std::max<size_t>(1, p->segs.size()));
+    std::vector<int32_t> st0(std::max<size_t>(1, p->segs.size()));
+    for (size_t i = 0; i < p->segs.size(); ++i) st0[i] = p->b.status[i];
+    int rc = plan_build(p, st.data());
+    if (rc) return rc;
+    for (size_t i = 0; i < p->segs.size(); ++i)
+      if (st[i] != st0[i]) return fail(ctx, SS_E_ARG, "plan segment %zu status changed to %d", i, st[i]);
+  }
+  if (p->b.M == 0) return SS_OK;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  // (under CUDA-graph capture the adapter uploads must already be complete: the capture
+  // cannot wait on an event recorded outside it)
+  if (!capturing(stream)) CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
+  return launch_batch(ctx, p->b, p->dev, stream);
+}
+
+int ss_plan_destroy(ss_plan* p) {
+  if (!p) return SS_E_ARG;
+  if (p->dev) {
+    cudaDeviceSynchronize();
+    cudaFree(p->dev);
+  }
+  delete p;
+  return SS_OK;
+}
+
+int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_seg* segs,
+                     void* stream_, int32_t* seg_status) {
+  if (!ctx) return SS_E_ARG;
+  if (n_seg < 0 || (n_seg > 0 && (!segs || !seg_status))) return fail(ctx, SS_E_ARG, "bad segment array");
+  auto lit = ctx->layers.find({block, role});
+  if (lit == ctx->layers.end()) return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", block, role);
+  Layer& L = lit->second;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const int d_in = L.d_in, d_out = L.d_out;
+
+  // ---- validate; split into LoRA and IA3 work
+  std::vector<DevSeg> sh;           // shrink records (pack_row, rank_pad, scale)
+  std::vector<LoraGradSeg> lg;
+  std::vector<const ss_grad_seg*> lsrc;
+  std::vector<Ia3GradSeg> ig;
+  int64_t qrows = 0;
+  int qld = 64;
+  for (int i = 0; i < n_seg; ++i) {
+    const ss_grad_seg& s = segs[i];
+    seg_status[i] = SS_SEG_OK;
+    auto a = L.adapters.find(s.client_id);
+    if (a == L.adapters.end()) { seg_status[i] = SS_SEG_NO_ADAPTER; continue; }
+    const AdapterSlot& as = a->second;
+    if ((as.kind & SS_ADAPTER_LORA) && (as.kind & SS_ADAPTER_IA3)) { seg_status[i] = SS_SEG_UNSUPPORTED; continue; }
+    if (s.rows == 0) continue;
+    if (!s.dy || s.dy_ld < d_out) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
+    const bool acc = s.flags & SS_GRADF_ACCUMULATE;
+    if (as.kind & SS_ADAPTER_LORA) {
+      if (!s.x || s.x_ld < d_in || !s.grad_a || !s.grad_b || !(s.flags & SS_GRADF_X_BF16) ||
+          !(s.flags & SS_GRADF_DY_BF16) || !aligned16(s.x, s.x_ld, 2) || !aligned16(s.dy, s.dy_ld, 2)) {
+        seg_status[i] = SS_SEG_BAD_PTR;
+        continue;
+      }
+      DevSeg d{};
+      d.rows = (int32_t)s.rows;
+      d.pack_row = as.pack_row;
+      d.rank_pad = as.rank_pad;
+      d.lora_scale = as.scale;
+      sh.push_back(d);
+      LoraGradSeg g{};
+      g.rows = (int32_t)s.rows;
+      g.qrow0 = (int32_t)qrows;
+      g.rank = as.rank;
+      g.npad = (int32_t)round_up(as.rank, 64);
+      g.accumulate = acc ? 1 : 0;
+      g.dA = s.grad_a;
+      g.dB = s.grad_b;
+      lg.push_back(g);
+      lsrc.push_back(&s);
+      qrows += round_up(s.rows, 64);
+      qld = std::max(qld, g.npad);
+    } else {
+      if (!s.y_base || s.base_ld < d_out || !s.grad_l) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
+      Ia3GradSeg g{};
+      g.rows = (int32_t)s.rows;
+      const bool dbf = s.flags & SS_GRADF_DY_BF16, bbf = s.flags & SS_GRADF_BASE_BF16;
+      g.flags = (dbf ? 1 : 0) | (bbf ? 2 : 0) |
+                ((aligned16(s.dy, s.dy_ld, dbf ? 2 : 4) && aligned16(s.y_base, s.base_ld, bbf ? 2 : 4)) ? 4 : 0) |
+                (acc ? 8 : 0);
+      g.dy = s.dy;
+      g.dy_ld = s.dy_ld;
+      g.yb = s.y_base;
+      g.yb_ld = s.base_ld;
+      g.dl = s.grad_l;
+      ig.push_back(g);
+    }
+  }
+  if (lg.empty() && ig.empty()) return SS_OK;
+  CK(cudaSetDevice(ctx->device));
+
+  // ---- LoRA tables: tensor maps [4j + 0/1] = x / g with box {64, 128} (shrink, K-major A),
+  // [4j + 2/3] = x / g with box {64, 64} (grad kernel, MN-major A); shrink and grad items
+  std::vector<CUtensorMap> tmaps(std::max<size_t>(1, 4 * lg.size()));
+  std::vector<ShrinkItem> sitems;   // x items (pack 0 = A^T rows, K = d_in), then g items (pack 1 = B rows, K = d_out)
+  std::vector<LoraGradItem> gitems;
+  int rc = SS_OK;
+  for (size_t j = 0; j < lg.size(); ++j) {
+    const ss_grad_seg& s = *lsrc[j];
+    if ((rc = encode_2d(ctx, &tmaps[4 * j + 0], s.x, d_in, s.rows, s.x_ld, 64, BM))) return rc;
+    if ((rc = encode_2d(ctx, &tmaps[4 * j + 1], s.dy, d_out, s.rows, s.dy_ld, 64, BM))) return rc;
+    if ((rc = encode_2d(ctx, &tmaps[4 * j + 2], s.x, d_in, s.rows, s.x_ld, 64, 64))) return rc;
+    if ((rc = encode_2d(ctx, &tmaps[4 * j + 3], s.dy, d_out, s.rows, s.dy_ld, 64, 64))) return rc;
+    lg[j].xmap = (int32_t)(4 * j + 2);
+    lg[j].gmap = (int32_t)(4 * j + 3);
+    for (int r = 0; r < (int)s.rows; r += BM) {
+      const int n = std::min<int>(BM, s.rows - r);
+      sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 0), r, n, lg[j].qrow0 + r, 0, 0, 0});
+      sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 1), r, n, (int32_t)qrows + lg[j].qrow0 + r, 0, 1, 0});
+    }
+    for (int m = 0; m < d_in; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 0, m, 0});
+    for (int m = 0; m < d_out; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 1, m, 0});
+  }
+  std::vector<Ia3GradItem> iitems;
+  for (size_t j = 0; j < ig.size(); ++j)
+    for (int c = 0; c < d_out; c += 256) iitems.push_back(Ia3GradItem{(int32_t)j, c});
+
+  auto sz = [](size_t n, size_t e) { return round_up((int64_t)std::max<size_t>(1, n) * e, 256); };
+  const size_t o_tm = 0;
+  const size_t o_sh = o_tm + sz(tmaps.size(), sizeof(CUtensorMap));
+  const size_t o_lg = o_sh + sz(sh.size(), sizeof(DevSeg));
+  const size_t o_ix = o_lg + sz(lg.size(), sizeof(LoraGradSeg));
+  const size_t o_gi = o_ix + sz(sitems.size(), sizeof(ShrinkItem));
+  const size_t o_is = o_gi + sz(gitems.size(), sizeof(LoraGradItem));
+  const size_t o_ii = o_is + sz(ig.size(), sizeof(Ia3GradSeg));
+  const size_t total = o_ii + sz(iitems.size(), sizeof(Ia3GradItem));
+  Staging* stp = nullptr;
+  if ((rc = acquire_staging(ctx, total, stp))) return rc;
+  char* h = static_cast<char*>(stp->host);
+  memcpy(h + o_tm, tmaps.data(), tmaps.size() * sizeof(CUtensorMap));
+  if (!lg.empty()) {
+    memcpy(h + o_sh, sh.data(), sh.size() * sizeof(DevSeg));
+    memcpy(h + o_lg, lg.data(), lg.size() * sizeof(LoraGradSeg));
+    memcpy(h + o_ix, sitems.data(), sitems.size() * sizeof(ShrinkItem));
+    memcpy(h + o_gi, gitems.data(), gitems.size() * sizeof(LoraGradItem));
+  }
+  if (!ig.empty()) {
+    memcpy(h + o_is, ig.data(), ig.size() * sizeof(Ia3GradSeg));
+    memcpy(h + o_ii, iitems.data(), iitems.size() * sizeof(Ia3GradItem));
+  }
+  CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
+  CK(cudaMemcpyAsync(stp->dev, stp->host, total, cudaMemcpyHostToDevice, stream));
+  CK(cudaEventRecord(stp->done, stream));
+  stp->pending = true;
+  char* dv = static_cast<char*>(stp->dev);
+
+  if (!lg.empty()) {
+    const size_t qbytes = (size_t)2 * qrows * qld * 2;
+    if ((rc = ensure_dev(ctx, ctx->qx, ctx->qx_cap, qbytes))) return rc;
+    ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap + ctx->qx_cap);
+    CK(cudaMemsetAsync(ctx->qx, 0, qbytes, stream));
+    double fl = 0, by = 0;
+    for (size_t j = 0; j < lg.size(); ++j) {
+      const double t = lg[j].rows, r = lg[j].rank;
+      fl += 2.0 * 2.0 * t * r * (d_in + d_out);  // two shrinks + two token contractions
+      by += t * (d_in + d_out) * 2.0 + r * (d_in + d_out) * (4.0 + 2.0);
+    }
+    const int pi = prof_begin(ctx, stream, SS_KERNEL_GRAD, fl, by);
+    // K3 (one launch): Q[0, qrows) = s * x.A (pack A^T rows, K = d_in),
+    //                  Q[qrows, 2 qrows) = s * g.B^T (pack B rows, K = d_out)
+    ShrinkParams sp;
+    sp.lora_ld = qld;
+    sp.segs = reinterpret_cast<const DevSeg*>(dv + o_sh);
+    sp.tmaps = reinterpret_cast<const CUtensorMap*>(dv + o_tm);
+    sp.K = d_in;
+    sp.K2 = d_out;
+    sp.items = reinterpret_cast<const ShrinkItem*>(dv + o_ix);
+    sp.a_lora = ctx->qx;
+    lora_shrink_kernel<<<(int)sitems.size(), GEMM_THREADS, SHRINK_SMEM, stream>>>(L.tm_at, L.tm_b, sp);
+    CK(cudaGetLastError());
+    // K6: token contractions
+    CUtensorMap tmQ;
+    if ((rc = encode_2d(ctx, &tmQ, ctx->qx, qld, 2 * qrows, qld, 64, 64))) return rc;
+    LoraGradParams gp;
+    gp.d_in = d_in;
+    gp.d_out = d_out;
+    gp.qrows = (int)qrows;
+    gp.segs = reinterpret_cast<const LoraGradSeg*>(dv + o_lg);
+    gp.items = reinterpret_cast<const LoraGradItem*>(dv + o_gi);
+    gp.tmaps = reinterpret_cast<const CUtensorMap*>(dv + o_tm);
+    lora_grad_kernel<<<(int)gitems.size(), GEMM_THREADS, GRAD_SMEM, stream>>>(tmQ, gp);
+    CK(cudaGetLastError());
+    prof_end(ctx, stream, pi);
+    ctx->launches += 2;
+  }
+  if (!ig.empty()) {
+    double by = 0;
+    for (const Ia3GradSeg& g : ig) by += (double)g.rows * d_out * (((g.flags & 1) ? 2 : 4) + ((g.flags & 2) ? 2 : 4)) + d_out * 4.0;
+    const int pi = prof_begin(ctx, stream, SS_KERNEL_GRAD, 2.0 * by / 4, by);
+    Ia3GradParams ip;
+    ip.d_out = d_out;
+    ip.segs = reinterpret_cast<const Ia3GradSeg*>(dv + o_is);
+    ip.items = reinterpret_cast<const Ia3GradItem*>(dv + o_ii);
+    ia3_grad_kernel<<<(int)iitems.size(), IA3_THREADS, 0, stream>>>(ip);
+    CK(cudaGetLastError());
+    prof_end(ctx, stream, pi);
+    ctx->launches += 1;
+  }
+  CK(cudaEventRecord(ctx->compute_done, stream));
+  ctx->any_compute = true;
+  return SS_OK;
+}
+
+// ---- host-buffer dispatch ---------------------------------------------------------------
+int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
+                          void* stream_, int32_t* seg_status) {
+  if (!ctx) return SS_E_ARG;
+  if (pass_kind < 0 || pass_kind > 2) return fail(ctx, SS_E_ARG, "unknown pass %d", pass_kind);
+  if (n_seg < 0 || (n_seg > 0 && (!segs || !seg_status))) return fail(ctx, SS_E_ARG, "bad segment array");
+  auto lit = ctx->layers.find({block, role});
+  if (lit == ctx->layers.end()) return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", block, role);
+  const Layer& L = lit->second;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const bool bwd = pass_kind == SS_PASS_BACKWARD;
+  const int K = bwd ? L.d_out : L.d_in;
+  const int N = bwd ? L.d_in : L.d_out;
+  CK(cudaSetDevice(ctx->device));
+
+  // ---- validate (the same per-segment checks as build_batch, so statuses agree)
+  std::vector<int> good;
+  int64_t rows_total = 0;
+  size_t esz_in = 2, esz_out = 2, esz_base = 2;
+  bool any_base = false;
+  for (int i = 0; i < n_seg; ++i) {
+    const ss_seg& s = segs[i];
+    seg_status[i] = SS_SEG_OK;
+    if ((int)s.width != K) { seg_status[i] = SS_SEG_BAD_WIDTH; continue; }
+    if (s.rows == 0) continue;
+    if (!s.src || !s.dst || s.src_ld < K || s.dst_ld < N) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
+    if ((s.flags & SS_SEGF_ADAPTER) && pass_kind != SS_PASS_NOISE_EFFECT &&
+        L.adapters.find(s.client_id) == L.adapters.end()) { seg_status[i] = SS_SEG_NO_ADAPTER; continue; }
+    if (s.dst_base && pass_kind == SS_PASS_FORWARD && s.base_ld < N) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
+    good.push_back(i);
+    rows_total += s.rows;
+  }
+  if (good.empty()) return SS_OK;
+  // one dtype per side for the staging ring (the kernels take bf16 / f32 per segment, but the
+  // ring's slot sizes are per dispatch)
+  esz_in = (segs[good[0]].flags & SS_SEGF_SRC_BF16) ? 2 : 4;
+  esz_out = (segs[good[0]].flags & SS_SEGF_DST_BF16) ? 2 : 4;
+  for (int i : good) {
+    const ss_seg& s = segs[i];
+    if (((s.flags & SS_SEGF_SRC_BF16) ? 2u : 4u) != esz_in || ((s.flags & SS_SEGF_DST_BF16) ? 2u : 4u) != esz_out)
+      return fail(ctx, SS_E_ARG, "host dispatch: all segments must share src / dst dtypes");
+    if (s.dst_base && pass_kind == SS_PASS_FORWARD) {
+      any_base = true;
+      esz_base = (s.flags & SS_SEGF_BASE_BF16) ? 2 : 4;
+    }
+  }
+
+  // ---- sub-batches of whole rows: the H2D of j+1, the kernels of j and the D2H of j-1 overlap
+  const int64_t wide = std::max<int64_t>(K * esz_in, N * esz_out);
+  const int64_t target = std::max<int64_t>(64, std::min<int64_t>(ctx->pipeline_rows, ctx->pipeline_bytes / wide));
+  struct Piece { int seg; int64_t r0, r1; };
+  std::vector<std::vector<Piece>> chunks(1);
+  int64_t cur = 0;
+  for (int i : good) {
+    const int64_t t = segs[i].rows;
+    int64_t r = 0;
+    while (r < t) {
+      const int64_t take = std::min(t - r, target - cur);
+      chunks.back().push_back(Piece{i, r, r + take});
+      cur += take;
+      r += take;
+      if (cur >= target) {
+        chunks.emplace_back();
+        cur = 0;
+      }
+    }
+  }
+  if (chunks.back().empty()) chunks.pop_back();
+  int rc = SS_OK;
+  const size_t in_need = (size_t)target * K * esz_in, out_need = (size_t)target * N * esz_out;
+  const size_t base_need = any_base ? (size_t)target * N * esz_base : 0;
+  for (auto& hs : ctx->hslot) {
+    if (hs.in_cap < in_need || hs.out_cap < out_need || hs.base_cap < base_need) {
+      if (hs.used) CK(cudaEventSynchronize(hs.ev_out));
+      if (hs.in_cap < in_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.in), hs.in_cap, in_need))) return rc;
+      if (hs.out_cap < out_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.out), hs.out_cap, out_need))) return rc;
+      if (hs.base_cap < base_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.base), hs.base_cap, base_need))) return rc;
+    }
+  }
+  ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap + ctx->qx_cap +
+                                            3 * (ctx->hslot[0].in_cap + ctx->hslot[0].out_cap + ctx->hslot[0].base_cap));
+
+  std::vector<ss_seg> cs;
+  std::vector<int32_t> cst;
+  for (size_t j = 0; j < chunks.size(); ++j) {
+    auto& hs = ctx->hslot[j % 3];
+    const auto& ch = chunks[j];
+    // H2D: the slot's previous kernels must have consumed its input buffer
+    if (hs.used) CK(cudaStreamWaitEvent(ctx->h2d, hs.ev_comp, 0));
+    int64_t pos = 0;
+    cs.clear();
+    for (const Piece& p : ch) {
+      const ss_seg& s = segs[p.seg];
+      const int64_t n = p.r1 - p.r0;
+      char* din = static_cast<char*>(hs.in) + pos * K * esz_in;
+      CK(cudaMemcpy2DAsync(din, (size_t)K * esz_in, static_cast<const char*>(s.src) + p.r0 * s.src_ld * esz_in,
+                           (size_t)s.src_ld * esz_in, (size_t)K * esz_in, (size_t)n, cudaMemcpyHostToDevice, ctx->h2d));
+      ss_seg d = s;
+      d.rows = (uint32_t)n;
+      d.src = din;
+      d.src_ld = K;
+      d.dst = static_cast<char*>(hs.out) + pos * N * esz_out;
+      d.dst_ld = N;
+      if (s.dst_base && pass_kind == SS_PASS_FORWARD) {
+        d.dst_base = static_cast<char*>(hs.base) + pos * N * esz_base;
+        d.base_ld = N;
+      } else {
+        d.dst_base = nullptr;
+        d.base_ld = 0;
+      }
+      cs.push_back(d);
+      pos += n;
+    }
+    CK(cudaEventRecord(hs.ev_in, ctx->h2d));
+    // kernels: after the input landed and the slot's previous outputs were drained
+    CK(cudaStreamWaitEvent(stream, hs.ev_in, 0));
+    if (hs.used) CK(cudaStreamWaitEvent(stream, hs.ev_out, 0));
+    cst.assign(cs.size(), 0);
+    if ((rc = ss_compute_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), stream, cst.data()))) return rc;
+    for (size_t k = 0; k < cs.size(); ++k)
+      if (cst[k] != SS_SEG_OK) seg_status[ch[k].seg] = cst[k];
+    CK(cudaEventRecord(hs.ev_comp, stream));
+    // D2H
+    CK(cudaStreamWaitEvent(ctx->d2h, hs.ev_comp, 0));
+    pos = 0;
+    for (const Piece& p : ch) {
+      const ss_seg& s = segs[p.seg];
+      const int64_t n = p.r1 - p.r0;
+      if (seg_status[p.seg] == SS_SEG_OK) {
+        CK(cudaMemcpy2DAsync(static_cast<char*>(s.dst) + p.r0 * s.dst_ld * esz_out, (size_t)s.dst_ld * esz_out,
+                             static_cast<const char*>(hs.out) + pos * N * esz_out, (size_t)N * esz_out,
+                             (size_t)N * esz_out, (size_t)n, cudaMemcpyDeviceToHost, ctx->d2h));
+        if (s.dst_base && pass_kind == SS_PASS_FORWARD)
+          CK(cudaMemcpy2DAsync(static_cast<char*>(s.dst_base) + p.r0 * s.base_ld * esz_base,
+                               (size_t)s.base_ld * esz_base, static_cast<const char*>(hs.base) + pos * N * esz_base,
+                               (size_t)N * esz_base, (size_t)N * esz_base, (size_t)n, cudaMemcpyDeviceToHost, ctx->d2h));
+      }
+      pos += n;
+    }
+    CK(cudaEventRecord(hs.ev_out, ctx->d2h));
+    hs.used = true;
+  }
+  // results are in the caller's host buffers when this returns (serve_* is synchronous)
+  CK(cudaStreamSynchronize(ctx->d2h));
   return SS_OK;
 }
 

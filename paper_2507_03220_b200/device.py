@@ -103,6 +103,96 @@ def fill_seg(c: SsSeg, s: Seg) -> None:
     c.flags = flags
 
 
+class Plan:
+    """A prebuilt dispatch (ss_plan_*): routing tables live on the device; ``launch`` only
+    launches kernels (CUDA-graph capturable). Keeps its segment tensors alive."""
+
+    def __init__(self, ctx: "SsContext", pass_kind: int, block: int, role: int, segs: Sequence[Seg]):
+        self.ctx, self.pass_kind, self.key = ctx, int(pass_kind), (int(block), int(role))
+        table = SegmentTable(segs)
+        self._table = table
+        h = ctypes.c_void_p()
+        check(ctx.h, ctx.lib.ss_plan_create(ctx.h, self.pass_kind, self.key[0], self.key[1], table.n,
+                                            table.arr, table.status, ctypes.byref(h)))
+        self.h = h
+        self.status = table.statuses()
+        ctx._plans.add(self)
+
+    def launch(self, stream: torch.cuda.Stream | None = None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream(self.ctx.device)
+        check(self.ctx.h, self.ctx.lib.ss_plan_launch(self.h, ctypes.c_void_p(s.cuda_stream)))
+
+    def destroy(self) -> None:
+        if getattr(self, "h", None):
+            self.ctx.lib.ss_plan_destroy(self.h)
+            self.h = None
+            self.ctx._plans.discard(self)
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+@dataclass
+class GradSeg:
+    """One client's adapter-gradient job for one layer (ss_adapter_grads): device tensors.
+
+    LoRA: ``x`` (the layer's forward input, bf16) and ``dy`` (bf16) -> ``grad_a`` [d_in, r],
+    ``grad_b`` [r, d_out] (f32). IA3: ``dy`` and ``y_base`` -> ``grad_l`` [d_out] (f32).
+    ``accumulate`` adds into the gradient tensors like the reference's ``_accumulate``."""
+
+    client_id: int
+    dy: torch.Tensor
+    x: torch.Tensor | None = None
+    y_base: torch.Tensor | None = None
+    grad_a: torch.Tensor | None = None
+    grad_b: torch.Tensor | None = None
+    grad_l: torch.Tensor | None = None
+    accumulate: bool = False
+
+
+def _ld(t: torch.Tensor) -> int:
+    return t.stride(0) if t.shape[0] > 1 else max(t.stride(0), t.shape[1])
+
+
+def _f32_out(t: torch.Tensor | None, name: str):
+    if t is None:
+        return None
+    if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+    return t.data_ptr()
+
+
+def fill_grad_seg(c, g: GradSeg) -> None:
+    for t in (g.dy, g.x, g.y_base):
+        if t is not None and (t.dim() != 2 or t.stride(1) != 1 or not t.is_cuda):
+            raise ValueError("gradient-job activations must be 2-d CUDA tensors with unit column stride")
+    c.client_id = int(g.client_id)
+    c.rows = int(g.dy.shape[0])
+    flags = _lib.SS_GRADF_ACCUMULATE if g.accumulate else 0
+    if tensor_flags(g.dy):
+        flags |= _lib.SS_GRADF_DY_BF16
+    c.dy, c.dy_ld = g.dy.data_ptr(), _ld(g.dy)
+    if g.x is not None:
+        if tensor_flags(g.x):
+            flags |= _lib.SS_GRADF_X_BF16
+        c.x, c.x_ld = g.x.data_ptr(), _ld(g.x)
+    else:
+        c.x, c.x_ld = None, 0
+    if g.y_base is not None:
+        if tensor_flags(g.y_base):
+            flags |= _lib.SS_GRADF_BASE_BF16
+        c.y_base, c.base_ld = g.y_base.data_ptr(), _ld(g.y_base)
+    else:
+        c.y_base, c.base_ld = None, 0
+    c.grad_a = _f32_out(g.grad_a, "grad_a")
+    c.grad_b = _f32_out(g.grad_b, "grad_b")
+    c.grad_l = _f32_out(g.grad_l, "grad_l")
+    c.flags = flags
+
+
 class SsContext:
     def __init__(self, device: int | torch.device = 0, tp_rank: int = 0, tp_size: int = 1):
         self.lib = _lib.load()
@@ -118,6 +208,8 @@ class SsContext:
                                    "(needs an sm_100 GPU)")
         self.h = h
         self.dims: dict[tuple[int, int], tuple[int, int]] = {}
+        import weakref
+        self._plans = weakref.WeakSet()
 
     # -- weights --------------------------------------------------------------------------
     def load_layer(self, block: int, role: int, weight, bias=None) -> None:
@@ -195,6 +287,33 @@ class SsContext:
                                        table.arr, ctypes.c_void_p(s.cuda_stream), table.status)
         check(self.h, rc)
 
+    def compute_host(self, pass_kind: int, block: int, role: int, segs: Sequence[Seg],
+                     stream: torch.cuda.Stream | None = None) -> list[int]:
+        """One dispatch over HOST (pinned) tensors: ss_compute_batch_host pipelines the H2D
+        copies, kernels and D2H copies natively and returns when the replies are in place."""
+        table = SegmentTable(segs)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(self.h, self.lib.ss_compute_batch_host(self.h, int(pass_kind), int(block), int(role), table.n,
+                                                     table.arr, ctypes.c_void_p(s.cuda_stream), table.status))
+        return table.statuses()
+
+    def plan(self, pass_kind: int, block: int, role: int, segs: Sequence[Seg]) -> "Plan":
+        """Prebuild a dispatch over fixed device buffers (ss_plan_create)."""
+        return Plan(self, pass_kind, block, role, segs)
+
+    def adapter_grads(self, block: int, role: int, jobs: Sequence[GradSeg],
+                      stream: torch.cuda.Stream | None = None) -> list[int]:
+        """LoRA / IA3 weight gradients of one layer for every job (ss_adapter_grads)."""
+        n = len(jobs)
+        arr = (_lib.SsGradSeg * max(1, n))()
+        status = (ctypes.c_int32 * max(1, n))()
+        for i, g in enumerate(jobs):
+            fill_grad_seg(arr[i], g)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(self.h, self.lib.ss_adapter_grads(self.h, int(block), int(role), n, arr,
+                                                ctypes.c_void_p(s.cuda_stream), status))
+        return [int(status[i]) for i in range(n)]
+
     # -- introspection --------------------------------------------------------------------
     def memory_stats(self) -> tuple[int, int, int]:
         w, a, ws = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
@@ -221,6 +340,8 @@ class SsContext:
     def close(self) -> None:
         if getattr(self, "h", None):
             torch.cuda.synchronize(self.device)
+            for p in list(self._plans):
+                p.destroy()
             self.lib.ss_ctx_destroy(self.h)
             self.h = None
 

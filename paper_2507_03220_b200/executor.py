@@ -107,22 +107,22 @@ class _LayerShape:
 
 
 class Dispatch:
-    """A prebuilt dispatch over fixed device buffers (one ss_compute_batch per ``run``).
+    """A prebuilt dispatch over fixed device buffers: one ss_plan (routing tables built once,
+    resident on the device), so each ``run`` is a kernel launch sequence with no table work.
 
     For device-resident clients whose exchange buffers do not move (DeviceChannel after its
-    first grow), the segment table is built once; each step is one C-ABI call."""
+    first grow). ``run`` is capturable in a CUDA graph (``GpuBaseExecutor.capture``)."""
 
     def __init__(self, ctx: SsContext, pass_kind: int, key, segs):
-        from .device import SegmentTable
         self.ctx, self.pass_kind, self.key = ctx, pass_kind, key
-        self.table = SegmentTable(segs)
+        self.plan = ctx.plan(pass_kind, key[0], key[1], segs)
         self.rows = sum(int(s.src.shape[0]) for s in segs)
-
-    def run(self, stream: torch.cuda.Stream | None = None) -> None:
-        self.ctx.compute_table(self.pass_kind, self.key[0], self.key[1], self.table, stream)
-        bad = [s for s in self.table.statuses() if s != _lib.SS_SEG_OK]
+        bad = [s for s in self.plan.status if s != _lib.SS_SEG_OK]
         if bad:
             raise ProtocolError(f"dispatch {self.key} pass {self.pass_kind}: segment status {bad}")
+
+    def run(self, stream: torch.cuda.Stream | None = None) -> None:
+        self.plan.launch(stream)
 
 
 def _is_device(x) -> bool:
@@ -265,6 +265,31 @@ class GpuBaseExecutor:
                 for c, src, dst, base in segments]
         return Dispatch(self.ctx, pass_kind, key, segs)
 
+    def capture(self, dispatches, stream: torch.cuda.Stream | None = None) -> torch.cuda.CUDAGraph:
+        """Capture a sequence of prebuilt dispatches into one CUDA graph (replay = one launch
+        for the whole sequence). Runs them once eagerly first so every plan's workspace is at
+        its high-water mark; adapters must not be re-registered between capture and replay
+        with a different rank (refreshing values in place is fine: the graph reads the packs)."""
+        s = stream if stream is not None else torch.cuda.Stream(self.device)
+        with torch.cuda.device(self.device):
+            for d in dispatches:
+                d.run(s)
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for d in dispatches:
+                    d.run(s)
+        return g
+
+    def adapter_grads(self, block: int, role: int, jobs, stream: torch.cuda.Stream | None = None) -> list:
+        """LoRA / IA3 weight gradients of one layer on the GPU (ss_adapter_grads) for the
+        client-side half of ``_layer_backward`` (client.py:286-305): ``jobs`` is a list of
+        ``device.GradSeg``. Returns one status per job (0 = computed)."""
+        key = (int(block), int(role))
+        if key not in self._dims:
+            raise ProtocolError(f"unknown layer {key}")
+        return self.ctx.adapter_grads(key[0], key[1], jobs, stream)
+
     def _sync_ledger(self) -> None:
         w, a, _ = self.ctx.memory_stats()
         self.ledger.set(ledger_mod.WEIGHTS, w)
@@ -387,7 +412,6 @@ class GpuBaseExecutor:
     # -- pipelined host path ----------------------------------------------------------------
     pipeline_rows = 4096          # max rows per sub-batch of a host-payload dispatch
     pipeline_bytes = 24 << 20     # target bytes of the wider side per sub-batch
-    pipeline_slots = 3            # staging ring depth (H2D / compute / D2H in flight)
 
     def _all_pinned_host(self, envelopes, good, out_w) -> bool:
         if self.save_activations:
@@ -404,83 +428,21 @@ class GpuBaseExecutor:
         return True
 
     def _pipelined_host(self, pass_kind, key, envelopes, good, out_w, stream) -> list[int]:
-        """Host clients (pinned payload + pinned reply buffer): the dispatch runs as row
-        sub-batches so the H2D copy of sub-batch j+1 and the D2H copy of j-1 overlap the GEMM
-        of j (two copy streams, a 3-slot device staging ring). Rows are independent and the
-        kernels never mix rows (tensor_ops.py:1-8), so results are bitwise those of one batch."""
-        if not hasattr(self, "_copy_streams"):
-            self._copy_streams = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
-        s_in, s_out = self._copy_streams
-        in_w = envelopes[good[0]].width
-        esz = envelopes[good[0]].payload.element_size()
-        # sub-batch size by bytes of the wider side, so fill / drain stay ~0.3 ms per dispatch
-        target = max(256, min(self.pipeline_rows, self.pipeline_bytes // (max(in_w, out_w) * esz)))
-        chunks, cur, rows = [], [], 0      # chunk = [(envelope index, row0, row1)]
-        for i in good:
-            t = envelopes[i].token_count
-            r = 0
-            while r < t or (t == 0 and r == 0):
-                take = min(t - r, target - rows)
-                cur.append((i, r, r + take))
-                rows += take
-                r += take
-                if rows >= target:
-                    chunks.append(cur)
-                    cur, rows = [], 0
-                if t == 0:
-                    break
-        if cur:
-            chunks.append(cur)
-        nslot = self.pipeline_slots
+        """Host clients (pinned payload + pinned reply buffer): one ss_compute_batch_host call.
+        The library splits the dispatch into row sub-batches so the H2D copy of sub-batch j+1
+        and the D2H copy of j-1 overlap the kernels of j (its own copy streams and device
+        staging ring). Rows are independent and the kernels never mix rows (tensor_ops.py:1-8),
+        so results are bitwise those of one device-resident batch."""
+        self.ctx.set_option("pipeline_rows", int(self.pipeline_rows))
+        self.ctx.set_option("pipeline_bytes", int(self.pipeline_bytes))
         fused = self._fused
-        ev_c, ev_out = [], []
-        bad: dict[int, int] = {}
-        for j, ch in enumerate(chunks):
-            slot = j % nslot
-            dt = envelopes[ch[0][0]].payload.dtype
-            n_rows = sum(r1 - r0 for _, r0, r1 in ch)
-            with torch.cuda.stream(s_in):
-                if j >= nslot:
-                    s_in.wait_event(ev_c[j - nslot])       # slot's previous GEMM has consumed it
-                dev_in = self._dev_buf(f"pin{slot}", n_rows * in_w, dt)
-                srcs, pos = [], 0
-                for i, r0, r1 in ch:
-                    n = (r1 - r0) * in_w
-                    v = dev_in[pos:pos + n].view(r1 - r0, in_w)
-                    v.copy_(envelopes[i].payload[r0:r1], non_blocking=True)
-                    srcs.append(v)
-                    pos += n
-                e_in = torch.cuda.Event()
-                e_in.record(s_in)
-            stream.wait_event(e_in)
-            if j >= nslot:
-                stream.wait_event(ev_out[j - nslot])      # slot's previous D2H has drained it
-            dev_out = self._dev_buf(f"pout{slot}", n_rows * out_w, dt)
-            segs, pos = [], 0
-            for (i, r0, r1), src in zip(ch, srcs):
-                env = envelopes[i]
-                n = (r1 - r0) * out_w
-                dst = dev_out[pos:pos + n].view(r1 - r0, out_w)
-                pos += n
-                segs.append(Seg(client_id=env.client_id, src=src, dst=dst, width=in_w,
-                                adapter=pass_kind != PASS_NOISE_EFFECT and key in fused.get(env.client_id, ())))
-            st = self.ctx.compute(pass_kind, key[0], key[1], segs, stream)
-            for (i, _, _), s in zip(ch, st):
-                if s != _lib.SS_SEG_OK:
-                    bad[i] = s
-            e_c = torch.cuda.Event()
-            e_c.record(stream)
-            ev_c.append(e_c)
-            s_out.wait_event(e_c)
-            with torch.cuda.stream(s_out):
-                for (i, r0, r1), sg in zip(ch, segs):
-                    envelopes[i].reply_to[r0:r1].copy_(sg.dst, non_blocking=True)
-                e_o = torch.cuda.Event()
-                e_o.record(s_out)
-                ev_out.append(e_o)
-        ev_out[-1].synchronize()
-        self.last_event = ev_out[-1]
-        return [bad.get(i, _lib.SS_SEG_OK) for i in good]
+        in_w = envelopes[good[0]].width
+        segs = [Seg(client_id=envelopes[i].client_id, src=envelopes[i].payload, dst=envelopes[i].reply_to,
+                    width=in_w, adapter=pass_kind != PASS_NOISE_EFFECT and key in fused.get(envelopes[i].client_id, ()))
+                for i in good]
+        status = self.ctx.compute_host(pass_kind, key[0], key[1], segs, stream)
+        self.last_event = None
+        return status
 
     # -- staging helpers --------------------------------------------------------------------
     def _stage_inputs(self, envelopes, good, stream):

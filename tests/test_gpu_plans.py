@@ -1,0 +1,114 @@
+"""Prebuilt dispatch plans (ss_plan_*) and CUDA-graph capture of a plan sequence: same kernels,
+same tables, so every result must be BITWISE the per-call ss_compute_batch result."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import splitserve_oracle as O
+
+from .test_gpu_parity import _Adapter, _addr, _env, _ex, _mixed_clients
+
+pytestmark = pytest.mark.gpu
+
+
+def _buffers(ex, counts, width_in, width_out, dtype=torch.bfloat16, seed=0):
+    g = torch.Generator(device=ex.device).manual_seed(seed)
+    xs = [torch.randn(t, width_in, generator=g, device=ex.device).to(dtype) for t in counts]
+    ys = [torch.empty(t, width_out, dtype=dtype, device=ex.device) for t in counts]
+    return xs, ys
+
+
+@pytest.mark.parametrize("shape", [(384, 640), (5120, 1536)])
+def test_plan_launch_bitwise_equals_compute_batch(shape):
+    d_in, d_out = shape
+    w, b = O.layer_params(21, 0, O.K, d_in, d_out)
+    ex = _ex({(0, O.K): (w, b)})
+    _, counts = _mixed_clients(ex, d_in, d_out, seed=21)
+    counts[2] = 1024   # a whole-tile client (direct TMA tiles) next to ragged ones
+    for pass_kind, (wi, wo) in ((0, (d_in, d_out)), (1, (d_out, d_in))):
+        xs, ys = _buffers(ex, counts, wi, wo, seed=pass_kind)
+        ref = ex._compute_batch(pass_kind, [_env(c, 10 + pass_kind, 0, O.K, pass_kind, x) for c, x in enumerate(xs)])
+        d = ex.compile_dispatch(pass_kind, 0, O.K, [(c, x, y, None) for c, (x, y) in enumerate(zip(xs, ys))])
+        for _ in range(2):       # relaunch: tables are reused, result unchanged
+            d.run()
+            torch.cuda.synchronize()
+            for c in range(len(xs)):
+                assert torch.equal(ys[c], ref[c]), (pass_kind, c)
+
+
+def test_plan_rebuilds_after_workspace_growth_and_rank_change():
+    d_in, d_out = 512, 768
+    w, b = O.layer_params(22, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)})
+    ad = O.lora_params(22, 0, 0, O.V, d_in, d_out, 8, 16.0)
+    ex.register_adapter(0, _Adapter(lora={_addr(0, O.V): (ad.a, ad.b)}, alpha=16.0, rank=8))
+    xs, ys = _buffers(ex, [37, 5], d_in, d_out)
+    d = ex.compile_dispatch(0, 0, O.V, [(0, xs[0], ys[0], None), (1, xs[1], ys[1], None)])
+    d.run()
+    # a much larger dispatch grows the shared workspace (X / LoRA operand are reallocated)
+    big = [torch.randn(3000, d_in, device=ex.device).to(torch.bfloat16) for _ in range(3)]
+    ex._compute_batch(0, [_env(c, 5, 0, O.V, 0, x) for c, x in enumerate(big)])
+    d.run()
+    torch.cuda.synchronize()
+    ref = ex._compute_batch(0, [_env(0, 6, 0, O.V, 0, xs[0]), _env(1, 6, 0, O.V, 0, xs[1])])
+    assert torch.equal(ys[0], ref[0]) and torch.equal(ys[1], ref[1])
+    # rank change moves the client's pack block: the plan must pick up the new adapter
+    ad2 = O.lora_params(23, 0, 0, O.V, d_in, d_out, 32, 64.0)
+    ex.register_adapter(0, _Adapter(lora={_addr(0, O.V): (ad2.a, ad2.b)}, alpha=64.0, rank=32))
+    d.run()
+    torch.cuda.synchronize()
+    ref = ex._compute_batch(0, [_env(0, 7, 0, O.V, 0, xs[0])])
+    assert torch.equal(ys[0], ref[0])
+    wr = O.bf16_round(w)
+    x0 = xs[0].float().cpu().numpy()
+    oracle = O.apply_adapter(O.OracleAdapter(a=O.bf16_round(ad2.a), b=O.bf16_round(ad2.b), alpha=64.0, rank=32),
+                             x0, O.affine_forward(x0, wr, b))
+    mx, mn = O.normwise_errors(ys[0].float().cpu().numpy(), oracle)
+    assert mx <= O.TOL_MAX_REL and mn <= O.TOL_MEAN_REL
+
+
+def test_cuda_graph_of_plans_bitwise_equals_eager():
+    """A whole executor step (forward over several layers, then backward in reverse) captured in
+    one CUDA graph gives the eager results bitwise, and replays deterministically."""
+    layers = {}
+    dims = {O.Q: (256, 256), O.FF_UP: (256, 512), O.FF_DOWN: (512, 256)}
+    for role, (di, do) in dims.items():
+        layers[(0, role)] = O.layer_params(24, 0, role, di, do)
+    ex = _ex(layers)
+    rng = np.random.default_rng(24)
+    for cid, r in enumerate((8, 16, 64)):
+        lo = {}
+        for role, (di, do) in dims.items():
+            ad = O.lora_params(24, cid, 0, role, di, do, r, 2.0 * r)
+            lo[_addr(0, role)] = (ad.a, ad.b)
+        ex.register_adapter(cid, _Adapter(lora=lo, alpha=2.0 * r, rank=r))
+    counts = [int(t) for t in rng.integers(1, 400, size=4)]
+    bufs = [torch.randn(t * 512, device=ex.device).to(torch.bfloat16) for t in counts]
+    outs = [torch.empty(t * 512, device=ex.device, dtype=torch.bfloat16) for t in counts]
+    plan = []
+    order = [O.Q, O.FF_UP, O.FF_DOWN]
+    for role in order:
+        di, do = dims[role]
+        plan.append(ex.compile_dispatch(0, 0, role, [(c, bufs[c][: t * di].view(t, di), outs[c][: t * do].view(t, do), None)
+                                                     for c, t in enumerate(counts)]))
+    for role in reversed(order):
+        di, do = dims[role]
+        plan.append(ex.compile_dispatch(1, 0, role, [(c, bufs[c][: t * do].view(t, do), outs[c][: t * di].view(t, di), None)
+                                                     for c, t in enumerate(counts)]))
+    # eager reference: each dispatch alone, snapshot its outputs
+    eager = []
+    for d in plan:
+        d.run()
+        torch.cuda.synchronize()
+        eager.append([o.clone() for o in outs])
+    g = ex.capture(plan)
+    for _ in range(2):
+        for o in outs:
+            o.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        # outputs of the last dispatch (and of every earlier one whose columns it did not
+        # overwrite) match the eager sequence
+        for c in range(len(counts)):
+            assert torch.equal(outs[c], eager[-1][c]), c

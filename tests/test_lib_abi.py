@@ -33,6 +33,9 @@ def test_struct_layout_matches_header():
     # 4 x u32 + (ptr, i64) x 3 = 16 + 48 bytes, natural alignment
     assert ctypes.sizeof(_lib.SsSeg) == 64
     assert _lib.SsSeg.src.offset == 16 and _lib.SsSeg.dst_base.offset == 48
+    # ss_grad_seg: 4 x u32 + (ptr, i64) x 3 + 3 ptrs
+    assert ctypes.sizeof(_lib.SsGradSeg) == 88
+    assert _lib.SsGradSeg.x.offset == 16 and _lib.SsGradSeg.grad_a.offset == 64
 
 
 def test_context_creation_fails_cleanly_without_gpu():
