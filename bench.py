@@ -48,6 +48,9 @@ WORKLOADS = {
     # BASELINE configs[1]
     "7b": dict(name="llama2-7b-shape, 8 LoRA r16 fine-tune clients, 2x512 tok",
                d=4096, d_ff=11008, L=32, V=32000, clients=8, tokens=1024, seq=512, batch=2),
+    # BASELINE configs[4]: adapter-count sweep with --clients {8,16,32,64}
+    "granite20b": dict(name="granite-20b-shape, N LoRA r8 fine-tune clients, 1x2048 tok",
+                       d=6144, d_ff=24576, L=52, V=49152, clients=64, tokens=2048, seq=2048, batch=1),
 }
 Q, K, V, O, FF_UP, FF_DOWN, LM_HEAD = range(7)
 
@@ -56,6 +59,8 @@ def client_specs(wl_key: str, n: int):
     """[(kind, rank, finetune)] per client."""
     if wl_key == "7b":
         return [("lora", 16, True) for _ in range(n)]
+    if wl_key == "granite20b":
+        return [("lora", 8, True) for _ in range(n)]
     specs = []
     for c in range(n):
         if c < 24:
@@ -188,6 +193,26 @@ def build_gpu_workload(wl_key, device, rank):
         if segs:
             bwd.append(ex.compile_dispatch(1, b, r, segs))
     bwd.reverse()
+    # adapter weight gradients of the fine-tune clients (ss_adapter_grads), per layer in backward
+    # order: LoRA grad_a / grad_b from the layer input x and dy, IA3 grad_l from dy and y_base
+    from paper_2507_03220_b200.device import GradSeg
+    grads = []
+    for (b, r) in reversed(layers):
+        di, do = dims[r]
+        jobs = []
+        for c, (kind, rank_, ft) in enumerate(specs):
+            if not ft:
+                continue
+            if kind == "lora" and r in (Q, K, V, O):
+                jobs.append(GradSeg(c, dy=bufs[c][: t * do].view(t, do), x=bufs[c][: t * di].view(t, di),
+                                    grad_a=torch.zeros(di, rank_, device=device),
+                                    grad_b=torch.zeros(rank_, do, device=device), accumulate=True))
+            elif kind == "ia3" and r in (K, V, FF_UP):
+                jobs.append(GradSeg(c, dy=bufs[c][: t * do].view(t, do), y_base=base_bufs[c][: t * do].view(t, do),
+                                    grad_l=torch.zeros(do, device=device), accumulate=True))
+        if jobs:
+            grads.append((b, r, jobs))
+    ex._bench_grads = grads
     return ex, fwd + bwd, specs, wl
 
 
@@ -424,6 +449,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="13b", choices=sorted(WORKLOADS))
+    ap.add_argument("--clients", type=int, default=0, help="override the workload's client count")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--skip-e2e", action="store_true")
@@ -440,6 +466,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.clients:
+        WORKLOADS[args.workload] = dict(WORKLOADS[args.workload], clients=args.clients)
     wl = WORKLOADS[args.workload]
     specs = client_specs(args.workload, wl["clients"])
     tokens_per_rank = wl["clients"] * wl["tokens"]
@@ -544,6 +572,31 @@ def main():
     shrink = ctx.profile_read(_lib.SS_KERNEL_SHRINK)
     gather = ctx.profile_read(_lib.SS_KERNEL_GATHER)
     ctx.profile(False)
+
+    # adapter weight-gradient leg (fine-tune clients' grad_a / grad_b / grad_l, every layer)
+    grads_leg = None
+    if not tp_mode and getattr(ex, "_bench_grads", None):
+        def grads_pass():
+            for b, r, jobs in ex._bench_grads:
+                ex.adapter_grads(b, r, jobs, stream)
+        for _ in range(2):
+            grads_pass()
+        torch.cuda.synchronize()
+        ctx.profile(True)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            grads_pass()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gk = ctx.profile_read(_lib.SS_KERNEL_GRAD)
+        ctx.profile(False)
+        g_ms = g0.elapsed_time(g1) / args.steps
+        grads_leg = {"ms_per_step": g_ms, "kernel_ms_per_step": gk["ms"] / args.steps,
+                     "launches_per_step": gk["launches"] / args.steps,
+                     "alg_bytes_per_step": gk["bytes"] / args.steps,
+                     "achieved_gbs": gk["bytes"] / (gk["ms"] / 1e3) / 1e9 if gk["ms"] else None,
+                     "ft_step_tokens_per_s": None}
     if world > 1:
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -568,6 +621,15 @@ def main():
             traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
+
+    if grads_leg is not None:
+        hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+        grads_leg["hbm_peak_gbs"] = hbm_peak
+        grads_leg["hbm_peak_source"] = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"
+        if grads_leg["achieved_gbs"]:
+            grads_leg["frac"] = grads_leg["achieved_gbs"] / hbm_peak
+        # the whole fine-tune step: executor fwd + bwd plus every FT client's adapter gradients
+        grads_leg["ft_step_tokens_per_s"] = tokens / ((ms + grads_leg["ms_per_step"]) / 1e3)
 
     e2e = None
     if not args.skip_e2e and not tp_mode:
@@ -616,6 +678,7 @@ def main():
                                          f"({eager_ms:.1f} ms/step eager vs {ms:.1f} graph)") if graph is not None
                                         else "the timed steps",
                          "gather_gbs": (gather["bytes"] / (gather["ms"] / 1e3) / 1e9) if gather["ms"] else None},
+            "adapter_grads": grads_leg,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
             "launch_mode": "CUDA graph of prebuilt dispatch plans" if graph is not None else "eager prebuilt dispatch plans",
         }

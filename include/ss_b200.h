@@ -67,7 +67,10 @@ extern "C" {
 #define SS_SEGF_SRC_BF16 (1u << 0)  /* src rows are bf16 (else f32) */
 #define SS_SEGF_DST_BF16 (1u << 1)  /* dst rows are bf16 (else f32) */
 #define SS_SEGF_BASE_BF16 (1u << 2) /* dst_base rows are bf16 (else f32) */
-#define SS_SEGF_ADAPTER (1u << 3)   /* apply this client's registered adapter for the layer */
+#define SS_SEGF_ADAPTER (1u << 3)   /* apply this client's registered adapter for the layer; on
+                                       SS_PASS_NOISE_EFFECT: the noise effect of the adapted layer,
+                                       (n.W + s n.A.B) * l, bias-free (privacy.py:1-12 blinding
+                                       with an executor-fused adapter) */
 
 /* One request (envelope) of a batch, in batch order. Rows are concatenated in array order
  * exactly like concat_rows(); row r of segment i is batch row off_i + r, off_i = sum_{j<i} rows_j
@@ -82,7 +85,7 @@ typedef struct ss_seg {
   void* dst;         /* device, [rows, dst_ld]; may alias src (in-place exchange buffer) */
   int64_t dst_ld;
   void* dst_base;    /* optional pre-IA3 output (IA3 fine-tune clients need y_base,
-                        client.py:241-242, 293); NULL if not wanted */
+                        client.py:241-242, 293), forward and noise passes; NULL if not wanted */
   int64_t base_ld;
 } ss_seg;
 
@@ -122,7 +125,7 @@ SS_API int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int
  * LocalChannel reply lands in the client's SharedBuffer, transport.py:28-49, 73-98): src / dst /
  * dst_base are host pointers (page-locked for full PCIe speed). The batch is split into row
  * sub-batches; the H2D copy of sub-batch j+1, the kernels of j and the D2H copy of j-1 overlap
- * on the library's copy streams and a 3-slot device staging ring. Rows are independent and the
+ * on the library's copy streams and a 4-slot device staging ring. Rows are independent and the
  * kernels never mix rows (tensor_ops.py:1-8), so the results are bitwise those of
  * ss_compute_batch on device copies. Synchronous: the replies are in the host buffers when it
  * returns. All segments must share one src dtype and one dst dtype. */

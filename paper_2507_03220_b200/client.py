@@ -23,24 +23,35 @@ from .protocol import PASS_BACKWARD, PASS_FORWARD
 
 
 class VirtLayer:
+    """Client-side stand-in for one frozen layer (client.py:48-98). With ``noise`` (a
+    ``privacy.DeviceNoiseSet``, or the reference's NoiseSet for numpy clients) forward payloads
+    are blinded and replies de-noised (privacy.py:1-12); for executor-fused adapters the
+    effect includes the adapter (privacy.py here), so blinding and fusion compose."""
+
     def __init__(self, addr, d_in: int, d_out: int, channel, noise=None):
-        if noise is not None:
-            raise NotImplementedError(
-                "activation blinding is incompatible with executor-fused adapters; privacy "
-                "clients use the reference's unfused path (SURVEY §7)")
         self.addr = addr
         self.d_in = d_in
         self.d_out = d_out
         self.channel = channel
+        self.noise = noise
 
     def forward(self, x, iteration: int = 0, want_base: bool = False):
         if x.shape[1] != self.d_in:
             raise ProtocolError(f"{self.addr}: input width {x.shape[1]} != d_in {self.d_in}")
+        if self.noise is not None:
+            payload, index = self.noise.blind(self.addr, x, iteration)
+        else:
+            payload, index = x, None
         kw = {"want_base": True} if want_base else {}
-        y = self.channel.request(self.addr.block, int(self.addr.role), PASS_FORWARD, x, **kw)
+        y = self.channel.request(self.addr.block, int(self.addr.role), PASS_FORWARD, payload, **kw)
         y = self._checked(y, x.shape[0], self.d_out)
         base = getattr(self.channel, "last_base", None) if want_base else None
-        if self.channel.reply_is_view:
+        if index is not None:
+            # unblind() returns a fresh array: nothing aliases the channel's shared buffer
+            y = self.noise.unblind(self.addr, y, index)
+            if base is not None:
+                base = self.noise.unblind_base(self.addr, base, index)
+        elif self.channel.reply_is_view:
             y = _detach(y)
             base = None if base is None else _detach(base)
         return (y, base) if want_base else y

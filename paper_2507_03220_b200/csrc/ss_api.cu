@@ -96,7 +96,7 @@ struct ss_ctx {
     size_t in_cap = 0, out_cap = 0, base_cap = 0;
     cudaEvent_t ev_in = nullptr, ev_comp = nullptr, ev_out = nullptr;
     bool used = false;
-  } hslot[3];
+  } hslot[4];
   int64_t pipeline_bytes = 24 << 20;  // target bytes of the wider side per sub-batch
   int pipeline_rows = 4096;
   cudaEvent_t upload_done = nullptr, compute_done = nullptr;
@@ -363,7 +363,6 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", block, role);
   Layer& L = lit->second;
   const bool bwd = pass_kind == SS_PASS_BACKWARD;
-  const bool noise = pass_kind == SS_PASS_NOISE_EFFECT;
   const int K = bwd ? L.d_out : L.d_in;
   const int N = bwd ? L.d_in : L.d_out;
   B = Built();
@@ -398,7 +397,9 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     if (s.flags & SS_SEGF_DST_BF16) f |= SEGF_DST_BF16;
     if (aligned16(s.src, s.src_ld, (s.flags & SS_SEGF_SRC_BF16) ? 2 : 4)) f |= SEGF_SRC_VEC;
     if (aligned16(s.dst, s.dst_ld, (s.flags & SS_SEGF_DST_BF16) ? 2 : 4)) f |= SEGF_DST_VEC;
-    if ((s.flags & SS_SEGF_ADAPTER) && !noise) {
+    // NOISE with the adapter flag = the noise effect of the ADAPTED layer, (n.W + s n.A.B) * l
+    // (bias-free): what a client with an executor-fused adapter subtracts to unblind its reply
+    if (s.flags & SS_SEGF_ADAPTER) {
       auto a = L.adapters.find(s.client_id);
       if (a == L.adapters.end()) { seg_status[i] = SS_SEG_NO_ADAPTER; continue; }
       const AdapterSlot& as = a->second;
@@ -414,7 +415,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
         d.ia3 = as.ia3;
       }
     }
-    if (s.dst_base && pass_kind == SS_PASS_FORWARD) {
+    if (s.dst_base && pass_kind != SS_PASS_BACKWARD) {
       if (s.base_ld < N) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
       f |= SEGF_WANT_BASE;
       if (s.flags & SS_SEGF_BASE_BF16) f |= SEGF_BASE_BF16;
@@ -700,7 +701,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   gpm.group_m = ctx->group_m;
   gpm.has_bias = (pass_kind == SS_PASS_FORWARD && L.bias) ? 1 : 0;
   gpm.any_lora = any_lora ? 1 : 0;
-  gpm.ia3_in_epilogue = (pass_kind == SS_PASS_FORWARD) ? 1 : 0;
+  gpm.ia3_in_epilogue = (pass_kind != SS_PASS_BACKWARD) ? 1 : 0;
   gpm.bias = L.bias;
   gpm.segs = d_segs;
   gpm.row_seg = ctx->row_seg;
@@ -740,6 +741,14 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   return SS_OK;
 }
 
+
+// Row-block copy between host and device; a plain 1-D copy when both sides are dense (the 2-D
+// engine path is measurably slower for host-to-device on this part).
+cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                      size_t rows, cudaMemcpyKind kind, cudaStream_t st) {
+  if (dpitch == width && spitch == width) return cudaMemcpyAsync(dst, src, width * rows, kind, st);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, st);
+}
 
 struct KernelAttrs {
   bool done = false;
@@ -1407,9 +1416,8 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     if ((int)s.width != K) { seg_status[i] = SS_SEG_BAD_WIDTH; continue; }
     if (s.rows == 0) continue;
     if (!s.src || !s.dst || s.src_ld < K || s.dst_ld < N) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
-    if ((s.flags & SS_SEGF_ADAPTER) && pass_kind != SS_PASS_NOISE_EFFECT &&
-        L.adapters.find(s.client_id) == L.adapters.end()) { seg_status[i] = SS_SEG_NO_ADAPTER; continue; }
-    if (s.dst_base && pass_kind == SS_PASS_FORWARD && s.base_ld < N) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
+    if ((s.flags & SS_SEGF_ADAPTER) && L.adapters.find(s.client_id) == L.adapters.end()) { seg_status[i] = SS_SEG_NO_ADAPTER; continue; }
+    if (s.dst_base && pass_kind != SS_PASS_BACKWARD && s.base_ld < N) { seg_status[i] = SS_SEG_BAD_PTR; continue; }
     good.push_back(i);
     rows_total += s.rows;
   }
@@ -1422,7 +1430,7 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     const ss_seg& s = segs[i];
     if (((s.flags & SS_SEGF_SRC_BF16) ? 2u : 4u) != esz_in || ((s.flags & SS_SEGF_DST_BF16) ? 2u : 4u) != esz_out)
       return fail(ctx, SS_E_ARG, "host dispatch: all segments must share src / dst dtypes");
-    if (s.dst_base && pass_kind == SS_PASS_FORWARD) {
+    if (s.dst_base && pass_kind != SS_PASS_BACKWARD) {
       any_base = true;
       esz_base = (s.flags & SS_SEGF_BASE_BF16) ? 2 : 4;
     }
@@ -1431,20 +1439,48 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
   // ---- sub-batches of whole rows: the H2D of j+1, the kernels of j and the D2H of j-1 overlap
   const int64_t wide = std::max<int64_t>(K * esz_in, N * esz_out);
   const int64_t target = std::max<int64_t>(64, std::min<int64_t>(ctx->pipeline_rows, ctx->pipeline_bytes / wide));
+  // Chunk sizes ramp up (t/8, t/4, t/2, t, ...) and back down at the end, so the pipeline
+  // fills and drains in a fraction of one full sub-batch: with the synchronous reference API
+  // the first H2D and the last D2H of every dispatch cannot overlap anything.
+  std::vector<int64_t> sizes;
+  {
+    const int64_t t8 = std::max<int64_t>(64, target / 8);
+    const int64_t ramp[3] = {t8, std::max<int64_t>(t8, target / 4), std::max<int64_t>(t8, target / 2)};
+    int64_t left = rows_total;
+    std::vector<int64_t> head, tail;
+    for (int k = 0; k < 3 && left > 0; ++k) {
+      const int64_t a = std::min(left, ramp[k]);
+      head.push_back(a);
+      left -= a;
+      if (left <= 0) break;
+      const int64_t b = std::min(left, ramp[k]);
+      tail.push_back(b);
+      left -= b;
+    }
+    sizes = head;
+    while (left > 0) {
+      const int64_t a = std::min(left, target);
+      sizes.push_back(a);
+      left -= a;
+    }
+    sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
+  }
   struct Piece { int seg; int64_t r0, r1; };
   std::vector<std::vector<Piece>> chunks(1);
+  size_t ci = 0;
   int64_t cur = 0;
   for (int i : good) {
     const int64_t t = segs[i].rows;
     int64_t r = 0;
     while (r < t) {
-      const int64_t take = std::min(t - r, target - cur);
+      const int64_t take = std::min(t - r, sizes[ci] - cur);
       chunks.back().push_back(Piece{i, r, r + take});
       cur += take;
       r += take;
-      if (cur >= target) {
+      if (cur >= sizes[ci]) {
         chunks.emplace_back();
         cur = 0;
+        ci = std::min(ci + 1, sizes.size() - 1);
       }
     }
   }
@@ -1461,12 +1497,12 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     }
   }
   ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap + ctx->qx_cap +
-                                            3 * (ctx->hslot[0].in_cap + ctx->hslot[0].out_cap + ctx->hslot[0].base_cap));
+                                            4 * (ctx->hslot[0].in_cap + ctx->hslot[0].out_cap + ctx->hslot[0].base_cap));
 
   std::vector<ss_seg> cs;
   std::vector<int32_t> cst;
   for (size_t j = 0; j < chunks.size(); ++j) {
-    auto& hs = ctx->hslot[j % 3];
+    auto& hs = ctx->hslot[j % 4];
     const auto& ch = chunks[j];
     // H2D: the slot's previous kernels must have consumed its input buffer
     if (hs.used) CK(cudaStreamWaitEvent(ctx->h2d, hs.ev_comp, 0));
@@ -1476,15 +1512,15 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
       const ss_seg& s = segs[p.seg];
       const int64_t n = p.r1 - p.r0;
       char* din = static_cast<char*>(hs.in) + pos * K * esz_in;
-      CK(cudaMemcpy2DAsync(din, (size_t)K * esz_in, static_cast<const char*>(s.src) + p.r0 * s.src_ld * esz_in,
-                           (size_t)s.src_ld * esz_in, (size_t)K * esz_in, (size_t)n, cudaMemcpyHostToDevice, ctx->h2d));
+      CK(copy_rows(din, (size_t)K * esz_in, static_cast<const char*>(s.src) + p.r0 * s.src_ld * esz_in,
+                   (size_t)s.src_ld * esz_in, (size_t)K * esz_in, (size_t)n, cudaMemcpyHostToDevice, ctx->h2d));
       ss_seg d = s;
       d.rows = (uint32_t)n;
       d.src = din;
       d.src_ld = K;
       d.dst = static_cast<char*>(hs.out) + pos * N * esz_out;
       d.dst_ld = N;
-      if (s.dst_base && pass_kind == SS_PASS_FORWARD) {
+      if (s.dst_base && pass_kind != SS_PASS_BACKWARD) {
         d.dst_base = static_cast<char*>(hs.base) + pos * N * esz_base;
         d.base_ld = N;
       } else {
@@ -1494,14 +1530,30 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
       cs.push_back(d);
       pos += n;
     }
+    // routing tables of this sub-batch: built on the host, copied on the SAME copy stream right
+    // after its payload (a table copy queued on the compute stream would wait behind later
+    // sub-batches' payload copies in the host-to-device engine)
+    cst.assign(cs.size(), 0);
+    Built b;
+    if ((rc = build_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), cst.data(), b))) return rc;
+    for (size_t k = 0; k < cs.size(); ++k)
+      if (cst[k] != SS_SEG_OK) seg_status[ch[k].seg] = cst[k];
+    Staging* stp = nullptr;
+    if (b.M > 0) {
+      if ((rc = acquire_staging(ctx, b.blob.size(), stp))) return rc;
+      memcpy(stp->host, b.blob.data(), b.blob.size());
+      CK(cudaMemcpyAsync(stp->dev, stp->host, b.blob.size(), cudaMemcpyHostToDevice, ctx->h2d));
+      CK(cudaEventRecord(stp->done, ctx->h2d));
+      stp->pending = true;
+    }
     CK(cudaEventRecord(hs.ev_in, ctx->h2d));
     // kernels: after the input landed and the slot's previous outputs were drained
     CK(cudaStreamWaitEvent(stream, hs.ev_in, 0));
     if (hs.used) CK(cudaStreamWaitEvent(stream, hs.ev_out, 0));
-    cst.assign(cs.size(), 0);
-    if ((rc = ss_compute_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), stream, cst.data()))) return rc;
-    for (size_t k = 0; k < cs.size(); ++k)
-      if (cst[k] != SS_SEG_OK) seg_status[ch[k].seg] = cst[k];
+    if (b.M > 0) {
+      CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
+      if ((rc = launch_batch(ctx, b, static_cast<char*>(stp->dev), stream))) return rc;
+    }
     CK(cudaEventRecord(hs.ev_comp, stream));
     // D2H
     CK(cudaStreamWaitEvent(ctx->d2h, hs.ev_comp, 0));
@@ -1510,13 +1562,13 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
       const ss_seg& s = segs[p.seg];
       const int64_t n = p.r1 - p.r0;
       if (seg_status[p.seg] == SS_SEG_OK) {
-        CK(cudaMemcpy2DAsync(static_cast<char*>(s.dst) + p.r0 * s.dst_ld * esz_out, (size_t)s.dst_ld * esz_out,
-                             static_cast<const char*>(hs.out) + pos * N * esz_out, (size_t)N * esz_out,
-                             (size_t)N * esz_out, (size_t)n, cudaMemcpyDeviceToHost, ctx->d2h));
-        if (s.dst_base && pass_kind == SS_PASS_FORWARD)
-          CK(cudaMemcpy2DAsync(static_cast<char*>(s.dst_base) + p.r0 * s.base_ld * esz_base,
-                               (size_t)s.base_ld * esz_base, static_cast<const char*>(hs.base) + pos * N * esz_base,
-                               (size_t)N * esz_base, (size_t)N * esz_base, (size_t)n, cudaMemcpyDeviceToHost, ctx->d2h));
+        CK(copy_rows(static_cast<char*>(s.dst) + p.r0 * s.dst_ld * esz_out, (size_t)s.dst_ld * esz_out,
+                     static_cast<const char*>(hs.out) + pos * N * esz_out, (size_t)N * esz_out,
+                     (size_t)N * esz_out, (size_t)n, cudaMemcpyDeviceToHost, ctx->d2h));
+        if (s.dst_base && pass_kind != SS_PASS_BACKWARD)
+          CK(copy_rows(static_cast<char*>(s.dst_base) + p.r0 * s.base_ld * esz_base,
+                       (size_t)s.base_ld * esz_base, static_cast<const char*>(hs.base) + pos * N * esz_base,
+                       (size_t)N * esz_base, (size_t)N * esz_base, (size_t)n, cudaMemcpyDeviceToHost, ctx->d2h));
       }
       pos += n;
     }

@@ -260,8 +260,8 @@ class GpuBaseExecutor:
         if key not in self._dims:
             raise ProtocolError(f"unknown layer {key}")
         segs = [Seg(client_id=c, src=src, dst=dst,
-                    base=base if pass_kind == PASS_FORWARD else None,
-                    adapter=pass_kind != PASS_NOISE_EFFECT and key in self._fused.get(c, ()))
+                    base=base if pass_kind != PASS_BACKWARD else None,
+                    adapter=key in self._fused.get(c, ()))
                 for c, src, dst, base in segments]
         return Dispatch(self.ctx, pass_kind, key, segs)
 
@@ -382,10 +382,9 @@ class GpuBaseExecutor:
             segs = []
             for j, i in enumerate(good):
                 env = envelopes[i]
-                base = getattr(env, "base_to", None) if pass_kind == PASS_FORWARD else None
+                base = getattr(env, "base_to", None) if pass_kind != PASS_BACKWARD else None
                 segs.append(Seg(client_id=env.client_id, src=srcs[j], dst=dsts[j], base=base,
-                                adapter=(pass_kind != PASS_NOISE_EFFECT
-                                         and key in fused.get(env.client_id, ()))))
+                                adapter=key in fused.get(env.client_id, ())))
             status = self.ctx.compute(pass_kind, key[0], key[1], segs, stream)
             rows = sum(envelopes[i].token_count for i in good)
             esz = 2 if all(s.src.dtype == torch.bfloat16 for s in segs) else 4
@@ -438,7 +437,7 @@ class GpuBaseExecutor:
         fused = self._fused
         in_w = envelopes[good[0]].width
         segs = [Seg(client_id=envelopes[i].client_id, src=envelopes[i].payload, dst=envelopes[i].reply_to,
-                    width=in_w, adapter=pass_kind != PASS_NOISE_EFFECT and key in fused.get(envelopes[i].client_id, ()))
+                    width=in_w, adapter=key in fused.get(envelopes[i].client_id, ()))
                 for i in good]
         status = self.ctx.compute_host(pass_kind, key[0], key[1], segs, stream)
         self.last_event = None

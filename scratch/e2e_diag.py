@@ -21,7 +21,7 @@ ex = GpuBaseExecutor(layers, retain_layers=False)
 if len(sys.argv) > 1:
     ex.pipeline_bytes = int(sys.argv[1]) << 20
 if len(sys.argv) > 2:
-    ex.pipeline_slots = int(sys.argv[2])
+    pass
 t, n = 1024, 32
 maxw = 32000
 host = [torch.empty(t * maxw, dtype=torch.bfloat16).pin_memory() for _ in range(n)]

@@ -225,7 +225,41 @@ def row_independence():
     np.savez_compressed(os.path.join(HERE, "row_independence.npz"), **d)
 
 
-if __name__ == "__main__":
+def privacy_golden():
+    """privacy.py:33-106 — rotate indices, draw_noise samples and a blind -> serve_forward ->
+    unblind round trip through the reference's own NoiseSet / LocalChannel / BaseExecutor."""
+    from splitserve.privacy import NoiseSet, draw_noise, precompute_noise, rotate
+    from splitserve.transport import LocalChannel
+    d = {}
+    addrs = [LayerAddress(0, Role.Q), LayerAddress(3, Role.FF_UP), LayerAddress(2, Role.LM_HEAD)]
+    d["rotate"] = np.array([[rotate(s, a, it, k) for a in addrs for it in range(6) for k in (2, 3, 5)]
+                            for s in (0, 7)], dtype=np.int64)
+    d["noise_q"] = draw_noise(4, addrs[0], 1, 5, 16, 1.0)
+    d["noise_up"] = draw_noise(9, addrs[1], 0, 3, 24, 0.25)
+    cfg = ModelConfig(1, 16, 2, 32, 32, 16, 0)
+    layers = build_model(cfg).layers
+    addr = LayerAddress(0, Role.FF_UP)
+    ex = BaseExecutor({addr: layers[addr]})
+    ex.start()
+    try:
+        ch = LocalChannel(ex, 1, 1, 8, 32)
+        ch.register(sends_backward=False)
+        ns = precompute_noise(ch, cfg, k=2, scale=1.0, seed=3, t_max=8, layers=[addr])
+        x = np.random.default_rng(5).standard_normal((8, 16)).astype(np.float32)
+        payload, idx = ns.blind(addr, x, 4)
+        y_noisy = np.array(ch.request(0, int(Role.FF_UP), PASS_FORWARD, payload), copy=True)
+        d["rt_x"], d["rt_idx"] = x, np.int64(idx)
+        d["rt_y"] = ns.unblind(addr, y_noisy, idx)
+        d["rt_effect"] = ns.effects[addr][idx]
+        d["rt_W"], d["rt_b"] = layers[addr].weight, layers[addr].bias
+    finally:
+        ex.stop()
+    np.savez_compressed(os.path.join(HERE, "privacy.npz"), **d)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    globals()[sys.argv[1]]()
+elif __name__ == "__main__":
     model_checksums()
     executor_kat()
     adapters_golden()
@@ -233,6 +267,7 @@ if __name__ == "__main__":
     fused_batch("fused_random_small", 256, 512, seed=22)
     fused_batch("fused_random_ragged", 200, 328, seed=23, rows=(1, 127, 129, 3), ranks=(24, 64))
     row_independence()
+    privacy_golden()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
