@@ -24,6 +24,7 @@
 #ifndef SS_B200_H
 #define SS_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__GNUC__)
@@ -43,6 +44,7 @@ extern "C" {
 #define SS_E_NOLAYER (-3)   /* unknown (block, role) — reference: "unknown layer" executor.py:172-174 */
 #define SS_E_NOMEM (-4)
 #define SS_E_UNSUPPORTED (-5)
+#define SS_E_PROTOCOL (-6)  /* LSV1 stream corrupt (bad magic / version): connection-level rejection */
 
 /* per-segment status written to seg_status[i] (0 = computed) */
 #define SS_SEG_OK 0
@@ -131,6 +133,28 @@ SS_API int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int
  * returns. All segments must share one src dtype and one dst dtype. */
 SS_API int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
                                  const ss_seg* segs, void* stream, int32_t* seg_status);
+
+/* ---- LSV1 wire frames ---------------------------------------------------------------------
+ * The reference's byte-stream channel frames every tensor (protocol.py:6-25: 30-byte
+ * little-endian header "LSV1", u16 version 1, u32 client_id, u64 request_id, u16 block, u8 role,
+ * u8 pass, u32 token_count, u32 width, then token_count*width f32), decoding and re-encoding
+ * payloads on the host (protocol.py:96-153, transport.py:104-275). ss_serve_frames serves a run
+ * of request frames as received from a stream WITHOUT a host-side decode:
+ *   - frames are parsed in place; each one goes through the executor's intake checks in order
+ *     (unknown pass, non-increasing request_id per client, unknown layer: executor.py:162-178);
+ *   - valid frames are grouped by (block, role, pass) in arrival order, one dispatch per group
+ *     (FIFO inside it, executor.py:247-300), each frame's f32 payload copied to the GPU straight
+ *     from the receive buffer through the host pipeline (ss_compute_batch_host), with the
+ *     client's registered adapter fused;
+ *   - every reply is written as a complete LSV1 frame into `out`, in request order: the reply
+ *     header echoes the request's ids and pass (executor.py:295-300) and its f32 payload is
+ *     copied back from the GPU directly behind it; a failed frame becomes a PASS_ERROR (255)
+ *     frame carrying the reference's UTF-8 message (protocol.py:86-89).
+ * *consumed = bytes of the whole frames parsed (a trailing partial frame stays for the next
+ * call, like try_decode). Bad magic / version: SS_E_PROTOCOL, nothing served. If out_cap is
+ * too small: SS_E_NOMEM with *out_len = the bytes needed, nothing served. */
+SS_API int ss_serve_frames(ss_ctx* ctx, const uint8_t* in, size_t in_len, size_t* consumed,
+                           uint8_t* out, size_t out_cap, size_t* out_len, void* stream);
 
 /* ---- prebuilt dispatch plans ------------------------------------------------------------
  * For clients whose exchange buffers do not move (DeviceChannel after its first grow), the

@@ -20,6 +20,7 @@ SS_E_CUDA = -2
 SS_E_NOLAYER = -3
 SS_E_NOMEM = -4
 SS_E_UNSUPPORTED = -5
+SS_E_PROTOCOL = -6
 
 SS_SEG_OK = 0
 SS_SEG_BAD_WIDTH = 1
@@ -49,7 +50,7 @@ EXPORTED = (
     "ss_unload_layer", "ss_set_adapter", "ss_clear_adapter", "ss_clear_client",
     "ss_compute_batch", "ss_memory_stats", "ss_kernel_launches", "ss_set_option",
     "ss_profile", "ss_profile_read", "ss_adapter_grads", "ss_plan_create", "ss_plan_launch",
-    "ss_plan_destroy", "ss_compute_batch_host",
+    "ss_plan_destroy", "ss_compute_batch_host", "ss_serve_frames",
 )
 
 SS_KERNEL_GATHER = 0
@@ -132,6 +133,8 @@ def load() -> ctypes.CDLL:
                                        ctypes.POINTER(ctypes.c_int32)]),
             "ss_compute_batch_host": (i32, [vp, i32, i32, i32, i32, ctypes.POINTER(SsSeg), vp,
                                             ctypes.POINTER(ctypes.c_int32)]),
+            "ss_serve_frames": (i32, [vp, vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), vp,
+                                      ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), vp]),
             "ss_plan_create": (i32, [vp, i32, i32, i32, i32, ctypes.POINTER(SsSeg),
                                      ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(vp)]),
             "ss_plan_launch": (i32, [vp, vp]),

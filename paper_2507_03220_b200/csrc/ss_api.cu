@@ -76,6 +76,7 @@ struct ss_ctx {
   std::string err;
   PFN_encodeTiled_t encode = nullptr;
   std::map<std::pair<int, int>, Layer> layers;
+  std::map<uint32_t, uint64_t> last_request_id;  // LSV1 intake (executor.py:164-169)
   // workspace
   __nv_bfloat16* X = nullptr;
   size_t x_cap = 0;
@@ -1581,3 +1582,176 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
 }
 
 }  // extern "C"
+
+// ---- LSV1 frames ------------------------------------------------------------------------
+namespace {
+constexpr size_t kHdr = 30;
+const char* kRoleNames[7] = {"Q", "K", "V", "O", "FF_UP", "FF_DOWN", "LM_HEAD"};
+
+struct Frame {
+  size_t off = 0;          // offset of the header in `in`
+  uint32_t client = 0;
+  uint64_t rid = 0;
+  uint16_t block = 0;
+  uint8_t role = 0, pass = 0;
+  uint32_t t = 0, w = 0;
+  std::string err;         // non-empty: reply is a PASS_ERROR frame with this message
+  uint32_t out_w = 0;      // reply width (compute frames)
+  size_t out_off = 0;      // offset of the reply frame in `out`
+};
+
+template <typename T>
+T rd(const uint8_t* p) {
+  T v;
+  memcpy(&v, p, sizeof(T));
+  return v;
+}
+template <typename T>
+void wr(uint8_t* p, T v) {
+  memcpy(p, &v, sizeof(T));
+}
+
+// repr of the reference's LayerAddress (config.py:27-33), as executor messages print it
+std::string addr_repr(int block, int role) {
+  char buf[96];
+  if (role >= 0 && role < 7)
+    snprintf(buf, sizeof buf, "LayerAddress(block=%d, role=<Role.%s: %d>)", block, kRoleNames[role], role);
+  else
+    snprintf(buf, sizeof buf, "LayerAddress(block=%d, role=%d)", block, role);
+  return buf;
+}
+
+void write_header(uint8_t* p, const Frame& f, uint8_t pass, uint32_t t, uint32_t w) {
+  memcpy(p, "LSV1", 4);
+  wr<uint16_t>(p + 4, 1);
+  wr<uint32_t>(p + 6, f.client);
+  wr<uint64_t>(p + 10, f.rid);
+  wr<uint16_t>(p + 18, f.block);
+  wr<uint8_t>(p + 20, f.role);
+  wr<uint8_t>(p + 21, pass);
+  wr<uint32_t>(p + 22, t);
+  wr<uint32_t>(p + 26, w);
+}
+}  // namespace
+
+extern "C" int ss_serve_frames(ss_ctx* ctx, const uint8_t* in, size_t in_len, size_t* consumed,
+                               uint8_t* out, size_t out_cap, size_t* out_len, void* stream) {
+  if (!ctx || (!in && in_len) || !consumed || !out_len) return SS_E_ARG;
+  *consumed = 0;
+  *out_len = 0;
+  // ---- parse whole frames (try_decode, protocol.py:125-153)
+  std::vector<Frame> fr;
+  size_t pos = 0;
+  while (true) {
+    const size_t left = in_len - pos;
+    if (left < kHdr) {
+      if (left >= 4 && memcmp(in + pos, "LSV1", 4) != 0) return fail(ctx, SS_E_PROTOCOL, "bad magic");
+      break;
+    }
+    const uint8_t* p = in + pos;
+    if (memcmp(p, "LSV1", 4) != 0) return fail(ctx, SS_E_PROTOCOL, "bad magic");
+    const uint16_t version = rd<uint16_t>(p + 4);
+    if (version != 1) return fail(ctx, SS_E_PROTOCOL, "unsupported protocol version %u", version);
+    Frame f;
+    f.off = pos;
+    f.client = rd<uint32_t>(p + 6);
+    f.rid = rd<uint64_t>(p + 10);
+    f.block = rd<uint16_t>(p + 18);
+    f.role = rd<uint8_t>(p + 20);
+    f.pass = rd<uint8_t>(p + 21);
+    f.t = rd<uint32_t>(p + 22);
+    f.w = rd<uint32_t>(p + 26);
+    const size_t size = f.pass == 255 ? (size_t)f.t : (size_t)4 * f.t * f.w;
+    if (left < kHdr + size) break;
+    fr.push_back(f);
+    pos += kHdr + size;
+  }
+  // ---- intake checks in arrival order (BaseExecutor.submit, executor.py:162-178)
+  for (Frame& f : fr) {
+    char msg[160];
+    if (f.pass > 2) {
+      snprintf(msg, sizeof msg, "unknown pass %u", f.pass);
+      f.err = msg;
+      continue;
+    }
+    auto it = ctx->last_request_id.find(f.client);
+    if (it != ctx->last_request_id.end() && f.rid <= it->second) {
+      snprintf(msg, sizeof msg, "request_id %llu not increasing (last %llu)", (unsigned long long)f.rid,
+               (unsigned long long)it->second);
+      f.err = msg;
+      continue;
+    }
+    ctx->last_request_id[f.client] = f.rid;
+    auto lit = ctx->layers.find({(int)f.block, (int)f.role});
+    if (lit == ctx->layers.end()) {
+      f.err = "unknown layer " + addr_repr(f.block, f.role);
+      continue;
+    }
+    const Layer& L = lit->second;
+    const uint32_t expected = f.pass == SS_PASS_BACKWARD ? L.d_out : L.d_in;
+    // _compute_batch's width check (executor.py:208-211)
+    if (f.w != expected) {
+      snprintf(msg, sizeof msg, "row width %u does not match layer %s expected %u", f.w,
+               addr_repr(f.block, f.role).c_str(), expected);
+      f.err = msg;
+      continue;
+    }
+    f.out_w = f.pass == SS_PASS_BACKWARD ? L.d_in : L.d_out;
+  }
+  // ---- reply layout (request order) and capacity
+  size_t need = 0;
+  for (Frame& f : fr) {
+    f.out_off = need;
+    need += kHdr + (f.err.empty() ? (size_t)4 * f.t * f.out_w : f.err.size());
+  }
+  if (need > out_cap) {
+    *out_len = need;
+    return fail(ctx, SS_E_NOMEM, "reply buffer too small: need %zu bytes", need);
+  }
+  for (const Frame& f : fr) {
+    uint8_t* o = out + f.out_off;
+    if (f.err.empty()) {
+      write_header(o, f, f.pass, f.t, f.out_w);
+    } else {
+      write_header(o, f, 255, (uint32_t)f.err.size(), 0);
+      memcpy(o + kHdr, f.err.data(), f.err.size());
+    }
+  }
+  // ---- one host-pipeline dispatch per (block, role, pass) group, FIFO within the group
+  std::vector<int> order;
+  std::vector<char> done(fr.size(), 0);
+  for (size_t i = 0; i < fr.size(); ++i) {
+    if (done[i] || !fr[i].err.empty()) continue;
+    std::vector<int> grp;
+    for (size_t j = i; j < fr.size(); ++j)
+      if (!done[j] && fr[j].err.empty() && fr[j].block == fr[i].block && fr[j].role == fr[i].role &&
+          fr[j].pass == fr[i].pass) {
+        grp.push_back((int)j);
+        done[j] = 1;
+      }
+    const Layer& L = ctx->layers.find({(int)fr[i].block, (int)fr[i].role})->second;
+    std::vector<ss_seg> segs;
+    for (int j : grp) {
+      const Frame& f = fr[j];
+      ss_seg s{};
+      s.client_id = f.client;
+      s.rows = f.t;
+      s.width = f.w;
+      s.flags = L.adapters.count(f.client) ? SS_SEGF_ADAPTER : 0;  // f32 in, f32 out
+      s.src = in + f.off + kHdr;
+      s.src_ld = f.w;
+      s.dst = out + f.out_off + kHdr;
+      s.dst_ld = f.out_w;
+      segs.push_back(s);
+    }
+    std::vector<int32_t> st(segs.size(), 0);
+    int rc = ss_compute_batch_host(ctx, fr[i].pass, fr[i].block, fr[i].role, (int)segs.size(), segs.data(),
+                                   stream, st.data());
+    if (rc) return rc;
+    for (size_t k = 0; k < segs.size(); ++k)
+      if (st[k] != SS_SEG_OK) return fail(ctx, SS_E_ARG, "frame %d rejected after validation (status %d)", grp[k], st[k]);
+  }
+  *consumed = pos;
+  *out_len = need;
+  return SS_OK;
+}
