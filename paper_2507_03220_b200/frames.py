@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -42,7 +43,7 @@ class FrameServer:
         n = mv.nbytes
         buf = self._grow("_in", n)
         if n:
-            buf[:n].numpy()[:] = mv
+            buf[:n].numpy()[:] = np.frombuffer(mv, dtype=np.uint8)
         return self.serve_pinned(buf, n)
 
     def serve_pinned(self, buf: torch.Tensor, n: int) -> tuple[bytes, int]:

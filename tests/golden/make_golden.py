@@ -257,6 +257,74 @@ def privacy_golden():
     np.savez_compressed(os.path.join(HERE, "privacy.npz"), **d)
 
 
+def frames_golden():
+    """protocol.py:96-153 + executor.py:162-231, 295-300 — a run of LSV1 request frames (valid
+    forward / backward / noise frames of two layers, exact-integer payloads, plus frames the
+    intake rejects) encoded by the reference, and the reply frames the reference executor
+    produces for them (submit's error replies; serve_* results wrapped as replies), encoded by
+    the reference codec."""
+    from splitserve.protocol import (PASS_ERROR, encode, error_envelope, try_decode)  # noqa: F401
+    cfg = ModelConfig(1, 16, 2, 32, 32, 16, 0)
+    model = build_model(cfg)
+    q, up = LayerAddress(0, Role.Q), LayerAddress(0, Role.FF_UP)
+    # exact-integer weights so f32 replies are exact regardless of accumulation order
+    rng = np.random.default_rng(31)
+    layers = {}
+    for a in (q, up):
+        p = model.layers[a]
+        w = rng.integers(-2, 3, p.weight.shape).astype(np.float32)
+        b = rng.integers(-2, 3, p.bias.shape).astype(np.float32)
+        layers[a] = AffineParams(w, b)
+    ex = BaseExecutor(layers)
+    def pay(t, w):
+        return rng.integers(-3, 4, (t, w)).astype(np.float32)
+    reqs = [
+        Envelope(1, 1, 0, int(Role.Q), PASS_FORWARD, pay(5, 16)),
+        Envelope(2, 1, 0, int(Role.Q), PASS_FORWARD, pay(3, 16)),
+        Envelope(1, 2, 0, int(Role.FF_UP), PASS_FORWARD, pay(4, 16)),
+        Envelope(3, 7, 0, int(Role.Q), 9, pay(1, 16)),               # unknown pass
+        Envelope(2, 1, 0, int(Role.Q), PASS_FORWARD, pay(2, 16)),     # request id not increasing
+        Envelope(4, 1, 5, int(Role.Q), PASS_FORWARD, pay(2, 16)),     # unknown layer
+        Envelope(5, 1, 0, int(Role.Q), PASS_FORWARD, pay(2, 12)),     # width mismatch
+        Envelope(1, 3, 0, int(Role.FF_UP), PASS_BACKWARD, pay(6, 32)),
+        Envelope(2, 2, 0, int(Role.Q), PASS_NOISE_EFFECT, pay(3, 16)),
+        Envelope(6, 1, 0, int(Role.Q), PASS_FORWARD, pay(0, 16)),     # zero tokens
+        Envelope(2, 3, 0, int(Role.Q), PASS_FORWARD, pay(7, 16)),
+    ]
+    stream = b"".join(encode(e) for e in reqs)
+    # the reference server path: decode, submit (intake errors reply at once), then each
+    # (layer, pass) queue in FIFO order through _compute_batch, replies wrapped per envelope
+    replies = {}
+    queues = {}
+    buf = memoryview(stream)
+    pos = 0
+    order = []
+    while pos < len(stream):
+        env, used = try_decode(buf[pos:])
+        pos += used
+        order.append((env.client_id, env.request_id, env.pass_kind, len(order)))
+        idx = len(order) - 1
+        def reply_fn(r, idx=idx):
+            replies[idx] = r
+        before = len(replies)
+        ex.submit(env, reply_fn)
+        if len(replies) == before:   # queued, not rejected
+            queues.setdefault((env.block, env.role, env.pass_kind), []).append((idx, env))
+    for key, items in queues.items():
+        envs = [e for _, e in items]
+        res = ex._compute_batch(key[2], envs)
+        for (idx, env), r in zip(items, res):
+            if isinstance(r, ProtocolError):
+                replies[idx] = error_envelope(env, str(r))
+            else:
+                replies[idx] = Envelope(env.client_id, env.request_id, env.block, env.role, env.pass_kind, r)
+    out = b"".join(encode(replies[i]) for i in range(len(order)))
+    d = {"requests": np.frombuffer(stream, dtype=np.uint8), "replies": np.frombuffer(out, dtype=np.uint8)}
+    for a, name in ((q, "q"), (up, "up")):
+        d[f"W_{name}"], d[f"b_{name}"] = layers[a].weight, layers[a].bias
+    np.savez_compressed(os.path.join(HERE, "frames.npz"), **d)
+
+
 if __name__ == "__main__" and len(sys.argv) > 1:
     globals()[sys.argv[1]]()
 elif __name__ == "__main__":
@@ -268,6 +336,7 @@ elif __name__ == "__main__":
     fused_batch("fused_random_ragged", 200, 328, seed=23, rows=(1, 127, 129, 3), ranks=(24, 64))
     row_independence()
     privacy_golden()
+    frames_golden()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
