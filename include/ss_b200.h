@@ -142,14 +142,14 @@ SS_API int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role
  * of request frames as received from a stream WITHOUT a host-side decode:
  *   - frames are parsed in place; each one goes through the executor's intake checks in order
  *     (unknown pass, non-increasing request_id per client, unknown layer: executor.py:162-178);
- *   - valid frames are grouped by (block, role, pass) in arrival order, one dispatch per group
- *     (FIFO inside it, executor.py:247-300), each frame's f32 payload copied to the GPU straight
- *     from the receive buffer through the host pipeline (ss_compute_batch_host), with the
- *     client's registered adapter fused;
- *   - every reply is written as a complete LSV1 frame into `out`, in request order: the reply
- *     header echoes the request's ids and pass (executor.py:295-300) and its f32 payload is
- *     copied back from the GPU directly behind it; a failed frame becomes a PASS_ERROR (255)
- *     frame carrying the reference's UTF-8 message (protocol.py:86-89).
+ *   - the run of frames is copied to the GPU as raw bytes in one transfer; the f32 payloads
+ *     (behind 30-byte headers, so not 4-byte aligned) are decoded THERE into bf16 operand rows;
+ *   - valid frames are grouped by (block, role, pass) in arrival order, one fused dispatch per
+ *     group (FIFO inside it, executor.py:247-300), with the client's registered adapter fused;
+ *   - the reply stream is encoded on the GPU — per frame in request order a complete LSV1 frame:
+ *     the header echoing the request's ids and pass (executor.py:295-300) and the f32 payload,
+ *     or a PASS_ERROR (255) frame with the reference's UTF-8 message (protocol.py:86-89) — and
+ *     returned to `out` in one transfer.
  * *consumed = bytes of the whole frames parsed (a trailing partial frame stays for the next
  * call, like try_decode). Bad magic / version: SS_E_PROTOCOL, nothing served. If out_cap is
  * too small: SS_E_NOMEM with *out_len = the bytes needed, nothing served. */

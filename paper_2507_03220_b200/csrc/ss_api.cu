@@ -19,6 +19,7 @@
 #include "../../include/ss_b200.h"
 #include "kernels.cuh"
 #include "grads.cuh"
+#include "frames.cuh"
 
 using namespace ss;
 
@@ -77,6 +78,12 @@ struct ss_ctx {
   PFN_encodeTiled_t encode = nullptr;
   std::map<std::pair<int, int>, Layer> layers;
   std::map<uint32_t, uint64_t> last_request_id;  // LSV1 intake (executor.py:164-169)
+  // LSV1 serving: device copies of the request / reply streams, decoded operand, f32 replies
+  char* fr_in = nullptr;
+  char* fr_out = nullptr;
+  char* fr_x = nullptr;
+  char* fr_o = nullptr;
+  size_t fr_in_cap = 0, fr_out_cap = 0, fr_x_cap = 0, fr_o_cap = 0;
   // workspace
   __nv_bfloat16* X = nullptr;
   size_t x_cap = 0;
@@ -873,6 +880,10 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   cudaFree(ctx->a_lora);
   cudaFree(ctx->row_seg);
   cudaFree(ctx->qx);
+  cudaFree(ctx->fr_in);
+  cudaFree(ctx->fr_out);
+  cudaFree(ctx->fr_x);
+  cudaFree(ctx->fr_o);
   for (auto& s : ctx->staging) {
     cudaFreeHost(s.host);
     cudaFree(s.dev);
@@ -1635,7 +1646,7 @@ void write_header(uint8_t* p, const Frame& f, uint8_t pass, uint32_t t, uint32_t
 }  // namespace
 
 extern "C" int ss_serve_frames(ss_ctx* ctx, const uint8_t* in, size_t in_len, size_t* consumed,
-                               uint8_t* out, size_t out_cap, size_t* out_len, void* stream) {
+                               uint8_t* out, size_t out_cap, size_t* out_len, void* stream_) {
   if (!ctx || (!in && in_len) || !consumed || !out_len) return SS_E_ARG;
   *consumed = 0;
   *out_len = 0;
@@ -1666,7 +1677,9 @@ extern "C" int ss_serve_frames(ss_ctx* ctx, const uint8_t* in, size_t in_len, si
     fr.push_back(f);
     pos += kHdr + size;
   }
-  // ---- intake checks in arrival order (BaseExecutor.submit, executor.py:162-178)
+  // ---- intake checks in arrival order (BaseExecutor.submit, executor.py:162-178), on a copy of
+  // the request-id table: nothing is committed unless the frames are actually served
+  std::map<uint32_t, uint64_t> rids = ctx->last_request_id;
   for (Frame& f : fr) {
     char msg[160];
     if (f.pass > 2) {
@@ -1674,14 +1687,14 @@ extern "C" int ss_serve_frames(ss_ctx* ctx, const uint8_t* in, size_t in_len, si
       f.err = msg;
       continue;
     }
-    auto it = ctx->last_request_id.find(f.client);
-    if (it != ctx->last_request_id.end() && f.rid <= it->second) {
+    auto it = rids.find(f.client);
+    if (it != rids.end() && f.rid <= it->second) {
       snprintf(msg, sizeof msg, "request_id %llu not increasing (last %llu)", (unsigned long long)f.rid,
                (unsigned long long)it->second);
       f.err = msg;
       continue;
     }
-    ctx->last_request_id[f.client] = f.rid;
+    rids[f.client] = f.rid;
     auto lit = ctx->layers.find({(int)f.block, (int)f.role});
     if (lit == ctx->layers.end()) {
       f.err = "unknown layer " + addr_repr(f.block, f.role);
@@ -1708,50 +1721,107 @@ extern "C" int ss_serve_frames(ss_ctx* ctx, const uint8_t* in, size_t in_len, si
     *out_len = need;
     return fail(ctx, SS_E_NOMEM, "reply buffer too small: need %zu bytes", need);
   }
-  for (const Frame& f : fr) {
-    uint8_t* o = out + f.out_off;
+  ctx->last_request_id.swap(rids);
+  *consumed = pos;
+  *out_len = need;
+  if (fr.empty()) return SS_OK;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+
+  // ---- device-side frame table: decoded-operand and reply-row offsets, reply headers, messages
+  std::vector<FrameDesc> fd(fr.size());
+  std::string msgs;
+  int64_t x_elems = 0, o_elems = 0, max_vals = 1;
+  for (size_t i = 0; i < fr.size(); ++i) {
+    const Frame& f = fr[i];
+    FrameDesc& d = fd[i];
+    memset(&d, 0, sizeof d);
+    d.in_off = (int64_t)(f.off + kHdr);
+    d.out_off = (int64_t)f.out_off;
     if (f.err.empty()) {
-      write_header(o, f, f.pass, f.t, f.out_w);
+      write_header(d.hdr, f, f.pass, f.t, f.out_w);
+      d.t = (int32_t)f.t;
+      d.w = (int32_t)f.w;
+      d.out_w = (int32_t)f.out_w;
+      d.x_off = x_elems;
+      d.o_off = o_elems;
+      x_elems += round_up((int64_t)f.t * f.w, 8);          // 16-byte aligned operand rows
+      o_elems += round_up((int64_t)f.t * f.out_w, 4);
+      max_vals = std::max<int64_t>(max_vals, (int64_t)f.t * std::max(f.w, f.out_w));
     } else {
-      write_header(o, f, 255, (uint32_t)f.err.size(), 0);
-      memcpy(o + kHdr, f.err.data(), f.err.size());
+      write_header(d.hdr, f, 255, (uint32_t)f.err.size(), 0);
+      d.is_err = 1;
+      d.msg_off = (int32_t)msgs.size();
+      d.msg_len = (int32_t)f.err.size();
+      msgs += f.err;
     }
   }
-  // ---- one host-pipeline dispatch per (block, role, pass) group, FIFO within the group
-  std::vector<int> order;
+  int rc = SS_OK;
+  if ((rc = ensure_dev(ctx, ctx->fr_in, ctx->fr_in_cap, round_up(in_len, 256) + 256))) return rc;
+  if ((rc = ensure_dev(ctx, ctx->fr_out, ctx->fr_out_cap, round_up(need, 256) + 256))) return rc;
+  if ((rc = ensure_dev(ctx, ctx->fr_x, ctx->fr_x_cap, (size_t)std::max<int64_t>(x_elems, 8) * 2))) return rc;
+  if ((rc = ensure_dev(ctx, ctx->fr_o, ctx->fr_o_cap, (size_t)std::max<int64_t>(o_elems, 4) * 4))) return rc;
+  const size_t t_bytes = round_up(fd.size() * sizeof(FrameDesc), 256);
+  const size_t total = t_bytes + round_up(std::max<size_t>(1, msgs.size()), 256);
+  Staging* stp = nullptr;
+  if ((rc = acquire_staging(ctx, total, stp))) return rc;
+  memcpy(stp->host, fd.data(), fd.size() * sizeof(FrameDesc));
+  if (!msgs.empty()) memcpy(static_cast<char*>(stp->host) + t_bytes, msgs.data(), msgs.size());
+  // raw request bytes and the frame table in, on the copy stream
+  CK(cudaMemcpyAsync(ctx->fr_in, in, in_len, cudaMemcpyHostToDevice, ctx->h2d));
+  CK(cudaMemcpyAsync(stp->dev, stp->host, total, cudaMemcpyHostToDevice, ctx->h2d));
+  CK(cudaEventRecord(stp->done, ctx->h2d));
+  stp->pending = true;
+  CK(cudaStreamWaitEvent(stream, stp->done, 0));
+  const FrameDesc* dfd = reinterpret_cast<const FrameDesc*>(stp->dev);
+  const uint8_t* dmsg = static_cast<const uint8_t*>(stp->dev) + t_bytes;
+  const int gx = (int)std::min<int64_t>((max_vals + 511) / 512, 4 * ctx->num_sms);
+  for (size_t f0 = 0; f0 < fd.size(); f0 += 65535) {
+    const unsigned gy = (unsigned)std::min<size_t>(65535, fd.size() - f0);
+    frame_decode_kernel<<<dim3(gx, gy), 256, 0, stream>>>(reinterpret_cast<const uint8_t*>(ctx->fr_in), dfd + f0,
+                                                          reinterpret_cast<__nv_bfloat16*>(ctx->fr_x));
+    CK(cudaGetLastError());
+    ctx->launches++;
+  }
+  // ---- one fused dispatch per (block, role, pass) group, FIFO within the group
   std::vector<char> done(fr.size(), 0);
   for (size_t i = 0; i < fr.size(); ++i) {
     if (done[i] || !fr[i].err.empty()) continue;
-    std::vector<int> grp;
-    for (size_t j = i; j < fr.size(); ++j)
-      if (!done[j] && fr[j].err.empty() && fr[j].block == fr[i].block && fr[j].role == fr[i].role &&
-          fr[j].pass == fr[i].pass) {
-        grp.push_back((int)j);
-        done[j] = 1;
-      }
     const Layer& L = ctx->layers.find({(int)fr[i].block, (int)fr[i].role})->second;
     std::vector<ss_seg> segs;
-    for (int j : grp) {
+    std::vector<int> grp;
+    for (size_t j = i; j < fr.size(); ++j) {
       const Frame& f = fr[j];
+      if (done[j] || !f.err.empty() || f.block != fr[i].block || f.role != fr[i].role || f.pass != fr[i].pass) continue;
+      done[j] = 1;
+      grp.push_back((int)j);
       ss_seg s{};
       s.client_id = f.client;
       s.rows = f.t;
       s.width = f.w;
-      s.flags = L.adapters.count(f.client) ? SS_SEGF_ADAPTER : 0;  // f32 in, f32 out
-      s.src = in + f.off + kHdr;
+      s.flags = SS_SEGF_SRC_BF16 | (L.adapters.count(f.client) ? SS_SEGF_ADAPTER : 0);  // f32 reply rows
+      s.src = reinterpret_cast<__nv_bfloat16*>(ctx->fr_x) + fd[j].x_off;
       s.src_ld = f.w;
-      s.dst = out + f.out_off + kHdr;
+      s.dst = reinterpret_cast<float*>(ctx->fr_o) + fd[j].o_off;
       s.dst_ld = f.out_w;
       segs.push_back(s);
     }
     std::vector<int32_t> st(segs.size(), 0);
-    int rc = ss_compute_batch_host(ctx, fr[i].pass, fr[i].block, fr[i].role, (int)segs.size(), segs.data(),
-                                   stream, st.data());
-    if (rc) return rc;
+    if ((rc = ss_compute_batch(ctx, fr[i].pass, fr[i].block, fr[i].role, (int)segs.size(), segs.data(), stream,
+                               st.data())))
+      return rc;
     for (size_t k = 0; k < segs.size(); ++k)
       if (st[k] != SS_SEG_OK) return fail(ctx, SS_E_ARG, "frame %d rejected after validation (status %d)", grp[k], st[k]);
   }
-  *consumed = pos;
-  *out_len = need;
+  // ---- reply stream encoded on the device, one copy back
+  for (size_t f0 = 0; f0 < fd.size(); f0 += 65535) {
+    const unsigned gy = (unsigned)std::min<size_t>(65535, fd.size() - f0);
+    frame_encode_kernel<<<dim3(gx, gy), 256, 0, stream>>>(reinterpret_cast<uint8_t*>(ctx->fr_out), dfd + f0,
+                                                          reinterpret_cast<const float*>(ctx->fr_o), dmsg);
+    CK(cudaGetLastError());
+    ctx->launches++;
+  }
+  CK(cudaMemcpyAsync(out, ctx->fr_out, need, cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
   return SS_OK;
 }

@@ -44,10 +44,13 @@ class FrameServer:
         buf = self._grow("_in", n)
         if n:
             buf[:n].numpy()[:] = np.frombuffer(mv, dtype=np.uint8)
-        return self.serve_pinned(buf, n)
+        out, used = self.serve_pinned(buf, n)
+        return bytes(out.numpy()), used
 
-    def serve_pinned(self, buf: torch.Tensor, n: int) -> tuple[bytes, int]:
-        """Same, reading the frames from a caller-owned pinned uint8 tensor (no host copy)."""
+    def serve_pinned(self, buf: torch.Tensor, n: int) -> tuple[torch.Tensor, int]:
+        """Same, reading the frames from a caller-owned pinned uint8 tensor and returning the reply
+        stream as a view of the server's pinned send buffer (valid until the next call, like the
+        reference LocalChannel's reply view) — no host-side copy of either stream."""
         lib = self.ctx.lib
         consumed, out_len = ctypes.c_size_t(), ctypes.c_size_t()
         stream = torch.cuda.current_stream(self.ctx.device)
@@ -59,6 +62,6 @@ class FrameServer:
                 self._grow("_out", out_len.value)
                 continue
             check(self.ctx.h, rc)
-            return bytes(self._out[: out_len.value].numpy()), consumed.value
+            return self._out[: out_len.value], consumed.value
         check(self.ctx.h, rc)
-        return b"", 0
+        return self._out[:0], 0

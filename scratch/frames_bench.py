@@ -31,8 +31,8 @@ for k in (1, 2, 3):
     t0 = time.perf_counter()
     out, used = srv.serve_pinned(buf, len(reqs[k]))
     dt = time.perf_counter() - t0
-    print(f"serve_pinned: {len(reqs[k])/1e6:.0f} MB in, {len(out)/1e6:.0f} MB out in {dt*1e3:.1f} ms -> "
-          f"{(len(reqs[k]) + len(out))/dt/1e9:.1f} GB/s, {n*t/dt:.0f} tokens/s for one Q layer")
+    print(f"serve_pinned: {len(reqs[k])/1e6:.0f} MB in, {out.numel()/1e6:.0f} MB out in {dt*1e3:.1f} ms -> "
+          f"{(len(reqs[k]) + out.numel())/dt/1e9:.1f} GB/s, {n*t/dt:.0f} tokens/s for one Q layer")
 # host codec cost of the reference path for the same stream (numpy frombuffer/astype + tobytes)
 t0 = time.perf_counter()
 pos, b = 0, reqs[1]
