@@ -450,6 +450,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="13b", choices=sorted(WORKLOADS))
     ap.add_argument("--clients", type=int, default=0, help="override the workload's client count")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="library tuning option key=value (ss_set_option), e.g. gemm_2cta=1, group_m=8")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--skip-e2e", action="store_true")
@@ -520,6 +522,12 @@ def main():
         ex, plan, specs, wl = build_gpu_workload(args.workload, device, rank)
         step_fn = lambda: run_step(plan, stream)  # noqa: E731
     ctx = ex.ctx
+    for kv in args.opt:
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
+    if args.opt and not tp_mode:   # options change kernel / tile choice: rebuild the plans
+        ex, plan, specs, wl = ex, [ex.compile_dispatch(d.pass_kind, d.key[0], d.key[1], d.segments) for d in plan], specs, wl
+        step_fn = lambda: run_step(plan, stream)  # noqa: E731
     stream = torch.cuda.current_stream(device)
     for _ in range(max(3, args.warmup)):
         step_fn()

@@ -111,9 +111,10 @@ struct ss_ctx {
   bool any_compute = false;
   int64_t launches = 0;
   int group_m = 16;
-  // -1 auto: CTA-pair kernel for K <= 8192 (smem-bandwidth-bound shapes), single-CTA kernel
-  // for long K (the pair's larger raster footprint doubles DRAM traffic there and the
-  // power-capped clock drops; profiles/r01_gemm_variants.md). 1 / 0 force one kernel.
+  // -1 auto: CTA-pair kernel whenever the dispatch has at least half an SM-pair wave of
+  // 256 x 256 tiles, else the single-CTA kernel with 256/128/64-wide tiles. (Round-1 v1 used the
+  // single-CTA kernel for K > 8192; with the current epilogue the pair wins there too: 13B step
+  // 699 vs 713 ms, profiles/r01_gemm_variants.md.) 1 / 0 force one kernel.
   int gemm_2cta = -1;
   int direct_tiles = 1;  // 1: TMA-load whole tiles of bf16 segments in place (no gather)
   int force_tbn = 0;     // testing: force the single-CTA tile width (64 / 128 / 256)
@@ -445,7 +446,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   // Kernel / tile choice depends only on the layer shape and the dispatch size, never on which
   // segments are present; every choice reduces K in the same order (bitwise-equal rows).
   const int n256 = (N + BN - 1) / BN;
-  const bool pair = ctx->gemm_2cta < 0 ? (K <= 8192 && ((M + BM2 - 1) / BM2) * n256 >= ctx->num_sms / 2)
+  const bool pair = ctx->gemm_2cta < 0 ? (((M + BM2 - 1) / BM2) * n256 >= ctx->num_sms / 2)
                                        : ctx->gemm_2cta != 0;
   const int TM = pair ? BM2 : BM;
   int tbn = BN;

@@ -113,8 +113,9 @@ class Dispatch:
     For device-resident clients whose exchange buffers do not move (DeviceChannel after its
     first grow). ``run`` is capturable in a CUDA graph (``GpuBaseExecutor.capture``)."""
 
-    def __init__(self, ctx: SsContext, pass_kind: int, key, segs):
+    def __init__(self, ctx: SsContext, pass_kind: int, key, segs, segments=None):
         self.ctx, self.pass_kind, self.key = ctx, pass_kind, key
+        self.segments = segments          # the (client, src, dst, base) tuples it was built from
         self.plan = ctx.plan(pass_kind, key[0], key[1], segs)
         self.rows = sum(int(s.src.shape[0]) for s in segs)
         bad = [s for s in self.plan.status if s != _lib.SS_SEG_OK]
@@ -263,7 +264,7 @@ class GpuBaseExecutor:
                     base=base if pass_kind != PASS_BACKWARD else None,
                     adapter=key in self._fused.get(c, ()))
                 for c, src, dst, base in segments]
-        return Dispatch(self.ctx, pass_kind, key, segs)
+        return Dispatch(self.ctx, pass_kind, key, segs, list(segments))
 
     def capture(self, dispatches, stream: torch.cuda.Stream | None = None) -> torch.cuda.CUDAGraph:
         """Capture a sequence of prebuilt dispatches into one CUDA graph (replay = one launch
