@@ -7,8 +7,9 @@
 //                         for both) into per-segment blocks of one Q buffer; this kernel then contracts over the TOKEN axis:
 //                         D[128 rows of d_in | d_out, npad] = Src^T . Q, with Src = x (grad_a)
 //                         or g (grad_b) loaded MN-major straight from the client's rows.
-//   K7 ia3_grad_kernel  : grad_l = sum_rows dy * y_base (ClientModel._layer_backward,
-//                         reference client.py:291-293), a deterministic column reduction.
+//   K7 ia3_grad_*       : grad_l = sum_rows dy * y_base (ClientModel._layer_backward,
+//                         reference client.py:291-293), a deterministic two-phase column
+//                         reduction (128-row chunk sums, then chunk-ordered totals).
 //
 // Both are HBM-bound (each reads the client's saved activations once; LoRA: 2*r FLOP per
 // byte of x / g per contraction), so they run 2 CTAs per SM.
@@ -175,15 +176,6 @@ struct Ia3GradSeg {
   int64_t yb_ld;
   float* dl;            // [d_out]
 };
-struct Ia3GradItem {
-  int32_t seg;
-  int32_t c0;           // first of 256 columns
-};
-struct Ia3GradParams {
-  int d_out;
-  const Ia3GradSeg* segs;
-  const Ia3GradItem* items;
-};
 
 __device__ __forceinline__ void load8(const void* base, int64_t off, bool bf, bool vec, int ncols,
                                       float (&v)[8]) {
@@ -212,24 +204,52 @@ __device__ __forceinline__ void load8(const void* base, int64_t off, bool bf, bo
   }
 }
 
-// Block = 1024 threads over 256 columns: lane group cg owns 8 columns, warp rg (of 32) strides
-// the rows by 32; the 32 partial sums per column are added in fixed order (deterministic, no
-// atomics). 32 warps per block keep enough loads in flight to stream dy / y_base from HBM.
-constexpr int IA3_THREADS = 1024;
-constexpr int IA3_RG = IA3_THREADS / 32;
+// Two deterministic phases, balanced over the SMs: K7a = one 256-thread block per (segment,
+// 256 columns, 128-row chunk) — lane group cg owns 8 columns, warp rg takes every 8th row of the
+// chunk — writes the chunk's column sums (fixed-order warp partials) to a workspace; K7b adds the
+// chunk sums of each (segment, column) in chunk order into grad_l. No atomics: the result does
+// not depend on scheduling (or on which other clients share the call).
+constexpr int IA3_ROWS = 128;
+constexpr int IA3_COLS = 256;
 
-__global__ void __launch_bounds__(IA3_THREADS) ia3_grad_kernel(const Ia3GradParams p) {
-  __shared__ float part[IA3_RG][257];
-  const Ia3GradItem it = p.items[blockIdx.x];
+struct Ia3PartItem {
+  int32_t seg;
+  int32_t c0;           // first of 256 columns
+  int32_t r0;           // first row of the 128-row chunk
+  int32_t part;         // workspace row of this item's 256 partial sums
+};
+struct Ia3FinItem {
+  int32_t seg;
+  int32_t c0;
+  int32_t part0;        // workspace row of chunk 0; chunks follow consecutively
+  int32_t nchunk;
+};
+struct Ia3PartParams {
+  int d_out;
+  const Ia3GradSeg* segs;
+  const Ia3PartItem* items;
+  float* part;          // [n_items, 256]
+};
+struct Ia3FinParams {
+  int d_out;
+  const Ia3GradSeg* segs;
+  const Ia3FinItem* items;
+  const float* part;
+};
+
+__global__ void __launch_bounds__(256) ia3_grad_partial_kernel(const Ia3PartParams p) {
+  __shared__ float sm[8][IA3_COLS + 1];
+  const Ia3PartItem it = p.items[blockIdx.x];
   const Ia3GradSeg sg = p.segs[it.seg];
   const int cg = threadIdx.x & 31, rg = threadIdx.x >> 5;
   const int c = it.c0 + cg * 8;
   const int ncols = max(0, min(8, p.d_out - c));
   const bool dbf = sg.flags & 1, bbf = sg.flags & 2, vec = sg.flags & 4;
+  const int r1 = min(sg.rows, it.r0 + IA3_ROWS);
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (ncols > 0) {
 #pragma unroll 4
-    for (int r = rg; r < sg.rows; r += IA3_RG) {
+    for (int r = it.r0 + rg; r < r1; r += 8) {
       float a[8], b[8];
       load8(sg.dy, (int64_t)r * sg.dy_ld + c, dbf, vec, ncols, a);
       load8(sg.yb, (int64_t)r * sg.yb_ld + c, bbf, vec, ncols, b);
@@ -238,18 +258,23 @@ __global__ void __launch_bounds__(IA3_THREADS) ia3_grad_kernel(const Ia3GradPara
     }
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) part[rg][cg * 8 + i] = acc[i];
+  for (int i = 0; i < 8; ++i) sm[rg][cg * 8 + i] = acc[i];
   __syncthreads();
-  if (threadIdx.x < 256) {
-    const int col = it.c0 + threadIdx.x;
-    if (col < p.d_out) {
-      float s = 0.f;
-#pragma unroll 8
-      for (int g = 0; g < IA3_RG; ++g) s += part[g][threadIdx.x];
-      float* o = sg.dl + col;
-      *o = (sg.flags & 8) ? *o + s : s;
-    }
-  }
+  float s = 0.f;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) s += sm[g][threadIdx.x];
+  p.part[(int64_t)it.part * IA3_COLS + threadIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) ia3_grad_finalize_kernel(const Ia3FinParams p) {
+  const Ia3FinItem it = p.items[blockIdx.x];
+  const int col = it.c0 + threadIdx.x;
+  if (col >= p.d_out) return;
+  const Ia3GradSeg sg = p.segs[it.seg];
+  float s = 0.f;
+  for (int k = 0; k < it.nchunk; ++k) s += p.part[(int64_t)(it.part0 + k) * IA3_COLS + threadIdx.x];
+  float* o = sg.dl + col;
+  *o = (sg.flags & 8) ? *o + s : s;
 }
 
 }  // namespace ss

@@ -133,6 +133,8 @@ struct ss_ctx {
   // adapter-gradient workspace: s*x.A and s*g.B^T per segment (Qx, Qg)
   __nv_bfloat16* qx = nullptr;   // [s*x.A ; s*g.B^T]
   size_t qx_cap = 0;
+  char* ia3_part = nullptr;       // IA3 grad_l chunk sums
+  size_t ia3_part_cap = 0;
 };
 
 namespace {
@@ -266,10 +268,12 @@ int grow_packs(ss_ctx* ctx, Layer& L, int need_rows) {
   return encode_2d(ctx, &L.tm_b, L.b_pack, L.d_out, cap, L.ld_b, 64, LORA_CHUNK);
 }
 
+// Grow-only device workspace. `plan_visible`: prebuilt plans embed this buffer's address (X,
+// LoRA operand, row_seg), so growing it must tell them to rebuild.
 template <typename T>
-int ensure_dev(ss_ctx* ctx, T*& ptr, size_t& cap, size_t bytes) {
+int ensure_dev(ss_ctx* ctx, T*& ptr, size_t& cap, size_t bytes, bool plan_visible = true) {
   if (bytes <= cap) return SS_OK;
-  ctx->ws_epoch++;
+  if (plan_visible) ctx->ws_epoch++;
   size_t n = std::max(bytes, cap + cap / 2);
   n = round_up((int64_t)n, 1 << 20);
   if (ptr) CK(cudaFree(ptr));
@@ -881,6 +885,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   cudaFree(ctx->a_lora);
   cudaFree(ctx->row_seg);
   cudaFree(ctx->qx);
+  cudaFree(ctx->ia3_part);
   cudaFree(ctx->fr_in);
   cudaFree(ctx->fr_out);
   cudaFree(ctx->fr_x);
@@ -1296,8 +1301,20 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
   std::vector<CUtensorMap> tmaps(std::max<size_t>(1, 4 * lg.size()));
   std::vector<ShrinkItem> sitems;   // x items (pack 0 = A^T rows, K = d_in), then g items (pack 1 = B rows, K = d_out)
   std::vector<LoraGradItem> gitems;
+  // Clients are processed in groups whose x + g fit comfortably in L2 (126 MB): K3 of a group
+  // streams its x / g from HBM, K6 right after re-reads them mostly from L2.
+  struct GradGroup { int s0, s1, g0, g1; };
+  std::vector<GradGroup> groups;
+  const double l2_budget = 48.0 * (1 << 20);
+  double gbytes = 0;
   int rc = SS_OK;
   for (size_t j = 0; j < lg.size(); ++j) {
+    const double segb = (double)lsrc[j]->rows * (d_in + d_out) * 2.0;
+    if (groups.empty() || (gbytes > 0 && gbytes + segb > l2_budget)) {
+      groups.push_back(GradGroup{(int)sitems.size(), (int)sitems.size(), (int)gitems.size(), (int)gitems.size()});
+      gbytes = 0;
+    }
+    gbytes += segb;
     const ss_grad_seg& s = *lsrc[j];
     if ((rc = encode_2d(ctx, &tmaps[4 * j + 0], s.x, d_in, s.rows, s.x_ld, 64, BM))) return rc;
     if ((rc = encode_2d(ctx, &tmaps[4 * j + 1], s.dy, d_out, s.rows, s.dy_ld, 64, BM))) return rc;
@@ -1312,10 +1329,18 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     }
     for (int m = 0; m < d_in; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 0, m, 0});
     for (int m = 0; m < d_out; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 1, m, 0});
+    groups.back().s1 = (int)sitems.size();
+    groups.back().g1 = (int)gitems.size();
   }
-  std::vector<Ia3GradItem> iitems;
+  std::vector<Ia3PartItem> pitems;
+  std::vector<Ia3FinItem> fitems;
   for (size_t j = 0; j < ig.size(); ++j)
-    for (int c = 0; c < d_out; c += 256) iitems.push_back(Ia3GradItem{(int32_t)j, c});
+    for (int c = 0; c < d_out; c += IA3_COLS) {
+      const int nch = (ig[j].rows + IA3_ROWS - 1) / IA3_ROWS;
+      fitems.push_back(Ia3FinItem{(int32_t)j, c, (int32_t)pitems.size(), nch});
+      for (int k = 0; k < nch; ++k)
+        pitems.push_back(Ia3PartItem{(int32_t)j, c, k * IA3_ROWS, (int32_t)pitems.size()});
+    }
 
   auto sz = [](size_t n, size_t e) { return round_up((int64_t)std::max<size_t>(1, n) * e, 256); };
   const size_t o_tm = 0;
@@ -1325,7 +1350,8 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
   const size_t o_gi = o_ix + sz(sitems.size(), sizeof(ShrinkItem));
   const size_t o_is = o_gi + sz(gitems.size(), sizeof(LoraGradItem));
   const size_t o_ii = o_is + sz(ig.size(), sizeof(Ia3GradSeg));
-  const size_t total = o_ii + sz(iitems.size(), sizeof(Ia3GradItem));
+  const size_t o_if = o_ii + sz(pitems.size(), sizeof(Ia3PartItem));
+  const size_t total = o_if + sz(fitems.size(), sizeof(Ia3FinItem));
   Staging* stp = nullptr;
   if ((rc = acquire_staging(ctx, total, stp))) return rc;
   char* h = static_cast<char*>(stp->host);
@@ -1338,7 +1364,8 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
   }
   if (!ig.empty()) {
     memcpy(h + o_is, ig.data(), ig.size() * sizeof(Ia3GradSeg));
-    memcpy(h + o_ii, iitems.data(), iitems.size() * sizeof(Ia3GradItem));
+    memcpy(h + o_ii, pitems.data(), pitems.size() * sizeof(Ia3PartItem));
+    memcpy(h + o_if, fitems.data(), fitems.size() * sizeof(Ia3FinItem));
   }
   CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
   CK(cudaMemcpyAsync(stp->dev, stp->host, total, cudaMemcpyHostToDevice, stream));
@@ -1348,7 +1375,7 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
 
   if (!lg.empty()) {
     const size_t qbytes = (size_t)2 * qrows * qld * 2;
-    if ((rc = ensure_dev(ctx, ctx->qx, ctx->qx_cap, qbytes))) return rc;
+    if ((rc = ensure_dev(ctx, ctx->qx, ctx->qx_cap, qbytes, false))) return rc;
     ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap + ctx->qx_cap);
     CK(cudaMemsetAsync(ctx->qx, 0, qbytes, stream));
     double fl = 0, by = 0;
@@ -1358,19 +1385,15 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
       by += t * (d_in + d_out) * 2.0 + r * (d_in + d_out) * (4.0 + 2.0);
     }
     const int pi = prof_begin(ctx, stream, SS_KERNEL_GRAD, fl, by);
-    // K3 (one launch): Q[0, qrows) = s * x.A (pack A^T rows, K = d_in),
-    //                  Q[qrows, 2 qrows) = s * g.B^T (pack B rows, K = d_out)
+    // per client group: K3 (one launch for both shrinks) Q[0, qrows) = s * x.A (pack A^T rows,
+    // K = d_in), Q[qrows, 2 qrows) = s * g.B^T (pack B rows, K = d_out); then K6 token contractions
     ShrinkParams sp;
     sp.lora_ld = qld;
     sp.segs = reinterpret_cast<const DevSeg*>(dv + o_sh);
     sp.tmaps = reinterpret_cast<const CUtensorMap*>(dv + o_tm);
     sp.K = d_in;
     sp.K2 = d_out;
-    sp.items = reinterpret_cast<const ShrinkItem*>(dv + o_ix);
     sp.a_lora = ctx->qx;
-    lora_shrink_kernel<<<(int)sitems.size(), GEMM_THREADS, SHRINK_SMEM, stream>>>(L.tm_at, L.tm_b, sp);
-    CK(cudaGetLastError());
-    // K6: token contractions
     CUtensorMap tmQ;
     if ((rc = encode_2d(ctx, &tmQ, ctx->qx, qld, 2 * qrows, qld, 64, 64))) return rc;
     LoraGradParams gp;
@@ -1378,25 +1401,41 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     gp.d_out = d_out;
     gp.qrows = (int)qrows;
     gp.segs = reinterpret_cast<const LoraGradSeg*>(dv + o_lg);
-    gp.items = reinterpret_cast<const LoraGradItem*>(dv + o_gi);
     gp.tmaps = reinterpret_cast<const CUtensorMap*>(dv + o_tm);
-    lora_grad_kernel<<<(int)gitems.size(), GEMM_THREADS, GRAD_SMEM, stream>>>(tmQ, gp);
-    CK(cudaGetLastError());
+    for (const GradGroup& g : groups) {
+      sp.items = reinterpret_cast<const ShrinkItem*>(dv + o_ix) + g.s0;
+      lora_shrink_kernel<<<g.s1 - g.s0, GEMM_THREADS, SHRINK_SMEM, stream>>>(L.tm_at, L.tm_b, sp);
+      CK(cudaGetLastError());
+      gp.items = reinterpret_cast<const LoraGradItem*>(dv + o_gi) + g.g0;
+      lora_grad_kernel<<<g.g1 - g.g0, GEMM_THREADS, GRAD_SMEM, stream>>>(tmQ, gp);
+      CK(cudaGetLastError());
+      ctx->launches += 2;
+    }
     prof_end(ctx, stream, pi);
-    ctx->launches += 2;
   }
   if (!ig.empty()) {
     double by = 0;
     for (const Ia3GradSeg& g : ig) by += (double)g.rows * d_out * (((g.flags & 1) ? 2 : 4) + ((g.flags & 2) ? 2 : 4)) + d_out * 4.0;
     const int pi = prof_begin(ctx, stream, SS_KERNEL_GRAD, 2.0 * by / 4, by);
-    Ia3GradParams ip;
-    ip.d_out = d_out;
-    ip.segs = reinterpret_cast<const Ia3GradSeg*>(dv + o_is);
-    ip.items = reinterpret_cast<const Ia3GradItem*>(dv + o_ii);
-    ia3_grad_kernel<<<(int)iitems.size(), IA3_THREADS, 0, stream>>>(ip);
+    float* part = nullptr;
+    if ((rc = ensure_dev(ctx, ctx->ia3_part, ctx->ia3_part_cap, pitems.size() * IA3_COLS * sizeof(float), false))) return rc;
+    part = reinterpret_cast<float*>(ctx->ia3_part);
+    Ia3PartParams pp;
+    pp.d_out = d_out;
+    pp.segs = reinterpret_cast<const Ia3GradSeg*>(dv + o_is);
+    pp.items = reinterpret_cast<const Ia3PartItem*>(dv + o_ii);
+    pp.part = part;
+    ia3_grad_partial_kernel<<<(int)pitems.size(), 256, 0, stream>>>(pp);
+    CK(cudaGetLastError());
+    Ia3FinParams fp;
+    fp.d_out = d_out;
+    fp.segs = pp.segs;
+    fp.items = reinterpret_cast<const Ia3FinItem*>(dv + o_if);
+    fp.part = part;
+    ia3_grad_finalize_kernel<<<(int)fitems.size(), 256, 0, stream>>>(fp);
     CK(cudaGetLastError());
     prof_end(ctx, stream, pi);
-    ctx->launches += 1;
+    ctx->launches += 2;
   }
   CK(cudaEventRecord(ctx->compute_done, stream));
   ctx->any_compute = true;
@@ -1504,9 +1543,9 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
   for (auto& hs : ctx->hslot) {
     if (hs.in_cap < in_need || hs.out_cap < out_need || hs.base_cap < base_need) {
       if (hs.used) CK(cudaEventSynchronize(hs.ev_out));
-      if (hs.in_cap < in_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.in), hs.in_cap, in_need))) return rc;
-      if (hs.out_cap < out_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.out), hs.out_cap, out_need))) return rc;
-      if (hs.base_cap < base_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.base), hs.base_cap, base_need))) return rc;
+      if (hs.in_cap < in_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.in), hs.in_cap, in_need, false))) return rc;
+      if (hs.out_cap < out_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.out), hs.out_cap, out_need, false))) return rc;
+      if (hs.base_cap < base_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.base), hs.base_cap, base_need, false))) return rc;
     }
   }
   ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap + ctx->qx_cap +
@@ -1758,10 +1797,10 @@ extern "C" int ss_serve_frames(ss_ctx* ctx, const uint8_t* in, size_t in_len, si
     }
   }
   int rc = SS_OK;
-  if ((rc = ensure_dev(ctx, ctx->fr_in, ctx->fr_in_cap, round_up(in_len, 256) + 256))) return rc;
-  if ((rc = ensure_dev(ctx, ctx->fr_out, ctx->fr_out_cap, round_up(need, 256) + 256))) return rc;
-  if ((rc = ensure_dev(ctx, ctx->fr_x, ctx->fr_x_cap, (size_t)std::max<int64_t>(x_elems, 8) * 2))) return rc;
-  if ((rc = ensure_dev(ctx, ctx->fr_o, ctx->fr_o_cap, (size_t)std::max<int64_t>(o_elems, 4) * 4))) return rc;
+  if ((rc = ensure_dev(ctx, ctx->fr_in, ctx->fr_in_cap, round_up(in_len, 256) + 256, false))) return rc;
+  if ((rc = ensure_dev(ctx, ctx->fr_out, ctx->fr_out_cap, round_up(need, 256) + 256, false))) return rc;
+  if ((rc = ensure_dev(ctx, ctx->fr_x, ctx->fr_x_cap, (size_t)std::max<int64_t>(x_elems, 8) * 2, false))) return rc;
+  if ((rc = ensure_dev(ctx, ctx->fr_o, ctx->fr_o_cap, (size_t)std::max<int64_t>(o_elems, 4) * 4, false))) return rc;
   const size_t t_bytes = round_up(fd.size() * sizeof(FrameDesc), 256);
   const size_t total = t_bytes + round_up(std::max<size_t>(1, msgs.size()), 256);
   Staging* stp = nullptr;
