@@ -687,6 +687,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 // The shrink is HBM-bound (it re-reads the LoRA segments' rows once, N = rank is tiny), so it
 // runs 2 CTAs per SM (110 KB smem, 256 TMEM columns each) with as many pipeline stages as the
 // item's rank leaves room for: stage = 16 KB of A + rank_pad x 128 B of the pack.
+//
+// K is split into fixed chunks of SHRINK_KB_CHUNK k-blocks (blockIdx.y = chunk): a slab of a
+// few decode rows would otherwise be one CTA walking all of K serially, and a prefill dispatch
+// would be one unbalanced wave. Each chunk's fp32 partial goes to a workspace; the LAST chunk
+// CTA of the slab to finish (atomic ticket) adds the partials in chunk order 0..S-1, scales,
+// rounds to bf16 and writes A_lora. The chunking depends only on K, and the order of every sum
+// is fixed, so a row's result never depends on the dispatch it rides in (batching invisible).
+constexpr int SHRINK_KB_CHUNK = 20;   // default k-blocks per chunk (1280 of K); ss_set_option("shrink_kb_chunk")
 constexpr int SHRINK_MAXN = 256;
 constexpr int SHRINK_MAX_STAGES = 12;
 constexpr int SHRINK_SMEM = 110 * 1024;
@@ -709,7 +717,16 @@ struct ShrinkParams {
   const ShrinkItem* items;
   const CUtensorMap* tmaps;
   __nv_bfloat16* a_lora;
+  float* part;            // [items, max chunks, 128, part_ld] fp32 chunk partials
+  int part_ld;            // >= every item's rank_pad
+  int max_chunks;         // gridDim.y
+  int* ticket;            // [items] arrival counters (zero between launches)
+  int kb_chunk;           // k-blocks per chunk (a per-context constant: the chunking must not vary)
 };
+
+__host__ __device__ inline int shrink_chunks(int K, int kb_chunk) {
+  return ((K + BK - 1) / BK + kb_chunk - 1) / kb_chunk;
+}
 
 __global__ void __launch_bounds__(GEMM_THREADS, 2)
     lora_shrink_kernel(const __grid_constant__ CUtensorMap tmP,   // pack [R, K] (K-major rows)
@@ -726,14 +743,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
   const CUtensorMap* tmA = p.tmaps + it.amap;
   const CUtensorMap* tmPk = it.pack ? &tmP2 : &tmP;
   const int Kc = it.pack ? p.K2 : p.K;
+  const int nkb_all = (Kc + BK - 1) / BK;
+  const int nchk = shrink_chunks(Kc, p.kb_chunk);
+  // whole mode (gridDim.y == 1): this CTA runs every chunk of the slab, double-buffering the
+  // chunk accumulators in TMEM and summing them in registers (npad <= 64); split mode: one
+  // chunk per CTA, partials through the workspace, the slab's last CTA sums them. Both add the
+  // chunk partials in the same order, so the two modes give bitwise-identical rows.
+  const bool whole = gridDim.y == 1;
+  const int c0 = whole ? 0 : (int)blockIdx.y;
+  const int c1 = whole ? nchk : c0 + 1;
+  if (c0 >= nchk) return;   // (gradient launches mix two K's; uniform exit before any barrier)
   const int b_bytes = npad * BK * 2;
   const int stage_bytes = A_STAGE_BYTES + b_bytes;
   const int SHRINK_STAGES = min(SHRINK_MAX_STAGES, (SHRINK_SMEM - 2048) / stage_bytes);
   // barriers in the first KB, then stages (each A | B, 1 KB aligned)
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty_bar = full_bar + SHRINK_MAX_STAGES;
-  uint64_t* tfull = empty_bar + SHRINK_MAX_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty_bar + SHRINK_MAX_STAGES;     // [2]
+  uint64_t* tempty = tfull + 2;                        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint8_t* stage0 = smem + 1024;
 #define SHRINK_A(s) (stage0 + (s) * stage_bytes)
 #define SHRINK_B(s) (stage0 + (s) * stage_bytes + A_STAGE_BYTES)
@@ -748,7 +776,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 256);
@@ -756,14 +787,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int nkb = (Kc + BK - 1) / BK;
   const int nchunk = npad / LORA_CHUNK;
+  __shared__ int last_flag;
 
   if (warp == 0) {
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
+      for (int kb = c0 * p.kb_chunk; kb < min(nkb_all, c1 * p.kb_chunk); ++kb) {
         mbar_wait(&empty_bar[s], ph ^ 1);
         mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nchunk * LORA_CHUNK_BYTES);
         tma_load_2d(SHRINK_A(s), tmA, &full_bar[s], kb * BK, it.arow);
@@ -777,46 +808,138 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
     const uint32_t idesc = make_idesc_bf16(BM, (uint32_t)npad, false, false);
     int s = 0;
     uint32_t ph = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
-      mbar_wait(&full_bar[s], ph);
+    for (int c = c0; c < c1; ++c) {
+      const int buf = (c - c0) & 1;
+      const uint32_t tph = (((c - c0) >> 1) & 1) ^ 1;
+      mbar_wait(&tempty[buf], tph);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t a_addr = smem_u32(SHRINK_A(s));
-        const uint32_t b_addr = smem_u32(SHRINK_B(s));
+      const uint32_t d_tmem = tmem_base + buf * 128;
+      const int kb0 = c * p.kb_chunk, kb1 = min(nkb_all, kb0 + p.kb_chunk);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(SHRINK_A(s));
+          const uint32_t b_addr = smem_u32(SHRINK_B(s));
 #pragma unroll
-        for (int k = 0; k < BK / UK; ++k)
-          mma_bf16_ss(tmem_base, make_sdesc_sw128(a_addr + k * 32, 16, 1024),
-                      make_sdesc_sw128(b_addr + k * 32, 16, 1024), idesc, (kb | k) != 0);
-        mma_commit(&empty_bar[s]);
+          for (int k = 0; k < BK / UK; ++k)
+            mma_bf16_ss(d_tmem, make_sdesc_sw128(a_addr + k * 32, 16, 1024),
+                        make_sdesc_sw128(b_addr + k * 32, 16, 1024), idesc, (kb != kb0 || k != 0));
+          mma_commit(&empty_bar[s]);
+        }
+        __syncwarp();
+        if (++s == SHRINK_STAGES) { s = 0; ph ^= 1; }
       }
+      if (lane == 0) mma_commit(&tfull[buf]);
       __syncwarp();
-      if (++s == SHRINK_STAGES) { s = 0; ph ^= 1; }
     }
-    if (lane == 0) mma_commit(tfull);
-    __syncwarp();
   } else if (warp >= 4) {
     const uint32_t ew = warp - 4;
     const int lr = ew * 32 + lane;  // row within the item
-    mbar_wait(tfull, 0);
-    tc_fence_after();
     const bool ok = lr < it.rows;
     __nv_bfloat16* out = p.a_lora + (int64_t)(it.orow + lr) * p.lora_ld + it.col0;
-    for (int c = 0; c < nchunk; ++c) {
-      uint32_t r[16];
-      tmem_ld_32x32b_x16(tmem_base + c * 16 + ((ew * 32u) << 16), r);
-      tmem_wait_ld();
-      if (ok) {
-        float v[16];
+    auto store_bf16 = [&](int c, const float* v) {
+      uint4* o = reinterpret_cast<uint4*>(out + c * 16);
+      o[0] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                        pack_bf16x2(v[6], v[7]));
+      o[1] = make_uint4(pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]),
+                        pack_bf16x2(v[12], v[13]), pack_bf16x2(v[14], v[15]));
+    };
+    if (whole && nchk > 1) {
+      // running fp32 sums of the chunk partials, in chunk order (npad <= 64: host-guaranteed)
+      float acc[64];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) * sg.lora_scale;
-        uint4* o = reinterpret_cast<uint4*>(out + c * 16);
-        o[0] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
-                          pack_bf16x2(v[6], v[7]));
-        o[1] = make_uint4(pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]),
-                          pack_bf16x2(v[12], v[13]), pack_bf16x2(v[14], v[15]));
+      for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+      for (int c = c0; c < c1; ++c) {
+        const int buf = (c - c0) & 1;
+        mbar_wait(&tfull[buf], ((c - c0) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          if (g < nchunk) {
+            uint32_t r[16];
+            tmem_ld_32x32b_x16(tmem_base + buf * 128 + g * 16 + ((ew * 32u) << 16), r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[g * 16 + j] += __uint_as_float(r[j]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+      }
+      if (ok) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          if (g < nchunk) {
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = acc[g * 16 + j] * sg.lora_scale;
+            store_bf16(g, v);
+          }
+        }
+      }
+    } else if (nchk == 1) {
+      mbar_wait(&tfull[0], 0);
+      tc_fence_after();
+      for (int c = 0; c < nchunk; ++c) {
+        uint32_t r[16];
+        tmem_ld_32x32b_x16(tmem_base + c * 16 + ((ew * 32u) << 16), r);
+        tmem_wait_ld();
+        if (ok) {
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) * sg.lora_scale;
+          store_bf16(c, v);
+        }
+      }
+      tc_fence_before();
+    } else {
+      // split mode: this chunk's fp32 partial -> workspace, the slab's last chunk sums in order
+      mbar_wait(&tfull[0], 0);
+      tc_fence_after();
+      float* mine = p.part + (((int64_t)blockIdx.x * p.max_chunks + c0) * BM + lr) * p.part_ld;
+      for (int c = 0; c < nchunk; ++c) {
+        uint32_t r[16];
+        tmem_ld_32x32b_x16(tmem_base + c * 16 + ((ew * 32u) << 16), r);
+        tmem_wait_ld();
+        if (ok) {
+          float4* o = reinterpret_cast<float4*>(mine + c * 16);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            __stcg(o + j, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                      __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+        }
+      }
+      tc_fence_before();
+      __threadfence();
+      named_bar_sync(1, 128);
+      if (ew == 0 && lane == 0) last_flag = atomicAdd(p.ticket + blockIdx.x, 1) == nchk - 1;
+      named_bar_sync(1, 128);
+      if (last_flag) {
+        __threadfence();
+        if (ok) {
+          const float* base = p.part + ((int64_t)blockIdx.x * p.max_chunks * BM + lr) * p.part_ld;
+          for (int c = 0; c < nchunk; ++c) {
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+            for (int q = 0; q < nchk; ++q) {
+              const float4* src = reinterpret_cast<const float4*>(base + (int64_t)q * BM * p.part_ld + c * 16);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 f = __ldcg(src + j);
+                v[4 * j] += f.x; v[4 * j + 1] += f.y; v[4 * j + 2] += f.z; v[4 * j + 3] += f.w;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] *= sg.lora_scale;
+            store_bf16(c, v);
+          }
+        }
+        if (ew == 0 && lane == 0) p.ticket[blockIdx.x] = 0;   // ready for the next launch
       }
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (warp == 2) {

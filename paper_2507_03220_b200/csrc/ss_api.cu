@@ -120,6 +120,8 @@ struct ss_ctx {
   int force_tbn = 0;     // testing: force the single-CTA tile width (64 / 128 / 256)
   int tma_store = 1;     // 1: bf16 outputs leave through swizzled smem + TMA bulk stores
   int pair_n = 256;      // CTA-pair tile width: 256 (double-buffered TMEM) or 512
+  int shrink_kb_chunk = SHRINK_KB_CHUNK;  // K-split of the LoRA shrink (k-blocks of 64 per chunk)
+  int shrink_mode = 0;   // 0 auto, 1 one CTA per slab (all chunks), 2 one CTA per (slab, chunk)
   int64_t weight_bytes = 0, adapter_bytes = 0;
   // Plans (ss_plan_*) cache routing tables that embed workspace and adapter pointers; these
   // counters tell a plan to rebuild itself after the workspace grew or an adapter moved.
@@ -135,6 +137,10 @@ struct ss_ctx {
   size_t qx_cap = 0;
   char* ia3_part = nullptr;       // IA3 grad_l chunk sums
   size_t ia3_part_cap = 0;
+  float* shrink_part = nullptr;   // K-split shrink: fp32 chunk partials
+  size_t shrink_part_cap = 0;
+  int* shrink_ticket = nullptr;   // per shrink item arrival counters (zero between launches)
+  size_t shrink_ticket_cap = 0;
 };
 
 namespace {
@@ -330,6 +336,20 @@ void prof_drain(ss_ctx* ctx) {
   ctx->prof.clear();
 }
 
+// Workspace of a K-split shrink launch over `n_items` slabs (kernels.cuh, SHRINK_KB_CHUNK).
+// Tickets must be zero when a launch starts: fresh ones are cleared, the kernel resets its own.
+int ensure_shrink_ws(ss_ctx* ctx, size_t n_items, int max_chunks, int part_ld) {
+  int rc = ensure_dev(ctx, ctx->shrink_part, ctx->shrink_part_cap,
+                      std::max<size_t>(1, n_items * (size_t)max_chunks * BM * part_ld) * sizeof(float), false);
+  if (rc) return rc;
+  if (ctx->shrink_ticket_cap < n_items * sizeof(int)) {
+    rc = ensure_dev(ctx, ctx->shrink_ticket, ctx->shrink_ticket_cap, n_items * sizeof(int), false);
+    if (rc) return rc;
+    CK(cudaMemset(ctx->shrink_ticket, 0, ctx->shrink_ticket_cap));
+  }
+  return SS_OK;
+}
+
 // Next pinned-host + device staging slot for a dispatch's routing tables (ring of
 // kStagingSlots; a slot is reused only after the dispatch that last used it has copied it).
 int acquire_staging(ss_ctx* ctx, size_t total, Staging*& out) {
@@ -358,7 +378,8 @@ struct Built {
   int pass_kind = 0, block = 0, role = 0, K = 0, N = 0;
   int64_t M = 0, MX = 0, lora_ld = 64, al_rows = 0, ldx = 0;
   bool any_lora = false, pair = false;
-  int tbn = BN, pn = 256, num_m = 0, n_piece = 0, n_items = 0;
+  int tbn = BN, pn = 256, num_m = 0, n_piece = 0, n_items = 0, part_ld = 16, shrink_chunks_ = 1;
+  int kb_chunk = SHRINK_KB_CHUNK;
   size_t off_tm = 0, off_seg = 0, off_tile = 0, off_piece = 0, off_ch = 0, off_st = 0, off_it = 0;
   std::vector<char> blob;
   std::vector<int32_t> status;
@@ -619,6 +640,13 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   B.M = M; B.MX = MX; B.lora_ld = lora_ld; B.al_rows = al_rows; B.ldx = ldx;
   B.any_lora = any_lora; B.pair = pair; B.tbn = tbn; B.pn = ctx->pair_n;
   B.num_m = num_m; B.n_piece = (int)piece_seg.size(); B.n_items = (int)items.size();
+  if (any_lora) {
+    for (const ShrinkItem& it : items) B.part_ld = std::max(B.part_ld, ds[it.seg].rank_pad);
+    B.shrink_chunks_ = shrink_chunks(K, ctx->shrink_kb_chunk);
+    B.kb_chunk = ctx->shrink_kb_chunk;
+    int rc2 = ensure_shrink_ws(ctx, items.size(), B.shrink_chunks_, B.part_ld);
+    if (rc2) return rc2;
+  }
   // algorithmic work for the in-stream profiler
   for (size_t k = 0; k < piece_seg.size(); ++k) {
     const DevSeg& d = ds[piece_seg[k]];
@@ -693,9 +721,18 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     sp.items = reinterpret_cast<const ShrinkItem*>(dv + B.off_it);
     sp.tmaps = d_tmaps;
     sp.a_lora = ctx->a_lora;
+    sp.part = ctx->shrink_part;
+    sp.part_ld = B.part_ld;
+    sp.max_chunks = B.shrink_chunks_;
+    sp.kb_chunk = B.kb_chunk;
+    sp.ticket = ctx->shrink_ticket;
     const int pi = prof_begin(ctx, stream, SS_KERNEL_SHRINK, B.shrink_flops, B.shrink_bytes);
     sp.K2 = K;
-    lora_shrink_kernel<<<B.n_items, GEMM_THREADS, SHRINK_SMEM, stream>>>(bwd ? L.tm_b : L.tm_at,
+    // one CTA per slab walking every K chunk when there are enough slabs to fill the GPU and the
+    // ranks fit the register sums; else one CTA per (slab, chunk). Same sums either way.
+    const bool whole = B.shrink_chunks_ == 1 ||
+                       (B.part_ld <= 64 && (ctx->shrink_mode == 1 || (ctx->shrink_mode == 0 && B.n_items >= ctx->num_sms)));
+    lora_shrink_kernel<<<dim3(B.n_items, whole ? 1 : B.shrink_chunks_), GEMM_THREADS, SHRINK_SMEM, stream>>>(bwd ? L.tm_b : L.tm_at,
                                                                                bwd ? L.tm_b : L.tm_at, sp);
     prof_end(ctx, stream, pi);
     CK(cudaGetLastError());
@@ -886,6 +923,8 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   cudaFree(ctx->row_seg);
   cudaFree(ctx->qx);
   cudaFree(ctx->ia3_part);
+  cudaFree(ctx->shrink_part);
+  cudaFree(ctx->shrink_ticket);
   cudaFree(ctx->fr_in);
   cudaFree(ctx->fr_out);
   cudaFree(ctx->fr_x);
@@ -914,6 +953,16 @@ int ss_ctx_destroy(ss_ctx* ctx) {
 
 int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!ctx || !key) return SS_E_ARG;
+  if (!strcmp(key, "shrink_mode")) {
+    if (value < 0 || value > 2) return fail(ctx, SS_E_ARG, "shrink_mode must be 0 (auto), 1 (whole) or 2 (split)");
+    ctx->shrink_mode = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "shrink_kb_chunk")) {
+    if (value < 1) return fail(ctx, SS_E_ARG, "shrink_kb_chunk must be >= 1");
+    ctx->shrink_kb_chunk = (int)value;
+    return SS_OK;
+  }
   if (!strcmp(key, "pipeline_rows")) {
     if (value < 1) return fail(ctx, SS_E_ARG, "pipeline_rows must be >= 1");
     ctx->pipeline_rows = (int)value;
@@ -1301,20 +1350,8 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
   std::vector<CUtensorMap> tmaps(std::max<size_t>(1, 4 * lg.size()));
   std::vector<ShrinkItem> sitems;   // x items (pack 0 = A^T rows, K = d_in), then g items (pack 1 = B rows, K = d_out)
   std::vector<LoraGradItem> gitems;
-  // Clients are processed in groups whose x + g fit comfortably in L2 (126 MB): K3 of a group
-  // streams its x / g from HBM, K6 right after re-reads them mostly from L2.
-  struct GradGroup { int s0, s1, g0, g1; };
-  std::vector<GradGroup> groups;
-  const double l2_budget = 48.0 * (1 << 20);
-  double gbytes = 0;
   int rc = SS_OK;
   for (size_t j = 0; j < lg.size(); ++j) {
-    const double segb = (double)lsrc[j]->rows * (d_in + d_out) * 2.0;
-    if (groups.empty() || (gbytes > 0 && gbytes + segb > l2_budget)) {
-      groups.push_back(GradGroup{(int)sitems.size(), (int)sitems.size(), (int)gitems.size(), (int)gitems.size()});
-      gbytes = 0;
-    }
-    gbytes += segb;
     const ss_grad_seg& s = *lsrc[j];
     if ((rc = encode_2d(ctx, &tmaps[4 * j + 0], s.x, d_in, s.rows, s.x_ld, 64, BM))) return rc;
     if ((rc = encode_2d(ctx, &tmaps[4 * j + 1], s.dy, d_out, s.rows, s.dy_ld, 64, BM))) return rc;
@@ -1329,8 +1366,6 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     }
     for (int m = 0; m < d_in; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 0, m, 0});
     for (int m = 0; m < d_out; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 1, m, 0});
-    groups.back().s1 = (int)sitems.size();
-    groups.back().g1 = (int)gitems.size();
   }
   std::vector<Ia3PartItem> pitems;
   std::vector<Ia3FinItem> fitems;
@@ -1385,8 +1420,8 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
       by += t * (d_in + d_out) * 2.0 + r * (d_in + d_out) * (4.0 + 2.0);
     }
     const int pi = prof_begin(ctx, stream, SS_KERNEL_GRAD, fl, by);
-    // per client group: K3 (one launch for both shrinks) Q[0, qrows) = s * x.A (pack A^T rows,
-    // K = d_in), Q[qrows, 2 qrows) = s * g.B^T (pack B rows, K = d_out); then K6 token contractions
+    // K3 (one launch for both shrinks): Q[0, qrows) = s * x.A (pack A^T rows, K = d_in),
+    // Q[qrows, 2 qrows) = s * g.B^T (pack B rows, K = d_out); then K6 token contractions
     ShrinkParams sp;
     sp.lora_ld = qld;
     sp.segs = reinterpret_cast<const DevSeg*>(dv + o_sh);
@@ -1394,6 +1429,15 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     sp.K = d_in;
     sp.K2 = d_out;
     sp.a_lora = ctx->qx;
+    int part_ld = 16;
+    for (const DevSeg& d : sh) part_ld = std::max(part_ld, d.rank_pad);
+    const int max_chunks = std::max(shrink_chunks(d_in, ctx->shrink_kb_chunk), shrink_chunks(d_out, ctx->shrink_kb_chunk));
+    sp.kb_chunk = ctx->shrink_kb_chunk;
+    if ((rc = ensure_shrink_ws(ctx, sitems.size(), max_chunks, part_ld))) return rc;
+    sp.part = ctx->shrink_part;
+    sp.part_ld = part_ld;
+    sp.max_chunks = max_chunks;
+    sp.ticket = ctx->shrink_ticket;
     CUtensorMap tmQ;
     if ((rc = encode_2d(ctx, &tmQ, ctx->qx, qld, 2 * qrows, qld, 64, 64))) return rc;
     LoraGradParams gp;
@@ -1402,15 +1446,18 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     gp.qrows = (int)qrows;
     gp.segs = reinterpret_cast<const LoraGradSeg*>(dv + o_lg);
     gp.tmaps = reinterpret_cast<const CUtensorMap*>(dv + o_tm);
-    for (const GradGroup& g : groups) {
-      sp.items = reinterpret_cast<const ShrinkItem*>(dv + o_ix) + g.s0;
-      lora_shrink_kernel<<<g.s1 - g.s0, GEMM_THREADS, SHRINK_SMEM, stream>>>(L.tm_at, L.tm_b, sp);
-      CK(cudaGetLastError());
-      gp.items = reinterpret_cast<const LoraGradItem*>(dv + o_gi) + g.g0;
-      lora_grad_kernel<<<g.g1 - g.g0, GEMM_THREADS, GRAD_SMEM, stream>>>(tmQ, gp);
-      CK(cudaGetLastError());
-      ctx->launches += 2;
-    }
+    // (one launch each over all clients: the shrink has only t/128 x 2 CTAs per client, so
+    // splitting the clients into L2-sized groups starves the GPU — measured 2.3x slower)
+    sp.items = reinterpret_cast<const ShrinkItem*>(dv + o_ix);
+    const bool whole = max_chunks == 1 ||
+                       (part_ld <= 64 && (ctx->shrink_mode == 1 || (ctx->shrink_mode == 0 && (int)sitems.size() >= ctx->num_sms)));
+    lora_shrink_kernel<<<dim3((unsigned)sitems.size(), whole ? 1 : max_chunks), GEMM_THREADS, SHRINK_SMEM, stream>>>(
+        L.tm_at, L.tm_b, sp);
+    CK(cudaGetLastError());
+    gp.items = reinterpret_cast<const LoraGradItem*>(dv + o_gi);
+    lora_grad_kernel<<<(int)gitems.size(), GEMM_THREADS, GRAD_SMEM, stream>>>(tmQ, gp);
+    CK(cudaGetLastError());
+    ctx->launches += 2;
     prof_end(ctx, stream, pi);
   }
   if (!ig.empty()) {

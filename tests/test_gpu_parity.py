@@ -565,3 +565,28 @@ def test_tma_store_epilogue_bitwise_equals_direct_stores(pair):
             assert torch.equal(outs[0][c], outs[1][c]), (pass_kind, c)
     ex.ctx.set_option("tma_store", 1)
     ex.ctx.set_option("gemm_2cta", -1)
+
+
+@pytest.mark.parametrize("d_in", [5120, 13824])
+def test_shrink_whole_and_split_modes_bitwise_equal(d_in):
+    """The LoRA shrink splits K into fixed chunks (kernels.cuh SHRINK_KB_CHUNK) and sums the chunk
+    partials in chunk order — either in one CTA per slab (large dispatches) or across CTAs via
+    the workspace (decode-size dispatches). Both must give the same bits, and a decode-size
+    client must get the same rows alone as inside a prefill-size dispatch."""
+    d_out = 512
+    w, b = O.layer_params(15, 0, O.Q, d_in, d_out)
+    ex = _ex({(0, O.Q): (w, b)})
+    _mixed_clients(ex, d_in, d_out, seed=15, role=O.Q)
+    counts = [2, 1, 2000, 3, 700, 1, 2]      # decode-size LoRA clients next to prefill-size ones
+    xs = [torch.randn(t, d_in, device=ex.device).to(torch.bfloat16) for t in counts]
+    outs = {}
+    for mode in (1, 2):
+        ex.ctx.set_option("shrink_mode", mode)
+        outs[mode] = ex._compute_batch(0, [_env(c, 80 + mode, 0, O.Q, 0, x) for c, x in enumerate(xs)])
+    ex.ctx.set_option("shrink_mode", 0)
+    for c in range(len(xs)):
+        assert torch.equal(outs[1][c], outs[2][c]), c
+    big = ex._compute_batch(0, [_env(c, 90, 0, O.Q, 0, x) for c, x in enumerate(xs)])
+    for c in (0, 2):                         # LoRA r8 (decode rows) and LoRA r64 (prefill rows)
+        solo = ex._compute_batch(0, [_env(c, 91 + c, 0, O.Q, 0, xs[c])])[0]
+        assert torch.equal(solo, big[c]), c
