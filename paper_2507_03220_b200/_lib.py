@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libss_b200.so")
+# SS_B200_LIB: load a differently built copy of the library (kernel-variant experiments)
+LIB_PATH = os.environ.get("SS_B200_LIB") or os.path.join(_HERE, "libss_b200.so")
 
 SS_OK = 0
 SS_E_ARG = -1

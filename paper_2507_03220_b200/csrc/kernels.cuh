@@ -80,6 +80,19 @@ struct TileDesc {
 struct GemmParams {
   int N, K;
   int num_m_tiles, num_n_tiles, group_m;
+  int group_n;                      // > 0: N-grouped raster (walk M inside groups of N tiles)
+  int hint_a, hint_b, hint_out;     // L2 policy of A loads / W loads / output stores (0 none,
+                                    // 1 evict_first, 2 evict_last)
+  int a_bytes;                      // bytes one A-operand TMA box delivers (64- or 128-row box)
+  // Weight-streaming (small-M) dispatches: L2 prefetch of the layer the executor serves next
+  // (its W and LoRA packs), spread over the CTAs and issued by an otherwise idle warp while
+  // this launch streams its own W.
+  int pf_depth;                     // > 0: prefetch this launch's own W boxes pf_depth k-blocks
+                                    // ahead of the TMA loads (weight-streaming dispatches)
+  int pf_n;
+  int pf_hint;                      // L2 policy of the prefetched lines (0 normal, 2 evict_last)
+  const char* pf_ptr[3];
+  int64_t pf_bytes[3];
   int has_bias;
   int any_lora;
   int ia3_in_epilogue;              // forward: scale output columns by IA3
@@ -92,15 +105,60 @@ struct GemmParams {
   const int2* stores;               // (dst tensor map, row coordinate of tile row 0) per op
 };
 
-__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb,
-                                            int& nb) {
-  const int per_group = group_m * num_n;
+// Persistent-tile raster. M-grouped (default): groups of `group_m` M-tiles, N walked inside a
+// group, so a group's A rows stay in L2 while W streams past (W read once per group).
+// N-grouped (`group_n` > 0): groups of `group_n` N-tiles, M walked inside, so a group's W
+// columns stay in L2 while A streams (A read once per group) — the cheaper order when W is
+// small next to A (Q/K/V/O at prefill sizes fit W in L2 whole).
+__device__ __forceinline__ void tile_coords(int t, const GemmParams& p, int& mb, int& nb) {
+  if (p.group_n > 0) {
+    const int per_group = p.group_n * p.num_m_tiles;
+    const int g = t / per_group;
+    const int first_n = g * p.group_n;
+    const int gsize = min(p.group_n, p.num_n_tiles - first_n);
+    const int r = t % per_group;
+    nb = first_n + r % gsize;
+    mb = r / gsize;
+    return;
+  }
+  const int per_group = p.group_m * p.num_n_tiles;
   const int g = t / per_group;
-  const int first_m = g * group_m;
-  const int gsize = min(group_m, num_m - first_m);
+  const int first_m = g * p.group_m;
+  const int gsize = min(p.group_m, p.num_m_tiles - first_m);
   const int r = t % per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
+}
+
+constexpr int64_t PF_CHUNK = 64 << 10;
+__device__ __forceinline__ void prefetch_regions(const GemmParams& p) {
+  const uint64_t pol = p.pf_hint == 2 ? policy_evict_last() : policy_evict_normal();
+  int64_t c0 = 0;
+  for (int r = 0; r < p.pf_n; ++r) {
+    const int64_t nch = (p.pf_bytes[r] + PF_CHUNK - 1) / PF_CHUNK;
+    // chunk index continues across regions so every CTA gets an even share
+    int64_t c = ((blockIdx.x - c0) % gridDim.x + gridDim.x) % gridDim.x;
+    for (; c < nch; c += gridDim.x) {
+      const int64_t off = c * PF_CHUNK;
+      const int64_t len = min(PF_CHUNK, p.pf_bytes[r] - off);
+      if (len >= 16) bulk_prefetch_l2(p.pf_ptr[r] + off, (uint32_t)(len & ~int64_t(15)), pol);
+    }
+    c0 += nch;
+  }
+}
+
+__device__ __forceinline__ uint64_t l2_policy(int h) {
+  return h == 2 ? policy_evict_last() : policy_evict_first();
+}
+__device__ __forceinline__ void load_a_or_b(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                            int32_t c1, int hint, uint64_t pol) {
+  if (hint) tma_load_2d_hint(dst, map, bar, c0, c1, pol);
+  else tma_load_2d(dst, map, bar, c0, c1);
+}
+__device__ __forceinline__ void load_a_or_b_2sm(void* dst, const CUtensorMap* map, uint32_t bar, int32_t c0,
+                                                int32_t c1, int hint, uint64_t pol) {
+  if (hint) tma_load_2d_2sm_hint(dst, map, bar, c0, c1, pol);
+  else tma_load_2d_2sm(dst, map, bar, c0, c1);
 }
 
 // Store `ncols` (<= 64) fp32 values of one row to a bf16 / f32 destination with plain global
@@ -249,9 +307,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
       fence_async_smem();
       named_bar_sync(1, 128);
       if (leader_thread && ncols > 0) {
+        const uint64_t pol = l2_policy(p.hint_out);
         for (int k = 0; k < td.store_count; ++k) {
           const int2 op = p.stores[td.store_begin + k];
-          tma_store_2d(p.tmaps + op.x, sb, n, op.y + store_row0);
+          if (p.hint_out) tma_store_2d_hint(p.tmaps + op.x, sb, n, op.y + store_row0, pol);
+          else tma_store_2d(p.tmaps + op.x, sb, n, op.y + store_row0);
         }
         bulk_commit();
       }
@@ -266,7 +326,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
 template <int TBN>
 struct TileCfg {
   static constexpr int B_STAGE = TBN * BK * 2;
-  static constexpr int STAGES_ = TBN == 256 ? 4 : (TBN == 128 ? 6 : 8);
+#ifndef SS_STAGES64
+#define SS_STAGES64 8
+#endif
+  static constexpr int STAGES_ = TBN == 256 ? 4 : (TBN == 128 ? 6 : SS_STAGES64);
   static constexpr int STAGE = A_STAGE_BYTES + B_STAGE;
   static constexpr int SMEM = STAGES_ * STAGE + EPI_SMEM + 1024 + 256;
 };
@@ -327,26 +390,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      const uint64_t pol_a = l2_policy(p.hint_a), pol_b = l2_policy(p.hint_b);
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int mb, nb;
-        tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+        tile_coords(t, p, mb, nb);
         const TileDesc td = p.tiles[mb];
         const CUtensorMap* tmA = p.tmaps + td.amap;
         const int m0 = mb * BM, n0 = nb * TBN;
         tensormap_acquire(tmA);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
-          mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-          tma_load_2d(smA + s * A_STAGE_BYTES, tmA, &full_bar[s], kb * BK, td.arow);
+          mbar_expect_tx(&full_bar[s], p.a_bytes + B_STAGE_BYTES);
+          load_a_or_b(smA + s * A_STAGE_BYTES, tmA, &full_bar[s], kb * BK, td.arow, p.hint_a, pol_a);
           uint8_t* b = smB + s * B_STAGE_BYTES;
+          if (p.pf_depth > 0) {
+            // weight streaming: keep pf_depth more k-blocks of W on their way into L2 than the
+            // smem ring can hold, so the ring's loads see L2 instead of DRAM latency
+            const int kp = kb == 0 ? 0 : kb + p.pf_depth - 1;
+            const int kp_end = min(nkb, kb + p.pf_depth);
+            for (int q = kp; q < kp_end; ++q) {
+              if (kBwd) {
+                tma_prefetch_2d(&tmB, q * BK, n0);
+              } else {
+#pragma unroll
+                for (int j = 0; j < TBN / 64; ++j) tma_prefetch_2d(&tmB, n0 + 64 * j, q * BK);
+              }
+            }
+          }
           if (kBwd) {
             // W viewed K-major: rows = d_in (the GEMM's N), cols = d_out (the GEMM's K).
-            tma_load_2d(b, &tmB, &full_bar[s], kb * BK, n0);
+            load_a_or_b(b, &tmB, &full_bar[s], kb * BK, n0, p.hint_b, pol_b);
           } else {
             // W MN-major: 4 chunks of 64 output columns x 64 K rows.
 #pragma unroll
             for (int j = 0; j < TBN / 64; ++j)
-              tma_load_2d(b + j * (BK * 128), &tmB, &full_bar[s], n0 + 64 * j, kb * BK);
+              load_a_or_b(b + j * (BK * 128), &tmB, &full_bar[s], n0 + 64 * j, kb * BK, p.hint_b, pol_b);
           }
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -381,7 +459,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t acc_ph = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
-      tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+      tile_coords(t, p, mb, nb);
       mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * TBN;
@@ -427,6 +505,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       __syncwarp();
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ next-layer L2 prefetch
+    if (lane == 0 && p.pf_n > 0) prefetch_regions(p);
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const uint32_t ew = warp - 4;  // TMEM lane quarter
@@ -435,7 +516,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t acc_ph = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
-      tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+      tile_coords(t, p, mb, nb);
       const TileDesc td = p.tiles[mb];
       epilogue_tile<TBN>(p, tmem_base + acc * TBN, ew, lane, td, 0, nb * TBN, &tfull_bar[acc], acc_ph,
                          epi_stage, tempty0 + acc * 8);
@@ -537,11 +618,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);
+      const uint64_t pol_a = l2_policy(p.hint_a), pol_b = l2_policy(p.hint_b);
       int s = 0;
       uint32_t ph = 0;
       for (int t = cluster_id; t < num_tiles; t += num_clusters) {
         int mb, nb;
-        tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+        tile_coords(t, p, mb, nb);
         const TileDesc td = p.tiles[mb];
         const CUtensorMap* tmA = p.tmaps + td.amap;
         const int arow = td.arow + crank * BM;
@@ -552,16 +634,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&empty_bar[s], ph ^ 1);
           const uint32_t fb = full0 + s * 8;
           if (leader) mbar_expect_tx(&full_bar[s], 2 * Cfg::STAGE);
-          tma_load_2d_2sm(smA + s * A_STAGE_BYTES, tmA, fb, kb * BK, arow);
+          load_a_or_b_2sm(smA + s * A_STAGE_BYTES, tmA, fb, kb * BK, arow, p.hint_a, pol_a);
           uint8_t* b = smB + s * Cfg::B_BYTES;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             if (kBwd) {
-              tma_load_2d_2sm(b + g * 16384, &tmB, fb, kb * BK, nh + g * 256);
+              load_a_or_b_2sm(b + g * 16384, &tmB, fb, kb * BK, nh + g * 256, p.hint_b, pol_b);
             } else {
 #pragma unroll
               for (int j = 0; j < 2; ++j)
-                tma_load_2d_2sm(b + g * 16384 + j * (BK * 128), &tmB, fb, nh + g * 256 + 64 * j, kb * BK);
+                load_a_or_b_2sm(b + g * 16384 + j * (BK * 128), &tmB, fb, nh + g * 256 + 64 * j, kb * BK,
+                                p.hint_b, pol_b);
             }
           }
           if (++s == STAGES2) { s = 0; ph ^= 1; }
@@ -602,7 +685,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       uint32_t acc_ph = 0;
       for (int t = cluster_id; t < num_tiles; t += num_clusters) {
         int mb, nb;
-        tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+        tile_coords(t, p, mb, nb);
         mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
@@ -662,7 +745,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     uint32_t acc_ph = 0;
     for (int t = cluster_id; t < num_tiles; t += num_clusters) {
       int mb, nb;
-      tile_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, mb, nb);
+      tile_coords(t, p, mb, nb);
       const TileDesc td = p.tiles[mb];
       epilogue_tile<PN>(p, tmem_base + acc * 256, ew, lane, td, crank * BM, nb * PN, &tfull_bar[acc],
                         acc_ph, epi_stage, tempty0 + acc * 8);

@@ -111,6 +111,22 @@ struct ss_ctx {
   bool any_compute = false;
   int64_t launches = 0;
   int group_m = 16;
+  // GEMM tile raster: 0 M-grouped (group_m M-tiles per group), 1 N-grouped (W columns of a group
+  // held in L2 while A streams), -1 auto: the order with fewer estimated DRAM bytes, where an
+  // N group is as many W column tiles as fit `l2_budget_mb`. group_n > 0 forces the group width.
+  int raster = 0;
+  int group_n = 0;
+  int a_rows64 = 1;          // 64-row A box for single-tile dispatches of <= 64 rows
+  // L2 prefetch of the successor layer (forward order for FWD / NOISE, reverse for BWD) from
+  // GEMMs of at most `prefetch_rows` rows, up to `prefetch_mb` MB (0 disables)
+  int prefetch_mb = 0;
+  int pf_depth = 0;          // own-W L2 prefetch distance (k-blocks) for weight-streaming GEMMs
+  int prefetch_rows = 256;
+  int prefetch_hint = 2;
+  int l2_budget_mb = 48;
+  // 1: L2 evict_last on the operand a raster group re-reads (A rows in M order, W columns in N
+  // order) and evict_first on the outputs (written once, never re-read by this launch)
+  int l2_hints = 1;
   // -1 auto: CTA-pair kernel whenever the dispatch has at least half an SM-pair wave of
   // 256 x 256 tiles, else the single-CTA kernel with 256/128/64-wide tiles. (Round-1 v1 used the
   // single-CTA kernel for K > 8192; with the current epilogue the pair wins there too: 13B step
@@ -377,7 +393,7 @@ int acquire_staging(ss_ctx* ctx, size_t total, Staging*& out) {
 struct Built {
   int pass_kind = 0, block = 0, role = 0, K = 0, N = 0;
   int64_t M = 0, MX = 0, lora_ld = 64, al_rows = 0, ldx = 0;
-  bool any_lora = false, pair = false;
+  bool any_lora = false, pair = false, a_rows64 = false;
   int tbn = BN, pn = 256, num_m = 0, n_piece = 0, n_items = 0, part_ld = 16, shrink_chunks_ = 1;
   int kb_chunk = SHRINK_KB_CHUNK;
   size_t off_tm = 0, off_seg = 0, off_tile = 0, off_piece = 0, off_ch = 0, off_st = 0, off_it = 0;
@@ -615,6 +631,16 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     }
   }
 
+  // ---- weight-streaming dispatch (one packed tile of <= 64 rows): the GEMM reads A through a
+  // 64-row box (MMA rows 64-127 are never stored), halving its per-stage operand bytes
+  if (ctx->a_rows64 && !pair && num_m == 1 && direct_src.empty() && MX <= 64) {
+    tiles[0].amap = (int32_t)tmaps.size();
+    tmaps.emplace_back();
+    rc = encode_2d(ctx, &tmaps.back(), ctx->X, K, MX, ldx, 64, 64);
+    if (rc) return rc;
+    B.a_rows64 = true;
+  }
+
   // ---- serialise the device tables
   const size_t off_tm = 0;
   const size_t off_seg = round_up(tmaps.size() * sizeof(CUtensorMap), 256);
@@ -749,6 +775,52 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   const int pn = B.pn;                      // CTA-pair tile width (256 or 512)
   gpm.num_n_tiles = pair ? (N + pn - 1) / pn : (N + tbn - 1) / tbn;
   gpm.group_m = ctx->group_m;
+  gpm.group_n = 0;
+  {
+    // DRAM bytes of the two raster orders (A = the dispatch rows, W = the layer; outputs equal)
+    const int tn = pair ? pn : tbn;
+    const double a_bytes = (double)B.M * K * 2, w_bytes = (double)K * N * 2;
+    const int nn = gpm.num_n_tiles;
+    int h = ctx->group_n > 0 ? ctx->group_n
+                             : (int)std::max<int64_t>(1, ((int64_t)ctx->l2_budget_mb << 20) / ((int64_t)tn * K * 2));
+    h = std::min(h, nn);
+    const double t_m = a_bytes + w_bytes * ((num_m + ctx->group_m - 1) / ctx->group_m);
+    const double t_n = w_bytes + a_bytes * ((nn + h - 1) / h);
+    if (ctx->raster == 1 || (ctx->raster < 0 && t_n < t_m)) gpm.group_n = h;
+  }
+  gpm.hint_a = (ctx->l2_hints && gpm.group_n == 0) ? 2 : 0;
+  gpm.hint_b = (ctx->l2_hints && gpm.group_n > 0) ? 2 : 0;
+  gpm.hint_out = ctx->l2_hints ? 1 : 0;
+  gpm.a_bytes = B.a_rows64 ? A_STAGE_BYTES / 2 : A_STAGE_BYTES;
+  gpm.pf_n = 0;
+  gpm.pf_hint = ctx->prefetch_hint;
+  gpm.pf_depth = (!pair && B.M <= ctx->prefetch_rows) ? ctx->pf_depth : 0;
+  if (ctx->prefetch_mb > 0 && !pair && B.M <= ctx->prefetch_rows) {
+    // weight-streaming dispatch: its own W is read once and not again soon (evict_first), and
+    // the layer served next is pulled into L2 behind it
+    gpm.hint_b = 1;
+    auto it = ctx->layers.find({B.block, B.role});
+    const Layer* nx = nullptr;
+    if (bwd) {
+      if (it != ctx->layers.begin()) nx = &std::prev(it)->second;
+    } else if (std::next(it) != ctx->layers.end()) {
+      nx = &std::next(it)->second;
+    }
+    if (nx) {
+      int64_t budget = (int64_t)ctx->prefetch_mb << 20;
+      auto add = [&](const void* ptr, int64_t bytes) {
+        bytes = std::min(bytes, budget) & ~int64_t(15);
+        if (!ptr || bytes <= 0 || gpm.pf_n == 3) return;
+        gpm.pf_ptr[gpm.pf_n] = static_cast<const char*>(ptr);
+        gpm.pf_bytes[gpm.pf_n++] = bytes;
+        budget -= bytes;
+      };
+      // the LoRA packs first (small, read by the shrink before the GEMM needs W)
+      add(nx->at_pack, (int64_t)nx->pack_rows * nx->ld_at * 2);
+      add(nx->b_pack, (int64_t)nx->pack_rows * nx->ld_b * 2);
+      add(nx->W, (int64_t)nx->d_in * nx->ldw * 2);
+    }
+  }
   gpm.has_bias = (pass_kind == SS_PASS_FORWARD && L.bias) ? 1 : 0;
   gpm.any_lora = any_lora ? 1 : 0;
   gpm.ia3_in_epilogue = (pass_kind != SS_PASS_BACKWARD) ? 1 : 0;
@@ -994,6 +1066,47 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   }
   if (!strcmp(key, "gemm_2cta")) {
     ctx->gemm_2cta = value < 0 ? -1 : (value ? 1 : 0);
+    return SS_OK;
+  }
+  if (!strcmp(key, "raster")) {
+    ctx->raster = value < 0 ? -1 : (value ? 1 : 0);
+    return SS_OK;
+  }
+  if (!strcmp(key, "group_n")) {
+    if (value < 0) return fail(ctx, SS_E_ARG, "group_n must be >= 0");
+    ctx->group_n = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "l2_budget_mb")) {
+    if (value < 1) return fail(ctx, SS_E_ARG, "l2_budget_mb must be >= 1");
+    ctx->l2_budget_mb = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "a_rows64")) {
+    ctx->a_rows64 = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "prefetch_mb")) {
+    if (value < 0) return fail(ctx, SS_E_ARG, "prefetch_mb must be >= 0");
+    ctx->prefetch_mb = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "pf_depth")) {
+    if (value < 0 || value > 64) return fail(ctx, SS_E_ARG, "pf_depth must be in [0, 64]");
+    ctx->pf_depth = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "prefetch_rows")) {
+    ctx->prefetch_rows = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "prefetch_hint")) {
+    if (value != 0 && value != 2) return fail(ctx, SS_E_ARG, "prefetch_hint must be 0 or 2");
+    ctx->prefetch_hint = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "l2_hints")) {
+    ctx->l2_hints = value ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "group_m")) {
