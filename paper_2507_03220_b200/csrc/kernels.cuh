@@ -30,6 +30,8 @@ enum : int32_t {
   SEGF_DST_VEC = 1 << 7,   // dst rows 16-byte aligned
   SEGF_BASE_VEC = 1 << 8,  // base rows 16-byte aligned
   SEGF_TMA_STORE = 1 << 9, // bf16 destination written by TMA bulk stores
+  SEGF_REMOTE_SRC = 1 << 10,  // source rows on a peer GPU (gathered with plain loads)
+  SEGF_REMOTE_DST = 1 << 11,  // destination on a peer GPU (plain stores over NVLink)
 };
 
 struct DevSeg {

@@ -116,6 +116,8 @@ struct ss_ctx {
   // N group is as many W column tiles as fit `l2_budget_mb`. group_n > 0 forces the group width.
   int raster = 0;
   int group_n = 0;
+  uint64_t peers_enabled = 0;  // peer GPUs whose memory this context's kernels may touch
+  int force_remote = 0;      // testing: route every segment as if it lived on a peer GPU
   int a_rows64 = 1;          // 64-row A box for single-tile dispatches of <= 64 rows
   // L2 prefetch of the successor layer (forward order for FWD / NOISE, reverse for BWD) from
   // GEMMs of at most `prefetch_rows` rows, up to `prefetch_mb` MB (0 disables)
@@ -306,6 +308,28 @@ int ensure_dev(ss_ctx* ctx, T*& ptr, size_t& cap, size_t bytes, bool plan_visibl
   return SS_OK;
 }
 
+// True when `p` is device memory of another GPU (a client on a peer GPU, reached over NVLink):
+// such segments are read by the gather kernel and written by plain stores (UVA peer access),
+// never through TMA tensor maps.
+bool is_remote(ss_ctx* ctx, const void* p) {
+  if (!p) return false;
+  if (ctx->force_remote) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a.type != cudaMemoryTypeDevice || a.device == ctx->device) return false;
+  if (a.device >= 0 && a.device < 64 && !(ctx->peers_enabled >> a.device & 1)) {
+    // first segment from this peer: map its memory into this GPU's address space (NVLink)
+    cudaSetDevice(ctx->device);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+    if (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) ctx->peers_enabled |= 1ull << a.device;
+    cudaGetLastError();
+  }
+  return true;
+}
+
 bool aligned16(const void* p, int64_t ld, size_t esz) {
   return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * (int64_t)esz) % 16 == 0);
 }
@@ -447,6 +471,8 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     if (s.flags & SS_SEGF_DST_BF16) f |= SEGF_DST_BF16;
     if (aligned16(s.src, s.src_ld, (s.flags & SS_SEGF_SRC_BF16) ? 2 : 4)) f |= SEGF_SRC_VEC;
     if (aligned16(s.dst, s.dst_ld, (s.flags & SS_SEGF_DST_BF16) ? 2 : 4)) f |= SEGF_DST_VEC;
+    if (is_remote(ctx, s.src)) f |= SEGF_REMOTE_SRC;
+    if (is_remote(ctx, s.dst) || (s.dst_base && is_remote(ctx, s.dst_base))) f |= SEGF_REMOTE_DST;
     // NOISE with the adapter flag = the noise effect of the ADAPTED layer, (n.W + s n.A.B) * l
     // (bias-free): what a client with an executor-fused adapter subtracts to unblind its reply
     if (s.flags & SS_SEGF_ADAPTER) {
@@ -503,6 +529,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   for (size_t j = 0; j < ds.size(); ++j) {
     DevSeg& d = ds[j];
     const bool direct_ok = ctx->direct_tiles && (d.flags & SEGF_SRC_BF16) && (d.flags & SEGF_SRC_VEC) &&
+                           !(d.flags & SEGF_REMOTE_SRC) &&
                            !(bwd && (d.flags & SEGF_IA3)) && (d.src_ld * 2) % 16 == 0;
     const int nd = direct_ok ? (d.rows / TM) * TM : 0;
     if (nd > 0) {
@@ -589,7 +616,9 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   std::vector<int32_t> dmap_full(ds.size(), -1), dmap_tail(ds.size(), -1);
   for (size_t j = 0; j < ds.size(); ++j) {
     DevSeg& d = ds[j];
-    if (!ctx->tma_store || !(d.flags & SEGF_DST_BF16) || !(d.flags & SEGF_DST_VEC)) continue;
+    if (!ctx->tma_store || !(d.flags & SEGF_DST_BF16) || !(d.flags & SEGF_DST_VEC) ||
+        (d.flags & SEGF_REMOTE_DST))
+      continue;
     d.flags |= SEGF_TMA_STORE;
     const bool has_direct = d.xrow0 < 0 || d.xlocal0 > 0;
     if (has_direct) {
@@ -1080,6 +1109,10 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "l2_budget_mb")) {
     if (value < 1) return fail(ctx, SS_E_ARG, "l2_budget_mb must be >= 1");
     ctx->l2_budget_mb = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "force_remote")) {
+    ctx->force_remote = value ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "a_rows64")) {

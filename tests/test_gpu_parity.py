@@ -590,3 +590,78 @@ def test_shrink_whole_and_split_modes_bitwise_equal(d_in):
     for c in (0, 2):                         # LoRA r8 (decode rows) and LoRA r64 (prefill rows)
         solo = ex._compute_batch(0, [_env(c, 91 + c, 0, O.Q, 0, xs[c])])[0]
         assert torch.equal(solo, big[c]), c
+
+
+def test_peer_gpu_routing_bitwise_equals_local():
+    """Segments whose buffers live on another GPU (clients reached over
+    NVLink) are gathered with plain loads and written with plain stores, never through TMA
+    tensor maps. `force_remote` routes every segment that way on one GPU: the rows (and the
+    IA3 client's pre-IA3 y_base) must be bitwise those of the local path."""
+    d_in, d_out = 512, 1088
+    w, b = O.layer_params(16, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)})
+    _mixed_clients(ex, d_in, d_out, seed=16, role=O.V)
+    counts = [300, 1, 700, 130, 5, 256, 77]
+    dev = ex.device
+    for pass_kind, width in ((0, d_in), (1, d_out)):
+        xs = [torch.randn(t, width, device=dev).to(torch.bfloat16) for t in counts]
+        outs, bases = {}, {}
+        for remote in (0, 1):
+            ex.ctx.set_option("force_remote", remote)
+            bs = [torch.full((t, d_out), 7.0, dtype=torch.bfloat16, device=dev) for t in counts]
+            envs = [_env(c, 100 + 2 * pass_kind + remote, 0, O.V, pass_kind, x,
+                         base_to=bs[c] if (pass_kind == 0 and c == 3) else None) for c, x in enumerate(xs)]
+            outs[remote] = ex._compute_batch(pass_kind, envs)
+            bases[remote] = bs[3]
+        ex.ctx.set_option("force_remote", 0)
+        for c in range(len(xs)):
+            assert torch.equal(outs[0][c], outs[1][c]), (pass_kind, c)
+        if pass_kind == 0:
+            assert torch.equal(bases[0], bases[1])
+
+
+def test_decode_size_dispatch_64_row_box_bitwise():
+    """A dispatch of <= 64 packed rows reads its operand through a 64-row TMA box (MMA rows
+    64-127 are never stored). Its rows must equal the 128-row-box rows and the same clients'
+    rows inside a prefill-size dispatch (batching invisibility at decode sizes)."""
+    d_in, d_out = 5120, 1024
+    w, b = O.layer_params(17, 0, O.K, d_in, d_out)
+    ex = _ex({(0, O.K): (w, b)})
+    _mixed_clients(ex, d_in, d_out, seed=17)
+    counts = [2, 2, 1, 2, 2, 3, 2]                      # 14 decode rows, every adapter kind
+    dev = ex.device
+    xs = [torch.randn(t, d_in, device=dev).to(torch.bfloat16) for t in counts]
+    outs = {}
+    for box64 in (1, 0):
+        ex.ctx.set_option("a_rows64", box64)
+        outs[box64] = ex._compute_batch(0, [_env(c, 110 + box64, 0, O.K, 0, x) for c, x in enumerate(xs)])
+    ex.ctx.set_option("a_rows64", 1)
+    filler = torch.randn(3000, d_in, device=dev).to(torch.bfloat16)
+    big = ex._compute_batch(0, [_env(c, 120, 0, O.K, 0, x) for c, x in enumerate(xs)] +
+                            [_env(1, 121, 0, O.K, 0, filler)])
+    for c in range(len(xs)):
+        assert torch.equal(outs[1][c], outs[0][c]), c
+        assert torch.equal(outs[1][c], big[c]), c
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs two GPUs (client buffers on a peer GPU)")
+def test_client_buffers_on_peer_gpu():
+    """the executor on cuda:0 serves a client whose exchange buffers live on
+    cuda:1 (NVLink peer loads / stores); rows must equal the co-located client's."""
+    from paper_2507_03220_b200.channel import enable_peer_access
+    assert enable_peer_access(0, 1)
+    d_in, d_out = 512, 1088
+    w, b = O.layer_params(18, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)}, device=0)
+    _mixed_clients(ex, d_in, d_out, seed=18, role=O.V)
+    counts = [300, 1, 700, 130, 5, 256, 77]
+    xs = [torch.randn(t, d_in, device="cuda:0").to(torch.bfloat16) for t in counts]
+    local = ex._compute_batch(0, [_env(c, 130, 0, O.V, 0, x) for c, x in enumerate(xs)])
+    xr = [x.to("cuda:1") for x in xs]
+    outr = [torch.empty(t, d_out, dtype=torch.bfloat16, device="cuda:1") for t in counts]
+    torch.cuda.synchronize(1)
+    ex._compute_batch(0, [_env(c, 131, 0, O.V, 0, x, reply_to=outr[c]) for c, x in enumerate(xr)])
+    torch.cuda.synchronize(0)
+    for c in range(len(xs)):
+        assert torch.equal(local[c], outr[c].to("cuda:0")), c
