@@ -133,6 +133,9 @@ def summarize_clocks(samples):
             "reasons": reasons, "samples": len(samples)}
 
 
+INPLACE = False   # --inplace: replies written over the request buffers (SharedBuffer style)
+
+
 def build_gpu_workload(wl_key, device, rank):
     import torch
     from paper_2507_03220_b200 import AffineParams, GpuBaseExecutor, LayerAddress, Role
@@ -181,7 +184,11 @@ def build_gpu_workload(wl_key, device, rank):
     # per-client device exchange buffers (DeviceChannel sizing: tokens x max layer width)
     t = wl["tokens"]
     maxw = max(wl["d"], wl["d_ff"], wl["V"])
+    # request and reply buffers per client (DeviceChannel keeps them apart: a reply written over
+    # its own request rows would force the gather path, SharedBuffer semantics)
     bufs = [torch.randn(t * maxw, generator=g, device=device).to(torch.bfloat16) for _ in specs]
+    outs = ([torch.empty(t * maxw, dtype=torch.bfloat16, device=device) for _ in specs]
+            if not INPLACE else bufs)
     base_bufs = {c: torch.empty(t * wl["d_ff"], dtype=torch.bfloat16, device=device)
                  for c, (k, _, ft) in enumerate(specs) if k == "ia3" and ft}
     fwd, bwd = [], []
@@ -192,9 +199,9 @@ def build_gpu_workload(wl_key, device, rank):
             base = None
             if c in base_bufs and r in (K, V, FF_UP):
                 base = base_bufs[c][: t * do].view(t, do)
-            segs.append((c, bufs[c][: t * di].view(t, di), bufs[c][: t * do].view(t, do), base))
+            segs.append((c, bufs[c][: t * di].view(t, di), outs[c][: t * do].view(t, do), base))
         fwd.append(ex.compile_dispatch(0, b, r, segs))
-        segs = [(c, bufs[c][: t * do].view(t, do), bufs[c][: t * di].view(t, di), None)
+        segs = [(c, bufs[c][: t * do].view(t, do), outs[c][: t * di].view(t, di), None)
                 for c, (kind, _, ft) in enumerate(specs) if ft]
         if segs:
             bwd.append(ex.compile_dispatch(1, b, r, segs))
@@ -272,7 +279,11 @@ def build_tp_workload(wl_key, device, rank, world):
         tp.register_adapter(c, ad)
     t = wl["tokens"]
     maxw = max(wl["d"], wl["d_ff"], wl["V"])
+    # request and reply buffers per client (DeviceChannel keeps them apart: a reply written over
+    # its own request rows would force the gather path, SharedBuffer semantics)
     bufs = [torch.randn(t * maxw, generator=g, device=device).to(torch.bfloat16) for _ in specs]
+    outs = ([torch.empty(t * maxw, dtype=torch.bfloat16, device=device) for _ in specs]
+            if not INPLACE else bufs)
     plan = []
     for (b, r) in layers:
         di, do = dims[r]
@@ -301,6 +312,7 @@ def e2e_leg(ex, wl_key, specs, steps, device):
     t = wl["tokens"]
     maxw = max(wl["d"], wl["d_ff"], wl["V"])
     host = [torch.empty(t * maxw, dtype=torch.bfloat16, pin_memory=True) for _ in specs]
+    reply = [torch.empty(t * maxw, dtype=torch.bfloat16, pin_memory=True) for _ in specs]
     for h in host:
         h.normal_()
     rid = [0]
@@ -315,7 +327,7 @@ def e2e_leg(ex, wl_key, specs, steps, device):
             for c in range(len(specs)):
                 rid[0] += 1
                 envs.append(Envelope(c, rid[0], b, r, 0, host[c][: t * di].view(t, di),
-                                     reply_to=host[c][: t * do].view(t, do)))
+                                     reply_to=reply[c][: t * do].view(t, do)))
                 h2d += t * di * 2
                 d2h += t * do * 2
             ex.serve_forward(envs)
@@ -327,7 +339,7 @@ def e2e_leg(ex, wl_key, specs, steps, device):
                     continue
                 rid[0] += 1
                 envs.append(Envelope(c, rid[0], b, r, 1, host[c][: t * do].view(t, do),
-                                     reply_to=host[c][: t * di].view(t, di)))
+                                     reply_to=reply[c][: t * di].view(t, di)))
                 h2d += t * do * 2
                 d2h += t * di * 2
             ex.serve_backward(envs)
@@ -466,10 +478,15 @@ def main():
     ap.add_argument("--graph", type=int, default=1,
                     help="1: replay the step's prebuilt dispatch plans as one CUDA graph (the kernel "
                          "roofline is still measured on an eager, event-bracketed pass)")
+    ap.add_argument("--inplace", action="store_true",
+                    help="device clients reuse one buffer for request and reply (SharedBuffer style; "
+                         "aliased sources are gathered before the GEMM)")
     ap.add_argument("--parallel", default="replicas", choices=("replicas", "tp"),
                     help="replicas: segment-parallel full replicas (weak scaling, no data-path "
                          "collective); tp: column/row-sharded layers + NCCL per dispatch (strong)")
     args = ap.parse_args()
+    global INPLACE
+    INPLACE = args.inplace
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

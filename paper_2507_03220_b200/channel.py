@@ -5,9 +5,11 @@ pass_kind, payload) -> array``, ``register(sends_backward)``, ``deregister()``, 
 ``reply_is_view``, ``extra_payload_copies``) over a per-client DEVICE exchange buffer that
 follows SharedBuffer's rule (transport.py:28-49): capacity batch*seq*max_width elements,
 grows to exactly the requested size and never shrinks. The request is written into the
-buffer, the executor gathers from it and scatters the reply back into the same buffer, and
-the client receives a view — no host round trip. When the client sits on another GPU the
-buffer lives on the client's GPU and the executor reads/writes it over NVLink peer access
+request buffer, the executor reads it in place and writes the reply into a reply buffer of
+the same size and rule, and the client receives a view of it — no host round trip. (The
+reference reuses ONE buffer for both; the executor supports that too — aliased sources are
+gathered before the GEMM writes — but two buffers let it read the request rows in place.)
+When the client sits on another GPU the buffers live on the client's GPU and the executor reads/writes it over NVLink peer access
 (the C ABI takes plain device pointers; enable peer access with ``enable_peer_access``).
 
 Ordering (payload visible before the control message): the request carries a
@@ -74,6 +76,7 @@ class DeviceChannel:
         self.max_width = max_width
         dev = device if device is not None else executor.device
         self.buffer = DeviceBuffer(batch_size * seq_len * max_width, dtype, dev)
+        self.reply_buffer = DeviceBuffer(batch_size * seq_len * max_width, dtype, dev)
         self.base_buffer: DeviceBuffer | None = None
         self.extra_payload_copies = 0
         self.last_base: torch.Tensor | None = None
@@ -96,6 +99,7 @@ class DeviceChannel:
         d_in, d_out = self.executor.layer_dims(block, role)
         out_cols = d_in if pass_kind == PASS_BACKWARD else d_out
         self.buffer.ensure(rows * self.max_width)
+        self.reply_buffer.ensure(rows * self.max_width)
         sent = self.buffer.view(rows, cols)
         if isinstance(payload, torch.Tensor):
             if payload.data_ptr() != sent.data_ptr():
@@ -104,7 +108,7 @@ class DeviceChannel:
             sent.copy_(torch.from_numpy(np.ascontiguousarray(payload, dtype=np.float32)))
         ready = torch.cuda.Event()
         ready.record(torch.cuda.current_stream(self.buffer.device))
-        reply_to = self.buffer.view(rows, out_cols)
+        reply_to = self.reply_buffer.view(rows, out_cols)
         base_to = None
         if want_base and pass_kind != PASS_BACKWARD:
             if self.base_buffer is None:

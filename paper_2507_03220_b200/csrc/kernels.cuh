@@ -32,6 +32,7 @@ enum : int32_t {
   SEGF_TMA_STORE = 1 << 9, // bf16 destination written by TMA bulk stores
   SEGF_REMOTE_SRC = 1 << 10,  // source rows on a peer GPU (gathered with plain loads)
   SEGF_REMOTE_DST = 1 << 11,  // destination on a peer GPU (plain stores over NVLink)
+  SEGF_SRC_ALIASED = 1 << 12, // source rows overlap a destination of the dispatch (gathered first)
 };
 
 struct DevSeg {

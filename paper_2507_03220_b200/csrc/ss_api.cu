@@ -116,6 +116,12 @@ struct ss_ctx {
   // N group is as many W column tiles as fit `l2_budget_mb`. group_n > 0 forces the group width.
   int raster = 0;
   int group_n = 0;
+  // whole-dispatch device slices + per-sub-batch events of the aliased host dispatch
+  void* ha_in = nullptr;
+  void* ha_out = nullptr;
+  void* ha_base = nullptr;
+  size_t ha_in_cap = 0, ha_out_cap = 0, ha_base_cap = 0;
+  std::vector<cudaEvent_t> chunk_ev;
   uint64_t peers_enabled = 0;  // peer GPUs whose memory this context's kernels may touch
   int force_remote = 0;      // testing: route every segment as if it lived on a peer GPU
   int a_rows64 = 1;          // 64-row A box for single-tile dispatches of <= 64 rows
@@ -505,6 +511,28 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     M += s.rows;
   }
   B.status.assign(seg_status, seg_status + n_seg);
+  // A reply written over request rows (the reference's SharedBuffer hand-off, transport.py:
+  // 76-97, reuses one buffer for both) must not be read in place: a tile's epilogue would
+  // overwrite rows other tiles still stream. Such segments are gathered into the operand first
+  // (the gather completes before the GEMM starts), like the reference's concat_rows copy.
+  {
+    struct Range { uintptr_t a, b; };
+    auto span = [](const void* p, int64_t rows, int64_t ld, int64_t width, size_t esz) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+      return Range{a, a + (uintptr_t)(((rows - 1) * ld + width) * (int64_t)esz)};
+    };
+    std::vector<Range> outs;
+    for (const DevSeg& d : ds) {
+      outs.push_back(span(d.dst, d.rows, d.dst_ld, N, (d.flags & SEGF_DST_BF16) ? 2 : 4));
+      if (d.flags & SEGF_WANT_BASE)
+        outs.push_back(span(d.dst_base, d.rows, d.base_ld, N, (d.flags & SEGF_BASE_BF16) ? 2 : 4));
+    }
+    for (DevSeg& d : ds) {
+      const Range in = span(d.src, d.rows, d.src_ld, K, (d.flags & SEGF_SRC_BF16) ? 2 : 4);
+      for (const Range& o : outs)
+        if (in.a < o.b && o.a < in.b) { d.flags |= SEGF_SRC_ALIASED; break; }
+    }
+  }
   if (M == 0) return SS_OK;
   if (M > (int64_t)1 << 30) return fail(ctx, SS_E_ARG, "batch too large (%lld rows)", (long long)M);
   CK(cudaSetDevice(ctx->device));
@@ -529,7 +557,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   for (size_t j = 0; j < ds.size(); ++j) {
     DevSeg& d = ds[j];
     const bool direct_ok = ctx->direct_tiles && (d.flags & SEGF_SRC_BF16) && (d.flags & SEGF_SRC_VEC) &&
-                           !(d.flags & SEGF_REMOTE_SRC) &&
+                           !(d.flags & (SEGF_REMOTE_SRC | SEGF_SRC_ALIASED)) &&
                            !(bwd && (d.flags & SEGF_IA3)) && (d.src_ld * 2) % 16 == 0;
     const int nd = direct_ok ? (d.rows / TM) * TM : 0;
     if (nd > 0) {
@@ -1020,6 +1048,10 @@ int ss_ctx_destroy(ss_ctx* ctx) {
     for (auto& a : L.adapters) cudaFree(a.second.ia3);
   }
   cudaFree(ctx->X);
+  cudaFree(ctx->ha_in);
+  cudaFree(ctx->ha_out);
+  cudaFree(ctx->ha_base);
+  for (cudaEvent_t e : ctx->chunk_ev) cudaEventDestroy(e);
   cudaFree(ctx->a_lora);
   cudaFree(ctx->row_seg);
   cudaFree(ctx->qx);
@@ -1635,6 +1667,127 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
   return SS_OK;
 }
 
+}  // extern "C"
+
+namespace {
+struct HostPiece { int seg; int64_t r0, r1; };
+
+// Host dispatch whose replies overwrite request rows of later sub-batches (see
+// ss_compute_batch_host): every sub-batch gets its own slice of dispatch-sized device buffers
+// (so the H2D stream never waits for compute), and the D2H of sub-batch j is issued right after
+// the H2D of sub-batch wait_for[j] was enqueued, waiting for it.
+int host_dispatch_aliased(ss_ctx* ctx, int pass_kind, int block, int role, const ss_seg* segs,
+                          int32_t* seg_status, cudaStream_t stream, int K, int N, size_t esz_in,
+                          size_t esz_out, size_t esz_base, int64_t rows_total,
+                          const std::vector<std::vector<HostPiece>>& chunks, const std::vector<int>& wait_for) {
+  int rc = SS_OK;
+  bool any_base = false;
+  for (const auto& ch : chunks)
+    for (const HostPiece& p : ch) any_base |= segs[p.seg].dst_base && pass_kind != SS_PASS_BACKWARD;
+  if ((rc = ensure_dev(ctx, ctx->ha_in, ctx->ha_in_cap, (size_t)rows_total * K * esz_in, false))) return rc;
+  if ((rc = ensure_dev(ctx, ctx->ha_out, ctx->ha_out_cap, (size_t)rows_total * N * esz_out, false))) return rc;
+  if (any_base && (rc = ensure_dev(ctx, ctx->ha_base, ctx->ha_base_cap, (size_t)rows_total * N * esz_base, false)))
+    return rc;
+  ctx->ws_high = std::max(ctx->ws_high, ctx->x_cap + ctx->al_cap + ctx->rs_cap + ctx->qx_cap + ctx->ha_in_cap +
+                                            ctx->ha_out_cap + ctx->ha_base_cap);
+  while (ctx->chunk_ev.size() < 2 * chunks.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->chunk_ev.push_back(e);
+  }
+  // the previous host dispatch drained its D2H before returning; the device path may still be
+  // reading an older dispatch's slices: order after everything queued on `stream`
+  CK(cudaEventRecord(ctx->chunk_ev[0], stream));
+  CK(cudaStreamWaitEvent(ctx->h2d, ctx->chunk_ev[0], 0));
+  std::vector<int64_t> row0(chunks.size() + 1, 0);
+  for (size_t j = 0; j < chunks.size(); ++j) {
+    int64_t n = 0;
+    for (const HostPiece& p : chunks[j]) n += p.r1 - p.r0;
+    row0[j + 1] = row0[j] + n;
+  }
+  std::vector<char> issued(chunks.size(), 0);
+  auto issue_d2h = [&](size_t j) -> int {
+    cudaEvent_t comp = ctx->chunk_ev[2 * j + 1];
+    CK(cudaStreamWaitEvent(ctx->d2h, comp, 0));
+    if (wait_for[j] >= 0) CK(cudaStreamWaitEvent(ctx->d2h, ctx->chunk_ev[2 * wait_for[j]], 0));
+    int64_t pos = row0[j];
+    for (const HostPiece& p : chunks[j]) {
+      const ss_seg& s = segs[p.seg];
+      const int64_t n = p.r1 - p.r0;
+      if (seg_status[p.seg] == SS_SEG_OK) {
+        CK(copy_rows(static_cast<char*>(s.dst) + p.r0 * s.dst_ld * esz_out, (size_t)s.dst_ld * esz_out,
+                     static_cast<const char*>(ctx->ha_out) + pos * N * esz_out, (size_t)N * esz_out,
+                     (size_t)N * esz_out, (size_t)n, cudaMemcpyDeviceToHost, ctx->d2h));
+        if (s.dst_base && pass_kind != SS_PASS_BACKWARD)
+          CK(copy_rows(static_cast<char*>(s.dst_base) + p.r0 * s.base_ld * esz_base, (size_t)s.base_ld * esz_base,
+                       static_cast<const char*>(ctx->ha_base) + pos * N * esz_base, (size_t)N * esz_base,
+                       (size_t)N * esz_base, (size_t)n, cudaMemcpyDeviceToHost, ctx->d2h));
+      }
+      pos += n;
+    }
+    issued[j] = 1;
+    return SS_OK;
+  };
+  std::vector<ss_seg> cs;
+  std::vector<int32_t> cst;
+  for (size_t k = 0; k < chunks.size(); ++k) {
+    cs.clear();
+    int64_t pos = row0[k];
+    for (const HostPiece& p : chunks[k]) {
+      const ss_seg& s = segs[p.seg];
+      const int64_t n = p.r1 - p.r0;
+      char* din = static_cast<char*>(ctx->ha_in) + pos * K * esz_in;
+      CK(copy_rows(din, (size_t)K * esz_in, static_cast<const char*>(s.src) + p.r0 * s.src_ld * esz_in,
+                   (size_t)s.src_ld * esz_in, (size_t)K * esz_in, (size_t)n, cudaMemcpyHostToDevice, ctx->h2d));
+      ss_seg d = s;
+      d.rows = (uint32_t)n;
+      d.src = din;
+      d.src_ld = K;
+      d.dst = static_cast<char*>(ctx->ha_out) + pos * N * esz_out;
+      d.dst_ld = N;
+      if (s.dst_base && pass_kind != SS_PASS_BACKWARD) {
+        d.dst_base = static_cast<char*>(ctx->ha_base) + pos * N * esz_base;
+        d.base_ld = N;
+      } else {
+        d.dst_base = nullptr;
+        d.base_ld = 0;
+      }
+      cs.push_back(d);
+      pos += n;
+    }
+    cst.assign(cs.size(), 0);
+    Built b;
+    if ((rc = build_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), cst.data(), b))) return rc;
+    for (size_t q = 0; q < cs.size(); ++q)
+      if (cst[q] != SS_SEG_OK) seg_status[chunks[k][q].seg] = cst[q];
+    Staging* stp = nullptr;
+    if (b.M > 0) {
+      if ((rc = acquire_staging(ctx, b.blob.size(), stp))) return rc;
+      memcpy(stp->host, b.blob.data(), b.blob.size());
+      CK(cudaMemcpyAsync(stp->dev, stp->host, b.blob.size(), cudaMemcpyHostToDevice, ctx->h2d));
+    }
+    CK(cudaEventRecord(ctx->chunk_ev[2 * k], ctx->h2d));
+    CK(cudaStreamWaitEvent(stream, ctx->chunk_ev[2 * k], 0));
+    if (b.M > 0) {
+      CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
+      if ((rc = launch_batch(ctx, b, static_cast<char*>(stp->dev), stream))) return rc;
+      // the staging slot may be reused only after these kernels read their tables
+      CK(cudaEventRecord(stp->done, stream));
+      stp->pending = true;
+    }
+    CK(cudaEventRecord(ctx->chunk_ev[2 * k + 1], stream));
+    for (size_t j = 0; j <= k; ++j)
+      if (!issued[j] && wait_for[j] <= (int)k && (rc = issue_d2h(j))) return rc;
+  }
+  for (size_t j = 0; j < chunks.size(); ++j)
+    if (!issued[j] && (rc = issue_d2h(j))) return rc;
+  CK(cudaStreamSynchronize(ctx->d2h));
+  return SS_OK;
+}
+}  // namespace
+
+extern "C" {
+
 // ---- host-buffer dispatch ---------------------------------------------------------------
 int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
                           void* stream_, int32_t* seg_status) {
@@ -1710,7 +1863,7 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     }
     sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
   }
-  struct Piece { int seg; int64_t r0, r1; };
+  using Piece = HostPiece;
   std::vector<std::vector<Piece>> chunks(1);
   size_t ci = 0;
   int64_t cur = 0;
@@ -1731,6 +1884,40 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
   }
   if (chunks.back().empty()) chunks.pop_back();
   int rc = SS_OK;
+  // In-place hand-off (the reference's SharedBuffer reuses one buffer for request and reply,
+  // transport.py:76-97): the D2H of sub-batch j may land on host rows a LATER sub-batch has
+  // not uploaded yet. wait_for[j] = the last later sub-batch whose H2D source bytes intersect
+  // sub-batch j's reply bytes; with any such hazard every sub-batch gets its own device slice
+  // (no ring reuse, so no wait cycle) and D2H j waits for that H2D.
+  std::vector<int> wait_for(chunks.size(), -1);
+  {
+    struct Range { uintptr_t a, b; };
+    auto rows_span = [](const void* p, int64_t r0, int64_t r1, int64_t ld, int64_t width, size_t esz) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(p) + (uintptr_t)(r0 * ld * (int64_t)esz);
+      return Range{a, a + (uintptr_t)(((r1 - r0 - 1) * ld + width) * (int64_t)esz)};
+    };
+    std::vector<std::vector<Range>> in_r(chunks.size()), out_r(chunks.size());
+    for (size_t j = 0; j < chunks.size(); ++j)
+      for (const Piece& p : chunks[j]) {
+        const ss_seg& sg = segs[p.seg];
+        in_r[j].push_back(rows_span(sg.src, p.r0, p.r1, sg.src_ld, K, esz_in));
+        out_r[j].push_back(rows_span(sg.dst, p.r0, p.r1, sg.dst_ld, N, esz_out));
+        if (sg.dst_base && pass_kind != SS_PASS_BACKWARD)
+          out_r[j].push_back(rows_span(sg.dst_base, p.r0, p.r1, sg.base_ld, N, esz_base));
+      }
+    for (size_t j = 0; j < chunks.size(); ++j)
+      for (size_t k = chunks.size() - 1; k > j && wait_for[j] < 0; --k)
+        for (const Range& o : out_r[j]) {
+          bool hit = false;
+          for (const Range& i : in_r[k])
+            if (i.a < o.b && o.a < i.b) { hit = true; break; }
+          if (hit) { wait_for[j] = (int)k; break; }
+        }
+  }
+  const bool aliased = std::any_of(wait_for.begin(), wait_for.end(), [](int k) { return k >= 0; });
+  if (aliased)
+    return host_dispatch_aliased(ctx, pass_kind, block, role, segs, seg_status, stream, K, N, esz_in, esz_out,
+                                 esz_base, rows_total, chunks, wait_for);
   const size_t in_need = (size_t)target * K * esz_in, out_need = (size_t)target * N * esz_out;
   const size_t base_need = any_base ? (size_t)target * N * esz_base : 0;
   for (auto& hs : ctx->hslot) {

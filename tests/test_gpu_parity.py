@@ -665,3 +665,52 @@ def test_client_buffers_on_peer_gpu():
     torch.cuda.synchronize(0)
     for c in range(len(xs)):
         assert torch.equal(local[c], outr[c].to("cuda:0")), c
+
+
+@pytest.mark.parametrize("dims", [(1024, 2048), (2048, 1024), (1536, 1536)])
+def test_in_place_device_handoff_bitwise(dims):
+    """The reference hands the reply back in the request's own buffer (SharedBuffer,
+    transport.py:76-97). With the reply written over the request rows of a multi-wave dispatch,
+    every row must still equal the separate-buffer result (aliased sources are gathered
+    before the GEMM writes)."""
+    d_in, d_out = dims
+    w, b = O.layer_params(19, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)})
+    _mixed_clients(ex, d_in, d_out, seed=19, role=O.V)
+    counts = [3000, 1, 2500, 130, 5, 2048, 77]
+    dev = ex.device
+    for pass_kind, (wi, wo) in ((0, (d_in, d_out)), (1, (d_out, d_in))):
+        xs = [torch.randn(t, wi, device=dev).to(torch.bfloat16) for t in counts]
+        ref = ex._compute_batch(pass_kind, [_env(c, 140 + pass_kind, 0, O.V, pass_kind, x) for c, x in enumerate(xs)])
+        bufs = [torch.empty(t * max(wi, wo), dtype=torch.bfloat16, device=dev) for t in counts]
+        for x, buf in zip(xs, bufs):
+            buf[: x.numel()].copy_(x.reshape(-1))
+        got = ex._compute_batch(pass_kind, [_env(c, 150 + pass_kind, 0, O.V, pass_kind, bufs[c][: t * wi].view(t, wi),
+                                                 reply_to=bufs[c][: t * wo].view(t, wo))
+                                            for c, t in enumerate(counts)])
+        for c in range(len(counts)):
+            assert torch.equal(got[c], ref[c]), (pass_kind, c)
+
+
+def test_in_place_host_handoff_bitwise():
+    """Pinned-host clients whose reply buffer IS the request buffer (the reference's in-place
+    hand-off) through the pipelined host path: a sub-batch's reply must never land on request
+    rows a later sub-batch has not uploaded yet."""
+    d_in, d_out = 512, 1408
+    w, b = O.layer_params(20, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)})
+    ex.pipeline_rows = 128   # many sub-batches
+    _mixed_clients(ex, d_in, d_out, seed=20, role=O.V)
+    counts = [900, 1, 700, 130, 5, 1024, 77]
+    for pass_kind, (wi, wo) in ((0, (d_in, d_out)), (1, (d_out, d_in))):
+        xs = [torch.randn(t, wi).to(torch.bfloat16) for t in counts]
+        dev = ex._compute_batch(pass_kind, [_env(c, 160 + pass_kind, 0, O.V, pass_kind, x.to(ex.device))
+                                            for c, x in enumerate(xs)])
+        bufs = [torch.empty(t * max(wi, wo), dtype=torch.bfloat16).pin_memory() for t in counts]
+        for x, buf in zip(xs, bufs):
+            buf[: x.numel()].copy_(x.reshape(-1))
+        got = ex._compute_batch(pass_kind, [_env(c, 170 + pass_kind, 0, O.V, pass_kind, bufs[c][: t * wi].view(t, wi),
+                                                 reply_to=bufs[c][: t * wo].view(t, wo))
+                                            for c, t in enumerate(counts)])
+        for c in range(len(counts)):
+            assert torch.equal(got[c], dev[c].cpu()), (pass_kind, c)
