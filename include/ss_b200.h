@@ -230,7 +230,24 @@ SS_API int ss_profile(ss_ctx* ctx, int enable);
 SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* launches,
                            double* flops, double* bytes);
 
-/* Tuning knob: M-tile grouping of the persistent raster (default 16). */
+/* Tuning / testing knobs (none changes results: every kernel choice gives bitwise the same rows).
+ *   group_m (16)        M-tiles per raster group of the persistent GEMM
+ *   raster (0)          0 M-grouped, 1 N-grouped (W columns held in L2), -1 fewer modelled bytes
+ *   group_n, l2_budget_mb (0, 48)  N-group width (0: as many W columns as fit the budget)
+ *   l2_hints (1)        L2 evict_last on the operand a raster group re-reads, evict_first on outputs
+ *   gemm_2cta (-1)      CTA-pair kernel: -1 by dispatch size, 1 / 0 forced
+ *   pair_n (256)        CTA-pair tile width 256 (double-buffered TMEM) or 512
+ *   tile_n (0)          force the single-CTA tile width 64 / 128 / 256 (0 auto)
+ *   direct_tiles (1)    TMA-load whole tiles of bf16 segments in place (else gather everything)
+ *   tma_store (1)       bf16 outputs through swizzled smem + TMA bulk stores
+ *   stream_gemm (1)     weight-streaming kernel for dispatches of <= 64 rows (K % 64 == 0)
+ *   a_rows64 (1)        64-row A box for such dispatches in the single-CTA kernel
+ *   shrink_mode (0)     LoRA shrink: 0 auto, 1 one CTA per slab, 2 one CTA per (slab, K chunk)
+ *   shrink_kb_chunk     k-blocks (of 64) per fixed K chunk of the shrink
+ *   prefetch_mb, prefetch_rows, prefetch_hint, pf_depth (0, 256, 2, 0)  L2 prefetch of the next
+ *                       layer / of the launch's own W for small dispatches (measured slower: off)
+ *   force_remote (0)    testing: route every segment as if it lived on a peer GPU
+ *   pipeline_rows, pipeline_bytes  sub-batch size of ss_compute_batch_host */
 SS_API int ss_set_option(ss_ctx* ctx, const char* key, int64_t value);
 
 #ifdef __cplusplus

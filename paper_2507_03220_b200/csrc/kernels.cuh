@@ -535,6 +535,191 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
+// ============================================================================ K1/K2/K5, streaming
+// Weight-streaming variant of the single-CTA kernel for decode-size dispatches (one packed tile
+// of <= 64 rows, 64-wide N tiles): the GEMM only streams W, and a CTA keeps about eight TMA
+// operations in flight whatever their size (profiles/r01_l2_and_decode.md: 0.24 us per 64-deep
+// k-block at 3..8 stages of 8 KB boxes). So each operation moves 32 KB: one stage is SK = 256
+// of K — A as ONE 3-D box {64 k, 64 rows, 4 k-chunks} (chunk c = k-block c's 64 rows, 8 KB apart)
+// and W as ONE box {64 n, 256 k} (forward, MN-major) or 3-D {64 k, 64 n, 4 k-chunks}
+// (backward, K-major). The MMA of k-block c reads 128 A rows from chunk c: rows 64-127 are the
+// next chunk (or the stage's W bytes) — garbage rows whose outputs are never stored. Same MMAs
+// in the same K order as the other kernels: bitwise the same rows.
+constexpr int SK = 256;                                  // K per streaming stage
+constexpr int S_A_BYTES = 4 * 64 * 128;                  // 32 KB: 4 chunks x 64 rows x 128 B
+constexpr int S_B_BYTES = 64 * SK * 2;                   // 32 KB
+constexpr int S_STAGE = S_A_BYTES + S_B_BYTES;
+constexpr int S_STAGES = 3;
+constexpr int STREAM_SMEM = S_STAGES * S_STAGE + EPI_SMEM + 1024 + 256;
+
+template <bool kBwd>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    seg_gemm_stream_kernel(const __grid_constant__ CUtensorMap tmB,   // W stream map (see above)
+                           const __grid_constant__ CUtensorMap tmAL,  // A_lora [M, R_w] bf16
+                           const __grid_constant__ CUtensorMap tmBP,  // pack [R, N] bf16
+                           const GemmParams p) {
+  constexpr int TBN = 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* epi_stage = smem + S_STAGES * S_STAGE;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_stage + EPI_SMEM);
+  uint64_t* empty_bar = full_bar + S_STAGES;
+  uint64_t* tfull_bar = empty_bar + S_STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmB);
+    if (p.any_lora) {
+      tma_prefetch_desc(&tmAL);
+      tma_prefetch_desc(&tmBP);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < S_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * TBN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  const int nkb = (p.K + BK - 1) / BK;        // 64-deep k-blocks
+  const int nst = (nkb + 3) / 4;              // streaming stages per tile
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      const uint64_t pol_b = l2_policy(p.hint_b);
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, p, mb, nb);
+        const TileDesc td = p.tiles[mb];
+        const CUtensorMap* tmA = p.tmaps + td.amap;
+        const int n0 = nb * TBN;
+        tensormap_acquire(tmA);
+        for (int st = 0; st < nst; ++st) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          mbar_expect_tx(&full_bar[s], S_STAGE);
+          uint8_t* a = smem + s * S_STAGE;
+          uint8_t* b = a + S_A_BYTES;
+          tma_load_3d(a, tmA, &full_bar[s], 0, td.arow, st * 4);
+          if (kBwd) tma_load_3d(b, &tmB, &full_bar[s], 0, n0, st * 4);
+          else load_a_or_b(b, &tmB, &full_bar[s], n0, st * SK, p.hint_b, pol_b);
+          if (++s == S_STAGES) { s = 0; ph ^= 1; }
+        }
+        if (p.any_lora) {
+          const int cb = td.chunk_begin;
+          const int cc = td.chunk_count;
+          const int m0 = mb * BM;
+          for (int ls = 0; ls * 4 < cc; ++ls) {
+            const int nq = min(4, cc - ls * 4);
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nq * LORA_CHUNK_BYTES);
+            uint8_t* a = smem + s * S_STAGE;
+            uint8_t* b = a + S_A_BYTES;
+            tma_load_2d(a, &tmAL, &full_bar[s], ls * BK, m0);
+            for (int q = 0; q < nq; ++q)
+              tma_load_2d(b + q * LORA_CHUNK_BYTES, &tmBP, &full_bar[s], n0, p.chunks[cb + ls * 4 + q]);
+            if (++s == S_STAGES) { s = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_base = make_idesc_bf16(BM, TBN, false, !kBwd);
+    constexpr uint32_t idesc_lora = make_idesc_bf16(BM, TBN, false, true);
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, p, mb, nb);
+      mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * TBN;
+      for (int st = 0; st < nst; ++st) {
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(smem + s * S_STAGE);
+          const uint32_t b_addr = a_addr + S_A_BYTES;
+          const int kbs = min(4, nkb - st * 4);
+          for (int c = 0; c < kbs; ++c) {
+#pragma unroll
+            for (int k = 0; k < BK / UK; ++k) {
+              const uint64_t ad = make_sdesc_sw128(a_addr + c * 8192 + k * 32, 16, 1024);
+              const uint64_t bd = kBwd ? make_sdesc_sw128(b_addr + c * 8192 + k * 32, 16, 1024)
+                                       : make_sdesc_sw128(b_addr + (c * 4 + k) * (UK * 128), BK * 128, 1024);
+              mma_bf16_ss(d_tmem, ad, bd, idesc_base, (st | c | k) != 0);
+            }
+          }
+          mma_commit(&empty_bar[s]);
+        }
+        __syncwarp();
+        if (++s == S_STAGES) { s = 0; ph ^= 1; }
+      }
+      if (p.any_lora) {
+        const int cc = p.tiles[mb].chunk_count;
+        for (int ls = 0; ls * 4 < cc; ++ls) {
+          const int nq = min(4, cc - ls * 4);
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(smem + s * S_STAGE);
+            const uint32_t b_addr = a_addr + S_A_BYTES;
+            for (int q = 0; q < nq; ++q) {
+              const uint64_t ad = make_sdesc_sw128(a_addr + q * 32, 16, 1024);
+              const uint64_t bd = make_sdesc_sw128(b_addr + q * LORA_CHUNK_BYTES, BK * 128, 1024);
+              mma_bf16_ss(d_tmem, ad, bd, idesc_lora, 1u);
+            }
+            mma_commit(&empty_bar[s]);
+          }
+          __syncwarp();
+          if (++s == S_STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+      if (lane == 0) mma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  } else if (warp >= 4) {
+    const uint32_t ew = warp - 4;
+    const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, p, mb, nb);
+      const TileDesc td = p.tiles[mb];
+      epilogue_tile<TBN>(p, tmem_base + acc * TBN, ew, lane, td, 0, nb * TBN, &tfull_bar[acc], acc_ph,
+                         epi_stage, tempty0 + acc * 8);
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+    if (ew == 0 && lane == 0) bulk_wait_all();
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * TBN);
+  }
+}
+
 // ============================================================================ K1/K2/K5, 2-CTA
 // CTA pair (cluster of 2 on one TPC), tcgen05 cta_group::2: UMMA 256 x 256 x 16 per K step and
 // 256-column group. Each CTA stages its own 128 rows of A and half of the pair's B columns, so

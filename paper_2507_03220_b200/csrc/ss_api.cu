@@ -47,6 +47,7 @@ struct Layer {
   int64_t ldw = 0;
   float* bias = nullptr;
   CUtensorMap tm_w_fwd, tm_w_bwd, tm_w_bwd2, tm_w_bwd64;  // bwd box rows 256 / 128 / 64
+  CUtensorMap tm_w_fwd_s, tm_w_bwd_s;                      // weight-streaming kernel
   // LoRA packs: rows = rank index of every registered client (16-aligned blocks)
   __nv_bfloat16* at_pack = nullptr;  // [cap, ld_at]  (A^T: rank rows x d_in)
   __nv_bfloat16* b_pack = nullptr;   // [cap, ld_b]   (B:   rank rows x d_out)
@@ -124,6 +125,7 @@ struct ss_ctx {
   std::vector<cudaEvent_t> chunk_ev;
   uint64_t peers_enabled = 0;  // peer GPUs whose memory this context's kernels may touch
   int force_remote = 0;      // testing: route every segment as if it lived on a peer GPU
+  int stream_gemm = 1;       // weight-streaming kernel for those dispatches (K % 64 == 0)
   int a_rows64 = 1;          // 64-row A box for single-tile dispatches of <= 64 rows
   // L2 prefetch of the successor layer (forward order for FWD / NOISE, reverse for BWD) from
   // GEMMs of at most `prefetch_rows` rows, up to `prefetch_mb` MB (0 disables)
@@ -203,6 +205,26 @@ int encode_2d(ss_ctx* ctx, CUtensorMap* map, const void* base, uint64_t cols, ui
     return fail(ctx, SS_E_CUDA, "cuTensorMapEncodeTiled failed (%d) cols=%llu rows=%llu ld=%llu",
                 (int)r, (unsigned long long)cols, (unsigned long long)rows,
                 (unsigned long long)ld_elems);
+  return SS_OK;
+}
+
+// K-major operand [rows, cols] (row stride ld_elems, cols a multiple of 64 within ld) viewed as
+// {64 k, rows, cols / 64 chunks}: one box of {64, box_rows, box_chunks} loads several 64-wide
+// K chunks of box_rows rows in a single TMA operation, chunk c landing box_rows * 128 B after
+// chunk c - 1 (the 128B-swizzled K-major layout of each chunk is unchanged).
+int encode_kchunks(ss_ctx* ctx, CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                   uint64_t ld_elems, uint32_t box_rows, uint32_t box_chunks) {
+  cuuint64_t dims[3] = {64, rows, (cols + 63) / 64};
+  cuuint64_t strides[2] = {ld_elems * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, box_chunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ctx, SS_E_CUDA, "cuTensorMapEncodeTiled (3-D) failed (%d) cols=%llu rows=%llu ld=%llu",
+                (int)r, (unsigned long long)cols, (unsigned long long)rows, (unsigned long long)ld_elems);
   return SS_OK;
 }
 
@@ -423,7 +445,7 @@ int acquire_staging(ss_ctx* ctx, size_t total, Staging*& out) {
 struct Built {
   int pass_kind = 0, block = 0, role = 0, K = 0, N = 0;
   int64_t M = 0, MX = 0, lora_ld = 64, al_rows = 0, ldx = 0;
-  bool any_lora = false, pair = false, a_rows64 = false;
+  bool any_lora = false, pair = false, a_rows64 = false, stream = false;
   int tbn = BN, pn = 256, num_m = 0, n_piece = 0, n_items = 0, part_ld = 16, shrink_chunks_ = 1;
   int kb_chunk = SHRINK_KB_CHUNK;
   size_t off_tm = 0, off_seg = 0, off_tile = 0, off_piece = 0, off_ch = 0, off_st = 0, off_it = 0;
@@ -689,11 +711,18 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   }
 
   // ---- weight-streaming dispatch (one packed tile of <= 64 rows): the GEMM reads A through a
-  // 64-row box (MMA rows 64-127 are never stored), halving its per-stage operand bytes
+  // 64-row box (MMA rows 64-127 are never stored); with `stream_gemm` (K a multiple of 64) the
+  // streaming kernel moves 4 k-blocks of A and of W per TMA operation instead
   if (ctx->a_rows64 && !pair && num_m == 1 && direct_src.empty() && MX <= 64) {
     tiles[0].amap = (int32_t)tmaps.size();
     tmaps.emplace_back();
-    rc = encode_2d(ctx, &tmaps.back(), ctx->X, K, MX, ldx, 64, 64);
+    if (ctx->stream_gemm && K % 64 == 0 && !ctx->force_tbn) {
+      rc = encode_kchunks(ctx, &tmaps.back(), ctx->X, K, MX, ldx, 64, 4);
+      B.stream = true;
+      tbn = 64;
+    } else {
+      rc = encode_2d(ctx, &tmaps.back(), ctx->X, K, MX, ldx, 64, 64);
+    }
     if (rc) return rc;
     B.a_rows64 = true;
   }
@@ -892,7 +921,12 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   const int grid = pair ? 2 * std::min(ntiles, ctx->num_sms / 2) : std::min(ntiles, ctx->num_sms);
   const CUtensorMap& tmBP = any_lora ? (bwd ? L.tm_at : L.tm_b) : L.tm_w_fwd;
   const int pg = prof_begin(ctx, stream, SS_KERNEL_GEMM, B.gemm_flops, B.gemm_bytes);
-  if (pair && pn == 512) {
+  if (B.stream) {
+    if (bwd)
+      seg_gemm_stream_kernel<true><<<grid, GEMM_THREADS, STREAM_SMEM, stream>>>(L.tm_w_bwd_s, tmAL, tmBP, gpm);
+    else
+      seg_gemm_stream_kernel<false><<<grid, GEMM_THREADS, STREAM_SMEM, stream>>>(L.tm_w_fwd_s, tmAL, tmBP, gpm);
+  } else if (pair && pn == 512) {
     if (bwd)
       seg_gemm2_kernel<true, 512><<<grid, GEMM_THREADS, GEMM2W_SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
     else
@@ -956,6 +990,10 @@ int set_kernel_attrs(ss_ctx* ctx) {
                           GEMM2W_SMEM));
   CK(cudaFuncSetAttribute(seg_gemm2_kernel<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           GEMM2W_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_stream_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          STREAM_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_stream_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          STREAM_SMEM));
   CK(cudaFuncSetAttribute(lora_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           SHRINK_SMEM));
   CK(cudaFuncSetAttribute(lora_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GRAD_SMEM));
@@ -1147,6 +1185,10 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
     ctx->force_remote = value ? 1 : 0;
     return SS_OK;
   }
+  if (!strcmp(key, "stream_gemm")) {
+    ctx->stream_gemm = value ? 1 : 0;
+    return SS_OK;
+  }
   if (!strcmp(key, "a_rows64")) {
     ctx->a_rows64 = value ? 1 : 0;
     return SS_OK;
@@ -1215,6 +1257,11 @@ int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const v
   rc = encode_2d(ctx, &L.tm_w_bwd2, L.W, d_out, d_in, L.ldw, 64, BN / 2);
   if (rc) return rc;
   rc = encode_2d(ctx, &L.tm_w_bwd64, L.W, d_out, d_in, L.ldw, 64, 64);
+  if (rc) return rc;
+  // weight-streaming kernel: forward box {64 n, 256 k}; backward 4 K-chunks of 64 rows at once
+  rc = encode_2d(ctx, &L.tm_w_fwd_s, L.W, d_out, d_in, L.ldw, 64, SK);
+  if (rc) return rc;
+  rc = encode_kchunks(ctx, &L.tm_w_bwd_s, L.W, L.ldw, d_in, L.ldw, 64, 4);
   if (rc) return rc;
   ctx->weight_bytes += (int64_t)d_in * L.ldw * 2 + (bias ? round_up(d_out, 64) * 4 : 0);
   ctx->layers[{block, role}] = L;

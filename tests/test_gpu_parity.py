@@ -621,27 +621,34 @@ def test_peer_gpu_routing_bitwise_equals_local():
 
 
 def test_decode_size_dispatch_64_row_box_bitwise():
-    """A dispatch of <= 64 packed rows reads its operand through a 64-row TMA box (MMA rows
-    64-127 are never stored). Its rows must equal the 128-row-box rows and the same clients'
-    rows inside a prefill-size dispatch (batching invisibility at decode sizes)."""
+    """A dispatch of <= 64 packed rows runs the weight-streaming kernel (4 k-blocks of A and W
+    per TMA operation, 64-row A boxes whose MMA rows 64-127 are never stored) or, with it off,
+    the single-CTA kernel with a 64- or 128-row A box. All must give the same bits, equal to
+    the same clients' rows inside a prefill-size dispatch (batching invisibility at decode
+    sizes), forward and backward, every adapter kind."""
     d_in, d_out = 5120, 1024
     w, b = O.layer_params(17, 0, O.K, d_in, d_out)
     ex = _ex({(0, O.K): (w, b)})
     _mixed_clients(ex, d_in, d_out, seed=17)
     counts = [2, 2, 1, 2, 2, 3, 2]                      # 14 decode rows, every adapter kind
     dev = ex.device
-    xs = [torch.randn(t, d_in, device=dev).to(torch.bfloat16) for t in counts]
-    outs = {}
-    for box64 in (1, 0):
-        ex.ctx.set_option("a_rows64", box64)
-        outs[box64] = ex._compute_batch(0, [_env(c, 110 + box64, 0, O.K, 0, x) for c, x in enumerate(xs)])
-    ex.ctx.set_option("a_rows64", 1)
-    filler = torch.randn(3000, d_in, device=dev).to(torch.bfloat16)
-    big = ex._compute_batch(0, [_env(c, 120, 0, O.K, 0, x) for c, x in enumerate(xs)] +
-                            [_env(1, 121, 0, O.K, 0, filler)])
-    for c in range(len(xs)):
-        assert torch.equal(outs[1][c], outs[0][c]), c
-        assert torch.equal(outs[1][c], big[c]), c
+    for pass_kind, width in ((0, d_in), (1, d_out)):
+        xs = [torch.randn(t, width, device=dev).to(torch.bfloat16) for t in counts]
+        outs = []
+        for stream, box64 in ((1, 1), (0, 1), (0, 0)):
+            ex.ctx.set_option("stream_gemm", stream)
+            ex.ctx.set_option("a_rows64", box64)
+            outs.append(ex._compute_batch(pass_kind, [_env(c, 110 + 4 * pass_kind + len(outs), 0, O.K, pass_kind, x)
+                                                      for c, x in enumerate(xs)]))
+        ex.ctx.set_option("stream_gemm", 1)
+        ex.ctx.set_option("a_rows64", 1)
+        filler = torch.randn(3000, width, device=dev).to(torch.bfloat16)
+        big = ex._compute_batch(pass_kind, [_env(c, 120 + pass_kind, 0, O.K, pass_kind, x) for c, x in enumerate(xs)] +
+                                [_env(1, 122 + pass_kind, 0, O.K, pass_kind, filler)])
+        for c in range(len(xs)):
+            for k in (1, 2):
+                assert torch.equal(outs[0][c], outs[k][c]), (pass_kind, k, c)
+            assert torch.equal(outs[0][c], big[c]), (pass_kind, c)
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
