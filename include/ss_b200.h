@@ -246,6 +246,7 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   shrink_kb_chunk     k-blocks (of 64) per fixed K chunk of the shrink
  *   prefetch_mb, prefetch_rows, prefetch_hint, pf_depth (0, 256, 2, 0)  L2 prefetch of the next
  *                       layer / of the launch's own W for small dispatches (measured slower: off)
+ *   pdl (0)             programmatic dependent launch between a dispatch's kernels (no gain measured)
  *   force_remote (0)    testing: route every segment as if it lived on a peer GPU
  *   pipeline_rows, pipeline_bytes  sub-batch size of ss_compute_batch_host */
 SS_API int ss_set_option(ss_ctx* ctx, const char* key, int64_t value);

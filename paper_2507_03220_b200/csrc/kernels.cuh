@@ -384,6 +384,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
   const int nkb = (p.K + BK - 1) / BK;
@@ -594,6 +596,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
   const int nkb = (p.K + BK - 1) / BK;        // 64-deep k-blocks
@@ -796,6 +800,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
   const int nkb = (p.K + BK - 1) / BK;
@@ -978,7 +984,8 @@ struct ShrinkItem {
   int32_t orow;   // first output row in A_lora (tile * TM + row offset within tile)
   int32_t col0;   // column of this segment's rank block in its tile
   int32_t pack;   // 0: pack map tmP, contraction K = p.K; 1: tmP2, K = p.K2 (gradient shrinks)
-  int32_t pad1;
+  int32_t a_rows; // rows one A box delivers (128, or 16 for short pieces: MMA rows past the box
+                  // are stale smem whose outputs are never written); 0 = 128
 };
 
 struct ShrinkParams {
@@ -1058,6 +1065,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
   const int nchunk = npad / LORA_CHUNK;
   __shared__ int last_flag;
 
@@ -1067,7 +1076,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
       uint32_t ph = 0;
       for (int kb = c0 * p.kb_chunk; kb < min(nkb_all, c1 * p.kb_chunk); ++kb) {
         mbar_wait(&empty_bar[s], ph ^ 1);
-        mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nchunk * LORA_CHUNK_BYTES);
+        mbar_expect_tx(&full_bar[s], (it.a_rows ? it.a_rows * 128 : A_STAGE_BYTES) + nchunk * LORA_CHUNK_BYTES);
         tma_load_2d(SHRINK_A(s), tmA, &full_bar[s], kb * BK, it.arow);
         for (int q = 0; q < nchunk; ++q)
           tma_load_2d(SHRINK_B(s) + q * LORA_CHUNK_BYTES, tmPk, &full_bar[s], kb * BK,
@@ -1229,6 +1238,7 @@ struct GatherParams {
   int MX, K;              // packed rows, width
   int ldx;
   int n_piece;
+  int nsplit;             // column chunks per row (several warps per row for small dispatches)
   int ia3_in_prologue;    // backward: g = dy * l
   const DevSeg* segs;
   const int32_t* piece_seg;  // segment of each packed piece, in X order
@@ -1246,13 +1256,30 @@ __device__ __forceinline__ int find_piece(const GatherParams& p, int xrow) {
 }
 
 // One warp per row, grid-stride.
+// Zero `n16` 16-byte words (the block-diagonal LoRA operand before the shrink writes its
+// blocks); a kernel rather than a memset node so the dispatch stays one chain of PDL launches.
+__global__ void __launch_bounds__(256) zero_kernel(uint4* __restrict__ p, int64_t n16) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = make_uint4(0, 0, 0, 0);
+}
+
 __global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
-  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < p.MX; row += gridDim.x * wpb) {
+  // work item = (row, column chunk): a decode-size dispatch (tens of rows) still spreads over
+  // the whole GPU instead of one latency-bound warp per row
+  const int nchunk8 = (p.K / 8 + p.nsplit - 1) / p.nsplit;     // 8-element units per chunk
+  for (int w = blockIdx.x * wpb + (threadIdx.x >> 5); w < p.MX * p.nsplit; w += gridDim.x * wpb) {
+    const int row = w / p.nsplit, part = w - row * p.nsplit;
+    const int u0 = part * nchunk8, u1 = min(p.K / 8, u0 + nchunk8);   // vector units [u0, u1)
+    const int e0 = part == 0 ? 0 : u0 * 8, e1 = part == p.nsplit - 1 ? p.K : u1 * 8;  // scalar range
     const int si = find_piece(p, row);
     const DevSeg& sg = p.segs[si];
-    if (lane == 0) p.row_seg[row] = si;
+    if (lane == 0 && part == 0) p.row_seg[row] = si;
     const int64_t lr = row - sg.xrow0 + sg.xlocal0;
     __nv_bfloat16* xr = p.X + (int64_t)row * p.ldx;
     const bool scale = p.ia3_in_prologue && (sg.flags & SEGF_IA3);
@@ -1263,12 +1290,13 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) 
       if (vec && !scale) {
         const uint4* s4 = reinterpret_cast<const uint4*>(sr);
         uint4* d4 = reinterpret_cast<uint4*>(xr);
-        for (int i = lane; i < p.K / 8; i += 32) d4[i] = __ldg(s4 + i);
+#pragma unroll 4
+        for (int i = u0 + lane; i < u1; i += 32) d4[i] = __ldg(s4 + i);
       } else if (vec) {
         // IA3 backward prologue, 8 bf16 per lane per step: g = dy * l (client.py:291-294)
         const uint4* s4 = reinterpret_cast<const uint4*>(sr);
         uint4* d4 = reinterpret_cast<uint4*>(xr);
-        for (int i = lane; i < p.K / 8; i += 32) {
+        for (int i = u0 + lane; i < u1; i += 32) {
           const uint4 raw = __ldg(s4 + i);
           const float4 la = __ldg(reinterpret_cast<const float4*>(l) + 2 * i);
           const float4 lb = __ldg(reinterpret_cast<const float4*>(l) + 2 * i + 1);
@@ -1279,7 +1307,7 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) 
                              pack_bf16x2(f2.x * lb.x, f2.y * lb.y), pack_bf16x2(f3.x * lb.z, f3.y * lb.w));
         }
       } else {
-        for (int i = lane; i < p.K; i += 32) {
+        for (int i = e0 + lane; i < e1; i += 32) {
           float v = __bfloat162float(sr[i]);
           if (scale) v *= __ldg(l + i);
           xr[i] = __float2bfloat16_rn(v);
@@ -1290,7 +1318,7 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) 
       if (vec) {
         const float4* s4 = reinterpret_cast<const float4*>(sr);
         uint4* d4 = reinterpret_cast<uint4*>(xr);
-        for (int i = lane; i < p.K / 8; i += 32) {
+        for (int i = u0 + lane; i < u1; i += 32) {
           float4 a = __ldg(s4 + 2 * i), b = __ldg(s4 + 2 * i + 1);
           if (scale) {
             const float4 la = __ldg(reinterpret_cast<const float4*>(l) + 2 * i);
@@ -1302,7 +1330,7 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) 
                              pack_bf16x2(b.z, b.w));
         }
       } else {
-        for (int i = lane; i < p.K; i += 32) {
+        for (int i = e0 + lane; i < e1; i += 32) {
           float v = sr[i];
           if (scale) v *= __ldg(l + i);
           xr[i] = __float2bfloat16_rn(v);

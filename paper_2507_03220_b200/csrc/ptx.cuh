@@ -78,6 +78,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels of a dispatch are launched with programmatic stream serialization: a kernel may be
+// scheduled while its predecessor drains, runs its prologue (barriers, TMEM, descriptor
+// prefetch), then waits here for the predecessor grid's completion and memory before touching
+// any global data. A no-op when launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

@@ -125,6 +125,7 @@ struct ss_ctx {
   std::vector<cudaEvent_t> chunk_ev;
   uint64_t peers_enabled = 0;  // peer GPUs whose memory this context's kernels may touch
   int force_remote = 0;      // testing: route every segment as if it lived on a peer GPU
+  int pdl = 0;               // programmatic dependent launch between a dispatch's kernels (measured: no gain)
   int stream_gemm = 1;       // weight-streaming kernel for those dispatches (K % 64 == 0)
   int a_rows64 = 1;          // 64-row A box for single-tile dispatches of <= 64 rows
   // L2 prefetch of the successor layer (forward order for FWD / NOISE, reverse for BWD) from
@@ -727,6 +728,23 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     B.a_rows64 = true;
   }
 
+  // ---- short LoRA pieces of the packed operand (decode rows): the shrink reads them through a
+  // 16-row box instead of 128 rows of neighbouring clients' rows
+  if (any_lora && MX > 0) {
+    int32_t small_map = -1;
+    for (ShrinkItem& it : items) {
+      if (it.amap != 0 || it.rows > 16) continue;
+      if (small_map < 0) {
+        small_map = (int32_t)tmaps.size();
+        tmaps.emplace_back();
+        rc = encode_2d(ctx, &tmaps.back(), ctx->X, K, MX, ldx, 64, 16);
+        if (rc) return rc;
+      }
+      it.amap = small_map;
+      it.a_rows = 16;
+    }
+  }
+
   // ---- serialise the device tables
   const size_t off_tm = 0;
   const size_t off_seg = round_up(tmaps.size() * sizeof(CUtensorMap), 256);
@@ -784,6 +802,25 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   return SS_OK;
 }
 
+// Kernel launch with programmatic stream serialization (ctx->pdl): the kernel may start its
+// prologue while the previous kernel on the stream drains; it waits (griddepcontrol.wait) before
+// touching global data. Captured into graphs as programmatic edges.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(const ss_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl && !ctx->profiling ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Launch the kernels of a built batch whose tables are at device address `dv` (stream-ordered
 // after whatever copied them there).
 int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
@@ -812,9 +849,11 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     gp.piece_seg = reinterpret_cast<const int32_t*>(dv + B.off_piece);
     gp.X = ctx->X;
     gp.row_seg = ctx->row_seg;
-    const int grid = (int)std::min<int64_t>((MX + 7) / 8, (int64_t)ctx->num_sms * 8);
+    // several warps per row when the dispatch has too few rows to fill the GPU
+    gp.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((K / 8 + 127) / 128, ((int64_t)ctx->num_sms * 16 + MX - 1) / MX));
+    const int grid = (int)std::min<int64_t>((MX * gp.nsplit + 7) / 8, (int64_t)ctx->num_sms * 8);
     const int pi = prof_begin(ctx, stream, SS_KERNEL_GATHER, 0.0, B.gather_bytes);
-    gather_rows_kernel<<<grid, 256, 0, stream>>>(gp);
+    CK(launch_k(ctx, gather_rows_kernel, grid, 256, 0, stream, gp));
     prof_end(ctx, stream, pi);
     CK(cudaGetLastError());
     ctx->launches++;
@@ -825,7 +864,12 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, BM);
     if (rc) return rc;
     // ---- K3 shrink into the zeroed block-diagonal operand
-    CK(cudaMemsetAsync(ctx->a_lora, 0, (size_t)al_rows * lora_ld * 2, stream));
+    {
+      const int64_t n16 = al_rows * lora_ld * 2 / 16;
+      CK(launch_k(ctx, zero_kernel, (int)std::min<int64_t>((n16 + 255) / 256, ctx->num_sms * 4), 256, 0, stream,
+                  reinterpret_cast<uint4*>(ctx->a_lora), n16));
+      ctx->launches++;
+    }
     ShrinkParams sp;
     sp.K = K;
     sp.lora_ld = (int)lora_ld;
@@ -844,8 +888,8 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     // ranks fit the register sums; else one CTA per (slab, chunk). Same sums either way.
     const bool whole = B.shrink_chunks_ == 1 ||
                        (B.part_ld <= 64 && (ctx->shrink_mode == 1 || (ctx->shrink_mode == 0 && B.n_items >= ctx->num_sms)));
-    lora_shrink_kernel<<<dim3(B.n_items, whole ? 1 : B.shrink_chunks_), GEMM_THREADS, SHRINK_SMEM, stream>>>(bwd ? L.tm_b : L.tm_at,
-                                                                               bwd ? L.tm_b : L.tm_at, sp);
+    CK(launch_k(ctx, lora_shrink_kernel, dim3(B.n_items, whole ? 1 : B.shrink_chunks_), GEMM_THREADS, SHRINK_SMEM,
+                stream, bwd ? L.tm_b : L.tm_at, bwd ? L.tm_b : L.tm_at, sp));
     prof_end(ctx, stream, pi);
     CK(cudaGetLastError());
     ctx->launches++;
@@ -923,28 +967,28 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   const int pg = prof_begin(ctx, stream, SS_KERNEL_GEMM, B.gemm_flops, B.gemm_bytes);
   if (B.stream) {
     if (bwd)
-      seg_gemm_stream_kernel<true><<<grid, GEMM_THREADS, STREAM_SMEM, stream>>>(L.tm_w_bwd_s, tmAL, tmBP, gpm);
+      CK(launch_k(ctx, seg_gemm_stream_kernel<true>, grid, GEMM_THREADS, STREAM_SMEM, stream, L.tm_w_bwd_s, tmAL, tmBP, gpm));
     else
-      seg_gemm_stream_kernel<false><<<grid, GEMM_THREADS, STREAM_SMEM, stream>>>(L.tm_w_fwd_s, tmAL, tmBP, gpm);
+      CK(launch_k(ctx, seg_gemm_stream_kernel<false>, grid, GEMM_THREADS, STREAM_SMEM, stream, L.tm_w_fwd_s, tmAL, tmBP, gpm));
   } else if (pair && pn == 512) {
     if (bwd)
-      seg_gemm2_kernel<true, 512><<<grid, GEMM_THREADS, GEMM2W_SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
+      CK(launch_k(ctx, seg_gemm2_kernel<true, 512>, grid, GEMM_THREADS, GEMM2W_SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, gpm));
     else
-      seg_gemm2_kernel<false, 512><<<grid, GEMM_THREADS, GEMM2W_SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
+      CK(launch_k(ctx, seg_gemm2_kernel<false, 512>, grid, GEMM_THREADS, GEMM2W_SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
   } else if (pair) {
     if (bwd)
-      seg_gemm2_kernel<true, 256><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
+      CK(launch_k(ctx, seg_gemm2_kernel<true, 256>, grid, GEMM_THREADS, GEMM2_SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, gpm));
     else
-      seg_gemm2_kernel<false, 256><<<grid, GEMM_THREADS, GEMM2_SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
+      CK(launch_k(ctx, seg_gemm2_kernel<false, 256>, grid, GEMM_THREADS, GEMM2_SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
   } else if (tbn == 256) {
-    if (bwd) seg_gemm_kernel<true, 256><<<grid, GEMM_THREADS, TileCfg<256>::SMEM, stream>>>(L.tm_w_bwd, tmAL, tmBP, gpm);
-    else seg_gemm_kernel<false, 256><<<grid, GEMM_THREADS, TileCfg<256>::SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
+    if (bwd) CK(launch_k(ctx, seg_gemm_kernel<true, 256>, grid, GEMM_THREADS, TileCfg<256>::SMEM, stream, L.tm_w_bwd, tmAL, tmBP, gpm));
+    else CK(launch_k(ctx, seg_gemm_kernel<false, 256>, grid, GEMM_THREADS, TileCfg<256>::SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
   } else if (tbn == 128) {
-    if (bwd) seg_gemm_kernel<true, 128><<<grid, GEMM_THREADS, TileCfg<128>::SMEM, stream>>>(L.tm_w_bwd2, tmAL, tmBP, gpm);
-    else seg_gemm_kernel<false, 128><<<grid, GEMM_THREADS, TileCfg<128>::SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
+    if (bwd) CK(launch_k(ctx, seg_gemm_kernel<true, 128>, grid, GEMM_THREADS, TileCfg<128>::SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, gpm));
+    else CK(launch_k(ctx, seg_gemm_kernel<false, 128>, grid, GEMM_THREADS, TileCfg<128>::SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
   } else {
-    if (bwd) seg_gemm_kernel<true, 64><<<grid, GEMM_THREADS, TileCfg<64>::SMEM, stream>>>(L.tm_w_bwd64, tmAL, tmBP, gpm);
-    else seg_gemm_kernel<false, 64><<<grid, GEMM_THREADS, TileCfg<64>::SMEM, stream>>>(L.tm_w_fwd, tmAL, tmBP, gpm);
+    if (bwd) CK(launch_k(ctx, seg_gemm_kernel<true, 64>, grid, GEMM_THREADS, TileCfg<64>::SMEM, stream, L.tm_w_bwd64, tmAL, tmBP, gpm));
+    else CK(launch_k(ctx, seg_gemm_kernel<false, 64>, grid, GEMM_THREADS, TileCfg<64>::SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
   }
   prof_end(ctx, stream, pg);
   CK(cudaGetLastError());
@@ -1183,6 +1227,10 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_remote")) {
     ctx->force_remote = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "pdl")) {
+    ctx->pdl = value ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "stream_gemm")) {
