@@ -317,6 +317,15 @@ def e2e_leg(ex, wl_key, specs, steps, device):
         h.normal_()
     rid = [0]
     h2d = d2h = 0
+    views = {}
+
+    def view(bufs, c, w):
+        # clients reuse their exchange buffers (SharedBuffer style): one view per (client, width)
+        key = (id(bufs), c, w)
+        v = views.get(key)
+        if v is None:
+            v = views[key] = bufs[c][: t * w].view(t, w)
+        return v
 
     def step():
         nonlocal h2d, d2h
@@ -326,8 +335,7 @@ def e2e_leg(ex, wl_key, specs, steps, device):
             envs = []
             for c in range(len(specs)):
                 rid[0] += 1
-                envs.append(Envelope(c, rid[0], b, r, 0, host[c][: t * di].view(t, di),
-                                     reply_to=reply[c][: t * do].view(t, do)))
+                envs.append(Envelope(c, rid[0], b, r, 0, view(host, c, di), reply_to=view(reply, c, do)))
                 h2d += t * di * 2
                 d2h += t * do * 2
             ex.serve_forward(envs)
@@ -338,8 +346,7 @@ def e2e_leg(ex, wl_key, specs, steps, device):
                 if not ft:
                     continue
                 rid[0] += 1
-                envs.append(Envelope(c, rid[0], b, r, 1, host[c][: t * do].view(t, do),
-                                     reply_to=reply[c][: t * di].view(t, di)))
+                envs.append(Envelope(c, rid[0], b, r, 1, view(host, c, do), reply_to=view(reply, c, di)))
                 h2d += t * do * 2
                 d2h += t * di * 2
             ex.serve_backward(envs)

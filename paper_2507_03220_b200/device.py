@@ -9,6 +9,7 @@ ctypes call.
 from __future__ import annotations
 
 import ctypes
+import struct
 from dataclasses import dataclass
 from typing import Any, Sequence
 
@@ -40,9 +41,10 @@ def _host_or_device(arr) -> tuple[Any, int, int, Any]:
 
 
 def tensor_flags(t: torch.Tensor) -> int:
-    if t.dtype == torch.bfloat16:
+    dt = t.dtype
+    if dt is _BF16:
         return 1
-    if t.dtype == torch.float32:
+    if dt is _F32:
         return 0
     raise TypeError(f"activations must be float32 or bfloat16, got {t.dtype}")
 
@@ -59,48 +61,53 @@ class Seg:
     width: int | None = None   # declared width (defaults to src.shape[1])
 
 
+_SEG_FMT = struct.Struct("<4I QqQqQq")          # ss_seg layout (include/ss_b200.h)
+assert _SEG_FMT.size == ctypes.sizeof(SsSeg)
+_BF16, _F32 = torch.bfloat16, torch.float32
+
+
 class SegmentTable:
-    """A prebuilt ctypes segment array for a fixed set of buffers (reused every step)."""
+    """A ctypes ss_seg array for one dispatch (prebuilt tables reuse it every step). Packed
+    with one struct.pack_into per segment into the array's buffer: a decode dispatch has tens
+    of segments and the per-field ctypes setters cost more than the dispatch's GPU work."""
 
     def __init__(self, segs: Sequence[Seg]):
         self.n = len(segs)
         self.arr = (SsSeg * max(1, self.n))()
         self.status = (ctypes.c_int32 * max(1, self.n))()
         self._keep = list(segs)
+        buf = memoryview(self.arr).cast("B")
         for i, s in enumerate(segs):
-            fill_seg(self.arr[i], s)
+            _SEG_FMT.pack_into(buf, i * _SEG_FMT.size, *seg_fields(s))
 
     def statuses(self) -> list[int]:
-        return [int(self.status[i]) for i in range(self.n)]
+        return list(self.status)[: self.n]
 
 
-def fill_seg(c: SsSeg, s: Seg) -> None:
-    src, dst = s.src, s.dst
-    if src.dim() != 2 or dst.dim() != 2 or src.stride(1) != 1 or dst.stride(1) != 1:
+def _row_ld(stride: tuple, shape) -> int:
+    return stride[0] if shape[0] > 1 else max(stride[0], shape[1])
+
+
+def seg_fields(s: Seg) -> tuple:
+    """The ss_seg field values of one segment (client_id, rows, width, flags, src, src_ld, dst,
+    dst_ld, dst_base, base_ld)."""
+    src, dst, base = s.src, s.dst, s.base
+    ss, sd = src.stride(), dst.stride()
+    if len(ss) != 2 or len(sd) != 2 or ss[1] != 1 or sd[1] != 1:
         raise ValueError("segment tensors must be 2-d with unit column stride")
-    c.client_id = int(s.client_id)
-    c.rows = int(src.shape[0])
-    c.width = int(s.width if s.width is not None else src.shape[1])
-    flags = 0
-    if tensor_flags(src):
-        flags |= _lib.SS_SEGF_SRC_BF16
-    if tensor_flags(dst):
-        flags |= _lib.SS_SEGF_DST_BF16
+    shs, shd = src.shape, dst.shape
+    flags = ((_lib.SS_SEGF_SRC_BF16 if tensor_flags(src) else 0) |
+             (_lib.SS_SEGF_DST_BF16 if tensor_flags(dst) else 0))
     if s.adapter:
         flags |= _lib.SS_SEGF_ADAPTER
-    c.src = src.data_ptr()
-    c.src_ld = src.stride(0) if src.shape[0] > 1 else max(src.stride(0), src.shape[1])
-    c.dst = dst.data_ptr()
-    c.dst_ld = dst.stride(0) if dst.shape[0] > 1 else max(dst.stride(0), dst.shape[1])
-    if s.base is not None:
-        if tensor_flags(s.base):
+    if base is not None:
+        if tensor_flags(base):
             flags |= _lib.SS_SEGF_BASE_BF16
-        c.dst_base = s.base.data_ptr()
-        c.base_ld = s.base.stride(0) if s.base.shape[0] > 1 else max(s.base.stride(0), s.base.shape[1])
+        bptr, bld = base.data_ptr(), _row_ld(base.stride(), base.shape)
     else:
-        c.dst_base = None
-        c.base_ld = 0
-    c.flags = flags
+        bptr, bld = 0, 0
+    return (int(s.client_id), shs[0], int(s.width if s.width is not None else shs[1]), flags,
+            src.data_ptr(), _row_ld(ss, shs), dst.data_ptr(), _row_ld(sd, shd), bptr, bld)
 
 
 class Plan:

@@ -433,8 +433,11 @@ class GpuBaseExecutor:
         and the D2H copy of j-1 overlap the kernels of j (its own copy streams and device
         staging ring). Rows are independent and the kernels never mix rows (tensor_ops.py:1-8),
         so results are bitwise those of one device-resident batch."""
-        self.ctx.set_option("pipeline_rows", int(self.pipeline_rows))
-        self.ctx.set_option("pipeline_bytes", int(self.pipeline_bytes))
+        knobs = (int(self.pipeline_rows), int(self.pipeline_bytes))
+        if knobs != getattr(self, "_pipeline_knobs", None):
+            self.ctx.set_option("pipeline_rows", knobs[0])
+            self.ctx.set_option("pipeline_bytes", knobs[1])
+            self._pipeline_knobs = knobs
         fused = self._fused
         in_w = envelopes[good[0]].width
         segs = [Seg(client_id=envelopes[i].client_id, src=envelopes[i].payload, dst=envelopes[i].reply_to,
