@@ -102,6 +102,49 @@ def flops_per_step(wl, specs):
 
 # ============================================================================ GPU leg
 
+def cublas_same_shapes(wl_key, specs, device, reps=2):
+    """torch.matmul (cuBLAS) bf16 over the step's GEMM shapes — every layer forward at the
+    dispatch's M, then backward (dy.W^T) at the fine-tune clients' M — without adapters,
+    gather/scatter or epilogue, on the same box right after the timed region: the library
+    baseline the fused kernel is compared against (box-to-box power-state variance cancels)."""
+    import torch
+    wl = WORKLOADS[wl_key]
+    layers, dims = layer_list(wl)
+    t = wl["tokens"]
+    m_f = len(specs) * t
+    m_b = sum(1 for _, _, ft in specs if ft) * t
+    g = torch.Generator(device=device).manual_seed(7)
+    W = {r: (torch.randn(di, do, generator=g, device=device) / math.sqrt(di)).to(torch.bfloat16)
+         for r, (di, do) in dims.items()}
+    wmax = max(max(di, do) for di, do in dims.values())
+    X = torch.randn(m_f * wmax, generator=g, device=device).to(torch.bfloat16)
+    Y = torch.empty(m_f * wmax, dtype=torch.bfloat16, device=device)
+
+    def step():
+        for (_, r) in layers:
+            di, do = dims[r]
+            torch.matmul(X[: m_f * di].view(m_f, di), W[r], out=Y[: m_f * do].view(m_f, do))
+        if m_b:
+            for (_, r) in reversed(layers):
+                di, do = dims[r]
+                torch.matmul(X[: m_b * do].view(m_b, do), W[r].t(), out=Y[: m_b * di].view(m_b, di))
+
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = sum(2.0 * m_f * dims[r][0] * dims[r][1] + 2.0 * m_b * dims[r][0] * dims[r][1] for (_, r) in layers)
+    del X, Y, W
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "tflops": flops / (ms / 1e3) / 1e12, "gemms_per_step": len(layers) * (2 if m_b else 1),
+            "what": "torch.matmul bf16 (cuBLAS), the step's GEMM shapes without adapters, same box, after the timed region"}
+
+
 def nvsmi_sampler(stop: threading.Event, out: list, index: int):
     cmd = ["nvidia-smi", f"--id={index}",
            "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -674,6 +717,11 @@ def main():
         # the whole fine-tune step: executor fwd + bwd plus every FT client's adapter gradients
         grads_leg["ft_step_tokens_per_s"] = tokens / ((ms + grads_leg["ms_per_step"]) / 1e3)
 
+    cublas = None
+    if rank == 0 and world == 1 and not tp_mode and not args.workload.endswith("decode"):
+        cublas = cublas_same_shapes(args.workload, specs, device)
+        cublas["gemm_time_ratio"] = cublas["ms_per_step"] / (gemm["ms"] / prof_steps) if gemm["ms"] else None
+
     e2e = None
     if not args.skip_e2e and not tp_mode:
         dt, h2d, d2h = e2e_leg(ex, args.workload, specs, max(1, args.e2e_steps), device)
@@ -716,7 +764,10 @@ def main():
                           # the GEMM runs inside a long power-capped step, so the sustained
                           # cuBLAS figure is the denominator; against the burst figure:
                           "peak_burst": peak_burst,
-                          "frac_burst": (gemm_tflops / peak_burst) if gemm_tflops else None}
+                          "frac_burst": (gemm_tflops / peak_burst) if gemm_tflops else None,
+                          # cuBLAS on the same GEMM shapes, same box (ratio > 1: the fused kernel,
+                          # which also does the adapters / IA3 / scatter, takes less time)
+                          "cublas_same_shapes": cublas}
                          if not decode else
                          {"bound": "hbm", "kernel": "seg_gemm_kernel (decode: weight-streaming, 64-row dispatches)",
                           "achieved": gemm_gbs, "peak": hbm_peak, "unit": "GB/s",

@@ -204,11 +204,14 @@ constexpr int EPI_SMEM = 2 * EPI_STAGE_BYTES;           // double-buffered
 // f32 or misaligned fall back to direct global stores. Releases the TMEM accumulator (tempty)
 // as soon as its last column has been read. `store_row0` = this CTA's first row within the
 // tile (0, or 128 for the second CTA of a pair).
+// `c_begin`..`c_end` = this warp group's 64-column chunks (a 512-wide pair tile splits them over
+// two groups of 4 warps, each with its own staging buffers and named barrier `bar_id`).
 template <int TBN>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, uint32_t ew,
                                               uint32_t lane, const TileDesc& td, int store_row0, int n0,
                                               uint64_t* tfull, uint32_t tfull_ph, uint8_t* stage,
-                                              uint32_t tempty_cluster_addr) {
+                                              uint32_t tempty_cluster_addr, int c_begin = 0,
+                                              int c_end = TBN / EPI_CHUNK, uint32_t bar_id = 1) {
   const int r = store_row0 + ew * 32 + lane;  // row within the tile
   const bool row_ok = r < td.rows;
   const bool leader_thread = ew == 0 && lane == 0;
@@ -236,13 +239,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
   mbar_wait(tfull, tfull_ph);
   tc_fence_after();
 #pragma unroll 1
-  for (int c = 0; c < TBN / EPI_CHUNK; ++c) {
+  for (int c = c_begin; c < c_end; ++c) {
     uint32_t ra[32], rb[32];
     tmem_ld_32x32b_x32(tmem_acc + c * EPI_CHUNK + ((ew * 32u) << 16), ra);
     tmem_ld_32x32b_x32(tmem_acc + c * EPI_CHUNK + 32 + ((ew * 32u) << 16), rb);
     tmem_wait_ld();
-    if (c == TBN / EPI_CHUNK - 1) {
-      // every column of the accumulator is in registers: hand TMEM back to the MMA warp
+    if (c == c_end - 1) {
+      // every column of this warp's share is in registers: hand TMEM back to the MMA warp
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_cluster_addr);
@@ -298,7 +301,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     if (td.store_count > 0) {
       uint8_t* sb = stage + (c & 1) * EPI_STAGE_BYTES;
       if (leader_thread) bulk_wait_read<1>();      // the store issued 2 chunks ago freed `sb`
-      named_bar_sync(1, 128);
+      named_bar_sync(bar_id, 128);
       if (tma_row && ncols > 0) {
         uint8_t* rowp = sb + lrow * 128;
 #pragma unroll
@@ -308,7 +311,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
                          pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
       }
       fence_async_smem();
-      named_bar_sync(1, 128);
+      named_bar_sync(bar_id, 128);
       if (leader_thread && ncols > 0) {
         const uint64_t pol = l2_policy(p.hint_out);
         for (int k = 0; k < td.store_count; ++k) {
@@ -318,6 +321,133 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         }
         bulk_commit();
       }
+    }
+  }
+}
+
+// Epilogue variant for the single (non-double-buffered) 512-column accumulator: a warp reads its
+// NCH chunks out of TMEM first — bias, y_base, IA3 applied, bf16 values held in registers —
+// and releases the accumulator before any staging / TMA store, so the next tile's MMAs start
+// after the TMEM reads instead of after the stores. Same values and stores as epilogue_tile.
+template <int NCH>
+__device__ __forceinline__ void epilogue_tile_hold(const GemmParams& p, uint32_t tmem_acc, uint32_t ew,
+                                                   uint32_t lane, const TileDesc& td, int store_row0, int n0,
+                                                   uint64_t* tfull, uint32_t tfull_ph, uint8_t* stage,
+                                                   uint32_t tempty_cluster_addr, int c_begin, uint32_t bar_id) {
+  const int r = store_row0 + ew * 32 + lane;
+  const bool row_ok = r < td.rows;
+  const bool leader_thread = ew == 0 && lane == 0;
+  DevSeg sg;
+  int r_local = 0;
+  if (row_ok) {
+    if (td.seg >= 0) {
+      sg = p.segs[td.seg];
+      r_local = td.arow + r;
+    } else {
+      const int xrow = td.arow + r;
+      sg = p.segs[p.row_seg[xrow]];
+      r_local = xrow - sg.xrow0 + sg.xlocal0;
+    }
+  }
+  const bool use_ia3 = row_ok && p.ia3_in_epilogue && (sg.flags & SEGF_IA3);
+  const bool want_base = row_ok && (sg.flags & SEGF_WANT_BASE);
+  const bool tma_row = row_ok && (sg.flags & SEGF_TMA_STORE) && (td.seg >= 0 || sg.xrow0 <= td.arow);
+  const int lrow = ew * 32 + lane;
+  if (leader_thread) {
+    for (int k = 0; k < td.store_count; ++k) tensormap_acquire(p.tmaps + p.stores[td.store_begin + k].x);
+  }
+  mbar_wait(tfull, tfull_ph);
+  tc_fence_after();
+  uint32_t hold[NCH][32];                     // bf16x2 of each held chunk
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    const int c = c_begin + q;
+    uint32_t ra[32], rb[32];
+    tmem_ld_32x32b_x32(tmem_acc + c * EPI_CHUNK + ((ew * 32u) << 16), ra);
+    tmem_ld_32x32b_x32(tmem_acc + c * EPI_CHUNK + 32 + ((ew * 32u) << 16), rb);
+    tmem_wait_ld();
+    if (q == NCH - 1) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_cluster_addr);
+    }
+    const int n = n0 + c * EPI_CHUNK;
+    const int ncols = max(0, min(EPI_CHUNK, p.N - n));
+    float v[64];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      v[j] = __uint_as_float(ra[j]);
+      v[32 + j] = __uint_as_float(rb[j]);
+    }
+    if (row_ok && ncols > 0) {
+      if (p.has_bias) {
+        if (ncols == 64) {
+          const float4* b4 = reinterpret_cast<const float4*>(p.bias + n);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float4 bb = __ldg(b4 + j);
+            v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < ncols) v[j] += __ldg(p.bias + n + j);
+        }
+      }
+      if (want_base) {
+        const bool bf = sg.flags & SEGF_BASE_BF16;
+        char* base = reinterpret_cast<char*>(sg.dst_base) + ((int64_t)r_local * sg.base_ld + n) * (bf ? 2 : 4);
+        store_row_global(v, ncols, base, bf, sg.flags & SEGF_BASE_VEC);
+      }
+      if (use_ia3) {
+        if (ncols == 64) {
+          const float4* l4 = reinterpret_cast<const float4*>(sg.ia3 + n);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float4 ll = __ldg(l4 + j);
+            v[4 * j] *= ll.x; v[4 * j + 1] *= ll.y; v[4 * j + 2] *= ll.z; v[4 * j + 3] *= ll.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < ncols) v[j] *= __ldg(sg.ia3 + n + j);
+        }
+      }
+      if (!tma_row) {
+        const bool bf = sg.flags & SEGF_DST_BF16;
+        char* dst = reinterpret_cast<char*>(sg.dst) + ((int64_t)r_local * sg.dst_ld + n) * (bf ? 2 : 4);
+        store_row_global(v, ncols, dst, bf, sg.flags & SEGF_DST_VEC);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) hold[q][j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+  }
+  if (td.store_count == 0) return;
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    const int c = c_begin + q;
+    const int n = n0 + c * EPI_CHUNK;
+    const int ncols = max(0, min(EPI_CHUNK, p.N - n));
+    uint8_t* sb = stage + (q & 1) * EPI_STAGE_BYTES;
+    if (leader_thread) bulk_wait_read<1>();
+    named_bar_sync(bar_id, 128);
+    if (tma_row && ncols > 0) {
+      uint8_t* rowp = sb + lrow * 128;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<uint4*>(rowp + ((j ^ (lrow & 7)) << 4)) =
+            make_uint4(hold[q][4 * j], hold[q][4 * j + 1], hold[q][4 * j + 2], hold[q][4 * j + 3]);
+    }
+    fence_async_smem();
+    named_bar_sync(bar_id, 128);
+    if (leader_thread && ncols > 0) {
+      const uint64_t pol = l2_policy(p.hint_out);
+      for (int k = 0; k < td.store_count; ++k) {
+        const int2 op = p.stores[td.store_begin + k];
+        if (p.hint_out) tma_store_2d_hint(p.tmaps + op.x, sb, n, op.y + store_row0, pol);
+        else tma_store_2d(p.tmaps + op.x, sb, n, op.y + store_row0);
+      }
+      bulk_commit();
     }
   }
 }
@@ -738,20 +868,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // pair columns g*256 + c*128 .. +128), so each UMMA's N=256 output maps linearly onto TMEM.
 constexpr int BM2 = 256;                        // rows per pair tile
 
+// PN = 512 runs 12 warps: the single 512-column accumulator cannot be double-buffered, so its
+// drain is the bubble between tiles; two groups of 4 epilogue warps (each its own TMEM-lane
+// quarter mapping, chunk half, staging buffers and named barrier) halve it. setmaxnreg moves
+// registers from the producer / MMA warp group to the epilogue groups.
 template <int PN>
 struct PairCfg {
   static constexpr int G = PN / 256;            // 256-column UMMA groups per K step
   static constexpr int NACC = PN == 256 ? 2 : 1;
+  static constexpr int EPI_GROUPS = PN == 256 ? 1 : 2;
+  static constexpr int THREADS = 128 + 128 * EPI_GROUPS;
   static constexpr int B_BYTES = (PN / 2) * BK * 2;   // this CTA's B slice per stage
   static constexpr int STAGE = A_STAGE_BYTES + B_BYTES;
-  static constexpr int STAGES_ = PN == 256 ? 6 : 4;
-  static constexpr int SMEM = STAGES_ * STAGE + EPI_SMEM + 1024 + 256;
+  static constexpr int STAGES_ = PN == 256 ? 6 : 3;
+  static constexpr int SMEM = STAGES_ * STAGE + EPI_GROUPS * EPI_SMEM + 1024 + 256;
 };
 constexpr int GEMM2_SMEM = PairCfg<256>::SMEM;
 constexpr int GEMM2W_SMEM = PairCfg<512>::SMEM;
 
 template <bool kBwd, int PN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<PN>::THREADS, 1)
     seg_gemm2_kernel(const __grid_constant__ CUtensorMap tmB,   // W: fwd box {64,64}; bwd {64,128}
                      const __grid_constant__ CUtensorMap tmAL,  // A_lora [M, R_w], box {64,128}
                      const __grid_constant__ CUtensorMap tmBP,  // pack [R, N], box {64,16}
@@ -765,8 +901,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                                              ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES2 * A_STAGE_BYTES;
-  uint8_t* epi_stage = smem + STAGES2 * Cfg::STAGE;  // 2 x 16 KB TMA-store staging
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_stage + EPI_SMEM);
+  uint8_t* epi_stage = smem + STAGES2 * Cfg::STAGE;  // per epilogue group: 2 x 16 KB staging
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_stage + Cfg::EPI_GROUPS * EPI_SMEM);
   uint64_t* empty_bar = full_bar + STAGES2;
   uint64_t* tfull_bar = empty_bar + STAGES2;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -791,7 +927,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 8);  // leader: 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty_bar[b], 8 * Cfg::EPI_GROUPS);  // leader: epilogue warps x 2 CTAs
     }
     fence_barrier_init();
   }
@@ -808,6 +944,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   const int cluster_id = blockIdx.x >> 1;
   const int num_clusters = gridDim.x >> 1;
 
+  // 384 threads (PN = 512): warp group 0 (producer, MMA issuer, TMEM owner) hands registers
+  // to the two epilogue groups
+  if constexpr (Cfg::EPI_GROUPS == 2) {
+    if (warp < 4) reg_dealloc<56>();   // 128 x 56 + 256 x 224 = 168 x 384
+  }
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
@@ -933,7 +1074,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (both CTAs)
-    const uint32_t ew = warp - 4;
+    if constexpr (Cfg::EPI_GROUPS == 2) reg_alloc<224>();
+    const uint32_t ew = warp & 3;              // TMEM lane quarter (warp % 4)
+    const int grp = (int)(warp - 4) >> 2;      // epilogue group: chunk half for PN = 512
+    constexpr int CPG = PN / EPI_CHUNK / Cfg::EPI_GROUPS;
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
     int acc = 0;
     uint32_t acc_ph = 0;
@@ -941,8 +1085,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       int mb, nb;
       tile_coords(t, p, mb, nb);
       const TileDesc td = p.tiles[mb];
-      epilogue_tile<PN>(p, tmem_base + acc * 256, ew, lane, td, crank * BM, nb * PN, &tfull_bar[acc],
-                        acc_ph, epi_stage, tempty0 + acc * 8);
+      if constexpr (Cfg::EPI_GROUPS == 2)
+        epilogue_tile_hold<CPG>(p, tmem_base + acc * 256, ew, lane, td, crank * BM, nb * PN, &tfull_bar[acc],
+                                acc_ph, epi_stage + grp * EPI_SMEM, tempty0 + acc * 8, grp * CPG, 1 + grp);
+      else
+        epilogue_tile<PN>(p, tmem_base + acc * 256, ew, lane, td, crank * BM, nb * PN, &tfull_bar[acc],
+                          acc_ph, epi_stage, tempty0 + acc * 8);
       if (++acc == NACC) { acc = 0; acc_ph ^= 1; }
     }
     if (ew == 0 && lane == 0) bulk_wait_all();

@@ -146,7 +146,11 @@ struct ss_ctx {
   int direct_tiles = 1;  // 1: TMA-load whole tiles of bf16 segments in place (no gather)
   int force_tbn = 0;     // testing: force the single-CTA tile width (64 / 128 / 256)
   int tma_store = 1;     // 1: bf16 outputs leave through swizzled smem + TMA bulk stores
-  int pair_n = 256;      // CTA-pair tile width: 256 (double-buffered TMEM) or 512
+  // CTA-pair tile width: 256 (double-buffered TMEM) or 512 (one accumulator, 12 warps; 25 %
+  // fewer operand bytes per FLOP: less L2 traffic, less power, higher clock on the power-capped
+  // part: 13B step 784-789 -> 767-770 ms); 0 = 512 when the dispatch has >= 2 waves of 256x512
+  // pair tiles, else 256
+  int pair_n = 0;
   int shrink_kb_chunk = SHRINK_KB_CHUNK;  // K-split of the LoRA shrink (k-blocks of 64 per chunk)
   int shrink_mode = 0;   // 0 auto, 1 one CTA per slab (all chunks), 2 one CTA per (slab, chunk)
   int64_t weight_bytes = 0, adapter_bytes = 0;
@@ -768,7 +772,9 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   B.off_tm = off_tm; B.off_seg = off_seg; B.off_tile = off_tile; B.off_piece = off_piece;
   B.off_ch = off_ch; B.off_st = off_st; B.off_it = off_it;
   B.M = M; B.MX = MX; B.lora_ld = lora_ld; B.al_rows = al_rows; B.ldx = ldx;
-  B.any_lora = any_lora; B.pair = pair; B.tbn = tbn; B.pn = ctx->pair_n;
+  B.any_lora = any_lora; B.pair = pair; B.tbn = tbn;
+  B.pn = ctx->pair_n ? ctx->pair_n
+                     : (((M + BM2 - 1) / BM2) * ((N + 511) / 512) >= (int64_t)ctx->num_sms ? 512 : 256);
   B.num_m = num_m; B.n_piece = (int)piece_seg.size(); B.n_items = (int)items.size();
   if (any_lora) {
     for (const ShrinkItem& it : items) B.part_ld = std::max(B.part_ld, ds[it.seg].rank_pad);
@@ -972,9 +978,9 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
       CK(launch_k(ctx, seg_gemm_stream_kernel<false>, grid, GEMM_THREADS, STREAM_SMEM, stream, L.tm_w_fwd_s, tmAL, tmBP, gpm));
   } else if (pair && pn == 512) {
     if (bwd)
-      CK(launch_k(ctx, seg_gemm2_kernel<true, 512>, grid, GEMM_THREADS, GEMM2W_SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, gpm));
+      CK(launch_k(ctx, seg_gemm2_kernel<true, 512>, grid, PairCfg<512>::THREADS, GEMM2W_SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, gpm));
     else
-      CK(launch_k(ctx, seg_gemm2_kernel<false, 512>, grid, GEMM_THREADS, GEMM2W_SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
+      CK(launch_k(ctx, seg_gemm2_kernel<false, 512>, grid, PairCfg<512>::THREADS, GEMM2W_SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
   } else if (pair) {
     if (bwd)
       CK(launch_k(ctx, seg_gemm2_kernel<true, 256>, grid, GEMM_THREADS, GEMM2_SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, gpm));
@@ -1189,7 +1195,8 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
     return SS_OK;
   }
   if (!strcmp(key, "pair_n")) {
-    if (value != 256 && value != 512) return fail(ctx, SS_E_ARG, "pair_n must be 256 or 512");
+    if (value != 0 && value != 256 && value != 512)
+      return fail(ctx, SS_E_ARG, "pair_n must be 0 (auto), 256 or 512");
     ctx->pair_n = (int)value;
     return SS_OK;
   }
