@@ -329,7 +329,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
 // NCH chunks out of TMEM first — bias, y_base, IA3 applied, bf16 values held in registers —
 // and releases the accumulator before any staging / TMA store, so the next tile's MMAs start
 // after the TMEM reads instead of after the stores. Same values and stores as epilogue_tile.
-template <int NCH>
+template <int NCH, int BUFS>
 __device__ __forceinline__ void epilogue_tile_hold(const GemmParams& p, uint32_t tmem_acc, uint32_t ew,
                                                    uint32_t lane, const TileDesc& td, int store_row0, int n0,
                                                    uint64_t* tfull, uint32_t tfull_ph, uint8_t* stage,
@@ -428,8 +428,8 @@ __device__ __forceinline__ void epilogue_tile_hold(const GemmParams& p, uint32_t
     const int c = c_begin + q;
     const int n = n0 + c * EPI_CHUNK;
     const int ncols = max(0, min(EPI_CHUNK, p.N - n));
-    uint8_t* sb = stage + (q & 1) * EPI_STAGE_BYTES;
-    if (leader_thread) bulk_wait_read<1>();
+    uint8_t* sb = stage + (q % BUFS) * EPI_STAGE_BYTES;
+    if (leader_thread) bulk_wait_read<BUFS - 1>();   // the store that last used `sb` has read it
     named_bar_sync(bar_id, 128);
     if (tma_row && ncols > 0) {
       uint8_t* rowp = sb + lrow * 128;
@@ -880,8 +880,14 @@ struct PairCfg {
   static constexpr int THREADS = 128 + 128 * EPI_GROUPS;
   static constexpr int B_BYTES = (PN / 2) * BK * 2;   // this CTA's B slice per stage
   static constexpr int STAGE = A_STAGE_BYTES + B_BYTES;
-  static constexpr int STAGES_ = PN == 256 ? 6 : 3;
-  static constexpr int SMEM = STAGES_ * STAGE + EPI_GROUPS * EPI_SMEM + 1024 + 256;
+#ifndef SS_PAIR512_STAGES
+#define SS_PAIR512_STAGES 3
+#endif
+  static constexpr int STAGES_ = PN == 256 ? 6 : SS_PAIR512_STAGES;
+  // 512: 3 stages + 2 x 16 KB staging per epilogue group, or 4 stages + one 16 KB buffer each
+  static constexpr int EPI_BUFS = (PN == 512 && STAGES_ > 3) ? 1 : 2;
+  static constexpr int EPI_GROUP_BYTES = EPI_BUFS * EPI_STAGE_BYTES;
+  static constexpr int SMEM = STAGES_ * STAGE + EPI_GROUPS * EPI_GROUP_BYTES + 1024 + 256;
 };
 constexpr int GEMM2_SMEM = PairCfg<256>::SMEM;
 constexpr int GEMM2W_SMEM = PairCfg<512>::SMEM;
@@ -902,7 +908,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<PN>::THREADS
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES2 * A_STAGE_BYTES;
   uint8_t* epi_stage = smem + STAGES2 * Cfg::STAGE;  // per epilogue group: 2 x 16 KB staging
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_stage + Cfg::EPI_GROUPS * EPI_SMEM);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_stage + Cfg::EPI_GROUPS * Cfg::EPI_GROUP_BYTES);
   uint64_t* empty_bar = full_bar + STAGES2;
   uint64_t* tfull_bar = empty_bar + STAGES2;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -1086,8 +1092,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<PN>::THREADS
       tile_coords(t, p, mb, nb);
       const TileDesc td = p.tiles[mb];
       if constexpr (Cfg::EPI_GROUPS == 2)
-        epilogue_tile_hold<CPG>(p, tmem_base + acc * 256, ew, lane, td, crank * BM, nb * PN, &tfull_bar[acc],
-                                acc_ph, epi_stage + grp * EPI_SMEM, tempty0 + acc * 8, grp * CPG, 1 + grp);
+        epilogue_tile_hold<CPG, Cfg::EPI_BUFS>(p, tmem_base + acc * 256, ew, lane, td, crank * BM, nb * PN,
+                                               &tfull_bar[acc], acc_ph, epi_stage + grp * Cfg::EPI_GROUP_BYTES,
+                                               tempty0 + acc * 8, grp * CPG, 1 + grp);
       else
         epilogue_tile<PN>(p, tmem_base + acc * 256, ew, lane, td, crank * BM, nb * PN, &tfull_bar[acc],
                           acc_ph, epi_stage, tempty0 + acc * 8);
