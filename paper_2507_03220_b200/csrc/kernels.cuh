@@ -356,6 +356,18 @@ __device__ __forceinline__ void epilogue_tile_hold(const GemmParams& p, uint32_t
   if (leader_thread) {
     for (int k = 0; k < td.store_count; ++k) tensormap_acquire(p.tmaps + p.stores[td.store_begin + k].x);
   }
+  // pull this group's bias / IA3 columns into L1 while the MMAs run, so the drain below (the
+  // bubble before the next tile's MMAs) does not wait on L2 for them
+#ifndef SS_NO_EPI_PF
+  {
+    const int nb0 = n0 + c_begin * EPI_CHUNK;
+    const int span = min(NCH * EPI_CHUNK, p.N - nb0);      // columns of this group
+    if (span > 0 && lane < (span + 31) / 32) {
+      if (p.has_bias) prefetch_l1(p.bias + nb0 + lane * 32);
+      if (use_ia3) prefetch_l1(sg.ia3 + nb0 + lane * 32);
+    }
+  }
+#endif
   mbar_wait(tfull, tfull_ph);
   tc_fence_after();
   uint32_t hold[NCH][32];                     // bf16x2 of each held chunk

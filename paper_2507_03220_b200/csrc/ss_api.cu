@@ -1057,7 +1057,7 @@ int set_kernel_attrs(ss_ctx* ctx) {
 extern "C" {
 
 const char* ss_version(void) {
-  return "ss_b200 1.0 (sm_100a tcgen05/TMEM/TMA segmented executor; CTA-pair 256x256x64 / single-CTA 128x256x64)";
+  return "ss_b200 1.0 (sm_100a tcgen05/TMEM/TMA segmented executor; CTA-pair 256x512 / 256x256, single-CTA 128x{256,128,64}, weight-streaming 128x64)";
 }
 
 const char* ss_last_error(const ss_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
