@@ -129,8 +129,11 @@ SS_API int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int
  * sub-batches; the H2D copy of sub-batch j+1, the kernels of j and the D2H copy of j-1 overlap
  * on the library's copy streams and a 4-slot device staging ring. Rows are independent and the
  * kernels never mix rows (tensor_ops.py:1-8), so the results are bitwise those of
- * ss_compute_batch on device copies. Synchronous: the replies are in the host buffers when it
- * returns. All segments must share one src dtype and one dst dtype. */
+ * ss_compute_batch on device copies. A dispatch of at most `zero_copy_bytes` payload bytes
+ * (option, default 4 MiB: decode-size batches) over page-locked buffers makes no copies: the
+ * kernels read the request rows and write the reply rows in host memory directly (UVA), one
+ * launch sequence instead of two memcpy calls per segment. Synchronous: the replies are in the
+ * host buffers when it returns. All segments must share one src dtype and one dst dtype. */
 SS_API int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
                                  const ss_seg* segs, void* stream, int32_t* seg_status);
 
@@ -247,6 +250,7 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   prefetch_mb, prefetch_rows, prefetch_hint, pf_depth (0, 256, 2, 0)  L2 prefetch of the next
  *                       layer / of the launch's own W for small dispatches (measured slower: off)
  *   pdl (0)             programmatic dependent launch between a dispatch's kernels (no gain measured)
+ *   zero_copy_bytes (4 MiB)  ss_compute_batch_host dispatches up to this size: no copies (UVA)
  *   force_remote (0)    testing: route every segment as if it lived on a peer GPU
  *   pipeline_rows, pipeline_bytes  sub-batch size of ss_compute_batch_host */
 SS_API int ss_set_option(ss_ctx* ctx, const char* key, int64_t value);

@@ -1553,4 +1553,33 @@ __global__ void copy_to_f32_kernel(const void* __restrict__ src, int src_bf16,
                       : reinterpret_cast<const float*>(src)[i];
 }
 
+// Row copies device staging -> (pinned host) destination rows, one warp per row, 16-byte
+// vectors: the reply leg of a zero-copy host dispatch (coalesced PCIe writes, one launch
+// instead of one D2H memcpy per segment).
+struct RowCopy {
+  const char* src;     // first row (device)
+  char* dst;           // first row (host, UVA)
+  int64_t src_ld, dst_ld;  // bytes
+  int32_t rows, row_bytes; // row_bytes % 16 == 0 when vec
+};
+
+__global__ void __launch_bounds__(256) copy_rows_kernel(const RowCopy* __restrict__ ops, int n_ops,
+                                                        int total_rows) {
+  const int lane = threadIdx.x & 31;
+  for (int w = blockIdx.x * 8 + (threadIdx.x >> 5); w < total_rows; w += gridDim.x * 8) {
+    int o = 0, r = w;
+    while (o < n_ops - 1 && r >= ops[o].rows) { r -= ops[o].rows; ++o; }
+    const RowCopy& op = ops[o];
+    const char* s = op.src + r * op.src_ld;
+    char* d = op.dst + r * op.dst_ld;
+    const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | op.row_bytes) & 15) == 0;
+    if (vec) {
+      for (int i = lane; i < op.row_bytes / 16; i += 32)
+        reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(s)[i];
+    } else {
+      for (int i = lane; i < op.row_bytes; i += 32) d[i] = s[i];
+    }
+  }
+}
+
 }  // namespace ss

@@ -124,6 +124,7 @@ struct ss_ctx {
   size_t ha_in_cap = 0, ha_out_cap = 0, ha_base_cap = 0;
   std::vector<cudaEvent_t> chunk_ev;
   uint64_t peers_enabled = 0;  // peer GPUs whose memory this context's kernels may touch
+  int64_t zero_copy_bytes = 4 << 20;  // host dispatches up to this many payload bytes: zero-copy
   int force_remote = 0;      // testing: route every segment as if it lived on a peer GPU
   int pdl = 0;               // programmatic dependent launch between a dispatch's kernels (measured: no gain)
   int stream_gemm = 1;       // weight-streaming kernel for those dispatches (K % 64 == 0)
@@ -352,6 +353,9 @@ bool is_remote(ss_ctx* ctx, const void* p) {
     cudaGetLastError();
     return false;
   }
+  // pinned host memory (UVA-mapped): the kernels read / write it over PCIe with plain loads and
+  // stores (the zero-copy path of small host dispatches)
+  if (a.type == cudaMemoryTypeHost) return true;
   if (a.type != cudaMemoryTypeDevice || a.device == ctx->device) return false;
   if (a.device >= 0 && a.device < 64 && !(ctx->peers_enabled >> a.device & 1)) {
     // first segment from this peer: map its memory into this GPU's address space (NVLink)
@@ -460,8 +464,10 @@ struct Built {
   uint64_t ws_epoch = 0, ad_epoch = 0;
 };
 
+// `local_buffers`: every pointer is a staging slice this context allocated on its own device
+// (host pipelines), so the per-pointer peer-GPU query is skipped.
 int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
-                int32_t* seg_status, Built& B) {
+                int32_t* seg_status, Built& B, bool local_buffers = false) {
   if (pass_kind < 0 || pass_kind > 2) return fail(ctx, SS_E_ARG, "unknown pass %d", pass_kind);
   if (n_seg < 0 || (n_seg > 0 && (!segs || !seg_status)))
     return fail(ctx, SS_E_ARG, "bad segment array");
@@ -504,8 +510,10 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     if (s.flags & SS_SEGF_DST_BF16) f |= SEGF_DST_BF16;
     if (aligned16(s.src, s.src_ld, (s.flags & SS_SEGF_SRC_BF16) ? 2 : 4)) f |= SEGF_SRC_VEC;
     if (aligned16(s.dst, s.dst_ld, (s.flags & SS_SEGF_DST_BF16) ? 2 : 4)) f |= SEGF_DST_VEC;
-    if (is_remote(ctx, s.src)) f |= SEGF_REMOTE_SRC;
-    if (is_remote(ctx, s.dst) || (s.dst_base && is_remote(ctx, s.dst_base))) f |= SEGF_REMOTE_DST;
+    if (!local_buffers || ctx->force_remote) {
+      if (is_remote(ctx, s.src)) f |= SEGF_REMOTE_SRC;
+      if (is_remote(ctx, s.dst) || (s.dst_base && is_remote(ctx, s.dst_base))) f |= SEGF_REMOTE_DST;
+    }
     // NOISE with the adapter flag = the noise effect of the ADAPTED layer, (n.W + s n.A.B) * l
     // (bias-free): what a client with an executor-fused adapter subtracts to unblind its reply
     if (s.flags & SS_SEGF_ADAPTER) {
@@ -1232,6 +1240,11 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
     ctx->l2_budget_mb = (int)value;
     return SS_OK;
   }
+  if (!strcmp(key, "zero_copy_bytes")) {
+    if (value < 0) return fail(ctx, SS_E_ARG, "zero_copy_bytes must be >= 0");
+    ctx->zero_copy_bytes = value;
+    return SS_OK;
+  }
   if (!strcmp(key, "force_remote")) {
     ctx->force_remote = value ? 1 : 0;
     return SS_OK;
@@ -1859,7 +1872,7 @@ int host_dispatch_aliased(ss_ctx* ctx, int pass_kind, int block, int role, const
     }
     cst.assign(cs.size(), 0);
     Built b;
-    if ((rc = build_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), cst.data(), b))) return rc;
+    if ((rc = build_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), cst.data(), b, true))) return rc;
     for (size_t q = 0; q < cs.size(); ++q)
       if (cst[q] != SS_SEG_OK) seg_status[chunks[k][q].seg] = cst[q];
     Staging* stp = nullptr;
@@ -1934,6 +1947,91 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
       any_base = true;
       esz_base = (s.flags & SS_SEGF_BASE_BF16) ? 2 : 4;
     }
+  }
+
+  // ---- small dispatches (decode: a few rows per client): no copies at all. The kernels read the
+  // request rows from pinned host memory (gather, UVA) and the epilogue stores the reply rows
+  // straight into it: one launch sequence and one synchronisation instead of two memcpy calls
+  // per segment, whose API cost dominates a dispatch of tens of two-row segments.
+  bool zero_copy = (double)rows_total * (K * esz_in + N * esz_out) <= (double)ctx->zero_copy_bytes;
+  for (size_t q = 0; zero_copy && q < good.size(); ++q) {
+    // only pinned (UVA-mapped) or device memory can be touched by the kernels directly
+    const ss_seg& sg = segs[good[q]];
+    for (const void* ptr : {sg.src, static_cast<const void*>(sg.dst), static_cast<const void*>(sg.dst_base)}) {
+      if (!ptr) continue;
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess ||
+          (a.type != cudaMemoryTypeHost && a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)) {
+        cudaGetLastError();
+        zero_copy = false;
+        break;
+      }
+    }
+  }
+  if (zero_copy) {
+    // request rows are gathered from host memory by the kernels (UVA); replies land in a device
+    // slot and one row-copy kernel writes them to the host rows (coalesced), so the dispatch
+    // makes no memcpy calls at all
+    auto& hs = ctx->hslot[0];
+    const size_t out_need = (size_t)rows_total * N * esz_out, base_need = any_base ? (size_t)rows_total * N * esz_base : 0;
+    if (hs.used) CK(cudaEventSynchronize(hs.ev_out));
+    int rc = SS_OK;
+    if (hs.out_cap < out_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.out), hs.out_cap, out_need, false))) return rc;
+    if (hs.base_cap < base_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.base), hs.base_cap, base_need, false))) return rc;
+    std::vector<ss_seg> cs;
+    std::vector<RowCopy> ops;
+    std::vector<int> op_seg;    // index into cs of each row copy
+    int64_t pos = 0;
+    for (int i : good) {
+      ss_seg d = segs[i];
+      d.dst = static_cast<char*>(hs.out) + pos * N * esz_out;
+      d.dst_ld = N;
+      ops.push_back(RowCopy{static_cast<const char*>(d.dst), static_cast<char*>(segs[i].dst), (int64_t)N * (int64_t)esz_out,
+                            segs[i].dst_ld * (int64_t)esz_out, (int32_t)segs[i].rows, (int32_t)(N * esz_out)});
+      op_seg.push_back((int)cs.size());
+      if (segs[i].dst_base && pass_kind != SS_PASS_BACKWARD) {
+        d.dst_base = static_cast<char*>(hs.base) + pos * N * esz_base;
+        d.base_ld = N;
+        ops.push_back(RowCopy{static_cast<const char*>(d.dst_base), static_cast<char*>(segs[i].dst_base),
+                              (int64_t)N * (int64_t)esz_base, segs[i].base_ld * (int64_t)esz_base,
+                              (int32_t)segs[i].rows, (int32_t)(N * esz_base)});
+        op_seg.push_back((int)cs.size());
+      }
+      cs.push_back(d);
+      pos += segs[i].rows;
+    }
+    std::vector<int32_t> cst(cs.size(), 0);
+    Built b;
+    if ((rc = build_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), cst.data(), b))) return rc;
+    for (size_t q = 0; q < cs.size(); ++q)
+      if (cst[q] != SS_SEG_OK) seg_status[good[q]] = cst[q];
+    if (b.M == 0) return SS_OK;
+    {
+      // rejected segments are not written: drop their row copies (their slot rows are stale)
+      size_t k = 0;
+      for (size_t o = 0; o < ops.size(); ++o)
+        if (cst[op_seg[o]] == SS_SEG_OK && ops[o].rows > 0) ops[k++] = ops[o];
+      ops.resize(k);
+    }
+    if (ops.empty()) return SS_OK;
+    const size_t ops_off = round_up((int64_t)b.blob.size(), 256);
+    Staging* stp = nullptr;
+    if ((rc = acquire_staging(ctx, ops_off + ops.size() * sizeof(RowCopy), stp))) return rc;
+    memcpy(stp->host, b.blob.data(), b.blob.size());
+    memcpy(static_cast<char*>(stp->host) + ops_off, ops.data(), ops.size() * sizeof(RowCopy));
+    CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
+    CK(cudaMemcpyAsync(stp->dev, stp->host, ops_off + ops.size() * sizeof(RowCopy), cudaMemcpyHostToDevice, stream));
+    if ((rc = launch_batch(ctx, b, static_cast<char*>(stp->dev), stream))) return rc;
+    int64_t copy_rows = 0;
+    for (const RowCopy& o : ops) copy_rows += o.rows;
+    copy_rows_kernel<<<(int)std::min<int64_t>((copy_rows + 7) / 8, (int64_t)ctx->num_sms * 8), 256, 0, stream>>>(
+        reinterpret_cast<const RowCopy*>(static_cast<char*>(stp->dev) + ops_off), (int)ops.size(), (int)copy_rows);
+    CK(cudaGetLastError());
+    ctx->launches++;
+    CK(cudaEventRecord(stp->done, stream));
+    stp->pending = true;
+    CK(cudaStreamSynchronize(stream));   // replies are in the caller's host buffers on return
+    return SS_OK;
   }
 
   // ---- sub-batches of whole rows: the H2D of j+1, the kernels of j and the D2H of j-1 overlap
@@ -2069,7 +2167,7 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     // sub-batches' payload copies in the host-to-device engine)
     cst.assign(cs.size(), 0);
     Built b;
-    if ((rc = build_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), cst.data(), b))) return rc;
+    if ((rc = build_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), cst.data(), b, true))) return rc;
     for (size_t k = 0; k < cs.size(); ++k)
       if (cst[k] != SS_SEG_OK) seg_status[ch[k].seg] = cst[k];
     Staging* stp = nullptr;

@@ -24,6 +24,7 @@ from __future__ import annotations
 import csv
 import threading
 import time
+import weakref
 from collections import defaultdict, deque
 from dataclasses import dataclass, field
 
@@ -136,6 +137,25 @@ def _out_dtype(payload) -> torch.dtype:
     return torch.float32
 
 
+def _host_tensor_info(t: torch.Tensor):
+    """(dtype, shape) of a contiguous pinned-host bf16/f32 tensor, else None. Cached per tensor
+    object by the executor (a tensor's placement, dtype and shape do not change)."""
+    if t.is_cuda or t.dtype not in (torch.bfloat16, torch.float32) or not t.is_contiguous() or not t.is_pinned():
+        return None
+    return (t.dtype, tuple(t.shape))
+
+
+def _cached_info(cache: dict, t: torch.Tensor):
+    hit = cache.get(id(t))
+    if hit is not None and hit[0]() is t:
+        return hit[1]
+    if len(cache) > 4096:
+        cache.clear()
+    v = _host_tensor_info(t)
+    cache[id(t)] = (weakref.ref(t), v)
+    return v
+
+
 class GpuBaseExecutor:
     """Stateless layer server: one scheduler thread, compute on the B200 via libss_b200."""
 
@@ -169,6 +189,9 @@ class GpuBaseExecutor:
         self.metrics = ExecutorMetrics()
         self.ledger = ledger_mod.MemoryLedger("executor")
         self._pinned: dict[str, torch.Tensor] = {}
+        # pinned-host checks of client payload / reply tensors, per live tensor object:
+        # id -> (weakref, info) (tensors compare elementwise, so they cannot be dict keys)
+        self._host_info: dict[int, tuple] = {}
         self._dev_staging: dict = {}
         self._host_replies: list = []
         self.last_event: torch.cuda.Event | None = None
@@ -416,14 +439,15 @@ class GpuBaseExecutor:
     def _all_pinned_host(self, envelopes, good, out_w) -> bool:
         if self.save_activations:
             return False
+        info = self._host_info
         for i in good:
             e = envelopes[i]
             p, r = e.payload, getattr(e, "reply_to", None)
-            if not (isinstance(p, torch.Tensor) and not p.is_cuda and p.is_pinned() and p.is_contiguous()
-                    and isinstance(r, torch.Tensor) and not r.is_cuda and r.is_pinned() and r.is_contiguous()
-                    and p.dtype == r.dtype and p.dtype in (torch.bfloat16, torch.float32)
-                    and tuple(r.shape) == (e.token_count, out_w)
-                    and getattr(e, "base_to", None) is None):
+            if not isinstance(p, torch.Tensor) or not isinstance(r, torch.Tensor) or \
+                    getattr(e, "base_to", None) is not None:
+                return False
+            ip, ir = _cached_info(info, p), _cached_info(info, r)
+            if not ip or not ir or ip[0] != ir[0] or ir[1] != (e.token_count, out_w):
                 return False
         return True
 

@@ -414,12 +414,15 @@ def test_submit_rejections_match_reference_messages():
     assert got[2].pass_kind == PASS_ERROR and "unknown layer" in error_message(got[2])
 
 
-def test_pipelined_host_dispatch_bitwise_equals_device_dispatch():
-    """Pinned-host clients take the pipelined path (row sub-batches, H2D/GEMM/D2H overlapped);
-    the result must be bitwise the device-resident single-batch result."""
+@pytest.mark.parametrize("zero_copy", [0, 1 << 30])
+def test_pipelined_host_dispatch_bitwise_equals_device_dispatch(zero_copy):
+    """Pinned-host clients take the pipelined path (row sub-batches, H2D/GEMM/D2H overlapped)
+    or, for small dispatches, the zero-copy path (kernels read / write the pinned host rows
+    directly); either result must be bitwise the device-resident single-batch result."""
     d_in, d_out = 512, 768
     w, b = O.layer_params(6, 0, O.V, d_in, d_out)
     ex = _ex({(0, O.V): (w, b)})
+    ex.ctx.set_option("zero_copy_bytes", zero_copy)
     ex.pipeline_rows = 200   # force several sub-batches and ring reuse
     specs, counts = _mixed_clients(ex, d_in, d_out, seed=9, role=O.V)
     for pass_kind, (wi, wo) in ((0, (d_in, d_out)), (1, (d_out, d_in))):
@@ -699,7 +702,8 @@ def test_in_place_device_handoff_bitwise(dims):
             assert torch.equal(got[c], ref[c]), (pass_kind, c)
 
 
-def test_in_place_host_handoff_bitwise():
+@pytest.mark.parametrize("zero_copy", [0, 1 << 30])
+def test_in_place_host_handoff_bitwise(zero_copy):
     """Pinned-host clients whose reply buffer IS the request buffer (the reference's in-place
     hand-off) through the pipelined host path: a sub-batch's reply must never land on request
     rows a later sub-batch has not uploaded yet."""
@@ -707,6 +711,7 @@ def test_in_place_host_handoff_bitwise():
     w, b = O.layer_params(20, 0, O.V, d_in, d_out)
     ex = _ex({(0, O.V): (w, b)})
     ex.pipeline_rows = 128   # many sub-batches
+    ex.ctx.set_option("zero_copy_bytes", zero_copy)
     _mixed_clients(ex, d_in, d_out, seed=20, role=O.V)
     counts = [900, 1, 700, 130, 5, 1024, 77]
     for pass_kind, (wi, wo) in ((0, (d_in, d_out)), (1, (d_out, d_in))):
