@@ -524,7 +524,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=1)
+    ap.add_argument("--cpu-tokens", type=int, default=8,
+                    help="tokens per client in each CPU-reference sample (~5 s of host work at 8)")
     ap.add_argument("--graph", type=int, default=1,
                     help="1: replay the step's prebuilt dispatch plans as one CUDA graph (the kernel "
                          "roofline is still measured on an eager, event-bracketed pass)")
