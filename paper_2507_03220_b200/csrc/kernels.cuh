@@ -1123,6 +1123,227 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<PN>::THREADS
   }
 }
 
+// ============================================================================ K1/K2/K5, 2 pairs
+// Cluster of 4 = two CTA pairs on the same N tile and consecutive M tiles: each pair keeps
+// 256 x 256 tiles with double-buffered accumulators (epilogue overlaps the MMAs), while the
+// pair's B columns are fetched once for both pairs — CTA (pair q, rank c) loads the 64-column
+// half q of rank c's 128 columns and multicasts it to ranks c and 2 + c. L2 -> SM bytes per
+// FLOP fall by 25 % (as with 256 x 512 tiles) without the single-accumulator drain bubble.
+// A stage is refilled only after BOTH pairs' MMAs released it (empty barriers count 2 commits).
+// The pairs walk the same stage ring in lockstep: LoRA K-extension stages are padded to the
+// larger chunk count of the two M tiles. A missing second M tile runs as a dummy (no stores).
+constexpr int GEMM4_STAGES = 6;
+constexpr int GEMM4_STAGE = A_STAGE_BYTES + 128 * BK * 2;
+constexpr int GEMM4_SMEM = GEMM4_STAGES * GEMM4_STAGE + EPI_SMEM + 1024 + 256;
+
+template <bool kBwd>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    seg_gemm4_kernel(const __grid_constant__ CUtensorMap tmB,   // W: fwd box {64,64}; bwd {64,64}
+                     const __grid_constant__ CUtensorMap tmAL,  // A_lora [M, R_w], box {64,128}
+                     const __grid_constant__ CUtensorMap tmBP,  // pack [R, N], box {64,16}
+                     const GemmParams p) {
+  constexpr int STAGES2 = GEMM4_STAGES;
+  constexpr int B_BYTES = 128 * BK * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES2 * A_STAGE_BYTES;
+  uint8_t* epi_stage = smem + STAGES2 * GEMM4_STAGE;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_stage + EPI_SMEM);
+  uint64_t* empty_bar = full_bar + STAGES2;
+  uint64_t* tfull_bar = empty_bar + STAGES2;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = rank & 1;           // rank within the pair
+  const uint32_t pq = rank >> 1;             // pair within the cluster
+  const bool leader = crank == 0;
+  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pq));
+  const uint16_t bmc_mask = (uint16_t)((1u << crank) | (1u << (2 + crank)));
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmB);
+    if (p.any_lora) {
+      tma_prefetch_desc(&tmAL);
+      tma_prefetch_desc(&tmBP);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full_bar[s], 1);    // pair leader: one arrive.expect_tx per stage
+      mbar_init(&empty_bar[s], 2);   // one commit from each pair's MMA issuer
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 8);  // pair leader: 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  const int num_m2 = (p.num_m_tiles + 1) >> 1;             // M-tile pairs
+  const int num_tiles = num_m2 * p.num_n_tiles;
+  const int nkb = (p.K + BK - 1) / BK;
+  const int cluster_id = blockIdx.x >> 2;
+  const int num_clusters = gridDim.x >> 2;
+  GemmParams q2 = p;
+  q2.num_m_tiles = num_m2;                                 // raster over M-tile pairs
+
+  // this pair's tile of super-tile (mb2, nb); a missing second M tile is a dummy (rows = 0)
+  auto pair_tile = [&](int mb2, TileDesc& td, int& mb, int& lora_stages) {
+    mb = 2 * mb2 + (int)pq;
+    const bool real = mb < p.num_m_tiles;
+    td = p.tiles[real ? mb : 2 * mb2];
+    if (!real) {
+      td.rows = 0;
+      td.chunk_count = 0;
+      td.store_count = 0;
+    }
+    int cc = td.chunk_count;
+    if (2 * mb2 + 1 - (int)pq < p.num_m_tiles) cc = max(cc, p.tiles[2 * mb2 + 1 - (int)pq].chunk_count);
+    lora_stages = p.any_lora ? (cc + 3) / 4 : 0;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t fullL = mapa_shared(smem_u32(full_bar), 2 * pq);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        int mb2, nb, mb, nls;
+        tile_coords(t, q2, mb2, nb);
+        TileDesc td;
+        pair_tile(mb2, td, mb, nls);
+        const CUtensorMap* tmA = p.tmaps + td.amap;
+        const int arow = td.arow + crank * BM;
+        tensormap_acquire(tmA);
+        const int m0 = mb * BM2 + crank * BM;
+        const int nh = nb * 256 + crank * 128;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          const uint32_t fb = fullL + s * 8;
+          if (leader) mbar_expect_tx(&full_bar[s], 2 * GEMM4_STAGE);
+          tma_load_2d_2sm(smA + s * A_STAGE_BYTES, tmA, fb, kb * BK, arow);
+          uint8_t* b = smB + s * B_BYTES;
+          if (kBwd)
+            tma_load_2d_2sm_mc(b + pq * (64 * 128), &tmB, &full_bar[s], bmc_mask, kb * BK, nh + 64 * pq);
+          else
+            tma_load_2d_2sm_mc(b + pq * (BK * 128), &tmB, &full_bar[s], bmc_mask, nh + 64 * pq, kb * BK);
+          if (++s == STAGES2) { s = 0; ph ^= 1; }
+        }
+        const int cb = td.chunk_begin;
+        const int cc = td.chunk_count;
+        for (int ls = 0; ls < nls; ++ls) {
+          const int nq = max(0, min(4, cc - ls * 4));
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          const uint32_t fb = fullL + s * 8;
+          if (nq > 0) {
+            if (leader) mbar_expect_tx(&full_bar[s], 2 * (A_STAGE_BYTES + nq * 2 * LORA_CHUNK_BYTES));
+            tma_load_2d_2sm(smA + s * A_STAGE_BYTES, &tmAL, fb, ls * BK, m0);
+            uint8_t* b = smB + s * B_BYTES;
+            for (int qq = 0; qq < nq; ++qq) {
+              const int prow = p.chunks[cb + ls * 4 + qq];
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                tma_load_2d_2sm(b + j * (BK * 128) + qq * LORA_CHUNK_BYTES, &tmBP, fb, nh + 64 * j, prow);
+            }
+          } else if (leader) {
+            mbar_expect_tx(&full_bar[s], 0);       // padding stage (the other pair has more chunks)
+          }
+          if (++s == STAGES2) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc_base = make_idesc_bf16(BM2, 256, false, !kBwd);
+      constexpr uint32_t idesc_lora = make_idesc_bf16(BM2, 256, false, true);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        int mb2, nb, mb, nls;
+        tile_coords(t, q2, mb2, nb);
+        TileDesc td;
+        pair_tile(mb2, td, mb, nls);
+        mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(smA + s * A_STAGE_BYTES);
+            const uint32_t b_addr = smem_u32(smB + s * B_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / UK; ++k) {
+              const uint64_t ad = make_sdesc_sw128(a_addr + k * 32, 16, 1024);
+              const uint64_t bd = kBwd ? make_sdesc_sw128(b_addr + k * 32, 16, 1024)
+                                       : make_sdesc_sw128(b_addr + k * (UK * 128), BK * 128, 1024);
+              mma_bf16_ss_2sm(d_tmem, ad, bd, idesc_base, (kb | k) != 0);
+            }
+            mma_commit_2sm_mc(&empty_bar[s], 0xF);
+          }
+          __syncwarp();
+          if (++s == STAGES2) { s = 0; ph ^= 1; }
+        }
+        const int cc = td.chunk_count;
+        for (int ls = 0; ls < nls; ++ls) {
+          const int nq = max(0, min(4, cc - ls * 4));
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(smA + s * A_STAGE_BYTES);
+            const uint32_t b_addr = smem_u32(smB + s * B_BYTES);
+            for (int qq = 0; qq < nq; ++qq)
+              mma_bf16_ss_2sm(d_tmem, make_sdesc_sw128(a_addr + qq * 32, 16, 1024),
+                              make_sdesc_sw128(b_addr + qq * LORA_CHUNK_BYTES, BK * 128, 1024), idesc_lora, 1u);
+            mma_commit_2sm_mc(&empty_bar[s], 0xF);
+          }
+          __syncwarp();
+          if (++s == STAGES2) { s = 0; ph ^= 1; }
+        }
+        if (lane == 0) mma_commit_2sm_mc(&tfull_bar[acc], pair_mask);
+        __syncwarp();
+        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t ew = warp - 4;
+    const uint32_t temptyL = mapa_shared(smem_u32(tempty_bar), 2 * pq);
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+      int mb2, nb, mb, nls;
+      tile_coords(t, q2, mb2, nb);
+      TileDesc td;
+      pair_tile(mb2, td, mb, nls);
+      epilogue_tile<256>(p, tmem_base + acc * 256, ew, lane, td, crank * BM, nb * 256, &tfull_bar[acc],
+                         acc_ph, epi_stage, temptyL + acc * 8);
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+    if (ew == 0 && lane == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, 512);
+  }
+}
+
 // ============================================================================ K3 shrink
 // One CTA per item = (M-tile, LoRA segment piece of that tile, <= 128 rows):
 //   T[rows, rank_pad] = A_src[rows, K] . P[rank rows, K]^T (tcgen05, M=128, N=rank_pad),

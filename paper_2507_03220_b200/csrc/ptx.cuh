@@ -353,6 +353,18 @@ __device__ __forceinline__ void tma_load_2d_2sm_hint(void* smem_dst, const CUten
       : "memory");
 }
 
+// 2-SM TMA with multicast: the box lands at the same smem offset in every CTA of `cta_mask`,
+// and its bytes complete on the full barrier of each destination CTA pair's leader (the
+// barrier operand is this CTA's barrier address with the pair-peer bit cleared).
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                                   uint16_t cta_mask, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%4, %5}], [%2], %3;\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(cta_mask), "r"(c0), "r"(c1)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* smem_result, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                    smem_u32(smem_result)),

@@ -126,6 +126,7 @@ struct ss_ctx {
   uint64_t peers_enabled = 0;  // peer GPUs whose memory this context's kernels may touch
   int64_t zero_copy_bytes = 4 << 20;  // host dispatches up to this many payload bytes: zero-copy
   int force_remote = 0;      // testing: route every segment as if it lived on a peer GPU
+  int cluster4 = 0;          // 256 x 256 pair tiles as clusters of two pairs sharing B (multicast)
   int pdl = 0;               // programmatic dependent launch between a dispatch's kernels (measured: no gain)
   int stream_gemm = 1;       // weight-streaming kernel for those dispatches (K % 64 == 0)
   int a_rows64 = 1;          // 64-row A box for single-tile dispatches of <= 64 rows
@@ -984,6 +985,12 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
       CK(launch_k(ctx, seg_gemm_stream_kernel<true>, grid, GEMM_THREADS, STREAM_SMEM, stream, L.tm_w_bwd_s, tmAL, tmBP, gpm));
     else
       CK(launch_k(ctx, seg_gemm_stream_kernel<false>, grid, GEMM_THREADS, STREAM_SMEM, stream, L.tm_w_fwd_s, tmAL, tmBP, gpm));
+  } else if (pair && pn == 256 && ctx->cluster4 && num_m >= 2) {
+    const int ng = (int)std::min<int64_t>((int64_t)((num_m + 1) / 2) * gpm.num_n_tiles, ctx->num_sms / 4);
+    if (bwd)
+      CK(launch_k(ctx, seg_gemm4_kernel<true>, 4 * ng, GEMM_THREADS, GEMM4_SMEM, stream, L.tm_w_bwd64, tmAL, tmBP, gpm));
+    else
+      CK(launch_k(ctx, seg_gemm4_kernel<false>, 4 * ng, GEMM_THREADS, GEMM4_SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
   } else if (pair && pn == 512) {
     if (bwd)
       CK(launch_k(ctx, seg_gemm2_kernel<true, 512>, grid, PairCfg<512>::THREADS, GEMM2W_SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, gpm));
@@ -1048,6 +1055,8 @@ int set_kernel_attrs(ss_ctx* ctx) {
                           GEMM2W_SMEM));
   CK(cudaFuncSetAttribute(seg_gemm2_kernel<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           GEMM2W_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm4_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM4_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm4_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM4_SMEM));
   CK(cudaFuncSetAttribute(seg_gemm_stream_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           STREAM_SMEM));
   CK(cudaFuncSetAttribute(seg_gemm_stream_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1247,6 +1256,10 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_remote")) {
     ctx->force_remote = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "cluster4")) {
+    ctx->cluster4 = value ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "pdl")) {

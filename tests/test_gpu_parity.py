@@ -532,15 +532,18 @@ def test_every_kernel_and_tile_width_gives_identical_rows(shape):
     for pass_kind, width in ((0, d_in), (1, d_out)):
         xs = [torch.randn(t, width, device=dev).to(torch.bfloat16) for t in counts]
         outs = []
-        for pair, tn, pn in ((1, 0, 256), (1, 0, 512), (0, 256, 256), (0, 128, 256), (0, 64, 256)):
+        for pair, tn, pn, c4 in ((1, 0, 256, 0), (1, 0, 512, 0), (1, 0, 256, 1), (0, 256, 256, 0),
+                                 (0, 128, 256, 0), (0, 64, 256, 0)):
             ex.ctx.set_option("gemm_2cta", pair)
             ex.ctx.set_option("tile_n", tn)
             ex.ctx.set_option("pair_n", pn)
+            ex.ctx.set_option("cluster4", c4)
             outs.append(ex._compute_batch(pass_kind, [_env(c, 70 + 10 * pass_kind + len(outs), 0, O.K, pass_kind, x)
                                                       for c, x in enumerate(xs)]))
         ex.ctx.set_option("gemm_2cta", -1)
         ex.ctx.set_option("tile_n", 0)
         ex.ctx.set_option("pair_n", 0)
+        ex.ctx.set_option("cluster4", 0)
         for k in range(1, len(outs)):
             for c in range(len(xs)):
                 assert torch.equal(outs[0][c], outs[k][c]), (pass_kind, k, c)
