@@ -1374,6 +1374,12 @@ struct ShrinkItem {
   int32_t pack;   // 0: pack map tmP, contraction K = p.K; 1: tmP2, K = p.K2 (gradient shrinks)
   int32_t a_rows; // rows one A box delivers (128, or 16 for short pieces: MMA rows past the box
                   // are stale smem whose outputs are never written); 0 = 128
+  // block-diagonal zeros: the first slab of a piece writes zeros into its column block for the
+  // tile's rows OUTSIDE the piece [piece_lo, piece_hi) (tile-relative; tile rows tile_row0 ..
+  // + tm), so rows of other clients in the tile get no contribution from this adapter
+  int32_t zero_fill;
+  int32_t tile_row0, tm, piece_lo, piece_hi;
+  int32_t pad_[3];
 };
 
 struct ShrinkParams {
@@ -1606,6 +1612,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
           }
         }
         if (ew == 0 && lane == 0) p.ticket[blockIdx.x] = 0;   // ready for the next launch
+      }
+    }
+    if (it.zero_fill && c0 == 0) {
+      // zeros of the block-diagonal operand (replaces a memset of the whole operand)
+      const int vec_per_row = npad / 8;                      // 16-byte vectors of bf16
+      const int nrow = it.tm - (it.piece_hi - it.piece_lo);
+      for (int v = (int)(ew * 32 + lane); v < nrow * vec_per_row; v += 128) {
+        const int k = v / vec_per_row;
+        const int row = k < it.piece_lo ? k : k + (it.piece_hi - it.piece_lo);
+        reinterpret_cast<uint4*>(p.a_lora + (int64_t)(it.tile_row0 + row) * p.lora_ld + it.col0)[v % vec_per_row] =
+            make_uint4(0, 0, 0, 0);
       }
     }
   }

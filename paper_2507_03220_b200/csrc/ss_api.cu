@@ -628,7 +628,8 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
         const int col = (int)(chunks.size() - td.chunk_begin) * LORA_CHUNK;
         for (int q = 0; q < d.rank_pad / LORA_CHUNK; ++q) chunks.push_back(d.pack_row + q * LORA_CHUNK);
         for (int r = 0; r < nrows; r += BM)
-          items.push_back(ShrinkItem{sj, amap, arow + r, std::min(BM, nrows - r), mt * TM + p0 + r, col, 0, 0});
+          items.push_back(ShrinkItem{sj, amap, arow + r, std::min(BM, nrows - r), mt * TM + p0 + r, col, 0, 0,
+                                     r == 0 ? 1 : 0, mt * TM, TM, p0, p0 + nrows, {0, 0, 0}});
       };
       if (td.seg >= 0) {
         add_piece(td.seg, td.amap, td.arow, 0, td.rows);
@@ -879,12 +880,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, BM);
     if (rc) return rc;
     // ---- K3 shrink into the zeroed block-diagonal operand
-    {
-      const int64_t n16 = al_rows * lora_ld * 2 / 16;
-      CK(launch_k(ctx, zero_kernel, (int)std::min<int64_t>((n16 + 255) / 256, ctx->num_sms * 4), 256, 0, stream,
-                  reinterpret_cast<uint4*>(ctx->a_lora), n16));
-      ctx->launches++;
-    }
+    // (no memset: the shrink's first slab of each piece writes the block-diagonal zeros)
     ShrinkParams sp;
     sp.K = K;
     sp.lora_ld = (int)lora_ld;
@@ -1667,8 +1663,9 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     lg[j].gmap = (int32_t)(4 * j + 3);
     for (int r = 0; r < (int)s.rows; r += BM) {
       const int n = std::min<int>(BM, s.rows - r);
-      sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 0), r, n, lg[j].qrow0 + r, 0, 0, 0});
-      sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 1), r, n, (int32_t)qrows + lg[j].qrow0 + r, 0, 1, 0});
+      sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 0), r, n, lg[j].qrow0 + r, 0, 0, 0, 0, 0, 0, 0, 0, {0, 0, 0}});
+      sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 1), r, n, (int32_t)qrows + lg[j].qrow0 + r, 0, 1, 0, 0,
+                                  0, 0, 0, 0, {0, 0, 0}});
     }
     for (int m = 0; m < d_in; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 0, m, 0});
     for (int m = 0; m < d_out; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 1, m, 0});
