@@ -249,8 +249,6 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   a_rows64 (1)        64-row A box for such dispatches in the single-CTA kernel
  *   shrink_mode (0)     LoRA shrink: 0 auto, 1 one CTA per slab, 2 one CTA per (slab, K chunk)
  *   shrink_kb_chunk     k-blocks (of 64) per fixed K chunk of the shrink
- *   prefetch_mb, prefetch_rows, prefetch_hint, pf_depth (0, 256, 2, 0)  L2 prefetch of the next
- *                       layer / of the launch's own W for small dispatches (measured slower: off)
  *   pdl (0)             programmatic dependent launch between a dispatch's kernels (no gain measured)
  *   zero_copy_bytes (4 MiB)  ss_compute_batch_host dispatches up to this size: no copies (UVA)
  *   force_remote (0)    testing: route every segment as if it lived on a peer GPU

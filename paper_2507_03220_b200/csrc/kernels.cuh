@@ -87,15 +87,6 @@ struct GemmParams {
   int hint_a, hint_b, hint_out;     // L2 policy of A loads / W loads / output stores (0 none,
                                     // 1 evict_first, 2 evict_last)
   int a_bytes;                      // bytes one A-operand TMA box delivers (64- or 128-row box)
-  // Weight-streaming (small-M) dispatches: L2 prefetch of the layer the executor serves next
-  // (its W and LoRA packs), spread over the CTAs and issued by an otherwise idle warp while
-  // this launch streams its own W.
-  int pf_depth;                     // > 0: prefetch this launch's own W boxes pf_depth k-blocks
-                                    // ahead of the TMA loads (weight-streaming dispatches)
-  int pf_n;
-  int pf_hint;                      // L2 policy of the prefetched lines (0 normal, 2 evict_last)
-  const char* pf_ptr[3];
-  int64_t pf_bytes[3];
   int has_bias;
   int any_lora;
   int ia3_in_epilogue;              // forward: scale output columns by IA3
@@ -131,23 +122,6 @@ __device__ __forceinline__ void tile_coords(int t, const GemmParams& p, int& mb,
   const int r = t % per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
-}
-
-constexpr int64_t PF_CHUNK = 64 << 10;
-__device__ __forceinline__ void prefetch_regions(const GemmParams& p) {
-  const uint64_t pol = p.pf_hint == 2 ? policy_evict_last() : policy_evict_normal();
-  int64_t c0 = 0;
-  for (int r = 0; r < p.pf_n; ++r) {
-    const int64_t nch = (p.pf_bytes[r] + PF_CHUNK - 1) / PF_CHUNK;
-    // chunk index continues across regions so every CTA gets an even share
-    int64_t c = ((blockIdx.x - c0) % gridDim.x + gridDim.x) % gridDim.x;
-    for (; c < nch; c += gridDim.x) {
-      const int64_t off = c * PF_CHUNK;
-      const int64_t len = min(PF_CHUNK, p.pf_bytes[r] - off);
-      if (len >= 16) bulk_prefetch_l2(p.pf_ptr[r] + off, (uint32_t)(len & ~int64_t(15)), pol);
-    }
-    c0 += nch;
-  }
 }
 
 __device__ __forceinline__ uint64_t l2_policy(int h) {
@@ -550,20 +524,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_expect_tx(&full_bar[s], p.a_bytes + B_STAGE_BYTES);
           load_a_or_b(smA + s * A_STAGE_BYTES, tmA, &full_bar[s], kb * BK, td.arow, p.hint_a, pol_a);
           uint8_t* b = smB + s * B_STAGE_BYTES;
-          if (p.pf_depth > 0) {
-            // weight streaming: keep pf_depth more k-blocks of W on their way into L2 than the
-            // smem ring can hold, so the ring's loads see L2 instead of DRAM latency
-            const int kp = kb == 0 ? 0 : kb + p.pf_depth - 1;
-            const int kp_end = min(nkb, kb + p.pf_depth);
-            for (int q = kp; q < kp_end; ++q) {
-              if (kBwd) {
-                tma_prefetch_2d(&tmB, q * BK, n0);
-              } else {
-#pragma unroll
-                for (int j = 0; j < TBN / 64; ++j) tma_prefetch_2d(&tmB, n0 + 64 * j, q * BK);
-              }
-            }
-          }
           if (kBwd) {
             // W viewed K-major: rows = d_in (the GEMM's N), cols = d_out (the GEMM's K).
             load_a_or_b(b, &tmB, &full_bar[s], kb * BK, n0, p.hint_b, pol_b);
@@ -652,9 +612,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       __syncwarp();
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
-  } else if (warp == 3) {
-    // ------------------------------------------------------------ next-layer L2 prefetch
-    if (lane == 0 && p.pf_n > 0) prefetch_regions(p);
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const uint32_t ew = warp - 4;  // TMEM lane quarter

@@ -130,12 +130,6 @@ struct ss_ctx {
   int pdl = 0;               // programmatic dependent launch between a dispatch's kernels (measured: no gain)
   int stream_gemm = 1;       // weight-streaming kernel for those dispatches (K % 64 == 0)
   int a_rows64 = 1;          // 64-row A box for single-tile dispatches of <= 64 rows
-  // L2 prefetch of the successor layer (forward order for FWD / NOISE, reverse for BWD) from
-  // GEMMs of at most `prefetch_rows` rows, up to `prefetch_mb` MB (0 disables)
-  int prefetch_mb = 0;
-  int pf_depth = 0;          // own-W L2 prefetch distance (k-blocks) for weight-streaming GEMMs
-  int prefetch_rows = 256;
-  int prefetch_hint = 2;
   int l2_budget_mb = 48;
   // 1: L2 evict_last on the operand a raster group re-reads (A rows in M order, W columns in N
   // order) and evict_first on the outputs (written once, never re-read by this launch)
@@ -933,35 +927,6 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   gpm.hint_b = (ctx->l2_hints && gpm.group_n > 0) ? 2 : 0;
   gpm.hint_out = ctx->l2_hints ? 1 : 0;
   gpm.a_bytes = B.a_rows64 ? A_STAGE_BYTES / 2 : A_STAGE_BYTES;
-  gpm.pf_n = 0;
-  gpm.pf_hint = ctx->prefetch_hint;
-  gpm.pf_depth = (!pair && B.M <= ctx->prefetch_rows) ? ctx->pf_depth : 0;
-  if (ctx->prefetch_mb > 0 && !pair && B.M <= ctx->prefetch_rows) {
-    // weight-streaming dispatch: its own W is read once and not again soon (evict_first), and
-    // the layer served next is pulled into L2 behind it
-    gpm.hint_b = 1;
-    auto it = ctx->layers.find({B.block, B.role});
-    const Layer* nx = nullptr;
-    if (bwd) {
-      if (it != ctx->layers.begin()) nx = &std::prev(it)->second;
-    } else if (std::next(it) != ctx->layers.end()) {
-      nx = &std::next(it)->second;
-    }
-    if (nx) {
-      int64_t budget = (int64_t)ctx->prefetch_mb << 20;
-      auto add = [&](const void* ptr, int64_t bytes) {
-        bytes = std::min(bytes, budget) & ~int64_t(15);
-        if (!ptr || bytes <= 0 || gpm.pf_n == 3) return;
-        gpm.pf_ptr[gpm.pf_n] = static_cast<const char*>(ptr);
-        gpm.pf_bytes[gpm.pf_n++] = bytes;
-        budget -= bytes;
-      };
-      // the LoRA packs first (small, read by the shrink before the GEMM needs W)
-      add(nx->at_pack, (int64_t)nx->pack_rows * nx->ld_at * 2);
-      add(nx->b_pack, (int64_t)nx->pack_rows * nx->ld_b * 2);
-      add(nx->W, (int64_t)nx->d_in * nx->ldw * 2);
-    }
-  }
   gpm.has_bias = (pass_kind == SS_PASS_FORWARD && L.bias) ? 1 : 0;
   gpm.any_lora = any_lora ? 1 : 0;
   gpm.ia3_in_epilogue = (pass_kind != SS_PASS_BACKWARD) ? 1 : 0;
@@ -1268,25 +1233,6 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   }
   if (!strcmp(key, "a_rows64")) {
     ctx->a_rows64 = value ? 1 : 0;
-    return SS_OK;
-  }
-  if (!strcmp(key, "prefetch_mb")) {
-    if (value < 0) return fail(ctx, SS_E_ARG, "prefetch_mb must be >= 0");
-    ctx->prefetch_mb = (int)value;
-    return SS_OK;
-  }
-  if (!strcmp(key, "pf_depth")) {
-    if (value < 0 || value > 64) return fail(ctx, SS_E_ARG, "pf_depth must be in [0, 64]");
-    ctx->pf_depth = (int)value;
-    return SS_OK;
-  }
-  if (!strcmp(key, "prefetch_rows")) {
-    ctx->prefetch_rows = (int)value;
-    return SS_OK;
-  }
-  if (!strcmp(key, "prefetch_hint")) {
-    if (value != 0 && value != 2) return fail(ctx, SS_E_ARG, "prefetch_hint must be 0 or 2");
-    ctx->prefetch_hint = (int)value;
     return SS_OK;
   }
   if (!strcmp(key, "l2_hints")) {
