@@ -703,7 +703,7 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tr_path):
+    if os.path.exists(tr_path) and args.workload == "13b":   # the capture is of the 13B step
         try:
             traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
         except (OSError, ValueError):
