@@ -729,3 +729,29 @@ def test_in_place_host_handoff_bitwise(zero_copy):
                                             for c, t in enumerate(counts)])
         for c in range(len(counts)):
             assert torch.equal(got[c], dev[c].cpu()), (pass_kind, c)
+
+
+@pytest.mark.parametrize("zero_copy", [0, 1 << 30])
+def test_host_dispatch_rejected_segment_untouched(zero_copy):
+    """ss_compute_batch_host (both the pipelined and the zero-copy path): a segment the library
+    rejects (wrong width) gets a nonzero status and its host reply buffer is not written; the
+    other segments' replies equal the device path bitwise (executor.py:192-215: a malformed
+    envelope fails alone)."""
+    from paper_2507_03220_b200 import _lib
+    from paper_2507_03220_b200.device import Seg
+    d_in, d_out = 512, 768
+    w, b = O.layer_params(21, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)})
+    ex.ctx.set_option("zero_copy_bytes", zero_copy)
+    _mixed_clients(ex, d_in, d_out, seed=21, role=O.V)
+    counts = [300, 2, 129, 64]
+    xs = [torch.randn(t, d_in).to(torch.bfloat16).pin_memory() for t in counts]
+    xs[2] = torch.randn(counts[2], d_in + 64).to(torch.bfloat16).pin_memory()   # malformed width
+    outs = [torch.full((t, d_out), 3.0, dtype=torch.bfloat16).pin_memory() for t in counts]
+    segs = [Seg(c, x, o, adapter=(0, O.V) in ex._fused.get(c, ())) for c, (x, o) in enumerate(zip(xs, outs))]
+    status = ex.ctx.compute_host(0, 0, O.V, segs)
+    assert status[2] == _lib.SS_SEG_BAD_WIDTH and [status[i] for i in (0, 1, 3)] == [0, 0, 0]
+    assert torch.equal(outs[2], torch.full((counts[2], d_out), 3.0, dtype=torch.bfloat16))
+    dev = ex._compute_batch(0, [_env(c, 200 + c, 0, O.V, 0, xs[c].to(ex.device)) for c in (0, 1, 3)])
+    for j, c in enumerate((0, 1, 3)):
+        assert torch.equal(outs[c], dev[j].cpu()), c
