@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int ls = 0; ls * 4 < cc; ++ls) {
             const int nq = min(4, cc - ls * 4);
             mbar_wait(&empty_bar[s], ph ^ 1);
-            mbar_expect_tx(&full_bar[s], A_STAGE_BYTES + nq * LORA_CHUNK_BYTES);
+            mbar_expect_tx(&full_bar[s], A_STAGE_BYTES / 2 + nq * LORA_CHUNK_BYTES);   // 64-row A_lora box
             uint8_t* a = smem + s * S_STAGE;
             uint8_t* b = a + S_A_BYTES;
             tma_load_2d(a, &tmAL, &full_bar[s], ls * BK, m0);

@@ -871,7 +871,8 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
 
   CUtensorMap tmAL;
   if (any_lora) {
-    rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, BM);
+    // the streaming kernel (<= 64 rows) reads the LoRA operand through a 64-row box too
+    rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, B.stream ? 64 : BM);
     if (rc) return rc;
     // ---- K3 shrink into the zeroed block-diagonal operand
     // (no memset: the shrink's first slab of each piece writes the block-diagonal zeros)
