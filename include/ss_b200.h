@@ -240,6 +240,7 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   l2_hints (1)        L2 evict_last on the operand a raster group re-reads, evict_first on outputs
  *   gemm_2cta (-1)      CTA-pair kernel: -1 by dispatch size, 1 / 0 forced
  *   pair_n (0)          CTA-pair tile width 256 (double-buffered TMEM) or 512 (12 warps); 0 auto
+ *   side_shrink (1)     a LoRA shrink that reads no packed rows runs on a side stream beside the gather
  *   cluster4 (0)        256x256 pair tiles as 4-CTA clusters sharing B by multicast (measured
  *                       35 % slower in the step: off)
  *   tile_n (0)          force the single-CTA tile width 64 / 128 / 256 (0 auto)

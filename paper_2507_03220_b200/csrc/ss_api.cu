@@ -98,6 +98,10 @@ struct ss_ctx {
   cudaStream_t upload = nullptr;
   // host-buffer dispatches (ss_compute_batch_host): copy streams + a device staging ring
   cudaStream_t h2d = nullptr, d2h = nullptr;
+  // side stream for a LoRA shrink that does not depend on the gather (fork / join events)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int side_shrink = 1;
   struct HostSlot {
     void* in = nullptr;
     void* out = nullptr;
@@ -450,6 +454,7 @@ struct Built {
   int pass_kind = 0, block = 0, role = 0, K = 0, N = 0;
   int64_t M = 0, MX = 0, lora_ld = 64, al_rows = 0, ldx = 0;
   bool any_lora = false, pair = false, a_rows64 = false, stream = false;
+  bool shrink_indep = false;   // the shrink reads no packed rows: it may run beside the gather
   int tbn = BN, pn = 256, num_m = 0, n_piece = 0, n_items = 0, part_ld = 16, shrink_chunks_ = 1;
   int kb_chunk = SHRINK_KB_CHUNK;
   size_t off_tm = 0, off_seg = 0, off_tile = 0, off_piece = 0, off_ch = 0, off_st = 0, off_it = 0;
@@ -736,21 +741,42 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     B.a_rows64 = true;
   }
 
-  // ---- short LoRA pieces of the packed operand (decode rows): the shrink reads them through a
-  // 16-row box instead of 128 rows of neighbouring clients' rows
+  // ---- short LoRA pieces of the packed operand (decode rows): the shrink reads them straight
+  // from the client's rows through a 16-row box over the segment (so it no longer waits for the
+  // gather and can run beside it), or, for sources TMA cannot read in place, through a 16-row
+  // box over the packed operand instead of 128 rows of neighbouring clients' rows
   if (any_lora && MX > 0) {
     int32_t small_map = -1;
+    std::vector<int32_t> seg_map(ds.size(), -1);
     for (ShrinkItem& it : items) {
       if (it.amap != 0 || it.rows > 16) continue;
-      if (small_map < 0) {
-        small_map = (int32_t)tmaps.size();
-        tmaps.emplace_back();
-        rc = encode_2d(ctx, &tmaps.back(), ctx->X, K, MX, ldx, 64, 16);
-        if (rc) return rc;
+      const DevSeg& d = ds[it.seg];
+      const bool in_place = (d.flags & SEGF_SRC_BF16) && (d.flags & SEGF_SRC_VEC) &&
+                            !(d.flags & (SEGF_REMOTE_SRC | SEGF_SRC_ALIASED)) && (d.src_ld * 2) % 16 == 0;
+      if (in_place) {
+        if (seg_map[it.seg] < 0) {
+          seg_map[it.seg] = (int32_t)tmaps.size();
+          tmaps.emplace_back();
+          rc = encode_2d(ctx, &tmaps.back(), d.src, K, d.rows, d.src_ld, 64, 16);
+          if (rc) return rc;
+        }
+        it.arow = it.arow - d.xrow0 + d.xlocal0;       // X row -> segment row
+        it.amap = seg_map[it.seg];
+      } else {
+        if (small_map < 0) {
+          small_map = (int32_t)tmaps.size();
+          tmaps.emplace_back();
+          rc = encode_2d(ctx, &tmaps.back(), ctx->X, K, MX, ldx, 64, 16);
+          if (rc) return rc;
+        }
+        it.amap = small_map;
       }
-      it.amap = small_map;
       it.a_rows = 16;
     }
+    // the shrink depends on the gather only if some item reads the packed operand
+    B.shrink_indep = true;
+    for (const ShrinkItem& it : items)
+      if (it.amap == 0 || it.amap == small_map) B.shrink_indep = false;
   }
 
   // ---- serialise the device tables
@@ -848,7 +874,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   const CUtensorMap* d_tmaps = reinterpret_cast<const CUtensorMap*>(dv + B.off_tm);
   const DevSeg* d_segs = reinterpret_cast<const DevSeg*>(dv + B.off_seg);
   // ---- K4 gather of the packed rows
-  if (MX > 0) {
+  auto launch_gather = [&]() -> int {
     GatherParams gp;
     gp.MX = (int)MX;
     gp.K = K;
@@ -867,10 +893,11 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     prof_end(ctx, stream, pi);
     CK(cudaGetLastError());
     ctx->launches++;
-  }
+    return SS_OK;
+  };
 
-  CUtensorMap tmAL;
-  if (any_lora) {
+  CUtensorMap tmAL = L.tm_w_fwd;  // (unused without LoRA)
+  auto launch_shrink = [&](cudaStream_t st) -> int {
     // the streaming kernel (<= 64 rows) reads the LoRA operand through a 64-row box too
     rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, B.stream ? 64 : BM);
     if (rc) return rc;
@@ -888,19 +915,33 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     sp.max_chunks = B.shrink_chunks_;
     sp.kb_chunk = B.kb_chunk;
     sp.ticket = ctx->shrink_ticket;
-    const int pi = prof_begin(ctx, stream, SS_KERNEL_SHRINK, B.shrink_flops, B.shrink_bytes);
+    const int pi = prof_begin(ctx, st, SS_KERNEL_SHRINK, B.shrink_flops, B.shrink_bytes);
     sp.K2 = K;
     // one CTA per slab walking every K chunk when there are enough slabs to fill the GPU and the
     // ranks fit the register sums; else one CTA per (slab, chunk). Same sums either way.
     const bool whole = B.shrink_chunks_ == 1 ||
                        (B.part_ld <= 64 && (ctx->shrink_mode == 1 || (ctx->shrink_mode == 0 && B.n_items >= ctx->num_sms)));
     CK(launch_k(ctx, lora_shrink_kernel, dim3(B.n_items, whole ? 1 : B.shrink_chunks_), GEMM_THREADS, SHRINK_SMEM,
-                stream, bwd ? L.tm_b : L.tm_at, bwd ? L.tm_b : L.tm_at, sp));
-    prof_end(ctx, stream, pi);
+                st, bwd ? L.tm_b : L.tm_at, bwd ? L.tm_b : L.tm_at, sp));
+    prof_end(ctx, st, pi);
     CK(cudaGetLastError());
     ctx->launches++;
+    return SS_OK;
+  };
+
+  // The shrink reads the client rows in place (no packed rows) -> it runs on the side stream
+  // beside the gather: fork after everything queued so far (the previous dispatch's GEMM reads
+  // the LoRA operand the shrink rewrites), join before the GEMM.
+  if (any_lora && MX > 0 && B.shrink_indep && ctx->side_shrink && !ctx->profiling) {
+    CK(cudaEventRecord(ctx->ev_fork, stream));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    if ((rc = launch_shrink(ctx->side))) return rc;
+    CK(cudaEventRecord(ctx->ev_join, ctx->side));
+    if ((rc = launch_gather())) return rc;
+    CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));
   } else {
-    tmAL = L.tm_w_fwd;  // unused
+    if (MX > 0 && (rc = launch_gather())) return rc;
+    if (any_lora && (rc = launch_shrink(stream))) return rc;
   }
 
   // ---- K1 / K2 / K5 fused GEMM
@@ -1075,7 +1116,10 @@ int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out) {
     return SS_E_CUDA;
   }
   if (cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     delete ctx;
     return SS_E_CUDA;
   }
@@ -1147,6 +1191,9 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   }
   cudaStreamDestroy(ctx->h2d);
   cudaStreamDestroy(ctx->d2h);
+  cudaStreamDestroy(ctx->side);
+  cudaEventDestroy(ctx->ev_fork);
+  cudaEventDestroy(ctx->ev_join);
   delete ctx;
   return SS_OK;
 }
@@ -1218,6 +1265,10 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_remote")) {
     ctx->force_remote = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "side_shrink")) {
+    ctx->side_shrink = value ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "cluster4")) {
