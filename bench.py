@@ -521,7 +521,8 @@ def main():
     ap.add_argument("--opt", action="append", default=[],
                     help="library tuning option key=value (ss_set_option), e.g. gemm_2cta=1, group_m=8")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="timed e2e steps (0: 1 for the prefill workloads, 10 for decode)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=8,
@@ -725,7 +726,8 @@ def main():
 
     e2e = None
     if not args.skip_e2e and not tp_mode:
-        dt, h2d, d2h = e2e_leg(ex, args.workload, specs, max(1, args.e2e_steps), device)
+        e2e_steps = args.e2e_steps or (10 if args.workload.endswith("decode") else 1)
+        dt, h2d, d2h = e2e_leg(ex, args.workload, specs, e2e_steps, device)
         if world > 1:
             t = torch.tensor([dt], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -733,7 +735,7 @@ def main():
         e2e = {"value": tokens / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
                "path": "GpuBaseExecutor.serve_forward / serve_backward, pinned host bf16 payloads + host reply buffers, "
-                       f"{max(1, args.e2e_steps)} timed step(s) after 1 warm-up"}
+                       f"{e2e_steps} timed step(s) after 1 warm-up"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
