@@ -67,7 +67,8 @@ class TensorParallelExecutor:
         if reduce:
             out_w = spec.d_in if pass_kind == PASS_BACKWARD else spec.d_out
         counts = [int(x.shape[0]) for x in payloads]
-        dt = self.reduce_dtype if reduce else payloads[0].dtype
+        # a single rank has nothing to sum: its "partials" are the final bf16 rows
+        dt = self.reduce_dtype if (reduce and self.world > 1) else payloads[0].dtype
         local = torch.empty((sum(counts), out_w), dtype=dt, device=self.device)
         envs, pos = [], 0
         for cid, x, t in zip(client_ids, payloads, counts):
@@ -84,7 +85,7 @@ class TensorParallelExecutor:
     def dispatch(self, pass_kind: int, block: int, role: int, payloads, client_ids):
         """Full-width outputs for every segment on every rank (one collective)."""
         spec, local, counts = self.dispatch_local(pass_kind, block, role, payloads, client_ids)
-        full = P.combine(spec, pass_kind, local, self.group)
+        full = P.combine(spec, pass_kind, local, self.group) if self.world > 1 else local
         if full.dtype != payloads[0].dtype:
             full = full.to(payloads[0].dtype)
         out, pos = [], 0
