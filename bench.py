@@ -332,7 +332,6 @@ def build_tp_workload(wl_key, device, rank, world):
     # dispatch-wide output; then ONE collective finishes the dispatch: all-reduce of fp32
     # partials (converted to bf16 into the reply rows) or all-gather of the column shards
     # (reassembled into the reply rows). World size 1: the shard IS the layer, no collective.
-    import torch.distributed as dist
     from paper_2507_03220_b200 import parallel_plan as P
     ft = [c for c, s_ in enumerate(specs) if s_[2]]
     plan = []
@@ -347,21 +346,8 @@ def build_tp_workload(wl_key, device, rank, world):
     def add(pass_kind, b, r, cids):
         di, do = dims[r]
         spec = tp.specs[(b, r)]
-        w_in, w_out = (do, di) if pass_kind == 1 else (di, do)
-        m = len(cids) * t
-        reply = buf("reply", (m, w_out), torch.bfloat16)          # the clients' reply rows
-        kind = spec.collective(pass_kind) if world > 1 else "none"
-        if kind == "all_reduce":
-            local = buf("partial", (m, w_out), torch.float32)
-            gbuf = None
-        elif kind == "all_gather":
-            sizes = [P.shard_bounds(spec.d_out if spec.split == "column" else spec.d_in, q, world) for q in range(world)]
-            wmax = max(hi - lo for lo, hi in sizes)
-            pad = buf("shard", (m, wmax), torch.bfloat16)
-            local = pad[:, : sizes[rank][1] - sizes[rank][0]]
-            gbuf = (pad, buf("gathered", (world * m, wmax), torch.bfloat16), sizes)
-        else:
-            local, gbuf = reply, None
+        w_in = do if pass_kind == 1 else di
+        kind, local, gbuf, reply = P.dispatch_buffers(spec, pass_kind, len(cids) * t, world, rank, buf)
         segs = [(c, P.shard_input(spec, pass_kind, bufs[c][: t * w_in].view(t, w_in)), local[j * t:(j + 1) * t], None)
                 for j, c in enumerate(cids)]
         plan.append((tp.ex.compile_dispatch(pass_kind, b, r, segs), kind, local, gbuf, reply))
@@ -371,25 +357,16 @@ def build_tp_workload(wl_key, device, rank, world):
     for (b, r) in reversed(layers):
         if ft:
             add(1, b, r, ft)
-    tp._bench_dist = dist
     return tp, plan, specs, wl
 
 
 def run_step_tp(tp, plan):
     import torch
+    from paper_2507_03220_b200.parallel_plan import finish_dispatch
     stream = torch.cuda.current_stream(tp.device)
-    dist = tp._bench_dist
     for disp, kind, local, gbuf, reply in plan:
         disp.run(stream)
-        if kind == "all_reduce":
-            dist.all_reduce(local, op=dist.ReduceOp.SUM, group=tp.group)
-            reply.copy_(local)
-        elif kind == "all_gather":
-            pad, out, sizes = gbuf
-            dist.all_gather_into_tensor(out, pad, group=tp.group)
-            m = pad.shape[0]
-            for q, (lo, hi) in enumerate(sizes):
-                reply[:, lo:hi].copy_(out[q * m:(q + 1) * m, : hi - lo])
+        finish_dispatch(kind, local, gbuf, reply, tp.group)
 
 
 def e2e_leg(ex, wl_key, specs, steps, device):

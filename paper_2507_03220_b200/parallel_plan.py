@@ -189,3 +189,39 @@ def comm_bytes_per_token(d_in: int, d_out: int, role, pass_kind: int, world: int
 
 def ratio_check(a, b, rtol=1e-5, atol=1e-5) -> bool:
     return np.allclose(np.asarray(a, np.float64), np.asarray(b, np.float64), rtol=rtol, atol=atol)
+
+
+def dispatch_buffers(spec: ShardSpec, pass_kind: int, rows: int, world: int, rank: int, alloc):
+    """Buffers of one prebuilt tensor-parallel dispatch: returns (kind, local, gbuf, reply).
+    `local` is what this rank's kernels write (fp32 [rows, full] partials for an all-reduce; a
+    column view of a padded bf16 shard buffer for an all-gather; the reply itself at world size
+    1). `alloc(tag, shape, dtype)` provides (possibly shared) tensors."""
+    import torch
+    full = spec.d_in if pass_kind == 1 else spec.d_out
+    reply = alloc("reply", (rows, full), torch.bfloat16)
+    kind = spec.collective(pass_kind) if world > 1 else "none"
+    if kind == "all_reduce":
+        return kind, alloc("partial", (rows, full), torch.float32), None, reply
+    if kind == "all_gather":
+        sizes = [shard_bounds(spec.d_out if spec.split == "column" else spec.d_in, q, world) for q in range(world)]
+        wmax = max(hi - lo for lo, hi in sizes)
+        pad = alloc("shard", (rows, wmax), torch.bfloat16)
+        local = pad[:, : sizes[rank][1] - sizes[rank][0]]
+        return kind, local, (pad, alloc("gathered", (world * rows, wmax), torch.bfloat16), sizes), reply
+    return kind, reply, None, reply
+
+
+def finish_dispatch(kind: str, local, gbuf, reply, group=None) -> None:
+    """The dispatch's one collective, landing the full-width result in `reply` on every rank:
+    all-reduce the fp32 partials (then round once to bf16), or all-gather the padded column
+    shards and reassemble them."""
+    import torch.distributed as dist
+    if kind == "all_reduce":
+        dist.all_reduce(local, op=dist.ReduceOp.SUM, group=group)
+        reply.copy_(local)
+    elif kind == "all_gather":
+        pad, out, sizes = gbuf
+        dist.all_gather_into_tensor(out, pad, group=group)
+        m = pad.shape[0]
+        for q, (lo, hi) in enumerate(sizes):
+            reply[:, lo:hi].copy_(out[q * m:(q + 1) * m, : hi - lo])

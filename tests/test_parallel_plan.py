@@ -118,3 +118,56 @@ def test_tensor_parallel_world2_matches_unsharded_oracle():
     for p in procs:
         p.join(60)
     assert all(msg == "ok" for _, msg in results), results
+
+
+def _finish_worker(rank, world, port, q):
+    """Each rank writes its share of a known full-width output into the buffers
+    dispatch_buffers hands out (what its plan's kernels write), then finish_dispatch must
+    leave the full result in `reply` on every rank: bitwise for the all-gather layers, the
+    one bf16 rounding of the fp32 sum for the all-reduce layers."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pool = {}
+
+        def alloc(tag, shape, dtype):
+            key = (tag, shape, dtype)
+            if key not in pool:
+                pool[key] = torch.full(shape, float("nan"), dtype=dtype)
+            return pool[key]
+
+        rows = 7
+        for role, d_in, d_out in CASES + [(Role.FF_UP, 48, 200)]:
+            spec = P.plan_layer(role, d_in, d_out, rank, world)
+            for pass_kind in (0, 1):
+                full_w = d_in if pass_kind == 1 else d_out
+                g = torch.Generator().manual_seed(int(role) * 10 + pass_kind)
+                want = torch.randn(rows, full_w, generator=g).to(torch.bfloat16)
+                kind, local, gbuf, reply = P.dispatch_buffers(spec, pass_kind, rows, world, rank, alloc)
+                if kind == "all_reduce":
+                    parts = [want.float() * 0.5 for _ in range(world)]     # exact halves
+                    local.copy_(parts[rank])
+                elif kind == "all_gather":
+                    lo, hi = spec.lo, spec.hi
+                    assert local.shape == (rows, hi - lo)
+                    local.copy_(want[:, lo:hi])
+                P.finish_dispatch(kind, local, gbuf, reply)
+                if not torch.equal(reply, want):
+                    q.put((rank, f"{role.name} pass {pass_kind} ({kind}) mismatch"))
+                    return
+        q.put((rank, "ok"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_plan_collectives_world2_reassemble_full_rows():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_finish_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(60)
+    assert all(msg == "ok" for _, msg in results), results
