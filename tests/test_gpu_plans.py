@@ -68,9 +68,12 @@ def test_plan_rebuilds_after_workspace_growth_and_rank_change():
     assert mx <= O.TOL_MAX_REL and mn <= O.TOL_MEAN_REL
 
 
-def test_cuda_graph_of_plans_bitwise_equals_eager():
+@pytest.mark.parametrize("decode", [False, True])
+def test_cuda_graph_of_plans_bitwise_equals_eager(decode):
     """A whole executor step (forward over several layers, then backward in reverse) captured in
-    one CUDA graph gives the eager results bitwise, and replays deterministically."""
+    one CUDA graph gives the eager results bitwise, and replays deterministically. `decode`:
+    two-row clients, so the weight-streaming kernel runs and the LoRA shrink reads the client
+    rows in place on the side stream (a parallel branch of the captured graph)."""
     layers = {}
     dims = {O.Q: (256, 256), O.FF_UP: (256, 512), O.FF_DOWN: (512, 256)}
     for role, (di, do) in dims.items():
@@ -83,7 +86,7 @@ def test_cuda_graph_of_plans_bitwise_equals_eager():
             ad = O.lora_params(24, cid, 0, role, di, do, r, 2.0 * r)
             lo[_addr(0, role)] = (ad.a, ad.b)
         ex.register_adapter(cid, _Adapter(lora=lo, alpha=2.0 * r, rank=r))
-    counts = [int(t) for t in rng.integers(1, 400, size=4)]
+    counts = [2, 2, 1, 2] if decode else [int(t) for t in rng.integers(1, 400, size=4)]
     bufs = [torch.randn(t * 512, device=ex.device).to(torch.bfloat16) for t in counts]
     outs = [torch.empty(t * 512, device=ex.device, dtype=torch.bfloat16) for t in counts]
     plan = []
