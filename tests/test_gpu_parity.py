@@ -755,3 +755,30 @@ def test_host_dispatch_rejected_segment_untouched(zero_copy):
     dev = ex._compute_batch(0, [_env(c, 200 + c, 0, O.V, 0, xs[c].to(ex.device)) for c in (0, 1, 3)])
     for j, c in enumerate((0, 1, 3)):
         assert torch.equal(outs[c], dev[j].cpu()), c
+
+
+def test_full_size_batched_equals_solo_13b_ff_up():
+    """BASELINE configs[2] size: a 13B FF_UP forward over 32 clients x 1024 rows (M = 32768,
+    the 256x512 CTA-pair kernel) against three of the clients alone (1024 rows: the 256x256
+    pair kernel) — a size-independent property (batching invisibility, acceptance C5), bitwise,
+    with LoRA r8 / r64 and IA3 y_base outputs."""
+    d_in, d_out = 5120, 13824
+    w, b = O.layer_params(30, 0, O.FF_UP, d_in, d_out)
+    ex = _ex({(0, O.FF_UP): (w, b)})
+    for cid, r in ((0, 8), (1, 64)):
+        ad = O.lora_params(30, cid, 0, O.FF_UP, d_in, d_out, r, 2.0 * r)
+        ex.register_adapter(cid, _Adapter(lora={_addr(0, O.FF_UP): (ad.a, ad.b)}, alpha=2.0 * r, rank=r))
+    ex.register_adapter(2, _Adapter(ia3={_addr(0, O.FF_UP): O.ia3_params(30, 2, 0, O.FF_UP, d_out).ia3}))
+    dev = ex.device
+    gen = torch.Generator(device=dev).manual_seed(30)
+    xs = [torch.randn(1024, d_in, generator=gen, device=dev).to(torch.bfloat16) for _ in range(32)]
+    base_b = torch.empty(1024, d_out, dtype=torch.bfloat16, device=dev)
+    batched = ex._compute_batch(0, [_env(c, 1, 0, O.FF_UP, 0, x, base_to=base_b if c == 2 else None)
+                                    for c, x in enumerate(xs)])
+    base_batched = base_b.clone()
+    for c in (0, 1, 2):
+        base_s = torch.empty(1024, d_out, dtype=torch.bfloat16, device=dev)
+        solo = ex._compute_batch(0, [_env(c, 2 + c, 0, O.FF_UP, 0, xs[c], base_to=base_s if c == 2 else None)])[0]
+        assert torch.equal(solo, batched[c]), c
+        if c == 2:
+            assert torch.equal(base_s, base_batched)
