@@ -1617,16 +1617,7 @@ __device__ __forceinline__ int find_piece(const GatherParams& p, int xrow) {
   return p.piece_seg[lo];
 }
 
-// One warp per row, grid-stride.
-// Zero `n16` 16-byte words (the block-diagonal LoRA operand before the shrink writes its
-// blocks); a kernel rather than a memset node so the dispatch stays one chain of PDL launches.
-__global__ void __launch_bounds__(256) zero_kernel(uint4* __restrict__ p, int64_t n16) {
-  pdl_wait();
-  pdl_trigger();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = make_uint4(0, 0, 0, 0);
-}
-
+// One warp per (row, column chunk), grid-stride.
 __global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) {
   pdl_wait();
   pdl_trigger();
