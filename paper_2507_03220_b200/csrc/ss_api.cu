@@ -466,8 +466,10 @@ struct Built {
 
 // `local_buffers`: every pointer is a staging slice this context allocated on its own device
 // (host pipelines), so the per-pointer peer-GPU query is skipped.
+// `src_remote`: the caller already established that every source is pinned host memory read
+// with plain loads (the zero-copy host dispatch; its destinations are local slots): no query.
 int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
-                int32_t* seg_status, Built& B, bool local_buffers = false) {
+                int32_t* seg_status, Built& B, bool local_buffers = false, bool src_remote = false) {
   if (pass_kind < 0 || pass_kind > 2) return fail(ctx, SS_E_ARG, "unknown pass %d", pass_kind);
   if (n_seg < 0 || (n_seg > 0 && (!segs || !seg_status)))
     return fail(ctx, SS_E_ARG, "bad segment array");
@@ -510,6 +512,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     if (s.flags & SS_SEGF_DST_BF16) f |= SEGF_DST_BF16;
     if (aligned16(s.src, s.src_ld, (s.flags & SS_SEGF_SRC_BF16) ? 2 : 4)) f |= SEGF_SRC_VEC;
     if (aligned16(s.dst, s.dst_ld, (s.flags & SS_SEGF_DST_BF16) ? 2 : 4)) f |= SEGF_DST_VEC;
+    if (src_remote) f |= SEGF_REMOTE_SRC;
     if (!local_buffers || ctx->force_remote) {
       if (is_remote(ctx, s.src)) f |= SEGF_REMOTE_SRC;
       if (is_remote(ctx, s.dst) || (s.dst_base && is_remote(ctx, s.dst_base))) f |= SEGF_REMOTE_DST;
@@ -2010,7 +2013,8 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     }
     std::vector<int32_t> cst(cs.size(), 0);
     Built b;
-    if ((rc = build_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), cst.data(), b))) return rc;
+    if ((rc = build_batch(ctx, pass_kind, block, role, (int)cs.size(), cs.data(), cst.data(), b, true, true)))
+      return rc;
     for (size_t q = 0; q < cs.size(); ++q)
       if (cst[q] != SS_SEG_OK) seg_status[good[q]] = cst[q];
     if (b.M == 0) return SS_OK;
