@@ -373,7 +373,7 @@ class GpuBaseExecutor:
         results: list = [None] * len(envelopes)
         good: list[int] = []
         for i, env in enumerate(envelopes):
-            if addr_key(env.layer) != key:
+            if (int(env.block), int(env.role)) != key:      # == addr_key(env.layer), no enum
                 results[i] = ProtocolError(f"layer mismatch in batch: {env.layer} != {addr}")
             elif env.pass_kind != pass_kind:
                 results[i] = ProtocolError(f"pass mismatch in batch: {env.pass_kind}")

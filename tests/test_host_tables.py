@@ -42,3 +42,18 @@ def test_segment_fields_reject_bad_tensors():
         seg_fields(Seg(0, torch.zeros(4, 8).t(), torch.zeros(8, 4)))
     with pytest.raises(TypeError):
         seg_fields(Seg(0, torch.zeros(4, 8, dtype=torch.float16), torch.zeros(4, 8)))
+
+
+def test_segment_table_cache_tracks_tensor_identity():
+    from paper_2507_03220_b200.device import _cached_fields
+    cache = {}
+    x = torch.zeros(3, 64, dtype=torch.bfloat16)
+    y = torch.zeros(3, 128, dtype=torch.bfloat16)
+    s1 = Seg(1, x, y, adapter=True)
+    assert _cached_fields(cache, s1) == seg_fields(s1)
+    assert _cached_fields(cache, Seg(1, x, y, adapter=True)) == seg_fields(s1)    # hit
+    x2 = torch.zeros(3, 64, dtype=torch.float32)                                  # new object
+    s2 = Seg(1, x2, y, adapter=True)
+    assert _cached_fields(cache, s2) == seg_fields(s2)
+    tab = SegmentTable([s1, s2], cache)
+    assert [c.src for c in tab.arr[:2]] == [x.data_ptr(), x2.data_ptr()]
