@@ -73,6 +73,9 @@ extern "C" {
                                        SS_PASS_NOISE_EFFECT: the noise effect of the adapted layer,
                                        (n.W + s n.A.B) * l, bias-free (privacy.py:1-12 blinding
                                        with an executor-fused adapter) */
+#define SS_SEGF_PINNED (1u << 4)    /* ss_compute_batch_host: the caller has verified that src / dst /
+                                       dst_base are page-locked host memory (skips the per-pointer
+                                       query of the zero-copy path) */
 
 /* One request (envelope) of a batch, in batch order. Rows are concatenated in array order
  * exactly like concat_rows(); row r of segment i is batch row off_i + r, off_i = sum_{j<i} rows_j

@@ -44,6 +44,7 @@ SS_SEGF_SRC_BF16 = 1 << 0
 SS_SEGF_DST_BF16 = 1 << 1
 SS_SEGF_BASE_BF16 = 1 << 2
 SS_SEGF_ADAPTER = 1 << 3
+SS_SEGF_PINNED = 1 << 4
 
 # Every symbol include/ss_b200.h declares (checked by tests/test_lib_abi.py).
 EXPORTED = (

@@ -1968,6 +1968,7 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
   for (size_t q = 0; zero_copy && q < good.size(); ++q) {
     // only pinned (UVA-mapped) or device memory can be touched by the kernels directly
     const ss_seg& sg = segs[good[q]];
+    if (sg.flags & SS_SEGF_PINNED) continue;   // verified by the caller
     for (const void* ptr : {sg.src, static_cast<const void*>(sg.dst), static_cast<const void*>(sg.dst_base)}) {
       if (!ptr) continue;
       cudaPointerAttributes a;

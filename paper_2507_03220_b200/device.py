@@ -60,6 +60,7 @@ class Seg:
     base: torch.Tensor | None = None
     adapter: bool = False
     width: int | None = None   # declared width (defaults to src.shape[1])
+    pinned: bool = False       # host tensors verified page-locked by the caller (SS_SEGF_PINNED)
 
 
 _SEG_FMT = struct.Struct("<4I QqQqQq")          # ss_seg layout (include/ss_b200.h)
@@ -88,7 +89,7 @@ class SegmentTable:
 def _cached_fields(cache: dict, s: Seg) -> tuple:
     """seg_fields of a segment whose tensors recur across dispatches (clients reuse their
     buffers): keyed by the tensor objects' ids, validated through weak references."""
-    key = (id(s.src), id(s.dst), id(s.base), s.client_id, s.adapter, s.width)
+    key = (id(s.src), id(s.dst), id(s.base), s.client_id, s.adapter, s.width, s.pinned)
     hit = cache.get(key)
     # same live objects AND same storage (in-place set_ / resize_ could move a tensor)
     if (hit is not None and hit[0]() is s.src and hit[1]() is s.dst and (s.base is None or hit[2]() is s.base)
@@ -117,6 +118,8 @@ def seg_fields(s: Seg) -> tuple:
              (_lib.SS_SEGF_DST_BF16 if tensor_flags(dst) else 0))
     if s.adapter:
         flags |= _lib.SS_SEGF_ADAPTER
+    if s.pinned:
+        flags |= _lib.SS_SEGF_PINNED
     if base is not None:
         if tensor_flags(base):
             flags |= _lib.SS_SEGF_BASE_BF16

@@ -147,12 +147,13 @@ def _host_tensor_info(t: torch.Tensor):
 
 def _cached_info(cache: dict, t: torch.Tensor):
     hit = cache.get(id(t))
-    if hit is not None and hit[0]() is t:
+    ptr = t.data_ptr()
+    if hit is not None and hit[0]() is t and hit[2] == ptr:    # same object, same storage
         return hit[1]
     if len(cache) > 4096:
         cache.clear()
     v = _host_tensor_info(t)
-    cache[id(t)] = (weakref.ref(t), v)
+    cache[id(t)] = (weakref.ref(t), v, ptr)
     return v
 
 
@@ -464,8 +465,9 @@ class GpuBaseExecutor:
             self._pipeline_knobs = knobs
         fused = self._fused
         in_w = envelopes[good[0]].width
+        # _all_pinned_host verified every payload / reply is page-locked: tell the library
         segs = [Seg(client_id=envelopes[i].client_id, src=envelopes[i].payload, dst=envelopes[i].reply_to,
-                    width=in_w, adapter=key in fused.get(envelopes[i].client_id, ()))
+                    width=in_w, adapter=key in fused.get(envelopes[i].client_id, ()), pinned=True)
                 for i in good]
         status = self.ctx.compute_host(pass_kind, key[0], key[1], segs, stream)
         self.last_event = None
