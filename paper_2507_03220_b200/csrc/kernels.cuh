@@ -87,6 +87,11 @@ struct GemmParams {
   int hint_a, hint_b, hint_out;     // L2 policy of A loads / W loads / output stores (0 none,
                                     // 1 evict_first, 2 evict_last)
   int a_bytes;                      // bytes one A-operand TMA box delivers (64- or 128-row box)
+  // Overlap mode (streaming kernel): the LoRA shrink runs concurrently on another stream; the
+  // producer waits until lora_ready[0] == lora_expect (shrink CTAs done) before its first LoRA
+  // stage. lora_ready[1] counts the CTAs past that point; the last one re-arms both counters.
+  int* lora_ready = nullptr;
+  int lora_expect = 0;
   int has_bias;
   int any_lora;
   int ia3_in_epilogue;              // forward: scale output columns by IA3
@@ -646,6 +651,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // (backward, K-major). The MMA of k-block c reads 128 A rows from chunk c: rows 64-127 are the
 // next chunk (or the stage's W bytes) — garbage rows whose outputs are never stored. Same MMAs
 // in the same K order as the other kernels: bitwise the same rows.
+// Overlap mode: wait for the concurrently running LoRA shrink (all its CTAs arrived), then
+// make its global writes visible to this thread's TMA loads.
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// (Bounded: the shrink runs on another stream and the GPU does not formally guarantee the two
+// kernels run concurrently; if it has not arrived within 2 s, fail loudly instead of hanging.)
+__device__ __forceinline__ void spin_until_ready(const GemmParams& p) {
+  const uint64_t t0 = global_ns();
+  while (ld_acquire_gpu(p.lora_ready) < p.lora_expect) {
+    __nanosleep(256);
+    if (global_ns() - t0 > 2000000000ull) __trap();
+  }
+}
+__device__ __forceinline__ void wait_lora_ready(const GemmParams& p) {
+  spin_until_ready(p);
+  fence_proxy_async_global();
+}
+// Every CTA takes one ticket once it no longer reads the counter; the last one re-arms both
+// counters for the next dispatch (after the shrink's last arrival, so none can land late).
+__device__ __forceinline__ void lora_ready_ticket(const GemmParams& p) {
+  if (atomicAdd(p.lora_ready + 1, 1) == (int)gridDim.x - 1) {
+    spin_until_ready(p);
+    atomicExch(p.lora_ready, 0);
+    atomicExch(p.lora_ready + 1, 0);
+  }
+}
+
 constexpr int SK = 256;                                  // K per streaming stage
 constexpr int S_A_BYTES = 4 * 64 * 128;                  // 32 KB: 4 chunks x 64 rows x 128 B
 constexpr int S_B_BYTES = 64 * SK * 2;                   // 32 KB
@@ -707,6 +742,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       const uint64_t pol_b = l2_policy(p.hint_b);
+      bool lora_waited = p.lora_ready == nullptr;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int mb, nb;
         tile_coords(t, p, mb, nb);
@@ -728,6 +764,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const int cb = td.chunk_begin;
           const int cc = td.chunk_count;
           const int m0 = mb * BM;
+          if (!lora_waited && cc > 0) {            // the base K loop ran beside the shrink
+            wait_lora_ready(p);
+            lora_ready_ticket(p);
+            lora_waited = true;
+          }
           for (int ls = 0; ls * 4 < cc; ++ls) {
             const int nq = min(4, cc - ls * 4);
             mbar_wait(&empty_bar[s], ph ^ 1);
@@ -741,6 +782,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       }
+      if (!lora_waited) lora_ready_ticket(p);
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc_base = make_idesc_bf16(BM, TBN, false, !kBwd);
@@ -1351,6 +1393,7 @@ struct ShrinkParams {
   int max_chunks;         // gridDim.y
   int* ticket;            // [items] arrival counters (zero between launches)
   int kb_chunk;           // k-blocks per chunk (a per-context constant: the chunking must not vary)
+  int* done_ctr = nullptr;  // overlap mode: every CTA adds 1 after its writes (the GEMM waits on it)
 };
 
 __host__ __device__ inline int shrink_chunks(int K, int kb_chunk) {
@@ -1381,7 +1424,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
   const bool whole = gridDim.y == 1;
   const int c0 = whole ? 0 : (int)blockIdx.y;
   const int c1 = whole ? nchk : c0 + 1;
-  if (c0 >= nchk) return;   // (gradient launches mix two K's; uniform exit before any barrier)
+  if (c0 >= nchk) {         // (gradient launches mix two K's; uniform exit before any barrier)
+    if (p.done_ctr && threadIdx.x == 0) atomicAdd(p.done_ctr, 1);
+    return;
+  }
   const int b_bytes = npad * BK * 2;
   const int stage_bytes = A_STAGE_BYTES + b_bytes;
   const int SHRINK_STAGES = min(SHRINK_MAX_STAGES, (SHRINK_SMEM - 2048) / stage_bytes);
@@ -1584,6 +1630,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
     }
   }
   __syncthreads();
+  if (p.done_ctr && threadIdx.x == 0) {
+    __threadfence();                 // this CTA's A_lora writes before the arrival (cumulative)
+    atomicAdd(p.done_ctr, 1);
+  }
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 256);

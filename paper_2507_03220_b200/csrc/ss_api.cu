@@ -102,6 +102,8 @@ struct ss_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int side_shrink = 1;
+  int lora_overlap = 1;          // streaming GEMM overlaps the side-stream shrink (see launch_batch)
+  int* sync_ctr = nullptr;       // [2] shrink-done counter + GEMM ticket (zero between dispatches)
   struct HostSlot {
     void* in = nullptr;
     void* out = nullptr;
@@ -900,6 +902,17 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   };
 
   CUtensorMap tmAL = L.tm_w_fwd;  // (unused without LoRA)
+  // one CTA per slab walking every K chunk when there are enough slabs to fill the GPU and the
+  // ranks fit the register sums; else one CTA per (slab, chunk). Same sums either way.
+  const bool whole = B.shrink_chunks_ == 1 ||
+                     (B.part_ld <= 64 && (ctx->shrink_mode == 1 || (ctx->shrink_mode == 0 && B.n_items >= ctx->num_sms)));
+  const int shrink_ctas = any_lora ? B.n_items * (whole ? 1 : B.shrink_chunks_) : 0;
+  const bool side = any_lora && MX > 0 && B.shrink_indep && ctx->side_shrink && !ctx->profiling;
+  // Overlap (streaming kernel): the GEMM does not wait for the side-stream shrink; its producer
+  // waits on the shrink's completion counter right before the LoRA stages. Only when the
+  // shrink's CTAs (2 per SM) and the GEMM's fit on the GPU together, so neither can starve.
+  const int gemm_ctas = (int)std::min<int64_t>((int64_t)num_m * ((N + 63) / 64), ctx->num_sms);
+  const bool overlap = side && B.stream && ctx->lora_overlap && gemm_ctas + (shrink_ctas + 1) / 2 <= ctx->num_sms;
   auto launch_shrink = [&](cudaStream_t st) -> int {
     // the streaming kernel (<= 64 rows) reads the LoRA operand through a 64-row box too
     rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, B.stream ? 64 : BM);
@@ -920,10 +933,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     sp.ticket = ctx->shrink_ticket;
     const int pi = prof_begin(ctx, st, SS_KERNEL_SHRINK, B.shrink_flops, B.shrink_bytes);
     sp.K2 = K;
-    // one CTA per slab walking every K chunk when there are enough slabs to fill the GPU and the
-    // ranks fit the register sums; else one CTA per (slab, chunk). Same sums either way.
-    const bool whole = B.shrink_chunks_ == 1 ||
-                       (B.part_ld <= 64 && (ctx->shrink_mode == 1 || (ctx->shrink_mode == 0 && B.n_items >= ctx->num_sms)));
+    sp.done_ctr = overlap ? ctx->sync_ctr : nullptr;
     CK(launch_k(ctx, lora_shrink_kernel, dim3(B.n_items, whole ? 1 : B.shrink_chunks_), GEMM_THREADS, SHRINK_SMEM,
                 st, bwd ? L.tm_b : L.tm_at, bwd ? L.tm_b : L.tm_at, sp));
     prof_end(ctx, st, pi);
@@ -935,13 +945,13 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   // The shrink reads the client rows in place (no packed rows) -> it runs on the side stream
   // beside the gather: fork after everything queued so far (the previous dispatch's GEMM reads
   // the LoRA operand the shrink rewrites), join before the GEMM.
-  if (any_lora && MX > 0 && B.shrink_indep && ctx->side_shrink && !ctx->profiling) {
+  if (side) {
     CK(cudaEventRecord(ctx->ev_fork, stream));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     if ((rc = launch_shrink(ctx->side))) return rc;
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
     if ((rc = launch_gather())) return rc;
-    CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));
+    if (!overlap) CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));
   } else {
     if (MX > 0 && (rc = launch_gather())) return rc;
     if (any_lora && (rc = launch_shrink(stream))) return rc;
@@ -972,6 +982,8 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   gpm.hint_b = (ctx->l2_hints && gpm.group_n > 0) ? 2 : 0;
   gpm.hint_out = ctx->l2_hints ? 1 : 0;
   gpm.a_bytes = B.a_rows64 ? A_STAGE_BYTES / 2 : A_STAGE_BYTES;
+  gpm.lora_ready = overlap ? ctx->sync_ctr : nullptr;
+  gpm.lora_expect = overlap ? shrink_ctas : 0;
   gpm.has_bias = (pass_kind == SS_PASS_FORWARD && L.bias) ? 1 : 0;
   gpm.any_lora = any_lora ? 1 : 0;
   gpm.ia3_in_epilogue = (pass_kind != SS_PASS_BACKWARD) ? 1 : 0;
@@ -1020,6 +1032,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   prof_end(ctx, stream, pg);
   CK(cudaGetLastError());
   ctx->launches++;
+  if (overlap) CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));   // join the side stream
   CK(cudaEventRecord(ctx->compute_done, stream));
   ctx->any_compute = true;
   return SS_OK;
@@ -1122,7 +1135,9 @@ int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out) {
       cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMalloc(&ctx->sync_ctr, 2 * sizeof(int)) != cudaSuccess ||
+      cudaMemset(ctx->sync_ctr, 0, 2 * sizeof(int)) != cudaSuccess) {
     delete ctx;
     return SS_E_CUDA;
   }
@@ -1195,6 +1210,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   cudaStreamDestroy(ctx->h2d);
   cudaStreamDestroy(ctx->d2h);
   cudaStreamDestroy(ctx->side);
+  cudaFree(ctx->sync_ctr);
   cudaEventDestroy(ctx->ev_fork);
   cudaEventDestroy(ctx->ev_join);
   delete ctx;
@@ -1268,6 +1284,10 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_remote")) {
     ctx->force_remote = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "lora_overlap")) {
+    ctx->lora_overlap = value ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "side_shrink")) {
