@@ -32,8 +32,7 @@ ctx = ctypes.c_void_p()
 L.check(None, lib.ss_ctx_create(0, 0, 1, ctypes.byref(ctx)))
 dev = torch.device("cuda:0")
 stream = torch.cuda.current_stream().cuda_stream
-defaults = {"raster": 0, "group_n": 0, "l2_budget_mb": 48, "l2_hints": 1, "group_m": 16,
-            "pf_depth": 0, "a_rows64": 1, "prefetch_mb": 0}
+defaults = {"raster": 0, "group_n": 0, "l2_budget_mb": 48, "l2_hints": 1, "group_m": 16, "a_rows64": 1}
 for li, (name, din, dout, M, pk) in enumerate(SHAPES):
     W = torch.randn(din, dout, device=dev, dtype=torch.bfloat16)
     L.check(ctx, lib.ss_load_layer(ctx, li, 4, din, dout, W.data_ptr(), dout, None, L.SS_MEM_DEVICE | L.SS_DT_BF16))
