@@ -256,6 +256,9 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   shrink_mode (0)     LoRA shrink: 0 auto, 1 one CTA per slab, 2 one CTA per (slab, K chunk)
  *   shrink_kb_chunk     k-blocks (of 64) per fixed K chunk of the shrink
  *   pdl (0)             programmatic dependent launch between a dispatch's kernels (no gain measured)
+ *   zc_cache (1)        zero-copy host dispatches that recur with the same segment array reuse their
+ *                       built routing tables (invalidated by workspace growth, adapter moves, any
+ *                       option change)
  *   zero_copy_bytes (4 MiB)  ss_compute_batch_host dispatches up to this size: no copies (UVA)
  *   force_remote (0)    testing: route every segment as if it lived on a peer GPU
  *   pipeline_rows, pipeline_bytes  sub-batch size of ss_compute_batch_host */

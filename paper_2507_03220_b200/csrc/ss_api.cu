@@ -73,6 +73,7 @@ struct Staging {
 
 }  // namespace
 
+namespace { struct ZcPlan; }
 struct ss_ctx {
   int device = 0, tp_rank = 0, tp_size = 1, num_sms = 148;
   std::string err;
@@ -159,6 +160,11 @@ struct ss_ctx {
   // Plans (ss_plan_*) cache routing tables that embed workspace and adapter pointers; these
   // counters tell a plan to rebuild itself after the workspace grew or an adapter moved.
   uint64_t ws_epoch = 0, ad_epoch = 0;
+  // zero-copy host dispatches that recur (decode: clients reuse their buffers every step) reuse
+  // their routing tables: keyed by the segment array's bytes, valid while the epochs, the
+  // options and the reply slot are unchanged (see ss_compute_batch_host)
+  std::map<uint64_t, ZcPlan*> zc_cache;
+  int zc_cache_on = 1;
   // in-stream profiling
   bool profiling = false;
   std::vector<ProfRec> prof;       // pending event pairs
@@ -465,6 +471,42 @@ struct Built {
   double gather_bytes = 0, shrink_flops = 0, shrink_bytes = 0, gemm_flops = 0, gemm_bytes = 0;
   uint64_t ws_epoch = 0, ad_epoch = 0;
 };
+
+// A cached zero-copy dispatch: its built tables and row-copy ops in plan-owned device memory.
+struct ZcPlan {
+  int pass_kind = 0, block = 0, role = 0;
+  std::vector<ss_seg> segs;
+  std::vector<int32_t> status;
+  Built b;
+  void* out = nullptr;
+  void* base = nullptr;
+  char* dev = nullptr;
+  size_t ops_off = 0;
+  int n_ops = 0;
+  int64_t copy_rows = 0;
+};
+
+static void zc_cache_clear(ss_ctx* ctx) {
+  if (ctx->zc_cache.empty()) return;
+  cudaDeviceSynchronize();   // (host dispatches synchronise on return: nothing still reads them)
+  for (auto& kv : ctx->zc_cache) {
+    cudaFree(kv.second->dev);
+    delete kv.second;
+  }
+  ctx->zc_cache.clear();
+}
+
+static uint64_t zc_key(int pass_kind, int block, int role, int n_seg, const ss_seg* segs) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+  };
+  const int hdr[4] = {pass_kind, block, role, n_seg};
+  mix(hdr, sizeof(hdr));
+  mix(segs, sizeof(ss_seg) * (size_t)n_seg);
+  return h;
+}
 
 // `local_buffers`: every pointer is a staging slice this context allocated on its own device
 // (host pipelines), so the per-pointer peer-GPU query is skipped.
@@ -1168,6 +1210,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   if (!ctx) return SS_E_ARG;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  zc_cache_clear(ctx);
   for (auto& kv : ctx->layers) {
     Layer& L = kv.second;
     cudaFree(L.W);
@@ -1219,6 +1262,11 @@ int ss_ctx_destroy(ss_ctx* ctx) {
 
 int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!ctx || !key) return SS_E_ARG;
+  zc_cache_clear(ctx);   // options shape the built tables
+  if (!strcmp(key, "zc_cache")) {
+    ctx->zc_cache_on = value ? 1 : 0;
+    return SS_OK;
+  }
   if (!strcmp(key, "shrink_mode")) {
     if (value < 0 || value > 2) return fail(ctx, SS_E_ARG, "shrink_mode must be 0 (auto), 1 (whole) or 2 (split)");
     ctx->shrink_mode = (int)value;
@@ -2010,6 +2058,25 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     int rc = SS_OK;
     if (hs.out_cap < out_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.out), hs.out_cap, out_need, false))) return rc;
     if (hs.base_cap < base_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.base), hs.base_cap, base_need, false))) return rc;
+    const uint64_t key = ctx->zc_cache_on ? zc_key(pass_kind, block, role, n_seg, segs) : 0;
+    if (ctx->zc_cache_on) {
+      auto it = ctx->zc_cache.find(key);
+      ZcPlan* z = it == ctx->zc_cache.end() ? nullptr : it->second;
+      if (z && z->pass_kind == pass_kind && z->block == block && z->role == role && z->segs.size() == (size_t)n_seg &&
+          !memcmp(z->segs.data(), segs, sizeof(ss_seg) * (size_t)n_seg) && z->b.ws_epoch == ctx->ws_epoch &&
+          z->b.ad_epoch == ctx->ad_epoch && z->out == hs.out && z->base == hs.base) {
+        // the same dispatch as before (same buffers, rows, clients): launch its tables as built
+        for (int i = 0; i < n_seg; ++i) seg_status[i] = z->status[i];
+        CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
+        if ((rc = launch_batch(ctx, z->b, z->dev, stream))) return rc;
+        copy_rows_kernel<<<(int)std::min<int64_t>((z->copy_rows + 7) / 8, (int64_t)ctx->num_sms * 8), 256, 0, stream>>>(
+            reinterpret_cast<const RowCopy*>(z->dev + z->ops_off), z->n_ops, (int)z->copy_rows);
+        CK(cudaGetLastError());
+        ctx->launches++;
+        CK(cudaStreamSynchronize(stream));
+        return SS_OK;
+      }
+    }
     std::vector<ss_seg> cs;
     std::vector<RowCopy> ops;
     std::vector<int> op_seg;    // index into cs of each row copy
@@ -2063,6 +2130,37 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     ctx->launches++;
     CK(cudaEventRecord(stp->done, stream));
     stp->pending = true;
+    if (ctx->zc_cache_on) {
+      // keep this dispatch's tables for its next occurrence (a copy of the staged bytes)
+      if (ctx->zc_cache.size() >= 4096) zc_cache_clear(ctx);
+      ZcPlan* z = new ZcPlan();
+      const size_t total = ops_off + ops.size() * sizeof(RowCopy);
+      if (cudaMalloc(&z->dev, total) != cudaSuccess) {
+        cudaGetLastError();
+        delete z;
+      } else {
+        CK(cudaMemcpyAsync(z->dev, stp->dev, total, cudaMemcpyDeviceToDevice, stream));
+        z->pass_kind = pass_kind;
+        z->block = block;
+        z->role = role;
+        z->segs.assign(segs, segs + n_seg);
+        z->status.assign(seg_status, seg_status + n_seg);
+        z->b = std::move(b);
+        z->b.blob.clear();
+        z->b.blob.shrink_to_fit();
+        z->out = hs.out;
+        z->base = hs.base;
+        z->ops_off = ops_off;
+        z->n_ops = (int)ops.size();
+        z->copy_rows = copy_rows;
+        auto it = ctx->zc_cache.find(key);
+        if (it != ctx->zc_cache.end()) {
+          cudaFree(it->second->dev);   // (stale: an epoch or the slot changed)
+          delete it->second;
+        }
+        ctx->zc_cache[key] = z;
+      }
+    }
     CK(cudaStreamSynchronize(stream));   // replies are in the caller's host buffers on return
     return SS_OK;
   }

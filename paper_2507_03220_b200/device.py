@@ -319,7 +319,10 @@ class SsContext:
                      stream: torch.cuda.Stream | None = None) -> list[int]:
         """One dispatch over HOST (pinned) tensors: ss_compute_batch_host pipelines the H2D
         copies, kernels and D2H copies natively and returns when the replies are in place."""
-        table = SegmentTable(segs, self._seg_cache)
+        return self.compute_host_table(pass_kind, block, role, SegmentTable(segs, self._seg_cache), stream)
+
+    def compute_host_table(self, pass_kind: int, block: int, role: int, table: SegmentTable,
+                           stream: torch.cuda.Stream | None = None) -> list[int]:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         check(self.h, self.lib.ss_compute_batch_host(self.h, int(pass_kind), int(block), int(role), table.n,
                                                      table.arr, ctypes.c_void_p(s.cuda_stream), table.status))

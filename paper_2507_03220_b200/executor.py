@@ -33,7 +33,7 @@ import torch
 
 from . import ledger as ledger_mod
 from .config import Role, addr_key
-from .device import Seg, SsContext
+from .device import Seg, SegmentTable, SsContext
 from .errors import ConfigError, ProtocolError
 from .protocol import (COMPUTE_PASSES, PASS_BACKWARD, PASS_FORWARD, PASS_NOISE_EFFECT,
                        Envelope, error_envelope)
@@ -193,6 +193,10 @@ class GpuBaseExecutor:
         # pinned-host checks of client payload / reply tensors, per live tensor object:
         # id -> (weakref, info) (tensors compare elementwise, so they cannot be dict keys)
         self._host_info: dict[int, tuple] = {}
+        # recurring host dispatches (decode: the same client buffers every step) -> their packed
+        # segment table; see _host_memo_get
+        self._host_memo: dict[tuple, tuple] = {}
+        self._fused_ver = 0
         self._dev_staging: dict = {}
         self._host_replies: list = []
         self.last_event: torch.cuda.Event | None = None
@@ -240,6 +244,7 @@ class GpuBaseExecutor:
         with self._cond:
             self._clients.pop(client_id, None)
             self._cond.notify_all()
+        self._host_memo.clear()   # (drops the memo's references to the client's buffers)
 
     def layer_dims(self, block: int, role: int) -> tuple[int, int]:
         return self._dims[(int(block), int(role))]
@@ -265,7 +270,9 @@ class GpuBaseExecutor:
                 a, b = by_key_lora[key]
                 lo = (a, b, float(adapter.alpha) / float(adapter.rank))
             self.ctx.set_adapter(client_id, key[0], key[1], lora=lo, ia3=by_key_ia3.get(key))
-            self._fused[client_id].add(key)
+            if key not in self._fused[client_id]:
+                self._fused[client_id].add(key)
+                self._fused_ver += 1
         self._sync_ledger()
 
     refresh_adapter = register_adapter
@@ -273,6 +280,8 @@ class GpuBaseExecutor:
     def deregister_adapter(self, client_id: int) -> None:
         self.ctx.clear_adapter(client_id)
         self._fused.pop(client_id, None)
+        self._fused_ver += 1
+        self._host_memo.clear()
         self._sync_ledger()
 
     def fused_addresses(self, client_id: int) -> set:
@@ -386,9 +395,10 @@ class GpuBaseExecutor:
         if not good:
             return results
         stream = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
-        if self._all_pinned_host(envelopes, good, out_w):
+        memo = self._host_memo_get(pass_kind, key, envelopes, good)
+        if (memo is not None and memo[2] is not None) or self._all_pinned_host(envelopes, good, out_w):
             with torch.cuda.device(self.device):
-                status = self._pipelined_host(pass_kind, key, envelopes, good, out_w, stream)
+                status = self._pipelined_host(pass_kind, key, envelopes, good, out_w, stream, memo)
             for j, i in enumerate(good):
                 results[i] = (ProtocolError(f"executor rejected segment (status {status[j]}) for layer {addr}")
                               if status[j] != _lib.SS_SEG_OK else envelopes[i].reply_to)
@@ -452,7 +462,31 @@ class GpuBaseExecutor:
                 return False
         return True
 
-    def _pipelined_host(self, pass_kind, key, envelopes, good, out_w, stream) -> list[int]:
+    def _host_memo_get(self, pass_kind, key, envelopes, good):
+        """(signature, fingerprint, table) of a host dispatch identical to an earlier one — the
+        same payload / reply tensor objects (held by the memo, so their ids stay theirs), the
+        same clients, storage and shapes, and no adapter-set change since — else (signature,
+        fingerprint, None). Decode clients send from the same buffers every step, and the
+        per-envelope checks and segment packing cost more than the dispatch's kernels."""
+        if self.save_activations:
+            return None
+        sig = [pass_kind, key, self._fused_ver]
+        fp = []
+        for i in good:
+            e = envelopes[i]
+            p, r = e.payload, getattr(e, "reply_to", None)
+            if not isinstance(p, torch.Tensor) or not isinstance(r, torch.Tensor) or \
+                    getattr(e, "base_to", None) is not None:
+                return None
+            sig += (id(p), id(r), e.client_id)
+            fp += (p.data_ptr(), r.data_ptr(), p.shape, r.shape)
+        sig, fp = tuple(sig), tuple(fp)
+        hit = self._host_memo.get(sig)
+        if hit is not None and hit[1] == fp:
+            return sig, fp, hit[2]
+        return sig, fp, None
+
+    def _pipelined_host(self, pass_kind, key, envelopes, good, out_w, stream, memo=None) -> list[int]:
         """Host clients (pinned payload + pinned reply buffer): one ss_compute_batch_host call.
         The library splits the dispatch into row sub-batches so the H2D copy of sub-batch j+1
         and the D2H copy of j-1 overlap the kernels of j (its own copy streams and device
@@ -463,14 +497,21 @@ class GpuBaseExecutor:
             self.ctx.set_option("pipeline_rows", knobs[0])
             self.ctx.set_option("pipeline_bytes", knobs[1])
             self._pipeline_knobs = knobs
+        self.last_event = None
+        if memo is not None and memo[2] is not None:
+            return self.ctx.compute_host_table(pass_kind, key[0], key[1], memo[2], stream)
         fused = self._fused
         in_w = envelopes[good[0]].width
         # _all_pinned_host verified every payload / reply is page-locked: tell the library
         segs = [Seg(client_id=envelopes[i].client_id, src=envelopes[i].payload, dst=envelopes[i].reply_to,
                     width=in_w, adapter=key in fused.get(envelopes[i].client_id, ()), pinned=True)
                 for i in good]
-        status = self.ctx.compute_host(pass_kind, key[0], key[1], segs, stream)
-        self.last_event = None
+        table = SegmentTable(segs, self.ctx._seg_cache)
+        status = self.ctx.compute_host_table(pass_kind, key[0], key[1], table, stream)
+        if memo is not None:
+            if len(self._host_memo) > 2048:
+                self._host_memo.clear()
+            self._host_memo[memo[0]] = (table._keep, memo[1], table)   # (table holds the tensors)
         return status
 
     # -- staging helpers --------------------------------------------------------------------

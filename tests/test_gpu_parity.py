@@ -734,6 +734,54 @@ def test_in_place_host_handoff_bitwise(zero_copy):
             assert torch.equal(got[c], dev[c].cpu()), (pass_kind, c)
 
 
+def test_zero_copy_dispatch_cache_follows_data_and_adapters():
+    """A zero-copy host dispatch that recurs (same client buffers and rows, as in decode) reuses
+    its packed segment table (executor memo) and its routing tables (library dispatch cache);
+    it must still read each call's new request rows, follow an adapter refresh (new values,
+    new rank) and a client gaining an adapter, and equal the uncached result bitwise."""
+    d_in, d_out = 512, 768
+    w, b = O.layer_params(8, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)})
+    ex.ctx.set_option("zero_copy_bytes", 1 << 30)
+    _mixed_clients(ex, d_in, d_out, seed=8, role=O.V)
+    counts = [2, 1, 2, 2, 3, 2, 1]
+    hosts = [torch.empty(t, d_in, dtype=torch.bfloat16).pin_memory() for t in counts]
+    replies = [torch.empty(t, d_out, dtype=torch.bfloat16).pin_memory() for t in counts]
+    gen = torch.Generator().manual_seed(3)
+    rid = [300]
+
+    def run():
+        out = []
+        for cache in (1, 0):
+            ex.ctx.set_option("zc_cache", cache)
+            for _ in range(2):                        # the second call of each is a cache hit
+                rid[0] += 1
+                ex._compute_batch(0, [_env(c, rid[0], 0, O.V, 0, h, reply_to=r)
+                                      for c, (h, r) in enumerate(zip(hosts, replies))])
+            out.append([r.clone() for r in replies])
+        for c in range(len(counts)):
+            assert torch.equal(out[0][c], out[1][c]), c
+        return out[0]
+
+    ex.ctx.set_option("zc_cache", 1)
+    seen = []
+    for step in range(3):
+        for h in hosts:
+            h.copy_(torch.randn(h.shape, generator=gen).to(torch.bfloat16))
+        if step == 2:     # refresh client 0's LoRA (new values and rank); client 1 gains an IA3
+            ad = O.lora_params(99, 0, 0, O.V, d_in, d_out, 32, 64.0)
+            ex.register_adapter(0, _Adapter(lora={_addr(0, O.V): (ad.a, ad.b)}, alpha=64.0, rank=32))
+            ex.register_adapter(1, _Adapter(ia3={_addr(0, O.V): O.ia3_params(99, 1, 0, O.V, d_out).ia3}))
+        got = run()
+        dev = ex._compute_batch(0, [_env(c, 900 + 10 * step + c, 0, O.V, 0, h.to(ex.device))
+                                    for c, h in enumerate(hosts)])
+        for c in range(len(counts)):
+            assert torch.equal(got[c], dev[c].cpu()), (step, c)
+        seen.append(got[0])
+    assert not torch.equal(seen[0], seen[1])
+    assert len(ex._host_memo) >= 1
+
+
 @pytest.mark.parametrize("zero_copy", [0, 1 << 30])
 def test_host_dispatch_rejected_segment_untouched(zero_copy):
     """ss_compute_batch_host (both the pipelined and the zero-copy path): a segment the library
