@@ -246,6 +246,8 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   side_shrink (1)     a LoRA shrink that reads no packed rows runs on a side stream beside the gather
  *   lora_overlap (1)    the weight-streaming kernel runs beside that shrink and waits on its
  *                       completion counter only before its LoRA k-blocks (when both fit the SMs)
+ *                       (default 0 under tools that serialise launches: CUDA_INJECTION64_PATH
+ *                       set, i.e. ncu / compute-sanitizer, or CUDA_LAUNCH_BLOCKING=1)
  *   cluster4 (0)        256x256 pair tiles as 4-CTA clusters sharing B by multicast (measured
  *                       35 % slower in the step: off)
  *   tile_n (0)          force the single-CTA tile width 64 / 128 / 256 (0 auto)

@@ -1159,6 +1159,13 @@ int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out) {
     delete ctx;
     return SS_E_UNSUPPORTED;  // sm_100a only
   }
+  // The GEMM / shrink overlap needs both kernels resident at once; tools that serialise kernel
+  // launches (ncu, compute-sanitizer, CUDA_LAUNCH_BLOCKING) would leave the GEMM waiting.
+  {
+    const char* inj = getenv("CUDA_INJECTION64_PATH");
+    const char* blk = getenv("CUDA_LAUNCH_BLOCKING");
+    if ((inj && *inj) || (blk && *blk == '1')) ctx->lora_overlap = 0;
+  }
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
