@@ -92,6 +92,9 @@ struct GemmParams {
   // stage. lora_ready[1] counts the CTAs past that point; the last one re-arms both counters.
   int* lora_ready = nullptr;
   int lora_expect = 0;
+  // Streaming kernel launched with programmatic dependent launch behind the gather / shrink:
+  // the producer issues the first stages' W loads, then griddepcontrol.wait, then their A loads.
+  int pdl_early = 0;
   int has_bias;
   int any_lora;
   int ia3_in_epilogue;              // forward: scale output columns by IA3
@@ -730,7 +733,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();
+  if (!p.pdl_early) pdl_wait();   // (else the producer waits, after its first W loads)
   pdl_trigger();
 
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
@@ -750,7 +753,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const CUtensorMap* tmA = p.tmaps + td.amap;
         const int n0 = nb * TBN;
         tensormap_acquire(tmA);
-        for (int st = 0; st < nst; ++st) {
+        int st0 = 0;
+        if (p.pdl_early && t == (int)blockIdx.x) {
+          // first tile: W of the first stages streams in while the gather finishes (the ring
+          // is empty, s == 0); A (the gathered rows) only after griddepcontrol.wait
+          const int pre = min(S_STAGES, nst);
+          for (int st = 0; st < pre; ++st) {
+            mbar_expect_tx(&full_bar[st], S_STAGE);
+            uint8_t* b = smem + st * S_STAGE + S_A_BYTES;
+            if (kBwd) tma_load_3d(b, &tmB, &full_bar[st], 0, n0, st * 4);
+            else load_a_or_b(b, &tmB, &full_bar[st], n0, st * SK, p.hint_b, pol_b);
+          }
+          pdl_wait();
+          for (int st = 0; st < pre; ++st)
+            tma_load_3d(smem + st * S_STAGE, tmA, &full_bar[st], 0, td.arow, st * 4);
+          st0 = pre;
+          s = pre == S_STAGES ? 0 : pre;
+          ph = pre == S_STAGES ? 1 : 0;
+        }
+        for (int st = st0; st < nst; ++st) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           mbar_expect_tx(&full_bar[s], S_STAGE);
           uint8_t* a = smem + s * S_STAGE;

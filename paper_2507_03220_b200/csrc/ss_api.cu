@@ -103,7 +103,8 @@ struct ss_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int side_shrink = 1;
-  int lora_overlap = 1;          // streaming GEMM overlaps the side-stream shrink (see launch_batch)
+  int lora_overlap = 1;
+  int stream_pdl = 1;            // streaming GEMM launched early behind the gather (see launch_batch)          // streaming GEMM overlaps the side-stream shrink (see launch_batch)
   int* sync_ctr = nullptr;       // [2] shrink-done counter + GEMM ticket (zero between dispatches)
   struct HostSlot {
     void* in = nullptr;
@@ -889,8 +890,8 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
 // prologue while the previous kernel on the stream drains; it waits (griddepcontrol.wait) before
 // touching global data. Captured into graphs as programmatic edges.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_k(const ss_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                     cudaStream_t st, Args... args) {
+cudaError_t launch_kp(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -898,10 +899,15 @@ cudaError_t launch_k(const ss_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl && !ctx->profiling ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(const ss_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args... args) {
+  return launch_kp(ctx->pdl && !ctx->profiling, kernel, grid, block, smem, st, args...);
 }
 
 // Launch the kernels of a built batch whose tables are at device address `dv` (stream-ordered
@@ -1026,6 +1032,10 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   gpm.a_bytes = B.a_rows64 ? A_STAGE_BYTES / 2 : A_STAGE_BYTES;
   gpm.lora_ready = overlap ? ctx->sync_ctr : nullptr;
   gpm.lora_expect = overlap ? shrink_ctas : 0;
+  // the streaming GEMM starts behind the kernel before it (gather, or the main-stream shrink)
+  // and streams its first W stages meanwhile; not across the side-stream join event
+  const bool early = B.stream && ctx->stream_pdl && !ctx->profiling && MX > 0 && !(side && !overlap);
+  gpm.pdl_early = early ? 1 : 0;
   gpm.has_bias = (pass_kind == SS_PASS_FORWARD && L.bias) ? 1 : 0;
   gpm.any_lora = any_lora ? 1 : 0;
   gpm.ia3_in_epilogue = (pass_kind != SS_PASS_BACKWARD) ? 1 : 0;
@@ -1042,9 +1052,11 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   const int pg = prof_begin(ctx, stream, SS_KERNEL_GEMM, B.gemm_flops, B.gemm_bytes);
   if (B.stream) {
     if (bwd)
-      CK(launch_k(ctx, seg_gemm_stream_kernel<true>, grid, GEMM_THREADS, STREAM_SMEM, stream, L.tm_w_bwd_s, tmAL, tmBP, gpm));
+      CK(launch_kp(early || (ctx->pdl && !ctx->profiling), seg_gemm_stream_kernel<true>, grid, GEMM_THREADS,
+                   STREAM_SMEM, stream, L.tm_w_bwd_s, tmAL, tmBP, gpm));
     else
-      CK(launch_k(ctx, seg_gemm_stream_kernel<false>, grid, GEMM_THREADS, STREAM_SMEM, stream, L.tm_w_fwd_s, tmAL, tmBP, gpm));
+      CK(launch_kp(early || (ctx->pdl && !ctx->profiling), seg_gemm_stream_kernel<false>, grid, GEMM_THREADS,
+                   STREAM_SMEM, stream, L.tm_w_fwd_s, tmAL, tmBP, gpm));
   } else if (pair && pn == 256 && ctx->cluster4 && num_m >= 2) {
     const int ng = (int)std::min<int64_t>((int64_t)((num_m + 1) / 2) * gpm.num_n_tiles, ctx->num_sms / 4);
     if (bwd)
@@ -1339,6 +1351,10 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_remote")) {
     ctx->force_remote = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "stream_pdl")) {
+    ctx->stream_pdl = value ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "lora_overlap")) {

@@ -630,7 +630,8 @@ def test_decode_size_dispatch_64_row_box_bitwise():
     """A dispatch of <= 64 packed rows runs the weight-streaming kernel (4 k-blocks of A and W
     per TMA operation, 64-row A boxes whose MMA rows 64-127 are never stored) or, with it off,
     the single-CTA kernel with a 64- or 128-row A box; the streaming kernel either overlaps the
-    side-stream LoRA shrink (waiting on its completion counter) or starts after it. All must
+    side-stream LoRA shrink (waiting on its completion counter) or starts after it, and is
+    launched early behind the gather (W streaming before griddepcontrol.wait) or not. All must
     give the same bits, equal to
     the same clients' rows inside a prefill-size dispatch (batching invisibility at decode
     sizes), forward and backward, every adapter kind."""
@@ -643,10 +644,11 @@ def test_decode_size_dispatch_64_row_box_bitwise():
     for pass_kind, width in ((0, d_in), (1, d_out)):
         xs = [torch.randn(t, width, device=dev).to(torch.bfloat16) for t in counts]
         outs = []
-        for stream, box64, overlap in ((1, 1, 1), (1, 1, 0), (0, 1, 1), (0, 0, 1)):
+        for stream, box64, overlap, pdl in ((1, 1, 1, 1), (1, 1, 0, 1), (1, 1, 1, 0), (0, 1, 1, 1), (0, 0, 1, 1)):
             ex.ctx.set_option("stream_gemm", stream)
             ex.ctx.set_option("a_rows64", box64)
             ex.ctx.set_option("lora_overlap", overlap)
+            ex.ctx.set_option("stream_pdl", pdl)
             outs.append(ex._compute_batch(pass_kind, [_env(c, 110 + 4 * pass_kind + len(outs), 0, O.K, pass_kind, x)
                                                       for c, x in enumerate(xs)]))
         ex.ctx.set_option("stream_gemm", 1)
@@ -655,7 +657,7 @@ def test_decode_size_dispatch_64_row_box_bitwise():
         big = ex._compute_batch(pass_kind, [_env(c, 120 + pass_kind, 0, O.K, pass_kind, x) for c, x in enumerate(xs)] +
                                 [_env(1, 122 + pass_kind, 0, O.K, pass_kind, filler)])
         for c in range(len(xs)):
-            for k in (1, 2, 3):
+            for k in (1, 2, 3, 4):
                 assert torch.equal(outs[0][c], outs[k][c]), (pass_kind, k, c)
             assert torch.equal(outs[0][c], big[c]), (pass_kind, c)
 
