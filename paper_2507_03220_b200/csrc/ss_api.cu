@@ -166,6 +166,7 @@ struct ss_ctx {
   // options and the reply slot are unchanged (see ss_compute_batch_host)
   std::map<uint64_t, ZcPlan*> zc_cache;
   int zc_cache_on = 1;
+  uint64_t opt_epoch = 0;        // bumped by every ss_set_option: cached tables depend on options
   // in-stream profiling
   bool profiling = false;
   std::vector<ProfRec> prof;       // pending event pairs
@@ -479,6 +480,7 @@ struct ZcPlan {
   std::vector<ss_seg> segs;
   std::vector<int32_t> status;
   Built b;
+  uint64_t opt_epoch = 0;
   void* out = nullptr;
   void* base = nullptr;
   char* dev = nullptr;
@@ -1281,7 +1283,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
 
 int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!ctx || !key) return SS_E_ARG;
-  zc_cache_clear(ctx);   // options shape the built tables
+  ctx->opt_epoch++;   // options shape the built tables: cached dispatches rebuild
   if (!strcmp(key, "zc_cache")) {
     ctx->zc_cache_on = value ? 1 : 0;
     return SS_OK;
@@ -2087,7 +2089,8 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
       ZcPlan* z = it == ctx->zc_cache.end() ? nullptr : it->second;
       if (z && z->pass_kind == pass_kind && z->block == block && z->role == role && z->segs.size() == (size_t)n_seg &&
           !memcmp(z->segs.data(), segs, sizeof(ss_seg) * (size_t)n_seg) && z->b.ws_epoch == ctx->ws_epoch &&
-          z->b.ad_epoch == ctx->ad_epoch && z->out == hs.out && z->base == hs.base) {
+          z->b.ad_epoch == ctx->ad_epoch && z->opt_epoch == ctx->opt_epoch && z->out == hs.out &&
+          z->base == hs.base) {
         // the same dispatch as before (same buffers, rows, clients): launch its tables as built
         for (int i = 0; i < n_seg; ++i) seg_status[i] = z->status[i];
         CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
@@ -2168,6 +2171,7 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
         z->role = role;
         z->segs.assign(segs, segs + n_seg);
         z->status.assign(seg_status, seg_status + n_seg);
+        z->opt_epoch = ctx->opt_epoch;
         z->b = std::move(b);
         z->b.blob.clear();
         z->b.blob.shrink_to_fit();
