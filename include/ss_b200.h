@@ -258,6 +258,8 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   shrink_mode (0)     LoRA shrink: 0 auto, 1 one CTA per slab, 2 one CTA per (slab, K chunk)
  *   shrink_kb_chunk     k-blocks (of 64) per fixed K chunk of the shrink
  *   pdl (0)             programmatic dependent launch between a dispatch's kernels (no gain measured)
+ *   wide_decode (1)     dispatches of <= 64 rows whose 64-wide tiles would need more than one wave
+ *                       but whose 128-wide tiles fit one run the single-CTA kernel with 128-wide tiles
  *   stream_pdl (1)      the weight-streaming GEMM is launched with programmatic dependent launch
  *                       behind the gather: its first W stages stream before griddepcontrol.wait
  *   zc_cache (1)        zero-copy host dispatches that recur with the same segment array reuse their

@@ -104,7 +104,8 @@ struct ss_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int side_shrink = 1;
   int lora_overlap = 1;
-  int stream_pdl = 1;            // streaming GEMM launched early behind the gather (see launch_batch)          // streaming GEMM overlaps the side-stream shrink (see launch_batch)
+  int stream_pdl = 1;
+  int wide_decode = 1;           // decode-size dispatches: 128-wide single-CTA tiles when they fit one wave            // streaming GEMM launched early behind the gather (see launch_batch)          // streaming GEMM overlaps the side-stream shrink (see launch_batch)
   int* sync_ctr = nullptr;       // [2] shrink-done counter + GEMM ticket (zero between dispatches)
   struct HostSlot {
     void* in = nullptr;
@@ -780,7 +781,14 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   if (ctx->a_rows64 && !pair && num_m == 1 && direct_src.empty() && MX <= 64) {
     tiles[0].amap = (int32_t)tmaps.size();
     tmaps.emplace_back();
-    if (ctx->stream_gemm && K % 64 == 0 && !ctx->force_tbn) {
+    // At these sizes a tile's time is set by its K/16-long chain of dependent UMMAs, not by its
+    // bytes (profiles/r01_l2_and_decode.md): when 64-wide tiles would need more than one wave
+    // and 128-wide ones fit in one, the single-CTA kernel's 128-wide tiles finish in one chain
+    const bool one_wave_128 = ctx->wide_decode && (N + 63) / 64 > ctx->num_sms && (N + 127) / 128 <= ctx->num_sms;
+    if (one_wave_128 && !ctx->force_tbn) {
+      rc = encode_2d(ctx, &tmaps.back(), ctx->X, K, MX, ldx, 64, 64);
+      tbn = 128;
+    } else if (ctx->stream_gemm && K % 64 == 0 && !ctx->force_tbn) {
       rc = encode_kchunks(ctx, &tmaps.back(), ctx->X, K, MX, ldx, 64, 4);
       B.stream = true;
       tbn = 64;
@@ -1353,6 +1361,10 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   }
   if (!strcmp(key, "force_remote")) {
     ctx->force_remote = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "wide_decode")) {
+    ctx->wide_decode = value ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "stream_pdl")) {

@@ -662,6 +662,31 @@ def test_decode_size_dispatch_64_row_box_bitwise():
             assert torch.equal(outs[0][c], big[c]), (pass_kind, c)
 
 
+def test_decode_wide_layer_128_tiles_bitwise():
+    """A decode-size dispatch over a layer whose 64-wide tiles would need more than one wave
+    (N = 10240: 160 tiles on 148 SMs) runs 128-wide single-CTA tiles instead of the streaming
+    kernel; rows must be bitwise those of the streaming kernel and of a prefill-size dispatch."""
+    d_in, d_out = 512, 10240
+    w, b = O.layer_params(23, 0, O.FF_UP, d_in, d_out)
+    ex = _ex({(0, O.FF_UP): (w, b)})
+    rng = np.random.default_rng(23)
+    ex.register_adapter(3, _Adapter(ia3={_addr(0, O.FF_UP): O.ia3_params(23, 3, 0, O.FF_UP, d_out).ia3}))
+    counts = [2, 1, 2, 2]
+    dev = ex.device
+    xs = [torch.from_numpy(rng.standard_normal((t, d_in), dtype=np.float32)).to(dev).to(torch.bfloat16) for t in counts]
+    outs = []
+    for wide in (1, 0):
+        ex.ctx.set_option("wide_decode", wide)
+        outs.append(ex._compute_batch(0, [_env(c, 10 + wide * 10 + c, 0, O.FF_UP, 0, x) for c, x in enumerate(xs)]))
+    ex.ctx.set_option("wide_decode", 1)
+    filler = torch.randn(700, d_in, device=dev).to(torch.bfloat16)
+    big = ex._compute_batch(0, [_env(c, 40 + c, 0, O.FF_UP, 0, x) for c, x in enumerate(xs)] +
+                            [_env(9, 50, 0, O.FF_UP, 0, filler)])
+    for c in range(len(xs)):
+        assert torch.equal(outs[0][c], outs[1][c]), c
+        assert torch.equal(outs[0][c], big[c]), c
+
+
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs two GPUs (client buffers on a peer GPU)")
 def test_client_buffers_on_peer_gpu():
