@@ -62,3 +62,14 @@ def test_executor_fails_loudly_without_gpu():
     from paper_2507_03220_b200 import GpuBaseExecutor
     with pytest.raises(RuntimeError):
         GpuBaseExecutor({})
+
+
+def test_every_context_option_is_documented_in_the_header():
+    """ss_set_option keys accepted by the library (ss_api.cu) all appear in the header's option
+    list, so a binding author sees every knob and its default."""
+    src = open(os.path.join(ROOT, "paper_2507_03220_b200", "csrc", "ss_api.cu")).read()
+    keys = sorted(set(re.findall(r'strcmp\(key, "(\w+)"\)', src)))
+    header = open(os.path.join(ROOT, "include", "ss_b200.h")).read()
+    assert keys
+    missing = [k for k in keys if not re.search(r"[\s,(]" + k + r"[\s,(]", header)]
+    assert not missing, missing
