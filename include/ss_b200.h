@@ -224,6 +224,13 @@ SS_API int ss_memory_stats(const ss_ctx* ctx, int64_t* weight_bytes, int64_t* ad
 /* Number of kernels launched by this context since creation (evidence / bench counter). */
 SS_API int64_t ss_kernel_launches(const ss_ctx* ctx);
 
+/* Monotonic counter that moves whenever the context frees or moves a device buffer that
+ * launched kernels reference (workspace growth, LoRA pack growth, adapter rank / kind / scale
+ * change, layer unload). Kernels captured into a CUDA graph bake those addresses: a graph
+ * captured at epoch E must not be replayed once ss_ctx_epoch() != E (re-capture instead;
+ * GpuBaseExecutor.capture does this automatically). Plans rebuild themselves on launch. */
+SS_API uint64_t ss_ctx_epoch(const ss_ctx* ctx);
+
 /* In-stream kernel timing (bench evidence): while enabled, every launch of kind
  * SS_KERNEL_{GATHER,SHRINK,GEMM} is bracketed by CUDA events on its own stream, and its
  * algorithmic FLOPs / bytes are accumulated. ss_profile_read synchronizes the recorded events
@@ -244,10 +251,12 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   gemm_2cta (-1)      CTA-pair kernel: -1 by dispatch size, 1 / 0 forced
  *   pair_n (0)          CTA-pair tile width 256 (double-buffered TMEM) or 512 (12 warps); 0 auto
  *   side_shrink (1)     a LoRA shrink that reads no packed rows runs on a side stream beside the gather
- *   lora_overlap (1)    the weight-streaming kernel runs beside that shrink and waits on its
- *                       completion counter only before its LoRA k-blocks (when both fit the SMs)
- *                       (default 0 under tools that serialise launches: CUDA_INJECTION64_PATH
- *                       set, i.e. ncu / compute-sanitizer, or CUDA_LAUNCH_BLOCKING=1)
+ *   lora_overlap (0)    the weight-streaming kernel runs beside that shrink and spins on its
+ *                       completion counter only before its LoRA k-blocks (when both fit the SMs).
+ *                       Opt-in: only safe when no other work on the GPU can keep the shrink's
+ *                       CTAs from being scheduled (the executor owns the GPU); ignored under
+ *                       tools that serialise launches (CUDA_INJECTION64_PATH, i.e. ncu /
+ *                       compute-sanitizer, or CUDA_LAUNCH_BLOCKING=1)
  *   cluster4 (0)        256x256 pair tiles as 4-CTA clusters sharing B by multicast (measured
  *                       35 % slower in the step: off)
  *   tile_n (0)          force the single-CTA tile width 64 / 128 / 256 (0 auto)

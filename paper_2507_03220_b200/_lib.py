@@ -52,7 +52,7 @@ EXPORTED = (
     "ss_unload_layer", "ss_set_adapter", "ss_clear_adapter", "ss_clear_client",
     "ss_compute_batch", "ss_memory_stats", "ss_kernel_launches", "ss_set_option",
     "ss_profile", "ss_profile_read", "ss_adapter_grads", "ss_plan_create", "ss_plan_launch",
-    "ss_plan_destroy", "ss_compute_batch_host", "ss_serve_frames",
+    "ss_plan_destroy", "ss_compute_batch_host", "ss_serve_frames", "ss_ctx_epoch",
 )
 
 SS_KERNEL_GATHER = 0
@@ -144,6 +144,7 @@ def load() -> ctypes.CDLL:
             "ss_memory_stats": (i32, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                       ctypes.POINTER(i64)]),
             "ss_kernel_launches": (i64, [vp]),
+            "ss_ctx_epoch": (ctypes.c_uint64, [vp]),
             "ss_set_option": (i32, [vp, ctypes.c_char_p, i64]),
             "ss_profile": (i32, [vp, i32]),
             "ss_profile_read": (i32, [vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64),

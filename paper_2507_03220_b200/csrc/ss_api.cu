@@ -103,9 +103,13 @@ struct ss_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int side_shrink = 1;
-  int lora_overlap = 1;
+  // 0 by default: the overlapped streaming GEMM spins on a counter the side-stream shrink
+  // writes, which is only safe when nothing else can keep the shrink's CTAs off the SMs (the
+  // executor owns the GPU). Opt in with ss_set_option("lora_overlap", 1).
+  int lora_overlap = 0;
+  int serial_launches = 0;       // a tool serialises kernel launches (ncu, sanitizer): no overlap
   int stream_pdl = 1;
-  int wide_decode = 1;           // decode-size dispatches: 128-wide single-CTA tiles when they fit one wave            // streaming GEMM launched early behind the gather (see launch_batch)          // streaming GEMM overlaps the side-stream shrink (see launch_batch)
+  int wide_decode = 1;           // decode-size dispatches: 128-wide single-CTA tiles when they fit one wave
   int* sync_ctr = nullptr;       // [2] shrink-done counter + GEMM ticket (zero between dispatches)
   struct HostSlot {
     void* in = nullptr;
@@ -162,6 +166,11 @@ struct ss_ctx {
   // Plans (ss_plan_*) cache routing tables that embed workspace and adapter pointers; these
   // counters tell a plan to rebuild itself after the workspace grew or an adapter moved.
   uint64_t ws_epoch = 0, ad_epoch = 0;
+  // bumped whenever ANY device buffer a launched kernel may reference is freed or replaced
+  // (workspace incl. the shrink partials, packs, IA3 vectors): a CUDA graph captured before
+  // must not be replayed (ss_ctx_epoch; GpuBaseExecutor.capture re-captures)
+  uint64_t free_epoch = 0;
+  uint64_t zc_swept = 0;         // ws + ad + opt epoch at the last stale-entry sweep of zc_cache
   // zero-copy host dispatches that recur (decode: clients reuse their buffers every step) reuse
   // their routing tables: keyed by the segment array's bytes, valid while the epochs, the
   // options and the reply slot are unchanged (see ss_compute_batch_host)
@@ -325,6 +334,7 @@ int grow_packs(ss_ctx* ctx, Layer& L, int need_rows) {
   if (L.at_pack) {
     CK(cudaFree(L.at_pack));
     CK(cudaFree(L.b_pack));
+    ctx->free_epoch++;
     ctx->adapter_bytes -= (int64_t)L.pack_cap * (L.ld_at + L.ld_b) * 2;
   }
   L.at_pack = at;
@@ -344,7 +354,10 @@ int ensure_dev(ss_ctx* ctx, T*& ptr, size_t& cap, size_t bytes, bool plan_visibl
   if (plan_visible) ctx->ws_epoch++;
   size_t n = std::max(bytes, cap + cap / 2);
   n = round_up((int64_t)n, 1 << 20);
-  if (ptr) CK(cudaFree(ptr));
+  if (ptr) {
+    CK(cudaFree(ptr));
+    ctx->free_epoch++;
+  }
   ptr = nullptr;
   cap = 0;
   CK(cudaMalloc(reinterpret_cast<void**>(&ptr), n));
@@ -809,8 +822,10 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     for (ShrinkItem& it : items) {
       if (it.amap != 0 || it.rows > 16) continue;
       const DevSeg& d = ds[it.seg];
+      // (backward + IA3: the shrink must read g = dy*l, which only the packed operand holds)
       const bool in_place = (d.flags & SEGF_SRC_BF16) && (d.flags & SEGF_SRC_VEC) &&
-                            !(d.flags & (SEGF_REMOTE_SRC | SEGF_SRC_ALIASED)) && (d.src_ld * 2) % 16 == 0;
+                            !(d.flags & (SEGF_REMOTE_SRC | SEGF_SRC_ALIASED)) &&
+                            !(bwd && (d.flags & SEGF_IA3)) && (d.src_ld * 2) % 16 == 0;
       if (in_place) {
         if (seg_map[it.seg] < 0) {
           seg_map[it.seg] = (int32_t)tmaps.size();
@@ -1186,7 +1201,7 @@ int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out) {
   {
     const char* inj = getenv("CUDA_INJECTION64_PATH");
     const char* blk = getenv("CUDA_LAUNCH_BLOCKING");
-    if ((inj && *inj) || (blk && *blk == '1')) ctx->lora_overlap = 0;
+    if ((inj && *inj) || (blk && *blk == '1')) ctx->serial_launches = 1;
   }
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -1372,7 +1387,7 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
     return SS_OK;
   }
   if (!strcmp(key, "lora_overlap")) {
-    ctx->lora_overlap = value ? 1 : 0;
+    ctx->lora_overlap = (value && !ctx->serial_launches) ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "side_shrink")) {
@@ -1488,6 +1503,9 @@ int ss_set_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role, uint32_
   int rc = upload_begin(ctx);
   if (rc) return rc;
   AdapterSlot& s = L.adapters[client_id];
+  // cached tables (plans, zero-copy entries, graphs) bake the kind's segment flags and the
+  // LoRA scale: any change of either invalidates them like a move does
+  if (s.kind != kind || ((kind & SS_ADAPTER_LORA) && s.scale != scale)) ctx->ad_epoch++;
   if (kind & SS_ADAPTER_LORA) {
     const int rp = (int)round_up(rank, LORA_CHUNK);
     if (s.pack_row < 0 || s.rank_pad != rp) {
@@ -1559,6 +1577,10 @@ int ss_memory_stats(const ss_ctx* ctx, int64_t* w, int64_t* a, int64_t* ws) {
 }
 
 int64_t ss_kernel_launches(const ss_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+uint64_t ss_ctx_epoch(const ss_ctx* ctx) {
+  return ctx ? ctx->ws_epoch + ctx->ad_epoch + ctx->free_epoch : 0;
+}
 
 int ss_profile(ss_ctx* ctx, int enable) {
   if (!ctx) return SS_E_ARG;
@@ -2096,6 +2118,21 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     if (hs.out_cap < out_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.out), hs.out_cap, out_need, false))) return rc;
     if (hs.base_cap < base_need && (rc = ensure_dev(ctx, reinterpret_cast<char*&>(hs.base), hs.base_cap, base_need, false))) return rc;
     const uint64_t key = ctx->zc_cache_on ? zc_key(pass_kind, block, role, n_seg, segs) : 0;
+    if (ctx->zc_cache_on && ctx->zc_swept != ctx->ws_epoch + ctx->ad_epoch + ctx->opt_epoch) {
+      // an epoch moved since the last sweep: entries built before can never hit again, free
+      // them now (every earlier host dispatch synchronised on return: nothing reads them)
+      for (auto it = ctx->zc_cache.begin(); it != ctx->zc_cache.end();) {
+        ZcPlan* z = it->second;
+        if (z->b.ws_epoch != ctx->ws_epoch || z->b.ad_epoch != ctx->ad_epoch || z->opt_epoch != ctx->opt_epoch) {
+          cudaFree(z->dev);
+          delete z;
+          it = ctx->zc_cache.erase(it);
+        } else {
+          ++it;
+        }
+      }
+      ctx->zc_swept = ctx->ws_epoch + ctx->ad_epoch + ctx->opt_epoch;
+    }
     if (ctx->zc_cache_on) {
       auto it = ctx->zc_cache.find(key);
       ZcPlan* z = it == ctx->zc_cache.end() ? nullptr : it->second;

@@ -354,6 +354,10 @@ class SsContext:
     def kernel_launches(self) -> int:
         return int(self.lib.ss_kernel_launches(self.h))
 
+    def epoch(self) -> int:
+        """ss_ctx_epoch: moves whenever a buffer captured kernels may reference was freed."""
+        return int(self.lib.ss_ctx_epoch(self.h))
+
     def profile(self, enable: bool) -> None:
         """Start (and reset) / stop in-stream CUDA-event timing of every kernel launch."""
         check(self.h, self.lib.ss_profile(self.h, 1 if enable else 0))

@@ -114,8 +114,9 @@ class Dispatch:
     For device-resident clients whose exchange buffers do not move (DeviceChannel after its
     first grow). ``run`` is capturable in a CUDA graph (``GpuBaseExecutor.capture``)."""
 
-    def __init__(self, ctx: SsContext, pass_kind: int, key, segs, segments=None):
+    def __init__(self, ctx: SsContext, pass_kind: int, key, segs, segments=None, lock=None):
         self.ctx, self.pass_kind, self.key = ctx, pass_kind, key
+        self._lock = lock if lock is not None else threading.RLock()
         self.segments = segments          # the (client, src, dst, base) tuples it was built from
         self.plan = ctx.plan(pass_kind, key[0], key[1], segs)
         self.rows = sum(int(s.src.shape[0]) for s in segs)
@@ -124,7 +125,53 @@ class Dispatch:
             raise ProtocolError(f"dispatch {self.key} pass {self.pass_kind}: segment status {bad}")
 
     def run(self, stream: torch.cuda.Stream | None = None) -> None:
-        self.plan.launch(stream)
+        with self._lock:
+            self.plan.launch(stream)
+
+
+class CapturedStep:
+    """A sequence of prebuilt dispatches captured as one CUDA graph (``GpuBaseExecutor.capture``).
+
+    Captured kernels bake the context's workspace / LoRA-pack / IA3 addresses. Any later call
+    that frees or moves one of them (a larger eager dispatch growing the workspace, an adapter
+    rank / kind / scale change, ...) moves ``ss_ctx_epoch``; ``replay`` then re-captures
+    (eagerly running the dispatches once, which rebuilds their plans) instead of replaying
+    freed memory. Adapter VALUE refreshes at the same rank write the packs in place and need
+    no re-capture."""
+
+    def __init__(self, executor: "GpuBaseExecutor", dispatches, stream: torch.cuda.Stream | None = None):
+        self.executor = executor
+        self.dispatches = list(dispatches)
+        self.stream = stream if stream is not None else torch.cuda.Stream(executor.device)
+        self.graph: torch.cuda.CUDAGraph | None = None
+        self.epoch = -1
+        self.recaptures = -1
+        self._capture()
+
+    def _capture(self) -> None:
+        ex, s = self.executor, self.stream
+        with ex._lock, torch.cuda.device(ex.device):
+            self.graph = None          # (the old graph's memory may be what just moved)
+            for d in self.dispatches:
+                d.run(s)
+            torch.cuda.synchronize(ex.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for d in self.dispatches:
+                    d.run(s)
+            self.graph = g
+            self.epoch = ex.ctx.epoch()
+            self.recaptures += 1
+
+    @property
+    def stale(self) -> bool:
+        return self.executor.ctx.epoch() != self.epoch
+
+    def replay(self) -> None:
+        with self.executor._lock:
+            if self.stale:
+                self._capture()
+            self.graph.replay()
 
 
 def _is_device(x) -> bool:
@@ -169,6 +216,11 @@ class GpuBaseExecutor:
         generator of pairs streams a large model through without a second copy."""
         self.policy = policy or BatchPolicy()
         self.save_activations = save_activations
+        # Serialises every call into the library context: the scheduler thread's dispatches,
+        # adapter (re-)registration from client threads, plans, graphs, gradient jobs. The
+        # library itself is single-threaded per context (pack growth frees what a concurrent
+        # table build would read).
+        self._lock = threading.RLock()
         self._saved_debug: list = []
         self.ctx = context if context is not None else SsContext(device)
         self.device = self.ctx.device
@@ -255,6 +307,10 @@ class GpuBaseExecutor:
         (adapters.py:44-60: ``lora {addr: (A, B)}``, ``ia3 {addr: l}``, ``alpha``, ``rank``).
         Call again after every optimizer step to refresh the device copy. From then on the
         client must NOT apply the adapter itself on these addresses (client.py:206-209)."""
+        with self._lock:
+            self._register_adapter(client_id, adapter, addresses)
+
+    def _register_adapter(self, client_id: int, adapter, addresses) -> None:
         lora = getattr(adapter, "lora", {}) or {}
         ia3 = getattr(adapter, "ia3", {}) or {}
         keys = {addr_key(a) for a in list(lora) + list(ia3)}
@@ -278,11 +334,12 @@ class GpuBaseExecutor:
     refresh_adapter = register_adapter
 
     def deregister_adapter(self, client_id: int) -> None:
-        self.ctx.clear_adapter(client_id)
-        self._fused.pop(client_id, None)
-        self._fused_ver += 1
-        self._host_memo.clear()
-        self._sync_ledger()
+        with self._lock:
+            self.ctx.clear_adapter(client_id)
+            self._fused.pop(client_id, None)
+            self._fused_ver += 1
+            self._host_memo.clear()
+            self._sync_ledger()
 
     def fused_addresses(self, client_id: int) -> set:
         return set(self._fused.get(client_id, ()))
@@ -297,23 +354,15 @@ class GpuBaseExecutor:
                     base=base if pass_kind != PASS_BACKWARD else None,
                     adapter=key in self._fused.get(c, ()))
                 for c, src, dst, base in segments]
-        return Dispatch(self.ctx, pass_kind, key, segs, list(segments))
+        with self._lock:
+            return Dispatch(self.ctx, pass_kind, key, segs, list(segments), self._lock)
 
-    def capture(self, dispatches, stream: torch.cuda.Stream | None = None) -> torch.cuda.CUDAGraph:
+    def capture(self, dispatches, stream: torch.cuda.Stream | None = None) -> CapturedStep:
         """Capture a sequence of prebuilt dispatches into one CUDA graph (replay = one launch
         for the whole sequence). Runs them once eagerly first so every plan's workspace is at
-        its high-water mark; adapters must not be re-registered between capture and replay
-        with a different rank (refreshing values in place is fine: the graph reads the packs)."""
-        s = stream if stream is not None else torch.cuda.Stream(self.device)
-        with torch.cuda.device(self.device):
-            for d in dispatches:
-                d.run(s)
-            torch.cuda.synchronize(self.device)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=s):
-                for d in dispatches:
-                    d.run(s)
-        return g
+        its high-water mark. The returned ``CapturedStep.replay()`` re-captures by itself when
+        the context freed or moved anything the graph references since (ss_ctx_epoch)."""
+        return CapturedStep(self, dispatches, stream)
 
     def adapter_grads(self, block: int, role: int, jobs, stream: torch.cuda.Stream | None = None) -> list:
         """LoRA / IA3 weight gradients of one layer on the GPU (ss_adapter_grads) for the
@@ -322,7 +371,8 @@ class GpuBaseExecutor:
         key = (int(block), int(role))
         if key not in self._dims:
             raise ProtocolError(f"unknown layer {key}")
-        return self.ctx.adapter_grads(key[0], key[1], jobs, stream)
+        with self._lock:
+            return self.ctx.adapter_grads(key[0], key[1], jobs, stream)
 
     def _sync_ledger(self) -> None:
         w, a, _ = self.ctx.memory_stats()
@@ -375,6 +425,10 @@ class GpuBaseExecutor:
         ss_compute_batch call (gather + GEMM + fused adapter + scatter)."""
         if not envelopes:
             return []
+        with self._lock:
+            return self._compute_batch_locked(pass_kind, envelopes)
+
+    def _compute_batch_locked(self, pass_kind: int, envelopes) -> list:
         addr = envelopes[0].layer
         key = addr_key(addr)
         d_in, d_out = self._dims[key]
@@ -451,6 +505,7 @@ class GpuBaseExecutor:
         if self.save_activations:
             return False
         info = self._host_info
+        dtype = None
         for i in good:
             e = envelopes[i]
             p, r = e.payload, getattr(e, "reply_to", None)
@@ -459,6 +514,12 @@ class GpuBaseExecutor:
                 return False
             ip, ir = _cached_info(info, p), _cached_info(info, r)
             if not ip or not ir or ip[0] != ir[0] or ir[1] != (e.token_count, out_w):
+                return False
+            # the native host pipeline needs one payload / reply dtype per dispatch; a mixed
+            # batch takes the staged path (every valid envelope still computes)
+            if dtype is None:
+                dtype = ip[0]
+            elif ip[0] != dtype:
                 return False
         return True
 

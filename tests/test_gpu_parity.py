@@ -209,13 +209,16 @@ def test_batched_equals_solo_bitwise(dtype):
 
 
 @pytest.mark.parametrize("shape", [("7b_q", 4096, 4096), ("13b_ff_up", 5120, 13824),
-                                   ("13b_ff_down", 13824, 5120), ("13b_lm_head", 5120, 32000)])
+                                   ("13b_ff_down", 13824, 5120), ("13b_lm_head", 5120, 32000),
+                                   # Granite-20B shape (BASELINE configs[4]): K up to 24576, V 49152
+                                   ("g20_q", 6144, 6144), ("g20_ff_up", 6144, 24576),
+                                   ("g20_ff_down", 24576, 6144), ("g20_lm_head", 6144, 49152)])
 def test_large_layer_parity_vs_fp32(shape):
     """Llama2-7B/13B layer shapes, mixed LoRA ranks 8..64 + IA3 + plain, bf16 in/out, against
     an fp32 torch evaluation of the same math on the same bf16 operands."""
     name, d_in, d_out = shape
     role = O.FF_UP if "ff_up" in name else (O.FF_DOWN if "ff_down" in name else (O.LM_HEAD if "head" in name else O.Q))
-    block = 40 if role == O.LM_HEAD else 0
+    block = (52 if name.startswith("g20") else 40) if role == O.LM_HEAD else 0
     w, b = O.layer_params(7, block, role, d_in, d_out)
     ex = _ex({(block, role): (w, b)})
     rng = np.random.default_rng(1)
@@ -860,3 +863,42 @@ def test_full_size_batched_equals_solo_13b_ff_up():
         assert torch.equal(solo, batched[c]), c
         if c == 2:
             assert torch.equal(base_s, base_batched)
+
+
+@pytest.mark.parametrize("rows", [[2, 3], [200, 7], [128 + 5]])
+def test_backward_lora_plus_ia3_short_pieces(rows):
+    """a client with LoRA AND IA3 on one layer, backward, with LoRA pieces of <= 16
+    rows (decode rows and short tails of larger segments). The shrink must read the IA3-scaled
+    g = dy*l (client.py:291-294 -> adapters.py:37), not dy."""
+    d_in, d_out = 512, 1024
+    w, b = O.layer_params(41, 0, O.FF_UP, d_in, d_out)
+    ex = _ex({(0, O.FF_UP): (w, b)})
+    lo = O.lora_params(41, 0, 0, O.FF_UP, d_in, d_out, 16, 32.0)
+    ia = O.ia3_params(41, 0, 0, O.FF_UP, d_out)
+    ex.register_adapter(0, _Adapter(lora={_addr(0, O.FF_UP): (lo.a, lo.b)}, ia3={_addr(0, O.FF_UP): ia.ia3},
+                                    alpha=32.0, rank=16))
+    ad = O.OracleAdapter(a=O.bf16_round(lo.a), b=O.bf16_round(lo.b), alpha=32.0, rank=16, ia3=ia.ia3)
+    wr = O.bf16_round(w)
+    for dtype in (torch.bfloat16, torch.float32):
+        gs = [torch.randn(t, d_out, device=ex.device).to(torch.bfloat16).to(dtype) for t in rows]
+        res = ex._compute_batch(1, [_env(0 if c == 0 else 1, 1, 0, O.FF_UP, 1, g) for c, g in enumerate(gs)])
+        g0 = gs[0].float().cpu().numpy()
+        _close(res[0].float().cpu().numpy(), O.layer_backward_dx(ad, wr, g0),
+               what=f"bwd LoRA+IA3 rows={rows} {dtype}")
+
+
+def test_host_batch_with_mixed_dtypes_computes_every_envelope():
+    """pinned-host clients sending bf16 and f32 in one dispatch must all compute
+    (the native host pipeline needs one dtype; mixed batches take the staged path)."""
+    d_in, d_out = 256, 512
+    w, b = O.layer_params(42, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)})
+    dts = (torch.bfloat16, torch.float32, torch.bfloat16)
+    hosts = [torch.randn(t, d_in).to(torch.bfloat16).to(dt).pin_memory() for t, dt in zip((9, 40, 3), dts)]
+    replies = [torch.empty(h.shape[0], d_out, dtype=dt).pin_memory() for h, dt in zip(hosts, dts)]
+    res = ex._compute_batch(0, [_env(c, 1, 0, O.V, 0, h, reply_to=r) for c, (h, r) in enumerate(zip(hosts, replies))])
+    wr = O.bf16_round(w)
+    for c, r in enumerate(res):
+        assert isinstance(r, torch.Tensor), r
+        ref = O.affine_forward(hosts[c].float().numpy(), wr, b)
+        _close(r.float().cpu().numpy(), ref, what=f"mixed host client {c}")
