@@ -387,12 +387,22 @@ def normwise_errors(got: np.ndarray, ref: np.ndarray) -> tuple[float, float]:
             float(d.mean()) / mn if mn else float(d.mean()))
 
 
-# Tolerances vs the f32 oracle fed the same bf16-rounded inputs (normwise).
-# bf16 activations in AND out: output rounding alone costs ~3e-3 max / ~1.4e-3 mean, and the
-# IA3 backward prologue rounds g*l to bf16 once more (~2.3e-3 mean measured on B200).
+# Tolerances vs the f32 oracle fed the same bf16-rounded inputs (normwise, SURVEY §8c;
+# measured per client kind in profiles/r02_precision.md, tools/precision_probe.py).
+# bf16 activations in AND out: output rounding alone costs ~3e-3 max / ~1.4e-3 mean; the LoRA
+# intermediate s*x.A is carried as a hi/lo bf16 pair (lora_hilo), so LoRA clients sit at the
+# same floor.
 TOL_MAX_REL = 2e-2
-TOL_MEAN_REL = 3e-3
-# fp32 outputs (bf16 operands, fp32 accumulate): the LoRA intermediate s*x.A is itself a bf16
-# tensor-core operand, which costs ~1.05e-3 mean for a rank-64, alpha=2r client (measured).
-TOL_F32_MAX_REL = 1e-2
-TOL_F32_MEAN_REL = 1.5e-3
+TOL_MEAN_REL = 2e-3
+# IA3 backward with bf16 outputs: the operand g = dy*l (client.py:291-294, f32 in the
+# reference) is itself rounded to bf16 once (the lo pass is reserved for f32 outputs, see
+# below): measured 2.3e-3 mean.
+TOL_IA3_BWD_MEAN_REL = 3e-3
+# fp32 outputs (bf16 operands, fp32 accumulate): LoRA's s*x.A as hi + lo, IA3 backward's
+# g*l as hi + lo with a second K pass (ia3_lo): measured <= 2e-5 max / 2e-5 mean at 13B
+# shapes (vs ~1e-3 with a single bf16 intermediate).
+TOL_F32_MAX_REL = 1e-3
+TOL_F32_MEAN_REL = 1e-4
+# LoRA weight gradients (ss_adapter_grads): the token contraction's operand s*x.A / s*g.B^T is
+# a bf16 tensor-core operand (fp32 outputs).
+TOL_GRAD_MEAN_REL = 3e-3

@@ -33,6 +33,8 @@ enum : int32_t {
   SEGF_REMOTE_SRC = 1 << 10,  // source rows on a peer GPU (gathered with plain loads)
   SEGF_REMOTE_DST = 1 << 11,  // destination on a peer GPU (plain stores over NVLink)
   SEGF_SRC_ALIASED = 1 << 12, // source rows overlap a destination of the dispatch (gathered first)
+  SEGF_IA3_LO = 1 << 13,      // backward IA3: g = dy*l also kept as lo = bf16(g - bf16(g)) in X_lo,
+                              // and the tile runs a second K pass over it (fp32-output tier)
 };
 
 struct DevSeg {
@@ -78,6 +80,8 @@ struct TileDesc {
   int32_t chunk_count;  // LoRA: 16-wide rank chunks (block-diagonal over the tile's segments)
   int32_t store_begin;  // TMA-store ops of this tile: entries in GemmParams::stores
   int32_t store_count;
+  int32_t amap_lo;      // >= 0: tensor map of X_lo; the tile's K loop runs twice (X, then X_lo)
+                        // so IA3-backward rows see g = hi + lo (SEGF_IA3_LO); -1: one pass
 };
 
 struct GemmParams {
@@ -525,12 +529,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tile_coords(t, p, mb, nb);
         const TileDesc td = p.tiles[mb];
         const CUtensorMap* tmA = p.tmaps + td.amap;
+        const CUtensorMap* tmA_lo = p.tmaps + (td.amap_lo >= 0 ? td.amap_lo : td.amap);
         const int m0 = mb * BM, n0 = nb * TBN;
         tensormap_acquire(tmA);
-        for (int kb = 0; kb < nkb; ++kb) {
+        if (td.amap_lo >= 0) tensormap_acquire(tmA_lo);
+        const int nkb_t = td.amap_lo >= 0 ? 2 * nkb : nkb;
+        for (int kb2 = 0; kb2 < nkb_t; ++kb2) {
+          const int kb = kb2 < nkb ? kb2 : kb2 - nkb;
           mbar_wait(&empty_bar[s], ph ^ 1);
           mbar_expect_tx(&full_bar[s], p.a_bytes + B_STAGE_BYTES);
-          load_a_or_b(smA + s * A_STAGE_BYTES, tmA, &full_bar[s], kb * BK, td.arow, p.hint_a, pol_a);
+          load_a_or_b(smA + s * A_STAGE_BYTES, kb2 < nkb ? tmA : tmA_lo, &full_bar[s], kb * BK, td.arow, p.hint_a, pol_a);
           uint8_t* b = smB + s * B_STAGE_BYTES;
           if (kBwd) {
             // W viewed K-major: rows = d_in (the GEMM's N), cols = d_out (the GEMM's K).
@@ -578,7 +586,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * TBN;
-      for (int kb = 0; kb < nkb; ++kb) {
+      const int nkb_t = p.tiles[mb].amap_lo >= 0 ? 2 * nkb : nkb;
+      for (int kb = 0; kb < nkb_t; ++kb) {
         mbar_wait(&full_bar[s], ph);
         tc_fence_after();
         if (lane == 0) {
@@ -999,15 +1008,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<PN>::THREADS
         tile_coords(t, p, mb, nb);
         const TileDesc td = p.tiles[mb];
         const CUtensorMap* tmA = p.tmaps + td.amap;
+        const CUtensorMap* tmA_lo = p.tmaps + (td.amap_lo >= 0 ? td.amap_lo : td.amap);
         const int arow = td.arow + crank * BM;
         tensormap_acquire(tmA);
+        if (td.amap_lo >= 0) tensormap_acquire(tmA_lo);
         const int m0 = mb * BM2 + crank * BM;       // row of this CTA's half in A_lora
         const int nh = nb * PN + crank * 128;      // first column of this CTA's group 0
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int nkb_t = td.amap_lo >= 0 ? 2 * nkb : nkb;
+        for (int kb2 = 0; kb2 < nkb_t; ++kb2) {
+          const int kb = kb2 < nkb ? kb2 : kb2 - nkb;
           mbar_wait(&empty_bar[s], ph ^ 1);
           const uint32_t fb = full0 + s * 8;
           if (leader) mbar_expect_tx(&full_bar[s], 2 * Cfg::STAGE);
-          load_a_or_b_2sm(smA + s * A_STAGE_BYTES, tmA, fb, kb * BK, arow, p.hint_a, pol_a);
+          load_a_or_b_2sm(smA + s * A_STAGE_BYTES, kb2 < nkb ? tmA : tmA_lo, fb, kb * BK, arow, p.hint_a, pol_a);
           uint8_t* b = smB + s * Cfg::B_BYTES;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
@@ -1062,7 +1075,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<PN>::THREADS
         mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int nkb_t = p.tiles[mb].amap_lo >= 0 ? 2 * nkb : nkb;
+        for (int kb = 0; kb < nkb_t; ++kb) {
           mbar_wait(&full_bar[s], ph);
           tc_fence_after();
           if (lane == 0) {
@@ -1399,7 +1413,11 @@ struct ShrinkItem {
   // + tm), so rows of other clients in the tile get no contribution from this adapter
   int32_t zero_fill;
   int32_t tile_row0, tm, piece_lo, piece_hi;
-  int32_t pad_[3];
+  // 1: the segment's column block is 2 x rank_pad wide: hi = bf16(v) in the first half and
+  // lo = bf16(v - hi) in the second, the GEMM's K-extension reading the same B rows for both
+  // (v = s*x.A kept to ~2^-17 instead of bf16's 2^-9: the fp32-output tier)
+  int32_t hilo;
+  int32_t pad_[2];
 };
 
 struct ShrinkParams {
@@ -1542,6 +1560,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
                         pack_bf16x2(v[6], v[7]));
       o[1] = make_uint4(pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]),
                         pack_bf16x2(v[12], v[13]), pack_bf16x2(v[14], v[15]));
+      if (it.hilo) {
+        float lo[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) lo[j] = v[j] - __bfloat162float(__float2bfloat16_rn(v[j]));
+        uint4* q = reinterpret_cast<uint4*>(out + npad + c * 16);
+        q[0] = make_uint4(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]), pack_bf16x2(lo[4], lo[5]),
+                          pack_bf16x2(lo[6], lo[7]));
+        q[1] = make_uint4(pack_bf16x2(lo[8], lo[9]), pack_bf16x2(lo[10], lo[11]),
+                          pack_bf16x2(lo[12], lo[13]), pack_bf16x2(lo[14], lo[15]));
+      }
     };
     if (whole && nchk > 1) {
       // running fp32 sums of the chunk partials, in chunk order (npad <= 64: host-guaranteed)
@@ -1640,7 +1668,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
     }
     if (it.zero_fill && c0 == 0) {
       // zeros of the block-diagonal operand (replaces a memset of the whole operand)
-      const int vec_per_row = npad / 8;                      // 16-byte vectors of bf16
+      const int vec_per_row = (it.hilo ? 2 : 1) * npad / 8;  // 16-byte vectors of bf16
       const int nrow = it.tm - (it.piece_hi - it.piece_lo);
       for (int v = (int)(ew * 32 + lane); v < nrow * vec_per_row; v += 128) {
         const int k = v / vec_per_row;
@@ -1677,7 +1705,11 @@ struct GatherParams {
   const int32_t* piece_seg;  // segment of each packed piece, in X order
   __nv_bfloat16* X;
   int32_t* row_seg;
+  // != nullptr when some segment is SEGF_IA3_LO: its rows get lo = bf16(g - bf16(g)) here (the
+  // second K pass of their tiles), every other packed row zeros
+  __nv_bfloat16* X_lo = nullptr;
 };
+
 
 __device__ __forceinline__ int find_piece(const GatherParams& p, int xrow) {
   int lo = 0, hi = p.n_piece - 1;
@@ -1709,6 +1741,24 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) 
     const bool scale = p.ia3_in_prologue && (sg.flags & SEGF_IA3);
     const float* l = sg.ia3;
     const bool vec = (sg.flags & SEGF_SRC_VEC) && ((p.K & 7) == 0);
+    if (p.X_lo) {
+      __nv_bfloat16* xl = p.X_lo + (int64_t)row * p.ldx;
+      if (!(scale && (sg.flags & SEGF_IA3_LO))) {
+        for (int i = e0 + lane; i < e1; i += 32) xl[i] = __float2bfloat16_rn(0.f);
+      } else {
+        // IA3 backward with the lo pass: g = dy * l as hi (X) + lo (X_lo), scalar per element
+        // (these dispatches are fine-tune backward slabs of f32-output clients; not the hot path)
+        for (int i = e0 + lane; i < e1; i += 32) {
+          const float v = ((sg.flags & SEGF_SRC_BF16)
+                               ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(sg.src)[lr * sg.src_ld + i])
+                               : reinterpret_cast<const float*>(sg.src)[lr * sg.src_ld + i]) * __ldg(l + i);
+          const __nv_bfloat16 h = __float2bfloat16_rn(v);
+          xr[i] = h;
+          xl[i] = __float2bfloat16_rn(v - __bfloat162float(h));
+        }
+        continue;
+      }
+    }
     if (sg.flags & SEGF_SRC_BF16) {
       const __nv_bfloat16* sr = reinterpret_cast<const __nv_bfloat16*>(sg.src) + lr * sg.src_ld;
       if (vec && !scale) {

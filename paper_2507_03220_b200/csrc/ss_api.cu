@@ -89,6 +89,8 @@ struct ss_ctx {
   // workspace
   __nv_bfloat16* X = nullptr;
   size_t x_cap = 0;
+  __nv_bfloat16* X_lo = nullptr;   // lo halves of IA3-backward operands (SEGF_IA3_LO)
+  size_t xlo_cap = 0;
   __nv_bfloat16* a_lora = nullptr;
   size_t al_cap = 0;
   int32_t* row_seg = nullptr;
@@ -162,6 +164,13 @@ struct ss_ctx {
   int pair_n = 0;
   int shrink_kb_chunk = SHRINK_KB_CHUNK;  // K-split of the LoRA shrink (k-blocks of 64 per chunk)
   int shrink_mode = 0;   // 0 auto, 1 one CTA per slab (all chunks), 2 one CTA per (slab, chunk)
+  // LoRA intermediate s*x.A as a hi / lo bf16 pair (ShrinkItem::hilo): 0 never, 1 segments with
+  // f32 destinations, 2 every segment. A per-segment property, so batching stays invisible.
+  int lora_hilo = 2;
+  // IA3 backward operand g = dy*l as hi + lo with a second K pass over lo (SEGF_IA3_LO):
+  // 0 never, 1 segments with f32 destinations (default; bf16 outputs round far coarser than
+  // the operand), 2 every IA3 backward segment
+  int ia3_lo = 1;
   int64_t weight_bytes = 0, adapter_bytes = 0;
   // Plans (ss_plan_*) cache routing tables that embed workspace and adapter pointers; these
   // counters tell a plan to rebuild itself after the workspace grew or an adapter moved.
@@ -479,6 +488,7 @@ struct Built {
   int64_t M = 0, MX = 0, lora_ld = 64, al_rows = 0, ldx = 0;
   bool any_lora = false, pair = false, a_rows64 = false, stream = false;
   bool shrink_indep = false;   // the shrink reads no packed rows: it may run beside the gather
+  bool any_lo = false;         // some segment is SEGF_IA3_LO (X_lo written, tiles run two passes)
   int tbn = BN, pn = 256, num_m = 0, n_piece = 0, n_items = 0, part_ld = 16, shrink_chunks_ = 1;
   int kb_chunk = SHRINK_KB_CHUNK;
   size_t off_tm = 0, off_seg = 0, off_tile = 0, off_piece = 0, off_ch = 0, off_st = 0, off_it = 0;
@@ -594,6 +604,10 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
       if (as.kind & SS_ADAPTER_IA3) {
         f |= SEGF_IA3;
         d.ia3 = as.ia3;
+        if (bwd && (ctx->ia3_lo == 2 || (ctx->ia3_lo == 1 && !(s.flags & SS_SEGF_DST_BF16)))) {
+          f |= SEGF_IA3_LO;
+          B.any_lo = true;
+        }
       }
     }
     if (s.dst_base && pass_kind != SS_PASS_BACKWARD) {
@@ -663,7 +677,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
       const int amap = 1 + (int)direct_src.size();
       direct_src.push_back((int32_t)j);
       for (int r = 0; r < nd; r += TM)
-        tiles.push_back(TileDesc{amap, r, (int32_t)j, TM, 0, 0, 0, 0});
+        tiles.push_back(TileDesc{amap, r, (int32_t)j, TM, 0, 0, 0, 0, -1});
     }
     if (d.rows > nd) {
       d.xrow0 = (int32_t)MX;
@@ -673,7 +687,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     }
   }
   for (int64_t x = 0; x < MX; x += TM)
-    tiles.push_back(TileDesc{0, (int32_t)x, -1, (int32_t)std::min<int64_t>(TM, MX - x), 0, 0, 0, 0});
+    tiles.push_back(TileDesc{0, (int32_t)x, -1, (int32_t)std::min<int64_t>(TM, MX - x), 0, 0, 0, 0, -1});
   const int num_m = (int)tiles.size();
 
   // ---- LoRA: per tile rank-chunk lists (block-diagonal over the tile's segments) + shrink items
@@ -689,10 +703,13 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
         const DevSeg& d = ds[sj];
         if (!(d.flags & SEGF_LORA)) return;
         const int col = (int)(chunks.size() - td.chunk_begin) * LORA_CHUNK;
-        for (int q = 0; q < d.rank_pad / LORA_CHUNK; ++q) chunks.push_back(d.pack_row + q * LORA_CHUNK);
+        // hi / lo halves of s*x.A (ShrinkItem::hilo): the expand reads the same B rows twice
+        const int hilo = ctx->lora_hilo == 2 || (ctx->lora_hilo == 1 && !(d.flags & SEGF_DST_BF16));
+        for (int rep = 0; rep <= hilo; ++rep)
+          for (int q = 0; q < d.rank_pad / LORA_CHUNK; ++q) chunks.push_back(d.pack_row + q * LORA_CHUNK);
         for (int r = 0; r < nrows; r += BM)
           items.push_back(ShrinkItem{sj, amap, arow + r, std::min(BM, nrows - r), mt * TM + p0 + r, col, 0, 0,
-                                     r == 0 ? 1 : 0, mt * TM, TM, p0, p0 + nrows, {0, 0, 0}});
+                                     r == 0 ? 1 : 0, mt * TM, TM, p0, p0 + nrows, hilo, {0, 0}});
       };
       if (td.seg >= 0) {
         add_piece(td.seg, td.amap, td.arow, 0, td.rows);
@@ -721,6 +738,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   const int64_t mx_pad = round_up(std::max<int64_t>(MX, 1), TM);
   int rc = ensure_dev(ctx, ctx->X, ctx->x_cap, (size_t)mx_pad * ldx * 2);
   if (rc) return rc;
+  if (B.any_lo && (rc = ensure_dev(ctx, ctx->X_lo, ctx->xlo_cap, (size_t)mx_pad * ldx * 2))) return rc;
   rc = ensure_dev(ctx, ctx->row_seg, ctx->rs_cap, (size_t)mx_pad * 4);
   if (rc) return rc;
   const int64_t al_rows = (int64_t)num_m * TM;
@@ -740,6 +758,22 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     const DevSeg& d = ds[direct_src[i]];
     rc = encode_2d(ctx, &tmaps[1 + i], d.src, K, d.rows, d.src_ld, 64, BM);
     if (rc) return rc;
+  }
+  if (B.any_lo) {
+    // X_lo map (same geometry as X) for every packed tile holding an SEGF_IA3_LO piece
+    const int32_t lo_map = (int32_t)tmaps.size();
+    tmaps.emplace_back();
+    rc = encode_2d(ctx, &tmaps.back(), ctx->X_lo, K, std::max<int64_t>(MX, 1), ldx, 64, BM);
+    if (rc) return rc;
+    for (TileDesc& td : tiles) {
+      if (td.seg >= 0) continue;
+      const int64_t x0 = td.arow, x1 = x0 + td.rows;
+      for (int32_t sj : piece_seg) {
+        const DevSeg& d = ds[sj];
+        const int64_t p0 = d.xrow0, p1 = d.xrow0 + (d.rows - d.xlocal0);
+        if ((d.flags & SEGF_IA3_LO) && p0 < x1 && x0 < p1) { td.amap_lo = lo_map; break; }
+      }
+    }
   }
   std::vector<int32_t> dmap_full(ds.size(), -1), dmap_tail(ds.size(), -1);
   for (size_t j = 0; j < ds.size(); ++j) {
@@ -791,7 +825,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   // ---- weight-streaming dispatch (one packed tile of <= 64 rows): the GEMM reads A through a
   // 64-row box (MMA rows 64-127 are never stored); with `stream_gemm` (K a multiple of 64) the
   // streaming kernel moves 4 k-blocks of A and of W per TMA operation instead
-  if (ctx->a_rows64 && !pair && num_m == 1 && direct_src.empty() && MX <= 64) {
+  if (ctx->a_rows64 && !pair && num_m == 1 && direct_src.empty() && MX <= 64 && !B.any_lo) {
     tiles[0].amap = (int32_t)tmaps.size();
     tmaps.emplace_back();
     // At these sizes a tile's time is set by its K/16-long chain of dependent UMMAs, not by its
@@ -875,7 +909,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   B.off_tm = off_tm; B.off_seg = off_seg; B.off_tile = off_tile; B.off_piece = off_piece;
   B.off_ch = off_ch; B.off_st = off_st; B.off_it = off_it;
   B.M = M; B.MX = MX; B.lora_ld = lora_ld; B.al_rows = al_rows; B.ldx = ldx;
-  B.any_lora = any_lora; B.pair = pair; B.tbn = tbn;
+  B.any_lora = any_lora; B.pair = pair; B.tbn = tbn;   // (B.any_lo set during validation)
   B.pn = ctx->pair_n ? ctx->pair_n
                      : (((M + BM2 - 1) / BM2) * ((N + 511) / 512) >= (int64_t)ctx->num_sms ? 512 : 256);
   B.num_m = num_m; B.n_piece = (int)piece_seg.size(); B.n_items = (int)items.size();
@@ -963,6 +997,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     gp.piece_seg = reinterpret_cast<const int32_t*>(dv + B.off_piece);
     gp.X = ctx->X;
     gp.row_seg = ctx->row_seg;
+    gp.X_lo = B.any_lo ? ctx->X_lo : nullptr;
     // several warps per row when the dispatch has too few rows to fill the GPU
     gp.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((K / 8 + 127) / 128, ((int64_t)ctx->num_sms * 16 + MX - 1) / MX));
     const int grid = (int)std::min<int64_t>((MX * gp.nsplit + 7) / 8, (int64_t)ctx->num_sms * 8);
@@ -1082,7 +1117,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     else
       CK(launch_kp(early || (ctx->pdl && !ctx->profiling), seg_gemm_stream_kernel<false>, grid, GEMM_THREADS,
                    STREAM_SMEM, stream, L.tm_w_fwd_s, tmAL, tmBP, gpm));
-  } else if (pair && pn == 256 && ctx->cluster4 && num_m >= 2) {
+  } else if (pair && pn == 256 && ctx->cluster4 && num_m >= 2 && !B.any_lo) {
     const int ng = (int)std::min<int64_t>((int64_t)((num_m + 1) / 2) * gpm.num_n_tiles, ctx->num_sms / 4);
     if (bwd)
       CK(launch_k(ctx, seg_gemm4_kernel<true>, 4 * ng, GEMM_THREADS, GEMM4_SMEM, stream, L.tm_w_bwd64, tmAL, tmBP, gpm));
@@ -1264,6 +1299,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
     for (auto& a : L.adapters) cudaFree(a.second.ia3);
   }
   cudaFree(ctx->X);
+  cudaFree(ctx->X_lo);
   cudaFree(ctx->ha_in);
   cudaFree(ctx->ha_out);
   cudaFree(ctx->ha_base);
@@ -1309,6 +1345,16 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   ctx->opt_epoch++;   // options shape the built tables: cached dispatches rebuild
   if (!strcmp(key, "zc_cache")) {
     ctx->zc_cache_on = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "ia3_lo")) {
+    if (value < 0 || value > 2) return fail(ctx, SS_E_ARG, "ia3_lo must be 0, 1 or 2");
+    ctx->ia3_lo = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "lora_hilo")) {
+    if (value < 0 || value > 2) return fail(ctx, SS_E_ARG, "lora_hilo must be 0, 1 or 2");
+    ctx->lora_hilo = (int)value;
     return SS_OK;
   }
   if (!strcmp(key, "shrink_mode")) {
@@ -1791,9 +1837,9 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     lg[j].gmap = (int32_t)(4 * j + 3);
     for (int r = 0; r < (int)s.rows; r += BM) {
       const int n = std::min<int>(BM, s.rows - r);
-      sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 0), r, n, lg[j].qrow0 + r, 0, 0, 0, 0, 0, 0, 0, 0, {0, 0, 0}});
+      sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 0), r, n, lg[j].qrow0 + r, 0, 0, 0, 0, 0, 0, 0, 0, 0, {0, 0}});
       sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 1), r, n, (int32_t)qrows + lg[j].qrow0 + r, 0, 1, 0, 0,
-                                  0, 0, 0, 0, {0, 0, 0}});
+                                  0, 0, 0, 0, 0, {0, 0}});
     }
     for (int m = 0; m < d_in; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 0, m, 0});
     for (int m = 0; m < d_out; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 1, m, 0});

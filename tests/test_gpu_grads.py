@@ -16,7 +16,7 @@ from oracle import splitserve_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-MAX_REL, MEAN_REL = O.TOL_MAX_REL, O.TOL_MEAN_REL
+MAX_REL, MEAN_REL = O.TOL_MAX_REL, O.TOL_GRAD_MEAN_REL
 
 
 class _Adapter:

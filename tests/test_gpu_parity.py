@@ -136,12 +136,13 @@ def test_fused_random_parity(golden, name, dtype):
     for c in range(len(ys)):
         _close(ys[c], g[f"fwd/y{c}"], *tol, what=f"{name} fwd client {c}")
         if c == 1:
-            # IA3 backward: the GEMM operand is g*l, which the device rounds to bf16 once more
-            # (client.py:291-294 computes it in f32). Same-operand check at the tier, and the
-            # reference golden at the bf16-activation tier.
-            gl = O.bf16_round(g[f"bwd/g{c}"].astype(np.float32) * g["l1"])
-            _close(dxs[c], O.affine_backward_input(gl, g["W"]), *tol, what="IA3 bwd vs oracle(bf16(g*l))")
-            _close(dxs[c], g[f"bwd/dx{c}"], MAX_REL, MEAN_REL, what="IA3 bwd vs golden")
+            # IA3 backward: the GEMM operand is g*l (client.py:291-294 computes it in f32). f32
+            # outputs carry it as hi + lo (second K pass): the golden at the f32 tier; bf16
+            # outputs round it to bf16 once: the golden at the IA3-backward bf16 tier.
+            if dtype == torch.float32:
+                _close(dxs[c], g[f"bwd/dx{c}"], *tol, what="IA3 bwd (hi+lo) vs golden")
+            else:
+                _close(dxs[c], g[f"bwd/dx{c}"], MAX_REL, O.TOL_IA3_BWD_MEAN_REL, what="IA3 bwd vs golden")
         else:
             _close(dxs[c], g[f"bwd/dx{c}"], *tol, what=f"{name} bwd client {c}")
     _close(bases[1], g["fwd/ybase1"], *tol, what="IA3 y_base")
@@ -262,7 +263,10 @@ def test_large_layer_parity_vs_fp32(shape):
                     A = torch.from_numpy(ad.a).to(dev).to(torch.bfloat16).float()
                     B = torch.from_numpy(ad.b).to(dev).to(torch.bfloat16).float()
                     ref = ref + ((gf @ B.T) @ A.T) * ad.scale
-            _close(y.float().cpu().numpy(), ref.cpu().numpy(), what=f"{name} pass {pass_kind} client {c}")
+            ia3_bwd = pass_kind == 1 and ad is not None and ad.ia3 is not None
+            _close(y.float().cpu().numpy(), ref.cpu().numpy(),
+                   mean_rel=O.TOL_IA3_BWD_MEAN_REL if ia3_bwd else MEAN_REL,
+                   what=f"{name} pass {pass_kind} client {c}")
 
 
 # ----------------------------------------------------------------------- statelessness / edges
@@ -883,7 +887,7 @@ def test_backward_lora_plus_ia3_short_pieces(rows):
         gs = [torch.randn(t, d_out, device=ex.device).to(torch.bfloat16).to(dtype) for t in rows]
         res = ex._compute_batch(1, [_env(0 if c == 0 else 1, 1, 0, O.FF_UP, 1, g) for c, g in enumerate(gs)])
         g0 = gs[0].float().cpu().numpy()
-        _close(res[0].float().cpu().numpy(), O.layer_backward_dx(ad, wr, g0),
+        _close(res[0].float().cpu().numpy(), O.layer_backward_dx(ad, wr, g0), mean_rel=O.TOL_IA3_BWD_MEAN_REL,
                what=f"bwd LoRA+IA3 rows={rows} {dtype}")
 
 
