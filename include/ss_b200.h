@@ -266,6 +266,10 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   a_rows64 (1)        64-row A box for such dispatches in the single-CTA kernel
  *   shrink_mode (0)     LoRA shrink: 0 auto, 1 one CTA per slab, 2 one CTA per (slab, K chunk)
  *   shrink_kb_chunk     k-blocks (of 64) per fixed K chunk of the shrink
+ *   lora_hilo (2)       LoRA intermediate s*x.A as a hi / lo bf16 pair read against the same B rows
+ *                       (fp32-output precision): 0 never, 1 f32-destination segments, 2 all
+ *   ia3_lo (1)          IA3 backward operand g = dy*l as hi + lo with a second K pass over lo:
+ *                       0 never, 1 f32-destination segments, 2 all IA3 backward segments
  *   pdl (0)             programmatic dependent launch between a dispatch's kernels (no gain measured)
  *   wide_decode (1)     dispatches of <= 64 rows whose 64-wide tiles would need more than one wave
  *                       but whose 128-wide tiles fit one run the single-CTA kernel with 128-wide tiles
