@@ -344,29 +344,86 @@ def build_tp_workload(wl_key, device, rank, world):
         return pool[key]
 
     def add(pass_kind, b, r, cids):
+        """One dispatch as `slabs` prebuilt sub-dispatches over consecutive client groups (rows
+        are independent: bitwise the same rows as one dispatch), each with its own collective,
+        so the collective of slab k runs on the comm stream under the GEMM of slab k+1."""
         di, do = dims[r]
         spec = tp.specs[(b, r)]
         w_in = do if pass_kind == 1 else di
-        kind, local, gbuf, reply = P.dispatch_buffers(spec, pass_kind, len(cids) * t, world, rank, buf)
-        segs = [(c, P.shard_input(spec, pass_kind, bufs[c][: t * w_in].view(t, w_in)), local[j * t:(j + 1) * t], None)
-                for j, c in enumerate(cids)]
-        plan.append((tp.ex.compile_dispatch(pass_kind, b, r, segs), kind, local, gbuf, reply))
+        parts = []
+        n = max(1, min(TP_SLABS, len(cids)))
+        groups = [cids[i * len(cids) // n:(i + 1) * len(cids) // n] for i in range(n)]
+        for k, grp in enumerate(groups):
+            kind, local, gbuf, reply = P.dispatch_buffers(spec, pass_kind, len(grp) * t, world, rank, buf, tag=f"/{k}")
+            segs = [(c, P.shard_input(spec, pass_kind, bufs[c][: t * w_in].view(t, w_in)), local[j * t:(j + 1) * t], None)
+                    for j, c in enumerate(grp)]
+            parts.append((tp.ex.compile_dispatch(pass_kind, b, r, segs), kind, local, gbuf, reply))
+        plan.append(parts)
 
     for (b, r) in layers:
         add(0, b, r, list(range(len(specs))))
     for (b, r) in reversed(layers):
         if ft:
             add(1, b, r, ft)
+    tp.comm_stream = torch.cuda.Stream(device)
     return tp, plan, specs, wl
+
+
+TP_SLABS = 4   # sub-dispatches per TP dispatch (collective of slab k overlaps the GEMM of slab k+1)
 
 
 def run_step_tp(tp, plan):
     import torch
     from paper_2507_03220_b200.parallel_plan import finish_dispatch
     stream = torch.cuda.current_stream(tp.device)
-    for disp, kind, local, gbuf, reply in plan:
-        disp.run(stream)
-        finish_dispatch(kind, local, gbuf, reply, tp.group)
+    comm = tp.comm_stream
+    for parts in plan:
+        for disp, kind, local, gbuf, reply in parts:
+            disp.run(stream)
+            if kind == "none":
+                continue
+            comm.wait_stream(stream)           # this slab's partials / shards are written
+            with torch.cuda.stream(comm):
+                finish_dispatch(kind, local, gbuf, reply, tp.group)
+        stream.wait_stream(comm)               # the dispatch's replies are complete
+
+
+def tp_leg(wl_key, device, rank, world, steps, warmup):
+    """Beside the replicas line at N > 1: the north star's tensor-parallel executor over the
+    same N GPUs (strong scaling: the SAME 32 clients served by N column/row shards, one
+    reduce-scatter+all-gather or all-gather per slab), timed like the main leg (barrier, CUDA
+    events, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2507_03220_b200 import parallel_plan as P
+    tp, plan, specs, wl = build_tp_workload(wl_key, device, rank, world)
+    stream = torch.cuda.current_stream(device)
+    for _ in range(max(3, warmup)):
+        run_step_tp(tp, plan)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        run_step_tp(tp, plan)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    layers, dims = layer_list(wl)
+    tok = wl["tokens"]
+    n_all, n_ft = len(specs), sum(1 for s_ in specs if s_[2])
+    comm = sum(P.comm_bytes_per_token(dims[r][0], dims[r][1], r, 0, world) * n_all * tok +
+               P.comm_bytes_per_token(dims[r][0], dims[r][1], r, 1, world) * n_ft * tok for (_, r) in layers)
+    tp.ex.close()
+    return {"value": n_all * tok / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms, "scaling": "strong",
+            "n_gpus": world, "slabs_per_dispatch": TP_SLABS,
+            "comm_bytes_per_rank_per_step": comm,
+            "what": "tensor-parallel executor (column split Q/K/V/FF_UP/LM_HEAD, row split O/FF_DOWN), "
+                    "same 32 clients on all ranks; fp32 reduce-scatter + bf16 all-gather / bf16 all-gather "
+                    "per slab on a comm stream overlapping the next slab's GEMM"}
 
 
 def e2e_leg(ex, wl_key, specs, steps, device):
@@ -430,6 +487,54 @@ def e2e_leg(ex, wl_key, specs, steps, device):
     return dt, h2d, d2h
 
 
+def e2e_numpy_leg(ex, wl_key, specs, steps):
+    """The reference's own payload type: f32 NUMPY activations (transport.py:36, 78), sent
+    through GpuBaseExecutor.serve_forward / serve_backward with no reply buffer (the executor
+    returns f32 numpy row views, like split_rows). Each dispatch runs the native host pipeline
+    (ss_compute_batch_host: H2D of sub-batch j+1 / kernels of j / D2H of j-1 overlapped, from
+    and into pageable client memory). Warm-up: block 0 and LM_HEAD only (the shapes of every
+    dispatch); then `steps` full timed steps."""
+    from paper_2507_03220_b200 import Envelope
+
+    wl = WORKLOADS[wl_key]
+    layers, dims = layer_list(wl)
+    t = wl["tokens"]
+    maxw = max(wl["d"], wl["d_ff"], wl["V"])
+    rng = np.random.default_rng(5)
+    host = [rng.standard_normal(t * maxw, dtype=np.float32) for _ in specs]
+    rid = [0]
+    moved = [0, 0]
+
+    def run(layer_set):
+        moved[0] = moved[1] = 0
+        for (b, r) in layer_set:
+            di, do = dims[r]
+            envs = []
+            for c in range(len(specs)):
+                rid[0] += 1
+                envs.append(Envelope(c, rid[0], b, r, 0, host[c][: t * di].reshape(t, di)))
+                moved[0] += t * di * 4
+                moved[1] += t * do * 4
+            ex.serve_forward(envs)
+        for (b, r) in reversed(layer_set):
+            di, do = dims[r]
+            envs = []
+            for c, (_, _, ft) in enumerate(specs):
+                if ft:
+                    rid[0] += 1
+                    envs.append(Envelope(c, rid[0], b, r, 1, host[c][: t * do].reshape(t, do)))
+                    moved[0] += t * do * 4
+                    moved[1] += t * di * 4
+            ex.serve_backward(envs)
+
+    run([l for l in layers if l[0] in (0, wl["L"])])
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run(layers)
+    dt = (time.perf_counter() - t0) / steps
+    return dt, moved[0], moved[1]
+
+
 # ============================================================================ CPU leg (oracle)
 
 _CPU = {}
@@ -439,9 +544,9 @@ def _cpu_task(args):
     """One (layer, pass, row-chunk) task of the reference algorithm: the batched base GEMM
     (executor.py:191-231 via the oracle's einsum) plus each client's own adapter step."""
     from oracle import splitserve_oracle as Or
-    li, pass_kind, clients = args
+    li, pass_kind, clients, rows = args
     w, bias, ads = _CPU["layers"][li]
-    xs = [_CPU["x"][pass_kind][li][c] for c in clients]
+    xs = [_CPU["x"][pass_kind][li][c][:rows] for c in clients]
     envs = [Or.OracleEnvelope(c, 1, 0, 0, pass_kind, x) for c, x in zip(clients, xs)]
     t0 = time.perf_counter()
     if pass_kind == 0:
@@ -486,16 +591,16 @@ class CpuReference:
                 elif kind == "ia3" and r in (K, V, FF_UP):
                     ads[c] = Or.ia3_params(99, c, b, r, do)
             _CPU["layers"].append((w, bias, ads))
-            _CPU["x"][0].append({c: rng.standard_normal((tokens_per_client, di)).astype(np.float32)
+            # 2x the sample's rows: the linearity check times the doubled token count too
+            _CPU["x"][0].append({c: rng.standard_normal((2 * tokens_per_client, di)).astype(np.float32)
                                  for c in range(len(specs))})
-            _CPU["x"][1].append({c: rng.standard_normal((tokens_per_client, do)).astype(np.float32)
+            _CPU["x"][1].append({c: rng.standard_normal((2 * tokens_per_client, do)).astype(np.float32)
                                  for c in range(len(specs))})
         all_c = list(range(len(specs)))
         self.ft_c = ft_c = [c for c, s in enumerate(specs) if s[2]]
         chunk = lambda cs: [cs[i:i + 4] for i in range(0, len(cs), 4)]  # noqa: E731
-        self.block_tasks = [(li, 0, cs) for li in range(6) for cs in chunk(all_c)] + \
-                           [(li, 1, cs) for li in range(6) for cs in chunk(ft_c)]
-        self.head_tasks = [(6, 0, cs) for cs in chunk(all_c)] + [(6, 1, cs) for cs in chunk(ft_c)]
+        self.block_tasks = self._tasks(range(6), all_c, ft_c, chunk, tokens_per_client)
+        self.head_tasks = self._tasks([6], all_c, ft_c, chunk, tokens_per_client)
         ncpu = procs or os.cpu_count() or 1
         self.n = max(1, min(ncpu, len(self.block_tasks)))
         for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
@@ -503,6 +608,24 @@ class CpuReference:
         import multiprocessing as mp
         self.pool = mp.get_context("fork").Pool(self.n)
         self.pool.map(_cpu_task, self.head_tasks[:1])  # fork + import warm-up, untimed
+
+    @staticmethod
+    def _tasks(layer_idx, all_c, ft_c, chunk, rows):
+        return [(li, 0, cs, rows) for li in layer_idx for cs in chunk(all_c)] + \
+               [(li, 1, cs, rows) for li in layer_idx for cs in chunk(ft_c)]
+
+    def linearity(self) -> dict:
+        """BASELINE.md §3: time the sample (block 0 + LM_HEAD) at n and 2n tokens per client;
+        the full-step model scales by tokens, so t(2n) / (2 t(n)) must be ~1 (reported)."""
+        times = {}
+        for rows in (self.tpc, 2 * self.tpc):
+            tasks = [(li, p, cs, rows) for li, p, cs, _ in self.block_tasks + self.head_tasks]
+            t0 = time.perf_counter()
+            self.pool.map(_cpu_task, tasks, chunksize=1)
+            times[rows] = time.perf_counter() - t0
+        n = self.tpc
+        return {"tokens_per_client": [n, 2 * n], "sample_s": [times[n], times[2 * n]],
+                "ratio_t2n_over_2tn": times[2 * n] / (2 * times[n])}
 
     def sample(self):
         wl = self.wl
@@ -523,6 +646,66 @@ class CpuReference:
     def close(self):
         self.pool.close()
         self.pool.join()
+
+
+def config_dict(wl, tokens_per_rank, world, tp_mode, step_flops, ms):
+    """The workload description both arms print (the driver compares the two dicts)."""
+    tokens = tokens_per_rank * (1 if tp_mode else world)
+    return {"workload": wl["name"], "model": f"d{wl['d']}-ff{wl['d_ff']}-L{wl['L']}-V{wl['V']}",
+            "clients": wl["clients"], "global_batch": tokens, "seq_len": wl["seq"],
+            "batch_per_client": wl["batch"], "rows_per_fwd_dispatch": tokens_per_rank,
+            "parallelism": (f"tensor-parallel x{world} (column/row shards, NCCL per dispatch)" if tp_mode
+                            else f"segment-parallel replicas x{world}" if world > 1 else "single GPU"),
+            "l2": "inputs larger than L2 (every step streams all 6L+1 weight matrices)",
+            "step_tflop": step_flops / 1e12}
+
+
+def self_launch(args) -> int | None:
+    """`python bench.py --gpus N` without a launcher: re-exec under torch.distributed.run with
+    N ranks (one per GPU) on 127.0.0.1, exactly as the driver launches N > 1; returns the
+    launcher's exit code. None when already inside a launcher or N == 1."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args) -> None:
+    """--dry-run: the launcher / rendezvous / barrier / max-over-ranks / JSON contract of an
+    N-rank run on the HOST (gloo), with a small numpy GEMM standing in for the step: what the
+    CPU test suite can check without a GPU."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = np.random.default_rng(rank).standard_normal((256, 256)).astype(np.float32)
+    for _ in range(args.warmup):
+        a @ a
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        a @ a
+    dt = time.perf_counter() - t0
+    if world > 1:
+        import torch
+        t = torch.tensor([dt], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+        dist.barrier()
+    if rank == 0:
+        toks = 256 * args.steps * world
+        print(json.dumps({"metric": METRIC, "value": toks / dt, "unit": "tokens/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+                          "higher_is_better": True, "scaling": "weak", "dry_run": True}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def cpu_model():
@@ -559,12 +742,24 @@ def main():
     ap.add_argument("--inplace", action="store_true",
                     help="device clients reuse one buffer for request and reply (SharedBuffer style; "
                          "aliased sources are gathered before the GEMM)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="host-only (gloo) run of the launcher / timing / JSON contract (CPU tests)")
+    ap.add_argument("--no-tp-leg", action="store_true",
+                    help="N > 1 replicas run: skip the tensor-parallel leg reported beside it")
+    ap.add_argument("--e2e-numpy-steps", type=int, default=1,
+                    help="timed steps of the f32-numpy e2e leg (0: skip)")
     ap.add_argument("--parallel", default="replicas", choices=("replicas", "tp"),
                     help="replicas: segment-parallel full replicas (weak scaling, no data-path "
                          "collective); tp: column/row-sharded layers + NCCL per dispatch (strong)")
     args = ap.parse_args()
     global INPLACE
     INPLACE = args.inplace
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
+    if args.dry_run:
+        dry_run(args)
+        return
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -579,25 +774,33 @@ def main():
         if rank != 0:
             return
         cpu_ref = CpuReference(args.workload, args.cpu_tokens)
-        vals = []
+        lin = cpu_ref.linearity()
+        vals, walls = [], []
         for i in range(max(0, args.warmup) + args.steps):
+            t0 = time.perf_counter()
             tok_s, info = cpu_ref.sample()
             if i >= args.warmup:
                 vals.append(tok_s)
+                walls.append(time.perf_counter() - t0)
         cpu_ref.close()
         cores = cpu_ref.n
         v = float(np.mean(vals))
+        world = args.gpus
+        # the reference arm serves the same workload: same config dict as our arm at this N
+        cfg = config_dict(wl, tokens_per_rank, world, args.parallel == "tp", flops_per_step(wl, specs), 0)
         line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * tokens_per_rank / v, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                # wall time of one bounded sample (a step of this arm); the full step it stands
+                # for would take full_step_s_modelled
+                "ms_per_step": 1e3 * float(np.mean(walls)), "higher_is_better": True,
+                "scaling": "strong" if args.parallel == "tp" else "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (seeded N(0,1) activations, reference-style random init)",
-                "impl": "reference",
-                "config": {"workload": wl["name"], "model": f"d{wl['d']}-ff{wl['d_ff']}-L{wl['L']}-V{wl['V']}",
-                           "clients": wl["clients"], "global_batch": tokens_per_rank, "seq_len": wl["seq"],
-                           "parallelism": "host process pool"},
+                "impl": "reference", "config": cfg,
+                "reference_execution": f"reference algorithm (oracle port, np.einsum optimize=False) on a "
+                                       f"{cores}-process host pool, rank 0 only",
+                "full_step_s_modelled": tokens_per_rank * (1 if args.parallel == "tp" else world) / v,
                 "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
-                                 "sample": info, "cpu": cpu_model()},
+                                 "sample": info, "cpu": cpu_model(), "linearity": lin},
                 "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -752,7 +955,7 @@ def main():
 
     e2e = None
     if not args.skip_e2e and not tp_mode:
-        e2e_steps = args.e2e_steps or (10 if args.workload.endswith("decode") else 1)
+        e2e_steps = args.e2e_steps or (10 if args.workload.endswith("decode") else 3)
         dt, h2d, d2h = e2e_leg(ex, args.workload, specs, e2e_steps, device)
         if world > 1:
             t = torch.tensor([dt], device=device)
@@ -762,15 +965,34 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
                "path": "GpuBaseExecutor.serve_forward / serve_backward, pinned host bf16 payloads + host reply buffers, "
                        f"{e2e_steps} timed step(s) after 1 warm-up"}
+        if args.e2e_numpy_steps > 0:
+            dt_n, h2d_n, d2h_n = e2e_numpy_leg(ex, args.workload, specs, args.e2e_numpy_steps)
+            if world > 1:
+                t = torch.tensor([dt_n], device=device)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt_n = float(t.item())
+            e2e["f32_numpy"] = {"value": tokens / dt_n, "unit": "tokens/s", "h2d_bytes_per_step": h2d_n,
+                                "d2h_bytes_per_step": d2h_n, "ms_per_step": dt_n * 1e3,
+                                "path": "GpuBaseExecutor.serve_forward / serve_backward, f32 numpy payloads "
+                                        "(the reference channels' payload type), replies returned as f32 numpy "
+                                        f"views; native host pipeline; {args.e2e_numpy_steps} timed step(s)"}
+
+    tp_info = None
+    if world > 1 and not tp_mode and not args.no_tp_leg:
+        try:
+            tp_info = tp_leg(args.workload, device, rank, world, args.steps, args.warmup)
+        except Exception as exc:   # the replicas line must still print
+            tp_info = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         cpu_ref = CpuReference(args.workload, args.cpu_tokens)
+        lin = cpu_ref.linearity()
         tok_s, info = cpu_ref.sample()
         tok_s2, info = cpu_ref.sample()
         cpu_ref.close()
         cpu = {"value": 0.5 * (tok_s + tok_s2), "unit": "tokens/s", "cores": cpu_ref.n, "kind": "port",
-               "sample": info + " (mean of 2 samples)", "cpu": cpu_model()}
+               "sample": info + " (mean of 2 samples)", "cpu": cpu_model(), "linearity": lin}
 
     if rank == 0:
         line = {
@@ -779,13 +1001,8 @@ def main():
             "higher_is_better": True, "scaling": "strong" if tp_mode else "weak", "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (random-init weights/adapters/activations, per-layer seeds)",
-            "config": {"workload": wl["name"], "model": f"d{wl['d']}-ff{wl['d_ff']}-L{wl['L']}-V{wl['V']}",
-                       "clients": wl["clients"], "global_batch": tokens, "seq_len": wl["seq"],
-                       "batch_per_client": wl["batch"], "rows_per_fwd_dispatch": tokens_per_rank,
-                       "parallelism": (f"tensor-parallel x{world} (NCCL all-gather/all-reduce per dispatch)" if tp_mode
-                                       else f"segment-parallel replicas x{world}" if world > 1 else "single GPU"),
-                       "l2": "inputs larger than L2 (every step streams all 6L+1 weight matrices)",
-                       "step_tflop": step_flops / 1e12, "achieved_step_tflops": step_flops / (ms / 1e3) / 1e12},
+            "config": config_dict(wl, tokens_per_rank, world, tp_mode, step_flops, ms),
+            "achieved_step_tflops": step_flops * (1 if tp_mode else world) / (ms / 1e3) / 1e12,
             "roofline": ({"bound": "tensor", "kernel": "seg_gemm_kernel (fused base GEMM + LoRA/IA3 epilogue)",
                           "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
                           "frac": (gemm_tflops / peak) if gemm_tflops else None, "traffic": traffic,
@@ -812,6 +1029,7 @@ def main():
                                         else "the timed steps",
                          "gather_gbs": (gather["bytes"] / (gather["ms"] / 1e3) / 1e9) if gather["ms"] else None},
             "adapter_grads": grads_leg,
+            "tensor_parallel": tp_info,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
             "launch_mode": "CUDA graph of prebuilt dispatch plans" if graph is not None else "eager prebuilt dispatch plans",
         }

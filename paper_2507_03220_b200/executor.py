@@ -192,6 +192,15 @@ def _host_tensor_info(t: torch.Tensor):
     return (t.dtype, tuple(t.shape))
 
 
+def _host_tensor(a: np.ndarray) -> torch.Tensor:
+    """Zero-copy CPU tensor over a numpy array (read-only arrays too: the library only reads
+    request rows)."""
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)   # non-writable arrays (frozen payloads)
+        return torch.from_numpy(a)
+
+
 def _cached_info(cache: dict, t: torch.Tensor):
     hit = cache.get(id(t))
     ptr = t.data_ptr()
@@ -460,6 +469,10 @@ class GpuBaseExecutor:
             self.ledger.set(ledger_mod.TRANSIENT_BUFFER, rows * (expected + out_w) * 2)
             self.ledger.set(ledger_mod.TRANSIENT_BUFFER, 0)
             return results
+        if self.numpy_native and self._all_numpy(envelopes, good):
+            with torch.cuda.device(self.device):
+                return self._numpy_host(pass_kind, key, envelopes, good, out_w, stream, results, addr,
+                                        expected)
         with torch.cuda.device(self.device), torch.cuda.stream(stream):
             for i in good:
                 ev = getattr(envelopes[i], "ready", None)
@@ -574,6 +587,49 @@ class GpuBaseExecutor:
                 self._host_memo.clear()
             self._host_memo[memo[0]] = (table._keep, memo[1], table)   # (table holds the tensors)
         return status
+
+    # -- numpy clients (the reference's LocalChannel / RemoteChannel payloads) ----------------
+    numpy_native = True   # False: the staged path below (one H2D / D2H per dispatch, synchronous)
+
+    def _all_numpy(self, envelopes, good) -> bool:
+        if self.save_activations:
+            return False
+        for i in good:
+            e = envelopes[i]
+            if not isinstance(e.payload, np.ndarray) or getattr(e, "reply_to", None) is not None or \
+                    getattr(e, "base_to", None) is not None or getattr(e, "ready", None) is not None:
+                return False
+        return True
+
+    def _numpy_host(self, pass_kind, key, envelopes, good, out_w, stream, results, addr, expected) -> list:
+        """f32 numpy payloads (what the reference's channels carry, transport.py:36, 78) through
+        the native host pipeline (ss_compute_batch_host): the H2D of row sub-batch j+1, the
+        kernels of j and the D2H of j-1 overlap, straight from / into the client arrays (no
+        executor-side host copy). The replies are row views of ONE fresh f32 array per dispatch,
+        like split_rows' views of the reference's ``out`` (tensor_ops.py:149-156)."""
+        rows = sum(envelopes[i].token_count for i in good)
+        out = np.empty((rows, out_w), dtype=np.float32)
+        fused = self._fused
+        segs, views, pos = [], [], 0
+        for i in good:
+            e = envelopes[i]
+            p = e.payload
+            if p.dtype != np.float32 or not p.flags.c_contiguous:
+                p = np.ascontiguousarray(p, dtype=np.float32)
+            t = e.token_count
+            view = out[pos:pos + t]
+            views.append(view)
+            pos += t
+            segs.append(Seg(client_id=e.client_id, src=_host_tensor(p), dst=torch.from_numpy(view),
+                            width=e.width, adapter=key in fused.get(e.client_id, ())))
+        status = self.ctx.compute_host(pass_kind, key[0], key[1], segs, stream)
+        self.last_event = None
+        for j, i in enumerate(good):
+            results[i] = (ProtocolError(f"executor rejected segment (status {status[j]}) for layer {addr}")
+                          if status[j] != _lib.SS_SEG_OK else views[j])
+        self.ledger.set(ledger_mod.TRANSIENT_BUFFER, rows * (expected + out_w) * 4)
+        self.ledger.set(ledger_mod.TRANSIENT_BUFFER, 0)
+        return results
 
     # -- staging helpers --------------------------------------------------------------------
     def _stage_inputs(self, envelopes, good, stream):

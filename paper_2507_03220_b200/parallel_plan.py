@@ -183,7 +183,8 @@ def comm_bytes_per_token(d_in: int, d_out: int, role, pass_kind: int, world: int
     width = spec.d_out if pass_kind != 1 else spec.d_in
     f = (world - 1) / world
     if spec.collective(pass_kind) == "all_reduce":
-        return 2 * f * width * esz
+        # reduce-scatter of fp32 partials + all-gather of the bf16 rows (dispatch_buffers)
+        return f * width * (4 + esz)
     return f * width * esz
 
 
@@ -191,34 +192,50 @@ def ratio_check(a, b, rtol=1e-5, atol=1e-5) -> bool:
     return np.allclose(np.asarray(a, np.float64), np.asarray(b, np.float64), rtol=rtol, atol=atol)
 
 
-def dispatch_buffers(spec: ShardSpec, pass_kind: int, rows: int, world: int, rank: int, alloc):
+def dispatch_buffers(spec: ShardSpec, pass_kind: int, rows: int, world: int, rank: int, alloc, tag=""):
     """Buffers of one prebuilt tensor-parallel dispatch: returns (kind, local, gbuf, reply).
-    `local` is what this rank's kernels write (fp32 [rows, full] partials for an all-reduce; a
-    column view of a padded bf16 shard buffer for an all-gather; the reply itself at world size
-    1). `alloc(tag, shape, dtype)` provides (possibly shared) tensors."""
+
+    `local` is what this rank's kernels write:
+    * all-reduce layers: fp32 partials [rows, full] (rows of a buffer padded to a multiple of
+      the world size). The collective is a REDUCE-SCATTER of the fp32 partials (each rank sums
+      1/world of the rows exactly, in fp32), one bf16 rounding, then an ALL-GATHER of bf16 rows
+      straight into the reply: (world-1)/world x (4 + 2) bytes per element instead of an fp32
+      all-reduce's 2 x 4, and the same single rounding as on one GPU;
+    * all-gather layers: a column view of a padded bf16 shard buffer;
+    * world size 1: the reply itself.
+    `alloc(tag, shape, dtype)` provides (possibly shared) tensors; `tag` separates the buffers of
+    pipelined slabs of one dispatch."""
     import torch
     full = spec.d_in if pass_kind == 1 else spec.d_out
-    reply = alloc("reply", (rows, full), torch.bfloat16)
     kind = spec.collective(pass_kind) if world > 1 else "none"
     if kind == "all_reduce":
-        return kind, alloc("partial", (rows, full), torch.float32), None, reply
+        rows_pad = -(-rows // world) * world
+        part = alloc("partial" + tag, (rows_pad, full), torch.float32)
+        rs = alloc("rs" + tag, (rows_pad // world, full), torch.float32)
+        rs_bf = alloc("rs_bf16" + tag, (rows_pad // world, full), torch.bfloat16)
+        gathered = alloc("gathered_rows" + tag, (rows_pad, full), torch.bfloat16)
+        return kind, part[:rows], (part, rs, rs_bf, gathered), gathered[:rows]
+    reply = alloc("reply" + tag, (rows, full), torch.bfloat16)
     if kind == "all_gather":
         sizes = [shard_bounds(spec.d_out if spec.split == "column" else spec.d_in, q, world) for q in range(world)]
         wmax = max(hi - lo for lo, hi in sizes)
-        pad = alloc("shard", (rows, wmax), torch.bfloat16)
+        pad = alloc("shard" + tag, (rows, wmax), torch.bfloat16)
         local = pad[:, : sizes[rank][1] - sizes[rank][0]]
-        return kind, local, (pad, alloc("gathered", (world * rows, wmax), torch.bfloat16), sizes), reply
+        return kind, local, (pad, alloc("gathered" + tag, (world * rows, wmax), torch.bfloat16), sizes), reply
     return kind, reply, None, reply
 
 
 def finish_dispatch(kind: str, local, gbuf, reply, group=None) -> None:
-    """The dispatch's one collective, landing the full-width result in `reply` on every rank:
-    all-reduce the fp32 partials (then round once to bf16), or all-gather the padded column
-    shards and reassemble them."""
+    """The dispatch's collective, landing the full-width result in `reply` on every rank:
+    reduce-scatter the fp32 partials, round once to bf16, all-gather the rows (all-reduce
+    layers); or all-gather the padded column shards and reassemble them (all-gather layers).
+    Runs on the caller's current CUDA stream (a comm stream when slabs are pipelined)."""
     import torch.distributed as dist
     if kind == "all_reduce":
-        dist.all_reduce(local, op=dist.ReduceOp.SUM, group=group)
-        reply.copy_(local)
+        part, rs, rs_bf, gathered = gbuf
+        dist.reduce_scatter_tensor(rs, part, op=dist.ReduceOp.SUM, group=group)
+        rs_bf.copy_(rs)
+        dist.all_gather_into_tensor(gathered, rs_bf, group=group)   # `reply` is a view of it
     elif kind == "all_gather":
         pad, out, sizes = gbuf
         dist.all_gather_into_tensor(out, pad, group=group)
