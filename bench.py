@@ -351,7 +351,7 @@ def build_tp_workload(wl_key, device, rank, world):
         spec = tp.specs[(b, r)]
         w_in = do if pass_kind == 1 else di
         parts = []
-        n = max(1, min(TP_SLABS, len(cids)))
+        n = 1 if world == 1 else max(1, min(TP_SLABS, len(cids)))   # (nothing to overlap alone)
         groups = [cids[i * len(cids) // n:(i + 1) * len(cids) // n] for i in range(n)]
         for k, grp in enumerate(groups):
             kind, local, gbuf, reply = P.dispatch_buffers(spec, pass_kind, len(grp) * t, world, rank, buf, tag=f"/{k}")
@@ -492,8 +492,11 @@ def e2e_numpy_leg(ex, wl_key, specs, steps):
     through GpuBaseExecutor.serve_forward / serve_backward with no reply buffer (the executor
     returns f32 numpy row views, like split_rows). Each dispatch runs the native host pipeline
     (ss_compute_batch_host: H2D of sub-batch j+1 / kernels of j / D2H of j-1 overlapped, from
-    and into pageable client memory). Warm-up: block 0 and LM_HEAD only (the shapes of every
-    dispatch); then `steps` full timed steps."""
+    the pageable client arrays into recycled page-locked reply arrays). A full step moves
+    ~630 GB over PCIe at 13B, so this leg times a bounded sample — block 0 (6 layers) and
+    LM_HEAD, forward for every client and backward for the fine-tune clients, `steps` times
+    after one warm-up — and scales it like the CPU baseline: step = L x t_block + t_head
+    (blocks are identical)."""
     from paper_2507_03220_b200 import Envelope
 
     wl = WORKLOADS[wl_key]
@@ -506,7 +509,6 @@ def e2e_numpy_leg(ex, wl_key, specs, steps):
     moved = [0, 0]
 
     def run(layer_set):
-        moved[0] = moved[1] = 0
         for (b, r) in layer_set:
             di, do = dims[r]
             envs = []
@@ -527,12 +529,26 @@ def e2e_numpy_leg(ex, wl_key, specs, steps):
                     moved[1] += t * di * 4
             ex.serve_backward(envs)
 
-    run([l for l in layers if l[0] in (0, wl["L"])])
-    t0 = time.perf_counter()
+    block = [l for l in layers if l[0] == 0]
+    head = [l for l in layers if l[0] == wl["L"]]
+    run(block + head)
+    tb = th = 0.0
     for _ in range(steps):
-        run(layers)
-    dt = (time.perf_counter() - t0) / steps
-    return dt, moved[0], moved[1]
+        t0 = time.perf_counter()
+        run(block)
+        tb += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        run(head)
+        th += time.perf_counter() - t0
+    tb, th = tb / steps, th / steps
+    moved[0] = moved[1] = 0
+    run([])
+    for l in layers:           # byte count of one full step (no compute)
+        di, do = dims[l[1]]
+        n_ft = sum(1 for s_ in specs if s_[2])
+        moved[0] += t * (len(specs) * di + n_ft * do) * 4
+        moved[1] += t * (len(specs) * do + n_ft * di) * 4
+    return wl["L"] * tb + th, moved[0], moved[1], (tb, th)
 
 
 # ============================================================================ CPU leg (oracle)
@@ -746,8 +762,8 @@ def main():
                     help="host-only (gloo) run of the launcher / timing / JSON contract (CPU tests)")
     ap.add_argument("--no-tp-leg", action="store_true",
                     help="N > 1 replicas run: skip the tensor-parallel leg reported beside it")
-    ap.add_argument("--e2e-numpy-steps", type=int, default=1,
-                    help="timed steps of the f32-numpy e2e leg (0: skip)")
+    ap.add_argument("--e2e-numpy-steps", type=int, default=2,
+                    help="timed samples of the f32-numpy e2e leg (0: skip)")
     ap.add_argument("--parallel", default="replicas", choices=("replicas", "tp"),
                     help="replicas: segment-parallel full replicas (weak scaling, no data-path "
                          "collective); tp: column/row-sharded layers + NCCL per dispatch (strong)")
@@ -966,7 +982,7 @@ def main():
                "path": "GpuBaseExecutor.serve_forward / serve_backward, pinned host bf16 payloads + host reply buffers, "
                        f"{e2e_steps} timed step(s) after 1 warm-up"}
         if args.e2e_numpy_steps > 0:
-            dt_n, h2d_n, d2h_n = e2e_numpy_leg(ex, args.workload, specs, args.e2e_numpy_steps)
+            dt_n, h2d_n, d2h_n, (tb_n, th_n) = e2e_numpy_leg(ex, args.workload, specs, args.e2e_numpy_steps)
             if world > 1:
                 t = torch.tensor([dt_n], device=device)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -975,7 +991,10 @@ def main():
                                 "d2h_bytes_per_step": d2h_n, "ms_per_step": dt_n * 1e3,
                                 "path": "GpuBaseExecutor.serve_forward / serve_backward, f32 numpy payloads "
                                         "(the reference channels' payload type), replies returned as f32 numpy "
-                                        f"views; native host pipeline; {args.e2e_numpy_steps} timed step(s)"}
+                                        "views; native host pipeline",
+                                "sample": f"block 0 ({tb_n * 1e3:.0f} ms) + LM_HEAD ({th_n * 1e3:.0f} ms), fwd all "
+                                          f"clients + bwd FT clients, mean of {args.e2e_numpy_steps} after 1 "
+                                          f"warm-up; step = L x block + head"}
 
     tp_info = None
     if world > 1 and not tp_mode and not args.no_tp_leg:

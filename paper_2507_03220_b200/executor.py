@@ -251,6 +251,7 @@ class GpuBaseExecutor:
         self.metrics = ExecutorMetrics()
         self.ledger = ledger_mod.MemoryLedger("executor")
         self._pinned: dict[str, torch.Tensor] = {}
+        self._np_pool: list = []         # (pinned tensor, its numpy base) reply arrays (_numpy_out)
         # pinned-host checks of client payload / reply tensors, per live tensor object:
         # id -> (weakref, info) (tensors compare elementwise, so they cannot be dict keys)
         self._host_info: dict[int, tuple] = {}
@@ -608,28 +609,57 @@ class GpuBaseExecutor:
         executor-side host copy). The replies are row views of ONE fresh f32 array per dispatch,
         like split_rows' views of the reference's ``out`` (tensor_ops.py:149-156)."""
         rows = sum(envelopes[i].token_count for i in good)
-        out = np.empty((rows, out_w), dtype=np.float32)
+        out = self._numpy_out(rows, out_w)
         fused = self._fused
-        segs, views, pos = [], [], 0
+        segs, views, seg_of, pos = [], [], [], 0
         for i in good:
             e = envelopes[i]
-            p = e.payload
-            if p.dtype != np.float32 or not p.flags.c_contiguous:
-                p = np.ascontiguousarray(p, dtype=np.float32)
             t = e.token_count
             view = out[pos:pos + t]
             views.append(view)
             pos += t
+            if t == 0:                 # (empty arrays have zero strides; nothing to compute)
+                seg_of.append(-1)
+                continue
+            p = e.payload
+            if p.dtype != np.float32 or not p.flags.c_contiguous:
+                p = np.ascontiguousarray(p, dtype=np.float32)
+            seg_of.append(len(segs))
             segs.append(Seg(client_id=e.client_id, src=_host_tensor(p), dst=torch.from_numpy(view),
                             width=e.width, adapter=key in fused.get(e.client_id, ())))
-        status = self.ctx.compute_host(pass_kind, key[0], key[1], segs, stream)
+        status = self.ctx.compute_host(pass_kind, key[0], key[1], segs, stream) if segs else []
         self.last_event = None
         for j, i in enumerate(good):
-            results[i] = (ProtocolError(f"executor rejected segment (status {status[j]}) for layer {addr}")
-                          if status[j] != _lib.SS_SEG_OK else views[j])
+            st = status[seg_of[j]] if seg_of[j] >= 0 else _lib.SS_SEG_OK
+            results[i] = (ProtocolError(f"executor rejected segment (status {st}) for layer {addr}")
+                          if st != _lib.SS_SEG_OK else views[j])
         self.ledger.set(ledger_mod.TRANSIENT_BUFFER, rows * (expected + out_w) * 4)
         self.ledger.set(ledger_mod.TRANSIENT_BUFFER, 0)
         return results
+
+    numpy_out_pool = 8    # page-locked reply arrays kept for reuse (0: fresh pageable arrays)
+
+    def _numpy_out(self, rows: int, width: int) -> np.ndarray:
+        """A [rows, width] f32 reply array in PAGE-LOCKED memory, recycled: an entry is reused
+        only when no view of it is alive any more (numpy views keep their base array referenced,
+        so the base's reference count says whether a caller still holds a reply). The reference
+        LocalChannel copies each reply into its shared buffer at once (transport.py:91-98), so
+        its replies free their entry immediately; D2H copies into page-locked memory run at
+        copy-engine speed instead of through the driver's pageable staging + page faults."""
+        import sys
+        need = rows * width
+        pool = self._np_pool
+        for entry in pool:
+            base = entry[1]
+            if base.size >= need and sys.getrefcount(base) <= 3:   # pool list + local + getrefcount arg
+                return base[:need].reshape(rows, width)
+        if len(pool) >= self.numpy_out_pool or need == 0:
+            return np.empty((rows, width), dtype=np.float32)
+        cap = 1 << max(20, (need - 1).bit_length())
+        t = torch.empty(cap, dtype=torch.float32, pin_memory=True)
+        base = t.numpy()
+        pool.append((t, base))
+        return base[:need].reshape(rows, width)
 
     # -- staging helpers --------------------------------------------------------------------
     def _stage_inputs(self, envelopes, good, stream):
