@@ -217,6 +217,48 @@ typedef struct ss_grad_seg {
 SS_API int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_seg* segs,
                             void* stream, int32_t* seg_status);
 
+/* ---- cross-process device hand-off (CUDA IPC) ---------------------------------------------
+ * The paper's co-located mode shares a pre-allocated CUDA exchange tensor between the client
+ * process and the executor process (share_memory_() / rebuild_cuda_tensor());
+ * the reference package's process mode (harness.py:243-260 _process_worker, :367-394
+ * _run_processes) otherwise serialises every payload through host memory and a socket
+ * (RemoteChannel / ExecutorServer, transport.py:104-275). With these calls a client process
+ * exports its request / reply / y_base buffers once per grow (SharedBuffer's grow-only rule,
+ * transport.py:28-49) and the executor process maps them; the segments of ss_compute_batch
+ * then point straight into the client's memory (a client on another GPU: peer memory over
+ * NVLink). Stream ordering between the processes uses interprocess events: the client records
+ * one after writing a request, the executor's stream waits on it; the executor records its
+ * own after the reply, the client's stream waits on that. No ss_ctx needed; errors of these
+ * calls are reported by ss_ipc_last_error() (per thread). */
+typedef struct ss_ipc_mem {
+  uint8_t handle[64];   /* cudaIpcMemHandle_t of the allocation that holds the buffer */
+  uint64_t offset;      /* byte offset of the buffer inside that allocation */
+  uint64_t bytes;
+  int32_t device;       /* CUDA device of the exporting process's allocation */
+  uint32_t reserved;
+} ss_ipc_mem;
+typedef struct ss_ipc_evt {
+  uint8_t handle[64];   /* cudaIpcEventHandle_t */
+} ss_ipc_evt;
+SS_API const char* ss_ipc_last_error(void);
+/* client side: export any cudaMalloc'd range (e.g. a torch tensor's storage), or allocate a
+ * dedicated exchange buffer and export it */
+SS_API int ss_ipc_export(const void* dptr, uint64_t bytes, ss_ipc_mem* out);
+SS_API int ss_ipc_alloc(int device, uint64_t bytes, void** dptr, ss_ipc_mem* out);
+SS_API int ss_ipc_free(void* dptr);
+/* executor side: map an exported buffer (one mapping per allocation per process, reference
+ * counted: opening the same handle twice returns pointers into one mapping); close unmaps the
+ * last reference. The caller must have ordered any work touching the buffer before close. */
+SS_API int ss_ipc_open(int device, const ss_ipc_mem* mem, void** dptr);
+SS_API int ss_ipc_close(void* dptr);
+/* interprocess events (cudaEventInterprocess | cudaEventDisableTiming) */
+SS_API int ss_ipc_event_create(int device, void** event, ss_ipc_evt* out);
+SS_API int ss_ipc_event_open(int device, const ss_ipc_evt* h, void** event);
+SS_API int ss_ipc_event_record(void* event, void* stream);
+SS_API int ss_ipc_event_wait(void* stream, void* event);
+SS_API int ss_ipc_event_sync(void* event);
+SS_API int ss_ipc_event_destroy(void* event);
+
 /* Device bytes held: weights (+bias), adapter packs, transient workspace high-water mark. */
 SS_API int ss_memory_stats(const ss_ctx* ctx, int64_t* weight_bytes, int64_t* adapter_bytes,
                     int64_t* workspace_bytes);

@@ -4,6 +4,7 @@ Public surface (drop-in for the reference's executor / channel / interception la
 
 * ``GpuBaseExecutor``, ``BatchPolicy``, ``ExecutorMetrics``  — executor.py
 * ``DeviceChannel``, ``DeviceBuffer``                          — channel.py
+* ``IpcChannel``, ``IpcExecutorServer`` (client processes, CUDA IPC) — ipc.py
 * ``VirtLayer``                                                — client.py
 * ``Envelope`` / ``PASS_*``, ``LayerAddress`` / ``Role``, ``AffineParams``, ``MemoryLedger``
 * ``SsContext`` — the raw C-ABI context (libss_b200.so, include/ss_b200.h)
@@ -31,6 +32,9 @@ def __getattr__(name):  # lazy: torch-heavy modules load on first use
     if name in ("DeviceChannel", "DeviceBuffer"):
         from . import channel
         return getattr(channel, name)
+    if name in ("IpcChannel", "IpcExecutorServer", "IpcBuffer", "IpcEvent"):
+        from . import ipc
+        return getattr(ipc, name)
     if name == "VirtLayer":
         from .client import VirtLayer
         return VirtLayer

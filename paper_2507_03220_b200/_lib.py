@@ -53,6 +53,9 @@ EXPORTED = (
     "ss_compute_batch", "ss_memory_stats", "ss_kernel_launches", "ss_set_option",
     "ss_profile", "ss_profile_read", "ss_adapter_grads", "ss_plan_create", "ss_plan_launch",
     "ss_plan_destroy", "ss_compute_batch_host", "ss_serve_frames", "ss_ctx_epoch",
+    "ss_ipc_last_error", "ss_ipc_export", "ss_ipc_alloc", "ss_ipc_free", "ss_ipc_open",
+    "ss_ipc_close", "ss_ipc_event_create", "ss_ipc_event_open", "ss_ipc_event_record",
+    "ss_ipc_event_wait", "ss_ipc_event_sync", "ss_ipc_event_destroy",
 )
 
 SS_KERNEL_GATHER = 0
@@ -92,6 +95,21 @@ class SsGradSeg(ctypes.Structure):
         ("grad_b", ctypes.c_void_p),
         ("grad_l", ctypes.c_void_p),
     ]
+
+
+class SsIpcMem(ctypes.Structure):
+    """ss_ipc_mem: an exported device buffer (CUDA IPC handle + offset in its allocation)."""
+    _fields_ = [
+        ("handle", ctypes.c_uint8 * 64),
+        ("offset", ctypes.c_uint64),
+        ("bytes", ctypes.c_uint64),
+        ("device", ctypes.c_int32),
+        ("reserved", ctypes.c_uint32),
+    ]
+
+
+class SsIpcEvt(ctypes.Structure):
+    _fields_ = [("handle", ctypes.c_uint8 * 64)]
 
 
 class LibraryMissing(RuntimeError):
@@ -149,6 +167,18 @@ def load() -> ctypes.CDLL:
             "ss_profile": (i32, [vp, i32]),
             "ss_profile_read": (i32, [vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64),
                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+            "ss_ipc_last_error": (ctypes.c_char_p, []),
+            "ss_ipc_export": (i32, [vp, ctypes.c_uint64, ctypes.POINTER(SsIpcMem)]),
+            "ss_ipc_alloc": (i32, [i32, ctypes.c_uint64, ctypes.POINTER(vp), ctypes.POINTER(SsIpcMem)]),
+            "ss_ipc_free": (i32, [vp]),
+            "ss_ipc_open": (i32, [i32, ctypes.POINTER(SsIpcMem), ctypes.POINTER(vp)]),
+            "ss_ipc_close": (i32, [vp]),
+            "ss_ipc_event_create": (i32, [i32, ctypes.POINTER(vp), ctypes.POINTER(SsIpcEvt)]),
+            "ss_ipc_event_open": (i32, [i32, ctypes.POINTER(SsIpcEvt), ctypes.POINTER(vp)]),
+            "ss_ipc_event_record": (i32, [vp, vp]),
+            "ss_ipc_event_wait": (i32, [vp, vp]),
+            "ss_ipc_event_sync": (i32, [vp]),
+            "ss_ipc_event_destroy": (i32, [vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -156,6 +186,12 @@ def load() -> ctypes.CDLL:
             fn.argtypes = args
         _lib = lib
         return lib
+
+
+def check_ipc(rc: int) -> None:
+    if rc != SS_OK:
+        msg = load().ss_ipc_last_error() or b""
+        raise SsError(rc, msg.decode("utf-8", "replace"))
 
 
 def check(ctx, rc: int) -> None:

@@ -36,6 +36,20 @@ def test_struct_layout_matches_header():
     # ss_grad_seg: 4 x u32 + (ptr, i64) x 3 + 3 ptrs
     assert ctypes.sizeof(_lib.SsGradSeg) == 88
     assert _lib.SsGradSeg.x.offset == 16 and _lib.SsGradSeg.grad_a.offset == 64
+    # ss_ipc_mem: 64-byte cudaIpcMemHandle_t + u64 offset + u64 bytes + i32 device + u32
+    assert ctypes.sizeof(_lib.SsIpcMem) == 88 and _lib.SsIpcMem.offset.offset == 64
+    assert ctypes.sizeof(_lib.SsIpcEvt) == 64
+
+
+def test_ipc_calls_fail_cleanly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = _lib.load()
+    ptr, mem = ctypes.c_void_p(), _lib.SsIpcMem()
+    assert lib.ss_ipc_alloc(0, 1024, ctypes.byref(ptr), ctypes.byref(mem)) != _lib.SS_OK
+    assert not ptr.value and lib.ss_ipc_last_error()
+    assert lib.ss_ipc_export(None, 0, ctypes.byref(mem)) == _lib.SS_E_ARG
 
 
 def test_context_creation_fails_cleanly_without_gpu():
