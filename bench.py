@@ -487,6 +487,82 @@ def e2e_leg(ex, wl_key, specs, steps, device):
     return dt, h2d, d2h
 
 
+def submit_leg(ex, wl_key, specs, steps, mode="lockstep", scheduler="python"):
+    """The full client path: one thread per client, each driving its layer sequence through
+    ``DeviceChannel.request`` -> ``GpuBaseExecutor.submit`` -> the scheduler thread's batch
+    formation (``BatchPolicy`` ``mode``) -> one fused dispatch per layer -> reply + completion
+    event (executor.py:162-178, 235-300 in the reference). Wall clock around ``steps`` steps of
+    every client (after one warm-up step), synchronized: this is what the Python scheduler and
+    per-request host work cost next to the graph-replayed ``value``."""
+    import torch
+    from paper_2507_03220_b200 import BatchPolicy, DeviceChannel
+
+    wl = WORKLOADS[wl_key]
+    layers, dims = layer_list(wl)
+    t = wl["tokens"]
+    maxw = max(wl["d"], wl["d_ff"], wl["V"])
+    old_policy, old_sched = ex.policy, ex.scheduler
+    ex.policy = BatchPolicy(mode=mode)
+    ex.scheduler = scheduler
+    ex._metrics = type(ex._metrics)()
+    ex.start()
+    chans = []
+    for c, (kind, _, ft) in enumerate(specs):
+        ch = DeviceChannel(ex, c, 1, t, maxw)
+        ch.buffer.buf.normal_()
+        ch.register(sends_backward=ft)
+        chans.append(ch)
+    n_req = [0]
+    barrier = threading.Barrier(len(specs) + 1)
+    errors = []
+
+    def client(c):
+        kind, _, ft = specs[c]
+        ch = chans[c]
+        try:
+            for _ in range(steps + 1):
+                barrier.wait()
+                for (b, r) in layers:
+                    di, do = dims[r]
+                    want = kind == "ia3" and ft and r in (K, V, FF_UP)
+                    # the payload is the channel's own request buffer: no client-side copy
+                    ch.request(b, r, 0, ch.buffer.view(t, di), want_base=want)
+                if ft:
+                    for (b, r) in reversed(layers):
+                        di, do = dims[r]
+                        ch.request(b, r, 1, ch.buffer.view(t, do))
+                barrier.wait()
+        except Exception as exc:   # noqa: BLE001
+            errors.append(repr(exc))
+            barrier.abort()
+
+    threads = [threading.Thread(target=client, args=(c,), daemon=True) for c in range(len(specs))]
+    for th in threads:
+        th.start()
+    times = []
+    try:
+        for i in range(steps + 1):
+            barrier.wait()
+            t0 = time.perf_counter()
+            barrier.wait()
+            torch.cuda.synchronize()
+            if i:
+                times.append(time.perf_counter() - t0)
+    except threading.BrokenBarrierError:
+        pass
+    for th in threads:
+        th.join(timeout=60)
+    for ch in chans:
+        ch.deregister()
+    ex.stop()
+    ex.policy, ex.scheduler = old_policy, old_sched
+    if errors:
+        raise RuntimeError(errors[0])
+    n_req = sum(len(layers) * (2 if ft else 1) for _, _, ft in specs)
+    dispatches = len(ex.metrics.batch_sizes) and sum(len(v) for v in ex.metrics.batch_sizes.values())
+    return float(np.mean(times)), n_req, dispatches
+
+
 def e2e_numpy_leg(ex, wl_key, specs, steps):
     """The reference's own payload type: f32 NUMPY activations (transport.py:36, 78), sent
     through GpuBaseExecutor.serve_forward / serve_backward with no reply buffer (the executor
@@ -764,6 +840,8 @@ def main():
                     help="N > 1 replicas run: skip the tensor-parallel leg reported beside it")
     ap.add_argument("--e2e-numpy-steps", type=int, default=2,
                     help="timed samples of the f32-numpy e2e leg (0: skip)")
+    ap.add_argument("--submit-steps", type=int, default=2,
+                    help="timed steps of the client-thread submit() leg (0: skip)")
     ap.add_argument("--parallel", default="replicas", choices=("replicas", "tp"),
                     help="replicas: segment-parallel full replicas (weak scaling, no data-path "
                          "collective); tp: column/row-sharded layers + NCCL per dispatch (strong)")
@@ -996,6 +1074,25 @@ def main():
                                           f"clients + bwd FT clients, mean of {args.e2e_numpy_steps} after 1 "
                                           f"warm-up; step = L x block + head"}
 
+    submit = None
+    if args.submit_steps > 0 and not tp_mode:
+        submit = {}
+        for sched in ("native", "python"):
+            try:
+                dt_s, n_req, n_disp = submit_leg(ex, args.workload, specs, args.submit_steps, scheduler=sched)
+                submit[sched] = {
+                    "value": tokens_per_rank / dt_s, "unit": "tokens/s", "ms_per_step": dt_s * 1e3,
+                    "requests_per_step": n_req, "requests_per_s": n_req / dt_s,
+                    "dispatches_recorded": n_disp, "policy": "lockstep",
+                    "path": f"{len(specs)} client threads, DeviceChannel.request -> "
+                            + ("ss_sched_request (library scheduler thread: batch formation + dispatch)"
+                               if sched == "native" else
+                               "GpuBaseExecutor.submit -> Python scheduler thread batch formation")
+                            + " -> one fused dispatch per layer and pass (no plans, no graph); wall clock, "
+                            f"{args.submit_steps} step(s) after 1 warm-up"}
+            except Exception as exc:   # noqa: BLE001 — the headline line must still print
+                submit[sched] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     tp_info = None
     if world > 1 and not tp_mode and not args.no_tp_leg:
         try:
@@ -1048,6 +1145,7 @@ def main():
                                         else "the timed steps",
                          "gather_gbs": (gather["bytes"] / (gather["ms"] / 1e3) / 1e9) if gather["ms"] else None},
             "adapter_grads": grads_leg,
+            "submit_path": submit,
             "tensor_parallel": tp_info,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
             "launch_mode": "CUDA graph of prebuilt dispatch plans" if graph is not None else "eager prebuilt dispatch plans",

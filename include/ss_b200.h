@@ -217,6 +217,79 @@ typedef struct ss_grad_seg {
 SS_API int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_seg* segs,
                             void* stream, int32_t* seg_status);
 
+/* Dims of a loaded layer (SS_E_NOLAYER if absent); device of a context. */
+SS_API int ss_layer_dims(ss_ctx* ctx, int block, int role, int* d_in, int* d_out);
+SS_API int ss_ctx_device(const ss_ctx* ctx);
+
+/* ---- native scheduler: batch formation + dispatch off the Python interpreter --------------
+ * The reference's executor forms batches in a scheduler thread: submit() validates and queues
+ * an envelope per (block, role, pass) (executor.py:162-178), _loop/_pick_ready pick a ripe
+ * queue under the BatchPolicy (executor.py:235-283: nolockstep = one request per dispatch;
+ * lockstep = wait until every registered client -- every backward sender for backward --
+ * has a request queued; opportunistic = dispatch when the queue holds max_batch_tokens, or
+ * when its oldest member has waited min(wait_cap, wait_per_token * smallest member's tokens);
+ * the noise pass is never batched), _dispatch computes it and replies (executor.py:285-300).
+ * ss_sched_* runs exactly that loop on a native thread over DEVICE-resident requests: a client
+ * thread's ss_sched_request() is one call that queues the request and blocks (without the
+ * Python GIL: ctypes releases it) until the batch holding it has been launched, then makes the
+ * client's stream wait for that batch's completion; the scheduler thread makes its stream wait
+ * for each request's `ready` event, runs ss_compute_batch, and records one completion event per
+ * batch. Validation mirrors submit(): unknown pass, non-increasing request_id per client,
+ * unknown layer complete immediately with a request status (the width check is the batch's
+ * per-segment status). Results are bitwise those of ss_compute_batch on the same batch. */
+#define SS_SCHED_NOLOCKSTEP 0
+#define SS_SCHED_LOCKSTEP 1
+#define SS_SCHED_OPPORTUNISTIC 2
+/* request status: SS_SEG_* (0 = computed) or */
+#define SS_REQ_BAD_PASS 16    /* "unknown pass {pass}" executor.py:163-165 */
+#define SS_REQ_BAD_ID 17      /* "request_id {id} not increasing (last {aux})" executor.py:166-171 */
+#define SS_REQ_NO_LAYER 18    /* "unknown layer {layer}" executor.py:172-174 */
+#define SS_REQ_FAILED 19      /* the batch's dispatch failed (ss_sched_last_error) */
+typedef struct ss_sched_policy {
+  int32_t mode;               /* SS_SCHED_* */
+  int32_t reserved;
+  double wait_per_token;      /* seconds */
+  double wait_cap;            /* seconds */
+  int64_t max_batch_tokens;
+} ss_sched_policy;
+typedef struct ss_request {
+  uint32_t client_id;
+  uint32_t pass_kind;
+  int32_t block;
+  int32_t role;
+  uint64_t request_id;
+  ss_seg seg;                 /* rows, width, flags, src / dst / dst_base (device); client_id unused */
+  void* ready;                /* cudaEvent_t recorded after the payload was written, or NULL */
+} ss_request;
+typedef struct ss_sched_rec { /* one per request of a dispatched batch */
+  uint64_t dispatch;          /* dispatch sequence number (requests of one batch share it) */
+  int32_t block, role, pass_kind, rows;
+  double wait_s;              /* queued -> batch picked */
+} ss_sched_rec;
+typedef struct ss_sched ss_sched;
+SS_API int ss_sched_create(ss_ctx* ctx, const ss_sched_policy* policy, void* stream, ss_sched** out);
+/* stops the thread after the queued requests are dispatched (drain != 0) or failed (drain == 0) */
+SS_API int ss_sched_destroy(ss_sched* s, int drain);
+SS_API int ss_sched_set_policy(ss_sched* s, const ss_sched_policy* policy);
+SS_API int ss_sched_register(ss_sched* s, uint32_t client_id, int sends_backward);
+SS_API int ss_sched_deregister(ss_sched* s, uint32_t client_id);
+/* queue a request; notify != 0: its completion is also reported by ss_sched_next_done */
+SS_API int ss_sched_submit(ss_sched* s, const ss_request* req, int notify, uint64_t* ticket);
+/* block until `ticket` completed (timeout_us < 0: forever); on completion make `wait_stream`
+ * wait for its batch (if not NULL). Returns SS_OK, or SS_E_ARG (unknown ticket) / 1 (timeout). */
+SS_API int ss_sched_wait(ss_sched* s, uint64_t ticket, void* wait_stream, int64_t timeout_us,
+                         int32_t* status, int64_t* aux);
+/* ss_sched_submit + ss_sched_wait in one call */
+SS_API int ss_sched_request(ss_sched* s, const ss_request* req, void* wait_stream, int64_t timeout_us,
+                            int32_t* status, int64_t* aux);
+/* next completed notify-ticket in completion order (1 = timeout, nothing completed) */
+SS_API int ss_sched_next_done(ss_sched* s, void* wait_stream, int64_t timeout_us, uint64_t* ticket,
+                              int32_t* status, int64_t* aux);
+/* move up to `cap` dispatch records out of the scheduler's log; *n = records returned */
+SS_API int ss_sched_log(ss_sched* s, ss_sched_rec* out, int cap, int* n);
+SS_API int64_t ss_sched_queued(ss_sched* s);
+SS_API const char* ss_sched_last_error(ss_sched* s);
+
 /* ---- cross-process device hand-off (CUDA IPC) ---------------------------------------------
  * The paper's co-located mode shares a pre-allocated CUDA exchange tensor between the client
  * process and the executor process (share_memory_() / rebuild_cuda_tensor());

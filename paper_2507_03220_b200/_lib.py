@@ -56,7 +56,19 @@ EXPORTED = (
     "ss_ipc_last_error", "ss_ipc_export", "ss_ipc_alloc", "ss_ipc_free", "ss_ipc_open",
     "ss_ipc_close", "ss_ipc_event_create", "ss_ipc_event_open", "ss_ipc_event_record",
     "ss_ipc_event_wait", "ss_ipc_event_sync", "ss_ipc_event_destroy",
+    "ss_layer_dims", "ss_ctx_device", "ss_sched_create", "ss_sched_destroy", "ss_sched_set_policy",
+    "ss_sched_register", "ss_sched_deregister", "ss_sched_submit", "ss_sched_wait",
+    "ss_sched_request", "ss_sched_next_done", "ss_sched_log", "ss_sched_queued",
+    "ss_sched_last_error",
 )
+
+SS_SCHED_NOLOCKSTEP = 0
+SS_SCHED_LOCKSTEP = 1
+SS_SCHED_OPPORTUNISTIC = 2
+SS_REQ_BAD_PASS = 16
+SS_REQ_BAD_ID = 17
+SS_REQ_NO_LAYER = 18
+SS_REQ_FAILED = 19
 
 SS_KERNEL_GATHER = 0
 SS_KERNEL_SHRINK = 1
@@ -94,6 +106,39 @@ class SsGradSeg(ctypes.Structure):
         ("grad_a", ctypes.c_void_p),
         ("grad_b", ctypes.c_void_p),
         ("grad_l", ctypes.c_void_p),
+    ]
+
+
+class SsRequest(ctypes.Structure):
+    _fields_ = [
+        ("client_id", ctypes.c_uint32),
+        ("pass_kind", ctypes.c_uint32),
+        ("block", ctypes.c_int32),
+        ("role", ctypes.c_int32),
+        ("request_id", ctypes.c_uint64),
+        ("seg", SsSeg),
+        ("ready", ctypes.c_void_p),
+    ]
+
+
+class SsSchedPolicy(ctypes.Structure):
+    _fields_ = [
+        ("mode", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("wait_per_token", ctypes.c_double),
+        ("wait_cap", ctypes.c_double),
+        ("max_batch_tokens", ctypes.c_int64),
+    ]
+
+
+class SsSchedRec(ctypes.Structure):
+    _fields_ = [
+        ("dispatch", ctypes.c_uint64),
+        ("block", ctypes.c_int32),
+        ("role", ctypes.c_int32),
+        ("pass_kind", ctypes.c_int32),
+        ("rows", ctypes.c_int32),
+        ("wait_s", ctypes.c_double),
     ]
 
 
@@ -167,6 +212,23 @@ def load() -> ctypes.CDLL:
             "ss_profile": (i32, [vp, i32]),
             "ss_profile_read": (i32, [vp, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64),
                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+            "ss_layer_dims": (i32, [vp, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+            "ss_ctx_device": (i32, [vp]),
+            "ss_sched_create": (i32, [vp, ctypes.POINTER(SsSchedPolicy), vp, ctypes.POINTER(vp)]),
+            "ss_sched_destroy": (i32, [vp, i32]),
+            "ss_sched_set_policy": (i32, [vp, ctypes.POINTER(SsSchedPolicy)]),
+            "ss_sched_register": (i32, [vp, u32, i32]),
+            "ss_sched_deregister": (i32, [vp, u32]),
+            "ss_sched_submit": (i32, [vp, ctypes.POINTER(SsRequest), i32, ctypes.POINTER(ctypes.c_uint64)]),
+            "ss_sched_wait": (i32, [vp, ctypes.c_uint64, vp, i64, ctypes.POINTER(ctypes.c_int32),
+                                    ctypes.POINTER(i64)]),
+            "ss_sched_request": (i32, [vp, ctypes.POINTER(SsRequest), vp, i64, ctypes.POINTER(ctypes.c_int32),
+                                       ctypes.POINTER(i64)]),
+            "ss_sched_next_done": (i32, [vp, vp, i64, ctypes.POINTER(ctypes.c_uint64),
+                                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(i64)]),
+            "ss_sched_log": (i32, [vp, ctypes.POINTER(SsSchedRec), i32, ctypes.POINTER(i32)]),
+            "ss_sched_queued": (i64, [vp]),
+            "ss_sched_last_error": (ctypes.c_char_p, [vp]),
             "ss_ipc_last_error": (ctypes.c_char_p, []),
             "ss_ipc_export": (i32, [vp, ctypes.c_uint64, ctypes.POINTER(SsIpcMem)]),
             "ss_ipc_alloc": (i32, [i32, ctypes.c_uint64, ctypes.POINTER(vp), ctypes.POINTER(SsIpcMem)]),

@@ -25,6 +25,7 @@ import queue
 import numpy as np
 import torch
 
+from . import _lib
 from .errors import ProtocolError, TransportError
 from .protocol import PASS_BACKWARD, PASS_ERROR, Envelope, error_message
 
@@ -82,6 +83,8 @@ class DeviceChannel:
         self.last_base: torch.Tensor | None = None
         self._replies: queue.Queue = queue.Queue()
         self._ids = itertools.count(1)
+        self._ready_ev: torch.cuda.Event | None = None
+        self._native_cache: dict = {}
 
     def register(self, sends_backward: bool = False) -> None:
         self.executor.register(self.client_id, sends_backward)
@@ -95,6 +98,8 @@ class DeviceChannel:
         return self.executor.fused_addresses(self.client_id)
 
     def request(self, block: int, role: int, pass_kind: int, payload, want_base: bool = False):
+        if getattr(self.executor, "_native", None) is not None and isinstance(payload, torch.Tensor):
+            return self._native_request(block, role, pass_kind, payload, want_base)
         rows, cols = int(payload.shape[0]), int(payload.shape[1])
         d_in, d_out = self.executor.layer_dims(block, role)
         out_cols = d_in if pass_kind == PASS_BACKWARD else d_out
@@ -126,6 +131,58 @@ class DeviceChannel:
             raise ProtocolError(value)
         if value is not None:
             torch.cuda.current_stream(self.buffer.device).wait_event(value)
+        self.last_base = base_to
+        return reply_to
+
+    def _native_request(self, block, role, pass_kind, payload, want_base):
+        """The native scheduler's path (GpuBaseExecutor(scheduler="native")): one library call
+        queues the request and returns once its batch is launched, the GIL released meanwhile;
+        the request struct of a recurring (layer, pass, shape) is built once."""
+        from .device import Seg, seg_fields
+        from .sched import pack_request, status_message
+        ex = self.executor
+        rows, cols = int(payload.shape[0]), int(payload.shape[1])
+        dims = ex._dims.get((int(block), int(role)))
+        expected, out_cols = (None, cols) if dims is None else \
+            ((dims[1], dims[0]) if pass_kind == PASS_BACKWARD else (dims[0], dims[1]))
+        self.buffer.ensure(rows * self.max_width)
+        self.reply_buffer.ensure(rows * self.max_width)
+        want_base = bool(want_base) and pass_kind != PASS_BACKWARD
+        if want_base:
+            if self.base_buffer is None:
+                self.base_buffer = DeviceBuffer(self.buffer.capacity, self.buffer.dtype, self.buffer.device)
+            self.base_buffer.ensure(rows * self.max_width)
+        key = (block, role, pass_kind, rows, cols, want_base, payload.dtype, self.buffer.resizes,
+               self.reply_buffer.resizes, self.base_buffer.resizes if want_base else -1, ex._fused_ver)
+        hit = self._native_cache.get(key)
+        if hit is None:
+            if len(self._native_cache) > 1024:
+                self._native_cache.clear()
+            sent = self.buffer.view(rows, cols)
+            reply_to = self.reply_buffer.view(rows, out_cols)
+            base_to = self.base_buffer.view(rows, out_cols) if want_base else None
+            req = _lib.SsRequest()
+            if self._ready_ev is None:
+                self._ready_ev = torch.cuda.Event()
+                self._ready_ev.record(torch.cuda.current_stream(self.buffer.device))
+            fields = seg_fields(Seg(self.client_id, sent, reply_to, base_to,
+                                    adapter=(int(block), int(role)) in ex._fused.get(self.client_id, ())))
+            pack_request(memoryview(req).cast("B"), self.client_id, pass_kind, block, role, 0, fields,
+                         int(self._ready_ev.cuda_event))
+            hit = self._native_cache[key] = (sent, reply_to, base_to, req)
+        sent, reply_to, base_to, req = hit
+        stream = torch.cuda.current_stream(self.buffer.device)
+        if payload.data_ptr() != sent.data_ptr():
+            sent.copy_(payload, non_blocking=True)
+        self._ready_ev.record(stream)
+        req.request_id = next(self._ids)
+        try:
+            status, aux = ex._native.request(req, stream.cuda_stream, REQUEST_TIMEOUT_S)
+        except TimeoutError:
+            raise TransportError("timed out waiting for executor reply") from None
+        if status != _lib.SS_SEG_OK:
+            env = Envelope(self.client_id, req.request_id, block, role, pass_kind, sent)
+            raise ProtocolError(status_message(status, aux, env, expected, ex._native))
         self.last_base = base_to
         return reply_to
 

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -76,6 +77,10 @@ struct Staging {
 namespace { struct ZcPlan; }
 struct ss_ctx {
   int device = 0, tp_rank = 0, tp_size = 1, num_sms = 148;
+  // Every entry point that reads or changes the context holds this (re-entrant: entry points
+  // call each other): the native scheduler thread (ss_sched_*) dispatches while client threads
+  // refresh adapters, and pack growth frees what a concurrent table build would read.
+  std::recursive_mutex mu;
   std::string err;
   PFN_encodeTiled_t encode = nullptr;
   std::map<std::pair<int, int>, Layer> layers;
@@ -1342,6 +1347,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
 
 int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!ctx || !key) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   ctx->opt_epoch++;   // options shape the built tables: cached dispatches rebuild
   if (!strcmp(key, "zc_cache")) {
     ctx->zc_cache_on = value ? 1 : 0;
@@ -1471,6 +1477,7 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
 int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const void* weight,
                   int64_t w_ld, const void* bias, uint32_t flags) {
   if (!ctx) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   if (d_in <= 0 || d_out <= 0 || !weight || w_ld < d_out)
     return fail(ctx, SS_E_ARG, "bad layer dims d_in=%d d_out=%d ld=%lld", d_in, d_out,
                 (long long)w_ld);
@@ -1514,6 +1521,7 @@ int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const v
 
 int ss_unload_layer(ss_ctx* ctx, int block, int role) {
   if (!ctx) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   auto it = ctx->layers.find({block, role});
   if (it == ctx->layers.end()) return SS_E_NOLAYER;
   cudaDeviceSynchronize();
@@ -1536,6 +1544,7 @@ int ss_unload_layer(ss_ctx* ctx, int block, int role) {
 int ss_set_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role, uint32_t kind, int rank,
                    float scale, const void* A, const void* B, const void* l, uint32_t flags) {
   if (!ctx) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   auto it = ctx->layers.find({block, role});
   if (it == ctx->layers.end())
     return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", block, role);
@@ -1594,6 +1603,7 @@ int ss_set_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role, uint32_
 
 int ss_clear_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role) {
   if (!ctx) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   auto it = ctx->layers.find({block, role});
   if (it == ctx->layers.end()) return SS_E_NOLAYER;
   auto a = it->second.adapters.find(client_id);
@@ -1610,6 +1620,7 @@ int ss_clear_adapter(ss_ctx* ctx, uint32_t client_id, int block, int role) {
 
 int ss_clear_client(ss_ctx* ctx, uint32_t client_id) {
   if (!ctx) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   for (auto& kv : ctx->layers) ss_clear_adapter(ctx, client_id, kv.first.first, kv.first.second);
   return SS_OK;
 }
@@ -1624,12 +1635,25 @@ int ss_memory_stats(const ss_ctx* ctx, int64_t* w, int64_t* a, int64_t* ws) {
 
 int64_t ss_kernel_launches(const ss_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+int ss_layer_dims(ss_ctx* ctx, int block, int role, int* d_in, int* d_out) {
+  if (!ctx) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
+  auto it = ctx->layers.find({block, role});
+  if (it == ctx->layers.end()) return SS_E_NOLAYER;
+  if (d_in) *d_in = it->second.d_in;
+  if (d_out) *d_out = it->second.d_out;
+  return SS_OK;
+}
+
+int ss_ctx_device(const ss_ctx* ctx) { return ctx ? ctx->device : -1; }
+
 uint64_t ss_ctx_epoch(const ss_ctx* ctx) {
   return ctx ? ctx->ws_epoch + ctx->ad_epoch + ctx->free_epoch : 0;
 }
 
 int ss_profile(ss_ctx* ctx, int enable) {
   if (!ctx) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   prof_drain(ctx);
   for (int k = 0; k < 4; ++k) {
     ctx->prof_ms[k] = ctx->prof_flops[k] = ctx->prof_bytes[k] = 0;
@@ -1642,6 +1666,7 @@ int ss_profile(ss_ctx* ctx, int enable) {
 int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* launches, double* flops,
                     double* bytes) {
   if (!ctx || kernel < 0 || kernel > 3) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   prof_drain(ctx);
   if (total_ms) *total_ms = ctx->prof_ms[kernel];
   if (launches) *launches = ctx->prof_n[kernel];
@@ -1654,6 +1679,7 @@ int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
                      void* stream_, int32_t* seg_status) {
   if (!ctx) return SS_E_ARG;
   Built b;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   int rc = build_batch(ctx, pass_kind, block, role, n_seg, segs, seg_status, b);
   if (rc || b.M == 0) return rc;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
@@ -1701,6 +1727,7 @@ static int plan_build(ss_plan* p, int32_t* seg_status) {
 int ss_plan_create(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
                    int32_t* seg_status, ss_plan** out) {
   if (!ctx || !out) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   *out = nullptr;
   if (n_seg < 0 || (n_seg > 0 && (!segs || !seg_status))) return fail(ctx, SS_E_ARG, "bad segment array");
   CK(cudaSetDevice(ctx->device));
@@ -1721,6 +1748,7 @@ int ss_plan_create(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, c
 
 int ss_plan_launch(ss_plan* p, void* stream_) {
   if (!p) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(p->ctx->mu);
   ss_ctx* ctx = p->ctx;
   if (p->b.ws_epoch != ctx->ws_epoch || p->b.ad_epoch != ctx->ad_epoch) {
     // workspace grew or an adapter moved since the tables were built: rebuild them (a plan's
@@ -1743,6 +1771,7 @@ int ss_plan_launch(ss_plan* p, void* stream_) {
 
 int ss_plan_destroy(ss_plan* p) {
   if (!p) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(p->ctx->mu);
   if (p->dev) {
     cudaDeviceSynchronize();
     cudaFree(p->dev);
@@ -1754,6 +1783,7 @@ int ss_plan_destroy(ss_plan* p) {
 int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_seg* segs,
                      void* stream_, int32_t* seg_status) {
   if (!ctx) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   if (n_seg < 0 || (n_seg > 0 && (!segs || !seg_status))) return fail(ctx, SS_E_ARG, "bad segment array");
   auto lit = ctx->layers.find({block, role});
   if (lit == ctx->layers.end()) return fail(ctx, SS_E_NOLAYER, "unknown layer (%d, %d)", block, role);
@@ -2091,6 +2121,7 @@ extern "C" {
 int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, const ss_seg* segs,
                           void* stream_, int32_t* seg_status) {
   if (!ctx) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   if (pass_kind < 0 || pass_kind > 2) return fail(ctx, SS_E_ARG, "unknown pass %d", pass_kind);
   if (n_seg < 0 || (n_seg > 0 && (!segs || !seg_status))) return fail(ctx, SS_E_ARG, "bad segment array");
   auto lit = ctx->layers.find({block, role});
@@ -2521,6 +2552,7 @@ void write_header(uint8_t* p, const Frame& f, uint8_t pass, uint32_t t, uint32_t
 extern "C" int ss_serve_frames(ss_ctx* ctx, const uint8_t* in, size_t in_len, size_t* consumed,
                                uint8_t* out, size_t out_cap, size_t* out_len, void* stream_) {
   if (!ctx || (!in && in_len) || !consumed || !out_len) return SS_E_ARG;
+  std::lock_guard<std::recursive_mutex> guard_(ctx->mu);
   *consumed = 0;
   *out_len = 0;
   // ---- parse whole frames (try_decode, protocol.py:125-153)

@@ -22,6 +22,7 @@ tensors, written into ``env.reply_to`` when the client supplies its exchange buf
 from __future__ import annotations
 
 import csv
+import os
 import threading
 import time
 import weakref
@@ -218,12 +219,24 @@ class GpuBaseExecutor:
 
     def __init__(self, layers, policy: BatchPolicy | None = None, save_activations: bool = False,
                  *, device: int = 0, stream: torch.cuda.Stream | None = None,
-                 context: SsContext | None = None, retain_layers: bool = True):
+                 context: SsContext | None = None, retain_layers: bool = True,
+                 scheduler: str | None = None):
         """``layers``: mapping (or iterable of pairs) LayerAddress -> AffineParams. Weights are
         copied to the device as bf16 (bias f32). With ``retain_layers=False`` the host-side
         parameters are dropped after upload (``layers`` then holds shape-only records), so a
-        generator of pairs streams a large model through without a second copy."""
+        generator of pairs streams a large model through without a second copy.
+
+        ``scheduler``: "python" (the reference's scheduler loop in a Python thread) or "native"
+        (batch formation and dispatch on a library thread, ss_sched_*: same policies, same
+        messages; client threads block without the GIL). Default: $SS_SCHEDULER or "python"."""
         self.policy = policy or BatchPolicy()
+        scheduler = scheduler or os.environ.get("SS_SCHEDULER", "python")
+        if scheduler not in ("python", "native"):
+            raise ConfigError(f"unknown scheduler {scheduler!r}")
+        self.scheduler = scheduler
+        self._native = None                 # NativeScheduler while started (scheduler="native")
+        self._native_pending: dict = {}     # ticket -> (env, reply_fn, dst, host_reply, expected)
+        self._native_thread: threading.Thread | None = None
         self.save_activations = save_activations
         # Serialises every call into the library context: the scheduler thread's dispatches,
         # adapter (re-)registration from client threads, plans, graphs, gradient jobs. The
@@ -248,7 +261,7 @@ class GpuBaseExecutor:
         self._last_request_id: dict[int, int] = {}
         self._running = False
         self._thread: threading.Thread | None = None
-        self.metrics = ExecutorMetrics()
+        self._metrics = ExecutorMetrics()
         self.ledger = ledger_mod.MemoryLedger("executor")
         self._pinned: dict[str, torch.Tensor] = {}
         self._np_pool: list = []         # (pinned tensor, its numpy base) reply arrays (_numpy_out)
@@ -270,11 +283,35 @@ class GpuBaseExecutor:
             if self._running:
                 return self
             self._running = True
+        if self.scheduler == "native":
+            from .sched import NativeScheduler
+            # a torch stream object, so staged request tensors can be tied to it (record_stream)
+            self._native_stream = self.stream if self.stream is not None else torch.cuda.Stream(self.device)
+            self._native = NativeScheduler(self.ctx, self.policy, self._native_stream)
+            for cid, bwd in self._clients.items():
+                self._native.register(cid, bwd)
+            self._reply_stream = torch.cuda.Stream(self.device)
+            self._native_thread = threading.Thread(target=self._native_completions, daemon=True,
+                                                   name="gpu-base-executor-replies")
+            self._native_thread.start()
+            return self
         self._thread = threading.Thread(target=self._loop, daemon=True, name="gpu-base-executor")
         self._thread.start()
         return self
 
     def stop(self, drain: bool = True) -> None:
+        if self._native is not None:
+            if drain:
+                while self._native.queued() or self._native_pending:
+                    time.sleep(0.005)
+            with self._cond:
+                self._running = False
+            self._native_thread.join()
+            self._native_thread = None
+            self._pull_native_log()
+            self._native.close(drain=False)
+            self._native = None
+            return
         if drain:
             with self._cond:
                 while self._running and any(self._queues.values()):
@@ -300,11 +337,15 @@ class GpuBaseExecutor:
     def register(self, client_id: int, sends_backward: bool = False) -> None:
         with self._cond:
             self._clients[client_id] = sends_backward
+            if self._native is not None:
+                self._native.register(client_id, sends_backward)
             self._cond.notify_all()
 
     def deregister(self, client_id: int) -> None:
         with self._cond:
             self._clients.pop(client_id, None)
+            if self._native is not None:
+                self._native.deregister(client_id)
             self._cond.notify_all()
         self._host_memo.clear()   # (drops the memo's references to the client's buffers)
 
@@ -391,6 +432,9 @@ class GpuBaseExecutor:
 
     # -- intake ---------------------------------------------------------------------------
     def submit(self, env, reply_fn) -> None:
+        if self._native is not None:
+            self._native_submit(env, reply_fn)
+            return
         if env.pass_kind not in COMPUTE_PASSES:
             reply_fn(error_envelope(env, f"unknown pass {env.pass_kind}"))
             return
@@ -410,6 +454,123 @@ class GpuBaseExecutor:
         with self._cond:
             self._queues[(env.block, env.role, env.pass_kind)].append((env, reply_fn, time.monotonic()))
             self._cond.notify_all()
+
+    # -- native scheduler (scheduler="native") ---------------------------------------------
+    @property
+    def metrics(self) -> ExecutorMetrics:
+        self._pull_native_log()
+        return self._metrics
+
+    def _pull_native_log(self) -> None:
+        nat = self._native
+        if nat is None:
+            return
+        recs = nat.drain_log()
+        i = 0
+        while i < len(recs):           # requests of one dispatch are contiguous in the log
+            j = i
+            while j < len(recs) and recs[j][0] == recs[i][0]:
+                j += 1
+            _, block, role, pass_kind, _, _ = recs[i]
+            self._metrics.record((block, role, pass_kind), j - i, sum(r[4] for r in recs[i:j]),
+                                 [r[5] for r in recs[i:j]])
+            i = j
+
+    def _native_request_fields(self, env, out_w):
+        """(segment fields, dst tensor, host reply target or None) of a native request. Device
+        payloads are served in place; host payloads are staged to the device here (the library
+        scheduler only sees device pointers) and their reply read back by the reply thread."""
+        p = env.payload
+        host_reply = None
+        if _is_device(p):
+            src = p if p.dtype in (torch.float32, torch.bfloat16) else p.float()
+            if src.dim() != 2 or src.stride(-1) != 1:
+                src = src.contiguous()
+        else:
+            a = p if isinstance(p, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(p, dtype=np.float32))
+            if a.dtype not in (torch.float32, torch.bfloat16):
+                a = a.float()
+            if a.dim() != 2:
+                a = a.reshape(a.shape[0] if a.dim() else 0, -1)
+            src = a.to(self.device, non_blocking=False)
+        reply = getattr(env, "reply_to", None)
+        if _is_device(reply):
+            dst = reply
+        else:
+            dst = torch.empty((src.shape[0], out_w), dtype=_out_dtype(p), device=self.device)
+            host_reply = reply if reply is not None else True
+        base = getattr(env, "base_to", None) if env.pass_kind != PASS_BACKWARD else None
+        if base is not None and not _is_device(base):
+            base = None
+        key = (int(env.block), int(env.role))
+        seg = Seg(client_id=env.client_id, src=src, dst=dst, base=base,
+                  adapter=key in self._fused.get(env.client_id, ()), width=env.width)
+        from .device import seg_fields
+        return seg_fields(seg), src, dst, host_reply
+
+    def _native_submit(self, env, reply_fn) -> None:
+        from .sched import pack_request, raw_event
+        key = (int(env.block), int(env.role))
+        dims = self._dims.get(key)
+        expected = out_w = None
+        if dims is not None:
+            expected = dims[1] if env.pass_kind == PASS_BACKWARD else dims[0]
+            out_w = dims[0] if env.pass_kind == PASS_BACKWARD else dims[1]
+        else:
+            out_w = env.width
+        with torch.cuda.device(self.device):
+            fields, src, dst, host_reply = self._native_request_fields(env, max(out_w, 1))
+            ready = raw_event(getattr(env, "ready", None))
+            keep = None
+            if not ready:
+                # the payload write (or the staging copy above) is ordered on this thread's
+                # stream: the scheduler's stream waits for this point
+                keep = torch.cuda.Event()
+                keep.record()
+                ready = raw_event(keep)
+            if src is not env.payload:
+                src.record_stream(self._native_stream)   # staged copy: freed only after the batch
+        req = _lib.SsRequest()
+        pack_request(memoryview(req).cast("B"), env.client_id, env.pass_kind, env.block, env.role,
+                     env.request_id, fields, ready)
+        with self._cond:   # the reply thread looks the ticket up under the same lock
+            ticket = self._native.submit(req, notify=True)
+            self._native_pending[ticket] = (env, reply_fn, src, dst, host_reply, expected, keep)
+            self._cond.notify_all()
+
+    def _native_completions(self) -> None:
+        from .sched import status_message
+        torch.cuda.set_device(self.device)
+        nat, rs = self._native, self._reply_stream
+        while True:
+            got = nat.next_done(rs.cuda_stream, 0.02)
+            if got is None:
+                with self._cond:
+                    if not self._running:
+                        return
+                continue
+            ticket, status, aux = got
+            with self._cond:
+                while ticket not in self._native_pending:   # submit() is between its two steps
+                    self._cond.wait(0.01)
+                env, reply_fn, src, dst, host_reply, expected, _ = self._native_pending.pop(ticket)
+            if status != _lib.SS_SEG_OK:
+                reply_fn(error_envelope(env, status_message(status, aux, env, expected, nat)))
+                continue
+            with torch.cuda.stream(rs):
+                done = torch.cuda.Event()
+                if host_reply is None:
+                    res = dst
+                else:
+                    h = dst.cpu()          # rs waits for the batch (next_done), then D2H
+                    if isinstance(host_reply, torch.Tensor):
+                        host_reply.copy_(h)
+                        res = host_reply
+                    else:
+                        res = h.float().numpy() if h.dtype == torch.float32 else h
+                done.record(rs)
+            reply_fn(Envelope(env.client_id, env.request_id, env.block, env.role, env.pass_kind, res,
+                              done=done))
 
     # -- batch surface --------------------------------------------------------------------
     def serve_forward(self, envelopes) -> list:
@@ -836,7 +997,7 @@ class GpuBaseExecutor:
             results = self._compute_batch(key[2], envs)
         except Exception as exc:  # a CUDA failure fails the batch, not the scheduler
             results = [ProtocolError(f"executor failure: {exc}")] * len(envs)
-        self.metrics.record(key, len(entries), sum(e.token_count for e in envs),
+        self._metrics.record(key, len(entries), sum(e.token_count for e in envs),
                             [now - t for _, _, t in entries])
         done = self.last_event
         for (env, reply_fn, _), res in zip(entries, results):

@@ -100,6 +100,14 @@ def _close_executors():
             pass
 
 
+@pytest.fixture(params=["python", "native"])
+def sched(request, monkeypatch):
+    """Run a test with either batch-formation loop: the Python scheduler thread (the
+    reference's loop) or the library's native one (ss_sched_*, GpuBaseExecutor(scheduler=))."""
+    monkeypatch.setenv("SS_SCHEDULER", request.param)
+    return request.param
+
+
 @pytest.fixture
 def on_gpu(monkeypatch):
     """harness.run / _run_threads / _run_processes build the executor through this name."""
@@ -226,7 +234,7 @@ def submit_and_wait(ex, envelope, timeout=10.0):
     return box["reply"]
 
 
-def test_submit_rejections_match_reference():
+def test_submit_rejections_match_reference(sched):
     """test_executor.py:120-138."""
     ex, ref = make_pair()
     with ex, ref:
@@ -245,7 +253,7 @@ def test_submit_rejections_match_reference():
         assert outs[0][0] == PASS_FORWARD and all(k == PASS_ERROR for k, _ in outs[0][1])
 
 
-def test_single_client_any_policy_batch_size_one():
+def test_single_client_any_policy_batch_size_one(sched):
     """test_executor.py:141-147."""
     for mode in ("nolockstep", "lockstep", "opportunistic"):
         ex, _ = make_pair(policy=BatchPolicy(mode=mode, wait_per_token=0.0001))
@@ -256,7 +264,7 @@ def test_single_client_any_policy_batch_size_one():
             assert ex.metrics.mean_batch_size() == 1.0
 
 
-def test_eight_simultaneous_clients_lockstep_one_batch():
+def test_eight_simultaneous_clients_lockstep_one_batch(sched):
     """test_executor.py:150-165, plus: every reply equals that client's solo dispatch."""
     ex, _ = make_pair(policy=BatchPolicy(mode="lockstep"))
     with ex:
@@ -279,7 +287,7 @@ def test_eight_simultaneous_clients_lockstep_one_batch():
         assert np.array_equal(np.asarray(replies[c].payload), solo)
 
 
-def test_lockstep_backward_waits_only_for_backward_senders():
+def test_lockstep_backward_waits_only_for_backward_senders(sched):
     """test_executor.py:168-175."""
     ex, _ = make_pair(policy=BatchPolicy(mode="lockstep"))
     with ex:
@@ -296,7 +304,7 @@ def test_opportunistic_wait_budget_uses_smallest_member():
     assert policy.wait_budget([1000]) == pytest.approx(0.05)
 
 
-def test_opportunistic_max_batch_tokens_flushes_immediately():
+def test_opportunistic_max_batch_tokens_flushes_immediately(sched):
     """test_executor.py:184-192."""
     ex, _ = make_pair(policy=BatchPolicy(mode="opportunistic", wait_per_token=10.0,
                                          wait_cap=10.0, max_batch_tokens=4))
@@ -307,7 +315,7 @@ def test_opportunistic_max_batch_tokens_flushes_immediately():
         assert time.monotonic() - start < 5.0
 
 
-def test_opportunistic_batches_concurrent_clients_invisibly():
+def test_opportunistic_batches_concurrent_clients_invisibly(sched):
     """Opportunistic policy under concurrency: the wait budget gathers several clients into
     one dispatch (mean batch > 1) and every reply is bitwise its solo result."""
     ex, _ = make_pair(policy=BatchPolicy(mode="opportunistic", wait_per_token=0.01, wait_cap=0.2))
@@ -342,7 +350,7 @@ def test_policy_validation():
         GpuPolicy(wait_per_token=-1.0)
 
 
-def test_metrics_csv(tmp_path):
+def test_metrics_csv(tmp_path, sched):
     """test_executor.py:202-210."""
     ex, _ = make_pair()
     with ex:
@@ -530,7 +538,7 @@ def _replay(scenario, result, fused_model=None):
 
 @pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("steps", [1, 2])
-def test_baseline_configs0_end_to_end_through_reference_harness(on_gpu, monkeypatch, fused, steps):
+def test_baseline_configs0_end_to_end_through_reference_harness(on_gpu, monkeypatch, fused, steps, sched):
     """harness.run with the GPU executor: every job completes, fine-tune and inference logits
     match the reference replay on the bf16 base, greedy tokens are the reference's, the
     executor saved no activations. ``fused``: the LoRA adapters run in the executor's GEMM
@@ -640,7 +648,7 @@ POLICIES = ("nolockstep", "lockstep", "opportunistic")
 
 
 @pytest.mark.parametrize("fused", [False, True])
-def test_criterion_05_batching_invisibility_bitwise(on_gpu, monkeypatch, fused):
+def test_criterion_05_batching_invisibility_bitwise(on_gpu, monkeypatch, fused, sched):
     """test_acceptance.py:214-233 with the GPU executor, BITWISE as in the reference: the 8
     heterogeneous clients of ``policy-sweep`` (4..2048 tokens per request) under all three
     policies produce per-iteration logits bitwise equal to solo runs. With ``fused`` the

@@ -30,7 +30,7 @@ pytestmark = pytest.mark.gpu
 D_IN, D_OUT = 512, 768
 
 
-def _executor():
+def _executor(scheduler=None):
     from paper_2507_03220_b200 import AffineParams, GpuBaseExecutor, LayerAddress, Role
     rng = np.random.default_rng(7)
     layers = {}
@@ -38,7 +38,7 @@ def _executor():
         w = (rng.standard_normal((di, do)) / np.sqrt(di)).astype(np.float32)
         b = (rng.standard_normal(do) * 0.1).astype(np.float32)
         layers[LayerAddress(0, role)] = AffineParams(w, b)
-    return GpuBaseExecutor(layers).start()
+    return GpuBaseExecutor(layers, scheduler=scheduler).start()
 
 
 def _plan():
@@ -74,10 +74,11 @@ def _in_process(ex, client_id, spec):
     return out
 
 
-def test_device_client_process_bitwise_equals_in_process_channel():
+@pytest.mark.parametrize("scheduler", ["python", "native"])
+def test_device_client_process_bitwise_equals_in_process_channel(scheduler):
     from paper_2507_03220_b200.executor import _is_device
     from paper_2507_03220_b200.ipc import IpcExecutorServer
-    ex = _executor()
+    ex = _executor(scheduler)
     seen = []
     orig_submit = ex.submit
 
