@@ -228,9 +228,9 @@ class GpuBaseExecutor:
 
         ``scheduler``: "python" (the reference's scheduler loop in a Python thread) or "native"
         (batch formation and dispatch on a library thread, ss_sched_*: same policies, same
-        messages; client threads block without the GIL). Default: $SS_SCHEDULER or "python"."""
+        messages; client threads block without the GIL). Default: $SS_SCHEDULER or "native"."""
         self.policy = policy or BatchPolicy()
-        scheduler = scheduler or os.environ.get("SS_SCHEDULER", "python")
+        scheduler = scheduler or os.environ.get("SS_SCHEDULER", "native")
         if scheduler not in ("python", "native"):
             raise ConfigError(f"unknown scheduler {scheduler!r}")
         self.scheduler = scheduler
@@ -487,7 +487,7 @@ class GpuBaseExecutor:
             if src.dim() != 2 or src.stride(-1) != 1:
                 src = src.contiguous()
         else:
-            a = p if isinstance(p, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(p, dtype=np.float32))
+            a = p if isinstance(p, torch.Tensor) else _host_tensor(np.ascontiguousarray(p, dtype=np.float32))
             if a.dtype not in (torch.float32, torch.bfloat16):
                 a = a.float()
             if a.dim() != 2:
