@@ -76,6 +76,12 @@ extern "C" {
 #define SS_SEGF_PINNED (1u << 4)    /* ss_compute_batch_host: the caller has verified that src / dst /
                                        dst_base are page-locked host memory (skips the per-pointer
                                        query of the zero-copy path) */
+/* Summation class of a segment's rows (see decode_rows below). Without either flag the class
+ * follows the segment's own row count; a caller that splits one request into several segments
+ * (the library's host pipelines do) sets the class of the whole request on every piece, so the
+ * pieces give the same bits as the request would in one piece. */
+#define SS_SEGF_CLASS_DECODE (1u << 5)   /* force the decode class (split-K order) */
+#define SS_SEGF_CLASS_PREFILL (1u << 6)  /* force the single-chain class */
 
 /* One request (envelope) of a batch, in batch order. Rows are concatenated in array order
  * exactly like concat_rows(); row r of segment i is batch row off_i + r, off_i = sum_{j<i} rows_j
@@ -358,7 +364,16 @@ SS_API int ss_profile(ss_ctx* ctx, int enable);
 SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* launches,
                            double* flops, double* bytes);
 
-/* Tuning / testing knobs (none changes results: every kernel choice gives bitwise the same rows).
+/* Numerics class of a request (a property of the request alone, so batching stays invisible):
+ *   decode_rows (0)     segments of at most this many rows (0..64; layers with K % 64 == 0) are
+ *                       "decode class": their rows reduce K as C = min(decode_chunks, ceil(K/128)) fixed
+ *                       contiguous chunks summed in chunk order (split-K kernel, K1d),
+ *                       then their own LoRA chain; every other row reduces K as one chain. 0: no
+ *                       decode class (every row single-chain).
+ *   decode_chunks (8)   at most this many K chunks (1..16) in the decode class's order
+ * Tuning / testing knobs (results unchanged):
+ *   decode_ctas (1)     CTAs per SM of the persistent decode-class kernel (1 or 2)
+ * Tuning / testing knobs (none changes results: every kernel choice gives bitwise the same rows).
  *   group_m (16)        M-tiles per raster group of the persistent GEMM
  *   raster (0)          0 M-grouped, 1 N-grouped (W columns held in L2), -1 fewer modelled bytes
  *   group_n, l2_budget_mb (0, 48)  N-group width (0: as many W columns as fit the budget)

@@ -1417,7 +1417,10 @@ struct ShrinkItem {
   // lo = bf16(v - hi) in the second, the GEMM's K-extension reading the same B rows for both
   // (v = s*x.A kept to ~2^-17 instead of bf16's 2^-9: the fp32-output tier)
   int32_t hilo;
-  int32_t pad_[2];
+  // > 0: tensor map of the lo halves (X_lo, same box) of an SEGF_IA3_LO backward segment: every
+  // K chunk runs a second pass over them into the same accumulator (g = hi + lo, fp32 tier)
+  int32_t amap_lo;
+  int32_t pad_;
 };
 
 struct ShrinkParams {
@@ -1480,10 +1483,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
 #define SHRINK_A(s) (stage0 + (s) * stage_bytes)
 #define SHRINK_B(s) (stage0 + (s) * stage_bytes + A_STAGE_BYTES)
 
+  const CUtensorMap* tmAlo = p.tmaps + (it.amap_lo > 0 ? it.amap_lo : it.amap);
+  const int npass = it.amap_lo > 0 ? 2 : 1;
   if (warp == 0 && lane == 0) {
     tensormap_acquire(tmA);
     tma_prefetch_desc(tmA);
     tma_prefetch_desc(tmPk);
+    if (npass == 2) tensormap_acquire(tmAlo);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < SHRINK_STAGES; ++s) {
@@ -1510,15 +1516,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int kb = c0 * p.kb_chunk; kb < min(nkb_all, c1 * p.kb_chunk); ++kb) {
-        mbar_wait(&empty_bar[s], ph ^ 1);
-        mbar_expect_tx(&full_bar[s], (it.a_rows ? it.a_rows * 128 : A_STAGE_BYTES) + nchunk * LORA_CHUNK_BYTES);
-        tma_load_2d(SHRINK_A(s), tmA, &full_bar[s], kb * BK, it.arow);
-        for (int q = 0; q < nchunk; ++q)
-          tma_load_2d(SHRINK_B(s) + q * LORA_CHUNK_BYTES, tmPk, &full_bar[s], kb * BK,
-                      sg.pack_row + q * LORA_CHUNK);
-        if (++s == SHRINK_STAGES) { s = 0; ph ^= 1; }
-      }
+      for (int c = c0; c < c1; ++c)
+        for (int pass = 0; pass < npass; ++pass)
+          for (int kb = c * p.kb_chunk; kb < min(nkb_all, (c + 1) * p.kb_chunk); ++kb) {
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            mbar_expect_tx(&full_bar[s], (it.a_rows ? it.a_rows * 128 : A_STAGE_BYTES) + nchunk * LORA_CHUNK_BYTES);
+            tma_load_2d(SHRINK_A(s), pass ? tmAlo : tmA, &full_bar[s], kb * BK, it.arow);
+            for (int q = 0; q < nchunk; ++q)
+              tma_load_2d(SHRINK_B(s) + q * LORA_CHUNK_BYTES, tmPk, &full_bar[s], kb * BK,
+                          sg.pack_row + q * LORA_CHUNK);
+            if (++s == SHRINK_STAGES) { s = 0; ph ^= 1; }
+          }
     }
   } else if (warp == 1) {
     const uint32_t idesc = make_idesc_bf16(BM, (uint32_t)npad, false, false);
@@ -1531,21 +1539,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + buf * 128;
       const int kb0 = c * p.kb_chunk, kb1 = min(nkb_all, kb0 + p.kb_chunk);
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full_bar[s], ph);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a_addr = smem_u32(SHRINK_A(s));
-          const uint32_t b_addr = smem_u32(SHRINK_B(s));
+      for (int pass = 0; pass < npass; ++pass)
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(SHRINK_A(s));
+            const uint32_t b_addr = smem_u32(SHRINK_B(s));
 #pragma unroll
-          for (int k = 0; k < BK / UK; ++k)
-            mma_bf16_ss(d_tmem, make_sdesc_sw128(a_addr + k * 32, 16, 1024),
-                        make_sdesc_sw128(b_addr + k * 32, 16, 1024), idesc, (kb != kb0 || k != 0));
-          mma_commit(&empty_bar[s]);
+            for (int k = 0; k < BK / UK; ++k)
+              mma_bf16_ss(d_tmem, make_sdesc_sw128(a_addr + k * 32, 16, 1024),
+                          make_sdesc_sw128(b_addr + k * 32, 16, 1024), idesc, (pass | (kb - kb0) | k) != 0);
+            mma_commit(&empty_bar[s]);
+          }
+          __syncwarp();
+          if (++s == SHRINK_STAGES) { s = 0; ph ^= 1; }
         }
-        __syncwarp();
-        if (++s == SHRINK_STAGES) { s = 0; ph ^= 1; }
-      }
       if (lane == 0) mma_commit(&tfull[buf]);
       __syncwarp();
     }

@@ -19,6 +19,7 @@
 
 #include "../../include/ss_b200.h"
 #include "kernels.cuh"
+#include "decode.cuh"
 #include "grads.cuh"
 #include "frames.cuh"
 
@@ -49,6 +50,7 @@ struct Layer {
   float* bias = nullptr;
   CUtensorMap tm_w_fwd, tm_w_bwd, tm_w_bwd2, tm_w_bwd64;  // bwd box rows 256 / 128 / 64
   CUtensorMap tm_w_fwd_s, tm_w_bwd_s;                      // weight-streaming kernel
+  CUtensorMap tm_w_fwd_d, tm_w_bwd_d;                      // split-K decode kernel (K1d)
   // LoRA packs: rows = rank index of every registered client (16-aligned blocks)
   __nv_bfloat16* at_pack = nullptr;  // [cap, ld_at]  (A^T: rank rows x d_in)
   __nv_bfloat16* b_pack = nullptr;   // [cap, ld_b]   (B:   rank rows x d_out)
@@ -117,6 +119,10 @@ struct ss_ctx {
   int serial_launches = 0;       // a tool serialises kernel launches (ncu, sanitizer): no overlap
   int stream_pdl = 1;
   int wide_decode = 1;           // decode-size dispatches: 128-wide single-CTA tiles when they fit one wave
+  // segments of <= decode_rows rows reduce K in the decode class's split-K order (K1d, decode.cuh)
+  int decode_rows = 0;
+  int decode_chunks = 8;           // max K chunks of the decode class's order (numerics!)
+  int decode_ctas = 1;             // K1d CTAs per SM (persistent grid)
   int* sync_ctr = nullptr;       // [2] shrink-done counter + GEMM ticket (zero between dispatches)
   struct HostSlot {
     void* in = nullptr;
@@ -169,6 +175,8 @@ struct ss_ctx {
   int pair_n = 0;
   int shrink_kb_chunk = SHRINK_KB_CHUNK;  // K-split of the LoRA shrink (k-blocks of 64 per chunk)
   int shrink_mode = 0;   // 0 auto, 1 one CTA per slab (all chunks), 2 one CTA per (slab, chunk)
+  float* dec_part = nullptr;      // K1d: fp32 chunk partials of the decode tiles
+  size_t dec_part_cap = 0;
   // LoRA intermediate s*x.A as a hi / lo bf16 pair (ShrinkItem::hilo): 0 never, 1 segments with
   // f32 destinations, 2 every segment. A per-segment property, so batching stays invisible.
   int lora_hilo = 2;
@@ -497,6 +505,13 @@ struct Built {
   int tbn = BN, pn = 256, num_m = 0, n_piece = 0, n_items = 0, part_ld = 16, shrink_chunks_ = 1;
   int kb_chunk = SHRINK_KB_CHUNK;
   size_t off_tm = 0, off_seg = 0, off_tile = 0, off_piece = 0, off_ch = 0, off_st = 0, off_it = 0;
+  // decode-class part (K1d): tiles, LoRA runs, X / X_lo tensor maps, cluster size
+  size_t off_dt = 0;
+  int dec_items_per_n = 0;
+  int n_dec = 0, dec_C = 0;
+  int32_t dec_amap = 0, dec_alo = 0;
+  int64_t Mp = 0;                      // single-chain rows (M - decode-class rows)
+  double dec_flops = 0, dec_bytes = 0;
   std::vector<char> blob;
   std::vector<int32_t> status;
   double gather_bytes = 0, shrink_flops = 0, shrink_bytes = 0, gemm_flops = 0, gemm_bytes = 0;
@@ -566,8 +581,10 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   // ---- validate + build device segment records (batch order == envelope order)
   std::vector<DevSeg> ds;
   std::vector<const ss_seg*> src_of;
+  std::vector<char> dec_of;       // decode class (K1d split-K order), see decode_rows
   ds.reserve(n_seg);
-  int64_t M = 0;
+  int64_t M = 0, Md = 0;
+  const bool dec_ok = K % 64 == 0 && ctx->decode_rows > 0;
   bool any_lora = false;
   for (int i = 0; i < n_seg; ++i) {
     const ss_seg& s = segs[i];
@@ -626,7 +643,12 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     d.flags = f;
     ds.push_back(d);
     src_of.push_back(&s);
+    const bool dec = dec_ok && (int)s.rows <= DEC_ROWS &&
+                     ((s.flags & SS_SEGF_CLASS_DECODE) ||
+                      (!(s.flags & SS_SEGF_CLASS_PREFILL) && (int)s.rows <= ctx->decode_rows));
+    dec_of.push_back(dec ? 1 : 0);
     M += s.rows;
+    if (dec) Md += s.rows;
   }
   B.status.assign(seg_status, seg_status + n_seg);
   // A reply written over request rows (the reference's SharedBuffer hand-off, transport.py:
@@ -658,13 +680,16 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   // ---- M-tiles: segment-aligned direct tiles for whole tiles of bf16 rows, the rest packed
   // Kernel / tile choice depends only on the layer shape and the dispatch size, never on which
   // segments are present; every choice reduces K in the same order (bitwise-equal rows).
+  // Decode-class rows (dec_of) are packed after every other row into 64-row tiles of whole
+  // segments for the split-K kernel; the choices below see the single-chain rows Mp only.
+  const int64_t Mp = M - Md;
   const int n256 = (N + BN - 1) / BN;
-  const bool pair = ctx->gemm_2cta < 0 ? (((M + BM2 - 1) / BM2) * n256 >= ctx->num_sms / 2)
+  const bool pair = ctx->gemm_2cta < 0 ? (((Mp + BM2 - 1) / BM2) * n256 >= ctx->num_sms / 2)
                                        : ctx->gemm_2cta != 0;
   const int TM = pair ? BM2 : BM;
   int tbn = BN;
   if (!pair) {
-    const int64_t m128 = (M + BM - 1) / BM;
+    const int64_t m128 = (Mp + BM - 1) / BM;
     if (m128 * n256 < ctx->num_sms) tbn = (m128 * ((N + 127) / 128) >= ctx->num_sms) ? 128 : 64;
     if (ctx->force_tbn) tbn = ctx->force_tbn;
   }
@@ -674,6 +699,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   int64_t MX = 0;
   for (size_t j = 0; j < ds.size(); ++j) {
     DevSeg& d = ds[j];
+    if (dec_of[j]) continue;
     const bool direct_ok = ctx->direct_tiles && (d.flags & SEGF_SRC_BF16) && (d.flags & SEGF_SRC_VEC) &&
                            !(d.flags & (SEGF_REMOTE_SRC | SEGF_SRC_ALIASED)) &&
                            !(bwd && (d.flags & SEGF_IA3)) && (d.src_ld * 2) % 16 == 0;
@@ -694,6 +720,28 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   for (int64_t x = 0; x < MX; x += TM)
     tiles.push_back(TileDesc{0, (int32_t)x, -1, (int32_t)std::min<int64_t>(TM, MX - x), 0, 0, 0, 0, -1});
   const int num_m = (int)tiles.size();
+  const int64_t MXp = MX;
+  // decode tiles: whole decode-class segments, in batch order, <= DEC_ROWS rows per tile
+  std::vector<DecTile> dtiles;
+  std::vector<int32_t> dtile_of(ds.size(), -1);
+  for (size_t j = 0; j < ds.size(); ++j) {
+    if (!dec_of[j]) continue;
+    DevSeg& d = ds[j];
+    if (dtiles.empty() || dtiles.back().rows + d.rows > DEC_ROWS) {
+      DecTile t{};
+      t.arow = (int32_t)MX;
+      dtiles.push_back(t);
+    }
+    DecTile& t = dtiles.back();
+    d.xrow0 = (int32_t)MX;
+    d.xlocal0 = 0;
+    piece_seg.push_back((int32_t)j);
+    MX += d.rows;
+    t.rows += d.rows;
+    if (d.flags & SEGF_IA3_LO) t.lo = 1;
+    dtile_of[j] = (int32_t)dtiles.size() - 1;
+  }
+  const int dec_C = dtiles.empty() ? 0 : std::min(dec_stages(K), ctx->decode_chunks);
 
   // ---- LoRA: per tile rank-chunk lists (block-diagonal over the tile's segments) + shrink items
   std::vector<int32_t> chunks;
@@ -714,7 +762,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
           for (int q = 0; q < d.rank_pad / LORA_CHUNK; ++q) chunks.push_back(d.pack_row + q * LORA_CHUNK);
         for (int r = 0; r < nrows; r += BM)
           items.push_back(ShrinkItem{sj, amap, arow + r, std::min(BM, nrows - r), mt * TM + p0 + r, col, 0, 0,
-                                     r == 0 ? 1 : 0, mt * TM, TM, p0, p0 + nrows, hilo, {0, 0}});
+                                     r == 0 ? 1 : 0, mt * TM, TM, p0, p0 + nrows, hilo, 0, 0});
       };
       if (td.seg >= 0) {
         add_piece(td.seg, td.amap, td.arow, 0, td.rows);
@@ -734,6 +782,25 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
       td.chunk_count = (int32_t)chunks.size() - td.chunk_begin;
       max_cols = std::max(max_cols, td.chunk_count * LORA_CHUNK);
     }
+    // decode tiles: the tile's rank chunks, block-diagonal over its segments (one piece each)
+    for (size_t t = 0; t < dtiles.size(); ++t) {
+      DecTile& dt = dtiles[t];
+      dt.al_row = (int32_t)((int64_t)num_m * TM + (int64_t)t * DEC_ROWS);
+      dt.chunk_begin = (int32_t)chunks.size();
+      for (size_t j = 0; j < ds.size(); ++j) {
+        if (dtile_of[j] != (int32_t)t || !(ds[j].flags & SEGF_LORA)) continue;
+        const DevSeg& d = ds[j];
+        const int col = (int)(chunks.size() - dt.chunk_begin) * LORA_CHUNK;
+        const int hilo = ctx->lora_hilo == 2 || (ctx->lora_hilo == 1 && !(d.flags & SEGF_DST_BF16));
+        for (int rep = 0; rep <= hilo; ++rep)
+          for (int q = 0; q < d.rank_pad / LORA_CHUNK; ++q) chunks.push_back(d.pack_row + q * LORA_CHUNK);
+        const int p0 = d.xrow0 - dt.arow;
+        items.push_back(ShrinkItem{(int32_t)j, 0, d.xrow0, d.rows, dt.al_row + p0, col, 0, 0, 1,
+                                   dt.al_row, DEC_ROWS, p0, p0 + d.rows, hilo, 0, 0});
+      }
+      dt.chunk_count = (int32_t)chunks.size() - dt.chunk_begin;
+      max_cols = std::max(max_cols, dt.chunk_count * LORA_CHUNK);
+    }
     if (chunks.empty()) chunks.push_back(0);
   }
   const int64_t lora_ld = std::max<int64_t>(64, round_up(max_cols, 64));
@@ -746,7 +813,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   if (B.any_lo && (rc = ensure_dev(ctx, ctx->X_lo, ctx->xlo_cap, (size_t)mx_pad * ldx * 2))) return rc;
   rc = ensure_dev(ctx, ctx->row_seg, ctx->rs_cap, (size_t)mx_pad * 4);
   if (rc) return rc;
-  const int64_t al_rows = (int64_t)num_m * TM;
+  const int64_t al_rows = (int64_t)num_m * TM + (int64_t)dtiles.size() * DEC_ROWS;
   if (any_lora) {
     rc = ensure_dev(ctx, ctx->a_lora, ctx->al_cap, (size_t)al_rows * lora_ld * 2);
     if (rc) return rc;
@@ -764,9 +831,10 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     rc = encode_2d(ctx, &tmaps[1 + i], d.src, K, d.rows, d.src_ld, 64, BM);
     if (rc) return rc;
   }
+  int32_t lo_map = -1;
   if (B.any_lo) {
     // X_lo map (same geometry as X) for every packed tile holding an SEGF_IA3_LO piece
-    const int32_t lo_map = (int32_t)tmaps.size();
+    lo_map = (int32_t)tmaps.size();
     tmaps.emplace_back();
     rc = encode_2d(ctx, &tmaps.back(), ctx->X_lo, K, std::max<int64_t>(MX, 1), ldx, 64, BM);
     if (rc) return rc;
@@ -830,7 +898,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   // ---- weight-streaming dispatch (one packed tile of <= 64 rows): the GEMM reads A through a
   // 64-row box (MMA rows 64-127 are never stored); with `stream_gemm` (K a multiple of 64) the
   // streaming kernel moves 4 k-blocks of A and of W per TMA operation instead
-  if (ctx->a_rows64 && !pair && num_m == 1 && direct_src.empty() && MX <= 64 && !B.any_lo) {
+  if (ctx->a_rows64 && !pair && num_m == 1 && direct_src.empty() && MXp <= 64 && !B.any_lo) {
     tiles[0].amap = (int32_t)tmaps.size();
     tmaps.emplace_back();
     // At these sizes a tile's time is set by its K/16-long chain of dependent UMMAs, not by its
@@ -851,13 +919,31 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     B.a_rows64 = true;
   }
 
+  // ---- decode tiles read X (and X_lo) as {64 k, 64 rows, 2 k-chunks} boxes
+  if (!dtiles.empty()) {
+    B.dec_amap = (int32_t)tmaps.size();
+    tmaps.emplace_back();
+    if ((rc = encode_kchunks(ctx, &tmaps.back(), ctx->X, K, MX, ldx, DEC_ROWS, DEC_KB))) return rc;
+    B.dec_alo = B.dec_amap;
+    for (const DecTile& t : dtiles) {
+      if (!t.lo) continue;
+      B.dec_alo = (int32_t)tmaps.size();
+      tmaps.emplace_back();
+      if ((rc = encode_kchunks(ctx, &tmaps.back(), ctx->X_lo, K, MX, ldx, DEC_ROWS, DEC_KB))) return rc;
+      break;
+    }
+  }
+
   // ---- short LoRA pieces of the packed operand (decode rows): the shrink reads them straight
   // from the client's rows through a 16-row box over the segment (so it no longer waits for the
   // gather and can run beside it), or, for sources TMA cannot read in place, through a 16-row
   // box over the packed operand instead of 128 rows of neighbouring clients' rows
   if (any_lora && MX > 0) {
-    int32_t small_map = -1;
+    int32_t small_map = -1, small_lo_map = -1;
     std::vector<int32_t> seg_map(ds.size(), -1);
+    // shrinks of IA3-backward rows with the lo pass read g = hi + lo like the GEMM does
+    for (ShrinkItem& it : items)
+      if (it.amap == 0 && (ds[it.seg].flags & SEGF_IA3_LO)) it.amap_lo = lo_map;
     for (ShrinkItem& it : items) {
       if (it.amap != 0 || it.rows > 16) continue;
       const DevSeg& d = ds[it.seg];
@@ -882,6 +968,14 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
           if (rc) return rc;
         }
         it.amap = small_map;
+        if (d.flags & SEGF_IA3_LO) {
+          if (small_lo_map < 0) {
+            small_lo_map = (int32_t)tmaps.size();
+            tmaps.emplace_back();
+            if ((rc = encode_2d(ctx, &tmaps.back(), ctx->X_lo, K, MX, ldx, 64, 16))) return rc;
+          }
+          it.amap_lo = small_lo_map;
+        }
       }
       it.a_rows = 16;
     }
@@ -899,7 +993,8 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   const size_t off_ch = off_piece + round_up(std::max<size_t>(1, piece_seg.size()) * 4, 256);
   const size_t off_st = off_ch + round_up(std::max<size_t>(1, chunks.size()) * 4, 256);
   const size_t off_it = off_st + round_up(std::max<size_t>(1, stores.size()) * sizeof(int2), 256);
-  const size_t total = off_it + round_up(std::max<size_t>(1, items.size()) * sizeof(ShrinkItem), 256);
+  const size_t off_dt = off_it + round_up(std::max<size_t>(1, items.size()) * sizeof(ShrinkItem), 256);
+  const size_t total = off_dt + round_up(std::max<size_t>(1, dtiles.size()) * sizeof(DecTile), 256);
   B.blob.assign(total, 0);
   char* h = B.blob.data();
   memcpy(h + off_tm, tmaps.data(), tmaps.size() * sizeof(CUtensorMap));
@@ -911,8 +1006,18 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     memcpy(h + off_ch, chunks.data(), chunks.size() * 4);
     memcpy(h + off_it, items.data(), items.size() * sizeof(ShrinkItem));
   }
+  if (!dtiles.empty()) memcpy(h + off_dt, dtiles.data(), dtiles.size() * sizeof(DecTile));
   B.off_tm = off_tm; B.off_seg = off_seg; B.off_tile = off_tile; B.off_piece = off_piece;
-  B.off_ch = off_ch; B.off_st = off_st; B.off_it = off_it;
+  B.off_ch = off_ch; B.off_st = off_st; B.off_it = off_it; B.off_dt = off_dt;
+  B.n_dec = (int)dtiles.size();
+  B.dec_C = dec_C;
+  for (const DecTile& t : dtiles) B.dec_items_per_n += dec_C + (t.chunk_count > 0 ? 1 : 0);
+  if (!dtiles.empty()) {
+    const int64_t tiles_dec = (int64_t)dtiles.size() * ((N + DEC_TN - 1) / DEC_TN);
+    if ((rc = ensure_dev(ctx, ctx->dec_part, ctx->dec_part_cap,
+                         (size_t)tiles_dec * (dec_C + 1) * DEC_PART * sizeof(float)))) return rc;
+  }
+  B.Mp = Mp;
   B.M = M; B.MX = MX; B.lora_ld = lora_ld; B.al_rows = al_rows; B.ldx = ldx;
   B.any_lora = any_lora; B.pair = pair; B.tbn = tbn;   // (B.any_lo set during validation)
   B.pn = ctx->pair_n ? ctx->pair_n
@@ -938,12 +1043,17 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   }
   // base GEMM + each LoRA segment's own rank (the block-diagonal zeros of neighbouring
   // segments are not counted); bytes: A rows, W, outputs
-  B.gemm_flops = 2.0 * (double)M * N * K;
-  B.gemm_bytes = (double)M * K * 2 + (double)K * N * 2;
-  for (const DevSeg& d : ds) {
-    B.gemm_bytes += (double)d.rows * N * ((d.flags & SEGF_DST_BF16) ? 2 : 4);
-    if (d.flags & SEGF_WANT_BASE) B.gemm_bytes += (double)d.rows * N * ((d.flags & SEGF_BASE_BF16) ? 2 : 4);
-    if (d.flags & SEGF_LORA) B.gemm_flops += 2.0 * d.rows * d.rank_pad * N;
+  B.gemm_flops = 2.0 * (double)Mp * N * K;
+  B.gemm_bytes = Mp ? (double)Mp * K * 2 + (double)K * N * 2 : 0.0;
+  B.dec_flops = 2.0 * (double)Md * N * K;
+  B.dec_bytes = Md ? (double)Md * K * 2 + (double)K * N * 2 : 0.0;
+  for (size_t j = 0; j < ds.size(); ++j) {
+    const DevSeg& d = ds[j];
+    double& fl = dec_of[j] ? B.dec_flops : B.gemm_flops;
+    double& by = dec_of[j] ? B.dec_bytes : B.gemm_bytes;
+    by += (double)d.rows * N * ((d.flags & SEGF_DST_BF16) ? 2 : 4);
+    if (d.flags & SEGF_WANT_BASE) by += (double)d.rows * N * ((d.flags & SEGF_BASE_BF16) ? 2 : 4);
+    if (d.flags & SEGF_LORA) fl += 2.0 * d.rows * d.rank_pad * N;
   }
   B.ws_epoch = ctx->ws_epoch;
   B.ad_epoch = ctx->ad_epoch;
@@ -1114,8 +1224,10 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   const int ntiles = gpm.num_m_tiles * gpm.num_n_tiles;
   const int grid = pair ? 2 * std::min(ntiles, ctx->num_sms / 2) : std::min(ntiles, ctx->num_sms);
   const CUtensorMap& tmBP = any_lora ? (bwd ? L.tm_at : L.tm_b) : L.tm_w_fwd;
-  const int pg = prof_begin(ctx, stream, SS_KERNEL_GEMM, B.gemm_flops, B.gemm_bytes);
-  if (B.stream) {
+  const int pg = num_m > 0 ? prof_begin(ctx, stream, SS_KERNEL_GEMM, B.gemm_flops, B.gemm_bytes) : -1;
+  if (num_m == 0) {
+    // only decode-class rows: no single-chain GEMM
+  } else if (B.stream) {
     if (bwd)
       CK(launch_kp(early || (ctx->pdl && !ctx->profiling), seg_gemm_stream_kernel<true>, grid, GEMM_THREADS,
                    STREAM_SMEM, stream, L.tm_w_bwd_s, tmAL, tmBP, gpm));
@@ -1148,10 +1260,46 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     if (bwd) CK(launch_k(ctx, seg_gemm_kernel<true, 64>, grid, GEMM_THREADS, TileCfg<64>::SMEM, stream, L.tm_w_bwd64, tmAL, tmBP, gpm));
     else CK(launch_k(ctx, seg_gemm_kernel<false, 64>, grid, GEMM_THREADS, TileCfg<64>::SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
   }
-  prof_end(ctx, stream, pg);
-  CK(cudaGetLastError());
-  ctx->launches++;
+  if (num_m > 0) {
+    prof_end(ctx, stream, pg);
+    CK(cudaGetLastError());
+    ctx->launches++;
+  }
   if (overlap) CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));   // join the side stream
+  // ---- K1d: decode-class rows, persistent split-K (dec_C chunks + a LoRA item per tile)
+  if (B.n_dec > 0) {
+    CUtensorMap tmALd = L.tm_w_fwd;   // (unused without LoRA)
+    if (any_lora && (rc = encode_2d(ctx, &tmALd, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, DEC_ROWS))) return rc;
+    DecParams dp;
+    dp.N = N;
+    dp.K = K;
+    dp.C = B.dec_C;
+    dp.nst = dec_stages(K);
+    dp.n_m = B.n_dec;
+    dp.n_n = (N + DEC_TN - 1) / DEC_TN;
+    dp.items_per_n = B.dec_items_per_n;
+    dp.has_bias = gpm.has_bias;
+    dp.ia3_in_epilogue = gpm.ia3_in_epilogue;
+    dp.bias = L.bias;
+    dp.segs = d_segs;
+    dp.row_seg = ctx->row_seg;
+    dp.tiles = reinterpret_cast<const DecTile*>(dv + B.off_dt);
+    dp.chunks = gpm.chunks;
+    dp.tmaps = d_tmaps;
+    dp.amap = B.dec_amap;
+    dp.alo_map = B.dec_alo;
+    dp.part = ctx->dec_part;
+    const int n_items = dp.n_n * dp.items_per_n;
+    const int dgrid = std::min(n_items, ctx->num_sms * ctx->decode_ctas);
+    const bool dpdl = ctx->pdl && !ctx->profiling;
+    const int pd = prof_begin(ctx, stream, SS_KERNEL_GEMM, B.dec_flops, B.dec_bytes);
+    if (bwd) CK(launch_kp(dpdl, seg_gemm_dec_kernel<true>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_bwd_d, tmALd, tmBP, dp));
+    else CK(launch_kp(dpdl, seg_gemm_dec_kernel<false>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_fwd_d, tmALd, tmBP, dp));
+    CK(launch_kp(dpdl, dec_fixup_kernel, dp.n_n * dp.n_m * (DEC_ROWS / DEC_FIX_ROWS), DEC_FIX_THREADS, 0, stream, dp));
+    prof_end(ctx, stream, pd);
+    CK(cudaGetLastError());
+    ctx->launches += 2;
+  }
   CK(cudaEventRecord(ctx->compute_done, stream));
   ctx->any_compute = true;
   return SS_OK;
@@ -1201,6 +1349,8 @@ int set_kernel_attrs(ss_ctx* ctx) {
                           STREAM_SMEM));
   CK(cudaFuncSetAttribute(lora_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           SHRINK_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_dec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC_SMEM));
+  CK(cudaFuncSetAttribute(seg_gemm_dec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC_SMEM));
   CK(cudaFuncSetAttribute(lora_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GRAD_SMEM));
   g_attrs.done = true;
   return SS_OK;
@@ -1315,6 +1465,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   cudaFree(ctx->ia3_part);
   cudaFree(ctx->shrink_part);
   cudaFree(ctx->shrink_ticket);
+  cudaFree(ctx->dec_part);
   cudaFree(ctx->fr_in);
   cudaFree(ctx->fr_out);
   cudaFree(ctx->fr_x);
@@ -1430,6 +1581,21 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
     ctx->force_remote = value ? 1 : 0;
     return SS_OK;
   }
+  if (!strcmp(key, "decode_rows")) {
+    if (value < 0 || value > DEC_ROWS) return fail(ctx, SS_E_ARG, "decode_rows must be 0..%d", DEC_ROWS);
+    ctx->decode_rows = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "decode_chunks")) {
+    if (value < 1 || value > DEC_MAX_C) return fail(ctx, SS_E_ARG, "decode_chunks must be 1..%d", DEC_MAX_C);
+    ctx->decode_chunks = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "decode_ctas")) {
+    if (value < 1 || value > 2) return fail(ctx, SS_E_ARG, "decode_ctas must be 1 or 2");
+    ctx->decode_ctas = (int)value;
+    return SS_OK;
+  }
   if (!strcmp(key, "wide_decode")) {
     ctx->wide_decode = value ? 1 : 0;
     return SS_OK;
@@ -1513,6 +1679,11 @@ int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const v
   rc = encode_2d(ctx, &L.tm_w_fwd_s, L.W, d_out, d_in, L.ldw, 64, SK);
   if (rc) return rc;
   rc = encode_kchunks(ctx, &L.tm_w_bwd_s, L.W, L.ldw, d_in, L.ldw, 64, 4);
+  if (rc) return rc;
+  // split-K decode kernel: forward box {64 n, 128 k}; backward 2 K-chunks of 128 rows
+  rc = encode_2d(ctx, &L.tm_w_fwd_d, L.W, d_out, d_in, L.ldw, 64, DEC_SK);
+  if (rc) return rc;
+  rc = encode_kchunks(ctx, &L.tm_w_bwd_d, L.W, L.ldw, d_in, L.ldw, DEC_TN, DEC_KB);
   if (rc) return rc;
   ctx->weight_bytes += (int64_t)d_in * L.ldw * 2 + (bias ? round_up(d_out, 64) * 4 : 0);
   ctx->layers[{block, role}] = L;
@@ -1867,12 +2038,17 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     lg[j].gmap = (int32_t)(4 * j + 3);
     for (int r = 0; r < (int)s.rows; r += BM) {
       const int n = std::min<int>(BM, s.rows - r);
-      sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 0), r, n, lg[j].qrow0 + r, 0, 0, 0, 0, 0, 0, 0, 0, 0, {0, 0}});
+      sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 0), r, n, lg[j].qrow0 + r, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0});
       sitems.push_back(ShrinkItem{(int32_t)j, (int32_t)(4 * j + 1), r, n, (int32_t)qrows + lg[j].qrow0 + r, 0, 1, 0, 0,
-                                  0, 0, 0, 0, 0, {0, 0}});
+                                  0, 0, 0, 0, 0, 0, 0});
     }
-    for (int m = 0; m < d_in; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 0, m, 0});
-    for (int m = 0; m < d_out; m += BM) gitems.push_back(LoraGradItem{(int32_t)j, 1, m, 0});
+  }
+  // token contractions in reverse client order: the shrink (items in client order) read the last
+  // clients' x / g most recently, so their second read is the likeliest to hit L2
+  for (size_t jj = lg.size(); jj-- > 0;) {
+    const int32_t j = (int32_t)jj;
+    for (int m = 0; m < d_in; m += BM) gitems.push_back(LoraGradItem{j, 0, m, 0});
+    for (int m = 0; m < d_out; m += BM) gitems.push_back(LoraGradItem{j, 1, m, 0});
   }
   std::vector<Ia3PartItem> pitems;
   std::vector<Ia3FinItem> fitems;
@@ -2001,6 +2177,14 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
 namespace {
 struct HostPiece { int seg; int64_t r0, r1; };
 
+// The numerics class of a whole request (decode_rows), for the pieces a host pipeline splits it
+// into: a piece must reduce K the way the request would in one piece.
+uint32_t class_flag(const ss_ctx* ctx, int K, const ss_seg& s) {
+  if (s.flags & (SS_SEGF_CLASS_DECODE | SS_SEGF_CLASS_PREFILL)) return 0;
+  return (K % 64 == 0 && ctx->decode_rows > 0 && (int)s.rows <= ctx->decode_rows) ? SS_SEGF_CLASS_DECODE
+                                                                                   : SS_SEGF_CLASS_PREFILL;
+}
+
 // Host dispatch whose replies overwrite request rows of later sub-batches (see
 // ss_compute_batch_host): every sub-batch gets its own slice of dispatch-sized device buffers
 // (so the H2D stream never waits for compute), and the D2H of sub-batch j is issued right after
@@ -2070,6 +2254,7 @@ int host_dispatch_aliased(ss_ctx* ctx, int pass_kind, int block, int role, const
                    (size_t)s.src_ld * esz_in, (size_t)K * esz_in, (size_t)n, cudaMemcpyHostToDevice, ctx->h2d));
       ss_seg d = s;
       d.rows = (uint32_t)n;
+      d.flags |= class_flag(ctx, K, s);   // a piece keeps its request's numerics class
       d.src = din;
       d.src_ld = K;
       d.dst = static_cast<char*>(ctx->ha_out) + pos * N * esz_out;
@@ -2432,6 +2617,7 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
                    (size_t)s.src_ld * esz_in, (size_t)K * esz_in, (size_t)n, cudaMemcpyHostToDevice, ctx->h2d));
       ss_seg d = s;
       d.rows = (uint32_t)n;
+      d.flags |= class_flag(ctx, K, s);   // a piece keeps its request's numerics class
       d.src = din;
       d.src_ld = K;
       d.dst = static_cast<char*>(hs.out) + pos * N * esz_out;

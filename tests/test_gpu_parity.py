@@ -633,7 +633,8 @@ def test_peer_gpu_routing_bitwise_equals_local():
             assert torch.equal(bases[0], bases[1])
 
 
-def test_decode_size_dispatch_64_row_box_bitwise():
+@pytest.mark.parametrize("decode_rows", [16, 0])
+def test_decode_size_dispatch_64_row_box_bitwise(decode_rows):
     """A dispatch of <= 64 packed rows runs the weight-streaming kernel (4 k-blocks of A and W
     per TMA operation, 64-row A boxes whose MMA rows 64-127 are never stored) or, with it off,
     the single-CTA kernel with a 64- or 128-row A box; the streaming kernel either overlaps the
@@ -645,6 +646,7 @@ def test_decode_size_dispatch_64_row_box_bitwise():
     d_in, d_out = 5120, 1024
     w, b = O.layer_params(17, 0, O.K, d_in, d_out)
     ex = _ex({(0, O.K): (w, b)})
+    ex.ctx.set_option("decode_rows", decode_rows)   # 0: these rows take the single-chain kernels
     _mixed_clients(ex, d_in, d_out, seed=17)
     counts = [2, 2, 1, 2, 2, 3, 2]                      # 14 decode rows, every adapter kind
     dev = ex.device
@@ -669,13 +671,15 @@ def test_decode_size_dispatch_64_row_box_bitwise():
             assert torch.equal(outs[0][c], big[c]), (pass_kind, c)
 
 
-def test_decode_wide_layer_128_tiles_bitwise():
+@pytest.mark.parametrize("decode_rows", [16, 0])
+def test_decode_wide_layer_128_tiles_bitwise(decode_rows):
     """A decode-size dispatch over a layer whose 64-wide tiles would need more than one wave
     (N = 10240: 160 tiles on 148 SMs) runs 128-wide single-CTA tiles instead of the streaming
     kernel; rows must be bitwise those of the streaming kernel and of a prefill-size dispatch."""
     d_in, d_out = 512, 10240
     w, b = O.layer_params(23, 0, O.FF_UP, d_in, d_out)
     ex = _ex({(0, O.FF_UP): (w, b)})
+    ex.ctx.set_option("decode_rows", decode_rows)
     rng = np.random.default_rng(23)
     ex.register_adapter(3, _Adapter(ia3={_addr(0, O.FF_UP): O.ia3_params(23, 3, 0, O.FF_UP, d_out).ia3}))
     counts = [2, 1, 2, 2]
