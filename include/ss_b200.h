@@ -365,14 +365,14 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
                            double* flops, double* bytes);
 
 /* Numerics class of a request (a property of the request alone, so batching stays invisible):
- *   decode_rows (0)     segments of at most this many rows (0..64; layers with K % 64 == 0) are
- *                       "decode class": their rows reduce K as C = min(decode_chunks, ceil(K/128)) fixed
- *                       contiguous chunks summed in chunk order (split-K kernel, K1d),
- *                       then their own LoRA chain; every other row reduces K as one chain. 0: no
- *                       decode class (every row single-chain).
- *   decode_chunks (8)   at most this many K chunks (1..16) in the decode class's order
- * Tuning / testing knobs (results unchanged):
- *   decode_ctas (1)     CTAs per SM of the persistent decode-class kernel (1 or 2)
+ *   decode_rows (16)    segments of at most this many rows (0..64; layers with K % 64 == 0) are
+ *                       "decode class": their rows reduce K as C = ceil(K / (64 * decode_chunk_kb))
+ *                       fixed contiguous chunks summed left to right in chunk order (split-K
+ *                       kernel K1d + fixup), then their own LoRA chain; every other row reduces K
+ *                       as one chain. 0: no decode class (every row single-chain).
+ *   decode_chunk_kb (20) 64-deep k-blocks per chunk of the decode class's order (1..64)
+ *   decode_trace (0)    testing: device address of an int64 buffer [4 x SMs] the decode-class
+ *                       kernel fills with {start ns, end ns, first unit, end unit} per CTA
  * Tuning / testing knobs (none changes results: every kernel choice gives bitwise the same rows).
  *   group_m (16)        M-tiles per raster group of the persistent GEMM
  *   raster (0)          0 M-grouped, 1 N-grouped (W columns held in L2), -1 fewer modelled bytes

@@ -1,4 +1,4 @@
-// K1d: split-K persistent GEMM for decode-class segments (SURVEY §8a affine_forward /
+// K1d: split-K GEMM for decode-class segments (SURVEY §8a affine_forward /
 // affine_backward_input / noise matmul + the fused adapter epilogue, for requests of a few rows).
 //
 // Why a separate kernel and a separate summation order. A decode dispatch streams W (HBM-bound in
@@ -8,86 +8,126 @@
 // summation order. Rows of a decode-class segment (its own row count <= decode_rows, a property
 // of the request alone) therefore use their own fixed order, independent of the dispatch:
 //
-//   K is cut into C = min(decode_chunks, ceil(K / 128)) contiguous chunks of whole 128-deep
-//   stages (a function of K only); chunk c is one UMMA chain in K order; the LoRA expand of the
-//   tile (its rank chunks, block-diagonal over the tile's segments as in the other kernels) is a
-//   chain of its own. y = ((p_0 + p_1) + ... + p_{C-1}) + p_lora, then bias / y_base / IA3.
+//   K is cut into C = ceil(K / (64 * kbc)) contiguous chunks of kbc 64-deep k-blocks (kbc =
+//   decode_chunk_kb, a per-context constant); chunk c is one UMMA chain in K order. Backward
+//   segments with the IA3 lo operand (SEGF_IA3_LO) add C more chains over the lo halves. The
+//   LoRA expand of a row is one chain over its own rank block: per 64-row slice, the hi columns,
+//   then the lo columns (fp32-tier hi / lo pair). y = fold(p_0 ..
+//   p_{C-1}, [lo_0 .. lo_{C-1}], [p_lora]) left to right, then bias / y_base / IA3.
 //
 // A row's bits depend only on its segment's class, K and its own values (foreign rows of the
-// block-diagonal LoRA operand contribute exact zeros): batched == solo holds for decode-class rows
-// exactly as for the single-chain kernels (tests/test_gpu_decode.py).
+// block-diagonal LoRA operand contribute exact zeros, and so do the lo chains of rows without a
+// lo half). The tile's LoRA operand is block-diagonal over its segments and is cut into pieces of
+// whole segments (shorter chains, spread over CTAs); a row reads the piece holding its block,
+// whose chain over the other segments' columns adds exact zeros. So batched == solo holds for decode-class rows exactly as for the single-chain kernels
+// (tests/test_gpu_decode.py).
 //
-// Work item = (64-row decode tile m, 128-column tile n, chunk c in 0..C, c == C the LoRA chain),
-// chunk fastest. A persistent grid walks the items: the producer streams stage after stage
-// across items, the MMA warp alternates two TMEM accumulators, and the epilogue warps write each
-// item's fp32 partial to an L2-resident workspace ([row][col], 512 B per row). No CTA waits on
-// another: the fixed-order sum, bias / y_base / IA3 and the stores run in dec_fixup_kernel,
-// launched behind the GEMM with programmatic dependent launch.
-// The UMMA is M = 128: A boxes deliver 64 rows, MMA rows 64-127 read the stage bytes that follow
-// and their outputs are never read. Stage = 128 of K: A {64 k, 64 rows, 2 k-chunks} (16 KB), W
-// two {64 n, 128 k} boxes (forward, MN-major) or {64 k, 128 n, 2 k-chunks} (backward) (32 KB).
+// Work. A unit is (64-row decode tile m, chunk c, 64-column tile n); units are ordered m, then
+// chunk (hi chunks, lo chunks, the LoRA chain), then n, and every CTA of a persistent grid takes
+// one contiguous, cost-balanced range (host-built `cta_begin`). Consecutive units of one chunk
+// run in groups of g <= DEC_G = 4 n tiles: one UMMA of N = 64 g covers the group (a chain of
+// kbc * 4 UMMAs per group instead of K / 16), and each stage carries one k-block of A (8 KB, read
+// once per group) beside the group's W boxes (32 KB). W is streamed with L2 evict_first; each
+// unit's fp32 partial goes to the workspace with evict_last, so it is still in L2 for the fixup; no CTA waits on another: the fixed-order sum, bias / y_base / IA3 and the stores run
+// in dec_fixup_kernel, launched behind the GEMM with programmatic dependent launch.
+//
+// The UMMA is M = 128: the A box holds 64 rows; MMA rows 64-127 read the W boxes that follow it in
+// the stage and their outputs are never read.
 #pragma once
 #include "kernels.cuh"
 
 namespace ss {
 
-constexpr int DEC_ROWS = 64;                            // packed rows per tile
-constexpr int DEC_TN = 128;                             // output columns per tile
-constexpr int DEC_KB = 2;                               // 64-deep k-blocks per stage
-constexpr int DEC_SK = DEC_KB * BK;                     // 128 of K per stage
-constexpr int DEC_A_BYTES = DEC_KB * DEC_ROWS * 128;    // 16 KB
-constexpr int DEC_WBOX = DEC_SK * 128;                  // one {64 n, 128 k} box: 16 KB
-constexpr int DEC_B_BYTES = DEC_TN * DEC_SK * 2;        // 32 KB
-constexpr int DEC_STAGE = DEC_A_BYTES + DEC_B_BYTES;    // 48 KB
-#ifndef SS_DEC_STAGES
-#define SS_DEC_STAGES 4
-#endif
-constexpr int DEC_STAGES = SS_DEC_STAGES;
-constexpr int DEC_MAX_C = 16;
-constexpr int DEC_PART = DEC_TN * DEC_ROWS;             // fp32 values per item partial (32 KB)
+constexpr int DEC_ROWS = 64;                            // packed rows per decode tile
+constexpr int DEC_TN = 64;                              // output columns per unit
+constexpr int DEC_G = 4;                                // n tiles interleaved per group
+constexpr int DEC_MAX_KBC = 64;                         // k-blocks per chunk (option bound)
+constexpr int DEC_KB_BYTES = DEC_ROWS * 128;            // one k-block of A (64 rows x 64 k): 8 KB
+constexpr int DEC_WBOX = 64 * 128;                      // one {64 n, 64 k} W box: 8 KB
+// stage (40 KB). Chunk units: one k-block, the A box (8 KB) + the group's W boxes (<= 32 KB).
+// LoRA units (groups of <= DEC_G_LORA n tiles): one <= 64-row slice of a segment's rank block,
+// its A_lora hi and lo columns (16 KB) + the group's pack boxes of those rows (<= 24 KB, read
+// once for hi and lo)
+constexpr int DEC_G_LORA = 3;
+constexpr int DEC_STAGE = DEC_KB_BYTES + DEC_G * DEC_WBOX;
+constexpr int DEC_STAGES = 5;
+__host__ __device__ constexpr int dec_b_off(int kind) { return kind ? 2 * DEC_KB_BYTES : DEC_KB_BYTES; }
+constexpr int DEC_LP_CHUNKS = 24;                       // max LoRA chunks per piece (unless one segment has more)
+constexpr int DEC_PART = DEC_ROWS * DEC_TN;             // fp32 values per unit partial (16 KB)
 constexpr int DEC_SMEM = DEC_STAGES * DEC_STAGE + 1024 + 256;
 
 struct DecTile {
   int32_t arow;          // first packed (X) row
   int32_t rows;          // valid rows (<= DEC_ROWS), whole segments
   int32_t al_row;        // first row of the tile's block-diagonal LoRA operand
-  int32_t lo;            // 1: some row is SEGF_IA3_LO -> every chunk runs a second pass over X_lo
+  int32_t lo;            // 1: some row is SEGF_IA3_LO -> C lo chains over X_lo
   int32_t chunk_begin;   // LoRA rank chunks (pack rows) of the tile in `chunks`
-  int32_t chunk_count;   // 0: no LoRA item for this tile
+  int32_t chunk_count;   // 0: no LoRA for this tile
+  int32_t unit_begin;    // first unit of the tile
+  int32_t lp_begin;      // the tile's LoRA pieces in `lpieces`
+  int32_t lp_count;
+  int32_t pad_[3];
 };
 
 struct DecParams {
   int N, K;
   int C;                 // K chunks
-  int nst;               // 128-deep stages over K
-  int n_m, n_n;          // decode tiles, 128-column tiles
-  int items_per_n;       // sum over decode tiles of C + (chunk_count > 0)
+  int kbc;               // k-blocks per chunk
+  int n_m, n_n;          // decode tiles, 64-column tiles
+  int S;                 // partial slots per (m, n): 2C + max pieces (hi chunks, lo chunks, LoRA pieces)
   int has_bias, ia3_in_epilogue;
   const float* bias;
   const DevSeg* segs;
   const int32_t* row_seg;
   const DecTile* tiles;
   const int32_t* chunks;
+  const int2* lpieces;        // LoRA pieces: {first entry in `lstages`, stage count}
+  const int4* lstages;        // LoRA stages: {pack row, 16-row chunks (<= 4), A_lora hi col, lo col | -1}
+  const int32_t* cta_begin;   // [gridDim.x + 1] unit ranges
   const CUtensorMap* tmaps;
-  int amap, alo_map;     // X / X_lo as {64 k, 64 rows, 2 k-chunks} boxes
-  float* part;           // [n_n * n_m * (C + 1)][DEC_ROWS][DEC_TN] fp32 partials (item c of tile
-                         // nt * n_m + mt at (tile * (C + 1) + c))
+  int amap, alo_map;     // X / X_lo as {64 k, 64 rows, kbc k-blocks} boxes
+  float* part;           // [(m * n_n + n) * S + slot][DEC_ROWS][DEC_TN] fp32 partials
+  long long* trace;      // testing: per CTA {start ns, end ns, first unit, end unit} (nullptr: off)
 };
 
-__host__ __device__ inline int dec_stages(int K) { return (K / BK + DEC_KB - 1) / DEC_KB; }
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
-// item w -> (n tile, decode tile m, chunk c); c == C is the tile's LoRA item
-__device__ __forceinline__ void dec_item(const DecParams& p, int w, int& n, int& m, int& c) {
-  n = w / p.items_per_n;
-  int r = w - n * p.items_per_n;
-  m = 0;
-  for (;;) {
-    const int k = p.C + (p.tiles[m].chunk_count > 0 ? 1 : 0);
-    if (r < k) break;
-    r -= k;
-    ++m;
+// A group of units one CTA runs back to back: kind 0 a chunk (slot c; the lo chains have slots
+// C + c), kind 1 LoRA piece c - 2C (slot c); g consecutive n tiles starting at nt0.
+struct DecGroup {
+  int mt, kind, c, nt0, g;
+};
+
+__device__ __forceinline__ void dec_unit(const DecParams& p, int u, int& mt, int& kind, int& c, int& nt) {
+  mt = 0;
+  while (mt + 1 < p.n_m && p.tiles[mt + 1].unit_begin <= u) ++mt;
+  int r = u - p.tiles[mt].unit_begin;
+  const int nc = p.C * p.n_n;
+  if (r < nc) { kind = 0; c = r / p.n_n; nt = r - c * p.n_n; return; }
+  r -= nc;
+  if (p.tiles[mt].lo) {
+    if (r < nc) { kind = 0; c = r / p.n_n; nt = r - c * p.n_n; c += p.C; return; }
+    r -= nc;
   }
-  c = r;
+  kind = 1; c = r / p.n_n; nt = r - c * p.n_n; c += 2 * p.C;
+}
+
+// Next group starting at unit u (< end); returns the unit after it.
+__device__ __forceinline__ int dec_next_group(const DecParams& p, int u, int end, DecGroup& gr) {
+  dec_unit(p, u, gr.mt, gr.kind, gr.c, gr.nt0);
+  gr.g = 1;
+  const int gmax = gr.kind ? DEC_G_LORA : DEC_G;
+  while (gr.g < gmax && u + gr.g < end && gr.nt0 + gr.g < p.n_n) {
+    int mt, kind, c, nt;
+    dec_unit(p, u + gr.g, mt, kind, c, nt);
+    if (mt != gr.mt || c != gr.c) break;
+    ++gr.g;
+  }
+  return u + gr.g;
 }
 
 __device__ __forceinline__ void dec_store8(const float (&v)[8], int ncols, char* dst, bool bf, bool vec) {
@@ -111,11 +151,18 @@ __device__ __forceinline__ void dec_store8(const float (&v)[8], int ncols, char*
   }
 }
 
+__device__ __forceinline__ void st_f4_evict_last(float4* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+
 template <bool kBwd>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    seg_gemm_dec_kernel(const __grid_constant__ CUtensorMap tmB,   // W (see above)
+    seg_gemm_dec_kernel(const __grid_constant__ CUtensorMap tmB,   // W: {64 n, 64 k} fwd / {64 k, 64 n} bwd
                         const __grid_constant__ CUtensorMap tmAL,  // A_lora, box {64, 64 rows}
                         const __grid_constant__ CUtensorMap tmBP,  // pack [R, N] (MN-major B), box {64, 16}
+                        const __grid_constant__ CUtensorMap tmBP64,  // same pack, box {64, 64}
                         const DecParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -128,13 +175,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
-  const int n_items = p.n_n * p.items_per_n;
+  const int u_begin = p.cta_begin[blockIdx.x], u_end = p.cta_begin[blockIdx.x + 1];
   const int nkb = p.K / BK;
+  if (p.trace && threadIdx.x == 0) p.trace[4 * blockIdx.x] = globaltimer_ns();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmAL);
     tma_prefetch_desc(&tmBP);
+    tma_prefetch_desc(&tmBP64);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < DEC_STAGES; ++s) {
@@ -143,11 +192,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 2);   // warps 4 and 5 (TMEM lanes 0-63) read the accumulator
+      mbar_init(&tempty_bar[b], 2);   // warps 4 and 5 (TMEM lanes 0-63) read the accumulators
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 2 * DEC_TN);
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * DEC_G * DEC_TN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -164,41 +213,47 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const CUtensorMap* tmAlo = p.tmaps + p.alo_map;
       tensormap_acquire(tmA);
       if (p.alo_map != p.amap) tensormap_acquire(tmAlo);
-      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
-        int nt, mt, c;
-        dec_item(p, w, nt, mt, c);
-        const DecTile td = p.tiles[mt];
-        const int n0 = nt * DEC_TN;
-        if (c < p.C) {
-          const int st0 = c * p.nst / p.C, st1 = (c + 1) * p.nst / p.C;
-          for (int pass = 0; pass < (td.lo ? 2 : 1); ++pass) {
-            for (int st = st0; st < st1; ++st) {
-              mbar_wait(&empty_bar[s], ph ^ 1);
-              mbar_expect_tx(&full_bar[s], DEC_STAGE);
-              uint8_t* a = smem + s * DEC_STAGE;
-              uint8_t* b = a + DEC_A_BYTES;
-              tma_load_3d(a, pass ? tmAlo : tmA, &full_bar[s], 0, td.arow, st * DEC_KB);
-              if (kBwd) {
-                tma_load_3d(b, &tmB, &full_bar[s], 0, n0, st * DEC_KB);
-              } else {
-                tma_load_2d(b, &tmB, &full_bar[s], n0, st * DEC_SK);
-                tma_load_2d(b + DEC_WBOX, &tmB, &full_bar[s], n0 + 64, st * DEC_SK);
-              }
-              if (++s == DEC_STAGES) { s = 0; ph ^= 1; }
+      const uint64_t pol_w = policy_evict_first();   // W streams once; keep L2 for the partials
+      DecGroup gr;
+      for (int u = u_begin; u < u_end;) {
+        u = dec_next_group(p, u, u_end, gr);
+        const DecTile td = p.tiles[gr.mt];
+        if (gr.kind == 0) {
+          const bool lo = gr.c >= p.C;
+          const int cc = lo ? gr.c - p.C : gr.c;
+          const int kb0 = cc * p.kbc, kb1 = min(nkb, kb0 + p.kbc);
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            mbar_expect_tx(&full_bar[s], DEC_KB_BYTES + gr.g * DEC_WBOX);
+            uint8_t* a = smem + s * DEC_STAGE;
+            uint8_t* b = a + dec_b_off(0);
+            tma_load_2d(a, lo ? tmAlo : tmA, &full_bar[s], kb * BK, td.arow);
+            for (int j = 0; j < gr.g; ++j) {
+              const int n0 = (gr.nt0 + j) * DEC_TN;
+              if (kBwd) tma_load_2d_hint(b + j * DEC_WBOX, &tmB, &full_bar[s], kb * BK, n0, pol_w);
+              else tma_load_2d_hint(b + j * DEC_WBOX, &tmB, &full_bar[s], n0, kb * BK, pol_w);
             }
+            if (++s == DEC_STAGES) { s = 0; ph ^= 1; }
           }
         } else {
-          for (int ls = 0; ls * 4 < td.chunk_count; ++ls) {
-            const int nq = min(4, td.chunk_count - ls * 4);
+          const int2 lp = p.lpieces[td.lp_begin + gr.c - 2 * p.C];
+          for (int e = lp.x; e < lp.x + lp.y; ++e) {
+            const int4 ls = p.lstages[e];
+            const bool lo_box = ls.w >= 0 && ls.w + ls.y * LORA_CHUNK > ls.z + 64;   // lo outside the hi box
             mbar_wait(&empty_bar[s], ph ^ 1);
-            mbar_expect_tx(&full_bar[s], DEC_ROWS * 128 + nq * 2 * LORA_CHUNK_BYTES);
+            mbar_expect_tx(&full_bar[s], (lo_box ? 2 : 1) * DEC_KB_BYTES + gr.g * ls.y * LORA_CHUNK_BYTES);
             uint8_t* a = smem + s * DEC_STAGE;
-            uint8_t* b = a + DEC_A_BYTES;
-            tma_load_2d(a, &tmAL, &full_bar[s], ls * BK, td.al_row);
-            for (int q = 0; q < nq; ++q) {
-              const int prow = p.chunks[td.chunk_begin + ls * 4 + q];
-              tma_load_2d(b + q * LORA_CHUNK_BYTES, &tmBP, &full_bar[s], n0, prow);
-              tma_load_2d(b + BK * 128 + q * LORA_CHUNK_BYTES, &tmBP, &full_bar[s], n0 + 64, prow);
+            uint8_t* b = a + dec_b_off(1);
+            tma_load_2d(a, &tmAL, &full_bar[s], ls.z, td.al_row);
+            if (lo_box) tma_load_2d(a + DEC_KB_BYTES, &tmAL, &full_bar[s], ls.w, td.al_row);
+            for (int j = 0; j < gr.g; ++j) {
+              const int n0 = (gr.nt0 + j) * DEC_TN;
+              if (ls.y == 4) {
+                tma_load_2d(b + j * DEC_WBOX, &tmBP64, &full_bar[s], n0, ls.x);
+              } else {
+                for (int q = 0; q < ls.y; ++q)
+                  tma_load_2d(b + j * DEC_WBOX + q * LORA_CHUNK_BYTES, &tmBP, &full_bar[s], n0, ls.x + q * LORA_CHUNK);
+              }
             }
             if (++s == DEC_STAGES) { s = 0; ph ^= 1; }
           }
@@ -207,94 +262,108 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc_base = make_idesc_bf16(BM, DEC_TN, false, !kBwd);
-    constexpr uint32_t idesc_lora = make_idesc_bf16(BM, DEC_TN, false, true);
     int s = 0;
     uint32_t ph = 0;
     int acc = 0;
     uint32_t acc_ph = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
-      int nt, mt, c;
-      dec_item(p, w, nt, mt, c);
-      const DecTile td = p.tiles[mt];
+    DecGroup gr;
+    for (int u = u_begin; u < u_end;) {
+      u = dec_next_group(p, u, u_end, gr);
+      const DecTile td = p.tiles[gr.mt];
       mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * DEC_TN;
-      uint32_t accum = 0;
-      if (c < p.C) {
-        const int st0 = c * p.nst / p.C, st1 = (c + 1) * p.nst / p.C;
-        for (int pass = 0; pass < (td.lo ? 2 : 1); ++pass) {
-          for (int st = st0; st < st1; ++st) {
-            mbar_wait(&full_bar[s], ph);
-            tc_fence_after();
-            if (lane == 0) {
-              const uint32_t a_addr = smem_u32(smem + s * DEC_STAGE);
-              const uint32_t b_addr = a_addr + DEC_A_BYTES;
-              const int kbs = min(DEC_KB, nkb - st * DEC_KB);
-              for (int cc = 0; cc < kbs; ++cc) {
-#pragma unroll
-                for (int k = 0; k < BK / UK; ++k) {
-                  const uint64_t ad = make_sdesc_sw128(a_addr + cc * (DEC_ROWS * 128) + k * 32, 16, 1024);
-                  const uint64_t bd = kBwd ? make_sdesc_sw128(b_addr + cc * (DEC_TN * 128) + k * 32, 16, 1024)
-                                           : make_sdesc_sw128(b_addr + (cc * 4 + k) * (UK * 128), DEC_WBOX, 1024);
-                  mma_bf16_ss(d_tmem, ad, bd, idesc_base, accum);
-                  accum = 1;
-                }
-              }
-              mma_commit(&empty_bar[s]);
-            }
-            __syncwarp();
-            if (++s == DEC_STAGES) { s = 0; ph ^= 1; }
-          }
-        }
+      const uint32_t d0 = tmem_base + acc * (DEC_G * DEC_TN);
+      // one UMMA covers the group's g n tiles (N = 64 g): their W boxes / pack boxes sit 8 KB /
+      // 2 KB apart (the MN-major LBO; backward: consecutive K-major row blocks)
+      const uint32_t idesc_base = make_idesc_bf16(BM, DEC_TN * gr.g, false, !kBwd);
+      const uint32_t idesc_lora = make_idesc_bf16(BM, DEC_TN * gr.g, false, true);
+      int nst, e0 = 0;
+      if (gr.kind == 0) {
+        const int cc = gr.c >= p.C ? gr.c - p.C : gr.c;
+        nst = min(nkb, (cc + 1) * p.kbc) - cc * p.kbc;
       } else {
-        for (int ls = 0; ls * 4 < td.chunk_count; ++ls) {
-          const int nq = min(4, td.chunk_count - ls * 4);
-          mbar_wait(&full_bar[s], ph);
-          tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a_addr = smem_u32(smem + s * DEC_STAGE);
-            const uint32_t b_addr = a_addr + DEC_A_BYTES;
-            for (int q = 0; q < nq; ++q) {
-              const uint64_t ad = make_sdesc_sw128(a_addr + q * 32, 16, 1024);
-              const uint64_t bd = make_sdesc_sw128(b_addr + q * LORA_CHUNK_BYTES, BK * 128, 1024);
-              mma_bf16_ss(d_tmem, ad, bd, idesc_lora, accum);
-              accum = 1;
+        const int2 lp = p.lpieces[td.lp_begin + gr.c - 2 * p.C];
+        e0 = lp.x;
+        nst = lp.y;
+      }
+      for (int st = 0; st < nst; ++st) {
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(smem + s * DEC_STAGE);
+          const uint32_t b_addr = a_addr + dec_b_off(gr.kind);
+          if (gr.kind == 0) {
+#pragma unroll
+            for (int k = 0; k < BK / UK; ++k) {
+              const uint64_t ad = make_sdesc_sw128(a_addr + k * 32, 16, 1024);
+              const uint64_t bd = kBwd ? make_sdesc_sw128(b_addr + k * 32, 16, 1024)
+                                       : make_sdesc_sw128(b_addr + k * (UK * 128), DEC_WBOX, 1024);
+              mma_bf16_ss(d0, ad, bd, idesc_base, (st != 0 || k != 0) ? 1u : 0u);
             }
-            mma_commit(&empty_bar[s]);
+          } else {
+            // this slice's hi columns, then its lo columns, against the same pack rows
+            const int4 ls = p.lstages[e0 + st];
+            const bool lo_box = ls.w >= 0 && ls.w + ls.y * LORA_CHUNK > ls.z + 64;
+            const uint32_t lo_addr = lo_box ? a_addr + DEC_KB_BYTES : a_addr + (ls.w - ls.z) * 2;
+            for (int h = 0; h < (ls.w >= 0 ? 2 : 1); ++h) {
+              for (int q = 0; q < ls.y; ++q) {
+                const uint64_t ad = make_sdesc_sw128((h ? lo_addr : a_addr) + q * 32, 16, 1024);
+                const uint64_t bd = make_sdesc_sw128(b_addr + q * LORA_CHUNK_BYTES, DEC_WBOX, 1024);
+                mma_bf16_ss(d0, ad, bd, idesc_lora, (st | h | q) != 0 ? 1u : 0u);
+              }
+            }
           }
-          __syncwarp();
-          if (++s == DEC_STAGES) { s = 0; ph ^= 1; }
+          mma_commit(&empty_bar[s]);
         }
+        __syncwarp();
+        if (++s == DEC_STAGES) { s = 0; ph ^= 1; }
       }
       if (lane == 0) mma_commit(&tfull_bar[acc]);
       __syncwarp();
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
   } else if (warp == 4 || warp == 5) {
-    // ------------------------------------------------------------ item partial -> workspace
-    // TMEM lane = tile row (warps 4 and 5 own lanes 0-63); layout [row][col], 512 B per row
+    // ------------------------------------------------------------ unit partials -> workspace
+    // TMEM lane = tile row (warps 4 and 5 own lanes 0-63); layout [row][col], 256 B per row;
+    // stored with L2 evict_last so the fixup finds them in L2 behind the streamed W
     const int row = (int)((warp - 4) * 32 + lane);
+    const uint64_t pol = policy_evict_last();
     int acc = 0;
     uint32_t acc_ph = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
-      int nt, mt, c;
-      dec_item(p, w, nt, mt, c);
-      const bool ok = row < p.tiles[mt].rows;
-      float4* dst = reinterpret_cast<float4*>(
-          p.part + ((int64_t)(nt * p.n_m + mt) * (p.C + 1) + c) * DEC_PART + (int64_t)row * DEC_TN);
+    int row_mt = -1, row_rows = 0, row_piece = -1;   // this row's tile / LoRA piece (-1: none)
+    DecGroup gr;
+    for (int u = u_begin; u < u_end;) {
+      u = dec_next_group(p, u, u_end, gr);
+      if (gr.mt != row_mt) {
+        row_mt = gr.mt;
+        const DecTile td = p.tiles[gr.mt];
+        row_rows = td.rows;
+        row_piece = -1;
+        if (row < td.rows && td.lp_count > 0) {
+          const DevSeg& sg = p.segs[p.row_seg[td.arow + row]];
+          if (sg.flags & SEGF_LORA) row_piece = sg.dec_piece;
+        }
+      }
+      // a LoRA piece stores only the rows whose rank block it holds (the fixup reads no other)
+      const bool ok = row < row_rows && (gr.kind == 0 || row_piece == gr.c - 2 * p.C);
       mbar_wait(&tfull_bar[acc], acc_ph);
       tc_fence_after();
+      for (int j = 0; j < gr.g; ++j) {
+        float4* dst = reinterpret_cast<float4*>(
+            p.part + ((int64_t)(gr.mt * p.n_n + gr.nt0 + j) * p.S + gr.c) * DEC_PART + (int64_t)row * DEC_TN);
 #pragma unroll
-      for (int h = 0; h < DEC_TN / 32; ++h) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + acc * DEC_TN + h * 32 + (((warp - 4) * 32u) << 16), r);
-        tmem_wait_ld();
-        if (ok) {
+        for (int h = 0; h < DEC_TN / 32; ++h) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + acc * (DEC_G * DEC_TN) + j * DEC_TN + h * 32 + (((warp - 4) * 32u) << 16), r);
+          tmem_wait_ld();
+          if (ok) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            __stcg(dst + h * 8 + j, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+            for (int q = 0; q < 8; ++q)
+              st_f4_evict_last(dst + h * 8 + q,
+                               make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])),
+                               pol);
+          }
         }
       }
       tc_fence_before();
@@ -304,25 +373,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   }
   __syncthreads();
+  if (p.trace && threadIdx.x == 0) {
+    p.trace[4 * blockIdx.x + 1] = globaltimer_ns();
+    p.trace[4 * blockIdx.x + 2] = u_begin;
+    p.trace[4 * blockIdx.x + 3] = u_end;
+  }
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * DEC_TN);
+    tmem_dealloc(tmem_base, 2 * DEC_G * DEC_TN);
   }
 }
 
-// K1d fixup: y = ((p_0 + p_1) + ... + p_{C-1}) + p_lora, then bias / y_base / IA3 / dst, for
-// every valid row of every decode tile. Launched behind the GEMM (PDL: the grid is resident
-// early and waits on griddepcontrol.wait, which covers the GEMM's partial stores). One CTA per
-// 16 rows x 128 columns of a tile; a thread owns one row x 8 columns and issues the loads of all
-// C (+1) partials before the first add (the sum order is fixed, the loads are not serialised).
-constexpr int DEC_FIX_ROWS = 16;
+// K1d fixup: y = fold(p_0 .. p_{C-1}, [lo_0 .. lo_{C-1}], [p_lora]) left to right, then bias /
+// y_base / IA3 / dst, for every valid row of every decode tile. Launched behind the GEMM (PDL: the
+// grid is resident early and waits on griddepcontrol.wait, which covers the GEMM's partial
+// stores). One CTA per 32 rows x 64 columns of a tile; a thread owns one row x 8 columns and
+// issues the loads of 8 partials at a time before adding them (the sum order is fixed, the loads
+// are not serialised).
+constexpr int DEC_FIX_ROWS = 32;
 constexpr int DEC_FIX_THREADS = DEC_FIX_ROWS * (DEC_TN / 8);   // 256
 
 __global__ void __launch_bounds__(DEC_FIX_THREADS)
     dec_fixup_kernel(const DecParams p) {
   const int q = blockIdx.x % (DEC_ROWS / DEC_FIX_ROWS);
-  const int tile = blockIdx.x / (DEC_ROWS / DEC_FIX_ROWS);
-  const int nt = tile / p.n_m, mt = tile - nt * p.n_m;
+  const int tile = blockIdx.x / (DEC_ROWS / DEC_FIX_ROWS);   // mt * n_n + nt
+  const int mt = tile / p.n_n, nt = tile - mt * p.n_n;
   const int row = q * DEC_FIX_ROWS + (int)(threadIdx.x / (DEC_TN / 8));
   const int col = (int)(threadIdx.x % (DEC_TN / 8)) * 8;
   const DecTile td = p.tiles[mt];
@@ -330,29 +405,43 @@ __global__ void __launch_bounds__(DEC_FIX_THREADS)
   pdl_trigger();
   const int n = nt * DEC_TN + col;
   if (row >= td.rows || n >= p.N) return;
-  const float4* src = reinterpret_cast<const float4*>(p.part + (int64_t)tile * (p.C + 1) * DEC_PART +
+  const float4* src = reinterpret_cast<const float4*>(p.part + (int64_t)tile * p.S * DEC_PART +
                                                       (int64_t)row * DEC_TN + col);
   constexpr int P4 = DEC_PART / 4;
-  float4 buf[DEC_MAX_C + 1][2];
+  const int xrow = td.arow + row;
+  const DevSeg sg = p.segs[p.row_seg[xrow]];
+  // slots in fold order: hi chunks 0..C-1, lo chunks C..2C-1 (lo tiles only), then the LoRA
+  // piece holding this row's rank block (every other piece is exact zeros for this row)
+  const int nhl = td.lo ? 2 * p.C : p.C;
+  const int nslots = nhl + ((sg.flags & SEGF_LORA) && td.lp_count > 0 ? 1 : 0);
+  float v[8];
+  for (int i0 = 0; i0 < nslots; i0 += 8) {
+    float4 buf[8][2];
 #pragma unroll
-  for (int c = 0; c <= DEC_MAX_C; ++c) {
-    if (c < p.C || (c == p.C && td.chunk_count > 0)) {
-      buf[c][0] = __ldcg(src + c * P4);
-      buf[c][1] = __ldcg(src + c * P4 + 1);
+    for (int i = 0; i < 8; ++i) {
+      if (i0 + i < nslots) {
+        const int slot = i0 + i < nhl ? i0 + i : 2 * p.C + sg.dec_piece;
+        const float4* s = src + (int64_t)slot * P4;
+        buf[i][0] = __ldcg(s);
+        buf[i][1] = __ldcg(s + 1);
+      }
     }
-  }
-  float v[8] = {buf[0][0].x, buf[0][0].y, buf[0][0].z, buf[0][0].w,
-                buf[0][1].x, buf[0][1].y, buf[0][1].z, buf[0][1].w};
 #pragma unroll
-  for (int c = 1; c <= DEC_MAX_C; ++c) {
-    if (c < p.C || (c == p.C && td.chunk_count > 0)) {
-      v[0] += buf[c][0].x; v[1] += buf[c][0].y; v[2] += buf[c][0].z; v[3] += buf[c][0].w;
-      v[4] += buf[c][1].x; v[5] += buf[c][1].y; v[6] += buf[c][1].z; v[7] += buf[c][1].w;
+    for (int i = 0; i < 8; ++i) {
+      if (i0 + i < nslots) {
+        const float w[8] = {buf[i][0].x, buf[i][0].y, buf[i][0].z, buf[i][0].w,
+                            buf[i][1].x, buf[i][1].y, buf[i][1].z, buf[i][1].w};
+        if (i0 + i == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = w[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] += w[j];
+        }
+      }
     }
   }
   const int ncols = min(8, p.N - n);
-  const int xrow = td.arow + row;
-  const DevSeg sg = p.segs[p.row_seg[xrow]];
   const int64_t r_local = xrow - sg.xrow0 + sg.xlocal0;
   const bool bf = sg.flags & SEGF_DST_BF16, bbf = sg.flags & SEGF_BASE_BF16;
   if (p.has_bias) {

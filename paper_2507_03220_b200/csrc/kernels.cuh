@@ -52,7 +52,7 @@ struct DevSeg {
   float lora_scale;    // alpha / r
   int32_t pack_row;    // first row of this client's rank block in the layer's LoRA packs
   int32_t rank_pad;    // rank rounded up to 16
-  int32_t pad_;
+  int32_t dec_piece;   // decode class (decode.cuh): the LoRA piece of its tile holding its rank block
 };
 
 constexpr int BM = 128;           // rows per tile == TMEM lanes

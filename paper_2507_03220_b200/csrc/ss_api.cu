@@ -50,13 +50,14 @@ struct Layer {
   float* bias = nullptr;
   CUtensorMap tm_w_fwd, tm_w_bwd, tm_w_bwd2, tm_w_bwd64;  // bwd box rows 256 / 128 / 64
   CUtensorMap tm_w_fwd_s, tm_w_bwd_s;                      // weight-streaming kernel
-  CUtensorMap tm_w_fwd_d, tm_w_bwd_d;                      // split-K decode kernel (K1d)
+  CUtensorMap tm_w_dec;                                    // split-K decode kernel (K1d): {64, 64} boxes
   // LoRA packs: rows = rank index of every registered client (16-aligned blocks)
   __nv_bfloat16* at_pack = nullptr;  // [cap, ld_at]  (A^T: rank rows x d_in)
   __nv_bfloat16* b_pack = nullptr;   // [cap, ld_b]   (B:   rank rows x d_out)
   int64_t ld_at = 0, ld_b = 0;
   int pack_rows = 0, pack_cap = 0;
   CUtensorMap tm_at, tm_b;
+  CUtensorMap tm_at64, tm_b64;   // same packs, {64, 64-row} boxes (decode-class LoRA stages)
   std::map<uint32_t, AdapterSlot> adapters;
 };
 
@@ -120,9 +121,9 @@ struct ss_ctx {
   int stream_pdl = 1;
   int wide_decode = 1;           // decode-size dispatches: 128-wide single-CTA tiles when they fit one wave
   // segments of <= decode_rows rows reduce K in the decode class's split-K order (K1d, decode.cuh)
-  int decode_rows = 0;
-  int decode_chunks = 8;           // max K chunks of the decode class's order (numerics!)
-  int decode_ctas = 1;             // K1d CTAs per SM (persistent grid)
+  int decode_rows = 16;
+  int decode_chunk_kb = 20;          // 64-deep k-blocks per K chunk of the decode class (numerics!)
+  long long* decode_trace = nullptr; // testing: K1d per-CTA timings (device buffer, 4 x int64 per CTA)
   int* sync_ctr = nullptr;       // [2] shrink-done counter + GEMM ticket (zero between dispatches)
   struct HostSlot {
     void* in = nullptr;
@@ -365,6 +366,8 @@ int grow_packs(ss_ctx* ctx, Layer& L, int need_rows) {
   ctx->adapter_bytes += (int64_t)cap * (L.ld_at + L.ld_b) * 2;
   int rc = encode_2d(ctx, &L.tm_at, L.at_pack, L.d_in, cap, L.ld_at, 64, LORA_CHUNK);
   if (rc) return rc;
+  if ((rc = encode_2d(ctx, &L.tm_at64, L.at_pack, L.d_in, cap, L.ld_at, 64, 64))) return rc;
+  if ((rc = encode_2d(ctx, &L.tm_b64, L.b_pack, L.d_out, cap, L.ld_b, 64, 64))) return rc;
   return encode_2d(ctx, &L.tm_b, L.b_pack, L.d_out, cap, L.ld_b, 64, LORA_CHUNK);
 }
 
@@ -507,8 +510,9 @@ struct Built {
   size_t off_tm = 0, off_seg = 0, off_tile = 0, off_piece = 0, off_ch = 0, off_st = 0, off_it = 0;
   // decode-class part (K1d): tiles, LoRA runs, X / X_lo tensor maps, cluster size
   size_t off_dt = 0;
-  int dec_items_per_n = 0;
-  int n_dec = 0, dec_C = 0;
+  size_t off_dcb = 0, off_lp = 0, off_ls = 0;   // K1d per-CTA unit ranges, LoRA pieces / stages
+  int dec_S = 0;
+  int n_dec = 0, dec_C = 0, dec_kbc = 0, dec_grid = 0;
   int32_t dec_amap = 0, dec_alo = 0;
   int64_t Mp = 0;                      // single-chain rows (M - decode-class rows)
   double dec_flops = 0, dec_bytes = 0;
@@ -741,10 +745,14 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     if (d.flags & SEGF_IA3_LO) t.lo = 1;
     dtile_of[j] = (int32_t)dtiles.size() - 1;
   }
-  const int dec_C = dtiles.empty() ? 0 : std::min(dec_stages(K), ctx->decode_chunks);
+  const int dec_kbc = ctx->decode_chunk_kb;
+  const int dec_C = dtiles.empty() ? 0 : (K / BK + dec_kbc - 1) / dec_kbc;
 
   // ---- LoRA: per tile rank-chunk lists (block-diagonal over the tile's segments) + shrink items
   std::vector<int32_t> chunks;
+  std::vector<int2> lpieces;      // decode tiles' LoRA pieces {first stage, stage count}
+  std::vector<int4> lstages;      // decode LoRA stages {pack row, 16-row chunks, A_lora hi col, lo col | -1}
+  int lp_chunks = 0;
   std::vector<ShrinkItem> items;
   int max_cols = 0;
   if (any_lora) {
@@ -782,16 +790,32 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
       td.chunk_count = (int32_t)chunks.size() - td.chunk_begin;
       max_cols = std::max(max_cols, td.chunk_count * LORA_CHUNK);
     }
-    // decode tiles: the tile's rank chunks, block-diagonal over its segments (one piece each)
+    // decode tiles: the tile's rank chunks, block-diagonal over its segments, cut into pieces of
+    // whole segments of <= DEC_LP_CHUNKS chunks (one LoRA chain each, see decode.cuh)
     for (size_t t = 0; t < dtiles.size(); ++t) {
       DecTile& dt = dtiles[t];
       dt.al_row = (int32_t)((int64_t)num_m * TM + (int64_t)t * DEC_ROWS);
       dt.chunk_begin = (int32_t)chunks.size();
+      dt.lp_begin = (int32_t)lpieces.size();
       for (size_t j = 0; j < ds.size(); ++j) {
         if (dtile_of[j] != (int32_t)t || !(ds[j].flags & SEGF_LORA)) continue;
-        const DevSeg& d = ds[j];
+        DevSeg& d = ds[j];
         const int col = (int)(chunks.size() - dt.chunk_begin) * LORA_CHUNK;
         const int hilo = ctx->lora_hilo == 2 || (ctx->lora_hilo == 1 && !(d.flags & SEGF_DST_BF16));
+        const int nch = (1 + hilo) * (d.rank_pad / LORA_CHUNK);
+        if (dt.lp_count == 0 || lp_chunks + nch > DEC_LP_CHUNKS) {
+          lpieces.push_back(make_int2((int)lstages.size(), 0));
+          dt.lp_count++;
+          lp_chunks = 0;
+        }
+        lp_chunks += nch;
+        // one stage per 64-row slice of the rank block: its B rows once, hi then lo columns
+        for (int r0 = 0; r0 < d.rank_pad; r0 += 64) {
+          lstages.push_back(make_int4(d.pack_row + r0, std::min(4, (d.rank_pad - r0) / LORA_CHUNK), col + r0,
+                                      hilo ? col + d.rank_pad + r0 : -1));
+          lpieces.back().y++;
+        }
+        d.dec_piece = dt.lp_count - 1;
         for (int rep = 0; rep <= hilo; ++rep)
           for (int q = 0; q < d.rank_pad / LORA_CHUNK; ++q) chunks.push_back(d.pack_row + q * LORA_CHUNK);
         const int p0 = d.xrow0 - dt.arow;
@@ -923,13 +947,13 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   if (!dtiles.empty()) {
     B.dec_amap = (int32_t)tmaps.size();
     tmaps.emplace_back();
-    if ((rc = encode_kchunks(ctx, &tmaps.back(), ctx->X, K, MX, ldx, DEC_ROWS, DEC_KB))) return rc;
+    if ((rc = encode_2d(ctx, &tmaps.back(), ctx->X, K, MX, ldx, 64, DEC_ROWS))) return rc;
     B.dec_alo = B.dec_amap;
     for (const DecTile& t : dtiles) {
       if (!t.lo) continue;
       B.dec_alo = (int32_t)tmaps.size();
       tmaps.emplace_back();
-      if ((rc = encode_kchunks(ctx, &tmaps.back(), ctx->X_lo, K, MX, ldx, DEC_ROWS, DEC_KB))) return rc;
+      if ((rc = encode_2d(ctx, &tmaps.back(), ctx->X_lo, K, MX, ldx, 64, DEC_ROWS))) return rc;
       break;
     }
   }
@@ -987,6 +1011,43 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
 
   // ---- serialise the device tables
   const size_t off_tm = 0;
+  // ---- K1d units (tile m, chunk, 64-column tile n) and their cost-balanced per-CTA ranges
+  std::vector<int32_t> dcb;
+  if (!dtiles.empty()) {
+    const int n_n = (N + DEC_TN - 1) / DEC_TN;
+    const int nkb = K / BK;
+    std::vector<double> cost;
+    for (DecTile& t : dtiles) {
+      t.unit_begin = (int32_t)cost.size();
+      for (int rep = 0; rep <= t.lo; ++rep)
+        for (int c = 0; c < dec_C; ++c) {
+          const int kbs = std::min(nkb, (c + 1) * dec_kbc) - c * dec_kbc;
+          for (int n = 0; n < n_n; ++n) cost.push_back(kbs * (DEC_WBOX + DEC_KB_BYTES / (double)DEC_G));
+        }
+      for (int q = 0; q < t.lp_count; ++q) {
+        double c = 0;
+        const int2 lp = lpieces[t.lp_begin + q];
+        for (int e = lp.x; e < lp.x + lp.y; ++e)
+          c += lstages[e].y * 2.0 * LORA_CHUNK_BYTES + DEC_KB_BYTES;   // (measured: ~2x the bytes' share)
+        for (int n = 0; n < n_n; ++n) cost.push_back(c);
+      }
+    }
+    const int units = (int)cost.size();
+    const int grid = std::min(units, ctx->num_sms);
+    double total_cost = 0;
+    for (double c : cost) total_cost += c;
+    dcb.assign(grid + 1, units);
+    dcb[0] = 0;
+    double run = 0;
+    int b = 1;
+    for (int u = 0; u < units && b < grid; ++u) {
+      run += cost[u];
+      // cut after unit u once this CTA holds its share (every CTA keeps at least one unit)
+      while (b < grid && run >= total_cost * b / grid && u + 1 >= b) dcb[b++] = u + 1;
+    }
+    for (; b < grid; ++b) dcb[b] = std::max(dcb[b - 1], units - (grid - b));
+    B.dec_grid = grid;
+  }
   const size_t off_seg = round_up(tmaps.size() * sizeof(CUtensorMap), 256);
   const size_t off_tile = off_seg + round_up(ds.size() * sizeof(DevSeg), 256);
   const size_t off_piece = off_tile + round_up(tiles.size() * sizeof(TileDesc), 256);
@@ -994,7 +1055,10 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   const size_t off_st = off_ch + round_up(std::max<size_t>(1, chunks.size()) * 4, 256);
   const size_t off_it = off_st + round_up(std::max<size_t>(1, stores.size()) * sizeof(int2), 256);
   const size_t off_dt = off_it + round_up(std::max<size_t>(1, items.size()) * sizeof(ShrinkItem), 256);
-  const size_t total = off_dt + round_up(std::max<size_t>(1, dtiles.size()) * sizeof(DecTile), 256);
+  const size_t off_dcb = off_dt + round_up(std::max<size_t>(1, dtiles.size()) * sizeof(DecTile), 256);
+  const size_t off_lp = off_dcb + round_up(std::max<size_t>(1, dcb.size()) * 4, 256);
+  const size_t off_ls = off_lp + round_up(std::max<size_t>(1, lpieces.size()) * sizeof(int2), 256);
+  const size_t total = off_ls + round_up(std::max<size_t>(1, lstages.size()) * sizeof(int4), 256);
   B.blob.assign(total, 0);
   char* h = B.blob.data();
   memcpy(h + off_tm, tmaps.data(), tmaps.size() * sizeof(CUtensorMap));
@@ -1006,16 +1070,25 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     memcpy(h + off_ch, chunks.data(), chunks.size() * 4);
     memcpy(h + off_it, items.data(), items.size() * sizeof(ShrinkItem));
   }
-  if (!dtiles.empty()) memcpy(h + off_dt, dtiles.data(), dtiles.size() * sizeof(DecTile));
+  if (!dtiles.empty()) {
+    memcpy(h + off_dt, dtiles.data(), dtiles.size() * sizeof(DecTile));
+    memcpy(h + off_dcb, dcb.data(), dcb.size() * 4);
+    if (!lpieces.empty()) memcpy(h + off_lp, lpieces.data(), lpieces.size() * sizeof(int2));
+    if (!lstages.empty()) memcpy(h + off_ls, lstages.data(), lstages.size() * sizeof(int4));
+  }
+  B.off_lp = off_lp;
+  B.off_ls = off_ls;
+  B.dec_S = 2 * dec_C + 1;
+  for (const DecTile& t : dtiles) B.dec_S = std::max(B.dec_S, 2 * dec_C + t.lp_count);
   B.off_tm = off_tm; B.off_seg = off_seg; B.off_tile = off_tile; B.off_piece = off_piece;
-  B.off_ch = off_ch; B.off_st = off_st; B.off_it = off_it; B.off_dt = off_dt;
+  B.off_ch = off_ch; B.off_st = off_st; B.off_it = off_it; B.off_dt = off_dt; B.off_dcb = off_dcb;
   B.n_dec = (int)dtiles.size();
   B.dec_C = dec_C;
-  for (const DecTile& t : dtiles) B.dec_items_per_n += dec_C + (t.chunk_count > 0 ? 1 : 0);
+  B.dec_kbc = dec_kbc;
   if (!dtiles.empty()) {
     const int64_t tiles_dec = (int64_t)dtiles.size() * ((N + DEC_TN - 1) / DEC_TN);
     if ((rc = ensure_dev(ctx, ctx->dec_part, ctx->dec_part_cap,
-                         (size_t)tiles_dec * (dec_C + 1) * DEC_PART * sizeof(float)))) return rc;
+                         (size_t)tiles_dec * B.dec_S * DEC_PART * sizeof(float)))) return rc;
   }
   B.Mp = Mp;
   B.M = M; B.MX = MX; B.lora_ld = lora_ld; B.al_rows = al_rows; B.ldx = ldx;
@@ -1266,7 +1339,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     ctx->launches++;
   }
   if (overlap) CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));   // join the side stream
-  // ---- K1d: decode-class rows, persistent split-K (dec_C chunks + a LoRA item per tile)
+  // ---- K1d: decode-class rows, persistent split-K (dec_C chunks + a LoRA chain per tile) + fixup
   if (B.n_dec > 0) {
     CUtensorMap tmALd = L.tm_w_fwd;   // (unused without LoRA)
     if (any_lora && (rc = encode_2d(ctx, &tmALd, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, DEC_ROWS))) return rc;
@@ -1274,10 +1347,10 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     dp.N = N;
     dp.K = K;
     dp.C = B.dec_C;
-    dp.nst = dec_stages(K);
+    dp.kbc = B.dec_kbc;
     dp.n_m = B.n_dec;
     dp.n_n = (N + DEC_TN - 1) / DEC_TN;
-    dp.items_per_n = B.dec_items_per_n;
+    dp.S = B.dec_S;
     dp.has_bias = gpm.has_bias;
     dp.ia3_in_epilogue = gpm.ia3_in_epilogue;
     dp.bias = L.bias;
@@ -1285,16 +1358,20 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     dp.row_seg = ctx->row_seg;
     dp.tiles = reinterpret_cast<const DecTile*>(dv + B.off_dt);
     dp.chunks = gpm.chunks;
+    dp.cta_begin = reinterpret_cast<const int32_t*>(dv + B.off_dcb);
+    dp.lpieces = reinterpret_cast<const int2*>(dv + B.off_lp);
+    dp.lstages = reinterpret_cast<const int4*>(dv + B.off_ls);
     dp.tmaps = d_tmaps;
     dp.amap = B.dec_amap;
     dp.alo_map = B.dec_alo;
     dp.part = ctx->dec_part;
-    const int n_items = dp.n_n * dp.items_per_n;
-    const int dgrid = std::min(n_items, ctx->num_sms * ctx->decode_ctas);
+    dp.trace = ctx->decode_trace;
+    const int dgrid = B.dec_grid;
     const bool dpdl = ctx->pdl && !ctx->profiling;
     const int pd = prof_begin(ctx, stream, SS_KERNEL_GEMM, B.dec_flops, B.dec_bytes);
-    if (bwd) CK(launch_kp(dpdl, seg_gemm_dec_kernel<true>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_bwd_d, tmALd, tmBP, dp));
-    else CK(launch_kp(dpdl, seg_gemm_dec_kernel<false>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_fwd_d, tmALd, tmBP, dp));
+    const CUtensorMap& tmBP64 = any_lora ? (bwd ? L.tm_at64 : L.tm_b64) : L.tm_w_fwd;
+    if (bwd) CK(launch_kp(dpdl, seg_gemm_dec_kernel<true>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_dec, tmALd, tmBP, tmBP64, dp));
+    else CK(launch_kp(dpdl, seg_gemm_dec_kernel<false>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_dec, tmALd, tmBP, tmBP64, dp));
     CK(launch_kp(dpdl, dec_fixup_kernel, dp.n_n * dp.n_m * (DEC_ROWS / DEC_FIX_ROWS), DEC_FIX_THREADS, 0, stream, dp));
     prof_end(ctx, stream, pd);
     CK(cudaGetLastError());
@@ -1586,14 +1663,13 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
     ctx->decode_rows = (int)value;
     return SS_OK;
   }
-  if (!strcmp(key, "decode_chunks")) {
-    if (value < 1 || value > DEC_MAX_C) return fail(ctx, SS_E_ARG, "decode_chunks must be 1..%d", DEC_MAX_C);
-    ctx->decode_chunks = (int)value;
+  if (!strcmp(key, "decode_trace")) {
+    ctx->decode_trace = reinterpret_cast<long long*>(static_cast<intptr_t>(value));
     return SS_OK;
   }
-  if (!strcmp(key, "decode_ctas")) {
-    if (value < 1 || value > 2) return fail(ctx, SS_E_ARG, "decode_ctas must be 1 or 2");
-    ctx->decode_ctas = (int)value;
+  if (!strcmp(key, "decode_chunk_kb")) {
+    if (value < 1 || value > DEC_MAX_KBC) return fail(ctx, SS_E_ARG, "decode_chunk_kb must be 1..%d", DEC_MAX_KBC);
+    ctx->decode_chunk_kb = (int)value;
     return SS_OK;
   }
   if (!strcmp(key, "wide_decode")) {
@@ -1680,10 +1756,8 @@ int ss_load_layer(ss_ctx* ctx, int block, int role, int d_in, int d_out, const v
   if (rc) return rc;
   rc = encode_kchunks(ctx, &L.tm_w_bwd_s, L.W, L.ldw, d_in, L.ldw, 64, 4);
   if (rc) return rc;
-  // split-K decode kernel: forward box {64 n, 128 k}; backward 2 K-chunks of 128 rows
-  rc = encode_2d(ctx, &L.tm_w_fwd_d, L.W, d_out, d_in, L.ldw, 64, DEC_SK);
-  if (rc) return rc;
-  rc = encode_kchunks(ctx, &L.tm_w_bwd_d, L.W, L.ldw, d_in, L.ldw, DEC_TN, DEC_KB);
+  // split-K decode kernel: {64, 64} boxes of W (forward {64 n, 64 k}, backward {64 k, 64 n})
+  rc = encode_2d(ctx, &L.tm_w_dec, L.W, d_out, d_in, L.ldw, 64, 64);
   if (rc) return rc;
   ctx->weight_bytes += (int64_t)d_in * L.ldw * 2 + (bias ? round_up(d_out, 64) * 4 : 0);
   ctx->layers[{block, role}] = L;

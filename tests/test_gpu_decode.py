@@ -1,11 +1,12 @@
-"""Decode-class rows (segments of <= decode_rows rows): the split-K cluster kernel K1d
-(csrc/decode.cuh). Their K reduction is C = min(8, ceil(K/128)) fixed chunks summed in chunk
-order, a property of the request and the layer alone, so
+"""Decode-class rows (segments of <= decode_rows rows): the split-K kernel K1d + its fixup
+(csrc/decode.cuh). Their K reduction is C = ceil(K / (64 * decode_chunk_kb)) fixed chunks folded
+left to right, then the row's own LoRA chain, a property of the request and the layer alone, so
 
 * parity: against an fp32 evaluation of the reference math (tensor_ops.py:71-89,
   adapters.py:19-40, 127-145, client.py:291-294) at the same tolerances as every other row;
 * batching invisibility (acceptance C5): a decode-class request gives the same bits solo, with
-  other decode requests (several 64-row decode tiles), and beside prefill-class requests;
+  other decode requests (several 64-row decode tiles, LoRA pieces cut differently), and beside
+  prefill-class requests;
 * pieces keep their request's class: the host pipelines split requests into sub-batches, and a
   piece of a decode (prefill) request reduces K as the whole request would.
 """

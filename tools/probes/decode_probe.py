@@ -1,7 +1,7 @@
 """Decode-size dispatches (32 clients x 2 rows) over 13B layer shapes through the C ABI: GEMM
 kernel time per dispatch (ss_profile) and achieved W bytes/s, decode class (decode_rows 16,
 K1d) against the single-chain kernels (decode_rows 0). args: [iters] [shapes...] [--lora]
-Shapes: q ff_up ff_down lm_head (default all)."""
+Shapes: q ff_up ff_down lm_head (default all). SS_OPTS="key=value,..." sets context options."""
 import ctypes
 import sys
 
@@ -67,6 +67,33 @@ for name in names:
         lib.ss_profile_read(ctx, 2, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl), ctypes.byref(by))
         L.check(ctx, lib.ss_profile(ctx, 0))
         g_us = ms.value / max(1, n.value) * 1e3
+        if "--trace" in sys.argv and mode:
+            tr = torch.zeros(4 * 148, dtype=torch.int64, device=dev)
+            L.check(ctx, lib.ss_set_option(ctx, b"decode_trace", tr.data_ptr()))
+            L.check(ctx, lib.ss_compute_batch(ctx, 0, 0, 4, n_cl, arr, stream, st))
+            torch.cuda.synchronize()
+            L.check(ctx, lib.ss_set_option(ctx, b"decode_trace", 0))
+            t = tr.view(148, 4).cpu().tolist()
+            t0 = min(r[0] for r in t if r[1])
+            nn = (N + 63) // 64
+            C = (K // 64 + 19) // 20
+            durs = []
+            for b, (s0, s1, u0, u1) in enumerate(t):
+                if not s1:
+                    continue
+                ch = max(0, min(u1, C * nn) - u0)
+                durs.append((s1 - s0) / 1e3)
+                if b % 8 == 0 or (s1 - s0) / 1e3 > 1.3 * 0 + 0:
+                    pass
+            order = sorted(range(len(durs)), key=lambda i: -durs[i])
+            print(f"   trace: start spread {(max(r[0] for r in t if r[1]) - t0)/1e3:.1f} us, "
+                  f"end max {(max(r[1] for r in t) - t0)/1e3:.1f} us, dur min/med/max "
+                  f"{min(durs):.1f}/{sorted(durs)[len(durs)//2]:.1f}/{max(durs):.1f} us")
+            for b in order[:6] + order[-3:]:
+                s0, s1, u0, u1 = t[b]
+                ch = max(0, min(u1, C * nn) - u0)
+                print(f"     cta {b:3d} start {(s0-t0)/1e3:6.1f} dur {(s1-s0)/1e3:6.1f} us units {u0}-{u1} "
+                      f"(chunk {ch}, lora {u1-u0-ch})")
         print(f"{name:8s} K={K:6d} N={N:6d} decode_rows={mode:2d} lora={int(lora)}: gemm {g_us:7.2f} us "
               f"({K * N * 2 / (g_us * 1e-6) / 1e9:6.0f} GB/s of W), dispatch {e0.elapsed_time(e1) / iters * 1e3:7.2f} us",
               flush=True)
