@@ -88,6 +88,8 @@ struct DecParams {
   int amap, alo_map;     // X / X_lo as {64 k, 64 rows, kbc k-blocks} boxes
   float* part;           // [(m * n_n + n) * S + slot][DEC_ROWS][DEC_TN] fp32 partials
   long long* trace;      // testing: per CTA {start ns, end ns, first unit, end unit} (nullptr: off)
+  int pdl_early;         // launched behind the gather / shrink: the producer streams its first W
+                         // stages before griddepcontrol.wait (every other role waits on its loads)
 };
 
 __device__ __forceinline__ long long globaltimer_ns() {
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();
+  if (!p.pdl_early) pdl_wait();
   pdl_trigger();
 
   if (warp == 0) {
@@ -209,12 +211,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      int pre = 0;      // stages whose W was issued before griddepcontrol.wait (A still to load)
       const CUtensorMap* tmA = p.tmaps + p.amap;
       const CUtensorMap* tmAlo = p.tmaps + p.alo_map;
       tensormap_acquire(tmA);
       if (p.alo_map != p.amap) tensormap_acquire(tmAlo);
       const uint64_t pol_w = policy_evict_first();   // W streams once; keep L2 for the partials
       DecGroup gr;
+      if (p.pdl_early) {
+        // the first group's first stages: W (no dependency on the previous kernels) now, A (the
+        // gathered rows) after griddepcontrol.wait
+        if (u_begin < u_end) {
+          dec_next_group(p, u_begin, u_end, gr);
+          if (gr.kind == 0) {
+            const int cc = gr.c >= p.C ? gr.c - p.C : gr.c;
+            pre = min(DEC_STAGES, min(nkb, (cc + 1) * p.kbc) - cc * p.kbc);
+            for (int st = 0; st < pre; ++st) {
+              const int kb = cc * p.kbc + st;
+              mbar_expect_tx(&full_bar[st], DEC_KB_BYTES + gr.g * DEC_WBOX);
+              uint8_t* b = smem + st * DEC_STAGE + dec_b_off(0);
+              for (int j = 0; j < gr.g; ++j) {
+                const int n0 = (gr.nt0 + j) * DEC_TN;
+                if (kBwd) tma_load_2d_hint(b + j * DEC_WBOX, &tmB, &full_bar[st], kb * BK, n0, pol_w);
+                else tma_load_2d_hint(b + j * DEC_WBOX, &tmB, &full_bar[st], n0, kb * BK, pol_w);
+              }
+            }
+          }
+        }
+        pdl_wait();
+      }
       for (int u = u_begin; u < u_end;) {
         u = dec_next_group(p, u, u_end, gr);
         const DecTile td = p.tiles[gr.mt];
@@ -223,6 +248,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const int cc = lo ? gr.c - p.C : gr.c;
           const int kb0 = cc * p.kbc, kb1 = min(nkb, kb0 + p.kbc);
           for (int kb = kb0; kb < kb1; ++kb) {
+            if (pre > 0) {
+              // W of this stage is already in flight (ring slot kb - kb0 of the first pass)
+              tma_load_2d(smem + s * DEC_STAGE, lo ? tmAlo : tmA, &full_bar[s], kb * BK, td.arow);
+              --pre;
+              if (++s == DEC_STAGES) { s = 0; ph ^= 1; }
+              continue;
+            }
             mbar_wait(&empty_bar[s], ph ^ 1);
             mbar_expect_tx(&full_bar[s], DEC_KB_BYTES + gr.g * DEC_WBOX);
             uint8_t* a = smem + s * DEC_STAGE;

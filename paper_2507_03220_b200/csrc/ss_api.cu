@@ -1366,8 +1366,12 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     dp.alo_map = B.dec_alo;
     dp.part = ctx->dec_part;
     dp.trace = ctx->decode_trace;
+    // streams its first W stages behind the kernel before it when that is the gather or the
+    // main-stream shrink of this dispatch (PDL edge; not across an event join)
+    const bool dec_early = ctx->stream_pdl && !ctx->profiling && MX > 0 && !side && num_m == 0;
+    dp.pdl_early = dec_early ? 1 : 0;
     const int dgrid = B.dec_grid;
-    const bool dpdl = ctx->pdl && !ctx->profiling;
+    const bool dpdl = (ctx->pdl || dec_early) && !ctx->profiling;
     const int pd = prof_begin(ctx, stream, SS_KERNEL_GEMM, B.dec_flops, B.dec_bytes);
     const CUtensorMap& tmBP64 = any_lora ? (bwd ? L.tm_at64 : L.tm_b64) : L.tm_w_fwd;
     if (bwd) CK(launch_kp(dpdl, seg_gemm_dec_kernel<true>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_dec, tmALd, tmBP, tmBP64, dp));
