@@ -371,6 +371,9 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *                       kernel K1d + fixup), then their own LoRA chain; every other row reduces K
  *                       as one chain. 0: no decode class (every row single-chain).
  *   decode_chunk_kb (20) 64-deep k-blocks per chunk of the decode class's order (1..64)
+ *   grad_fused (0)      ss_adapter_grads: LoRA shrinks + token contractions in one launch, client
+ *                       by client (x / g re-read from L2); 0: two launches (bitwise the same)
+ *   grad_fused_lag (2)  clients between a client's shrinks and its contractions (fused path)
  *   decode_trace (0)    testing: device address of an int64 buffer [4 x SMs] the decode-class
  *                       kernel fills with {start ns, end ns, first unit, end unit} per CTA
  * Tuning / testing knobs (none changes results: every kernel choice gives bitwise the same rows).

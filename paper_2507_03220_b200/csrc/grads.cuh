@@ -50,15 +50,14 @@ constexpr int GRAD_SMEM = 110 * 1024;
 constexpr int GRAD_MAX_STAGES = 8;
 constexpr int GRAD_CHUNK_BYTES = 64 * 64 * 2;  // one {64 MN, 64 K} SW128 box = 8 KB
 
-__global__ void __launch_bounds__(GEMM_THREADS, 2)
-    lora_grad_kernel(const __grid_constant__ CUtensorMap tmQ,  // [s*x.A ; s*g.B^T] [2*qrows, qld] bf16
-                     const LoraGradParams p) {
+__device__ __forceinline__ void lora_grad_body(const CUtensorMap& tmQ,  // [s*x.A ; s*g.B^T] [2*qrows, qld] bf16
+                                               const LoraGradParams& p, const int item) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
-  const LoraGradItem it = p.items[blockIdx.x];
+  const LoraGradItem it = p.items[item];
   const LoraGradSeg sg = p.segs[it.seg];
   const int npad = sg.npad;
   const int nq = npad / 64;
@@ -163,6 +162,53 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 256);
+  }
+}
+
+__global__ void __launch_bounds__(GEMM_THREADS, 2)
+    lora_grad_kernel(const __grid_constant__ CUtensorMap tmQ, const LoraGradParams p) {
+  lora_grad_body(tmQ, p, (int)blockIdx.x);
+}
+
+// K3 + K6 in one launch, client by client. Two launches (every shrink, then every token
+// contraction) read each client's x and g twice from HBM: by the time the contractions run, the
+// shrinks have streamed every other client's activations through L2. Here a CTA takes the next
+// entry of a work list (atomic ticket, so entries start in list order) that interleaves the
+// shrink items of client j with the contraction items of client j - lag; a contraction waits
+// until its client's shrink items have all finished (Q complete), which are earlier entries,
+// already running on started CTAs, so the wait always ends (no co-residency assumption) and
+// the client's x / g are still in L2 when the contraction re-reads them. Per-item code is the
+// two kernels' own, so every output is bitwise that of the two-launch path.
+constexpr int GRAD_FUSED_SMEM = SHRINK_SMEM > GRAD_SMEM ? SHRINK_SMEM : GRAD_SMEM;
+
+struct GradFusedParams {
+  const int2* work;   // {0: shrink item | 1: contraction item, index}
+  int* queue;         // ticket (zero before the launch)
+  int* done;          // [clients] finished shrink items (zero before the launch)
+  const int* need;    // [clients] shrink items per client
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 2)
+    lora_grad_fused_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP2,
+                           const __grid_constant__ CUtensorMap tmQ, const ShrinkParams sp,
+                           const LoraGradParams gp, const GradFusedParams fp) {
+  __shared__ int s_entry;
+  if (threadIdx.x == 0) s_entry = atomicAdd(fp.queue, 1);
+  __syncthreads();
+  const int2 w = fp.work[s_entry];
+  if (w.x == 0) {
+    lora_shrink_body(tmP, tmP2, sp, w.y, 0, 1);
+    __threadfence();   // this CTA's Q rows before the arrival
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(fp.done + sp.items[w.y].seg, 1);
+  } else {
+    const int seg = gp.items[w.y].seg;
+    if (threadIdx.x == 0) {
+      while (ld_acquire_gpu(fp.done + seg) < fp.need[seg]) __nanosleep(64);
+      fence_proxy_async_global();   // Q (generic-proxy stores) before this CTA's TMA reads
+    }
+    __syncthreads();
+    lora_grad_body(tmQ, gp, w.y);
   }
 }
 

@@ -1442,16 +1442,18 @@ __host__ __device__ inline int shrink_chunks(int K, int kb_chunk) {
   return ((K + BK - 1) / BK + kb_chunk - 1) / kb_chunk;
 }
 
-__global__ void __launch_bounds__(GEMM_THREADS, 2)
-    lora_shrink_kernel(const __grid_constant__ CUtensorMap tmP,   // pack [R, K] (K-major rows)
-                       const __grid_constant__ CUtensorMap tmP2,  // second pack (items with pack = 1)
-                       const ShrinkParams p) {
+// One shrink item (bx) and K chunk (by of gy; gy == 1: every chunk, whole mode) per CTA; the
+// kernel below, and the fused adapter-gradient kernel (grads.cuh), which picks items itself.
+__device__ __forceinline__ void lora_shrink_body(const CUtensorMap& tmP,   // pack [R, K] (K-major rows)
+                                                 const CUtensorMap& tmP2,  // second pack (items with pack = 1)
+                                                 const ShrinkParams& p, const int bx, const int by,
+                                                 const int gy) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
-  const ShrinkItem it = p.items[blockIdx.x];
+  const ShrinkItem it = p.items[bx];
   const DevSeg sg = p.segs[it.seg];
   const int npad = sg.rank_pad;  // multiple of 16, <= 256
   const CUtensorMap* tmA = p.tmaps + it.amap;
@@ -1463,8 +1465,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
   // chunk accumulators in TMEM and summing them in registers (npad <= 64); split mode: one
   // chunk per CTA, partials through the workspace, the slab's last CTA sums them. Both add the
   // chunk partials in the same order, so the two modes give bitwise-identical rows.
-  const bool whole = gridDim.y == 1;
-  const int c0 = whole ? 0 : (int)blockIdx.y;
+  const bool whole = gy == 1;
+  const int c0 = whole ? 0 : by;
   const int c1 = whole ? nchk : c0 + 1;
   if (c0 >= nchk) {         // (gradient launches mix two K's; uniform exit before any barrier)
     if (p.done_ctr && threadIdx.x == 0) atomicAdd(p.done_ctr, 1);
@@ -1633,7 +1635,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
       // split mode: this chunk's fp32 partial -> workspace, the slab's last chunk sums in order
       mbar_wait(&tfull[0], 0);
       tc_fence_after();
-      float* mine = p.part + (((int64_t)blockIdx.x * p.max_chunks + c0) * BM + lr) * p.part_ld;
+      float* mine = p.part + (((int64_t)bx * p.max_chunks + c0) * BM + lr) * p.part_ld;
       for (int c = 0; c < nchunk; ++c) {
         uint32_t r[16];
         tmem_ld_32x32b_x16(tmem_base + c * 16 + ((ew * 32u) << 16), r);
@@ -1649,12 +1651,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
       tc_fence_before();
       __threadfence();
       named_bar_sync(1, 128);
-      if (ew == 0 && lane == 0) last_flag = atomicAdd(p.ticket + blockIdx.x, 1) == nchk - 1;
+      if (ew == 0 && lane == 0) last_flag = atomicAdd(p.ticket + bx, 1) == nchk - 1;
       named_bar_sync(1, 128);
       if (last_flag) {
         __threadfence();
         if (ok) {
-          const float* base = p.part + ((int64_t)blockIdx.x * p.max_chunks * BM + lr) * p.part_ld;
+          const float* base = p.part + ((int64_t)bx * p.max_chunks * BM + lr) * p.part_ld;
           for (int c = 0; c < nchunk; ++c) {
             float v[16];
 #pragma unroll
@@ -1672,7 +1674,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
             store_bf16(c, v);
           }
         }
-        if (ew == 0 && lane == 0) p.ticket[blockIdx.x] = 0;   // ready for the next launch
+        if (ew == 0 && lane == 0) p.ticket[bx] = 0;   // ready for the next launch
       }
     }
     if (it.zero_fill && c0 == 0) {
@@ -1696,6 +1698,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2)
     tc_fence_after();
     tmem_dealloc(tmem_base, 256);
   }
+}
+
+__global__ void __launch_bounds__(GEMM_THREADS, 2)
+    lora_shrink_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmP2,
+                       const ShrinkParams p) {
+  lora_shrink_body(tmP, tmP2, p, (int)blockIdx.x, (int)blockIdx.y, (int)gridDim.y);
 }
 #undef SHRINK_A
 #undef SHRINK_B

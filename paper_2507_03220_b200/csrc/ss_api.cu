@@ -176,6 +176,10 @@ struct ss_ctx {
   int pair_n = 0;
   int shrink_kb_chunk = SHRINK_KB_CHUNK;  // K-split of the LoRA shrink (k-blocks of 64 per chunk)
   int shrink_mode = 0;   // 0 auto, 1 one CTA per slab (all chunks), 2 one CTA per (slab, chunk)
+  int* grad_sync = nullptr;       // fused adapter-gradient kernel: ticket + per-client counters
+  size_t grad_sync_cap = 0;
+  int grad_fused = 0;             // ss_adapter_grads: K3 + K6 in one launch (grads.cuh; measured slower)
+  int grad_fused_lag = 2;         // clients between a client's shrinks and its contractions
   float* dec_part = nullptr;      // K1d: fp32 chunk partials of the decode tiles
   size_t dec_part_cap = 0;
   // LoRA intermediate s*x.A as a hi / lo bf16 pair (ShrinkItem::hilo): 0 never, 1 segments with
@@ -1433,6 +1437,7 @@ int set_kernel_attrs(ss_ctx* ctx) {
   CK(cudaFuncSetAttribute(seg_gemm_dec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC_SMEM));
   CK(cudaFuncSetAttribute(seg_gemm_dec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC_SMEM));
   CK(cudaFuncSetAttribute(lora_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GRAD_SMEM));
+  CK(cudaFuncSetAttribute(lora_grad_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GRAD_FUSED_SMEM));
   g_attrs.done = true;
   return SS_OK;
 }
@@ -1547,6 +1552,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   cudaFree(ctx->shrink_part);
   cudaFree(ctx->shrink_ticket);
   cudaFree(ctx->dec_part);
+  cudaFree(ctx->grad_sync);
   cudaFree(ctx->fr_in);
   cudaFree(ctx->fr_out);
   cudaFree(ctx->fr_x);
@@ -1665,6 +1671,15 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "decode_rows")) {
     if (value < 0 || value > DEC_ROWS) return fail(ctx, SS_E_ARG, "decode_rows must be 0..%d", DEC_ROWS);
     ctx->decode_rows = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "grad_fused")) {
+    ctx->grad_fused = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "grad_fused_lag")) {
+    if (value < 0) return fail(ctx, SS_E_ARG, "grad_fused_lag must be >= 0");
+    ctx->grad_fused_lag = (int)value;
     return SS_OK;
   }
   if (!strcmp(key, "decode_trace")) {
@@ -2122,11 +2137,35 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     }
   }
   // token contractions in reverse client order: the shrink (items in client order) read the last
-  // clients' x / g most recently, so their second read is the likeliest to hit L2
+  // clients' x / g most recently, so their second read is the likeliest to hit L2 (two-launch
+  // path); the fused path walks `work` instead
+  std::vector<int32_t> g_first(lg.size() + 1, 0);
   for (size_t jj = lg.size(); jj-- > 0;) {
     const int32_t j = (int32_t)jj;
+    g_first[j] = (int32_t)gitems.size();
     for (int m = 0; m < d_in; m += BM) gitems.push_back(LoraGradItem{j, 0, m, 0});
     for (int m = 0; m < d_out; m += BM) gitems.push_back(LoraGradItem{j, 1, m, 0});
+  }
+  // fused K3 + K6 (grads.cuh lora_grad_fused_kernel): shrink items of client j, then the
+  // contractions of client j - lag; whole-mode shrinks only (rank_pad <= 64)
+  int max_rank_pad = 0;
+  for (const DevSeg& d : sh) max_rank_pad = std::max(max_rank_pad, d.rank_pad);
+  const bool fused = ctx->grad_fused && !lg.empty() && max_rank_pad <= 64;
+  std::vector<int2> work;
+  std::vector<int32_t> need(std::max<size_t>(1, lg.size()), 0);
+  if (fused) {
+    for (size_t i = 0; i < sitems.size(); ++i) need[sitems[i].seg]++;
+    const int lag = ctx->grad_fused_lag;
+    size_t si = 0;
+    auto contractions = [&](int32_t j) {
+      const int32_t g0 = g_first[j], g1 = g0 + (d_in + BM - 1) / BM + (d_out + BM - 1) / BM;
+      for (int32_t q = g0; q < g1; ++q) work.push_back(make_int2(1, q));
+    };
+    for (size_t j = 0; j < lg.size(); ++j) {
+      for (; si < sitems.size() && sitems[si].seg == (int32_t)j; ++si) work.push_back(make_int2(0, (int)si));
+      if ((int)j >= lag) contractions((int32_t)(j - lag));
+    }
+    for (int j = std::max<int>(0, (int)lg.size() - lag); j < (int)lg.size(); ++j) contractions(j);
   }
   std::vector<Ia3PartItem> pitems;
   std::vector<Ia3FinItem> fitems;
@@ -2147,7 +2186,9 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
   const size_t o_is = o_gi + sz(gitems.size(), sizeof(LoraGradItem));
   const size_t o_ii = o_is + sz(ig.size(), sizeof(Ia3GradSeg));
   const size_t o_if = o_ii + sz(pitems.size(), sizeof(Ia3PartItem));
-  const size_t total = o_if + sz(fitems.size(), sizeof(Ia3FinItem));
+  const size_t o_wk = o_if + sz(fitems.size(), sizeof(Ia3FinItem));
+  const size_t o_nd = o_wk + sz(work.size(), sizeof(int2));
+  const size_t total = o_nd + sz(need.size(), sizeof(int32_t));
   Staging* stp = nullptr;
   if ((rc = acquire_staging(ctx, total, stp))) return rc;
   char* h = static_cast<char*>(stp->host);
@@ -2157,6 +2198,10 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     memcpy(h + o_lg, lg.data(), lg.size() * sizeof(LoraGradSeg));
     memcpy(h + o_ix, sitems.data(), sitems.size() * sizeof(ShrinkItem));
     memcpy(h + o_gi, gitems.data(), gitems.size() * sizeof(LoraGradItem));
+  }
+  if (fused) {
+    memcpy(h + o_wk, work.data(), work.size() * sizeof(int2));
+    memcpy(h + o_nd, need.data(), need.size() * sizeof(int32_t));
   }
   if (!ig.empty()) {
     memcpy(h + o_is, ig.data(), ig.size() * sizeof(Ia3GradSeg));
@@ -2210,15 +2255,30 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     // (one launch each over all clients: the shrink has only t/128 x 2 CTAs per client, so
     // splitting the clients into L2-sized groups starves the GPU — measured 2.3x slower)
     sp.items = reinterpret_cast<const ShrinkItem*>(dv + o_ix);
-    const bool whole = max_chunks == 1 ||
-                       (part_ld <= 64 && (ctx->shrink_mode == 1 || (ctx->shrink_mode == 0 && (int)sitems.size() >= ctx->num_sms)));
-    lora_shrink_kernel<<<dim3((unsigned)sitems.size(), whole ? 1 : max_chunks), GEMM_THREADS, SHRINK_SMEM, stream>>>(
-        L.tm_at, L.tm_b, sp);
-    CK(cudaGetLastError());
     gp.items = reinterpret_cast<const LoraGradItem*>(dv + o_gi);
-    lora_grad_kernel<<<(int)gitems.size(), GEMM_THREADS, GRAD_SMEM, stream>>>(tmQ, gp);
-    CK(cudaGetLastError());
-    ctx->launches += 2;
+    if (fused) {
+      // one launch; the ticket and per-client counters are zeroed in stream order first
+      const size_t sync_bytes = (1 + lg.size()) * sizeof(int);
+      if ((rc = ensure_dev(ctx, ctx->grad_sync, ctx->grad_sync_cap, sync_bytes, false))) return rc;
+      CK(cudaMemsetAsync(ctx->grad_sync, 0, sync_bytes, stream));
+      GradFusedParams fp;
+      fp.work = reinterpret_cast<const int2*>(dv + o_wk);
+      fp.queue = ctx->grad_sync;
+      fp.done = ctx->grad_sync + 1;
+      fp.need = reinterpret_cast<const int32_t*>(dv + o_nd);
+      lora_grad_fused_kernel<<<(int)work.size(), GEMM_THREADS, GRAD_FUSED_SMEM, stream>>>(L.tm_at, L.tm_b, tmQ, sp, gp, fp);
+      CK(cudaGetLastError());
+      ctx->launches += 1;
+    } else {
+      const bool whole = max_chunks == 1 ||
+                         (part_ld <= 64 && (ctx->shrink_mode == 1 || (ctx->shrink_mode == 0 && (int)sitems.size() >= ctx->num_sms)));
+      lora_shrink_kernel<<<dim3((unsigned)sitems.size(), whole ? 1 : max_chunks), GEMM_THREADS, SHRINK_SMEM, stream>>>(
+          L.tm_at, L.tm_b, sp);
+      CK(cudaGetLastError());
+      lora_grad_kernel<<<(int)gitems.size(), GEMM_THREADS, GRAD_SMEM, stream>>>(tmQ, gp);
+      CK(cudaGetLastError());
+      ctx->launches += 2;
+    }
     prof_end(ctx, stream, pi);
   }
   if (!ig.empty()) {

@@ -122,6 +122,35 @@ def test_lora_grads_random_mixed_ranks_ragged(d_in, d_out, role):
     ex.close()
 
 
+@pytest.mark.parametrize("lag", [0, 1, 2, 5])
+def test_lora_grads_fused_launch_bitwise(lag):
+    """grad_fused (one launch: each client's shrinks, then its token contractions `lag` clients
+    later, picked up through an atomic work ticket) equals the two-launch path bitwise, for more
+    clients than the lag, mixed ranks 8..64, ragged token counts."""
+    d_in, d_out, role = 1024, 1536, O.V
+    rng = np.random.default_rng(41 + lag)
+    ex, _ = _ex(d_in, d_out, role, seed=41)
+    specs = [(c, (8, 16, 32, 64)[c % 4], t) for c, t in enumerate((1, 37, 130, 512, 64, 300, 17, 256))]
+    xs = []
+    for cid, rank, t in specs:
+        ad = O.lora_params(7, cid, 0, role, d_in, d_out, rank, 2.0 * rank)
+        ex.register_adapter(cid, _Adapter(lora={_addr(0, role): (ad.a, ad.b)}, alpha=2.0 * rank, rank=rank))
+        xs.append((_dev(rng.standard_normal((t, d_in))), _dev(rng.standard_normal((t, d_out)))))
+
+    def run(fused):
+        ex.ctx.set_option("grad_fused", fused)
+        ex.ctx.set_option("grad_fused_lag", lag)
+        jobs = [_lora_job(cid, x, dy, rank, d_in, d_out) for (cid, rank, _), (x, dy) in zip(specs, xs)]
+        assert ex.adapter_grads(0, role, jobs) == [0] * len(jobs)
+        torch.cuda.synchronize()
+        return jobs
+
+    two, one = run(0), run(1)
+    for (cid, _, _), a, b in zip(specs, two, one):
+        assert torch.equal(a.grad_a, b.grad_a) and torch.equal(a.grad_b, b.grad_b), cid
+    ex.close()
+
+
 def test_lora_grads_accumulate():
     rng = np.random.default_rng(11)
     d_in, d_out, r = 256, 384, 16
