@@ -1131,7 +1131,7 @@ def main():
                           # which also does the adapters / IA3 / scatter, takes less time)
                           "cublas_same_shapes": cublas}
                          if not decode else
-                         {"bound": "hbm", "kernel": "seg_gemm_kernel (decode: weight-streaming, 64-row dispatches)",
+                         {"bound": "hbm", "kernel": "seg_gemm_dec_kernel + dec_fixup_kernel (decode class: split-K in the class order, 64-row decode tiles)",
                           "achieved": gemm_gbs, "peak": hbm_peak, "unit": "GB/s",
                           "frac": (gemm_gbs / hbm_peak) if gemm_gbs else None, "traffic": None,
                           "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
