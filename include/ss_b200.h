@@ -371,6 +371,9 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *                       kernel K1d + fixup), then their own LoRA chain; every other row reduces K
  *                       as one chain. 0: no decode class (every row single-chain).
  *   decode_chunk_kb (20) 64-deep k-blocks per chunk of the decode class's order (1..64)
+ *   decode_split (0)    decode-only dispatch with a side-stream shrink: the decode-class GEMM's
+ *                       chunk groups launch behind the gather, beside the shrink; its LoRA groups
+ *                       after the join (results unchanged; measured 9.84 vs 9.29 ms per 13B decode step)
  *   grad_fused (0)      ss_adapter_grads: LoRA shrinks + token contractions in one launch, client
  *                       by client (x / g re-read from L2); 0: two launches (bitwise the same)
  *   grad_fused_lag (2)  clients between a client's shrinks and its contractions (fused path)

@@ -22,10 +22,9 @@
 // whose chain over the other segments' columns adds exact zeros. So batched == solo holds for decode-class rows exactly as for the single-chain kernels
 // (tests/test_gpu_decode.py).
 //
-// Work. A unit is (64-row decode tile m, chunk c, 64-column tile n); units are ordered m, then
-// chunk (hi chunks, lo chunks, the LoRA chain), then n, and every CTA of a persistent grid takes
-// one contiguous, cost-balanced range (host-built `cta_begin`). Consecutive units of one chunk
-// run in groups of g <= DEC_G = 4 n tiles: one UMMA of N = 64 g covers the group (a chain of
+// Work. A unit is (64-row decode tile m, chunk c, 64-column tile n). Consecutive units of one
+// chunk form host-built groups of g <= DEC_G = 4 n tiles (LoRA pieces: DEC_G_LORA), which the
+// CTAs of a persistent grid claim through an atomic ticket (a CTA that starts late does fewer): one UMMA of N = 64 g covers the group (a chain of
 // kbc * 4 UMMAs per group instead of K / 16), and each stage carries one k-block of A (8 KB, read
 // once per group) beside the group's W boxes (32 KB). W is streamed with L2 evict_first; each
 // unit's fp32 partial goes to the workspace with evict_last, so it is still in L2 for the fixup; no CTA waits on another: the fixed-order sum, bias / y_base / IA3 and the stores run
@@ -54,7 +53,8 @@ constexpr int DEC_STAGES = 5;
 __host__ __device__ constexpr int dec_b_off(int kind) { return kind ? 2 * DEC_KB_BYTES : DEC_KB_BYTES; }
 constexpr int DEC_LP_CHUNKS = 24;                       // max LoRA chunks per piece (unless one segment has more)
 constexpr int DEC_PART = DEC_ROWS * DEC_TN;             // fp32 values per unit partial (16 KB)
-constexpr int DEC_SMEM = DEC_STAGES * DEC_STAGE + 1024 + 256;
+constexpr int DEC_GQ = 8;                               // claimed-group ring depth
+constexpr int DEC_SMEM = DEC_STAGES * DEC_STAGE + 1024 + 512;
 
 struct DecTile {
   int32_t arow;          // first packed (X) row
@@ -83,11 +83,14 @@ struct DecParams {
   const int32_t* chunks;
   const int2* lpieces;        // LoRA pieces: {first entry in `lstages`, stage count}
   const int4* lstages;        // LoRA stages: {pack row, 16-row chunks (<= 4), A_lora hi col, lo col | -1}
-  const int32_t* cta_begin;   // [gridDim.x + 1] unit ranges
+  const int4* groups;         // work groups {mt, kind << 8 | g, c, nt0}: chunk groups, then LoRA groups
+  int g_begin, g_end;         // this launch's groups
+  int* claim;                 // [2] group ticket + exiting-CTA count (zero between launches: the
+                              // last CTA to exit resets both)
   const CUtensorMap* tmaps;
   int amap, alo_map;     // X / X_lo as {64 k, 64 rows, kbc k-blocks} boxes
   float* part;           // [(m * n_n + n) * S + slot][DEC_ROWS][DEC_TN] fp32 partials
-  long long* trace;      // testing: per CTA {start ns, end ns, first unit, end unit} (nullptr: off)
+  long long* trace;      // testing: per CTA {start ns, end ns, groups run, units run} (nullptr: off)
   int pdl_early;         // launched behind the gather / shrink: the producer streams its first W
                          // stages before griddepcontrol.wait (every other role waits on its loads)
 };
@@ -99,37 +102,22 @@ __device__ __forceinline__ long long globaltimer_ns() {
 }
 
 // A group of units one CTA runs back to back: kind 0 a chunk (slot c; the lo chains have slots
-// C + c), kind 1 LoRA piece c - 2C (slot c); g consecutive n tiles starting at nt0.
+// C + c), kind 1 LoRA piece c - 2C (slot c); g consecutive n tiles starting at nt0. Groups are
+// host-built and claimed dynamically (atomic ticket), so a CTA that starts late (its SM busy with
+// the side-stream shrink) simply runs fewer of them.
 struct DecGroup {
   int mt, kind, c, nt0, g;
 };
 
-__device__ __forceinline__ void dec_unit(const DecParams& p, int u, int& mt, int& kind, int& c, int& nt) {
-  mt = 0;
-  while (mt + 1 < p.n_m && p.tiles[mt + 1].unit_begin <= u) ++mt;
-  int r = u - p.tiles[mt].unit_begin;
-  const int nc = p.C * p.n_n;
-  if (r < nc) { kind = 0; c = r / p.n_n; nt = r - c * p.n_n; return; }
-  r -= nc;
-  if (p.tiles[mt].lo) {
-    if (r < nc) { kind = 0; c = r / p.n_n; nt = r - c * p.n_n; c += p.C; return; }
-    r -= nc;
-  }
-  kind = 1; c = r / p.n_n; nt = r - c * p.n_n; c += 2 * p.C;
-}
-
-// Next group starting at unit u (< end); returns the unit after it.
-__device__ __forceinline__ int dec_next_group(const DecParams& p, int u, int end, DecGroup& gr) {
-  dec_unit(p, u, gr.mt, gr.kind, gr.c, gr.nt0);
-  gr.g = 1;
-  const int gmax = gr.kind ? DEC_G_LORA : DEC_G;
-  while (gr.g < gmax && u + gr.g < end && gr.nt0 + gr.g < p.n_n) {
-    int mt, kind, c, nt;
-    dec_unit(p, u + gr.g, mt, kind, c, nt);
-    if (mt != gr.mt || c != gr.c) break;
-    ++gr.g;
-  }
-  return u + gr.g;
+__device__ __forceinline__ DecGroup dec_group(const DecParams& p, int id) {
+  const int4 v = p.groups[id];
+  DecGroup gr;
+  gr.mt = v.x;
+  gr.kind = v.y >> 8;
+  gr.g = v.y & 0xff;
+  gr.c = v.z;
+  gr.nt0 = v.w;
+  return gr;
 }
 
 __device__ __forceinline__ void dec_store8(const float (&v)[8], int ncols, char* dst, bool bf, bool vec) {
@@ -173,13 +161,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* empty_bar = full_bar + DEC_STAGES;
   uint64_t* tfull_bar = empty_bar + DEC_STAGES;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;           // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* qfull_bar = tempty_bar + 2;           // [DEC_GQ] claimed-group ring
+  uint64_t* qempty_bar = qfull_bar + DEC_GQ;      // [DEC_GQ]
+  int* q_id = reinterpret_cast<int*>(qempty_bar + DEC_GQ);   // [DEC_GQ]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_id + DEC_GQ);
 
   const uint32_t warp = warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
-  const int u_begin = p.cta_begin[blockIdx.x], u_end = p.cta_begin[blockIdx.x + 1];
   const int nkb = p.K / BK;
-  if (p.trace && threadIdx.x == 0) p.trace[4 * blockIdx.x] = globaltimer_ns();
+  long long t_start = 0;
+  if (p.trace && threadIdx.x == 0) t_start = globaltimer_ns();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmB);
@@ -195,6 +186,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 2);   // warps 4 and 5 (TMEM lanes 0-63) read the accumulators
+    }
+    for (int q = 0; q < DEC_GQ; ++q) {
+      mbar_init(&qfull_bar[q], 1);
+      mbar_init(&qempty_bar[q], 3);   // the MMA warp and epilogue warps 4, 5
     }
     fence_barrier_init();
   }
@@ -217,12 +212,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tensormap_acquire(tmA);
       if (p.alo_map != p.amap) tensormap_acquire(tmAlo);
       const uint64_t pol_w = policy_evict_first();   // W streams once; keep L2 for the partials
+      int qi = 0;
+      uint32_t qph = 0;
+      int n_groups = 0, n_units = 0;
+      // claim the next group and hand its id to the MMA / epilogue warps (-1: no more)
+      auto claim = [&]() {
+        const int t = atomicAdd(p.claim, 1) + p.g_begin;
+        const int id = t < p.g_end ? t : -1;
+        mbar_wait(&qempty_bar[qi], qph ^ 1);
+        q_id[qi] = id;
+        mbar_arrive(&qfull_bar[qi]);
+        if (++qi == DEC_GQ) { qi = 0; qph ^= 1; }
+        return id;
+      };
+      int id = claim();
       DecGroup gr;
       if (p.pdl_early) {
         // the first group's first stages: W (no dependency on the previous kernels) now, A (the
         // gathered rows) after griddepcontrol.wait
-        if (u_begin < u_end) {
-          dec_next_group(p, u_begin, u_end, gr);
+        if (id >= 0) {
+          gr = dec_group(p, id);
           if (gr.kind == 0) {
             const int cc = gr.c >= p.C ? gr.c - p.C : gr.c;
             pre = min(DEC_STAGES, min(nkb, (cc + 1) * p.kbc) - cc * p.kbc);
@@ -240,8 +249,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         pdl_wait();
       }
-      for (int u = u_begin; u < u_end;) {
-        u = dec_next_group(p, u, u_end, gr);
+      for (; id >= 0; id = claim()) {
+        gr = dec_group(p, id);
+        ++n_groups;
+        n_units += gr.g;
         const DecTile td = p.tiles[gr.mt];
         if (gr.kind == 0) {
           const bool lo = gr.c >= p.C;
@@ -291,6 +302,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       }
+      if (p.trace) {
+        p.trace[4 * blockIdx.x + 2] = n_groups;
+        p.trace[4 * blockIdx.x + 3] = n_units;
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -298,9 +313,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t ph = 0;
     int acc = 0;
     uint32_t acc_ph = 0;
-    DecGroup gr;
-    for (int u = u_begin; u < u_end;) {
-      u = dec_next_group(p, u, u_end, gr);
+    int qi = 0;
+    uint32_t qph = 0;
+    for (;;) {
+      mbar_wait(&qfull_bar[qi], qph);
+      const int id = q_id[qi];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty_bar[qi]);
+      if (++qi == DEC_GQ) { qi = 0; qph ^= 1; }
+      if (id < 0) break;
+      const DecGroup gr = dec_group(p, id);
       const DecTile td = p.tiles[gr.mt];
       mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
       tc_fence_after();
@@ -363,9 +385,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int acc = 0;
     uint32_t acc_ph = 0;
     int row_mt = -1, row_rows = 0, row_piece = -1;   // this row's tile / LoRA piece (-1: none)
-    DecGroup gr;
-    for (int u = u_begin; u < u_end;) {
-      u = dec_next_group(p, u, u_end, gr);
+    int qi = 0;
+    uint32_t qph = 0;
+    for (;;) {
+      mbar_wait(&qfull_bar[qi], qph);
+      const int id = q_id[qi];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty_bar[qi]);
+      if (++qi == DEC_GQ) { qi = 0; qph ^= 1; }
+      if (id < 0) break;
+      const DecGroup gr = dec_group(p, id);
       if (gr.mt != row_mt) {
         row_mt = gr.mt;
         const DecTile td = p.tiles[gr.mt];
@@ -405,10 +434,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   }
   __syncthreads();
-  if (p.trace && threadIdx.x == 0) {
-    p.trace[4 * blockIdx.x + 1] = globaltimer_ns();
-    p.trace[4 * blockIdx.x + 2] = u_begin;
-    p.trace[4 * blockIdx.x + 3] = u_end;
+  if (threadIdx.x == 0) {
+    if (p.trace) {
+      p.trace[4 * blockIdx.x] = t_start;
+      p.trace[4 * blockIdx.x + 1] = globaltimer_ns();
+    }
+    // the last CTA out resets the ticket for the next launch (every claim is made by now)
+    if (atomicAdd(p.claim + 1, 1) == (int)gridDim.x - 1) {
+      p.claim[0] = 0;
+      p.claim[1] = 0;
+      __threadfence();
+    }
   }
   if (warp == 2) {
     tc_fence_after();

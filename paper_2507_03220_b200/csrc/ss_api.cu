@@ -180,6 +180,8 @@ struct ss_ctx {
   size_t grad_sync_cap = 0;
   int grad_fused = 0;             // ss_adapter_grads: K3 + K6 in one launch (grads.cuh; measured slower)
   int grad_fused_lag = 2;         // clients between a client's shrinks and its contractions
+  int* dec_claim = nullptr;       // K1d group tickets: [0..1] main launch, [2..3] LoRA launch
+  int decode_split = 0;           // K1d chunk groups beside the side-stream shrink, LoRA groups after (slower)
   float* dec_part = nullptr;      // K1d: fp32 chunk partials of the decode tiles
   size_t dec_part_cap = 0;
   // LoRA intermediate s*x.A as a hi / lo bf16 pair (ShrinkItem::hilo): 0 never, 1 segments with
@@ -514,9 +516,9 @@ struct Built {
   size_t off_tm = 0, off_seg = 0, off_tile = 0, off_piece = 0, off_ch = 0, off_st = 0, off_it = 0;
   // decode-class part (K1d): tiles, LoRA runs, X / X_lo tensor maps, cluster size
   size_t off_dt = 0;
-  size_t off_dcb = 0, off_lp = 0, off_ls = 0;   // K1d per-CTA unit ranges, LoRA pieces / stages
+  size_t off_dcb = 0, off_lp = 0, off_ls = 0;   // K1d work groups, LoRA pieces / stages
   int dec_S = 0;
-  int n_dec = 0, dec_C = 0, dec_kbc = 0, dec_grid = 0;
+  int n_dec = 0, dec_C = 0, dec_kbc = 0, dec_chunk_groups = 0, dec_groups = 0;
   int32_t dec_amap = 0, dec_alo = 0;
   int64_t Mp = 0;                      // single-chain rows (M - decode-class rows)
   double dec_flops = 0, dec_bytes = 0;
@@ -1015,42 +1017,22 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
 
   // ---- serialise the device tables
   const size_t off_tm = 0;
-  // ---- K1d units (tile m, chunk, 64-column tile n) and their cost-balanced per-CTA ranges
-  std::vector<int32_t> dcb;
+  // ---- K1d work groups {mt, kind << 8 | g, slot, first n tile}: every chunk group (groups of
+  // DEC_G column tiles of one chunk), then every LoRA-piece group (DEC_G_LORA column tiles)
+  std::vector<int4> dgroups;
   if (!dtiles.empty()) {
     const int n_n = (N + DEC_TN - 1) / DEC_TN;
-    const int nkb = K / BK;
-    std::vector<double> cost;
-    for (DecTile& t : dtiles) {
-      t.unit_begin = (int32_t)cost.size();
-      for (int rep = 0; rep <= t.lo; ++rep)
-        for (int c = 0; c < dec_C; ++c) {
-          const int kbs = std::min(nkb, (c + 1) * dec_kbc) - c * dec_kbc;
-          for (int n = 0; n < n_n; ++n) cost.push_back(kbs * (DEC_WBOX + DEC_KB_BYTES / (double)DEC_G));
-        }
-      for (int q = 0; q < t.lp_count; ++q) {
-        double c = 0;
-        const int2 lp = lpieces[t.lp_begin + q];
-        for (int e = lp.x; e < lp.x + lp.y; ++e)
-          c += lstages[e].y * 2.0 * LORA_CHUNK_BYTES + DEC_KB_BYTES;   // (measured: ~2x the bytes' share)
-        for (int n = 0; n < n_n; ++n) cost.push_back(c);
-      }
-    }
-    const int units = (int)cost.size();
-    const int grid = std::min(units, ctx->num_sms);
-    double total_cost = 0;
-    for (double c : cost) total_cost += c;
-    dcb.assign(grid + 1, units);
-    dcb[0] = 0;
-    double run = 0;
-    int b = 1;
-    for (int u = 0; u < units && b < grid; ++u) {
-      run += cost[u];
-      // cut after unit u once this CTA holds its share (every CTA keeps at least one unit)
-      while (b < grid && run >= total_cost * b / grid && u + 1 >= b) dcb[b++] = u + 1;
-    }
-    for (; b < grid; ++b) dcb[b] = std::max(dcb[b - 1], units - (grid - b));
-    B.dec_grid = grid;
+    for (size_t m = 0; m < dtiles.size(); ++m)
+      for (int rep = 0; rep <= dtiles[m].lo; ++rep)
+        for (int c = 0; c < dec_C; ++c)
+          for (int n = 0; n < n_n; n += DEC_G)
+            dgroups.push_back(make_int4((int)m, std::min(DEC_G, n_n - n), rep * dec_C + c, n));
+    B.dec_chunk_groups = (int)dgroups.size();
+    for (size_t m = 0; m < dtiles.size(); ++m)
+      for (int q = 0; q < dtiles[m].lp_count; ++q)
+        for (int n = 0; n < n_n; n += DEC_G_LORA)
+          dgroups.push_back(make_int4((int)m, (1 << 8) | std::min(DEC_G_LORA, n_n - n), 2 * dec_C + q, n));
+    B.dec_groups = (int)dgroups.size();
   }
   const size_t off_seg = round_up(tmaps.size() * sizeof(CUtensorMap), 256);
   const size_t off_tile = off_seg + round_up(ds.size() * sizeof(DevSeg), 256);
@@ -1060,7 +1042,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   const size_t off_it = off_st + round_up(std::max<size_t>(1, stores.size()) * sizeof(int2), 256);
   const size_t off_dt = off_it + round_up(std::max<size_t>(1, items.size()) * sizeof(ShrinkItem), 256);
   const size_t off_dcb = off_dt + round_up(std::max<size_t>(1, dtiles.size()) * sizeof(DecTile), 256);
-  const size_t off_lp = off_dcb + round_up(std::max<size_t>(1, dcb.size()) * 4, 256);
+  const size_t off_lp = off_dcb + round_up(std::max<size_t>(1, dgroups.size()) * sizeof(int4), 256);
   const size_t off_ls = off_lp + round_up(std::max<size_t>(1, lpieces.size()) * sizeof(int2), 256);
   const size_t total = off_ls + round_up(std::max<size_t>(1, lstages.size()) * sizeof(int4), 256);
   B.blob.assign(total, 0);
@@ -1076,7 +1058,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   }
   if (!dtiles.empty()) {
     memcpy(h + off_dt, dtiles.data(), dtiles.size() * sizeof(DecTile));
-    memcpy(h + off_dcb, dcb.data(), dcb.size() * 4);
+    memcpy(h + off_dcb, dgroups.data(), dgroups.size() * sizeof(int4));
     if (!lpieces.empty()) memcpy(h + off_lp, lpieces.data(), lpieces.size() * sizeof(int2));
     if (!lstages.empty()) memcpy(h + off_ls, lstages.data(), lstages.size() * sizeof(int4));
   }
@@ -1213,6 +1195,9 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   // shrink's CTAs (2 per SM) and the GEMM's fit on the GPU together, so neither can starve.
   const int gemm_ctas = (int)std::min<int64_t>((int64_t)num_m * ((N + 63) / 64), ctx->num_sms);
   const bool overlap = side && B.stream && ctx->lora_overlap && gemm_ctas + (shrink_ctas + 1) / 2 <= ctx->num_sms;
+  // decode-only dispatch with a side-stream shrink: the decode GEMM's chunk groups run beside the
+  // shrink (their own launch, right behind the gather); the LoRA groups after the join
+  const bool dec_split = side && !overlap && ctx->decode_split && B.num_m == 0 && B.dec_groups > B.dec_chunk_groups;
   auto launch_shrink = [&](cudaStream_t st) -> int {
     // the streaming kernel (<= 64 rows) reads the LoRA operand through a 64-row box too
     rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, B.stream ? 64 : BM);
@@ -1251,7 +1236,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     if ((rc = launch_shrink(ctx->side))) return rc;
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
     if ((rc = launch_gather())) return rc;
-    if (!overlap) CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));
+    if (!overlap && !dec_split) CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));
   } else {
     if (MX > 0 && (rc = launch_gather())) return rc;
     if (any_lora && (rc = launch_shrink(stream))) return rc;
@@ -1362,7 +1347,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     dp.row_seg = ctx->row_seg;
     dp.tiles = reinterpret_cast<const DecTile*>(dv + B.off_dt);
     dp.chunks = gpm.chunks;
-    dp.cta_begin = reinterpret_cast<const int32_t*>(dv + B.off_dcb);
+    dp.groups = reinterpret_cast<const int4*>(dv + B.off_dcb);
     dp.lpieces = reinterpret_cast<const int2*>(dv + B.off_lp);
     dp.lstages = reinterpret_cast<const int4*>(dv + B.off_ls);
     dp.tmaps = d_tmaps;
@@ -1372,18 +1357,32 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     dp.trace = ctx->decode_trace;
     // streams its first W stages behind the kernel before it when that is the gather or the
     // main-stream shrink of this dispatch (PDL edge; not across an event join)
-    const bool dec_early = ctx->stream_pdl && !ctx->profiling && MX > 0 && !side && num_m == 0;
-    dp.pdl_early = dec_early ? 1 : 0;
-    const int dgrid = B.dec_grid;
+    const bool dec_early = ctx->stream_pdl && !ctx->profiling && MX > 0 && (!side || dec_split) && num_m == 0;
     const bool dpdl = (ctx->pdl || dec_early) && !ctx->profiling;
     const int pd = prof_begin(ctx, stream, SS_KERNEL_GEMM, B.dec_flops, B.dec_bytes);
     const CUtensorMap& tmBP64 = any_lora ? (bwd ? L.tm_at64 : L.tm_b64) : L.tm_w_fwd;
-    if (bwd) CK(launch_kp(dpdl, seg_gemm_dec_kernel<true>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_dec, tmALd, tmBP, tmBP64, dp));
-    else CK(launch_kp(dpdl, seg_gemm_dec_kernel<false>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_dec, tmALd, tmBP, tmBP64, dp));
+    auto launch_dec = [&](int g0, int g1, int* claim, bool early, bool pdl) -> int {
+      dp.g_begin = g0;
+      dp.g_end = g1;
+      dp.claim = claim;
+      dp.pdl_early = early ? 1 : 0;
+      const int dgrid = std::min(g1 - g0, ctx->num_sms);
+      if (bwd) CK(launch_kp(pdl, seg_gemm_dec_kernel<true>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_dec, tmALd, tmBP, tmBP64, dp));
+      else CK(launch_kp(pdl, seg_gemm_dec_kernel<false>, dgrid, GEMM_THREADS, DEC_SMEM, stream, L.tm_w_dec, tmALd, tmBP, tmBP64, dp));
+      ctx->launches++;
+      return SS_OK;
+    };
+    if (dec_split) {
+      if ((rc = launch_dec(0, B.dec_chunk_groups, ctx->dec_claim, dec_early, dpdl))) return rc;
+      CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));   // the shrink's A_lora
+      if ((rc = launch_dec(B.dec_chunk_groups, B.dec_groups, ctx->dec_claim + 2, false, false))) return rc;
+    } else {
+      if ((rc = launch_dec(0, B.dec_groups, ctx->dec_claim, dec_early, dpdl))) return rc;
+    }
     CK(launch_kp(dpdl, dec_fixup_kernel, dp.n_n * dp.n_m * (DEC_ROWS / DEC_FIX_ROWS), DEC_FIX_THREADS, 0, stream, dp));
     prof_end(ctx, stream, pd);
     CK(cudaGetLastError());
-    ctx->launches += 2;
+    ctx->launches += 1;
   }
   CK(cudaEventRecord(ctx->compute_done, stream));
   ctx->any_compute = true;
@@ -1499,7 +1498,9 @@ int ss_ctx_create(int device, int tp_rank, int tp_size, ss_ctx** out) {
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaMalloc(&ctx->sync_ctr, 2 * sizeof(int)) != cudaSuccess ||
-      cudaMemset(ctx->sync_ctr, 0, 2 * sizeof(int)) != cudaSuccess) {
+      cudaMemset(ctx->sync_ctr, 0, 2 * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&ctx->dec_claim, 4 * sizeof(int)) != cudaSuccess ||
+      cudaMemset(ctx->dec_claim, 0, 4 * sizeof(int)) != cudaSuccess) {
     delete ctx;
     return SS_E_CUDA;
   }
@@ -1552,6 +1553,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   cudaFree(ctx->shrink_part);
   cudaFree(ctx->shrink_ticket);
   cudaFree(ctx->dec_part);
+  cudaFree(ctx->dec_claim);
   cudaFree(ctx->grad_sync);
   cudaFree(ctx->fr_in);
   cudaFree(ctx->fr_out);
@@ -1671,6 +1673,10 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "decode_rows")) {
     if (value < 0 || value > DEC_ROWS) return fail(ctx, SS_E_ARG, "decode_rows must be 0..%d", DEC_ROWS);
     ctx->decode_rows = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "decode_split")) {
+    ctx->decode_split = value ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "grad_fused")) {

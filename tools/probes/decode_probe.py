@@ -92,8 +92,7 @@ for name in names:
             for b in order[:6] + order[-3:]:
                 s0, s1, u0, u1 = t[b]
                 ch = max(0, min(u1, C * nn) - u0)
-                print(f"     cta {b:3d} start {(s0-t0)/1e3:6.1f} dur {(s1-s0)/1e3:6.1f} us units {u0}-{u1} "
-                      f"(chunk {ch}, lora {u1-u0-ch})")
+                print(f"     cta {b:3d} start {(s0-t0)/1e3:6.1f} dur {(s1-s0)/1e3:6.1f} us groups {u0} units {u1}")
         print(f"{name:8s} K={K:6d} N={N:6d} decode_rows={mode:2d} lora={int(lora)}: gemm {g_us:7.2f} us "
               f"({K * N * 2 / (g_us * 1e-6) / 1e9:6.0f} GB/s of W), dispatch {e0.elapsed_time(e1) / iters * 1e3:7.2f} us",
               flush=True)
