@@ -619,10 +619,15 @@ def e2e_numpy_leg(ex, wl_key, specs, steps):
     tb, th = tb / steps, th / steps
     moved[0] = moved[1] = 0
     run([])
-    for l in layers:           # byte count of one full step (no compute)
+    # byte count of one full step (no compute). Request rows cross PCIe as bf16: the library
+    # converts pageable f32 rows on host threads (`host_convert`), except backward dispatches
+    # holding IA3 fine-tune rows (dy is scaled by l in f32 on the device first); replies are f32.
+    ia3_ft = any(s_[0] == "ia3" and s_[2] for s_ in specs)
+    for l in layers:
         di, do = dims[l[1]]
         n_ft = sum(1 for s_ in specs if s_[2])
-        moved[0] += t * (len(specs) * di + n_ft * do) * 4
+        bwd_esz = 4 if (ia3_ft and l[1] in (K, V, FF_UP)) else 2
+        moved[0] += t * len(specs) * di * 2 + t * n_ft * do * bwd_esz
         moved[1] += t * (len(specs) * do + n_ft * di) * 4
     return wl["L"] * tb + th, moved[0], moved[1], (tb, th)
 
@@ -1069,7 +1074,8 @@ def main():
                                 "d2h_bytes_per_step": d2h_n, "ms_per_step": dt_n * 1e3,
                                 "path": "GpuBaseExecutor.serve_forward / serve_backward, f32 numpy payloads "
                                         "(the reference channels' payload type), replies returned as f32 numpy "
-                                        "views; native host pipeline",
+                                        "views; native host pipeline, request rows converted to bf16 by host "
+                                        "threads before the DMA (bytes: what crosses PCIe)",
                                 "sample": f"block 0 ({tb_n * 1e3:.0f} ms) + LM_HEAD ({th_n * 1e3:.0f} ms), fwd all "
                                           f"clients + bwd FT clients, mean of {args.e2e_numpy_steps} after 1 "
                                           f"warm-up; step = L x block + head"}

@@ -371,6 +371,11 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *                       kernel K1d + fixup), then their own LoRA chain; every other row reduces K
  *                       as one chain. 0: no decode class (every row single-chain).
  *   decode_chunk_kb (20) 64-deep k-blocks per chunk of the decode class's order (1..64)
+ *   host_convert (1)    ss_compute_batch_host: pageable f32 request rows are converted to bf16 by
+ *                       host threads into a page-locked ring, one DMA per sub-batch (results
+ *                       unchanged: the same rounding as the device gather; not for backward
+ *                       IA3 rows)
+ *   host_threads (0)    threads of that conversion (0: min(16, hardware threads))
  *   decode_split (0)    decode-only dispatch with a side-stream shrink: the decode-class GEMM's
  *                       chunk groups launch behind the gather, beside the shrink; its LoRA groups
  *                       after the join (results unchanged; measured 9.84 vs 9.29 ms per 13B decode step)

@@ -9,12 +9,17 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <functional>
+#include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ss_b200.h"
@@ -78,6 +83,66 @@ struct Staging {
 }  // namespace
 
 namespace { struct ZcPlan; }
+// Host worker threads for the host side of a dispatch (f32 -> bf16 payload conversion into
+// page-locked staging, ss_compute_batch_host): run(T, fn) runs fn(0 .. T-1) over the workers and
+// the calling thread and returns when every task is done.
+class HostPool {
+ public:
+  explicit HostPool(int n) {
+    for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void run(int tasks, const std::function<void(int)>& fn) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      fn_ = &fn;
+      tasks_ = tasks;
+      next_.store(0);
+      pending_ = (int)th_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> l(m_);
+    done_cv_.wait(l, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void work() {
+    for (int t; (t = next_.fetch_add(1)) < tasks_;) (*fn_)(t);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> l(m_);
+      cv_.wait(l, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (stop_) return;
+      l.unlock();
+      work();
+      l.lock();
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int tasks_ = 0, pending_ = 0;
+  std::atomic<int> next_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 struct ss_ctx {
   int device = 0, tp_rank = 0, tp_size = 1, num_sms = 148;
   // Every entry point that reads or changes the context holds this (re-entrant: entry points
@@ -133,6 +198,17 @@ struct ss_ctx {
     cudaEvent_t ev_in = nullptr, ev_comp = nullptr, ev_out = nullptr;
     bool used = false;
   } hslot[4];
+  // pageable f32 request rows (numpy clients): converted to bf16 on the host by `pool` into a
+  // page-locked ring, then one DMA per sub-batch (half the PCIe bytes, no driver staging)
+  struct HostConv {
+    uint16_t* buf = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool used = false;
+  } hconv[4];
+  int host_convert = 1;
+  int host_threads = 0;            // 0: min(16, hardware threads)
+  std::unique_ptr<HostPool> pool;
   int64_t pipeline_bytes = 24 << 20;  // target bytes of the wider side per sub-batch
   int pipeline_rows = 4096;
   cudaEvent_t upload_done = nullptr, compute_done = nullptr;
@@ -1575,6 +1651,12 @@ int ss_ctx_destroy(ss_ctx* ctx) {
     cudaEventDestroy(hs.ev_comp);
     cudaEventDestroy(hs.ev_out);
   }
+  for (auto& hc : ctx->hconv) {
+    if (hc.ev) cudaEventSynchronize(hc.ev);
+    cudaFreeHost(hc.buf);
+    if (hc.ev) cudaEventDestroy(hc.ev);
+  }
+  ctx->pool.reset();
   cudaStreamDestroy(ctx->h2d);
   cudaStreamDestroy(ctx->d2h);
   cudaStreamDestroy(ctx->side);
@@ -1673,6 +1755,16 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "decode_rows")) {
     if (value < 0 || value > DEC_ROWS) return fail(ctx, SS_E_ARG, "decode_rows must be 0..%d", DEC_ROWS);
     ctx->decode_rows = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "host_convert")) {
+    ctx->host_convert = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "host_threads")) {
+    if (value < 0 || value > 256) return fail(ctx, SS_E_ARG, "host_threads must be 0..256");
+    ctx->host_threads = (int)value;
+    ctx->pool.reset();
     return SS_OK;
   }
   if (!strcmp(key, "decode_split")) {
@@ -2321,6 +2413,38 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
 namespace {
 struct HostPiece { int seg; int64_t r0, r1; };
 
+// f32 -> bf16 on the host: round to nearest even, NaN -> 0x7FFF, the conversion the gather kernel
+// applies to f32 request rows (cvt.rn.bf16), so converting on the host gives the same bits.
+
+// One row of f32_to_bf16_rn, branch-free so the compiler vectorises it (AVX2 where present).
+#define SS_CVT_BODY                                                                     \
+  for (int64_t k = 0; k < K; ++k) {                                                     \
+    uint32_t u;                                                                         \
+    memcpy(&u, src + k, 4);                                                             \
+    const uint32_t r = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;                          \
+    dst[k] = (uint16_t)(((u & 0x7fffffffu) > 0x7f800000u) ? 0x7fffu : r);               \
+  }
+__attribute__((target("avx2"))) void cvt_row_avx2(const float* __restrict src, uint16_t* __restrict dst, int64_t K) {
+  SS_CVT_BODY
+}
+void cvt_row_base(const float* __restrict src, uint16_t* __restrict dst, int64_t K) { SS_CVT_BODY }
+#undef SS_CVT_BODY
+inline void cvt_row(const float* src, uint16_t* dst, int64_t K) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (avx2) cvt_row_avx2(src, dst, K);
+  else cvt_row_base(src, dst, K);
+}
+
+// True when `p` is ordinary pageable host memory (not device, not page-locked / registered).
+bool pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
 // The numerics class of a whole request (decode_rows), for the pieces a host pipeline splits it
 // into: a piece must reduce K the way the request would in one piece.
 uint32_t class_flag(const ss_ctx* ctx, int K, const ss_seg& s) {
@@ -2731,7 +2855,42 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
   if (aliased)
     return host_dispatch_aliased(ctx, pass_kind, block, role, segs, seg_status, stream, K, N, esz_in, esz_out,
                                  esz_base, rows_total, chunks, wait_for);
-  const size_t in_need = (size_t)target * K * esz_in, out_need = (size_t)target * N * esz_out;
+  // Pageable f32 request rows (the reference's numpy payloads): the host pool converts each
+  // sub-batch to bf16 into a page-locked ring slot, one DMA moves it (half the PCIe bytes of f32,
+  // no driver bounce copies), and the kernels see bf16 rows — the same bits the gather's own
+  // f32 -> bf16 conversion would give. Not for backward IA3 rows (the gather scales dy by l in
+  // f32 before rounding) or page-locked / device sources (DMA-able as they are).
+  bool conv = ctx->host_convert && esz_in == 4;
+  for (size_t q = 0; conv && q < good.size(); ++q) {
+    const ss_seg& s = segs[good[q]];
+    if ((s.flags & SS_SEGF_PINNED) || !pageable(s.src)) conv = false;
+    if (bwd && (s.flags & SS_SEGF_ADAPTER)) {
+      auto ad = L.adapters.find(s.client_id);
+      if (ad != L.adapters.end() && (ad->second.kind & SS_ADAPTER_IA3)) conv = false;
+    }
+  }
+  const size_t esz_dev = conv ? 2 : esz_in;   // request row bytes per value on the device
+  if (conv) {
+    if (!ctx->pool) {
+      const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+      const int n = ctx->host_threads > 0 ? ctx->host_threads : std::min(16, hw);
+      ctx->pool.reset(new HostPool(std::max(0, n - 1)));   // + the calling thread
+    }
+    for (auto& hc : ctx->hconv) {
+      if (!hc.ev) CK(cudaEventCreateWithFlags(&hc.ev, cudaEventDisableTiming));
+      const size_t need = (size_t)target * K * 2;
+      if (hc.cap < need) {
+        if (hc.used) CK(cudaEventSynchronize(hc.ev));
+        CK(cudaFreeHost(hc.buf));
+        hc.buf = nullptr;
+        hc.cap = 0;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&hc.buf), need, cudaHostAllocDefault));
+        hc.cap = need;
+        hc.used = false;
+      }
+    }
+  }
+  const size_t in_need = (size_t)target * K * esz_dev, out_need = (size_t)target * N * esz_out;
   const size_t base_need = any_base ? (size_t)target * N * esz_base : 0;
   for (auto& hs : ctx->hslot) {
     if (hs.in_cap < in_need || hs.out_cap < out_need || hs.base_cap < base_need) {
@@ -2753,15 +2912,42 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     if (hs.used) CK(cudaStreamWaitEvent(ctx->h2d, hs.ev_comp, 0));
     int64_t pos = 0;
     cs.clear();
+    if (conv) {
+      // this sub-batch's rows, converted by the pool into ring slot j % 4 (once its previous
+      // DMA has read it), then one copy
+      auto& hc = ctx->hconv[j % 4];
+      if (hc.used) CK(cudaEventSynchronize(hc.ev));
+      std::vector<int64_t> row0(ch.size() + 1, 0);
+      for (size_t q = 0; q < ch.size(); ++q) row0[q + 1] = row0[q] + (ch[q].r1 - ch[q].r0);
+      const int64_t nrows = row0.back();
+      constexpr int64_t kRowsPerTask = 16;
+      const int tasks = (int)((nrows + kRowsPerTask - 1) / kRowsPerTask);
+      uint16_t* dstb = hc.buf;
+      ctx->pool->run(tasks, [&](int t) {
+        const int64_t a0 = t * kRowsPerTask, a1 = std::min(nrows, a0 + kRowsPerTask);
+        size_t q = std::upper_bound(row0.begin(), row0.end(), a0) - row0.begin() - 1;
+        for (int64_t r = a0; r < a1; ++r) {
+          while (r >= row0[q + 1]) ++q;
+          const ss_seg& s = segs[ch[q].seg];
+          const float* src = static_cast<const float*>(s.src) + (ch[q].r0 + (r - row0[q])) * s.src_ld;
+          cvt_row(src, dstb + r * K, K);
+        }
+      });
+      CK(cudaMemcpyAsync(hs.in, hc.buf, (size_t)nrows * K * 2, cudaMemcpyHostToDevice, ctx->h2d));
+      CK(cudaEventRecord(hc.ev, ctx->h2d));
+      hc.used = true;
+    }
     for (const Piece& p : ch) {
       const ss_seg& s = segs[p.seg];
       const int64_t n = p.r1 - p.r0;
-      char* din = static_cast<char*>(hs.in) + pos * K * esz_in;
-      CK(copy_rows(din, (size_t)K * esz_in, static_cast<const char*>(s.src) + p.r0 * s.src_ld * esz_in,
-                   (size_t)s.src_ld * esz_in, (size_t)K * esz_in, (size_t)n, cudaMemcpyHostToDevice, ctx->h2d));
+      char* din = static_cast<char*>(hs.in) + pos * K * esz_dev;
+      if (!conv)
+        CK(copy_rows(din, (size_t)K * esz_in, static_cast<const char*>(s.src) + p.r0 * s.src_ld * esz_in,
+                     (size_t)s.src_ld * esz_in, (size_t)K * esz_in, (size_t)n, cudaMemcpyHostToDevice, ctx->h2d));
       ss_seg d = s;
       d.rows = (uint32_t)n;
       d.flags |= class_flag(ctx, K, s);   // a piece keeps its request's numerics class
+      if (conv) d.flags |= SS_SEGF_SRC_BF16;
       d.src = din;
       d.src_ld = K;
       d.dst = static_cast<char*>(hs.out) + pos * N * esz_out;
