@@ -370,7 +370,7 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *                       fixed contiguous chunks summed left to right in chunk order (split-K
  *                       kernel K1d + fixup), then their own LoRA chain; every other row reduces K
  *                       as one chain. 0: no decode class (every row single-chain).
- *   decode_chunk_kb (20) 64-deep k-blocks per chunk of the decode class's order (1..64)
+ *   decode_chunk_kb (20) 64-deep k-blocks per chunk of the decode class's order (1..48)
  *   host_convert (1)    ss_compute_batch_host: pageable f32 request rows are converted to bf16 by
  *                       host threads into a page-locked ring, one DMA per sub-batch (results
  *                       unchanged: the same rounding as the device gather; not for backward

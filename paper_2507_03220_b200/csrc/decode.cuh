@@ -40,7 +40,7 @@ namespace ss {
 constexpr int DEC_ROWS = 64;                            // packed rows per decode tile
 constexpr int DEC_TN = 64;                              // output columns per unit
 constexpr int DEC_G = 4;                                // n tiles interleaved per group
-constexpr int DEC_MAX_KBC = 64;                         // k-blocks per chunk (option bound)
+constexpr int DEC_MAX_KBC = 48;                         // k-blocks per chunk (option bound: decode shrink smem)
 constexpr int DEC_KB_BYTES = DEC_ROWS * 128;            // one k-block of A (64 rows x 64 k): 8 KB
 constexpr int DEC_WBOX = 64 * 128;                      // one {64 n, 64 k} W box: 8 KB
 // stage (40 KB). Chunk units: one k-block, the A box (8 KB) + the group's W boxes (<= 32 KB).
@@ -139,6 +139,186 @@ __device__ __forceinline__ void dec_store8(const float (&v)[8], int ncols, char*
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------- decode shrink
+// The LoRA intermediate s*x.A (forward) / s*g.B^T (backward) of decode-class segments (<= 16
+// rows), on CUDA cores: at a few rows the tensor-core shrink is a chain of K/16 UMMAs per CTA for
+// M = 2, and its time is that chain plus a split-K tail. Order (part of the decode class's
+// numerics): K in the class's chunks (kbc k-blocks, as the GEMM); within a chunk, lane l of a
+// warp owns k = 8 l + 256 i (ascending i, the 8 products in order), then an xor-shuffle tree over
+// the 32 lanes (grid: item x chunk x 32-row rank group; a warp takes 4 rank rows); chunks added in order by the item's last CTA, times alpha / r, rounded to bf16
+// (hi) and, for hi / lo segments, bf16(v - hi) (lo) into the tile's block-diagonal LoRA operand;
+// the tile's other rows get zeros in this segment's columns.
+struct DecShrinkItem {
+  int32_t seg;          // DevSeg (pack_row, rank_pad, lora_scale)
+  int32_t rows;         // <= 16
+  int32_t kind;         // 0: bf16 rows at src, 1: f32 rows at src (rounded to bf16 on load)
+  int32_t hilo;         // 1: write the lo half too
+  const void* src;      // first row (the client's rows in place, or the packed X rows)
+  int64_t ld;           // elements
+  const __nv_bfloat16* src_lo;   // non-null: + X_lo rows (backward IA3 lo operand), ld `ld`
+  int32_t col;          // first column of the segment's rank block
+  int32_t tile_row0;    // A_lora row of its decode tile's first row
+  int32_t p0;           // the segment's first row within the tile
+};
+
+struct DecShrinkParams {
+  int K, kbc, C;
+  int lora_ld;
+  const DevSeg* segs;
+  const DecShrinkItem* items;
+  const __nv_bfloat16* pack;     // [R, K] K-major pack rows (A^T forward, B backward)
+  int64_t pack_ld;
+  __nv_bfloat16* a_lora;
+  float* part;                   // [items][C][16][256] fp32 chunk partials
+  int* ticket;                   // [items] (zero between launches; the last CTA resets)
+};
+
+constexpr int DEC_SHR_THREADS = 256;
+constexpr int DEC_SHR_MAXROWS = 16;
+
+template <int MAXR>   // rows per item bound (4 or DEC_SHR_MAXROWS): the accumulators' registers
+__global__ void __launch_bounds__(DEC_SHR_THREADS)
+    dec_shrink_kernel(const DecShrinkParams p) {
+  extern __shared__ float xs[];   // [rows][kbc * 64] bf16-rounded x of this chunk
+  __shared__ int last;
+  const DecShrinkItem it = p.items[blockIdx.x];
+  const DevSeg sg = p.segs[it.seg];
+  const int R = sg.rank_pad, rows = it.rows;
+  const int c = blockIdx.y;
+  const int kc = p.kbc * 64;
+  const int k0 = c * kc, kn = min(p.K - k0, kc);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_wait();
+  pdl_trigger();
+  // x rows of the chunk -> shared memory (as the GEMM's bf16 operand would hold them)
+  // (8 consecutive values per thread and load: 16-byte bf16 / 2 x 16-byte f32 vectors when the
+  // rows are 16-byte aligned, all of a thread's loads issued before its shared-memory stores)
+  const bool vec = it.kind == 0 ? ((reinterpret_cast<uintptr_t>(it.src) | (uintptr_t)(it.ld * 2)) & 15) == 0
+                                : ((reinterpret_cast<uintptr_t>(it.src) | (uintptr_t)(it.ld * 4)) & 15) == 0;
+  const int n8 = rows * (kn / 8);
+  for (int i = tid; i < n8; i += DEC_SHR_THREADS) {
+    const int r = i / (kn / 8), k = (i - r * (kn / 8)) * 8;
+    const int64_t off = (int64_t)r * it.ld + k0 + k;
+    float v[8];
+    if (vec && it.kind == 0) {
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(it.src) + off));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        v[2 * j] = f.x;
+        v[2 * j + 1] = f.y;
+      }
+    } else if (vec) {
+      const float4* f4 = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(it.src) + off);
+      const float4 a = __ldg(f4), b = __ldg(f4 + 1);
+      const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(f[j]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        v[j] = it.kind == 0 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(it.src)[off + j])
+                            : __bfloat162float(__float2bfloat16_rn(reinterpret_cast<const float*>(it.src)[off + j]));
+    }
+    if (it.src_lo) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += __bfloat162float(it.src_lo[off + j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xs[r * kc + k + j] = v[j];
+  }
+  __syncthreads();
+  float* part = p.part + ((int64_t)blockIdx.x * p.C + c) * DEC_SHR_MAXROWS * 256;
+  // this CTA: rank rows [32 z, 32 z + 32); warp w: 4 of them, every load of a 4 x 1024-k block
+  // issued before its FMAs (the kernel is load-latency bound at these sizes)
+  const int q0 = (int)blockIdx.z * 32 + warp * 4;
+  const __nv_bfloat16* prow = p.pack + (int64_t)(sg.pack_row + q0) * p.pack_ld + k0;
+  float acc[4][MAXR];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int r = 0; r < MAXR; ++r) acc[i][r] = 0.f;
+  for (int kb = 0; kb < kn; kb += 4 * 256) {
+    uint4 raw[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int k = kb + v * 256 + lane * 8;
+        raw[i][v] = (q0 + i < R && k < kn) ? __ldg(reinterpret_cast<const uint4*>(prow + (int64_t)i * p.pack_ld + k))
+                                           : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int k = kb + v * 256 + lane * 8;
+      if (k >= kn) break;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[i][v]);
+        float w[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(h[j]);
+          w[2 * j] = f.x;
+          w[2 * j + 1] = f.y;
+        }
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) {
+          if (r < rows) {
+            const float4 xa = *reinterpret_cast<const float4*>(xs + r * kc + k);
+            const float4 xb = *reinterpret_cast<const float4*>(xs + r * kc + k + 4);
+            float a = acc[i][r];
+            a = fmaf(xa.x, w[0], a); a = fmaf(xa.y, w[1], a); a = fmaf(xa.z, w[2], a); a = fmaf(xa.w, w[3], a);
+            a = fmaf(xb.x, w[4], a); a = fmaf(xb.y, w[5], a); a = fmaf(xb.z, w[6], a); a = fmaf(xb.w, w[7], a);
+            acc[i][r] = a;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int r = 0; r < MAXR; ++r) {
+      if (r < rows) {
+        float v = acc[i][r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && q0 + i < R) part[r * 256 + q0 + i] = v;
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(p.ticket + blockIdx.x, 1) == p.C * (int)gridDim.z - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* base = p.part + (int64_t)blockIdx.x * p.C * DEC_SHR_MAXROWS * 256;
+  const int nh = it.hilo ? 2 : 1;
+  // the tile's other rows: zeros in this segment's columns
+  for (int i = tid; i < (DEC_ROWS - rows) * R; i += DEC_SHR_THREADS) {
+    const int k = i / R, q = i - k * R;
+    const int tr = k < it.p0 ? k : k + rows;
+    __nv_bfloat16* out = p.a_lora + (int64_t)(it.tile_row0 + tr) * p.lora_ld + it.col + q;
+    out[0] = __float2bfloat16_rn(0.f);
+    if (nh == 2) out[R] = __float2bfloat16_rn(0.f);
+  }
+  // the segment's rows: chunk partials in chunk order, x alpha / r, hi (and lo) bf16
+  for (int i = tid; i < rows * R; i += DEC_SHR_THREADS) {
+    const int r = i / R, q = i - r * R;
+    float v = 0.f;
+    for (int cc = 0; cc < p.C; ++cc) v += __ldcg(base + (int64_t)cc * DEC_SHR_MAXROWS * 256 + r * 256 + q);
+    v *= sg.lora_scale;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    __nv_bfloat16* out = p.a_lora + (int64_t)(it.tile_row0 + it.p0 + r) * p.lora_ld + it.col + q;
+    out[0] = hi;
+    if (nh == 2) out[R] = __float2bfloat16_rn(v - __bfloat162float(hi));
+  }
+  if (tid == 0) p.ticket[blockIdx.x] = 0;   // ready for the next launch
 }
 
 __device__ __forceinline__ void st_f4_evict_last(float4* p, float4 v, uint64_t pol) {

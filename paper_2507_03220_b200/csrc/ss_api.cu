@@ -257,6 +257,10 @@ struct ss_ctx {
   int grad_fused = 0;             // ss_adapter_grads: K3 + K6 in one launch (grads.cuh; measured slower)
   int grad_fused_lag = 2;         // clients between a client's shrinks and its contractions
   int* dec_claim = nullptr;       // K1d group tickets: [0..1] main launch, [2..3] LoRA launch
+  float* dshr_part = nullptr;     // decode shrink: fp32 chunk partials
+  size_t dshr_part_cap = 0;
+  int* dshr_ticket = nullptr;     // decode shrink: per-item arrival counters (zero between launches)
+  size_t dshr_ticket_cap = 0;
   int decode_split = 0;           // K1d chunk groups beside the side-stream shrink, LoRA groups after (slower)
   float* dec_part = nullptr;      // K1d: fp32 chunk partials of the decode tiles
   size_t dec_part_cap = 0;
@@ -592,7 +596,8 @@ struct Built {
   size_t off_tm = 0, off_seg = 0, off_tile = 0, off_piece = 0, off_ch = 0, off_st = 0, off_it = 0;
   // decode-class part (K1d): tiles, LoRA runs, X / X_lo tensor maps, cluster size
   size_t off_dt = 0;
-  size_t off_dcb = 0, off_lp = 0, off_ls = 0;   // K1d work groups, LoRA pieces / stages
+  size_t off_dcb = 0, off_lp = 0, off_ls = 0, off_di = 0;   // K1d work groups, LoRA pieces / stages, decode shrink items
+  int n_ditems = 0, dec_rank_max = 0, dec_rows_max = 0;
   int dec_S = 0;
   int n_dec = 0, dec_C = 0, dec_kbc = 0, dec_chunk_groups = 0, dec_groups = 0;
   int32_t dec_amap = 0, dec_alo = 0;
@@ -833,6 +838,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   // ---- LoRA: per tile rank-chunk lists (block-diagonal over the tile's segments) + shrink items
   std::vector<int32_t> chunks;
   std::vector<int2> lpieces;      // decode tiles' LoRA pieces {first stage, stage count}
+  std::vector<DecShrinkItem> ditems;   // decode-class segments' LoRA shrink (dec_shrink_kernel)
   std::vector<int4> lstages;      // decode LoRA stages {pack row, 16-row chunks, A_lora hi col, lo col | -1}
   int lp_chunks = 0;
   std::vector<ShrinkItem> items;
@@ -900,9 +906,16 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
         d.dec_piece = dt.lp_count - 1;
         for (int rep = 0; rep <= hilo; ++rep)
           for (int q = 0; q < d.rank_pad / LORA_CHUNK; ++q) chunks.push_back(d.pack_row + q * LORA_CHUNK);
-        const int p0 = d.xrow0 - dt.arow;
-        items.push_back(ShrinkItem{(int32_t)j, 0, d.xrow0, d.rows, dt.al_row + p0, col, 0, 0, 1,
-                                   dt.al_row, DEC_ROWS, p0, p0 + d.rows, hilo, 0, 0});
+        // its LoRA intermediate: the decode-class shrink (CUDA cores, decode.cuh); the source
+        // rows are resolved once X is allocated (below)
+        DecShrinkItem di{};
+        di.seg = (int32_t)j;
+        di.rows = d.rows;
+        di.hilo = hilo;
+        di.col = col;
+        di.tile_row0 = dt.al_row;
+        di.p0 = d.xrow0 - dt.arow;
+        ditems.push_back(di);
       }
       dt.chunk_count = (int32_t)chunks.size() - dt.chunk_begin;
       max_cols = std::max(max_cols, dt.chunk_count * LORA_CHUNK);
@@ -1089,6 +1102,24 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     B.shrink_indep = true;
     for (const ShrinkItem& it : items)
       if (it.amap == 0 || it.amap == small_map) B.shrink_indep = false;
+    // decode-class shrink items: the client's rows in place (bf16 or f32, device or page-locked
+    // host), or the packed rows where only they hold the operand (backward IA3: g = dy*l)
+    for (DecShrinkItem& di : ditems) {
+      const DevSeg& d = ds[di.seg];
+      const bool in_place = !(d.flags & (SEGF_REMOTE_SRC | SEGF_SRC_ALIASED)) && !(bwd && (d.flags & SEGF_IA3));
+      if (in_place) {
+        di.src = d.src;
+        di.ld = d.src_ld;
+        di.kind = (d.flags & SEGF_SRC_BF16) ? 0 : 1;
+        di.src_lo = nullptr;
+      } else {
+        di.src = ctx->X + (int64_t)d.xrow0 * ldx;
+        di.ld = ldx;
+        di.kind = 0;
+        di.src_lo = (d.flags & SEGF_IA3_LO) ? ctx->X_lo + (int64_t)d.xrow0 * ldx : nullptr;
+        B.shrink_indep = false;
+      }
+    }
   }
 
   // ---- serialise the device tables
@@ -1120,7 +1151,8 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
   const size_t off_dcb = off_dt + round_up(std::max<size_t>(1, dtiles.size()) * sizeof(DecTile), 256);
   const size_t off_lp = off_dcb + round_up(std::max<size_t>(1, dgroups.size()) * sizeof(int4), 256);
   const size_t off_ls = off_lp + round_up(std::max<size_t>(1, lpieces.size()) * sizeof(int2), 256);
-  const size_t total = off_ls + round_up(std::max<size_t>(1, lstages.size()) * sizeof(int4), 256);
+  const size_t off_di = off_ls + round_up(std::max<size_t>(1, lstages.size()) * sizeof(int4), 256);
+  const size_t total = off_di + round_up(std::max<size_t>(1, ditems.size()) * sizeof(DecShrinkItem), 256);
   B.blob.assign(total, 0);
   char* h = B.blob.data();
   memcpy(h + off_tm, tmaps.data(), tmaps.size() * sizeof(CUtensorMap));
@@ -1137,6 +1169,26 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     memcpy(h + off_dcb, dgroups.data(), dgroups.size() * sizeof(int4));
     if (!lpieces.empty()) memcpy(h + off_lp, lpieces.data(), lpieces.size() * sizeof(int2));
     if (!lstages.empty()) memcpy(h + off_ls, lstages.data(), lstages.size() * sizeof(int4));
+    if (!ditems.empty()) memcpy(h + off_di, ditems.data(), ditems.size() * sizeof(DecShrinkItem));
+  }
+  B.off_di = off_di;
+  B.n_ditems = (int)ditems.size();
+  for (const DecShrinkItem& di : ditems) {
+    B.dec_rank_max = std::max(B.dec_rank_max, (int)ds[di.seg].rank_pad);
+    B.dec_rows_max = std::max(B.dec_rows_max, (int)di.rows);
+  }
+  if (!ditems.empty()) {
+    const size_t pbytes = ditems.size() * (size_t)dec_C * DEC_SHR_MAXROWS * 256 * sizeof(float);
+    if ((rc = ensure_dev(ctx, ctx->dshr_part, ctx->dshr_part_cap, pbytes))) return rc;
+    if (ctx->dshr_ticket_cap < ditems.size() * sizeof(int)) {
+      if ((rc = ensure_dev(ctx, ctx->dshr_ticket, ctx->dshr_ticket_cap, ditems.size() * sizeof(int)))) return rc;
+      CK(cudaMemset(ctx->dshr_ticket, 0, ctx->dshr_ticket_cap));
+    }
+    for (const DecShrinkItem& di : ditems) {
+      const double r = ds[di.seg].rank_pad;
+      B.shrink_flops += 2.0 * di.rows * r * K;
+      B.shrink_bytes += r * K * 2.0 + (double)di.rows * K * (di.kind ? 4 : 2) + DEC_ROWS * r * 2 * (1 + di.hilo);
+    }
   }
   B.off_lp = off_lp;
   B.off_ls = off_ls;
@@ -1295,11 +1347,33 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     const int pi = prof_begin(ctx, st, SS_KERNEL_SHRINK, B.shrink_flops, B.shrink_bytes);
     sp.K2 = K;
     sp.done_ctr = overlap ? ctx->sync_ctr : nullptr;
-    CK(launch_k(ctx, lora_shrink_kernel, dim3(B.n_items, whole ? 1 : B.shrink_chunks_), GEMM_THREADS, SHRINK_SMEM,
-                st, bwd ? L.tm_b : L.tm_at, bwd ? L.tm_b : L.tm_at, sp));
+    if (B.n_items > 0) {
+      CK(launch_k(ctx, lora_shrink_kernel, dim3(B.n_items, whole ? 1 : B.shrink_chunks_), GEMM_THREADS, SHRINK_SMEM,
+                  st, bwd ? L.tm_b : L.tm_at, bwd ? L.tm_b : L.tm_at, sp));
+      ctx->launches++;
+    }
+    if (B.n_ditems > 0) {
+      DecShrinkParams dsp;
+      dsp.K = K;
+      dsp.kbc = B.dec_kbc;
+      dsp.C = B.dec_C;
+      dsp.lora_ld = (int)lora_ld;
+      dsp.segs = d_segs;
+      dsp.items = reinterpret_cast<const DecShrinkItem*>(dv + B.off_di);
+      dsp.pack = bwd ? L.b_pack : L.at_pack;
+      dsp.pack_ld = bwd ? L.ld_b : L.ld_at;
+      dsp.a_lora = ctx->a_lora;
+      dsp.part = ctx->dshr_part;
+      dsp.ticket = ctx->dshr_ticket;
+      const int rmax = std::max(16, B.dec_rank_max);
+      const dim3 g(B.n_ditems, B.dec_C, (rmax + 31) / 32);
+      const size_t smem = (size_t)DEC_SHR_MAXROWS * B.dec_kbc * 64 * sizeof(float);
+      if (B.dec_rows_max <= 4) CK(launch_k(ctx, dec_shrink_kernel<4>, g, DEC_SHR_THREADS, smem, st, dsp));
+      else CK(launch_k(ctx, dec_shrink_kernel<DEC_SHR_MAXROWS>, g, DEC_SHR_THREADS, smem, st, dsp));
+      ctx->launches++;
+    }
     prof_end(ctx, st, pi);
     CK(cudaGetLastError());
-    ctx->launches++;
     return SS_OK;
   };
 
@@ -1510,6 +1584,10 @@ int set_kernel_attrs(ss_ctx* ctx) {
   CK(cudaFuncSetAttribute(lora_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           SHRINK_SMEM));
   CK(cudaFuncSetAttribute(seg_gemm_dec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC_SMEM));
+  CK(cudaFuncSetAttribute(dec_shrink_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          DEC_SHR_MAXROWS * DEC_MAX_KBC * 64 * (int)sizeof(float)));
+  CK(cudaFuncSetAttribute(dec_shrink_kernel<DEC_SHR_MAXROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          DEC_SHR_MAXROWS * DEC_MAX_KBC * 64 * (int)sizeof(float)));
   CK(cudaFuncSetAttribute(seg_gemm_dec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC_SMEM));
   CK(cudaFuncSetAttribute(lora_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GRAD_SMEM));
   CK(cudaFuncSetAttribute(lora_grad_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GRAD_FUSED_SMEM));
@@ -1630,6 +1708,8 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   cudaFree(ctx->shrink_ticket);
   cudaFree(ctx->dec_part);
   cudaFree(ctx->dec_claim);
+  cudaFree(ctx->dshr_part);
+  cudaFree(ctx->dshr_ticket);
   cudaFree(ctx->grad_sync);
   cudaFree(ctx->fr_in);
   cudaFree(ctx->fr_out);
