@@ -620,14 +620,14 @@ def e2e_numpy_leg(ex, wl_key, specs, steps):
     moved[0] = moved[1] = 0
     run([])
     # byte count of one full step (no compute). Request rows cross PCIe as bf16: the library
-    # converts pageable f32 rows on host threads (`host_convert`), except backward dispatches
-    # holding IA3 fine-tune rows (dy is scaled by l in f32 on the device first); replies are f32.
-    ia3_ft = any(s_[0] == "ia3" and s_[2] for s_ in specs)
+    # converts pageable f32 rows on host threads (`host_convert`), except backward IA3 rows (dy
+    # is scaled by l in f32 on the device first: copied as f32); replies are f32.
+    n_ft = sum(1 for s_ in specs if s_[2])
+    n_ft_ia3 = sum(1 for s_ in specs if s_[2] and s_[0] == "ia3")
     for l in layers:
         di, do = dims[l[1]]
-        n_ft = sum(1 for s_ in specs if s_[2])
-        bwd_esz = 4 if (ia3_ft and l[1] in (K, V, FF_UP)) else 2
-        moved[0] += t * len(specs) * di * 2 + t * n_ft * do * bwd_esz
+        f32_rows = n_ft_ia3 if l[1] in (K, V, FF_UP) else 0      # backward IA3 rows stay f32
+        moved[0] += t * len(specs) * di * 2 + t * ((n_ft - f32_rows) * do * 2 + f32_rows * do * 4)
         moved[1] += t * (len(specs) * do + n_ft * di) * 4
     return wl["L"] * tb + th, moved[0], moved[1], (tb, th)
 

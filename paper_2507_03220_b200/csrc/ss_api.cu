@@ -2940,16 +2940,19 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
   // no driver bounce copies), and the kernels see bf16 rows — the same bits the gather's own
   // f32 -> bf16 conversion would give. Not for backward IA3 rows (the gather scales dy by l in
   // f32 before rounding) or page-locked / device sources (DMA-able as they are).
+  // Backward IA3 rows stay f32 (copied, not converted, by the same threads into the same ring).
   bool conv = ctx->host_convert && esz_in == 4;
+  std::vector<char> keep_f32(n_seg, 0);
   for (size_t q = 0; conv && q < good.size(); ++q) {
     const ss_seg& s = segs[good[q]];
     if ((s.flags & SS_SEGF_PINNED) || !pageable(s.src)) conv = false;
     if (bwd && (s.flags & SS_SEGF_ADAPTER)) {
       auto ad = L.adapters.find(s.client_id);
-      if (ad != L.adapters.end() && (ad->second.kind & SS_ADAPTER_IA3)) conv = false;
+      if (ad != L.adapters.end() && (ad->second.kind & SS_ADAPTER_IA3)) keep_f32[good[q]] = 1;
     }
   }
-  const size_t esz_dev = conv ? 2 : esz_in;   // request row bytes per value on the device
+  // request row bytes per value in the device slot / the ring (bf16 where converted)
+  auto esz_of = [&](int seg) -> size_t { return conv && !keep_f32[seg] ? 2 : esz_in; };
   if (conv) {
     if (!ctx->pool) {
       const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
@@ -2958,7 +2961,7 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     }
     for (auto& hc : ctx->hconv) {
       if (!hc.ev) CK(cudaEventCreateWithFlags(&hc.ev, cudaEventDisableTiming));
-      const size_t need = (size_t)target * K * 2;
+      const size_t need = (size_t)target * K * 4;
       if (hc.cap < need) {
         if (hc.used) CK(cudaEventSynchronize(hc.ev));
         CK(cudaFreeHost(hc.buf));
@@ -2970,7 +2973,7 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
       }
     }
   }
-  const size_t in_need = (size_t)target * K * esz_dev, out_need = (size_t)target * N * esz_out;
+  const size_t in_need = (size_t)target * K * esz_in, out_need = (size_t)target * N * esz_out;
   const size_t base_need = any_base ? (size_t)target * N * esz_base : 0;
   for (auto& hs : ctx->hslot) {
     if (hs.in_cap < in_need || hs.out_cap < out_need || hs.base_cap < base_need) {
@@ -2993,16 +2996,19 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
     int64_t pos = 0;
     cs.clear();
     if (conv) {
-      // this sub-batch's rows, converted by the pool into ring slot j % 4 (once its previous
-      // DMA has read it), then one copy
+      // this sub-batch's rows, converted (or, backward IA3 rows, copied) by the pool into ring
+      // slot j % 4 (once its previous DMA has read it), then one copy
       auto& hc = ctx->hconv[j % 4];
       if (hc.used) CK(cudaEventSynchronize(hc.ev));
-      std::vector<int64_t> row0(ch.size() + 1, 0);
-      for (size_t q = 0; q < ch.size(); ++q) row0[q + 1] = row0[q] + (ch[q].r1 - ch[q].r0);
+      std::vector<int64_t> row0(ch.size() + 1, 0), byte0(ch.size() + 1, 0);
+      for (size_t q = 0; q < ch.size(); ++q) {
+        row0[q + 1] = row0[q] + (ch[q].r1 - ch[q].r0);
+        byte0[q + 1] = byte0[q] + (ch[q].r1 - ch[q].r0) * K * (int64_t)esz_of(ch[q].seg);
+      }
       const int64_t nrows = row0.back();
       constexpr int64_t kRowsPerTask = 16;
       const int tasks = (int)((nrows + kRowsPerTask - 1) / kRowsPerTask);
-      uint16_t* dstb = hc.buf;
+      char* ring = reinterpret_cast<char*>(hc.buf);
       ctx->pool->run(tasks, [&](int t) {
         const int64_t a0 = t * kRowsPerTask, a1 = std::min(nrows, a0 + kRowsPerTask);
         size_t q = std::upper_bound(row0.begin(), row0.end(), a0) - row0.begin() - 1;
@@ -3010,24 +3016,29 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
           while (r >= row0[q + 1]) ++q;
           const ss_seg& s = segs[ch[q].seg];
           const float* src = static_cast<const float*>(s.src) + (ch[q].r0 + (r - row0[q])) * s.src_ld;
-          cvt_row(src, dstb + r * K, K);
+          const size_t e = esz_of(ch[q].seg);
+          char* dst = ring + byte0[q] + (r - row0[q]) * K * (int64_t)e;
+          if (e == 2) cvt_row(src, reinterpret_cast<uint16_t*>(dst), K);
+          else memcpy(dst, src, (size_t)K * 4);
         }
       });
-      CK(cudaMemcpyAsync(hs.in, hc.buf, (size_t)nrows * K * 2, cudaMemcpyHostToDevice, ctx->h2d));
+      CK(cudaMemcpyAsync(hs.in, hc.buf, (size_t)byte0.back(), cudaMemcpyHostToDevice, ctx->h2d));
       CK(cudaEventRecord(hc.ev, ctx->h2d));
       hc.used = true;
     }
+    int64_t in_off = 0;   // bytes into the device slot
     for (const Piece& p : ch) {
       const ss_seg& s = segs[p.seg];
       const int64_t n = p.r1 - p.r0;
-      char* din = static_cast<char*>(hs.in) + pos * K * esz_dev;
+      char* din = static_cast<char*>(hs.in) + in_off;
+      in_off += n * K * (int64_t)esz_of(p.seg);
       if (!conv)
         CK(copy_rows(din, (size_t)K * esz_in, static_cast<const char*>(s.src) + p.r0 * s.src_ld * esz_in,
                      (size_t)s.src_ld * esz_in, (size_t)K * esz_in, (size_t)n, cudaMemcpyHostToDevice, ctx->h2d));
       ss_seg d = s;
       d.rows = (uint32_t)n;
       d.flags |= class_flag(ctx, K, s);   // a piece keeps its request's numerics class
-      if (conv) d.flags |= SS_SEGF_SRC_BF16;
+      if (esz_of(p.seg) == 2) d.flags |= SS_SEGF_SRC_BF16;
       d.src = din;
       d.src_ld = K;
       d.dst = static_cast<char*>(hs.out) + pos * N * esz_out;
