@@ -2525,6 +2525,28 @@ bool pageable(const void* p) {
   return a.type == cudaMemoryTypeUnregistered;
 }
 
+// The host conversion pool and page-locked ring slots of at least `bytes` each.
+int ensure_host_conv(ss_ctx* ctx, size_t bytes) {
+  if (!ctx->pool) {
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int n = ctx->host_threads > 0 ? ctx->host_threads : std::min(16, hw);
+    ctx->pool.reset(new HostPool(std::max(0, n - 1)));   // + the calling thread
+  }
+  for (auto& hc : ctx->hconv) {
+    if (!hc.ev) CK(cudaEventCreateWithFlags(&hc.ev, cudaEventDisableTiming));
+    if (hc.cap < bytes) {
+      if (hc.used) CK(cudaEventSynchronize(hc.ev));
+      CK(cudaFreeHost(hc.buf));
+      hc.buf = nullptr;
+      hc.cap = 0;
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&hc.buf), bytes, cudaHostAllocDefault));
+      hc.cap = bytes;
+      hc.used = false;
+    }
+  }
+  return SS_OK;
+}
+
 // The numerics class of a whole request (decode_rows), for the pieces a host pipeline splits it
 // into: a piece must reduce K the way the request would in one piece.
 uint32_t class_flag(const ss_ctx* ctx, int K, const ss_seg& s) {
@@ -2701,6 +2723,62 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
   // request rows from pinned host memory (gather, UVA) and the epilogue stores the reply rows
   // straight into it: one launch sequence and one synchronisation instead of two memcpy calls
   // per segment, whose API cost dominates a dispatch of tens of two-row segments.
+  // Small dispatch of pageable f32 request rows (numpy decode clients): the host threads convert
+  // them into a page-locked slot (bf16), and the dispatch goes on as a zero-copy one over those
+  // rows (the same bits as the device gather's conversion).
+  std::vector<ss_seg> conv_segs;
+  if (ctx->host_convert && esz_in == 4 &&
+      (double)rows_total * (K * 2 + N * esz_out) <= (double)ctx->zero_copy_bytes) {
+    // (only when every row converts and the replies can be written in place: then the dispatch
+    // surely takes the zero-copy path below)
+    bool eligible = true;
+    for (int i : good) {
+      const ss_seg& s = segs[i];
+      if ((s.flags & SS_SEGF_PINNED) || !pageable(s.src) || pageable(s.dst) || (s.dst_base && pageable(s.dst_base))) {
+        eligible = false;
+        break;
+      }
+      if (bwd && (s.flags & SS_SEGF_ADAPTER)) {
+        auto ad = L.adapters.find(s.client_id);
+        if (ad != L.adapters.end() && (ad->second.kind & SS_ADAPTER_IA3)) { eligible = false; break; }
+      }
+    }
+    if (eligible) {
+      std::vector<char> f32(n_seg, 0);   // (none here; kept for the row layout below)
+      int64_t bytes = 0;
+      for (int i : good) bytes += (int64_t)segs[i].rows * K * 2;
+      int rc0 = ensure_host_conv(ctx, (size_t)std::max<int64_t>(bytes, 1 << 20));
+      if (rc0) return rc0;
+      auto& hc = ctx->hconv[0];
+      if (hc.used) CK(cudaEventSynchronize(hc.ev));
+      conv_segs.assign(segs, segs + n_seg);
+      std::vector<int64_t> off(n_seg, 0);
+      int64_t o = 0;
+      for (int i : good) {
+        off[i] = o;
+        o += (int64_t)segs[i].rows * K * (f32[i] ? 4 : 2);
+      }
+      char* ring = reinterpret_cast<char*>(hc.buf);
+      ctx->pool->run((int)good.size(), [&](int t) {
+        const int i = good[t];
+        const ss_seg& s = segs[i];
+        for (int64_t r = 0; r < (int64_t)s.rows; ++r) {
+          const float* src = static_cast<const float*>(s.src) + r * s.src_ld;
+          char* dst = ring + off[i] + r * K * (f32[i] ? 4 : 2);
+          if (f32[i]) memcpy(dst, src, (size_t)K * 4);
+          else cvt_row(src, reinterpret_cast<uint16_t*>(dst), K);
+        }
+      });
+      for (int i : good) {
+        ss_seg& d = conv_segs[i];
+        d.src = ring + off[i];
+        d.src_ld = K;
+        d.flags |= SS_SEGF_SRC_BF16 | SS_SEGF_PINNED;   // (dst / dst_base checked above)
+      }
+      segs = conv_segs.data();
+      esz_in = 2;
+    }
+  }
   bool zero_copy = (double)rows_total * (K * esz_in + N * esz_out) <= (double)ctx->zero_copy_bytes;
   for (size_t q = 0; zero_copy && q < good.size(); ++q) {
     // only pinned (UVA-mapped) or device memory can be touched by the kernels directly
@@ -2953,26 +3031,7 @@ int ss_compute_batch_host(ss_ctx* ctx, int pass_kind, int block, int role, int n
   }
   // request row bytes per value in the device slot / the ring (bf16 where converted)
   auto esz_of = [&](int seg) -> size_t { return conv && !keep_f32[seg] ? 2 : esz_in; };
-  if (conv) {
-    if (!ctx->pool) {
-      const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-      const int n = ctx->host_threads > 0 ? ctx->host_threads : std::min(16, hw);
-      ctx->pool.reset(new HostPool(std::max(0, n - 1)));   // + the calling thread
-    }
-    for (auto& hc : ctx->hconv) {
-      if (!hc.ev) CK(cudaEventCreateWithFlags(&hc.ev, cudaEventDisableTiming));
-      const size_t need = (size_t)target * K * 4;
-      if (hc.cap < need) {
-        if (hc.used) CK(cudaEventSynchronize(hc.ev));
-        CK(cudaFreeHost(hc.buf));
-        hc.buf = nullptr;
-        hc.cap = 0;
-        CK(cudaHostAlloc(reinterpret_cast<void**>(&hc.buf), need, cudaHostAllocDefault));
-        hc.cap = need;
-        hc.used = false;
-      }
-    }
-  }
+  if (conv && (rc = ensure_host_conv(ctx, (size_t)target * K * 4))) return rc;
   const size_t in_need = (size_t)target * K * esz_in, out_need = (size_t)target * N * esz_out;
   const size_t base_need = any_base ? (size_t)target * N * esz_base : 0;
   for (auto& hs : ctx->hslot) {

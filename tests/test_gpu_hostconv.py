@@ -43,3 +43,27 @@ def test_numpy_f32_host_convert_bitwise(pass_kind, ia3):
         assert a[c].shape == b_[c].shape
         assert np.array_equal(a[c], b_[c], equal_nan=True), c
     ex.close()
+
+
+@pytest.mark.parametrize("pass_kind", [0, 1])
+def test_numpy_f32_small_dispatch_host_convert_bitwise(pass_kind):
+    """Decode-size numpy f32 dispatches (1-16 rows per client) take the host conversion into a
+    page-locked slot and then the zero-copy path: replies bitwise those of the device gather's own
+    conversion (host_convert 0), repeated (recurring-dispatch cache) and with changed values."""
+    d_in, d_out, role = 2048, 1024, O.Q
+    w, b = O.layer_params(53, 0, role, d_in, d_out)
+    ex = _ex({(0, role): (w, b)})
+    for c, r in enumerate((8, 16, 64, 32)):
+        ad = O.lora_params(53, c, 0, role, d_in, d_out, r, 2.0 * r)
+        ex.register_adapter(c, _Adapter(lora={_addr(0, role): (ad.a, ad.b)}, alpha=2.0 * r, rank=r))
+    rng = np.random.default_rng(53 + pass_kind)
+    counts = [2, 1, 16, 2, 5, 2]
+    width = d_out if pass_kind == 1 else d_in
+    for _ in range(2):
+        payloads = [rng.standard_normal((t, width)).astype(np.float32) for t in counts]
+        a = _run(ex, pass_kind, role, payloads, 0)
+        b1 = _run(ex, pass_kind, role, payloads, 1)
+        b2 = _run(ex, pass_kind, role, payloads, 1)
+        for c in range(len(counts)):
+            assert np.array_equal(a[c], b1[c]) and np.array_equal(a[c], b2[c]), c
+    ex.close()
