@@ -1037,6 +1037,16 @@ def main():
             traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
+    dec_traffic = None
+    dtr_path = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    if os.path.exists(dtr_path) and args.workload == "13b-decode":   # Q-shaped launches of this step
+        try:
+            dtr = json.load(open(dtr_path))
+            dec_traffic = {"dram_bytes_per_launch": dtr["dram_bytes_per_launch"],
+                           "algorithmic_bytes_per_launch": dtr["algorithmic_bytes_per_launch"],
+                           "launch": "Q-shaped decode dispatch (ncu capture, profiles/r02/ncu_decode_gemm.md)"}
+        except (OSError, ValueError, KeyError):
+            dec_traffic = None
 
     if grads_leg is not None:
         hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -1139,7 +1149,9 @@ def main():
                          if not decode else
                          {"bound": "hbm", "kernel": "seg_gemm_dec_kernel + dec_fixup_kernel (decode class: split-K in the class order, 64-row decode tiles)",
                           "achieved": gemm_gbs, "peak": hbm_peak, "unit": "GB/s",
-                          "frac": (gemm_gbs / hbm_peak) if gemm_gbs else None, "traffic": None,
+                          "frac": (gemm_gbs / hbm_peak) if gemm_gbs else None,
+                          "traffic": dec_traffic["dram_bytes_per_launch"] if dec_traffic else None,
+                          "traffic_detail": dec_traffic,
                           "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
                           "tflops": gemm_tflops}) | {
                          "gemm_share_of_step": gemm["ms"] / (ms * prof_steps),
