@@ -197,6 +197,23 @@ __global__ void __launch_bounds__(DEC_SHR_THREADS)
   // rows are 16-byte aligned, all of a thread's loads issued before its shared-memory stores)
   const bool vec = it.kind == 0 ? ((reinterpret_cast<uintptr_t>(it.src) | (uintptr_t)(it.ld * 2)) & 15) == 0
                                 : ((reinterpret_cast<uintptr_t>(it.src) | (uintptr_t)(it.ld * 4)) & 15) == 0;
+  // this CTA: rank rows [32 z, 32 z + 32); warp w: 4 of them, every load of a 4 x 1024-k block
+  // issued before its FMAs (the kernel is load-latency bound at these sizes); the first block's
+  // loads go out before the x rows are even read
+  const int q0 = (int)blockIdx.z * 32 + warp * 4;
+  const __nv_bfloat16* prow = p.pack + (int64_t)(sg.pack_row + q0) * p.pack_ld + k0;
+  uint4 raw[4][4];
+  auto load_block = [&](int kb) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int k = kb + v * 256 + lane * 8;
+        raw[i][v] = (q0 + i < R && k < kn) ? __ldg(reinterpret_cast<const uint4*>(prow + (int64_t)i * p.pack_ld + k))
+                                           : make_uint4(0, 0, 0, 0);
+      }
+  };
+  load_block(0);
   const int n8 = rows * (kn / 8);
   for (int i = tid; i < n8; i += DEC_SHR_THREADS) {
     const int r = i / (kn / 8), k = (i - r * (kn / 8)) * 8;
@@ -232,25 +249,13 @@ __global__ void __launch_bounds__(DEC_SHR_THREADS)
   }
   __syncthreads();
   float* part = p.part + ((int64_t)blockIdx.x * p.C + c) * DEC_SHR_MAXROWS * 256;
-  // this CTA: rank rows [32 z, 32 z + 32); warp w: 4 of them, every load of a 4 x 1024-k block
-  // issued before its FMAs (the kernel is load-latency bound at these sizes)
-  const int q0 = (int)blockIdx.z * 32 + warp * 4;
-  const __nv_bfloat16* prow = p.pack + (int64_t)(sg.pack_row + q0) * p.pack_ld + k0;
   float acc[4][MAXR];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int r = 0; r < MAXR; ++r) acc[i][r] = 0.f;
   for (int kb = 0; kb < kn; kb += 4 * 256) {
-    uint4 raw[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int k = kb + v * 256 + lane * 8;
-        raw[i][v] = (q0 + i < R && k < kn) ? __ldg(reinterpret_cast<const uint4*>(prow + (int64_t)i * p.pack_ld + k))
-                                           : make_uint4(0, 0, 0, 0);
-      }
+    if (kb > 0) load_block(kb);
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int k = kb + v * 256 + lane * 8;
