@@ -80,7 +80,8 @@ extern "C" {
  * follows the segment's own row count; a caller that splits one request into several segments
  * (the library's host pipelines do) sets the class of the whole request on every piece, so the
  * pieces give the same bits as the request would in one piece. */
-#define SS_SEGF_CLASS_DECODE (1u << 5)   /* force the decode class (split-K order) */
+#define SS_SEGF_CLASS_DECODE (1u << 5)   /* force the decode class (split-K order; segments of
+                                            at most 16 rows, ignored on longer ones) */
 #define SS_SEGF_CLASS_PREFILL (1u << 6)  /* force the single-chain class */
 
 /* One request (envelope) of a batch, in batch order. Rows are concatenated in array order
@@ -365,7 +366,7 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
                            double* flops, double* bytes);
 
 /* Numerics class of a request (a property of the request alone, so batching stays invisible):
- *   decode_rows (16)    segments of at most this many rows (0..64; layers with K % 64 == 0) are
+ *   decode_rows (16)    segments of at most this many rows (0..16; layers with K % 64 == 0) are
  *                       "decode class": their rows reduce K as C = ceil(K / (64 * decode_chunk_kb))
  *                       fixed contiguous chunks summed left to right in chunk order (split-K
  *                       kernel K1d + fixup), then their own LoRA chain; every other row reduces K

@@ -45,6 +45,8 @@ SS_SEGF_DST_BF16 = 1 << 1
 SS_SEGF_BASE_BF16 = 1 << 2
 SS_SEGF_ADAPTER = 1 << 3
 SS_SEGF_PINNED = 1 << 4
+SS_SEGF_CLASS_DECODE = 1 << 5
+SS_SEGF_CLASS_PREFILL = 1 << 6
 
 # Every symbol include/ss_b200.h declares (checked by tests/test_lib_abi.py).
 EXPORTED = (

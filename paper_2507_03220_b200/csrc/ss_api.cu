@@ -734,7 +734,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     d.flags = f;
     ds.push_back(d);
     src_of.push_back(&s);
-    const bool dec = dec_ok && (int)s.rows <= DEC_ROWS &&
+    const bool dec = dec_ok && (int)s.rows <= DEC_SHR_MAXROWS &&
                      ((s.flags & SS_SEGF_CLASS_DECODE) ||
                       (!(s.flags & SS_SEGF_CLASS_PREFILL) && (int)s.rows <= ctx->decode_rows));
     dec_of.push_back(dec ? 1 : 0);
@@ -1833,7 +1833,7 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
     return SS_OK;
   }
   if (!strcmp(key, "decode_rows")) {
-    if (value < 0 || value > DEC_ROWS) return fail(ctx, SS_E_ARG, "decode_rows must be 0..%d", DEC_ROWS);
+    if (value < 0 || value > DEC_SHR_MAXROWS) return fail(ctx, SS_E_ARG, "decode_rows must be 0..%d", DEC_SHR_MAXROWS);
     ctx->decode_rows = (int)value;
     return SS_OK;
   }

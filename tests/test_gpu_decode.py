@@ -185,3 +185,33 @@ def test_host_pipeline_pieces_keep_request_class(zero_copy):
                                             for c in range(len(counts))])
         for c in range(len(counts)):
             assert torch.equal(got[c], devr[c].cpu()), (pass_kind, c)
+
+
+def test_class_decode_flag_ignored_beyond_16_rows():
+    """SS_SEGF_CLASS_DECODE on a segment of more than 16 rows is ignored (single-chain order,
+    the rows of the same segment without the flag), through the C ABI."""
+    import ctypes
+    from paper_2507_03220_b200 import _lib as L
+    lib = L.load()
+    dev = torch.device("cuda:0")
+    ctx = ctypes.c_void_p()
+    L.check(None, lib.ss_ctx_create(0, 0, 1, ctypes.byref(ctx)))
+    K, N, t = 1024, 768, 20
+    W = (torch.randn(K, N, device=dev) / K ** 0.5).to(torch.bfloat16)
+    L.check(ctx, lib.ss_load_layer(ctx, 0, 0, K, N, W.data_ptr(), N, None, L.SS_MEM_DEVICE | L.SS_DT_BF16))
+    x = torch.randn(t, K, device=dev).to(torch.bfloat16)
+    outs = []
+    for extra in (0, L.SS_SEGF_CLASS_DECODE):
+        out = torch.empty(t, N, device=dev, dtype=torch.bfloat16)
+        arr = (L.SsSeg * 1)()
+        s = arr[0]
+        s.client_id, s.rows, s.width = 0, t, K
+        s.flags = L.SS_SEGF_SRC_BF16 | L.SS_SEGF_DST_BF16 | extra
+        s.src, s.src_ld, s.dst, s.dst_ld = x.data_ptr(), K, out.data_ptr(), N
+        st = (ctypes.c_int32 * 1)()
+        L.check(ctx, lib.ss_compute_batch(ctx, 0, 0, 0, 1, arr, torch.cuda.current_stream().cuda_stream, st))
+        torch.cuda.synchronize()
+        assert st[0] == 0
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    lib.ss_ctx_destroy(ctx)
