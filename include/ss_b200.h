@@ -129,7 +129,9 @@ SS_API int ss_clear_client(ss_ctx* ctx, uint32_t client_id);
 
 /* Compute one batch for layer (block, role) and pass. `stream` is a cudaStream_t (NULL =
  * legacy default stream). Asynchronous: results are visible after the stream reaches this
- * point. seg_status[n_seg] receives per-segment status; rejected segments are not written. */
+ * point. seg_status[n_seg] receives per-segment status; rejected segments are not written.
+ * A context's dispatches share one device workspace: a dispatch on a different stream than the
+ * context's previous one is ordered after it (stream wait on its completion event). */
 SS_API int ss_compute_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg,
                      const ss_seg* segs, void* stream, int32_t* seg_status);
 

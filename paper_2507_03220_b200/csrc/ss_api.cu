@@ -212,6 +212,8 @@ struct ss_ctx {
   int64_t pipeline_bytes = 24 << 20;  // target bytes of the wider side per sub-batch
   int pipeline_rows = 4096;
   cudaEvent_t upload_done = nullptr, compute_done = nullptr;
+  cudaStream_t last_stream = nullptr;   // stream of the previous dispatch (cross-stream ordering)
+  bool done_captured = false;           // compute_done was last recorded inside a graph capture
   bool any_compute = false;
   int64_t launches = 0;
   int group_m = 16;
@@ -1286,6 +1288,16 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   const int tbn = B.tbn, num_m = B.num_m;
   int rc = SS_OK;
   const CUtensorMap* d_tmaps = reinterpret_cast<const CUtensorMap*>(dv + B.off_tm);
+  // One workspace per context (X, the LoRA operand, partials, tickets): a dispatch issued on a
+  // different stream than the previous one waits for it (not while capturing a graph: the
+  // captured sequence is ordered on its own stream, and the capture follows a synchronised run).
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(stream, &cs));
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
+  if (ctx->any_compute && stream != ctx->last_stream && !capturing && !ctx->done_captured)
+    CK(cudaStreamWaitEvent(stream, ctx->compute_done, 0));
+  ctx->last_stream = stream;
+  ctx->done_captured = capturing;   // (an event recorded inside a capture cannot be waited on outside)
   const DevSeg* d_segs = reinterpret_cast<const DevSeg*>(dv + B.off_seg);
   // ---- K4 gather of the packed rows
   auto launch_gather = [&]() -> int {

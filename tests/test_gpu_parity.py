@@ -910,3 +910,36 @@ def test_host_batch_with_mixed_dtypes_computes_every_envelope():
         assert isinstance(r, torch.Tensor), r
         ref = O.affine_forward(hosts[c].float().numpy(), wr, b)
         _close(r.float().cpu().numpy(), ref, what=f"mixed host client {c}")
+
+
+def test_dispatches_on_two_streams_are_ordered():
+    """One context, consecutive dispatches on two different streams with no synchronisation in
+    between: the second is ordered after the first (they share the context's workspace), so both
+    give their solo results bitwise."""
+    d_in, d_out = 2048, 3072
+    w, b = O.layer_params(61, 0, O.V, d_in, d_out)
+    ex = _ex({(0, O.V): (w, b)})
+    dev = ex.device
+    xa = [torch.randn(t, d_in, device=dev).to(torch.bfloat16) for t in (3000, 700, 5)]
+    xb = [torch.randn(t, d_in, device=dev).to(torch.bfloat16) for t in (2500, 2, 900)]
+    solo_a = ex._compute_batch(0, [_env(c, 1, 0, O.V, 0, x) for c, x in enumerate(xa)])
+    solo_b = ex._compute_batch(0, [_env(c, 2, 0, O.V, 0, x) for c, x in enumerate(xb)])
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        outs_a = [torch.empty(x.shape[0], d_out, device=dev, dtype=torch.bfloat16) for x in xa]
+        outs_b = [torch.empty(x.shape[0], d_out, device=dev, dtype=torch.bfloat16) for x in xb]
+        segs_a = [(c, x, outs_a[c], None) for c, x in enumerate(xa)]
+        segs_b = [(c, x, outs_b[c], None) for c, x in enumerate(xb)]
+        da = ex.compile_dispatch(0, 0, O.V, segs_a)
+        db = ex.compile_dispatch(0, 0, O.V, segs_b)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            da.run()
+        with torch.cuda.stream(s2):
+            db.run()
+        torch.cuda.synchronize()
+        for c in range(len(xa)):
+            assert torch.equal(outs_a[c], solo_a[c]), ("a", c)
+        for c in range(len(xb)):
+            assert torch.equal(outs_b[c], solo_b[c]), ("b", c)
