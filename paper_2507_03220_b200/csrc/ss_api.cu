@@ -1273,6 +1273,21 @@ cudaError_t launch_k(const ss_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim
   return launch_kp(ctx->pdl && !ctx->profiling, kernel, grid, block, smem, st, args...);
 }
 
+// One workspace per context (X, the LoRA operand, shrink / decode partials, tickets): work issued
+// on a different stream than the context's previous work waits for it (not while capturing a
+// graph: the captured sequence is ordered on its own stream and follows a synchronised run; and
+// not on an event last recorded inside a capture, which cannot be waited on outside it).
+int order_after_previous(ss_ctx* ctx, cudaStream_t stream) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(stream, &cs));
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
+  if (ctx->any_compute && stream != ctx->last_stream && !capturing && !ctx->done_captured)
+    CK(cudaStreamWaitEvent(stream, ctx->compute_done, 0));
+  ctx->last_stream = stream;
+  ctx->done_captured = capturing;
+  return SS_OK;
+}
+
 // Launch the kernels of a built batch whose tables are at device address `dv` (stream-ordered
 // after whatever copied them there).
 int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
@@ -1288,16 +1303,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   const int tbn = B.tbn, num_m = B.num_m;
   int rc = SS_OK;
   const CUtensorMap* d_tmaps = reinterpret_cast<const CUtensorMap*>(dv + B.off_tm);
-  // One workspace per context (X, the LoRA operand, partials, tickets): a dispatch issued on a
-  // different stream than the previous one waits for it (not while capturing a graph: the
-  // captured sequence is ordered on its own stream, and the capture follows a synchronised run).
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  CK(cudaStreamIsCapturing(stream, &cs));
-  const bool capturing = cs != cudaStreamCaptureStatusNone;
-  if (ctx->any_compute && stream != ctx->last_stream && !capturing && !ctx->done_captured)
-    CK(cudaStreamWaitEvent(stream, ctx->compute_done, 0));
-  ctx->last_stream = stream;
-  ctx->done_captured = capturing;   // (an event recorded inside a capture cannot be waited on outside)
+  if ((rc = order_after_previous(ctx, stream))) return rc;
   const DevSeg* d_segs = reinterpret_cast<const DevSeg*>(dv + B.off_seg);
   // ---- K4 gather of the packed rows
   auto launch_gather = [&]() -> int {
@@ -2398,6 +2404,7 @@ int ss_adapter_grads(ss_ctx* ctx, int block, int role, int n_seg, const ss_grad_
     memcpy(h + o_ii, pitems.data(), pitems.size() * sizeof(Ia3PartItem));
     memcpy(h + o_if, fitems.data(), fitems.size() * sizeof(Ia3FinItem));
   }
+  if ((rc = order_after_previous(ctx, stream))) return rc;   // (shared shrink partials / tickets)
   CK(cudaStreamWaitEvent(stream, ctx->upload_done, 0));
   CK(cudaMemcpyAsync(stp->dev, stp->host, total, cudaMemcpyHostToDevice, stream));
   CK(cudaEventRecord(stp->done, stream));
