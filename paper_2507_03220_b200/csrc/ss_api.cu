@@ -263,6 +263,7 @@ struct ss_ctx {
   size_t dshr_part_cap = 0;
   int* dshr_ticket = nullptr;     // decode shrink: per-item arrival counters (zero between launches)
   size_t dshr_ticket_cap = 0;
+  int decode_lora_piece = DEC_LP_CHUNKS;   // max 16-row rank chunks per decode LoRA piece (tuning)
   int decode_split = 0;           // K1d chunk groups beside the side-stream shrink, LoRA groups after (slower)
   float* dec_part = nullptr;      // K1d: fp32 chunk partials of the decode tiles
   size_t dec_part_cap = 0;
@@ -881,7 +882,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
       max_cols = std::max(max_cols, td.chunk_count * LORA_CHUNK);
     }
     // decode tiles: the tile's rank chunks, block-diagonal over its segments, cut into pieces of
-    // whole segments of <= DEC_LP_CHUNKS chunks (one LoRA chain each, see decode.cuh)
+    // whole segments of <= decode_lora_piece chunks (one LoRA chain each, see decode.cuh)
     for (size_t t = 0; t < dtiles.size(); ++t) {
       DecTile& dt = dtiles[t];
       dt.al_row = (int32_t)((int64_t)num_m * TM + (int64_t)t * DEC_ROWS);
@@ -893,7 +894,7 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
         const int col = (int)(chunks.size() - dt.chunk_begin) * LORA_CHUNK;
         const int hilo = ctx->lora_hilo == 2 || (ctx->lora_hilo == 1 && !(d.flags & SEGF_DST_BF16));
         const int nch = (1 + hilo) * (d.rank_pad / LORA_CHUNK);
-        if (dt.lp_count == 0 || lp_chunks + nch > DEC_LP_CHUNKS) {
+        if (dt.lp_count == 0 || lp_chunks + nch > ctx->decode_lora_piece) {
           lpieces.push_back(make_int2((int)lstages.size(), 0));
           dt.lp_count++;
           lp_chunks = 0;
@@ -1863,6 +1864,11 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
     if (value < 0 || value > 256) return fail(ctx, SS_E_ARG, "host_threads must be 0..256");
     ctx->host_threads = (int)value;
     ctx->pool.reset();
+    return SS_OK;
+  }
+  if (!strcmp(key, "decode_lora_piece")) {
+    if (value < 1 || value > 1024) return fail(ctx, SS_E_ARG, "decode_lora_piece must be 1..1024");
+    ctx->decode_lora_piece = (int)value;
     return SS_OK;
   }
   if (!strcmp(key, "decode_split")) {
