@@ -382,6 +382,9 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   decode_lora_piece (24) rank chunks (16 rows, hi and lo counted) per LoRA piece of a decode tile:
  *                       pieces are whole segments, each one chain and one unit per column tile
  *                       (results unchanged: a row's LoRA chain is its own segment's)
+ *   decode_prologue (1) decode-only dispatch with decode-class LoRA rows: their shrink and the
+ *                       row gather in one launch (else a side-stream shrink beside the gather;
+ *                       results unchanged)
  *   decode_split (0)    decode-only dispatch with a side-stream shrink: the decode-class GEMM's
  *                       chunk groups launch behind the gather, beside the shrink; its LoRA groups
  *                       after the join (results unchanged; measured 9.84 vs 9.29 ms per 13B decode step)

@@ -178,20 +178,20 @@ struct DecShrinkParams {
 constexpr int DEC_SHR_THREADS = 256;
 constexpr int DEC_SHR_MAXROWS = 16;
 
+// Block (bx, by, bz) of a (items, C, gz) grid: the kernel below, or a share of a combined
+// launch with the gather (dec_prologue_kernel).
 template <int MAXR>   // rows per item bound (4 or DEC_SHR_MAXROWS): the accumulators' registers
-__global__ void __launch_bounds__(DEC_SHR_THREADS)
-    dec_shrink_kernel(const DecShrinkParams p) {
+__device__ __forceinline__ void dec_shrink_body(const DecShrinkParams& p, const int bx, const int by, const int bz,
+                                                const int gz) {
   extern __shared__ float xs[];   // [rows][kbc * 64] bf16-rounded x of this chunk
   __shared__ int last;
-  const DecShrinkItem it = p.items[blockIdx.x];
+  const DecShrinkItem it = p.items[bx];
   const DevSeg sg = p.segs[it.seg];
   const int R = sg.rank_pad, rows = it.rows;
-  const int c = blockIdx.y;
+  const int c = by;
   const int kc = p.kbc * 64;
   const int k0 = c * kc, kn = min(p.K - k0, kc);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  pdl_wait();
-  pdl_trigger();
   // x rows of the chunk -> shared memory (as the GEMM's bf16 operand would hold them)
   // (8 consecutive values per thread and load: 16-byte bf16 / 2 x 16-byte f32 vectors when the
   // rows are 16-byte aligned, all of a thread's loads issued before its shared-memory stores)
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(DEC_SHR_THREADS)
   // this CTA: rank rows [32 z, 32 z + 32); warp w: 4 of them, every load of a 4 x 1024-k block
   // issued before its FMAs (the kernel is load-latency bound at these sizes); the first block's
   // loads go out before the x rows are even read
-  const int q0 = (int)blockIdx.z * 32 + warp * 4;
+  const int q0 = bz * 32 + warp * 4;
   const __nv_bfloat16* prow = p.pack + (int64_t)(sg.pack_row + q0) * p.pack_ld + k0;
   uint4 raw[4][4];
   auto load_block = [&](int kb) {
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(DEC_SHR_THREADS)
     for (int j = 0; j < 8; ++j) xs[r * kc + k + j] = v[j];
   }
   __syncthreads();
-  float* part = p.part + ((int64_t)blockIdx.x * p.C + c) * DEC_SHR_MAXROWS * 256;
+  float* part = p.part + ((int64_t)bx * p.C + c) * DEC_SHR_MAXROWS * 256;
   float acc[4][MAXR];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -298,11 +298,11 @@ __global__ void __launch_bounds__(DEC_SHR_THREADS)
   }
   __threadfence();
   __syncthreads();
-  if (tid == 0) last = atomicAdd(p.ticket + blockIdx.x, 1) == p.C * (int)gridDim.z - 1;
+  if (tid == 0) last = atomicAdd(p.ticket + bx, 1) == p.C * gz - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const float* base = p.part + (int64_t)blockIdx.x * p.C * DEC_SHR_MAXROWS * 256;
+  const float* base = p.part + (int64_t)bx * p.C * DEC_SHR_MAXROWS * 256;
   const int nh = it.hilo ? 2 : 1;
   // the tile's other rows: zeros in this segment's columns
   for (int i = tid; i < (DEC_ROWS - rows) * R; i += DEC_SHR_THREADS) {
@@ -323,7 +323,34 @@ __global__ void __launch_bounds__(DEC_SHR_THREADS)
     out[0] = hi;
     if (nh == 2) out[R] = __float2bfloat16_rn(v - __bfloat162float(hi));
   }
-  if (tid == 0) p.ticket[blockIdx.x] = 0;   // ready for the next launch
+  if (tid == 0) p.ticket[bx] = 0;   // ready for the next launch
+}
+
+template <int MAXR>
+__global__ void __launch_bounds__(DEC_SHR_THREADS)
+    dec_shrink_kernel(const DecShrinkParams p) {
+  pdl_wait();
+  pdl_trigger();
+  dec_shrink_body<MAXR>(p, (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)gridDim.z);
+}
+
+// A decode-only dispatch's prologue in ONE launch: blocks [0, n_shr) run the decode-class LoRA
+// shrink (items x C x gz), the rest gather the rows into X. The two are independent (the shrink
+// reads the client rows in place), so they run side by side as with a side-stream shrink, but
+// the GEMM behind them keeps its programmatic edge (it streams W before griddepcontrol.wait).
+template <int MAXR>
+__global__ void __launch_bounds__(DEC_SHR_THREADS)
+    dec_prologue_kernel(const DecShrinkParams sp, const GatherParams gp, const int n_shr, const int sy,
+                        const int sz) {
+  pdl_wait();
+  pdl_trigger();
+  const int b = (int)blockIdx.x;
+  if (b < n_shr) {
+    const int bz = b % sz, by = (b / sz) % sy, bx = b / (sz * sy);
+    dec_shrink_body<MAXR>(sp, bx, by, bz, sz);
+  } else {
+    gather_rows_body(gp, b - n_shr, (int)gridDim.x - n_shr);
+  }
 }
 
 __device__ __forceinline__ void st_f4_evict_last(float4* p, float4 v, uint64_t pol) {

@@ -1738,15 +1738,14 @@ __device__ __forceinline__ int find_piece(const GatherParams& p, int xrow) {
 }
 
 // One warp per (row, column chunk), grid-stride.
-__global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) {
-  pdl_wait();
-  pdl_trigger();
+// Block `bx` of `nb` (the kernel below; or a share of a combined launch, decode.cuh).
+__device__ __forceinline__ void gather_rows_body(const GatherParams& p, const int bx, const int nb) {
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   // work item = (row, column chunk): a decode-size dispatch (tens of rows) still spreads over
   // the whole GPU instead of one latency-bound warp per row
   const int nchunk8 = (p.K / 8 + p.nsplit - 1) / p.nsplit;     // 8-element units per chunk
-  for (int w = blockIdx.x * wpb + (threadIdx.x >> 5); w < p.MX * p.nsplit; w += gridDim.x * wpb) {
+  for (int w = bx * wpb + (threadIdx.x >> 5); w < p.MX * p.nsplit; w += nb * wpb) {
     const int row = w / p.nsplit, part = w - row * p.nsplit;
     const int u0 = part * nchunk8, u1 = min(p.K / 8, u0 + nchunk8);   // vector units [u0, u1)
     const int e0 = part == 0 ? 0 : u0 * 8, e1 = part == p.nsplit - 1 ? p.K : u1 * 8;  // scalar range
@@ -1829,6 +1828,12 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) 
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) gather_rows_kernel(const GatherParams p) {
+  pdl_wait();
+  pdl_trigger();
+  gather_rows_body(p, (int)blockIdx.x, (int)gridDim.x);
 }
 
 // f32 -> bf16 conversion for weight / pack uploads.

@@ -264,6 +264,7 @@ struct ss_ctx {
   int* dshr_ticket = nullptr;     // decode shrink: per-item arrival counters (zero between launches)
   size_t dshr_ticket_cap = 0;
   int decode_lora_piece = DEC_LP_CHUNKS;   // max 16-row rank chunks per decode LoRA piece (tuning)
+  int decode_prologue = 1;          // decode-only dispatch: decode shrink + gather in one launch
   int decode_split = 0;           // K1d chunk groups beside the side-stream shrink, LoRA groups after (slower)
   float* dec_part = nullptr;      // K1d: fp32 chunk partials of the decode tiles
   size_t dec_part_cap = 0;
@@ -1307,8 +1308,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   if ((rc = order_after_previous(ctx, stream))) return rc;
   const DevSeg* d_segs = reinterpret_cast<const DevSeg*>(dv + B.off_seg);
   // ---- K4 gather of the packed rows
-  auto launch_gather = [&]() -> int {
-    GatherParams gp;
+  auto gather_params = [&](GatherParams& gp, int& grid) {
     gp.MX = (int)MX;
     gp.K = K;
     gp.ldx = (int)ldx;
@@ -1321,7 +1321,12 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     gp.X_lo = B.any_lo ? ctx->X_lo : nullptr;
     // several warps per row when the dispatch has too few rows to fill the GPU
     gp.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((K / 8 + 127) / 128, ((int64_t)ctx->num_sms * 16 + MX - 1) / MX));
-    const int grid = (int)std::min<int64_t>((MX * gp.nsplit + 7) / 8, (int64_t)ctx->num_sms * 8);
+    grid = (int)std::min<int64_t>((MX * gp.nsplit + 7) / 8, (int64_t)ctx->num_sms * 8);
+  };
+  auto launch_gather = [&]() -> int {
+    GatherParams gp;
+    int grid = 0;
+    gather_params(gp, grid);
     const int pi = prof_begin(ctx, stream, SS_KERNEL_GATHER, 0.0, B.gather_bytes);
     CK(launch_k(ctx, gather_rows_kernel, grid, 256, 0, stream, gp));
     prof_end(ctx, stream, pi);
@@ -1336,7 +1341,11 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   const bool whole = B.shrink_chunks_ == 1 ||
                      (B.part_ld <= 64 && (ctx->shrink_mode == 1 || (ctx->shrink_mode == 0 && B.n_items >= ctx->num_sms)));
   const int shrink_ctas = any_lora ? B.n_items * (whole ? 1 : B.shrink_chunks_) : 0;
-  const bool side = any_lora && MX > 0 && B.shrink_indep && ctx->side_shrink && !ctx->profiling;
+  // decode-only dispatch whose LoRA shrink is all decode-class items reading rows in place: the
+  // shrink and the gather share one launch (no side stream, the GEMM keeps its PDL edge)
+  const bool prologue = ctx->decode_prologue && any_lora && MX > 0 && num_m == 0 && B.n_items == 0 &&
+                        B.n_ditems > 0 && B.shrink_indep && !ctx->profiling && !ctx->decode_split;
+  const bool side = !prologue && any_lora && MX > 0 && B.shrink_indep && ctx->side_shrink && !ctx->profiling;
   // Overlap (streaming kernel): the GEMM does not wait for the side-stream shrink; its producer
   // waits on the shrink's completion counter right before the LoRA stages. Only when the
   // shrink's CTAs (2 per SM) and the GEMM's fit on the GPU together, so neither can starve.
@@ -1345,6 +1354,19 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   // decode-only dispatch with a side-stream shrink: the decode GEMM's chunk groups run beside the
   // shrink (their own launch, right behind the gather); the LoRA groups after the join
   const bool dec_split = side && !overlap && ctx->decode_split && B.num_m == 0 && B.dec_groups > B.dec_chunk_groups;
+  auto dec_shrink_params = [&](DecShrinkParams& dsp) {
+    dsp.K = K;
+    dsp.kbc = B.dec_kbc;
+    dsp.C = B.dec_C;
+    dsp.lora_ld = (int)lora_ld;
+    dsp.segs = d_segs;
+    dsp.items = reinterpret_cast<const DecShrinkItem*>(dv + B.off_di);
+    dsp.pack = bwd ? L.b_pack : L.at_pack;
+    dsp.pack_ld = bwd ? L.ld_b : L.ld_at;
+    dsp.a_lora = ctx->a_lora;
+    dsp.part = ctx->dshr_part;
+    dsp.ticket = ctx->dshr_ticket;
+  };
   auto launch_shrink = [&](cudaStream_t st) -> int {
     // the streaming kernel (<= 64 rows) reads the LoRA operand through a 64-row box too
     rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, B.stream ? 64 : BM);
@@ -1373,17 +1395,7 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     }
     if (B.n_ditems > 0) {
       DecShrinkParams dsp;
-      dsp.K = K;
-      dsp.kbc = B.dec_kbc;
-      dsp.C = B.dec_C;
-      dsp.lora_ld = (int)lora_ld;
-      dsp.segs = d_segs;
-      dsp.items = reinterpret_cast<const DecShrinkItem*>(dv + B.off_di);
-      dsp.pack = bwd ? L.b_pack : L.at_pack;
-      dsp.pack_ld = bwd ? L.ld_b : L.ld_at;
-      dsp.a_lora = ctx->a_lora;
-      dsp.part = ctx->dshr_part;
-      dsp.ticket = ctx->dshr_ticket;
+      dec_shrink_params(dsp);
       const int rmax = std::max(16, B.dec_rank_max);
       const dim3 g(B.n_ditems, B.dec_C, (rmax + 31) / 32);
       const size_t smem = (size_t)DEC_SHR_MAXROWS * B.dec_kbc * 64 * sizeof(float);
@@ -1395,7 +1407,6 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     CK(cudaGetLastError());
     return SS_OK;
   };
-
   // The shrink reads the client rows in place (no packed rows) -> it runs on the side stream
   // beside the gather: fork after everything queued so far (the previous dispatch's GEMM reads
   // the LoRA operand the shrink rewrites), join before the GEMM.
@@ -1406,6 +1417,27 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
     if ((rc = launch_gather())) return rc;
     if (!overlap && !dec_split) CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));
+  } else if (prologue) {
+    // decode-only dispatch: shrink + gather in one launch (dec_prologue_kernel)
+    rc = encode_2d(ctx, &tmAL, ctx->a_lora, lora_ld, al_rows, lora_ld, 64, B.stream ? 64 : BM);
+    if (rc) return rc;
+    DecShrinkParams dsp;
+    dec_shrink_params(dsp);
+    GatherParams gp;
+    int ggrid = 0;
+    gather_params(gp, ggrid);
+    const int sy = B.dec_C, sz = (std::max(16, B.dec_rank_max) + 31) / 32;
+    const int n_shr = B.n_ditems * sy * sz;
+    const size_t smem = (size_t)DEC_SHR_MAXROWS * B.dec_kbc * 64 * sizeof(float);
+    const int pi = prof_begin(ctx, stream, SS_KERNEL_SHRINK, B.shrink_flops, B.shrink_bytes + B.gather_bytes);
+    if (B.dec_rows_max <= 4)
+      CK(launch_k(ctx, dec_prologue_kernel<4>, n_shr + ggrid, DEC_SHR_THREADS, smem, stream, dsp, gp, n_shr, sy, sz));
+    else
+      CK(launch_k(ctx, dec_prologue_kernel<DEC_SHR_MAXROWS>, n_shr + ggrid, DEC_SHR_THREADS, smem, stream, dsp, gp,
+                  n_shr, sy, sz));
+    prof_end(ctx, stream, pi);
+    CK(cudaGetLastError());
+    ctx->launches++;
   } else {
     if (MX > 0 && (rc = launch_gather())) return rc;
     if (any_lora && (rc = launch_shrink(stream))) return rc;
@@ -1606,6 +1638,10 @@ int set_kernel_attrs(ss_ctx* ctx) {
   CK(cudaFuncSetAttribute(dec_shrink_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           DEC_SHR_MAXROWS * DEC_MAX_KBC * 64 * (int)sizeof(float)));
   CK(cudaFuncSetAttribute(dec_shrink_kernel<DEC_SHR_MAXROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          DEC_SHR_MAXROWS * DEC_MAX_KBC * 64 * (int)sizeof(float)));
+  CK(cudaFuncSetAttribute(dec_prologue_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          DEC_SHR_MAXROWS * DEC_MAX_KBC * 64 * (int)sizeof(float)));
+  CK(cudaFuncSetAttribute(dec_prologue_kernel<DEC_SHR_MAXROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           DEC_SHR_MAXROWS * DEC_MAX_KBC * 64 * (int)sizeof(float)));
   CK(cudaFuncSetAttribute(seg_gemm_dec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC_SMEM));
   CK(cudaFuncSetAttribute(lora_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GRAD_SMEM));
@@ -1869,6 +1905,10 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "decode_lora_piece")) {
     if (value < 1 || value > 1024) return fail(ctx, SS_E_ARG, "decode_lora_piece must be 1..1024");
     ctx->decode_lora_piece = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "decode_prologue")) {
+    ctx->decode_prologue = value ? 1 : 0;
     return SS_OK;
   }
   if (!strcmp(key, "decode_split")) {
