@@ -385,6 +385,11 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   decode_prologue (1) decode-only dispatch with decode-class LoRA rows: their shrink and the
  *                       row gather in one launch (else a side-stream shrink beside the gather;
  *                       results unchanged)
+ *   decode_fixup_fused (0) decode class: the ordered chunk fold + epilogue run inside the GEMM
+ *                       launch (each CTA once its groups are done, behind per-tile completion
+ *                       counters) instead of a separate fixup launch (bitwise the same fold;
+ *                       measured 9.26 vs 8.69 ms per 13B decode step: the fixup launch folds with
+ *                       far more threads in flight)
  *   decode_split (0)    decode-only dispatch with a side-stream shrink: the decode-class GEMM's
  *                       chunk groups launch behind the gather, beside the shrink; its LoRA groups
  *                       after the join (results unchanged; measured 9.84 vs 9.29 ms per 13B decode step)

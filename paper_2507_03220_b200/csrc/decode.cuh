@@ -93,6 +93,12 @@ struct DecParams {
   long long* trace;      // testing: per CTA {start ns, end ns, groups run, units run} (nullptr: off)
   int pdl_early;         // launched behind the gather / shrink: the producer streams its first W
                          // stages before griddepcontrol.wait (every other role waits on its loads)
+  // In-kernel fixup (nullptr: the separate dec_fixup_kernel runs behind the GEMM). fx_cnt counts,
+  // per (m, n tile, 32-row half), the groups whose partials are stored (release by the epilogue
+  // warp of that half; self-resetting); the CTA's otherwise idle warps claim fixup units through
+  // fx_claim[0] in unit order and fold a unit once its count is complete.
+  int* fx_cnt;
+  int* fx_claim;
 };
 
 __device__ __forceinline__ long long globaltimer_ns() {
@@ -357,6 +363,80 @@ __device__ __forceinline__ void st_f4_evict_last(float4* p, float4 v, uint64_t p
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(p), "f"(v.x), "f"(v.y),
                "f"(v.z), "f"(v.w), "l"(pol)
                : "memory");
+}
+
+// K1d fixup: y = fold(p_0 .. p_{C-1}, [lo_0 .. lo_{C-1}], [p_lora]) left to right, then bias /
+// y_base / IA3 / dst, for every valid row of every decode tile. Launched behind the GEMM (PDL: the
+// grid is resident early and waits on griddepcontrol.wait, which covers the GEMM's partial
+// stores). One CTA per 32 rows x 64 columns of a tile; a thread owns one row x 8 columns and
+// issues the loads of 8 partials at a time before adding them (the sum order is fixed, the loads
+// are not serialised).
+constexpr int DEC_FIX_ROWS = 32;
+constexpr int DEC_FIX_THREADS = DEC_FIX_ROWS * (DEC_TN / 8);   // 256
+
+__device__ __forceinline__ void dec_fixup_unit(const DecParams& p, const int unit, const int t) {
+  const int q = unit % (DEC_ROWS / DEC_FIX_ROWS);
+  const int tile = unit / (DEC_ROWS / DEC_FIX_ROWS);   // mt * n_n + nt
+  const int mt = tile / p.n_n, nt = tile - mt * p.n_n;
+  const int row = q * DEC_FIX_ROWS + t / (DEC_TN / 8);
+  const int col = (t % (DEC_TN / 8)) * 8;
+  const DecTile td = p.tiles[mt];
+  const int n = nt * DEC_TN + col;
+  if (row >= td.rows || n >= p.N) return;
+  const float4* src = reinterpret_cast<const float4*>(p.part + (int64_t)tile * p.S * DEC_PART +
+                                                      (int64_t)row * DEC_TN + col);
+  constexpr int P4 = DEC_PART / 4;
+  const int xrow = td.arow + row;
+  const DevSeg sg = p.segs[p.row_seg[xrow]];
+  // slots in fold order: hi chunks 0..C-1, lo chunks C..2C-1 (lo tiles only), then the LoRA
+  // piece holding this row's rank block (every other piece is exact zeros for this row)
+  const int nhl = td.lo ? 2 * p.C : p.C;
+  const int nslots = nhl + ((sg.flags & SEGF_LORA) && td.lp_count > 0 ? 1 : 0);
+  float v[8];
+  for (int i0 = 0; i0 < nslots; i0 += 8) {
+    float4 buf[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i0 + i < nslots) {
+        const int slot = i0 + i < nhl ? i0 + i : 2 * p.C + sg.dec_piece;
+        const float4* s = src + (int64_t)slot * P4;
+        buf[i][0] = __ldcg(s);
+        buf[i][1] = __ldcg(s + 1);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i0 + i < nslots) {
+        const float w[8] = {buf[i][0].x, buf[i][0].y, buf[i][0].z, buf[i][0].w,
+                            buf[i][1].x, buf[i][1].y, buf[i][1].z, buf[i][1].w};
+        if (i0 + i == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = w[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] += w[j];
+        }
+      }
+    }
+  }
+  const int ncols = min(8, p.N - n);
+  const int64_t r_local = xrow - sg.xrow0 + sg.xlocal0;
+  const bool bf = sg.flags & SEGF_DST_BF16, bbf = sg.flags & SEGF_BASE_BF16;
+  if (p.has_bias) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < ncols) v[j] += __ldg(p.bias + n + j);
+  }
+  if (sg.flags & SEGF_WANT_BASE)
+    dec_store8(v, ncols, reinterpret_cast<char*>(sg.dst_base) + (r_local * sg.base_ld + n) * (bbf ? 2 : 4), bbf,
+               sg.flags & SEGF_BASE_VEC);
+  if (p.ia3_in_epilogue && (sg.flags & SEGF_IA3)) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < ncols) v[j] *= __ldg(sg.ia3 + n + j);
+  }
+  dec_store8(v, ncols, reinterpret_cast<char*>(sg.dst) + (r_local * sg.dst_ld + n) * (bf ? 2 : 4), bf,
+             sg.flags & SEGF_DST_VEC);
 }
 
 template <bool kBwd>
@@ -642,7 +722,44 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (p.fx_cnt) {
+        __threadfence();   // this lane's partial stores before the count (release)
+        __syncwarp();
+        if (lane == 0)
+          for (int j = 0; j < gr.g; ++j)
+            atomicAdd(p.fx_cnt + (int64_t)(gr.mt * p.n_n + gr.nt0 + j) * 2 + (warp - 4), 1);
+      }
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  }
+  if (p.fx_cnt) {
+    // ------------------------------------------------------------ in-kernel fixup (whole CTA)
+    // Once this CTA's groups are done, its 256 threads claim fixup units (the fixup kernel's
+    // blocks: 32 rows x 64 columns of one tile, thread t = the fixup kernel's thread t, the same
+    // fold bit for bit) in unit order and fold each once its tile half has counted every group.
+    int* unit_slot = reinterpret_cast<int*>(tmem_slot + 1);   // smem broadcast of the claimed unit
+    const int n_units = p.n_m * p.n_n * (DEC_ROWS / DEC_FIX_ROWS);
+    pdl_wait();   // the destinations may alias rows the kernels before this one read
+    for (;;) {
+      __syncthreads();   // everyone has read the previous slot
+      if (threadIdx.x == 0) {
+        int u = atomicAdd(p.fx_claim, 1);
+        if (u < n_units) {
+          const int q = u % (DEC_ROWS / DEC_FIX_ROWS), tile = u / (DEC_ROWS / DEC_FIX_ROWS);
+          const DecTile td = p.tiles[tile / p.n_n];
+          const int want = (1 + (td.lo ? 1 : 0)) * p.C + td.lp_count;
+          int* cnt = p.fx_cnt + (int64_t)tile * 2 + q;
+          while (ld_acquire_gpu(cnt) < want) __nanosleep(64);
+          *cnt = 0;   // every group of this launch has counted: ready for the next launch
+        } else {
+          u = -1;
+        }
+        *(volatile int*)unit_slot = u;
+      }
+      __syncthreads();
+      const int u = *(volatile int*)unit_slot;
+      if (u < 0) break;
+      dec_fixup_unit(p, u, (int)threadIdx.x);
     }
   }
   __syncthreads();
@@ -655,6 +772,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (atomicAdd(p.claim + 1, 1) == (int)gridDim.x - 1) {
       p.claim[0] = 0;
       p.claim[1] = 0;
+      if (p.fx_claim) p.fx_claim[0] = 0;
       __threadfence();
     }
   }
@@ -664,81 +782,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-// K1d fixup: y = fold(p_0 .. p_{C-1}, [lo_0 .. lo_{C-1}], [p_lora]) left to right, then bias /
-// y_base / IA3 / dst, for every valid row of every decode tile. Launched behind the GEMM (PDL: the
-// grid is resident early and waits on griddepcontrol.wait, which covers the GEMM's partial
-// stores). One CTA per 32 rows x 64 columns of a tile; a thread owns one row x 8 columns and
-// issues the loads of 8 partials at a time before adding them (the sum order is fixed, the loads
-// are not serialised).
-constexpr int DEC_FIX_ROWS = 32;
-constexpr int DEC_FIX_THREADS = DEC_FIX_ROWS * (DEC_TN / 8);   // 256
-
 __global__ void __launch_bounds__(DEC_FIX_THREADS)
     dec_fixup_kernel(const DecParams p) {
-  const int q = blockIdx.x % (DEC_ROWS / DEC_FIX_ROWS);
-  const int tile = blockIdx.x / (DEC_ROWS / DEC_FIX_ROWS);   // mt * n_n + nt
-  const int mt = tile / p.n_n, nt = tile - mt * p.n_n;
-  const int row = q * DEC_FIX_ROWS + (int)(threadIdx.x / (DEC_TN / 8));
-  const int col = (int)(threadIdx.x % (DEC_TN / 8)) * 8;
-  const DecTile td = p.tiles[mt];
   pdl_wait();
   pdl_trigger();
-  const int n = nt * DEC_TN + col;
-  if (row >= td.rows || n >= p.N) return;
-  const float4* src = reinterpret_cast<const float4*>(p.part + (int64_t)tile * p.S * DEC_PART +
-                                                      (int64_t)row * DEC_TN + col);
-  constexpr int P4 = DEC_PART / 4;
-  const int xrow = td.arow + row;
-  const DevSeg sg = p.segs[p.row_seg[xrow]];
-  // slots in fold order: hi chunks 0..C-1, lo chunks C..2C-1 (lo tiles only), then the LoRA
-  // piece holding this row's rank block (every other piece is exact zeros for this row)
-  const int nhl = td.lo ? 2 * p.C : p.C;
-  const int nslots = nhl + ((sg.flags & SEGF_LORA) && td.lp_count > 0 ? 1 : 0);
-  float v[8];
-  for (int i0 = 0; i0 < nslots; i0 += 8) {
-    float4 buf[8][2];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (i0 + i < nslots) {
-        const int slot = i0 + i < nhl ? i0 + i : 2 * p.C + sg.dec_piece;
-        const float4* s = src + (int64_t)slot * P4;
-        buf[i][0] = __ldcg(s);
-        buf[i][1] = __ldcg(s + 1);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (i0 + i < nslots) {
-        const float w[8] = {buf[i][0].x, buf[i][0].y, buf[i][0].z, buf[i][0].w,
-                            buf[i][1].x, buf[i][1].y, buf[i][1].z, buf[i][1].w};
-        if (i0 + i == 0) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = w[j];
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] += w[j];
-        }
-      }
-    }
-  }
-  const int ncols = min(8, p.N - n);
-  const int64_t r_local = xrow - sg.xrow0 + sg.xlocal0;
-  const bool bf = sg.flags & SEGF_DST_BF16, bbf = sg.flags & SEGF_BASE_BF16;
-  if (p.has_bias) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < ncols) v[j] += __ldg(p.bias + n + j);
-  }
-  if (sg.flags & SEGF_WANT_BASE)
-    dec_store8(v, ncols, reinterpret_cast<char*>(sg.dst_base) + (r_local * sg.base_ld + n) * (bbf ? 2 : 4), bbf,
-               sg.flags & SEGF_BASE_VEC);
-  if (p.ia3_in_epilogue && (sg.flags & SEGF_IA3)) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < ncols) v[j] *= __ldg(sg.ia3 + n + j);
-  }
-  dec_store8(v, ncols, reinterpret_cast<char*>(sg.dst) + (r_local * sg.dst_ld + n) * (bf ? 2 : 4), bf,
-             sg.flags & SEGF_DST_VEC);
+  dec_fixup_unit(p, (int)blockIdx.x, (int)threadIdx.x);
 }
 
 }  // namespace ss

@@ -264,6 +264,9 @@ struct ss_ctx {
   int* dshr_ticket = nullptr;     // decode shrink: per-item arrival counters (zero between launches)
   size_t dshr_ticket_cap = 0;
   int decode_lora_piece = DEC_LP_CHUNKS;   // max 16-row rank chunks per decode LoRA piece (tuning)
+  int decode_fixup_fused = 0;       // decode class: chunk fold + epilogue inside K1d (whole CTA after its groups), no fixup launch (measured slower)
+  int* dec_fx = nullptr;            // [0] fixup-unit ticket, then per (tile, n tile, half) group counters
+  size_t dec_fx_cap = 0;
   int decode_prologue = 1;          // decode-only dispatch: decode shrink + gather in one launch
   int decode_split = 0;           // K1d chunk groups beside the side-stream shrink, LoRA groups after (slower)
   float* dec_part = nullptr;      // K1d: fp32 chunk partials of the decode tiles
@@ -1207,6 +1210,12 @@ int build_batch(ss_ctx* ctx, int pass_kind, int block, int role, int n_seg, cons
     const int64_t tiles_dec = (int64_t)dtiles.size() * ((N + DEC_TN - 1) / DEC_TN);
     if ((rc = ensure_dev(ctx, ctx->dec_part, ctx->dec_part_cap,
                          (size_t)tiles_dec * B.dec_S * DEC_PART * sizeof(float)))) return rc;
+    // in-kernel fixup: ticket + per (tile, half) counters, all zero between launches
+    const size_t fx_bytes = (size_t)(1 + 2 * tiles_dec) * sizeof(int);
+    if (ctx->dec_fx_cap < fx_bytes) {
+      if ((rc = ensure_dev(ctx, ctx->dec_fx, ctx->dec_fx_cap, fx_bytes))) return rc;
+      CK(cudaMemset(ctx->dec_fx, 0, ctx->dec_fx_cap));
+    }
   }
   B.Mp = Mp;
   B.M = M; B.MX = MX; B.lora_ld = lora_ld; B.al_rows = al_rows; B.ldx = ldx;
@@ -1573,6 +1582,9 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
       ctx->launches++;
       return SS_OK;
     };
+    const bool fx_fused = ctx->decode_fixup_fused && !dec_split;
+    dp.fx_claim = fx_fused ? ctx->dec_fx : nullptr;
+    dp.fx_cnt = fx_fused ? ctx->dec_fx + 1 : nullptr;
     if (dec_split) {
       if ((rc = launch_dec(0, B.dec_chunk_groups, ctx->dec_claim, dec_early, dpdl))) return rc;
       CK(cudaStreamWaitEvent(stream, ctx->ev_join, 0));   // the shrink's A_lora
@@ -1580,10 +1592,12 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     } else {
       if ((rc = launch_dec(0, B.dec_groups, ctx->dec_claim, dec_early, dpdl))) return rc;
     }
-    CK(launch_kp(dpdl, dec_fixup_kernel, dp.n_n * dp.n_m * (DEC_ROWS / DEC_FIX_ROWS), DEC_FIX_THREADS, 0, stream, dp));
+    if (!fx_fused) {
+      CK(launch_kp(dpdl, dec_fixup_kernel, dp.n_n * dp.n_m * (DEC_ROWS / DEC_FIX_ROWS), DEC_FIX_THREADS, 0, stream, dp));
+      ctx->launches += 1;
+    }
     prof_end(ctx, stream, pd);
     CK(cudaGetLastError());
-    ctx->launches += 1;
   }
   CK(cudaEventRecord(ctx->compute_done, stream));
   ctx->any_compute = true;
@@ -1762,6 +1776,7 @@ int ss_ctx_destroy(ss_ctx* ctx) {
   cudaFree(ctx->shrink_part);
   cudaFree(ctx->shrink_ticket);
   cudaFree(ctx->dec_part);
+  cudaFree(ctx->dec_fx);
   cudaFree(ctx->dec_claim);
   cudaFree(ctx->dshr_part);
   cudaFree(ctx->dshr_ticket);
@@ -1905,6 +1920,11 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "decode_lora_piece")) {
     if (value < 1 || value > 1024) return fail(ctx, SS_E_ARG, "decode_lora_piece must be 1..1024");
     ctx->decode_lora_piece = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "decode_fixup_fused")) {
+    ctx->decode_fixup_fused = value ? 1 : 0;
+    ctx->opt_epoch++;
     return SS_OK;
   }
   if (!strcmp(key, "decode_prologue")) {

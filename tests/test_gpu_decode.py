@@ -147,6 +147,39 @@ def test_decode_class_batched_equals_solo_bitwise(pass_kind):
         assert torch.equal(mixed[n + j], alone[j]), j
 
 
+@pytest.mark.parametrize("pass_kind", [0, 1, 2])
+def test_fused_fixup_equals_fixup_launch_bitwise(pass_kind):
+    """decode_fixup_fused (the fold + epilogue run by K1d's idle warps behind per-tile completion
+    counters) gives the same bits as the separate fixup launch, for ~40 mixed decode requests
+    (several tiles, LoRA pieces, IA3, hi/lo rows), repeated launches (self-resetting counters and
+    ticket) and f32 outputs."""
+    d_in, d_out = 4096, 1408
+    role = O.K
+    w, b = O.layer_params(37, 0, role, d_in, d_out)
+    ex = _ex({(0, role): (w, b)})
+    dev = ex.device
+    n = 40
+    _clients(ex, 37, 0, role, d_in, d_out, n)
+    rng = np.random.default_rng(37)
+    counts = [int(t) for t in rng.integers(1, 17, size=n)]
+    width = d_out if pass_kind == 1 else d_in
+    xs = [torch.randn(t, width, device=dev).to(torch.bfloat16) for t in counts]
+    xf = [torch.randn(t, width, device=dev) for t in counts[:9]]
+
+    def run(rid):
+        envs = [_env(c, rid, 0, role, pass_kind, xs[c]) for c in range(n)]
+        envs += [_env(n + c, rid, 0, role, pass_kind, x) for c, x in enumerate(xf)]
+        return ex._compute_batch(pass_kind, envs)
+
+    ex.ctx.set_option("decode_fixup_fused", 0)
+    ref = run(1)
+    ex.ctx.set_option("decode_fixup_fused", 1)
+    for rep in range(3):
+        got = run(2 + rep)
+        for c in range(len(ref)):
+            assert torch.equal(got[c], ref[c]), (rep, c)
+
+
 def test_decode_rows_option_zero_restores_single_chain():
     """decode_rows = 0: no decode class, a 2-row request equals its rows inside a prefill-size
     dispatch of the single-chain kernels (the round-1 invariant)."""
