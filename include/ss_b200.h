@@ -385,6 +385,9 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   decode_prologue (1) decode-only dispatch with decode-class LoRA rows: their shrink and the
  *                       row gather in one launch (else a side-stream shrink beside the gather;
  *                       results unchanged)
+ *   tail_split (1)      CTA-pair 256 x 512 dispatches whose last wave is under half full: the last
+ *                       (partial + one full) wave of tiles runs as 256 x 256 tiles in a second,
+ *                       programmatically launched kernel (results unchanged)
  *   decode_fixup_fused (0) decode class: the ordered chunk fold + epilogue run inside the GEMM
  *                       launch (each CTA once its groups are done, behind per-tile completion
  *                       counters) instead of a separate fixup launch (bitwise the same fold;

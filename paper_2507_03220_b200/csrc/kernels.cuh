@@ -99,6 +99,14 @@ struct GemmParams {
   // Streaming kernel launched with programmatic dependent launch behind the gather / shrink:
   // the producer issues the first stages' W loads, then griddepcontrol.wait, then their A loads.
   int pdl_early = 0;
+  // CTA-pair tail split: a 512-wide launch stops at raster tile `tiles_total`, and a 256-wide
+  // launch behind it (programmatic launch, griddepcontrol.wait only before exiting, so it fills
+  // the SMs the 512-wide tiles free and still completes after them) runs the remaining tiles of
+  // the 512 raster as two 256-wide halves each: tail_nn = the 512 raster's N tiles (0: off),
+  // tail_from = its first tile. tiles_total > 0 overrides num_m_tiles * num_n_tiles.
+  int tiles_total = 0;
+  int tail_from = 0, tail_nn = 0;
+  int wait_at_end = 0;
   int has_bias;
   int any_lora;
   int ia3_in_epilogue;              // forward: scale output columns by IA3
@@ -116,24 +124,34 @@ struct GemmParams {
 // N-grouped (`group_n` > 0): groups of `group_n` N-tiles, M walked inside, so a group's W
 // columns stay in L2 while A streams (A read once per group) — the cheaper order when W is
 // small next to A (Q/K/V/O at prefill sizes fit W in L2 whole).
-__device__ __forceinline__ void tile_coords(int t, const GemmParams& p, int& mb, int& nb) {
-  if (p.group_n > 0) {
-    const int per_group = p.group_n * p.num_m_tiles;
+__device__ __forceinline__ void raster_coords(int t, int num_m, int num_n, int group_m, int group_n, int& mb,
+                                              int& nb) {
+  if (group_n > 0) {
+    const int per_group = group_n * num_m;
     const int g = t / per_group;
-    const int first_n = g * p.group_n;
-    const int gsize = min(p.group_n, p.num_n_tiles - first_n);
+    const int first_n = g * group_n;
+    const int gsize = min(group_n, num_n - first_n);
     const int r = t % per_group;
     nb = first_n + r % gsize;
     mb = r / gsize;
     return;
   }
-  const int per_group = p.group_m * p.num_n_tiles;
+  const int per_group = group_m * num_n;
   const int g = t / per_group;
-  const int first_m = g * p.group_m;
-  const int gsize = min(p.group_m, p.num_m_tiles - first_m);
+  const int first_m = g * group_m;
+  const int gsize = min(group_m, num_m - first_m);
   const int r = t % per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
+}
+__device__ __forceinline__ void tile_coords(int t, const GemmParams& p, int& mb, int& nb) {
+  if (p.tail_nn > 0) {
+    // tail launch: 256-wide halves of the 512 raster's tiles from tail_from on
+    raster_coords(p.tail_from + (t >> 1), p.num_m_tiles, p.tail_nn, p.group_m, p.group_n, mb, nb);
+    nb = 2 * nb + (t & 1);
+    return;
+  }
+  raster_coords(t, p.num_m_tiles, p.num_n_tiles, p.group_m, p.group_n, mb, nb);
 }
 
 __device__ __forceinline__ uint64_t l2_policy(int h) {
@@ -983,10 +1001,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<PN>::THREADS
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();
+  if (!p.wait_at_end) pdl_wait();
   pdl_trigger();
 
-  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  const int num_tiles = p.tiles_total > 0 ? p.tiles_total : p.num_m_tiles * p.num_n_tiles;
   const int nkb = (p.K + BK - 1) / BK;
   const int cluster_id = blockIdx.x >> 1;
   const int num_clusters = gridDim.x >> 1;
@@ -1155,6 +1173,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<PN>::THREADS
     tc_fence_after();
     tmem_dealloc_2sm(tmem_base, 512);
   }
+  if (p.wait_at_end) pdl_wait();   // complete only after the launch before this one
 }
 
 // ============================================================================ K1/K2/K5, 2 pairs

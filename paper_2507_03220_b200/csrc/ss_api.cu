@@ -264,6 +264,7 @@ struct ss_ctx {
   int* dshr_ticket = nullptr;     // decode shrink: per-item arrival counters (zero between launches)
   size_t dshr_ticket_cap = 0;
   int decode_lora_piece = DEC_LP_CHUNKS;   // max 16-row rank chunks per decode LoRA piece (tuning)
+  int tail_split = 1;               // CTA-pair 512 dispatches: an under-half-full last wave runs as 256-wide tiles (second launch)
   int decode_fixup_fused = 0;       // decode class: chunk fold + epilogue inside K1d (whole CTA after its groups), no fixup launch (measured slower)
   int* dec_fx = nullptr;            // [0] fixup-unit ticket, then per (tile, n tile, half) group counters
   size_t dec_fx_cap = 0;
@@ -1513,10 +1514,34 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     else
       CK(launch_k(ctx, seg_gemm4_kernel<false>, 4 * ng, GEMM_THREADS, GEMM4_SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
   } else if (pair && pn == 512) {
+    // Tail split: when the last wave of 512-wide tiles is under half full (T = W x P + r, r < P/2
+    // clusters), the last r + P raster tiles run as 2 (r + P) 256-wide tiles in a second launch
+    // that fills the SMs the first one frees: W + 1/2 wave times instead of W + 1 (the two
+    // kernels give every output element the same bits, tests/test_gpu_parity.py).
+    const int P = grid / 2;
+    const int T = ntiles;
+    const int r = T % P;
+    const bool split = ctx->tail_split && r > 0 && 2 * r < P && T > 2 * P;
+    GemmParams g1 = gpm;
+    if (split) g1.tiles_total = T - (r + P);
     if (bwd)
-      CK(launch_k(ctx, seg_gemm2_kernel<true, 512>, grid, PairCfg<512>::THREADS, GEMM2W_SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, gpm));
+      CK(launch_k(ctx, seg_gemm2_kernel<true, 512>, grid, PairCfg<512>::THREADS, GEMM2W_SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, g1));
     else
-      CK(launch_k(ctx, seg_gemm2_kernel<false, 512>, grid, PairCfg<512>::THREADS, GEMM2W_SMEM, stream, L.tm_w_fwd, tmAL, tmBP, gpm));
+      CK(launch_k(ctx, seg_gemm2_kernel<false, 512>, grid, PairCfg<512>::THREADS, GEMM2W_SMEM, stream, L.tm_w_fwd, tmAL, tmBP, g1));
+    if (split) {
+      GemmParams g2 = gpm;
+      g2.tail_from = T - (r + P);
+      g2.tail_nn = gpm.num_n_tiles;
+      g2.tiles_total = 2 * (r + P);
+      g2.wait_at_end = 1;
+      const int grid2 = 2 * std::min(g2.tiles_total, ctx->num_sms / 2);
+      const bool tpdl = !ctx->profiling;
+      if (bwd)
+        CK(launch_kp(tpdl, seg_gemm2_kernel<true, 256>, grid2, GEMM_THREADS, GEMM2_SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, g2));
+      else
+        CK(launch_kp(tpdl, seg_gemm2_kernel<false, 256>, grid2, GEMM_THREADS, GEMM2_SMEM, stream, L.tm_w_fwd, tmAL, tmBP, g2));
+      ctx->launches++;
+    }
   } else if (pair) {
     if (bwd)
       CK(launch_k(ctx, seg_gemm2_kernel<true, 256>, grid, GEMM_THREADS, GEMM2_SMEM, stream, L.tm_w_bwd2, tmAL, tmBP, gpm));
@@ -1920,6 +1945,11 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "decode_lora_piece")) {
     if (value < 1 || value > 1024) return fail(ctx, SS_E_ARG, "decode_lora_piece must be 1..1024");
     ctx->decode_lora_piece = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "tail_split")) {
+    ctx->tail_split = value ? 1 : 0;
+    ctx->opt_epoch++;
     return SS_OK;
   }
   if (!strcmp(key, "decode_fixup_fused")) {
