@@ -285,7 +285,8 @@ SS_API int ss_sched_deregister(ss_sched* s, uint32_t client_id);
 /* queue a request; notify != 0: its completion is also reported by ss_sched_next_done */
 SS_API int ss_sched_submit(ss_sched* s, const ss_request* req, int notify, uint64_t* ticket);
 /* block until `ticket` completed (timeout_us < 0: forever); on completion make `wait_stream`
- * wait for its batch (if not NULL). Returns SS_OK, or SS_E_ARG (unknown ticket) / 1 (timeout). */
+ * wait for its batch (if not NULL; a client on the legacy default stream passes cudaStreamLegacy,
+ * since NULL means "no stream"). Returns SS_OK, or SS_E_ARG (unknown ticket) / 1 (timeout). */
 SS_API int ss_sched_wait(ss_sched* s, uint64_t ticket, void* wait_stream, int64_t timeout_us,
                          int32_t* status, int64_t* aux);
 /* ss_sched_submit + ss_sched_wait in one call */

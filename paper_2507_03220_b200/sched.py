@@ -61,6 +61,21 @@ def status_message(status: int, aux: int, env_like, expected: int | None, schedu
     return f"executor rejected segment (status {status}) for layer {env_like.layer}"
 
 
+CUDA_STREAM_LEGACY = 0x1   # cudaStreamLegacy: the legacy default stream as an explicit handle
+
+
+def stream_handle(cuda_stream):
+    """The handle to give the scheduler's ``wait_stream`` for a torch ``Stream.cuda_stream``.
+
+    The C ABI reads NULL as "no stream to order" (ss_b200.h, ss_sched_wait), while torch reports
+    its default stream -- the legacy default stream -- as 0: passed through, a client on the
+    default stream would read its reply before the batch's kernels finished. None stays "no
+    wait"; 0 becomes cudaStreamLegacy."""
+    if cuda_stream is None:
+        return None
+    return int(cuda_stream) or CUDA_STREAM_LEGACY
+
+
 class NativeScheduler:
     def __init__(self, ctx, policy, stream: torch.cuda.Stream | None = None):
         self.lib = ctx.lib
@@ -93,7 +108,7 @@ class NativeScheduler:
     def request(self, req: SsRequest, wait_stream: int, timeout_s: float) -> tuple[int, int]:
         """Queue + block until launched (GIL released); ``wait_stream`` then waits for the batch."""
         st, aux = ctypes.c_int32(), ctypes.c_int64()
-        rc = self.lib.ss_sched_request(self.h, ctypes.byref(req), wait_stream, int(timeout_s * 1e6),
+        rc = self.lib.ss_sched_request(self.h, ctypes.byref(req), stream_handle(wait_stream), int(timeout_s * 1e6),
                                        ctypes.byref(st), ctypes.byref(aux))
         if rc == 1:
             raise TimeoutError("timed out waiting for executor reply")
@@ -104,7 +119,7 @@ class NativeScheduler:
     def next_done(self, wait_stream: int, timeout_s: float):
         """(ticket, status, aux) of the next completed notify-request, or None on timeout."""
         t, st, aux = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_int64()
-        rc = self.lib.ss_sched_next_done(self.h, wait_stream, int(timeout_s * 1e6), ctypes.byref(t),
+        rc = self.lib.ss_sched_next_done(self.h, stream_handle(wait_stream), int(timeout_s * 1e6), ctypes.byref(t),
                                          ctypes.byref(st), ctypes.byref(aux))
         if rc == 1:
             return None

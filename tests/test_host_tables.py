@@ -57,3 +57,12 @@ def test_segment_table_cache_tracks_tensor_identity():
     assert _cached_fields(cache, s2) == seg_fields(s2)
     tab = SegmentTable([s1, s2], cache)
     assert [c.src for c in tab.arr[:2]] == [x.data_ptr(), x2.data_ptr()]
+
+
+def test_native_scheduler_wait_stream_handle():
+    """torch reports the legacy default stream as 0, which the scheduler ABI reads as "no stream":
+    the wrapper must pass cudaStreamLegacy so a default-stream client waits for its batch."""
+    from paper_2507_03220_b200.sched import CUDA_STREAM_LEGACY, stream_handle
+    assert stream_handle(0) == CUDA_STREAM_LEGACY == 1
+    assert stream_handle(None) is None
+    assert stream_handle(0x7f00dead) == 0x7f00dead
