@@ -993,16 +993,21 @@ def main():
         for _ in range(2):
             grads_pass()
         torch.cuda.synchronize()
-        ctx.profile(True)
+        # wall time of the passes without per-launch profiling events, then one profiled pass
+        # per step for the kernel-only time and bytes
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
         for _ in range(args.steps):
             grads_pass()
         g1.record(stream)
         torch.cuda.synchronize()
+        g_ms = g0.elapsed_time(g1) / args.steps
+        ctx.profile(True)
+        for _ in range(args.steps):
+            grads_pass()
+        torch.cuda.synchronize()
         gk = ctx.profile_read(_lib.SS_KERNEL_GRAD)
         ctx.profile(False)
-        g_ms = g0.elapsed_time(g1) / args.steps
         grads_leg = {"ms_per_step": g_ms, "kernel_ms_per_step": gk["ms"] / args.steps,
                      "launches_per_step": gk["launches"] / args.steps,
                      "alg_bytes_per_step": gk["bytes"] / args.steps,
