@@ -1521,7 +1521,8 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
     const int P = grid / 2;
     const int T = ntiles;
     const int r = T % P;
-    const bool split = ctx->tail_split && r > 0 && 2 * r < P && T > 2 * P;
+    // (N a multiple of 512: no 256-wide half starts past the last column)
+    const bool split = ctx->tail_split && r > 0 && 2 * r < P && T > 2 * P && N % 512 == 0;
     GemmParams g1 = gpm;
     if (split) g1.tiles_total = T - (r + P);
     if (bwd)
