@@ -386,6 +386,8 @@ SS_API int ss_profile_read(ss_ctx* ctx, int kernel, double* total_ms, int64_t* l
  *   decode_prologue (1) decode-only dispatch with decode-class LoRA rows: their shrink and the
  *                       row gather in one launch (else a side-stream shrink beside the gather;
  *                       results unchanged)
+ *   group_m_longk (0)   M-grouped raster group size of dispatches with K >= longk (0: group_m)
+ *   longk (8192)        the K from which group_m_longk applies
  *   tail_split (1)      CTA-pair 256 x 512 dispatches whose last wave is under half full: the last
  *                       (partial + one full) wave of tiles runs as 256 x 256 tiles in a second,
  *                       programmatically launched kernel (results unchanged)

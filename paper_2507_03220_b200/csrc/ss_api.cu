@@ -217,6 +217,8 @@ struct ss_ctx {
   bool any_compute = false;
   int64_t launches = 0;
   int group_m = 16;
+  int group_m_longk = 0;     // > 0: group_m of dispatches with K >= longk (0: group_m)
+  int longk = 8192;
   // GEMM tile raster: 0 M-grouped (group_m M-tiles per group), 1 N-grouped (W columns of a group
   // held in L2 while A streams), -1 auto: the order with fewer estimated DRAM bytes, where an
   // N group is as many W column tiles as fit `l2_budget_mb`. group_n > 0 forces the group width.
@@ -1460,7 +1462,9 @@ int launch_batch(ss_ctx* ctx, const Built& B, char* dv, cudaStream_t stream) {
   gpm.num_m_tiles = num_m;
   const int pn = B.pn;                      // CTA-pair tile width (256 or 512)
   gpm.num_n_tiles = pair ? (N + pn - 1) / pn : (N + tbn - 1) / tbn;
-  gpm.group_m = ctx->group_m;
+  // long-K dispatches: a raster group's A rows (group_m x 256 rows x K) must stay in L2 while W
+  // streams past; at K = 13824 sixteen pair M-tiles are 113 MB
+  gpm.group_m = (ctx->group_m_longk > 0 && K >= ctx->longk) ? ctx->group_m_longk : ctx->group_m;
   gpm.group_n = 0;
   {
     // DRAM bytes of the two raster orders (A = the dispatch rows, W = the layer; outputs equal)
@@ -2018,6 +2022,16 @@ int ss_set_option(ss_ctx* ctx, const char* key, int64_t value) {
   }
   if (!strcmp(key, "l2_hints")) {
     ctx->l2_hints = value ? 1 : 0;
+    return SS_OK;
+  }
+  if (!strcmp(key, "group_m_longk")) {
+    if (value < 0) return fail(ctx, SS_E_ARG, "group_m_longk must be >= 0");
+    ctx->group_m_longk = (int)value;
+    return SS_OK;
+  }
+  if (!strcmp(key, "longk")) {
+    if (value < 1) return fail(ctx, SS_E_ARG, "longk must be >= 1");
+    ctx->longk = (int)value;
     return SS_OK;
   }
   if (!strcmp(key, "group_m")) {
