@@ -873,31 +873,33 @@ def test_full_size_batched_equals_solo_13b_ff_up():
             assert torch.equal(base_s, base_batched)
 
 
-@pytest.mark.parametrize("pass_kind", [0, 1])
-def test_tail_split_bitwise(pass_kind):
-    """tail_split: a 13B K-projection dispatch of 32 clients x 1024 rows (forward: 1280 tiles of
-    256 x 512 = 17 waves of 74 CTA pairs + 22; backward at 16 x 1024 rows: 640 tiles, not split)
-    whose last 96 raster tiles run as 192 tiles of 256 x 256 in a second launch gives the same
-    bits as one 256 x 512 launch, and as a client alone; LoRA r16 / r64 and IA3 with y_base."""
-    d_in, d_out = 5120, 5120
-    role = O.K
+@pytest.mark.parametrize("pass_kind,role,d_in,d_out", [(0, O.K, 5120, 5120), (1, O.K, 5120, 5120),
+                                                       (1, O.FF_DOWN, 13824, 5120)])
+def test_tail_split_bitwise(pass_kind, role, d_in, d_out):
+    """tail_split: a 13B K-projection forward of 32 clients x 1024 rows (1280 tiles of 256 x 512
+    = 17 waves of 74 CTA pairs + 22: the last 96 raster tiles run as 192 tiles of 256 x 256 in a
+    second launch), its backward at 16 x 1024 rows (640 tiles: not split) and an FF_DOWN backward
+    (N = 13824: 1728 tiles, 23 waves + 26: split, backward kernels) give the same bits as one
+    256 x 512 launch, and as a client alone; LoRA r16 / r64 and IA3 (forward: with y_base)."""
     w, b = O.layer_params(31, 0, role, d_in, d_out)
     ex = _ex({(0, role): (w, b)})
     for cid, r in ((0, 16), (5, 64)):
         ad = O.lora_params(31, cid, 0, role, d_in, d_out, r, 2.0 * r)
         ex.register_adapter(cid, _Adapter(lora={_addr(0, role): (ad.a, ad.b)}, alpha=2.0 * r, rank=r))
-    ex.register_adapter(2, _Adapter(ia3={_addr(0, role): O.ia3_params(31, 2, 0, role, d_out).ia3}))
+    if role in O.IA3_ROLES:
+        ex.register_adapter(2, _Adapter(ia3={_addr(0, role): O.ia3_params(31, 2, 0, role, d_out).ia3}))
     dev = ex.device
     gen = torch.Generator(device=dev).manual_seed(31)
     n = 32 if pass_kind == 0 else 16
-    xs = [torch.randn(1024, d_in, generator=gen, device=dev).to(torch.bfloat16) for _ in range(n)]
+    width = d_out if pass_kind == 1 else d_in
+    xs = [torch.randn(1024, width, generator=gen, device=dev).to(torch.bfloat16) for _ in range(n)]
     base = {}
 
     def run(rid, idx):
         envs = []
         for c in idx:
             kw = {}
-            if c == 2 and pass_kind == 0:
+            if c == 2 and pass_kind == 0 and role in O.IA3_ROLES:
                 base[rid] = torch.empty(1024, d_out, dtype=torch.bfloat16, device=dev)
                 kw["base_to"] = base[rid]
             envs.append(_env(c, rid, 0, role, pass_kind, xs[c], **kw))
@@ -909,7 +911,7 @@ def test_tail_split_bitwise(pass_kind):
     got = run(2, range(n))
     for c in range(n):
         assert torch.equal(got[c], ref[c]), c
-    if pass_kind == 0:
+    if base:
         assert torch.equal(base[1], base[2])
     for c in (0, 2, n - 1):
         solo = run(10 + c, [c])[0]
