@@ -240,3 +240,36 @@ def test_concurrent_adapter_refresh_during_dispatch():
                                                  rank=ad.rank), x0, O.affine_forward(x0, wr, b))
         mx, mn = O.normwise_errors(out[c].float().cpu().numpy(), oracle)
         assert mx <= O.TOL_MAX_REL and mn <= O.TOL_MEAN_REL, (c, mx, mn)
+
+
+def test_cuda_graph_of_tail_split_dispatches_bitwise():
+    """The bench's path for split dispatches: two consecutive 13B K-projection forwards of
+    32 x 1024 rows (each a 256 x 512 launch + the programmatically launched 256 x 256 tail, the
+    second reading the first's output) captured as one graph equal the eager plans and the
+    unsplit launch, replay after replay."""
+    d = 5120
+    w, b = O.layer_params(23, 0, O.K, d, d)
+    w2, b2 = O.layer_params(23, 0, O.V, d, d)
+    ex = _ex({(0, O.K): (w, b), (0, O.V): (w2, b2)})
+    for cid, r in ((0, 16), (7, 64)):
+        for role in (O.K, O.V):
+            ad = O.lora_params(23, cid, 0, role, d, d, r, 2.0 * r)
+            ex.register_adapter(cid, _Adapter(lora={_addr(0, role): (ad.a, ad.b)}, alpha=2.0 * r, rank=r))
+    n = 32
+    xs, mid = _buffers(ex, [1024] * n, d, d, seed=23)
+    out = [torch.empty_like(m) for m in mid]
+    plan = [ex.compile_dispatch(0, 0, O.K, [(c, xs[c], mid[c], None) for c in range(n)]),
+            ex.compile_dispatch(0, 0, O.V, [(c, mid[c], out[c], None) for c in range(n)])]
+    ex.ctx.set_option("tail_split", 0)
+    ref_mid = ex._compute_batch(0, [_env(c, 1, 0, O.K, 0, xs[c]) for c in range(n)])
+    ref_out = ex._compute_batch(0, [_env(c, 2, 0, O.V, 0, ref_mid[c]) for c in range(n)])
+    ex.ctx.set_option("tail_split", 1)
+    g = ex.capture(plan)
+    for _ in range(3):
+        for t in mid + out:
+            t.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for c in range(n):
+            assert torch.equal(mid[c], ref_mid[c]), c
+            assert torch.equal(out[c], ref_out[c]), c
