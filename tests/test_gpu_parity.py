@@ -988,3 +988,23 @@ def test_dispatches_on_two_streams_are_ordered():
             assert torch.equal(outs_a[c], solo_a[c]), ("a", c)
         for c in range(len(xb)):
             assert torch.equal(outs_b[c], solo_b[c]), ("b", c)
+
+
+def test_long_k_raster_group_bitwise():
+    """group_m_longk (raster group size of K >= longk dispatches) only reorders tiles: a K = 13824
+    forward of 8 x 1024 rows gives the same bits with groups of 16, 6 and 1 pair M-tiles."""
+    d_in, d_out = 13824, 1536
+    w, b = O.layer_params(43, 0, O.FF_DOWN, d_in, d_out)
+    ex = _ex({(0, O.FF_DOWN): (w, b)})
+    ad = O.lora_params(43, 1, 0, O.FF_DOWN, d_in, d_out, 32, 64.0)
+    ex.register_adapter(1, _Adapter(lora={_addr(0, O.FF_DOWN): (ad.a, ad.b)}, alpha=64.0, rank=32))
+    gen = torch.Generator(device=ex.device).manual_seed(43)
+    xs = [torch.randn(1024, d_in, generator=gen, device=ex.device).to(torch.bfloat16) for _ in range(8)]
+    outs = []
+    for g in (0, 6, 1):
+        ex.ctx.set_option("group_m_longk", g)
+        outs.append(ex._compute_batch(0, [_env(c, 1 + g, 0, O.FF_DOWN, 0, x) for c, x in enumerate(xs)]))
+    ex.ctx.set_option("group_m_longk", 0)
+    for o in outs[1:]:
+        for c in range(len(xs)):
+            assert torch.equal(o[c], outs[0][c]), c
